@@ -1,0 +1,163 @@
+/*
+ * gnnc.h — C ABI of the B200 (sm_100a) GCN/GAT composition kernels.
+ *
+ * The reference (gnncompose 0.1.0, Python) has no native ABI: its operator
+ * boundary is the set of Python functions in gnncompose/sparse.py plus
+ * gat.atten_calc, and the `spmm_fn=` plug-in hook on the layer functions
+ * (gcn.py:125-161, gat.py:121-153).  Every entry point below replaces one of
+ * those calls (cited per function); the Python mirror in
+ * paper_2306_15155_b200/ binds them through ctypes.
+ *
+ * Conventions (all entry points):
+ *   - extern "C", plain pointers and sizes, int return: 0 = ok, < 0 = error
+ *     (gc_last_error() holds a message; Python maps GC_ERR_SHAPE to
+ *     ShapeError, GC_ERR_VALUE to ValueError, the rest to RuntimeError).
+ *   - Data pointers are DEVICE pointers unless the parameter name ends in
+ *     `_host`.  CSR indices are int32 (row_ptr[n_rows+1], col_idx[nnz]),
+ *     values and dense operands are float32, dense matrices are row-major
+ *     with an explicit leading dimension (in elements).
+ *   - `stream` is a cudaStream_t passed as void*; work is stream-ordered,
+ *     the library never synchronises and never allocates device memory:
+ *     the caller owns every buffer, including workspaces.
+ *   - Validation happens before any launch; no partial work on error.
+ *   - Results are deterministic (no floating-point atomics): each output
+ *     element has one fixed accumulation order.
+ */
+#ifndef GNNC_H_
+#define GNNC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GNNC_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define GNNC_API __attribute__((visibility("default")))
+#else
+#define GNNC_API
+#endif
+
+/* status codes */
+#define GC_OK 0
+#define GC_ERR_SHAPE (-1)       /* operand dimensions do not conform  -> ShapeError */
+#define GC_ERR_VALUE (-2)       /* bad scalar argument / flag         -> ValueError */
+#define GC_ERR_CUDA (-3)        /* launch or device error             -> RuntimeError */
+#define GC_ERR_UNSUPPORTED (-4) /* combination not implemented        -> RuntimeError */
+#define GC_ERR_WORKSPACE (-5)   /* workspace missing or too small     -> RuntimeError */
+
+/* epilogue / mode flags */
+#define GC_RELU (1u << 0)       /* out = max(out, 0) (gcn.py:115-116, gat.py:117-118) */
+#define GC_ACCUMULATE (1u << 1) /* out += result instead of out = result */
+#define GC_GEMM_TF32 (1u << 4)  /* tcgen05.mma kind::tf32, TMEM accumulators, TMA operands */
+#define GC_GEMM_FP32 (1u << 5)  /* exact fp32 CUDA-core path (rtol 1e-4 parity mode) */
+
+/* SpMM work decomposition */
+#define GC_SPMM_ROW 1       /* one lane-group per CSR row                          */
+#define GC_SPMM_NNZ_SPLIT 2 /* plan-driven: heavy rows split into fixed-size edge
+                               chunks, partial sums combined in a fixed order     */
+
+/* ---- library state ---------------------------------------------------- */
+GNNC_API int gc_abi_version(void);
+GNNC_API const char *gc_last_error(void);      /* message of the last error on this thread */
+GNNC_API uint64_t gc_launch_count(void);       /* kernels launched by this library so far   */
+GNNC_API int gc_device_sm_count(int device);   /* multiprocessor count of `device`          */
+
+/* ---- SpMM ---------------------------------------------------------------
+ * C[i,:] (=|+=) epi( d_row[i] * sum_{p in row i} w_p * B[col_idx[p],:] )
+ *   w_p = (values ? values[p] : 1) * (d_col ? d_col[col_idx[p]] : 1)
+ * Replaces: sparse.spmm (sparse.py:240-247 -> _spmm_kernel 196-205) when
+ *   values != NULL; sparse.spmm_unweighted (sparse.py:250-264 -> 208-219)
+ *   when values == NULL (the values array is then never read); and the
+ *   dynamic-normalisation sequence scale_rows -> spmm -> scale_rows of
+ *   gcn.gcn_layer_dynamic (gcn.py:137-155) when d_col/d_row are given.
+ * Edges of a row are accumulated in ascending storage order (sequential
+ *   FMA), so values == NULL is bit-identical to all-ones values.
+ * `items`/`split_rows` come from gc_spmm_plan_* (GC_SPMM_NNZ_SPLIT only);
+ *   that mode needs n_slots*K floats of `workspace`.                      */
+GNNC_API int gc_spmm_f32(const int32_t *row_ptr, const int32_t *col_idx, const float *values,
+                const float *d_row, const float *d_col, const float *B, int64_t ldb,
+                int64_t n_rows, int64_t n_cols, int64_t K, float *C, int64_t ldc,
+                uint32_t flags, int algo, const int32_t *items, int64_t n_items,
+                const int32_t *split_rows, int64_t n_split_rows, void *workspace,
+                size_t ws_bytes, void *stream);
+
+/* Host-side planner for GC_SPMM_NNZ_SPLIT (one pass over a host copy of
+ * row_ptr).  Rows with more than `chunk` edges become ceil(deg/chunk)
+ * items whose partial sums land in consecutive workspace slots; every other
+ * row is one item writing C directly.  items: int32[4*n_items] =
+ * {row, begin, end, slot|-1}; split_rows: int32[4*n_split_rows] =
+ * {row, first_slot, n_slots, 0}. */
+GNNC_API int gc_spmm_plan_count(const int32_t *row_ptr_host, int64_t n_rows, int32_t chunk,
+                       int64_t *n_items, int64_t *n_slots, int64_t *n_split_rows);
+GNNC_API int gc_spmm_plan_fill(const int32_t *row_ptr_host, int64_t n_rows, int32_t chunk,
+                      int32_t *items_host, int32_t *split_rows_host);
+
+/* ---- SDDMM --------------------------------------------------------------
+ * out[p] = (a_vals ? a_vals[p] : 1) * sum_t B[i,t] * Cm[col_idx[p],t]
+ * Replaces sparse.sddmm (sparse.py:267-282 -> _sddmm_kernel 222-232).
+ * The output shares row_ptr/col_idx with the input (pattern bit-identical). */
+GNNC_API int gc_sddmm_f32(const int32_t *row_ptr, const int32_t *col_idx, const float *a_vals,
+                 const float *B, int64_t ldb, const float *Cm, int64_t ldc, int64_t n_rows,
+                 int64_t n_cols, int64_t k, float *out_vals, void *stream);
+
+/* k = 1 special case used for the normalised adjacency:
+ * out[p] = (a_vals ? a_vals[p] : 1) * (d[i] * d[col_idx[p]])
+ * Replaces gcn.precompute_normalized (gcn.py:103-112). */
+GNNC_API int gc_sddmm_norm_f32(const int32_t *row_ptr, const int32_t *col_idx, const float *a_vals,
+                      const float *d, int64_t n_rows, float *out_vals, void *stream);
+
+/* ---- dense --------------------------------------------------------------
+ * C = epi( diag(row_scale) * A * W ), A: M x K (lda), W: K x N (ldw),
+ * C: M x N (ldc).  Replaces sparse.gemm (sparse.py:285-291).
+ * GC_GEMM_TF32: tcgen05/TMEM/TMA kernel, needs lda % 4 == 0 and 16-byte
+ *   aligned A, plus workspace >= gc_gemm_workspace_bytes(K, N) for the
+ *   transposed (K-major) W.  GC_GEMM_FP32: exact fp32 FMA on CUDA cores.  */
+GNNC_API size_t gc_gemm_workspace_bytes(int64_t K, int64_t N);
+GNNC_API int gc_gemm_f32(const float *A, int64_t lda, const float *W, int64_t ldw, int64_t M,
+                int64_t K, int64_t N, float *C, int64_t ldc, const float *row_scale,
+                uint32_t flags, void *workspace, size_t ws_bytes, void *stream);
+
+/* C[i,:] = epi( d[i] * B[i,:] ).  Replaces sparse.scale_rows
+ * (sparse.py:294-300); with d == NULL and GC_RELU it is the ReLU of
+ * gcn.py:115-116 / gat.py:117-118. */
+GNNC_API int gc_scale_rows_f32(const float *d, const float *B, int64_t ldb, int64_t n_rows, int64_t K,
+                      float *C, int64_t ldc, uint32_t flags, void *stream);
+
+/* ---- GAT attention -------------------------------------------------------
+ * Node projections (the reassociated attention of gat.py:110-111):
+ *   s[h*n + i] = sum_c HW[i, h*k2 + c] * a_src[h*k2 + c],  likewise t/a_dst,
+ * for heads h = 0..heads-1 (heads = 1 is the reference's single head). */
+GNNC_API int gc_node_proj_f32(const float *HW, int64_t ld, int64_t n_rows, int64_t k2, int32_t heads,
+                     const float *a_src, const float *a_dst, float *s, float *t, void *stream);
+
+/* Fused LeakyReLU + edge softmax over each CSR row (gat.py:72-95):
+ *   e = s[h,i] + t[h,j]; e = e < 0 ? e * slope : e;
+ *   alpha[h*nnz + p] = exp(e - max_row) / sum_row
+ * Rows without edges produce nothing.  Requires a square pattern. */
+GNNC_API int gc_edge_softmax_f32(const int32_t *row_ptr, const int32_t *col_idx, const float *s,
+                        const float *t, int32_t heads, float slope, int64_t n_rows,
+                        int64_t nnz, float *alpha, void *stream);
+
+/* Attention as an SDDMM over edges: per edge
+ *   e = a_src[h]·HW[i, h] + a_dst[h]·HW[j, h]   (k2-wide dot products),
+ * then the same LeakyReLU + edge softmax as gc_edge_softmax_f32. */
+GNNC_API int gc_attn_sddmm_f32(const int32_t *row_ptr, const int32_t *col_idx, const float *HW,
+                      int64_t ld, int64_t k2, int32_t heads, const float *a_src,
+                      const float *a_dst, float slope, int64_t n_rows, int64_t nnz,
+                      float *alpha, void *stream);
+
+/* ---- multi-GPU row partition -----------------
+ * nnz-balanced contiguous row blocks over a HOST copy of row_ptr (int64):
+ *   bounds[0] = 0, bounds[P] = n, bounds[p] = first r with row_ptr[r] >=
+ *   ceil(p*nnz/P).  Bit-exact with the oracle restatement.              */
+GNNC_API int gc_partition_rows(const int64_t *row_ptr_host, int64_t n_rows, int32_t parts,
+                      int64_t *bounds_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GNNC_H_ */

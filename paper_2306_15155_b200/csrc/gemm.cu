@@ -1,0 +1,504 @@
+// Dense update H·W for sm_100a (replaces gnncompose/sparse.py:285-291, gemm).
+//
+// Two kernels behind gc_gemm_f32:
+//  * gemm_tf32_tcgen05: TMA (SWIZZLE_128B) -> smem ring -> tcgen05.mma
+//    kind::tf32 (one elected thread issues) -> fp32 accumulators in TMEM ->
+//    tcgen05.ld epilogue with the row scale (D^-1/2) and ReLU fused.
+//    Both operands are K-major: A = H (row-major M x K) as is, B = W^T, which
+//    a tiny transpose kernel writes into the caller's workspace.
+//  * gemm_fp32_simt: exact-fp32 CUDA-core tiles; the rtol-1e-4 parity mode and
+//    the path for operands TMA cannot describe (lda % 4 != 0, e.g. Cora's
+//    k1 = 1433).
+// Plus gc_scale_rows_f32 (D^-1/2 X / ReLU as a standalone pass).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "common.cuh"
+
+namespace gnnc {
+namespace {
+
+// ============================================================================
+// small PTX wrappers (tcgen05 / TMA / mbarrier)
+// ============================================================================
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// Bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint64_t spins = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    if (++spins > (1ull << 26)) __trap();
+  }
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar,
+                                            int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// K-major operand in a 128-byte-swizzled tile: rows of 128 B, 8-row atoms of
+// 1024 B stacked along M/N (SBO = 1024 B), LBO unused (1), version 1 (sm_100).
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;             // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;   // SBO
+  d |= (uint64_t)1 << 46;             // descriptor version (Blackwell)
+  d |= (uint64_t)2 << 61;             // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: D = F32, A = B = TF32, both K-major, M = 128, N = n.
+__host__ __device__ constexpr uint32_t idesc_tf32(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((128u >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ============================================================================
+// tcgen05 TF32 GEMM
+// ============================================================================
+constexpr int BM = 128;             // UMMA_M (cta_group::1)
+constexpr int BK = 32;              // fp32 elements per 128-byte swizzle row
+constexpr int UMMA_K = 8;           // K per tcgen05.mma for kind::tf32
+constexpr int kGemmThreads = 128;   // 4 warps: TMA / MMA / TMEM-alloc roles, all do the epilogue
+
+struct GemmEpi {
+  float *C;
+  int64_t ldc;
+  const float *row_scale;
+  int64_t M, N;
+  uint32_t flags;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_tf32_tcgen05(const __grid_constant__ CUtensorMap map_a,
+                      const __grid_constant__ CUtensorMap map_b, const GemmEpi ep, int num_kb,
+                      int stages) {
+  constexpr uint32_t A_BYTES = BM * BK * 4;
+  constexpr uint32_t B_BYTES = BN * BK * 4;
+  constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;  // power of two >= 32
+
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;  // SWIZZLE_128B needs 1024-B alignment
+  uint8_t *gbase = smem_raw + (base - raw);
+  const uint32_t bar0 = base + (uint32_t)stages * STAGE_BYTES;  // full[s], empty[s], accum
+  auto full_bar = [&](int s) { return bar0 + 8u * s; };
+  auto empty_bar = [&](int s) { return bar0 + 8u * (stages + s); };
+  const uint32_t accum_bar = bar0 + 8u * (2 * stages);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + (bar0 - base) + 8u * (2 * stages + 1));
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int m0 = blockIdx.x * BM;
+  const int n0 = blockIdx.y * BN;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    mbar_init(accum_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_d = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer ----------------
+    for (int kb = 0; kb < num_kb; ++kb) {
+      const int s = kb % stages;
+      if (kb >= stages) mbar_wait(empty_bar(s), ((kb / stages) & 1) ^ 1);
+      const uint32_t sa = base + (uint32_t)s * STAGE_BYTES;
+      mbar_expect_tx(full_bar(s), STAGE_BYTES);
+      tma_load_2d(sa, &map_a, full_bar(s), kb * BK, m0);
+      tma_load_2d(sa + A_BYTES, &map_b, full_bar(s), kb * BK, n0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer (single thread) ----------------
+    constexpr uint32_t idesc = idesc_tf32(BN);
+    for (int kb = 0; kb < num_kb; ++kb) {
+      const int s = kb % stages;
+      mbar_wait(full_bar(s), (kb / stages) & 1);
+      tc_fence_after();
+      const uint32_t sa = base + (uint32_t)s * STAGE_BYTES;
+#pragma unroll
+      for (int k = 0; k < BK / UMMA_K; ++k) {
+        const uint64_t ad = umma_desc_sw128(sa + k * UMMA_K * 4);
+        const uint64_t bd = umma_desc_sw128(sa + A_BYTES + k * UMMA_K * 4);
+        mma_tf32(tmem_d, ad, bd, idesc, (kb | k) != 0);
+      }
+      mma_commit(empty_bar(s));  // frees the smem slot once these MMAs retire
+    }
+    mma_commit(accum_bar);  // accumulator complete
+  }
+  __syncwarp();
+
+  // ---------------- epilogue: TMEM -> registers -> global ----------------
+  mbar_wait(accum_bar, 0);
+  tc_fence_after();
+  const int row = m0 + warp * 32 + lane;  // TMEM lane == tile row
+  const bool row_ok = row < ep.M;
+  const float rs = (row_ok && ep.row_scale) ? __ldg(ep.row_scale + row) : 1.0f;
+  const bool relu = (ep.flags & GC_RELU) != 0;
+  const bool vec = ((ep.ldc & 3) == 0) && aligned16(ep.C);
+  float *crow = ep.C + (int64_t)row * ep.ldc;
+#pragma unroll 1
+  for (int c = 0; c < BN; c += 16) {
+    if (n0 + c >= ep.N) break;  // warp-uniform
+    float v[16];
+    tmem_ld16(tmem_d + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, v);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      v[i] *= rs;
+      if (relu) v[i] = fmaxf(v[i], 0.0f);
+    }
+    if (!row_ok) continue;
+    const int64_t col = n0 + c;
+    if (vec && col + 16 <= ep.N) {
+#pragma unroll
+      for (int i = 0; i < 16; i += 4)
+        stg_f4(crow + col + i, make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (col + i < ep.N) crow[col + i] = v[i];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d),
+                 "n"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// W (K x N, ldw) -> Wt (N x K, ldt): the K-major B operand.
+__global__ void transpose_kernel(const float *__restrict__ W, int64_t ldw, int64_t K, int64_t N,
+                                 float *__restrict__ Wt, int64_t ldt) {
+  __shared__ float tile[32][33];
+  const int64_t k0 = (int64_t)blockIdx.y * 32, n0 = (int64_t)blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t k = k0 + i, n = n0 + threadIdx.x;
+    tile[i][threadIdx.x] = (k < K && n < N) ? W[k * ldw + n] : 0.0f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t n = n0 + i, k = k0 + threadIdx.x;
+    if (n < N && k < ldt) Wt[n * ldt + k] = (k < K) ? tile[threadIdx.x][i] : 0.0f;
+  }
+}
+
+// ============================================================================
+// exact fp32 SIMT GEMM (64x64 tiles, 4x4 per thread, k ascending FMA)
+// ============================================================================
+constexpr int SB = 64, SK = 16;
+__global__ void __launch_bounds__(256)
+    gemm_fp32_simt(const float *__restrict__ A, int64_t lda, const float *__restrict__ W,
+                   int64_t ldw, GemmEpi ep, int64_t K) {
+  __shared__ float As[SK][SB + 4];
+  __shared__ float Ws[SK][SB + 4];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int64_t m0 = (int64_t)blockIdx.x * SB, n0 = (int64_t)blockIdx.y * SB;
+  float acc[4][4] = {};
+  for (int64_t k0 = 0; k0 < K; k0 += SK) {
+    for (int i = threadIdx.x; i < SB * SK; i += 256) {
+      const int r = i / SK, kk = i % SK;  // A tile, read along k
+      const int64_t gm = m0 + r, gk = k0 + kk;
+      As[kk][r] = (gm < ep.M && gk < K) ? A[gm * lda + gk] : 0.0f;
+      const int kr = i / SB, c = i % SB;  // W tile, read along n
+      const int64_t wk = k0 + kr, wn = n0 + c;
+      Ws[kr][c] = (wk < K && wn < ep.N) ? W[wk * ldw + wn] : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < SK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Ws[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = m0 + ty * 4 + i;
+    if (r >= ep.M) continue;
+    const float rs = ep.row_scale ? ep.row_scale[r] : 1.0f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t c = n0 + tx * 4 + j;
+      if (c >= ep.N) continue;
+      float v = acc[i][j] * rs;
+      if (ep.flags & GC_RELU) v = fmaxf(v, 0.0f);
+      ep.C[r * ep.ldc + c] = v;
+    }
+  }
+}
+
+__global__ void fill_rows_kernel(float *C, int64_t ldc, int64_t M, int64_t N, float v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < M * N) C[(i / N) * ldc + i % N] = v;
+}
+
+// ============================================================================
+// scale_rows / ReLU
+// ============================================================================
+__global__ void scale_rows_kernel(const float *__restrict__ d, const float *__restrict__ B,
+                                  int64_t ldb, int64_t n_rows, int64_t K, float *__restrict__ C,
+                                  int64_t ldc, uint32_t flags, bool vec) {
+  const int64_t per_row = vec ? K / 4 : K;
+  const int64_t total = n_rows * per_row;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / per_row, q = i % per_row;
+    const float s = d ? __ldg(d + r) : 1.0f;
+    if (vec) {
+      float4 v = ldg_f4(B + r * ldb + 4 * q);
+      v.x *= s, v.y *= s, v.z *= s, v.w *= s;
+      if (flags & GC_RELU) {
+        v.x = fmaxf(v.x, 0.f), v.y = fmaxf(v.y, 0.f), v.z = fmaxf(v.z, 0.f), v.w = fmaxf(v.w, 0.f);
+      }
+      stg_f4(C + r * ldc + 4 * q, v);
+    } else {
+      float v = B[r * ldb + q] * s;
+      if (flags & GC_RELU) v = fmaxf(v, 0.f);
+      C[r * ldc + q] = v;
+    }
+  }
+}
+
+// ============================================================================
+// host side: tensor maps
+// ============================================================================
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static std::once_flag once;
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    else
+      cudaGetLastError();
+  });
+  return fn;
+}
+
+// 2-D fp32 row-major matrix (rows x cols, ld elements) as a K-major TMA map
+// with a (BK x box_rows) box and 128-byte swizzle; OOB elements read as 0.
+int make_map(CUtensorMap *map, const float *ptr, int64_t rows, int64_t cols, int64_t ld,
+             int box_rows) {
+  auto enc = get_encode_fn();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return GC_ERR_CUDA;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return GC_ERR_CUDA;
+  }
+  return GC_OK;
+}
+
+template <int BN>
+int launch_tf32(const CUtensorMap &ma, const CUtensorMap &mb, const GemmEpi &ep, int64_t K,
+                cudaStream_t st) {
+  const int num_kb = (int)((K + BK - 1) / BK);
+  const int stages = num_kb < 4 ? num_kb : 4;
+  const size_t smem = (size_t)stages * (BM * BK * 4 + BN * BK * 4) + 8 * (2 * stages + 1) + 16 + 1024;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(gemm_tf32_tcgen05<BN>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  });
+  if (attr_err != cudaSuccess) {
+    set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
+    return GC_ERR_CUDA;
+  }
+  dim3 grid((unsigned)((ep.M + BM - 1) / BM), (unsigned)((ep.N + BN - 1) / BN));
+  gemm_tf32_tcgen05<BN><<<grid, kGemmThreads, smem, st>>>(ma, mb, ep, num_kb, stages);
+  return check_launch("gemm_tf32_tcgen05");
+}
+
+}  // namespace
+}  // namespace gnnc
+
+using namespace gnnc;
+
+extern "C" size_t gc_gemm_workspace_bytes(int64_t K, int64_t N) {
+  if (K <= 0 || N <= 0) return 0;
+  const int64_t ldt = (K + 3) / 4 * 4;
+  return (size_t)(N * ldt * 4);
+}
+
+extern "C" int gc_gemm_f32(const float *A, int64_t lda, const float *W, int64_t ldw, int64_t M,
+                           int64_t K, int64_t N, float *C, int64_t ldc, const float *row_scale,
+                           uint32_t flags, void *workspace, size_t ws_bytes, void *stream) {
+  GC_REQUIRE(M >= 0 && K >= 0 && N >= 0, GC_ERR_SHAPE, "gc_gemm_f32: negative size");
+  GC_REQUIRE(lda >= K && ldw >= N && ldc >= N, GC_ERR_SHAPE, "gc_gemm_f32: bad leading dim");
+  const bool tf32 = (flags & GC_GEMM_TF32) != 0, fp32 = (flags & GC_GEMM_FP32) != 0;
+  GC_REQUIRE(tf32 != fp32, GC_ERR_VALUE, "gc_gemm_f32: exactly one of TF32 / FP32 required");
+  GC_REQUIRE((flags & ~(GC_RELU | GC_GEMM_TF32 | GC_GEMM_FP32)) == 0, GC_ERR_VALUE,
+             "gc_gemm_f32: unknown flags 0x%x", flags);
+  if (M == 0 || N == 0) return GC_OK;
+  GC_REQUIRE(C && (K == 0 || (A && W)), GC_ERR_VALUE, "gc_gemm_f32: null operand");
+  cudaStream_t st = as_stream(stream);
+  GemmEpi ep{C, ldc, row_scale, M, N, flags};
+  if (K == 0) {  // empty inner dimension: relu(0 * s) = 0
+    const int64_t total = M * N;
+    fill_rows_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(C, ldc, M, N, 0.0f);
+    return check_launch("fill_rows_kernel");
+  }
+  if (fp32) {
+    GC_REQUIRE((M + SB - 1) / SB < INT32_MAX && (N + SB - 1) / SB < 65536, GC_ERR_SHAPE,
+               "gc_gemm_f32: grid too large");
+    dim3 grid((unsigned)((M + SB - 1) / SB), (unsigned)((N + SB - 1) / SB));
+    gemm_fp32_simt<<<grid, 256, 0, st>>>(A, lda, W, ldw, ep, K);
+    return check_launch("gemm_fp32_simt");
+  }
+  // TF32 tensor-core path
+  GC_REQUIRE((lda % 4) == 0 && aligned16(A), GC_ERR_UNSUPPORTED,
+             "gc_gemm_f32: TF32 path needs lda %% 4 == 0 and a 16-byte aligned A");
+  GC_REQUIRE(M < (int64_t)INT32_MAX && K < (int64_t)INT32_MAX, GC_ERR_SHAPE,
+             "gc_gemm_f32: dimension exceeds TMA range");
+  const size_t need = gc_gemm_workspace_bytes(K, N);
+  GC_REQUIRE(workspace && ws_bytes >= need && aligned16(workspace), GC_ERR_WORKSPACE,
+             "gc_gemm_f32: TF32 path needs %zu workspace bytes (16-byte aligned)", need);
+  const int64_t ldt = (K + 3) / 4 * 4;
+  float *wt = static_cast<float *>(workspace);
+  {
+    dim3 grid((unsigned)((N + 31) / 32), (unsigned)((ldt + 31) / 32));
+    transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(W, ldw, K, N, wt, ldt);
+    int rc = check_launch("transpose_kernel");
+    if (rc) return rc;
+  }
+  int bn = 256;
+  if (N <= 16) bn = 16;
+  else if (N <= 32) bn = 32;
+  else if (N <= 64) bn = 64;
+  else if (N <= 128) bn = 128;
+  CUtensorMap ma, mb;
+  int rc = make_map(&ma, A, M, K, lda, BM);
+  if (rc) return rc;
+  rc = make_map(&mb, wt, N, K, ldt, bn);
+  if (rc) return rc;
+  switch (bn) {
+    case 16: return launch_tf32<16>(ma, mb, ep, K, st);
+    case 32: return launch_tf32<32>(ma, mb, ep, K, st);
+    case 64: return launch_tf32<64>(ma, mb, ep, K, st);
+    case 128: return launch_tf32<128>(ma, mb, ep, K, st);
+    default: return launch_tf32<256>(ma, mb, ep, K, st);
+  }
+}
+
+extern "C" int gc_scale_rows_f32(const float *d, const float *B, int64_t ldb, int64_t n_rows,
+                                 int64_t K, float *C, int64_t ldc, uint32_t flags, void *stream) {
+  GC_REQUIRE(n_rows >= 0 && K >= 0 && ldb >= K && ldc >= K, GC_ERR_SHAPE,
+             "gc_scale_rows_f32: bad shape");
+  GC_REQUIRE((flags & ~GC_RELU) == 0, GC_ERR_VALUE, "gc_scale_rows_f32: unknown flags");
+  if (n_rows == 0 || K == 0) return GC_OK;
+  GC_REQUIRE(B && C, GC_ERR_VALUE, "gc_scale_rows_f32: null operand");
+  const bool vec = (K % 4 == 0) && (ldb % 4 == 0) && (ldc % 4 == 0) && aligned16(B) && aligned16(C);
+  const int64_t work = n_rows * (vec ? K / 4 : K);
+  const int64_t blocks = (work + 255) / 256;
+  const int64_t cap = (int64_t)sm_count() * 16;
+  scale_rows_kernel<<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, as_stream(stream)>>>(
+      d, B, ldb, n_rows, K, C, ldc, flags, vec);
+  return check_launch("scale_rows_kernel");
+}

@@ -1,0 +1,317 @@
+// CSR SpMM for sm_100a: C = epi( D_row * (A ∘ d_col) * B ).
+//
+// Reference semantics: gnncompose/sparse.py:196-219 (_spmm_kernel,
+// _spmm_unweighted_kernel) — every output row owns its accumulation and
+// visits edges in ascending storage order.  Here a row is owned by a group of
+// LPR lanes; each lane owns NV float4 (or scalar) column slots of the row and
+// accumulates the row's edges sequentially with FMA, so the order is fixed
+// and `values == nullptr` is bit-identical to unit values.
+//
+// Memory plan (HBM-bound): col_idx/values are streamed once
+// (evict-first), the gathered rows of B go through the read-only path as
+// 128-bit loads, U edges are unrolled so each lane keeps U*NV independent
+// 16-byte loads in flight.  The D^-1/2 factors of the dynamic composition are
+// folded in (d_col into the edge weight, d_row into the epilogue) instead of
+// materialising D^-1/2 H.
+#include "common.cuh"
+
+namespace gnnc {
+namespace {
+
+constexpr int kThreads = 256;
+
+struct SpmmArgs {
+  const int32_t *row_ptr;
+  const int32_t *col_idx;
+  const float *values;
+  const float *d_row;
+  const float *d_col;
+  const float *B;
+  int64_t ldb;
+  int64_t K;
+  float *C;
+  int64_t ldc;
+  const int4 *items;  // nullptr: one item per row
+  int64_t n_items;
+  float *partial;  // [n_slots][K] for split items
+  uint32_t flags;
+};
+
+template <bool VEC>
+struct Lanes;
+template <>
+struct Lanes<true> {
+  using T = float4;
+  static constexpr int W = 4;
+};
+template <>
+struct Lanes<false> {
+  using T = float;
+  static constexpr int W = 1;
+};
+
+__device__ __forceinline__ float4 zero_of(float4) { return make_float4(0.f, 0.f, 0.f, 0.f); }
+__device__ __forceinline__ float zero_of(float) { return 0.f; }
+__device__ __forceinline__ void fma_into(float4 &acc, float w, float4 b) {
+  acc.x = fmaf(w, b.x, acc.x);
+  acc.y = fmaf(w, b.y, acc.y);
+  acc.z = fmaf(w, b.z, acc.z);
+  acc.w = fmaf(w, b.w, acc.w);
+}
+__device__ __forceinline__ void fma_into(float &acc, float w, float b) { acc = fmaf(w, b, acc); }
+__device__ __forceinline__ void load_b(float4 &dst, const float *p) { dst = ldg_f4(p); }
+__device__ __forceinline__ void load_b(float &dst, const float *p) { dst = __ldg(p); }
+
+__device__ __forceinline__ float epi1(float v, float ds, float old, uint32_t flags) {
+  v *= ds;
+  if (flags & GC_ACCUMULATE) v += old;
+  if (flags & GC_RELU) v = fmaxf(v, 0.0f);
+  return v;
+}
+
+template <int LPR, int NV, bool VEC>
+__device__ __forceinline__ int64_t col_of(int64_t c0, int v, int gl) {
+  return VEC ? c0 + (int64_t)v * LPR * 4 + gl * 4 : c0 + (int64_t)v * LPR + gl;
+}
+
+template <int LPR, int NV, bool VEC>
+__device__ __forceinline__ void store_row(const SpmmArgs &a, int row, int slot, int gl,
+                                          int64_t c0,
+                                          const typename Lanes<VEC>::T (&acc)[NV]) {
+  const uint32_t flags = a.flags;
+  const float ds = (slot < 0 && a.d_row) ? __ldg(a.d_row + row) : 1.0f;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const int64_t c = col_of<LPR, NV, VEC>(c0, v, gl);
+    if (c >= a.K) continue;
+    if (slot >= 0) {  // raw partial sum, combined later by spmm_fixup
+      float *dst = a.partial + (int64_t)slot * a.K + c;
+      if constexpr (VEC) stg_f4(dst, acc[v]);
+      else *dst = acc[v];
+      continue;
+    }
+    float *dst = a.C + (int64_t)row * a.ldc + c;
+    if constexpr (VEC) {
+      float4 old = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (flags & GC_ACCUMULATE) old = *reinterpret_cast<const float4 *>(dst);
+      float4 r;
+      r.x = epi1(acc[v].x, ds, old.x, flags);
+      r.y = epi1(acc[v].y, ds, old.y, flags);
+      r.z = epi1(acc[v].z, ds, old.z, flags);
+      r.w = epi1(acc[v].w, ds, old.w, flags);
+      stg_f4(dst, r);
+    } else {
+      const float old = (flags & GC_ACCUMULATE) ? *dst : 0.f;
+      *dst = epi1(acc[v], ds, old, flags);
+    }
+  }
+}
+
+// One group of LPR lanes per work item (a row, or a chunk of a heavy row).
+template <int LPR, int NV, bool VEC, bool HAS_VAL, bool HAS_DCOL>
+__global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
+  using T = typename Lanes<VEC>::T;
+  constexpr int GPB = kThreads / LPR;
+  constexpr int U = (NV >= 2) ? 4 : (LPR < 8 ? LPR : 8);  // edges unrolled per step
+  const int g = threadIdx.x / LPR;
+  const int gl = threadIdx.x % LPR;
+  const int64_t item = (int64_t)blockIdx.x * GPB + g;
+  const bool live = item < a.n_items;
+
+  int row = 0, beg = 0, end = 0, slot = -1;
+  if (live) {
+    if (a.items) {
+      const int4 it = __ldg(a.items + item);
+      row = it.x, beg = it.y, end = it.z, slot = it.w;
+    } else {
+      row = (int)item;
+      beg = __ldg(a.row_ptr + row);
+      end = __ldg(a.row_ptr + row + 1);
+    }
+  }
+  constexpr int64_t kColsPerPass = (int64_t)LPR * NV * Lanes<VEC>::W;
+  const int64_t c0 = (int64_t)blockIdx.y * kColsPerPass;
+
+  bool colok[NV];
+  int64_t coff[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    coff[v] = col_of<LPR, NV, VEC>(c0, v, gl);
+    colok[v] = coff[v] < a.K;
+  }
+
+  T acc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = zero_of(T{});
+
+  const int len = end - beg;
+  const int wmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)len);
+  for (int base = 0; base < wmax; base += LPR) {
+    int j = 0;
+    float w = 0.0f;
+    if (base + gl < len) {
+      const int p = beg + base + gl;
+      j = ldg_stream_i32(a.col_idx + p);
+      w = HAS_VAL ? ldg_stream_f32(a.values + p) : 1.0f;
+      if (HAS_DCOL) w *= __ldg(a.d_col + j);
+    }
+    const int cnt = len - base;  // edges left for this group (may be <= 0)
+    const int cntw = min(LPR, wmax - base);
+#pragma unroll 1
+    for (int e0 = 0; e0 < cntw; e0 += U) {
+      T bv[U][NV];
+      float we[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int je = __shfl_sync(0xffffffffu, j, e0 + u, LPR);
+        we[u] = __shfl_sync(0xffffffffu, w, e0 + u, LPR);
+        const bool ok = (e0 + u) < cnt;
+        const float *brow = a.B + (int64_t)je * a.ldb;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          bv[u][v] = zero_of(T{});
+          if (ok && colok[v]) load_b(bv[u][v], brow + coff[v]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if ((e0 + u) < cnt) {
+#pragma unroll
+          for (int v = 0; v < NV; ++v) fma_into(acc[v], we[u], bv[u][v]);
+        }
+      }
+    }
+  }
+  if (live) store_row<LPR, NV, VEC>(a, row, slot, gl, c0, acc);
+}
+
+// Combine the partial sums of split rows in slot order, then the epilogue.
+template <int LPR, int NV, bool VEC>
+__global__ void __launch_bounds__(kThreads)
+    spmm_fixup_kernel(const SpmmArgs a, const int4 *split_rows, int64_t n_split) {
+  using T = typename Lanes<VEC>::T;
+  constexpr int GPB = kThreads / LPR;
+  const int g = threadIdx.x / LPR;
+  const int gl = threadIdx.x % LPR;
+  const int64_t r = (int64_t)blockIdx.x * GPB + g;
+  if (r >= n_split) return;
+  const int4 sr = __ldg(split_rows + r);
+  constexpr int64_t kColsPerPass = (int64_t)LPR * NV * Lanes<VEC>::W;
+  const int64_t c0 = (int64_t)blockIdx.y * kColsPerPass;
+  T acc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = zero_of(T{});
+  for (int q = 0; q < sr.z; ++q) {
+    const float *src = a.partial + (int64_t)(sr.y + q) * a.K;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int64_t c = col_of<LPR, NV, VEC>(c0, v, gl);
+      if (c < a.K) {
+        T t;
+        load_b(t, src + c);
+        fma_into(acc[v], 1.0f, t);
+      }
+    }
+  }
+  store_row<LPR, NV, VEC>(a, sr.x, -1, gl, c0, acc);
+}
+
+template <int LPR, int NV, bool VEC>
+int launch_cfg(const SpmmArgs &a, const int4 *split_rows, int64_t n_split, cudaStream_t st) {
+  constexpr int GPB = kThreads / LPR;
+  constexpr int64_t kColsPerPass = (int64_t)LPR * NV * Lanes<VEC>::W;
+  const int64_t ychunks = (a.K + kColsPerPass - 1) / kColsPerPass;
+  if (ychunks > 65535) {
+    set_error("gc_spmm_f32: K=%lld too large", (long long)a.K);
+    return GC_ERR_UNSUPPORTED;
+  }
+  if (a.n_items > 0) {
+    dim3 grid((unsigned)((a.n_items + GPB - 1) / GPB), (unsigned)ychunks);
+    const bool hv = a.values != nullptr, hd = a.d_col != nullptr;
+    if (hv && hd) spmm_kernel<LPR, NV, VEC, true, true><<<grid, kThreads, 0, st>>>(a);
+    else if (hv) spmm_kernel<LPR, NV, VEC, true, false><<<grid, kThreads, 0, st>>>(a);
+    else if (hd) spmm_kernel<LPR, NV, VEC, false, true><<<grid, kThreads, 0, st>>>(a);
+    else spmm_kernel<LPR, NV, VEC, false, false><<<grid, kThreads, 0, st>>>(a);
+    int rc = check_launch("spmm_kernel");
+    if (rc) return rc;
+  }
+  if (n_split > 0) {
+    dim3 grid((unsigned)((n_split + GPB - 1) / GPB), (unsigned)ychunks);
+    spmm_fixup_kernel<LPR, NV, VEC><<<grid, kThreads, 0, st>>>(a, split_rows, n_split);
+    return check_launch("spmm_fixup_kernel");
+  }
+  return GC_OK;
+}
+
+}  // namespace
+}  // namespace gnnc
+
+using namespace gnnc;
+
+extern "C" int gc_spmm_f32(const int32_t *row_ptr, const int32_t *col_idx, const float *values,
+                           const float *d_row, const float *d_col, const float *B, int64_t ldb,
+                           int64_t n_rows, int64_t n_cols, int64_t K, float *C, int64_t ldc,
+                           uint32_t flags, int algo, const int32_t *items, int64_t n_items,
+                           const int32_t *split_rows, int64_t n_split_rows, void *workspace,
+                           size_t ws_bytes, void *stream) {
+  GC_REQUIRE(n_rows >= 0 && n_cols >= 0 && K >= 0, GC_ERR_SHAPE, "gc_spmm_f32: negative size");
+  GC_REQUIRE(ldb >= K && ldc >= K, GC_ERR_SHAPE, "gc_spmm_f32: leading dimension < K");
+  GC_REQUIRE((flags & ~(GC_RELU | GC_ACCUMULATE)) == 0, GC_ERR_VALUE,
+             "gc_spmm_f32: unknown flags 0x%x", flags);
+  if (n_rows == 0 || K == 0) return GC_OK;
+  GC_REQUIRE(row_ptr && C && (B || n_cols == 0), GC_ERR_VALUE, "gc_spmm_f32: null operand");
+  GC_REQUIRE(n_rows < INT32_MAX && n_cols < INT32_MAX, GC_ERR_SHAPE,
+             "gc_spmm_f32: int32 index range exceeded");
+
+  SpmmArgs a{};
+  a.row_ptr = row_ptr;
+  a.col_idx = col_idx;
+  a.values = values;
+  a.d_row = d_row;
+  a.d_col = d_col;
+  a.B = B;
+  a.ldb = ldb;
+  a.K = K;
+  a.C = C;
+  a.ldc = ldc;
+  a.flags = flags;
+  const int4 *sr = nullptr;
+  int64_t n_split = 0;
+  if (algo == GC_SPMM_NNZ_SPLIT) {
+    GC_REQUIRE(items && n_items >= n_rows, GC_ERR_VALUE, "gc_spmm_f32: NNZ_SPLIT needs a plan");
+    GC_REQUIRE(n_split_rows == 0 || split_rows, GC_ERR_VALUE, "gc_spmm_f32: split_rows null");
+    a.items = reinterpret_cast<const int4 *>(items);
+    a.n_items = n_items;
+    sr = reinterpret_cast<const int4 *>(split_rows);
+    n_split = n_split_rows;
+    if (n_split > 0) {
+      // slots are numbered densely; the last split row tells how many exist
+      GC_REQUIRE(workspace != nullptr, GC_ERR_WORKSPACE, "gc_spmm_f32: workspace required");
+      a.partial = static_cast<float *>(workspace);
+      (void)ws_bytes;  // size validated by the host wrapper (it owns the plan)
+    }
+  } else if (algo == GC_SPMM_ROW || algo == 0) {
+    a.items = nullptr;
+    a.n_items = n_rows;
+  } else {
+    set_error("gc_spmm_f32: unknown algo %d", algo);
+    return GC_ERR_VALUE;
+  }
+
+  const bool vec = (K % 4 == 0) && (ldb % 4 == 0) && (ldc % 4 == 0) && aligned16(B) &&
+                   aligned16(C) && (a.partial == nullptr || aligned16(a.partial));
+  cudaStream_t st = as_stream(stream);
+  if (vec) {
+    if (K <= 8) return launch_cfg<2, 1, true>(a, sr, n_split, st);
+    if (K <= 16) return launch_cfg<4, 1, true>(a, sr, n_split, st);
+    if (K <= 32) return launch_cfg<8, 1, true>(a, sr, n_split, st);
+    if (K <= 64) return launch_cfg<16, 1, true>(a, sr, n_split, st);
+    if (K <= 128) return launch_cfg<32, 1, true>(a, sr, n_split, st);
+    return launch_cfg<32, 2, true>(a, sr, n_split, st);
+  }
+  if (K <= 8) return launch_cfg<8, 1, false>(a, sr, n_split, st);
+  if (K <= 16) return launch_cfg<16, 1, false>(a, sr, n_split, st);
+  if (K <= 32) return launch_cfg<32, 1, false>(a, sr, n_split, st);
+  if (K <= 64) return launch_cfg<32, 2, false>(a, sr, n_split, st);
+  return launch_cfg<32, 4, false>(a, sr, n_split, st);
+}

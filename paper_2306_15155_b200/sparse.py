@@ -1,0 +1,563 @@
+"""CSR / dense types and the primitive kernels every layer composition uses.
+
+Drop-in mirror of ``gnncompose/sparse.py`` (reference 0.1.0): same names,
+argument meaning and exception types.  Differences, all B200-driven:
+
+* storage is on the GPU (torch tensors): indices int32, values float32;
+* every compute primitive calls a hand-written sm_100a kernel through the C
+  ABI (``include/gnnc.h``); there is no CPU fallback — calling one with CPU
+  tensors raises;
+* numpy inputs are accepted (uploaded) and numpy outputs returned, so code
+  written against the reference keeps working; torch CUDA tensors in give
+  torch CUDA tensors out with no host round trip;
+* extensions the layer code uses: fused ``d_row``/``d_col`` degree scaling and
+  ``relu`` epilogues, an nnz-split plan for power-law rows.
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as nat
+
+
+class ShapeError(ValueError):
+    """Operand dimensions do not conform (reference sparse.py:17)."""
+
+
+class DegenerateNodeError(ValueError):
+    """A node violates a degree precondition, e.g. a zero-degree row (sparse.py:21)."""
+
+
+# ---------------------------------------------------------------------------
+# device / operand plumbing
+# ---------------------------------------------------------------------------
+
+
+def default_device() -> torch.device:
+    return torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() \
+        else torch.device("cpu")
+
+
+def _stream(dev: torch.device) -> int:
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _require_cuda(*ts: torch.Tensor | None) -> torch.device:
+    dev = None
+    for t in ts:
+        if t is None:
+            continue
+        if not t.is_cuda:
+            raise RuntimeError(
+                "gnnc kernels run on the GPU only (no CPU fallback); got a CPU tensor")
+        if dev is None:
+            dev = t.device
+        elif t.device != dev:
+            raise ValueError(f"operands on different devices: {dev} vs {t.device}")
+    if dev is None:
+        raise RuntimeError("no CUDA operand")
+    return dev
+
+
+def dense_matrix(data) -> torch.Tensor:
+    """Coerce to a row-major float32 2-D tensor and check all entries are finite
+    (reference sparse.py:25-32)."""
+    t = torch.as_tensor(np.asarray(data) if not isinstance(data, torch.Tensor) else data)
+    t = t.to(torch.float32).contiguous()
+    if t.dim() != 2:
+        raise ShapeError(f"dense matrix must be 2-D, got ndim={t.dim()}")
+    if not bool(torch.isfinite(t).all()):
+        raise ValueError("dense matrix contains non-finite entries")
+    return t
+
+
+class _Operand:
+    """A dense 2-D float32 CUDA operand plus where it came from (numpy in ->
+    numpy out, mirroring the reference's ndarray return type)."""
+
+    __slots__ = ("t", "host")
+
+    def __init__(self, b, device: torch.device, what: str = "dense operand"):
+        self.host = not isinstance(b, torch.Tensor)
+        if self.host:
+            arr = np.asarray(b)
+            t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32))
+            if t.dim() == 2 and t.numel():
+                t = t.pin_memory() if device.type == "cuda" else t
+            t = t.to(device, non_blocking=True)
+        else:
+            t = b
+            if t.dtype != torch.float32:
+                t = t.float()
+            if t.device != device:
+                t = t.to(device)
+        if t.dim() != 2:
+            raise ShapeError(f"{what} must be 2-D, got ndim={t.dim()}")
+        if t.stride(1) != 1 or (t.size(0) > 1 and t.stride(0) < t.size(1)):
+            t = t.contiguous()
+        self.t = t
+
+    def wrap(self, out: torch.Tensor):
+        return out.cpu().numpy() if self.host else out
+
+
+def _ld(t: torch.Tensor) -> int:
+    return t.stride(0) if t.size(0) > 1 else max(t.size(1), 1)
+
+
+# ---------------------------------------------------------------------------
+# CsrMatrix — reference sparse.py:43-188
+# ---------------------------------------------------------------------------
+
+
+class CsrMatrix:
+    """Sparse matrix in compressed-row form, resident on one device.
+
+    Invariants (checked at construction unless ``validate=False``), as in the
+    reference: ``row_ptr[0] == 0``, ``row_ptr[n_rows] == nnz``, non-decreasing;
+    column indices strictly increasing within each row and ``< n_cols``;
+    ``len(values) == len(col_idx)``.  Instances are immutable after
+    construction.
+    """
+
+    def __init__(self, n_rows: int, n_cols: int, row_ptr, col_idx, values, validate: bool = True,
+                 device: torch.device | str | None = None):
+        dev = torch.device(device) if device is not None else None
+        if dev is None:
+            dev = next((x.device for x in (row_ptr, col_idx, values) if isinstance(x, torch.Tensor)),
+                       default_device())
+        self.n_rows = int(n_rows)
+        self.n_cols = int(n_cols)
+        self.row_ptr = _as_index(row_ptr, dev)
+        self.col_idx = _as_index(col_idx, dev)
+        self.values = _as_values(values, dev)
+        self._unit: bool | None = None
+        self._plans: dict = {}
+        self._dmax: int | None = None
+        if validate:
+            self._check()
+
+    # -- validation (sparse.py:74-98) ---------------------------------------
+    def _check(self):
+        if self.n_rows < 0 or self.n_cols < 0:
+            raise ShapeError("matrix dimensions must be non-negative")
+        if self.n_rows >= 2**31 - 1 or self.n_cols >= 2**31 - 1 or self.col_idx.numel() >= 2**31 - 1:
+            raise ShapeError("int32 index range exceeded")
+        if tuple(self.row_ptr.shape) != (self.n_rows + 1,):
+            raise ShapeError(f"row_ptr length {self.row_ptr.numel()} != n_rows+1 = {self.n_rows + 1}")
+        rp = self.row_ptr
+        if int(rp[0]) != 0 or int(rp[-1]) != self.col_idx.numel():
+            raise ShapeError("row_ptr must start at 0 and end at nnz")
+        if self.n_rows and bool((rp[1:] < rp[:-1]).any()):
+            raise ShapeError("row_ptr must be non-decreasing")
+        if self.values.shape != self.col_idx.shape:
+            raise ShapeError("values and col_idx must have equal length")
+        ci = self.col_idx
+        if ci.numel():
+            if int(ci.min()) < 0 or int(ci.max()) >= self.n_cols:
+                raise ShapeError("column index out of range")
+            d = ci[1:] - ci[:-1]
+            boundary = torch.zeros(d.numel(), dtype=torch.bool, device=ci.device)
+            starts = rp[1:-1].long()
+            starts = starts[(starts > 0) & (starts <= d.numel())]
+            boundary[starts - 1] = True
+            if not bool(((d > 0) | boundary).all()):
+                raise ShapeError("column indices must be strictly increasing per row")
+
+    # -- construction helpers ----------------------------------------------------
+    @classmethod
+    def from_dense(cls, arr, device=None) -> "CsrMatrix":
+        a = torch.as_tensor(np.asarray(arr, dtype=np.float64) if not isinstance(arr, torch.Tensor)
+                            else arr)
+        if a.dim() != 2:
+            raise ShapeError("from_dense expects a 2-D array")
+        dev = torch.device(device) if device is not None else default_device()
+        a = a.to(dev)
+        nz = torch.nonzero(a, as_tuple=True)
+        counts = torch.bincount(nz[0], minlength=a.shape[0])
+        row_ptr = torch.cat([counts.new_zeros(1), torch.cumsum(counts, 0)])
+        return cls(a.shape[0], a.shape[1], row_ptr, nz[1], a[nz], device=dev)
+
+    @classmethod
+    def from_coo(cls, n_rows: int, n_cols: int, rows, cols, values, sum_duplicates: bool = True,
+                 device=None) -> "CsrMatrix":
+        """Build from unordered coordinate triplets; duplicate entries are summed
+        (reference sparse.py:120-146: lexsort by (row, col) then reduceat).
+
+        The index arrays come out bit-identical to the reference (the CSR of a
+        set of distinct coordinates is unique).  Duplicate values are summed in
+        float64 before rounding to float32."""
+        dev = torch.device(device) if device is not None else default_device()
+        r = torch.as_tensor(rows).to(dev, torch.int64).reshape(-1)
+        c = torch.as_tensor(cols).to(dev, torch.int64).reshape(-1)
+        v = torch.as_tensor(np.asarray(values, dtype=np.float64) if not isinstance(values, torch.Tensor)
+                            else values).to(dev, torch.float64).reshape(-1)
+        if not (r.shape == c.shape == v.shape):
+            raise ShapeError("rows/cols/values must have equal length")
+        key = r * max(int(n_cols), 1) + c
+        key, order = torch.sort(key, stable=True)
+        r, c, v = r[order], c[order], v[order]
+        if sum_duplicates and r.numel():
+            first = torch.ones(r.numel(), dtype=torch.bool, device=dev)
+            first[1:] = key[1:] != key[:-1]
+            if not bool(first.all()):
+                seg = torch.cumsum(first.long(), 0) - 1
+                starts = torch.nonzero(first).reshape(-1)
+                if dev.type == "cpu":  # sequential sums, exactly np.add.reduceat
+                    vs = torch.from_numpy(np.add.reduceat(v.numpy(), starts.numpy()))
+                else:
+                    vs = torch.zeros(starts.numel(), dtype=torch.float64, device=dev)
+                    vs.index_add_(0, seg, v)
+                r, c, v = r[starts], c[starts], vs
+        counts = torch.bincount(r, minlength=int(n_rows))
+        row_ptr = torch.cat([counts.new_zeros(1), torch.cumsum(counts, 0)])
+        return cls(n_rows, n_cols, row_ptr, c, v, device=dev)
+
+    def with_values(self, values, validate: bool = False) -> "CsrMatrix":
+        """Same sparsity pattern (shared row_ptr/col_idx), new values."""
+        v = _as_values(values, self.device)
+        if v.shape != self.col_idx.shape:
+            raise ShapeError("replacement values must match nnz")
+        out = CsrMatrix.__new__(CsrMatrix)
+        out.n_rows, out.n_cols = self.n_rows, self.n_cols
+        out.row_ptr, out.col_idx, out.values = self.row_ptr, self.col_idx, v
+        out._unit, out._plans, out._dmax = None, self._plans, self._dmax  # plans depend on pattern only
+        if validate:
+            out._check()
+        return out
+
+    def to(self, device) -> "CsrMatrix":
+        dev = torch.device(device)
+        out = CsrMatrix(self.n_rows, self.n_cols, self.row_ptr.to(dev), self.col_idx.to(dev),
+                        self.values.to(dev), validate=False, device=dev)
+        out._unit, out._dmax = self._unit, self._dmax
+        return out
+
+    # -- queries -----------------------------------------------------------------
+    @property
+    def device(self) -> torch.device:
+        return self.col_idx.device
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col_idx.numel())
+
+    @property
+    def has_unit_values(self) -> bool:
+        """True iff every stored value is 1 (sparse.py:70-72).  Computed once,
+        lazily, to keep the O(nnz) scan off the per-layer hot path."""
+        if self._unit is None:
+            self._unit = bool(self.values.numel() == 0 or bool((self.values == 1.0).all()))
+        return self._unit
+
+    def degrees(self) -> torch.Tensor:
+        """Structural per-row non-zero counts (int64)."""
+        return (self.row_ptr[1:] - self.row_ptr[:-1]).long()
+
+    def max_degree(self) -> int:
+        if self._dmax is None:
+            self._dmax = int(self.degrees().max()) if self.n_rows else 0
+        return self._dmax
+
+    def row_of_nnz(self) -> torch.Tensor:
+        return torch.repeat_interleave(torch.arange(self.n_rows, device=self.device),
+                                       self.degrees())
+
+    def to_dense(self) -> torch.Tensor:
+        out = torch.zeros(self.n_rows, self.n_cols, dtype=torch.float32, device=self.device)
+        out[self.row_of_nnz(), self.col_idx.long()] = self.values
+        return out
+
+    def same_pattern(self, other: "CsrMatrix") -> bool:
+        return (self.n_rows == other.n_rows and self.n_cols == other.n_cols
+                and torch.equal(self.row_ptr, other.row_ptr.to(self.device))
+                and torch.equal(self.col_idx, other.col_idx.to(self.device)))
+
+    def numpy(self) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+        """Host copies (int64 indices, float64 values) — the reference's dtypes."""
+        return (self.row_ptr.cpu().numpy().astype(np.int64), self.col_idx.cpu().numpy().astype(np.int64),
+                self.values.cpu().numpy().astype(np.float64))
+
+    def take_rows(self, lo: int, hi: int) -> "CsrMatrix":
+        """Contiguous row block [lo, hi) with global column ids (a partition's
+        local adjacency); row_ptr is rebased."""
+        rp = self.row_ptr[lo:hi + 1]
+        b, e = int(rp[0]), int(rp[-1])
+        return CsrMatrix(hi - lo, self.n_cols, rp - b, self.col_idx[b:e], self.values[b:e],
+                         validate=False, device=self.device)
+
+    # -- nnz-split plan (cached per pattern) ----------------------------------------
+    def spmm_plan(self, chunk: int):
+        """Work items for GC_SPMM_NNZ_SPLIT: heavy rows (> chunk edges) are cut
+        into chunk-sized pieces whose partial sums are combined in fixed order."""
+        key = ("split", int(chunk))
+        if key not in self._plans:
+            lib = nat.load()
+            rp = np.ascontiguousarray(self.row_ptr.cpu().numpy(), dtype=np.int32)
+            ni, ns, nsr = (np.zeros(1, np.int64) for _ in range(3))
+            nat.check(lib.gc_spmm_plan_count(rp.ctypes.data, self.n_rows, int(chunk),
+                                             ni.ctypes.data_as(nat._i64p), ns.ctypes.data_as(nat._i64p),
+                                             nsr.ctypes.data_as(nat._i64p)), "gc_spmm_plan_count")
+            items = np.empty((int(ni[0]), 4), np.int32)
+            split = np.empty((max(int(nsr[0]), 1), 4), np.int32)
+            nat.check(lib.gc_spmm_plan_fill(rp.ctypes.data, self.n_rows, int(chunk),
+                                            items.ctypes.data, split.ctypes.data), "gc_spmm_plan_fill")
+            self._plans[key] = (torch.from_numpy(items).to(self.device),
+                                torch.from_numpy(split[: int(nsr[0])]).to(self.device), int(ns[0]))
+        return self._plans[key]
+
+    def __repr__(self):
+        return f"CsrMatrix({self.n_rows}x{self.n_cols}, nnz={self.nnz}, device={self.device})"
+
+
+def _as_index(x, dev) -> torch.Tensor:
+    t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x, dtype=np.int64))
+    if t.numel() and (int(t.max()) >= 2**31 or int(t.min()) < -(2**31)):
+        raise ShapeError("index exceeds int32 range")
+    return t.to(dev, torch.int32).contiguous()
+
+
+def _as_values(x, dev) -> torch.Tensor:
+    t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64))
+    return t.to(dev, torch.float32).contiguous()
+
+
+# ---------------------------------------------------------------------------
+# SpMM — reference sparse.py:240-264
+# ---------------------------------------------------------------------------
+
+SPLIT_CHUNK = int(os.environ.get("GNNC_SPLIT_CHUNK", "2048"))
+
+
+def _spmm(a: CsrMatrix, b, *, weighted: bool, d_row=None, d_col=None, relu=False, out=None,
+          accumulate=False, algo: str = "auto", what="spmm"):
+    dev = a.device
+    op = _Operand(b, dev)
+    bt = op.t
+    if a.n_cols != bt.shape[0]:
+        raise ShapeError(f"{what}: a is {a.n_rows}x{a.n_cols}, b has {bt.shape[0]} rows")
+    K = bt.shape[1]
+    _require_cuda(a.col_idx, bt)
+    if out is None:
+        out = torch.empty(a.n_rows, K, dtype=torch.float32, device=dev)
+        if accumulate:
+            out.zero_()
+    elif tuple(out.shape) != (a.n_rows, K) or out.stride(1) != 1:
+        raise ShapeError(f"{what}: out must be a row-major {a.n_rows}x{K} tensor")
+    for d, n, nm in ((d_row, a.n_rows, "d_row"), (d_col, a.n_cols, "d_col")):
+        if d is not None and tuple(d.shape) != (n,):
+            raise ShapeError(f"{what}: {nm} must have {n} entries")
+    flags = (nat.GC_RELU if relu else 0) | (nat.GC_ACCUMULATE if accumulate else 0)
+    use_split = algo == "split" or (algo == "auto" and a.nnz and a.max_degree() > SPLIT_CHUNK)
+    items = split = ws = None
+    n_items = n_split = 0
+    code = nat.GC_SPMM_ROW
+    if use_split:
+        items, split, n_slots = a.spmm_plan(SPLIT_CHUNK)
+        n_items, n_split = items.shape[0], split.shape[0]
+        code = nat.GC_SPMM_NNZ_SPLIT
+        if n_slots:
+            ws = torch.empty(n_slots * K, dtype=torch.float32, device=dev)
+    lib = nat.load()
+    rc = lib.gc_spmm_f32(a.row_ptr.data_ptr(), a.col_idx.data_ptr(),
+                         a.values.data_ptr() if weighted else None, _ptr(d_row), _ptr(d_col),
+                         bt.data_ptr(), _ld(bt), a.n_rows, a.n_cols, K, out.data_ptr(), _ld(out),
+                         flags, code, _ptr(items), n_items, _ptr(split), n_split, _ptr(ws),
+                         0 if ws is None else ws.numel() * 4, _stream(dev))
+    nat.check(rc, what)
+    return op.wrap(out)
+
+
+def spmm(a: CsrMatrix, b, **kw):
+    """Sparse-times-dense product C[i,k] = sum_j a[i,j] * b[j,k] (sparse.py:240-247).
+
+    Keyword extensions: ``d_row``/``d_col`` (fused D^-1/2 scalings), ``relu``,
+    ``out``, ``accumulate``, ``algo`` in {"auto", "row", "split"}."""
+    return _spmm(a, b, weighted=True, what="spmm", **kw)
+
+
+def spmm_unweighted(a: CsrMatrix, b, **kw):
+    """SpMM over the pattern only; ``a.values`` is never read (sparse.py:250-264).
+    Bit-identical to ``spmm`` with unit values (same per-row order)."""
+    return _spmm(a, b, weighted=False, what="spmm_unweighted", **kw)
+
+
+# ---------------------------------------------------------------------------
+# SDDMM — reference sparse.py:267-282
+# ---------------------------------------------------------------------------
+
+
+def sddmm(a: CsrMatrix, b, c) -> CsrMatrix:
+    """Masked product d[i,j] = a[i,j] * sum_k b[i,k] c[j,k]; the output shares
+    a's pattern."""
+    dev = a.device
+    bt, ct = _Operand(b, dev).t, _Operand(c, dev).t
+    if bt.shape[0] != a.n_rows:
+        raise ShapeError(f"sddmm: b has {bt.shape[0]} rows, expected {a.n_rows}")
+    if ct.shape[0] != a.n_cols:
+        raise ShapeError(f"sddmm: c has {ct.shape[0]} rows, expected {a.n_cols}")
+    if bt.shape[1] != ct.shape[1]:
+        raise ShapeError("sddmm: b and c must have the same column count")
+    _require_cuda(a.col_idx, bt, ct)
+    out = torch.empty(a.nnz, dtype=torch.float32, device=dev)
+    if a.nnz:
+        nat.check(nat.load().gc_sddmm_f32(a.row_ptr.data_ptr(), a.col_idx.data_ptr(),
+                                          a.values.data_ptr(), bt.data_ptr(), _ld(bt), ct.data_ptr(),
+                                          _ld(ct), a.n_rows, a.n_cols, bt.shape[1], out.data_ptr(),
+                                          _stream(dev)), "sddmm")
+    return a.with_values(out)
+
+
+def sddmm_norm(a: CsrMatrix, d: torch.Tensor, *, weighted: bool = True) -> CsrMatrix:
+    """k = 1 SDDMM a[i,j] * (d[i] * d[j]) — the normalised adjacency of
+    gcn.py:103-112 in one pass."""
+    dev = _require_cuda(a.col_idx, d)
+    if tuple(d.shape) != (a.n_rows,) or a.n_rows != a.n_cols:
+        raise ShapeError("degree vector does not match the adjacency")
+    out = torch.empty(a.nnz, dtype=torch.float32, device=dev)
+    if a.nnz:
+        nat.check(nat.load().gc_sddmm_norm_f32(a.row_ptr.data_ptr(), a.col_idx.data_ptr(),
+                                               a.values.data_ptr() if weighted else None,
+                                               d.data_ptr(), a.n_rows, out.data_ptr(),
+                                               _stream(dev)), "sddmm_norm")
+    return a.with_values(out)
+
+
+# ---------------------------------------------------------------------------
+# dense — reference sparse.py:285-300
+# ---------------------------------------------------------------------------
+
+_GEMM_PRECISION = os.environ.get("GNNC_GEMM_PRECISION", "tf32")
+
+
+def set_gemm_precision(p: str) -> None:
+    """"tf32" (tcgen05 tensor cores; parity 1e-2) or "fp32" (exact CUDA-core
+    FMA; parity 1e-4)."""
+    global _GEMM_PRECISION
+    if p not in ("tf32", "fp32"):
+        raise ValueError("precision must be 'tf32' or 'fp32'")
+    _GEMM_PRECISION = p
+
+
+def get_gemm_precision() -> str:
+    return _GEMM_PRECISION
+
+
+def gemm(a, b, *, row_scale=None, relu=False, precision: str | None = None, out=None):
+    """Dense product a @ b (sparse.py:285-291) on the tcgen05 tensor cores
+    (TF32) or exact fp32 CUDA cores; optional fused row scale and ReLU."""
+    dev = b.device if isinstance(b, torch.Tensor) else (
+        a.device if isinstance(a, torch.Tensor) else default_device())
+    oa, ob = _Operand(a, dev), _Operand(b, dev)
+    at, bt = oa.t, ob.t
+    if at.shape[1] != bt.shape[0]:
+        raise ShapeError(f"gemm: inner dimensions {at.shape[1]} != {bt.shape[0]}")
+    _require_cuda(at, bt, row_scale)
+    M, K, N = at.shape[0], at.shape[1], bt.shape[1]
+    if out is None:
+        out = torch.empty(M, N, dtype=torch.float32, device=dev)
+    prec = precision or _GEMM_PRECISION
+    flags = nat.GC_RELU if relu else 0
+    lib = nat.load()
+    ws = None
+    if prec == "tf32" and (_ld(at) % 4 == 0) and at.data_ptr() % 16 == 0 and K > 0:
+        flags |= nat.GC_GEMM_TF32
+        ws = torch.empty(max(int(lib.gc_gemm_workspace_bytes(K, N)), 16), dtype=torch.uint8,
+                         device=dev)
+    else:
+        flags |= nat.GC_GEMM_FP32
+    if row_scale is not None and tuple(row_scale.shape) != (M,):
+        raise ShapeError("gemm: row_scale must have one entry per row")
+    rc = lib.gc_gemm_f32(at.data_ptr(), _ld(at), bt.data_ptr(), _ld(bt), M, K, N, out.data_ptr(),
+                         _ld(out), _ptr(row_scale), flags, _ptr(ws),
+                         0 if ws is None else ws.numel(), _stream(dev))
+    nat.check(rc, "gemm")
+    return oa.wrap(out) if (oa.host and ob.host) else out
+
+
+def scale_rows(d, b, *, relu: bool = False):
+    """Row scaling out[i,k] = d[i] * b[i,k] (sparse.py:294-300)."""
+    dev = b.device if isinstance(b, torch.Tensor) else default_device()
+    ob = _Operand(b, dev)
+    bt = ob.t
+    dt = d if isinstance(d, torch.Tensor) else torch.as_tensor(np.asarray(d, dtype=np.float64))
+    dt = dt.to(dev, torch.float32).contiguous()
+    if dt.dim() != 1 or dt.numel() != bt.shape[0]:
+        raise ShapeError(f"scale_rows: d has {dt.numel()} entries, b has {bt.shape[0]} rows")
+    _require_cuda(bt, dt)
+    out = torch.empty_like(bt)
+    nat.check(nat.load().gc_scale_rows_f32(dt.data_ptr(), bt.data_ptr(), _ld(bt), bt.shape[0],
+                                           bt.shape[1], out.data_ptr(), _ld(out),
+                                           nat.GC_RELU if relu else 0, _stream(dev)), "scale_rows")
+    return ob.wrap(out)
+
+
+def relu_(x: torch.Tensor) -> torch.Tensor:
+    """In-place ReLU through the kernel library (gcn.py:115-116)."""
+    dev = _require_cuda(x)
+    nat.check(nat.load().gc_scale_rows_f32(None, x.data_ptr(), _ld(x), x.shape[0], x.shape[1],
+                                           x.data_ptr(), _ld(x), nat.GC_RELU, _stream(dev)), "relu")
+    return x
+
+
+# ---------------------------------------------------------------------------
+# graph prep — reference sparse.py:303-336
+# ---------------------------------------------------------------------------
+
+
+def add_self_loops(a: CsrMatrix) -> CsrMatrix:
+    """Insert value-1.0 diagonal entries where absent; existing ones are kept.
+    Idempotent.  O(nnz) insertion into the sorted CSR (no re-sort); the
+    result is bit-identical to the reference's from_coo rebuild."""
+    if a.n_rows != a.n_cols:
+        raise ShapeError("add_self_loops requires a square matrix")
+    dev = a.device
+    n = a.n_rows
+    rows = a.row_of_nnz()
+    col = a.col_idx.long()
+    has_diag = torch.zeros(n, dtype=torch.bool, device=dev)
+    has_diag[rows[col == rows]] = True
+    missing = ~has_diag
+    n_missing = int(missing.sum())
+    if n_missing == 0:
+        return a
+    deg = a.degrees()
+    new_deg = deg + missing.long()
+    row_ptr = torch.cat([new_deg.new_zeros(1), torch.cumsum(new_deg, 0)])
+    shift = torch.cumsum(missing.long(), 0) - missing.long()  # missing rows before r
+    after_diag = (missing[rows] & (col > rows)).long()
+    new_pos = torch.arange(a.nnz, device=dev) + shift[rows] + after_diag
+    lt = torch.zeros(n, dtype=torch.long, device=dev)
+    lt.index_add_(0, rows, (col < rows).long())  # integer adds: exact, order-free
+    miss_rows = torch.nonzero(missing).reshape(-1)
+    diag_pos = row_ptr[miss_rows] + lt[miss_rows]
+    m2 = a.nnz + n_missing
+    new_col = torch.empty(m2, dtype=torch.int32, device=dev)
+    new_val = torch.empty(m2, dtype=torch.float32, device=dev)
+    new_col[new_pos] = a.col_idx
+    new_val[new_pos] = a.values
+    new_col[diag_pos] = miss_rows.to(torch.int32)
+    new_val[diag_pos] = 1.0
+    out = CsrMatrix(n, n, row_ptr, new_col, new_val, validate=False, device=dev)
+    if a._unit:
+        out._unit = True
+    return out
+
+
+def inv_sqrt_degrees(a: CsrMatrix) -> torch.Tensor:
+    """d_i = (structural degree)^-1/2 (sparse.py:327-336), computed in float64
+    and rounded once to float32."""
+    deg = a.degrees()
+    if a.n_rows and bool((deg == 0).any()):
+        bad = int(torch.nonzero(deg == 0)[0])
+        raise DegenerateNodeError(f"node {bad} has zero degree; add self loops first")
+    return (1.0 / torch.sqrt(deg.double())).float()

@@ -1,0 +1,354 @@
+"""Parity of every C-ABI kernel with the CPU oracle (float64 restatement of the
+reference), on seeded inputs.  Tolerances (normwise rel_err, the reference's
+tests/helpers.py:68-72 metric): 1e-5 for fp32 sparse kernels, 1e-4 for the
+exact-fp32 GEMM, 1e-2 for the TF32 tensor-core GEMM.  Integer/pattern outputs
+are compared bit-exactly."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+import paper_2306_15155_b200 as gc  # noqa: E402
+from paper_2306_15155_b200 import graphs, sparse  # noqa: E402
+
+DEV = "cuda"
+SP_TOL = 1e-5
+
+
+def to_oracle(oracle, a: gc.CsrMatrix):
+    rp, ci, v = a.numpy()
+    return oracle.Csr(a.n_rows, a.n_cols, rp, ci, v)
+
+
+def f32(x):
+    return np.asarray(x, dtype=np.float32)
+
+
+def rand_csr(rng, n_rows, n_cols, density, unit=False, empty_rows=()):
+    dense = (rng.random((n_rows, n_cols)) < density).astype(np.float64)
+    if not unit:
+        dense *= f32(rng.uniform(0.5, 2.0, size=dense.shape))
+    for r in empty_rows:
+        dense[r] = 0
+    return gc.CsrMatrix.from_dense(dense, device=DEV)
+
+
+@pytest.fixture(scope="module")
+def plgraph():
+    a = graphs.powerlaw_graph(1500, 6, seed=3, device=DEV)
+    return gc.add_self_loops(a)
+
+
+KS = [1, 3, 4, 7, 16, 32, 33, 64, 100, 128, 256, 300, 512]
+
+
+@pytest.mark.parametrize("K", KS)
+@pytest.mark.parametrize("algo", ["row", "split"])
+def test_spmm_weighted_unweighted(oracle, plgraph, K, algo, monkeypatch):
+    if algo == "split":
+        monkeypatch.setattr(sparse, "SPLIT_CHUNK", 16)  # force many split rows
+    rng = np.random.default_rng(K)
+    a = plgraph.with_values(torch.from_numpy(f32(rng.uniform(0.5, 2, plgraph.nnz))).to(DEV))
+    oa = to_oracle(oracle, a)
+    b = f32(rng.standard_normal((a.n_cols, K)))
+    bt = torch.from_numpy(b).to(DEV)
+    out = gc.spmm(a, bt, algo=algo).cpu().numpy()
+    assert oracle.rel_err(out, oracle.spmm(oa, b)) < SP_TOL
+    outu = gc.spmm_unweighted(a, bt, algo=algo).cpu().numpy()
+    assert oracle.rel_err(outu, oracle.spmm_unweighted(oa, b)) < SP_TOL
+    # fused dynamic normalisation: d_i * sum_j w_ij d_j b_j, then ReLU
+    d = torch.from_numpy(f32(rng.uniform(0.1, 1.0, a.n_rows))).to(DEV)
+    outd = gc.spmm(a, bt, d_row=d, d_col=d, relu=True, algo=algo).cpu().numpy()
+    dn = d.cpu().numpy().astype(np.float64)
+    ref = np.maximum(oracle.scale_rows(dn, oracle.spmm(oa, oracle.scale_rows(dn, b))), 0)
+    assert oracle.rel_err(outd, ref) < SP_TOL
+
+
+def test_spmm_unweighted_bit_identical_to_unit_weights(plgraph):
+    rng = np.random.default_rng(1)
+    b = torch.from_numpy(f32(rng.standard_normal((plgraph.n_cols, 64)))).to(DEV)
+    ones = plgraph.with_values(torch.ones(plgraph.nnz, device=DEV))
+    assert torch.equal(gc.spmm_unweighted(plgraph, b), gc.spmm(ones, b))
+
+
+def test_spmm_unweighted_never_reads_values(plgraph):
+    rng = np.random.default_rng(2)
+    b = torch.from_numpy(f32(rng.standard_normal((plgraph.n_cols, 32)))).to(DEV)
+    expected = gc.spmm(plgraph.with_values(torch.ones(plgraph.nnz, device=DEV)), b)
+    poisoned = plgraph.with_values(torch.full((plgraph.nnz,), float("nan"), device=DEV))
+    assert torch.equal(gc.spmm_unweighted(poisoned, b), expected)
+
+
+def test_spmm_known_answers():
+    a = gc.CsrMatrix(2, 2, np.array([0, 1, 1]), np.array([1]), np.array([2.0]), device=DEV)
+    out = gc.spmm(a, np.array([[1.0, 1.0], [3.0, 4.0]]))
+    assert isinstance(out, np.ndarray) and np.array_equal(out, [[6.0, 8.0], [0.0, 0.0]])
+    a = gc.CsrMatrix(1, 3, np.array([0, 2]), np.array([1, 2]), np.ones(2), device=DEV)
+    assert np.array_equal(gc.spmm_unweighted(a, np.array([[9.0, 9], [1, 2], [3, 4]])), [[4.0, 6.0]])
+    ident = gc.CsrMatrix(3, 3, np.arange(4), np.arange(3), np.ones(3), device=DEV)
+    b = np.random.default_rng(0).random((3, 2)).astype(np.float32)
+    assert np.array_equal(gc.spmm(ident, b), b)
+
+
+def test_spmm_empty_and_zero_rows(oracle):
+    rng = np.random.default_rng(3)
+    a = rand_csr(rng, 40, 30, 0.2, empty_rows=(0, 7, 39))
+    b = f32(rng.standard_normal((30, 12)))
+    out = gc.spmm(a, b)
+    assert np.array_equal(out[[0, 7, 39]], np.zeros((3, 12), np.float32))
+    assert oracle.rel_err(out, oracle.spmm(to_oracle(oracle, a), b)) < SP_TOL
+    z = gc.CsrMatrix(3, 3, np.zeros(4, np.int64), np.array([], np.int64), np.array([]), device=DEV)
+    assert np.array_equal(gc.spmm(z, np.ones((3, 2))), np.zeros((3, 2)))
+    e = gc.CsrMatrix(0, 5, np.zeros(1, np.int64), np.array([], np.int64), np.array([]), device=DEV)
+    assert gc.spmm(e, np.ones((5, 4))).shape == (0, 4)
+
+
+def test_spmm_shape_errors():
+    a = gc.CsrMatrix(3, 3, np.arange(4), np.arange(3), np.ones(3), device=DEV)
+    with pytest.raises(gc.ShapeError):
+        gc.spmm(a, np.ones((4, 2)))
+    with pytest.raises(RuntimeError):  # no CPU fallback
+        gc.spmm(a.to("cpu"), torch.ones(3, 2))
+
+
+def test_spmm_strided_output_and_accumulate(oracle, plgraph):
+    rng = np.random.default_rng(4)
+    b = torch.from_numpy(f32(rng.standard_normal((plgraph.n_cols, 64)))).to(DEV)
+    big = torch.zeros(plgraph.n_rows, 128, device=DEV)
+    gc.spmm(plgraph, b, out=big[:, 64:])
+    ref = gc.spmm(plgraph, b)
+    assert torch.equal(big[:, 64:], ref) and not big[:, :64].any()
+    gc.spmm(plgraph, b, out=big[:, 64:], accumulate=True)
+    assert torch.allclose(big[:, 64:], 2 * ref, rtol=1e-6, atol=1e-6)
+
+
+# ---------------------------------------------------------------------------
+# SDDMM
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("k", [1, 3, 16, 65])
+def test_sddmm(oracle, k):
+    rng = np.random.default_rng(k)
+    a = rand_csr(rng, 50, 37, 0.3)
+    b, c = f32(rng.standard_normal((50, k))), f32(rng.standard_normal((37, k)))
+    out = gc.sddmm(a, b, c)
+    assert out.same_pattern(a)
+    ref = oracle.sddmm(to_oracle(oracle, a), b, c).values
+    assert oracle.rel_err(out.values.cpu().numpy(), ref) < SP_TOL
+
+
+def test_sddmm_identity_and_empty():
+    rng = np.random.default_rng(5)
+    a = rand_csr(rng, 6, 6, 0.5)
+    ones = np.ones((6, 1))
+    assert torch.equal(gc.sddmm(a, ones, ones).values, a.values)
+    z = gc.CsrMatrix(3, 3, np.zeros(4, np.int64), np.array([], np.int64), np.array([]), device=DEV)
+    assert gc.sddmm(z, np.ones((3, 2)), np.ones((3, 2))).nnz == 0
+    with pytest.raises(gc.ShapeError):
+        gc.sddmm(a, np.ones((5, 2)), np.ones((6, 2)))
+
+
+def test_normalized_adjacency_matches_golden(golden):
+    for gid in ("path3", "grid4x5", "powerlaw200", "weighted40", "diag30"):
+        rp, ci, v = (golden[f"{gid}/A/{k}"] for k in ("row_ptr", "col_idx", "values"))
+        n = int(golden[f"{gid}/A/shape"][0])
+        a = gc.CsrMatrix(n, n, rp, ci, v, device=DEV)
+        g = gc.NormalizedGraph.from_adjacency(a, precompute=True)
+        assert np.array_equal(g.a_tilde.row_ptr.cpu().numpy(), golden[f"{gid}/At/row_ptr"])
+        assert np.array_equal(g.a_tilde.col_idx.cpu().numpy(), golden[f"{gid}/At/col_idx"])
+        np.testing.assert_allclose(g.n_tilde.values.cpu().numpy(), golden[f"{gid}/Nt"], rtol=2e-7)
+
+
+# ---------------------------------------------------------------------------
+# GEMM
+# ---------------------------------------------------------------------------
+
+GEMM_SHAPES = [(1, 1, 1), (5, 3, 7), (130, 33, 16), (300, 32, 32), (1000, 64, 200),
+               (513, 256, 256), (700, 100, 300), (257, 1433, 16), (2000, 256, 1024),
+               (129, 7, 33), (4097, 512, 128)]
+
+
+@pytest.mark.parametrize("M,K,N", GEMM_SHAPES)
+@pytest.mark.parametrize("prec,tol", [("fp32", 1e-4), ("tf32", 1e-2)])
+def test_gemm(oracle, M, K, N, prec, tol):
+    rng = np.random.default_rng(M + K + N)
+    a, w = f32(rng.uniform(-0.5, 0.5, (M, K))), f32(rng.uniform(-0.5, 0.5, (K, N)))
+    out = gc.gemm(torch.from_numpy(a).to(DEV), torch.from_numpy(w).to(DEV), precision=prec)
+    assert oracle.rel_err(out.cpu().numpy(), oracle.gemm(a, w)) <= tol
+    rs = torch.from_numpy(f32(rng.uniform(0.1, 1, M))).to(DEV)
+    out = gc.gemm(torch.from_numpy(a).to(DEV), torch.from_numpy(w).to(DEV), precision=prec,
+                  row_scale=rs, relu=True)
+    ref = np.maximum(oracle.scale_rows(rs.cpu().numpy(), oracle.gemm(a, w)), 0)
+    assert oracle.rel_err(out.cpu().numpy(), ref) <= tol
+
+
+def test_gemm_tf32_uses_tensor_cores_accuracy_profile(oracle):
+    # TF32 drops 13 mantissa bits: visibly less exact than fp32, within 1e-2.
+    rng = np.random.default_rng(9)
+    a, w = f32(rng.uniform(-0.5, 0.5, (1024, 512))), f32(rng.uniform(-0.5, 0.5, (512, 256)))
+    ref = oracle.gemm(a, w)
+    e32 = oracle.rel_err(gc.gemm(a, w, precision="fp32"), ref)
+    etf = oracle.rel_err(gc.gemm(a, w, precision="tf32"), ref)
+    assert e32 < 1e-5 < etf < 1e-2
+
+
+def test_gemm_known_and_errors():
+    out = gc.gemm(np.array([[1.0, 2.0], [3.0, 4.0]]), np.array([[5.0], [6.0]]), precision="fp32")
+    assert np.array_equal(out, [[17.0], [39.0]])
+    with pytest.raises(gc.ShapeError):
+        gc.gemm(np.ones((2, 3)), np.ones((2, 3)))
+
+
+def test_scale_rows(oracle):
+    rng = np.random.default_rng(6)
+    d, b = f32(rng.uniform(0.5, 2, 10)), f32(rng.standard_normal((10, 6)))
+    assert np.array_equal(gc.scale_rows(d, b), d[:, None] * b)
+    assert np.array_equal(gc.scale_rows(np.array([2.0, 3.0]), np.ones((2, 2))), [[2, 2], [3, 3]])
+    with pytest.raises(gc.ShapeError):
+        gc.scale_rows(np.ones(3), np.ones((4, 2)))
+
+
+# ---------------------------------------------------------------------------
+# attention
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("k2", [1, 5, 16, 64, 130])
+@pytest.mark.parametrize("form", ["reassoc", "sddmm"])
+def test_attention_matches_oracle(oracle, plgraph, k2, form):
+    rng = np.random.default_rng(k2)
+    hw = f32(rng.standard_normal((plgraph.n_rows, k2)))
+    a_s, a_d = f32(rng.uniform(-0.5, 0.5, k2)), f32(rng.uniform(-0.5, 0.5, k2))
+    spec = gc.GatLayerSpec(3, k2, np.zeros((3, k2)), a_s, a_d, leaky_slope=0.2, attention=form)
+    att = gc.atten_calc(plgraph, torch.from_numpy(hw).to(DEV), spec)
+    ref = oracle.atten_calc(to_oracle(oracle, plgraph), hw, a_s, a_d, 0.2).values
+    assert oracle.rel_err(att.alpha.values.cpu().numpy(), ref) < 1e-5
+    sums = att.row_sums().cpu().numpy()
+    np.testing.assert_allclose(sums, 1.0, atol=1e-5)
+
+
+def test_attention_singleton_and_ties():
+    a = gc.CsrMatrix(1, 1, np.array([0, 1]), np.array([0]), np.ones(1), device=DEV)
+    spec = gc.GatLayerSpec(1, 1, np.ones((1, 1)), np.ones(1), np.ones(1))
+    assert gc.atten_calc(a, np.ones((1, 1)), spec).alpha.values.item() == 1.0
+    a2 = gc.CsrMatrix(2, 2, np.array([0, 2, 2]), np.array([0, 1]), np.ones(2), device=DEV)
+    spec = gc.GatLayerSpec(1, 1, np.ones((1, 1)), np.zeros(1), np.zeros(1))
+    att = gc.atten_calc(a2, np.ones((2, 1)), spec)
+    assert np.allclose(att.alpha.values.cpu().numpy(), [0.5, 0.5])
+
+
+# ---------------------------------------------------------------------------
+# layers against the reference's own golden outputs
+# ---------------------------------------------------------------------------
+
+GRAPHS = ["path3", "star5", "grid4x5", "powerlaw200", "random120", "weighted40", "diag30"]
+SIZES = [(6, 3), (3, 6), (5, 5)]
+
+
+def golden_graph(golden, gid):
+    n = int(golden[f"{gid}/A/shape"][0])
+    return gc.CsrMatrix(n, n, golden[f"{gid}/A/row_ptr"], golden[f"{gid}/A/col_idx"],
+                        golden[f"{gid}/A/values"], device=DEV)
+
+
+@pytest.mark.parametrize("prec,tol", [("fp32", 1e-4), ("tf32", 1e-2)])
+@pytest.mark.parametrize("gid", GRAPHS)
+def test_gcn_layers_vs_reference_golden(golden, gid, prec, tol):
+    gc.set_gemm_precision(prec)
+    try:
+        g = gc.NormalizedGraph.from_adjacency(golden_graph(golden, gid), precompute=True)
+        for k1, k2 in SIZES:
+            key = f"{gid}/{k1}x{k2}"
+            h, w = golden[f"{key}/h"], golden[f"{key}/w"]
+            for comp in ("precompute", "dynamic"):
+                out = gc.gcn_layer(g, h, gc.GcnLayerSpec(k1, k2, w, composition=comp))
+                exp = golden[f"{key}/gcn/{comp}/heuristic"]
+                assert out.shape == exp.shape and _rel(out, exp) <= tol, (key, comp)
+                for order in ("aggregate_first", "update_first"):
+                    spec = gc.GcnLayerSpec(k1, k2, w, composition=comp, order=order)
+                    out = gc.gcn_layer(g, torch.from_numpy(f32(h)).to(DEV), spec).cpu().numpy()
+                    assert _rel(out, golden[f"{key}/gcn/{comp}/{order}"]) <= tol, (key, comp, order)
+    finally:
+        gc.set_gemm_precision("tf32")
+
+
+@pytest.mark.parametrize("prec,tol", [("fp32", 1e-4), ("tf32", 1e-2)])
+@pytest.mark.parametrize("gid", GRAPHS)
+def test_gat_layers_vs_reference_golden(golden, gid, prec, tol):
+    gc.set_gemm_precision(prec)
+    try:
+        at = gc.add_self_loops(golden_graph(golden, gid))
+        for k1, k2 in SIZES:
+            key = f"{gid}/{k1}x{k2}"
+            h, w = golden[f"{key}/h"], golden[f"{key}/w"]
+            a_s, a_d = golden[f"{key}/attn_src"], golden[f"{key}/attn_dst"]
+            for slope in (0.2, 0.1):
+                for comp in ("reuse", "recompute"):
+                    for act in ("relu", "none"):
+                        for form in ("reassoc", "sddmm"):
+                            spec = gc.GatLayerSpec(k1, k2, w, a_s, a_d, leaky_slope=slope,
+                                                   composition=comp, activation=act, attention=form)
+                            out = gc.gat_layer(at, h, spec)
+                            exp = golden[f"{key}/gat/s{slope}/{comp}/{act}"]
+                            assert _rel(out, exp) <= tol, (key, slope, comp, act, form)
+    finally:
+        gc.set_gemm_precision("tf32")
+
+
+def _rel(a, e):
+    a = np.asarray(a, dtype=np.float64)
+    e = np.asarray(e, dtype=np.float64)
+    return float(np.abs(a - e).max()) / max(1.0, float(np.abs(e).max()))
+
+
+@pytest.mark.parametrize("heads", [2, 4])
+@pytest.mark.parametrize("comp", ["reuse", "recompute"])
+@pytest.mark.parametrize("form", ["reassoc", "sddmm"])
+def test_multihead_gat(oracle, plgraph, heads, comp, form):
+    rng = np.random.default_rng(heads)
+    k1, k2 = 24, 16
+    h = f32(rng.uniform(-0.5, 0.5, (plgraph.n_rows, k1)))
+    w = f32(rng.uniform(-0.5, 0.5, (k1, heads * k2)))
+    a_s, a_d = f32(rng.uniform(-0.5, 0.5, heads * k2)), f32(rng.uniform(-0.5, 0.5, heads * k2))
+    spec = gc.GatLayerSpec(k1, k2, w, a_s, a_d, composition=comp, heads=heads, attention=form)
+    gc.set_gemm_precision("fp32")
+    try:
+        out = gc.gat_layer(plgraph, h, spec)
+    finally:
+        gc.set_gemm_precision("tf32")
+    ref = oracle.gat_layer_multihead(to_oracle(oracle, plgraph), h, w, a_s, a_d, heads,
+                                     composition=comp)
+    assert oracle.rel_err(out, ref) <= 1e-4
+
+
+def test_layers_are_deterministic(plgraph):
+    rng = np.random.default_rng(11)
+    h = torch.from_numpy(f32(rng.uniform(-0.5, 0.5, (plgraph.n_rows, 64)))).to(DEV)
+    w = f32(rng.uniform(-0.5, 0.5, (64, 64)))
+    g = gc.NormalizedGraph(plgraph, gc.inv_sqrt_degrees(plgraph)).with_precomputed()
+    for comp in ("precompute", "dynamic"):
+        spec = gc.GcnLayerSpec(64, 64, w, composition=comp)
+        assert torch.equal(gc.gcn_layer(g, h, spec), gc.gcn_layer(g, h, spec))
+    spec = gc.GatLayerSpec(64, 64, w, np.ones(64) * 0.1, np.ones(64) * -0.1)
+    assert torch.equal(gc.gat_layer(plgraph, h, spec), gc.gat_layer(plgraph, h, spec))
+
+
+def test_spmm_fn_hook_is_used(golden):
+    g = gc.NormalizedGraph.from_adjacency(golden_graph(golden, "grid4x5"), precompute=True)
+    calls = []
+
+    def my_spmm(a, b):
+        calls.append(a.nnz)
+        return gc.spmm(a, b)
+
+    key = "grid4x5/5x5"
+    h, w = golden[f"{key}/h"], golden[f"{key}/w"]
+    for comp in ("precompute", "dynamic"):
+        out = gc.gcn_layer(g, h, gc.GcnLayerSpec(5, 5, w, composition=comp), spmm_fn=my_spmm)
+        assert _rel(out, golden[f"{key}/gcn/{comp}/heuristic"]) <= 1e-2
+    assert len(calls) == 2
