@@ -1,0 +1,264 @@
+"""Host-side logic on CPU: CSR construction/validation semantics, graph prep
+bit-exactness, features, the input recipe, the selector (trained trees must
+equal the reference's on the same records), synthetic generators."""
+
+from __future__ import annotations
+
+import json
+import warnings
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2306_15155_b200 as gc
+from paper_2306_15155_b200 import graphs, profiling, selector
+
+from conftest import GOLDEN
+
+CPU = "cpu"
+GRAPHS = ["path3", "star5", "grid4x5", "powerlaw200", "random120", "weighted40", "diag30"]
+
+
+def gcsr(golden, key):
+    n_rows, n_cols = (int(x) for x in golden[f"{key}/shape"])
+    return gc.CsrMatrix(n_rows, n_cols, golden[f"{key}/row_ptr"], golden[f"{key}/col_idx"],
+                        golden[f"{key}/values"], device=CPU)
+
+
+# ---- CsrMatrix semantics (reference tests/test_sparse.py:32-68) ----------------
+
+
+def test_from_coo_sums_duplicates():
+    a = gc.CsrMatrix.from_coo(2, 2, [0, 0, 1], [1, 1, 0], [2.0, 3.0, 1.0], device=CPU)
+    assert a.nnz == 2 and a.to_dense()[0, 1] == 5.0
+
+
+def test_from_coo_matches_reference_golden(golden):
+    a = gc.CsrMatrix.from_coo(4, 3, golden["coo/rows"], golden["coo/cols"], golden["coo/vals"],
+                              device=CPU)
+    rp, ci, v = a.numpy()
+    assert np.array_equal(rp, golden["coo/out/row_ptr"])
+    assert np.array_equal(ci, golden["coo/out/col_idx"])
+    assert np.array_equal(v, golden["coo/out/values"].astype(np.float32))
+
+
+def test_validation_rejects_bad_row_ptr():
+    with pytest.raises(gc.ShapeError):
+        gc.CsrMatrix(2, 2, np.array([0, 1]), np.array([0]), np.array([1.0]), device=CPU)
+    with pytest.raises(gc.ShapeError):
+        gc.CsrMatrix(2, 2, np.array([0, 2, 1]), np.array([0, 1]), np.ones(2), device=CPU)
+
+
+def test_validation_rejects_bad_columns():
+    with pytest.raises(gc.ShapeError):
+        gc.CsrMatrix(2, 2, np.array([0, 1, 2]), np.array([0, 5]), np.ones(2), device=CPU)
+    with pytest.raises(gc.ShapeError):
+        gc.CsrMatrix(1, 3, np.array([0, 2]), np.array([2, 0]), np.ones(2), device=CPU)
+    gc.CsrMatrix(2, 3, np.array([0, 1, 2]), np.array([2, 0]), np.ones(2), device=CPU)
+
+
+def test_unit_value_flag():
+    assert gc.CsrMatrix(3, 3, np.arange(4), np.arange(3), np.ones(3), device=CPU).has_unit_values
+    a = gc.CsrMatrix(1, 2, np.array([0, 2]), np.array([0, 1]), np.array([1.0, 2.0]), device=CPU)
+    assert not a.has_unit_values
+
+
+def test_dense_matrix_rejects_non_finite():
+    with pytest.raises(ValueError):
+        gc.dense_matrix(np.array([[1.0, np.nan]]))
+
+
+@pytest.mark.parametrize("gid", GRAPHS)
+def test_graph_prep_bit_exact(golden, gid):
+    a = gcsr(golden, f"{gid}/A")
+    at = gc.add_self_loops(a)
+    rp, ci, v = at.numpy()
+    assert np.array_equal(rp, golden[f"{gid}/At/row_ptr"])
+    assert np.array_equal(ci, golden[f"{gid}/At/col_idx"])
+    assert np.array_equal(v, golden[f"{gid}/At/values"].astype(np.float32))
+    assert gc.add_self_loops(at).same_pattern(at)  # idempotent
+    d = gc.inv_sqrt_degrees(at).numpy()
+    assert np.array_equal(d, golden[f"{gid}/d"].astype(np.float32))
+    f = gc.extract_features(a).vector()
+    assert np.array_equal(f, golden[f"{gid}/features"])
+
+
+def test_add_self_loops_edge_cases():
+    e = gc.CsrMatrix(2, 2, np.zeros(3, np.int64), np.array([], np.int64), np.array([]), device=CPU)
+    assert torch.equal(gc.add_self_loops(e).to_dense(), torch.eye(2))
+    with pytest.raises(gc.ShapeError):
+        gc.add_self_loops(gc.CsrMatrix(2, 3, np.zeros(3, np.int64), np.array([], np.int64),
+                                       np.array([]), device=CPU))
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_add_self_loops_random_counting(seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 30))
+    dense = (rng.random((n, n)) < rng.uniform(0, 0.8)) * rng.uniform(0.5, 2, (n, n))
+    a = gc.CsrMatrix.from_dense(dense, device=CPU)
+    missing = int((np.diag(dense) == 0).sum())
+    out = gc.add_self_loops(a)
+    assert out.nnz == a.nnz + missing
+    ref = dense.copy()
+    ref[np.diag_indices(n)] = np.where(np.diag(dense) != 0, np.diag(dense), 1.0)
+    assert np.allclose(out.to_dense().numpy(), ref)
+    out._check()
+
+
+def test_inv_sqrt_degrees_errors_and_values():
+    a = gc.CsrMatrix(2, 2, np.array([0, 1, 1]), np.array([0]), np.ones(1), device=CPU)
+    with pytest.raises(gc.DegenerateNodeError):
+        gc.inv_sqrt_degrees(a)
+    a = gc.CsrMatrix(1, 4, np.array([0, 4]), np.arange(4), np.ones(4), device=CPU)
+    assert gc.inv_sqrt_degrees(a)[0].item() == 0.5
+
+
+# ---- layer specs (reference gcn.py:58-73, gat.py:30-57) ------------------------------
+
+
+def test_spec_validation():
+    with pytest.raises(gc.ShapeError):
+        gc.GcnLayerSpec(3, 2, np.ones((2, 3)))
+    with pytest.raises(ValueError):
+        gc.GcnLayerSpec(0, 2, np.ones((0, 2)))
+    with pytest.raises(ValueError):
+        gc.GatLayerSpec(2, 2, np.ones((2, 2)), np.ones(2), np.ones(2), leaky_slope=1.5)
+    with pytest.raises(ValueError):
+        gc.GatLayerSpec(2, 2, np.ones((2, 2)), np.ones(2), np.ones(2), activation="tanh")
+    with pytest.raises(gc.ShapeError):
+        gc.GatLayerSpec(2, 2, np.ones((2, 2)), np.ones(3), np.ones(2))
+    s = gc.GatLayerSpec(2, 3, np.ones((2, 6)), np.ones(6), np.ones(6), heads=2)
+    assert s.heads == 2
+
+
+def test_ordering_heuristic_known_answers():
+    assert gc.ordering_heuristic(1024, 32) is gc.AggregationOrder.UPDATE_FIRST
+    assert gc.ordering_heuristic(32, 256) is gc.AggregationOrder.AGGREGATE_FIRST
+    assert gc.ordering_heuristic(64, 64) is gc.AggregationOrder.AGGREGATE_FIRST
+    with pytest.raises(ValueError):
+        gc.ordering_heuristic(0, 3)
+
+
+def test_input_recipe_matches_reference(golden):
+    inp = profiling.draw_inputs(profiling.config_rng(0, "cora", 5, 3), 7, 5, 3, "gat")
+    for k in ("h", "w", "attn_src", "attn_dst"):
+        assert np.array_equal(inp[k], golden[f"recipe/{k}"])
+
+
+# ---- selector: same trees as the reference on the same records ----------------
+
+
+@pytest.fixture(scope="module")
+def sel_golden():
+    return json.loads((GOLDEN / "selector_golden.json").read_text())
+
+
+@pytest.mark.parametrize("model", ["gcn", "gat"])
+def test_selector_trains_reference_identical_trees(sel_golden, model):
+    recs = [profiling.ProfileRecord.from_dict(d) for d in sel_golden["records"]]
+    hyper = gc.SelectorHyperparams(n_estimators=12, learning_rate=0.1, max_depth=3, reg_lambda=1.0)
+    with warnings.catch_warnings(record=True) as w:
+        warnings.simplefilter("always")
+        m = gc.train(recs, model, hyper)
+    assert any("single composition" in str(x.message) for x in w)
+    exp = sel_golden[f"{model}/model"]
+    got = m.to_dict()
+    assert got["feature_names"] == exp["feature_names"]
+    assert len(got["trees"]) == len(exp["trees"])
+    for tg, te in zip(got["trees"], exp["trees"]):
+        assert tg["feature"] == te["feature"]
+        assert tg["left"] == te["left"] and tg["right"] == te["right"]
+        np.testing.assert_array_equal(tg["threshold"], te["threshold"])
+        np.testing.assert_allclose(tg["value"], te["value"], rtol=1e-12, atol=1e-15)
+    np.testing.assert_allclose(got["feature_gain"], exp["feature_gain"], rtol=1e-12)
+    # the reference's model file loads and scores identically here
+    ref_model = gc.SelectorModel.from_dict(exp)
+    for pick in sel_golden[f"{model}/picks"]:
+        feats = recs[[r.graph_id for r in recs].index(pick["graph"])].features
+        inp = gc.SelectorInput(features=feats, k1=pick["k1"], k2=pick["k2"])
+        choice, scores = gc.select_with_scores(ref_model, inp)
+        assert choice == pick["choice"]
+        for k, v in pick["scores"].items():
+            assert scores[k] == pytest.approx(v, rel=1e-12, abs=1e-15)
+    imp = gc.feature_importance(ref_model)
+    assert [n for n, _ in imp] == [n for n, _ in sel_golden[f"{model}/importance"]]
+
+
+def test_selector_errors_and_defaults(sel_golden):
+    recs = [profiling.ProfileRecord.from_dict(d) for d in sel_golden["records"]][:10]
+    with pytest.raises(gc.InsufficientDataError):
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            gc.train(recs, "gcn")
+    with pytest.raises(ValueError):
+        gc.train(recs, "mlp")
+    empty = gc.SelectorModel("gcn", selector.feature_layout(0))
+    inp = gc.SelectorInput(features=recs[0].features, k1=8, k2=8)
+    assert gc.select(empty, inp) == "dynamic"
+    with pytest.raises(gc.SchemaError):
+        gc.SelectorModel.from_dict({"format_version": 99})
+    with pytest.raises(gc.SchemaError):
+        empty.score(np.zeros(3))
+
+
+def test_selector_multiway_roundtrip(tmp_path, sel_golden):
+    base = [profiling.ProfileRecord.from_dict(d) for d in sel_golden["records"] if d["model"] == "gcn"]
+    comps = selector.B200_COMPOSITIONS["gcn"]
+    recs = []
+    for r in base:
+        if r.composition != "precompute":
+            continue
+        for i, c in enumerate(comps):
+            t = r.median_time_s * (1 + 0.1 * ((i + r.k1 // 32) % 4))
+            recs.append(profiling.ProfileRecord.from_dict({**r.to_dict(), "composition": c,
+                                                           "median_time_s": t}))
+    m = gc.train(recs, "gcn", gc.SelectorHyperparams(n_estimators=20, learning_rate=0.3, max_depth=3),
+                 compositions=comps)
+    p = tmp_path / "m.json"
+    m.save(p)
+    m2 = gc.SelectorModel.load(p)
+    assert m2.candidates == comps
+    inp = gc.SelectorInput(features=recs[0].features, k1=recs[0].k1, k2=recs[0].k2)
+    assert gc.select(m2, inp) in comps
+
+
+# ---- synthetic generators ------------------------------------------------------
+
+
+@pytest.mark.parametrize("kind,n,nnz", [("uniform", 500, 3000), ("rmat", 1000, 20000),
+                                        ("rmat", 3000, 40000)])
+def test_synthetic_graph_exact_and_symmetric(kind, n, nnz):
+    a = graphs.synthetic_graph(kind, n, nnz, seed=1, device=CPU)
+    assert a.nnz == nnz and a.n_rows == n
+    a._check()
+    d = a.to_dense()
+    assert torch.equal(d, d.T) and not bool(torch.diagonal(d).any())
+    b = graphs.synthetic_graph(kind, n, nnz, seed=1, device=CPU)
+    assert a.same_pattern(b)
+    c = graphs.synthetic_graph(kind, n, nnz, seed=2, device=CPU)
+    assert not a.same_pattern(c)
+
+
+def test_synthetic_graph_is_a_prefix_in_counter_order():
+    # a smaller target is the earliest-generated subset of a larger one
+    small = graphs.synthetic_graph("rmat", 2000, 10000, seed=3, device=CPU)
+    big = graphs.synthetic_graph("rmat", 2000, 14000, seed=3, device=CPU)
+    ds, db = small.to_dense(), big.to_dense()
+    assert bool((db[ds > 0] > 0).all())
+
+
+def test_rmat_is_power_law():
+    a = graphs.synthetic_graph("rmat", 4096, 80000, seed=0, device=CPU)
+    f = gc.extract_features(a)
+    assert f.d_max > 20 * f.nnz_mean
+    u = graphs.synthetic_graph("uniform", 4096, 80000, seed=0, device=CPU)
+    assert gc.extract_features(u).d_max < 3 * f.nnz_mean
+
+
+def test_hash_matches_python_reference():
+    x = torch.tensor([0, 1, 12345, -7], dtype=torch.int64)
+    got = graphs.splitmix64(x).tolist()
+    exp = [graphs._s64(graphs._splitmix64_int(v & graphs._M64)) for v in (0, 1, 12345, -7)]
+    assert got == exp
