@@ -1,0 +1,556 @@
+#!/usr/bin/env python
+"""Benchmark: one GCN layer on the Reddit-shaped power-law graph (BASELINE.json
+configs[1]) through the B200 composition engine.
+
+A "step" is one forward pass of the selected GCN layer composition over the
+whole graph (n = 232,965, nnz(A) = 114,615,892, m = nnz(Ã) = nnz(A) + n) at
+k1 = k2 = K (default 256), inputs resident in HBM.  ``value`` is whole-job
+edges/s = m / step time.  ``e2e`` is the same layer through the public API
+with HOST (pinned) H in and the host result out, copies inside the timed
+region.  ``sweep`` times every composition at K in {32..1024}; ``roofline``
+is the dominant kernel (the SpMM) against measured HBM bandwidth;
+``cpu_baseline`` is the CPU oracle (the reference's algorithm, float64,
+numba-equivalent C/OpenMP + OpenBLAS) on a bounded row sample.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun, one rank per GPU, NCCL): Ã is row-partitioned (nnz-balanced)
+and each step is the partitioned layer with its per-layer all-gather; the
+time is the max over ranks (strong scaling of the same graph).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+BASELINE = json.loads((ROOT / "BASELINE.json").read_text())
+METRIC = BASELINE["metric"]
+UNIT = "edges/s"
+KSWEEP = (32, 64, 128, 256, 512, 1024)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    p.add_argument("--shape", default="reddit")
+    p.add_argument("--k", type=int, default=256)
+    p.add_argument("--composition", default="auto",
+                   help="auto (selector) or '<precompute|dynamic>:<aggregate_first|update_first>'")
+    p.add_argument("--no-sweep", action="store_true")
+    p.add_argument("--sweep-ks", default=",".join(map(str, KSWEEP)))
+    p.add_argument("--sweep-reps", type=int, default=5)
+    p.add_argument("--cpu-sample-edges", type=float, default=0.08,
+                   help="fraction of the edges in the CPU-oracle row sample")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--out", default=None, help="also write the JSON line to this file")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# helpers
+# ---------------------------------------------------------------------------
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the
+    timed region (the profiling recipe's clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,utilization.gpu,power.draw,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        rows = []
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                rows.append((float(f[1]), float(f[2]), float(f[3]), f[5:9]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        load = [r for r in rows if r[2] >= 50] or rows
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for r in load for i, v in enumerate(r[3]) if v == "Active"})
+        return {"sm_mhz": float(np.median([r[0] for r in load])), "sm_max_mhz": rows[0][1],
+                "reasons": reasons, "samples": len(rows), "samples_under_load": len(load)}
+
+
+def spmm_alg_bytes(n_rows: int, m: int, K: int, weighted: bool, dcol: bool, drow: bool) -> int:
+    """Edge-gather model of SURVEY.md §8(d): row_ptr + col_idx + (values) +
+    (d_j gathers) + one K-row of B per edge + the output (+ d_i)."""
+    b = 4 * (n_rows + 1) + 4 * m + 4 * m * K + 4 * n_rows * K
+    b += 4 * m if weighted else 0
+    b += 4 * m if dcol else 0
+    b += 4 * n_rows if drow else 0
+    return b
+
+
+def layer_flops(n: int, m: int, k1: int, k2: int, order: str) -> int:
+    k_agg = k1 if order == "aggregate_first" else k2
+    return 2 * m * k_agg + 2 * n * k1 * k2
+
+
+def choose_composition(arg: str, feats, k1: int, k2: int) -> tuple[str, str]:
+    if arg != "auto":
+        return arg, "forced"
+    from paper_2306_15155_b200 import selector
+
+    model = selector.load_b200_model("gcn")
+    if model is not None:
+        inp = selector.SelectorInput(features=feats, k1=k1, k2=k2)
+        return selector.select(model, inp), "selector (B200-trained)"
+    from paper_2306_15155_b200.gcn import ordering_heuristic
+
+    return f"dynamic:{ordering_heuristic(k1, k2).value}", "reference default (dynamic + heuristic)"
+
+
+def strided_rows(row_ptr: np.ndarray, frac: float) -> np.ndarray:
+    """Every s-th row, s chosen so the sample holds ~frac of the edges."""
+    n = row_ptr.size - 1
+    s = max(1, int(round(1.0 / max(frac, 1e-6))))
+    return np.arange(0, n, s, dtype=np.int64)
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline leg and the --impl reference arm)
+# ---------------------------------------------------------------------------
+
+
+def cpu_oracle_setup(a_tilde_host, d_host, frac: float):
+    from oracle import gnn_oracle as orc
+
+    rows = strided_rows(a_tilde_host.row_ptr, frac)
+    sub = a_tilde_host.take_rows(rows)
+    return orc, rows, sub
+
+
+def cpu_oracle_layer(orc, sub, d, rows, h, w):
+    """The reference default for k1 == k2: dynamic composition, heuristic order
+    (aggregate first): relu(d_s ⊙ ((Ã_s (d ⊙ H)) W)) — gcn.py:137-155 on the
+    sampled rows."""
+    order = orc.ordering_heuristic(w.shape[0], w.shape[1])
+    scaled = orc.scale_rows(d, h)
+    agg = orc.spmm_unweighted if sub.has_unit_values else orc.spmm
+    if order == orc.UPDATE_FIRST:
+        out = agg(sub, orc.gemm(scaled, w))
+    else:
+        out = orc.gemm(agg(sub, scaled), w)
+    return np.maximum(orc.scale_rows(d[rows], out), 0.0)
+
+
+def time_cpu(fn, warmup: int, reps: int) -> float:
+    for _ in range(warmup):
+        fn()
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+    return float(np.median(ts))
+
+
+def host_graph(A_dev):
+    """Reference-dtype host copy (int64 / float64) of a device CSR."""
+    from oracle import gnn_oracle as orc
+
+    rp, ci, v = A_dev.numpy()
+    return orc.Csr(A_dev.n_rows, A_dev.n_cols, rp, ci, v)
+
+
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------
+# main
+# ---------------------------------------------------------------------------
+
+
+def main():
+    args = parse()
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2306_15155_b200 as gc
+    from paper_2306_15155_b200 import _native, graphs, profiling, sparse
+    from paper_2306_15155_b200.distributed import RowPartition, dist_gcn_layer
+
+    _native.load()
+    shape = graphs.SHAPES[args.shape]
+    t0 = time.perf_counter()
+    A = graphs.shape_graph(args.shape, seed=args.seed, device=dev)
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+    feats = gc.extract_features(A)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    g = gc.NormalizedGraph.from_adjacency(A)
+    torch.cuda.synchronize()
+    prep_s = time.perf_counter() - t0
+    e0.record()
+    g.with_precomputed()
+    e1.record()
+    torch.cuda.synchronize()
+    norm_ms = e0.elapsed_time(e1)
+    del A
+    n, m, K = g.a_tilde.n_rows, g.a_tilde.nnz, args.k
+    comp, selected_by = choose_composition(args.composition, feats, K, K)
+    base, order = comp.split(":")
+    spec = gc.GcnLayerSpec(K, K, np.zeros((K, K)), composition=base, order=order)
+
+    rng = profiling.config_rng(args.seed, args.shape, K, K)
+    inp = profiling.draw_inputs(rng, n, K, K, "gcn")
+    h_host32 = inp["h"].astype(np.float32)
+    spec.weights = torch.from_numpy(inp["w"].astype(np.float32)).to(dev)
+
+    part = None
+    if world > 1:
+        a_full = g.n_tilde if base == "precompute" else g.a_tilde
+        part = RowPartition.of(a_full, rank, world)
+        h_dev = torch.from_numpy(h_host32[part.lo:part.hi]).to(dev)
+        d_full = g.d_inv_sqrt.to(dev)
+
+        def step():
+            return dist_gcn_layer(part, h_dev, spec.weights, composition=base, order=order,
+                                  d=d_full)
+    else:
+        h_dev = torch.from_numpy(h_host32).to(dev)
+
+        def step():
+            return gc.gcn_layer(g, h_dev, spec)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- warmup + timed region ------------------------------------------------
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    launches0 = _native.launch_count()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks, sparse.kernel_timing("spmm", "gemm") as kt:
+        t_start.record()
+        for _ in range(args.steps):
+            out = step()
+        t_end.record()
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+    launches = _native.launch_count() - launches0
+    ms = t_start.elapsed_time(t_end) / args.steps
+    if world > 1:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    spmm_ms = float(np.mean(kt.durations_ms("spmm"))) if kt.durations_ms("spmm") else None
+    gemm_ms = float(np.mean(kt.durations_ms("gemm"))) if kt.durations_ms("gemm") else None
+    value = m / (ms * 1e-3)
+
+    # ---- roofline of the dominant kernel (SpMM) ------------------------------
+    pk = peaks()
+    dyn = base == "dynamic"
+    a_used = part.local if part is not None else (g.a_tilde if dyn else g.n_tilde)
+    weighted = not (dyn and g.a_tilde.has_unit_values)
+    spmm_bytes = spmm_alg_bytes(a_used.n_rows, a_used.nnz, K, weighted, dyn, dyn)
+    roof = None
+    if spmm_ms:
+        ach = spmm_bytes / (spmm_ms * 1e-3) / 1e9
+        traffic = None
+        tf = ROOT / "profiles" / "traffic.json"
+        if tf.exists():
+            traffic = json.loads(tf.read_text()).get(f"{args.shape}/K{K}/{comp}")
+        roof = {"kernel": "spmm_kernel", "bound": "hbm", "achieved": round(ach, 1),
+                "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(ach / pk["hbm_gbs"], 3),
+                "traffic": traffic, "alg_bytes_per_launch": spmm_bytes,
+                "kernel_ms": round(spmm_ms, 4), "share_of_step": round(spmm_ms / ms, 3),
+                "peak_source": pk["source"],
+                "model": "edge-gather: 4(n+1)+4m[+4m values][+4m d_j]+4mK+4nK[+4n]"}
+    result = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": f"synthetic {shape.kind.upper()} graph, {args.shape}-shaped (n={n - 0}, "
+                f"nnz(A)={shape.nnz}); H,W ~ U(-0.5,0.5) by the reference recipe",
+        "config": {"workload": f"gcn_layer/{args.shape}/k1=k2={K}", "shape": args.shape, "n": n,
+                   "nnz_A": shape.nnz, "m_tilde": m, "K": K, "composition": comp,
+                   "selected_by": selected_by, "gemm_precision": gc.get_gemm_precision(),
+                   "l2": "inputs larger than L2 (CSR 0.9 GB, H 0.24 GB at K=256); no flush",
+                   "parallelism": f"row-partition x{world}" if world > 1 else "single GPU"},
+        "gpu_launches": int(launches),
+        "kernel_ms": {"spmm": spmm_ms, "gemm": gemm_ms},
+        "roofline": roof,
+        "setup": {"graph_gen_s": round(gen_s, 2), "prep_s": round(prep_s, 3),
+                  "normalize_sddmm_ms": round(norm_ms, 3)},
+    }
+    result["clocks"] = clocks.summary()
+
+    if rank == 0 and world == 1:
+        # ---- parity of the timed step on sampled rows vs the oracle -------------
+        result["parity"] = parity_check(g, out, h_host32, inp["w"].astype(np.float32), comp, dev)
+        # ---- e2e through the public API with host buffers ----------------------
+        result["e2e"] = e2e(gc, g, spec, h_host32, args, m, n, K)
+        # ---- composition sweep -------------------------------------------------
+        if not args.no_sweep:
+            result["sweep"] = sweep(gc, g, feats, args, dev, pk)
+        # ---- CPU baseline --------------------------------------------------------
+        if not args.no_cpu:
+            result["cpu_baseline"] = cpu_baseline(g, h_host32, inp["w"].astype(np.float32), args)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        line = json.dumps(result)
+        print(line, flush=True)
+        if args.out:
+            Path(args.out).write_text(line + "\n")
+
+
+def parity_check(g, out, h32, w32, comp, dev) -> dict:
+    import torch
+
+    from oracle import gnn_oracle as orc
+
+    host = host_graph(g.a_tilde)
+    rng = np.random.default_rng(0)
+    rows = np.sort(rng.choice(host.n_rows, size=min(2048, host.n_rows), replace=False))
+    sub = host.take_rows(rows)
+    d = g.d_inv_sqrt.cpu().numpy().astype(np.float64)
+    h, w = h32.astype(np.float64), w32.astype(np.float64)
+    base, order = comp.split(":")
+    dn = d[rows]
+    if base == "precompute":
+        vals = sub.values * dn[np.repeat(np.arange(rows.size), np.diff(sub.row_ptr))] * d[sub.col_idx]
+        subn = sub.with_values(vals)
+        if order == "update_first":
+            ref = orc.spmm(subn, orc.gemm(h, w))
+        else:
+            ref = orc.gemm(orc.spmm(subn, h), w)
+        ref = np.maximum(ref, 0)
+    else:
+        sc = orc.scale_rows(d, h)
+        r = orc.spmm_unweighted(sub, orc.gemm(sc, w)) if order == "update_first" else \
+            orc.gemm(orc.spmm_unweighted(sub, sc), w)
+        ref = np.maximum(orc.scale_rows(dn, r), 0)
+    got = out[torch.from_numpy(rows).to(dev)].cpu().numpy()
+    err = orc.rel_err(got, ref)
+    from paper_2306_15155_b200.sparse import get_gemm_precision
+
+    tol = 1e-2 if get_gemm_precision() == "tf32" else 1e-4
+    return {"rows_checked": int(rows.size), "rel_err": err, "tol": tol, "ok": bool(err <= tol),
+            "metric": "max|a-e|/max(1,max|e|) (reference tests/helpers.py:68-72)"}
+
+
+def e2e(gc, g, spec, h_host32, args, m, n, K) -> dict:
+    import torch
+
+    h_pin = torch.from_numpy(h_host32).pin_memory()
+    for _ in range(max(args.warmup, 1)):
+        gc.gcn_layer(g, h_pin, spec)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        res = gc.gcn_layer(g, h_pin, spec)  # pinned host tensor in -> pinned host tensor out
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / args.steps
+    return {"value": round(m / dt, 1), "unit": UNIT, "ms_per_step": round(dt * 1e3, 3),
+            "h2d_bytes_per_step": int(h_pin.numel() * 4), "d2h_bytes_per_step": int(res.numel() * 4),
+            "api": "paper_2306_15155_b200.gcn_layer(NormalizedGraph, pinned host H, spec)"}
+
+
+def sweep(gc, g, feats, args, dev, pk) -> list[dict]:
+    import torch
+
+    from paper_2306_15155_b200 import profiling, selector, sparse
+
+    model = selector.load_b200_model("gcn")
+    n, m = g.a_tilde.n_rows, g.a_tilde.nnz
+    rows = []
+    for K in [int(k) for k in args.sweep_ks.split(",") if k]:
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(K)
+        h = torch.rand(n, K, device=dev, generator=gen) - 0.5
+        w = torch.rand(K, K, device=dev, generator=gen) - 0.5
+        entry = {"K": K, "compositions": {}}
+        for comp in selector.B200_COMPOSITIONS["gcn"]:
+            base, order = comp.split(":")
+            spec = gc.GcnLayerSpec(K, K, w, composition=base, order=order)
+            try:
+                with sparse.kernel_timing("spmm") as kt:
+                    med, cv = profiling.time_iterations(lambda: gc.gcn_layer(g, h, spec), 2,
+                                                        args.sweep_reps)
+                torch.cuda.synchronize()
+            except torch.cuda.OutOfMemoryError:
+                torch.cuda.empty_cache()
+                entry["compositions"][comp] = {"oom": True}
+                continue
+            sp = float(np.median(kt.durations_ms("spmm")))
+            ka = K
+            dyn = base == "dynamic"
+            b = spmm_alg_bytes(n, m, ka, not dyn, dyn, dyn)
+            entry["compositions"][comp] = {
+                "ms": round(med * 1e3, 4), "edges_per_s": round(m / med, 1),
+                "gflops": round(layer_flops(n, m, K, K, order) / med / 1e9, 1),
+                "spmm_ms": round(sp, 4),
+                "spmm_hbm_frac": round(b / (sp * 1e-3) / 1e9 / pk["hbm_gbs"], 3), "cv": round(cv, 3)}
+        ok = {c: v["ms"] for c, v in entry["compositions"].items() if "ms" in v}
+        best = min(ok, key=ok.get)
+        entry["fastest"] = best
+        if model is not None:
+            pick = selector.select(model, selector.SelectorInput(features=feats, k1=K, k2=K))
+        else:
+            pick = f"dynamic:{gc.ordering_heuristic(K, K).value}"
+        entry["selected"] = pick
+        entry["selected_over_fastest"] = round(ok[pick] / ok[best], 3) if pick in ok else None
+        rows.append(entry)
+        del h, w
+    return rows
+
+
+def cpu_baseline(g, h32, w32, args) -> dict:
+    from oracle import gnn_oracle as orc
+
+    threads = orc.set_threads(os.cpu_count())
+    host = host_graph(g.a_tilde)
+    d = g.d_inv_sqrt.cpu().numpy().astype(np.float64)
+    _, rows, sub = cpu_oracle_setup(host, d, args.cpu_sample_edges)
+    h, w = h32.astype(np.float64), w32.astype(np.float64)
+    t = time_cpu(lambda: cpu_oracle_layer(orc, sub, d, rows, h, w), 1, 3)
+    return {"value": round(sub.nnz / t, 1), "unit": UNIT, "cores": threads, "kind": "port",
+            "cpu": cpu_model(), "seconds_per_layer_sample": round(t, 3),
+            "sample": f"every {max(1, round(1 / args.cpu_sample_edges))}-th row of Ã "
+                      f"({rows.size} rows, {sub.nnz} edges), full H; reference default "
+                      f"composition (dynamic, heuristic order), float64, median of 3 after 1 warmup"}
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    """The reference's CPU implementation (oracle port of gnncompose, float64,
+    all host threads) on a bounded row sample of the same workload."""
+    if rank != 0:
+        return
+    import torch
+
+    from oracle import gnn_oracle as orc
+    from paper_2306_15155_b200 import graphs, profiling
+
+    # input synthesis only: the graph generator is plain torch integer ops
+    # (GPU if present, else CPU); no gnnc kernel runs in this arm.
+    dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
+    A = graphs.shape_graph(args.shape, seed=args.seed, device=dev)
+    host_a = host_graph(A)
+    del A
+    at = orc.add_self_loops(host_a)
+    d = orc.inv_sqrt_degrees(at)
+    K = args.k
+    n, m = at.n_rows, at.nnz
+    rng = profiling.config_rng(args.seed, args.shape, K, K)
+    inp = profiling.draw_inputs(rng, n, K, K, "gcn")
+    h = inp["h"].astype(np.float32).astype(np.float64)
+    w = inp["w"].astype(np.float32).astype(np.float64)
+    threads = orc.set_threads(os.cpu_count())
+    rows = strided_rows(at.row_ptr, args.cpu_sample_edges)
+    sub = at.take_rows(rows)
+    for _ in range(args.warmup):
+        cpu_oracle_layer(orc, sub, d, rows, h, w)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        cpu_oracle_layer(orc, sub, d, rows, h, w)
+        ts.append(time.perf_counter() - t0)
+    t = float(np.mean(ts))
+    value = sub.nnz / t
+    sample = (f"every {max(1, round(1 / args.cpu_sample_edges))}-th row of Ã ({rows.size} rows, "
+              f"{sub.nnz} of {m} edges), full H; reference default composition "
+              f"(dynamic, heuristic order), float64")
+    out = {"impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": UNIT,
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64", "data": f"synthetic RMAT {args.shape}-shaped",
+           "config": {"workload": f"gcn_layer/{args.shape}/k1=k2={K}", "shape": args.shape, "n": n,
+                      "m_tilde": m, "K": K, "composition": "dynamic:aggregate_first"},
+           "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": threads, "kind": "port",
+                            "sample": sample, "cpu": cpu_model()},
+           "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0},
+           "gpu_launches": 0}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

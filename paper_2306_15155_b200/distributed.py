@@ -1,0 +1,126 @@
+"""Row-partitioned layers across GPUs.
+
+One process per GPU (``torch.distributed``, NCCL over NVLink on the box,
+gloo in the CPU tests).  Ã is cut into contiguous, nnz-balanced row blocks
+(``partition_rows`` — the C-ABI host function, bit-exact with the oracle);
+rank p owns rows [b_p, b_{p+1}) with global column ids.  Per layer exactly one
+all-gather assembles the operand the local SpMM gathers:
+
+    composition              all-gathered operand
+    GCN A(HW)                (H_p W)          (d ⊙ folded into the SpMM gather)
+    GCN (AH)W                H_p
+    GAT reuse                H_p W and t_p
+    GAT recompute            H_p and t_p (+ H_p W for the local attention)
+
+Output rows stay partitioned and feed the next layer.  Blocks are padded to
+the largest block for ``all_gather_into_tensor``.
+
+The compute ops are injectable (``ops``) so the host logic — partition,
+padding, gather, unpad, assembly — is testable on CPU with gloo and the
+oracle standing in for the CUDA kernels.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _native as nat
+from .sparse import CsrMatrix
+
+
+def partition_rows(row_ptr, parts: int) -> np.ndarray:
+    """nnz-balanced contiguous row blocks: bounds[p] = first r with
+    row_ptr[r] >= ceil(p*nnz/P) (C ABI gc_partition_rows)."""
+    rp = np.ascontiguousarray(
+        row_ptr.cpu().numpy() if isinstance(row_ptr, torch.Tensor) else row_ptr, dtype=np.int64)
+    out = np.zeros(parts + 1, dtype=np.int64)
+    nat.check(nat.load().gc_partition_rows(rp.ctypes.data, rp.size - 1, int(parts), out.ctypes.data),
+              "partition_rows")
+    return out
+
+
+@dataclass
+class RowPartition:
+    rank: int
+    world: int
+    bounds: np.ndarray  # P+1 row boundaries
+    local: CsrMatrix  # rows [lo, hi) of Ã (or Ñ), global column ids
+
+    @property
+    def lo(self) -> int:
+        return int(self.bounds[self.rank])
+
+    @property
+    def hi(self) -> int:
+        return int(self.bounds[self.rank + 1])
+
+    @property
+    def rows(self) -> int:
+        return self.hi - self.lo
+
+    @property
+    def max_rows(self) -> int:
+        return int(np.diff(self.bounds).max())
+
+    @classmethod
+    def of(cls, a: CsrMatrix, rank: int, world: int) -> "RowPartition":
+        b = partition_rows(a.row_ptr, world)
+        return cls(rank, world, b, a.take_rows(int(b[rank]), int(b[rank + 1])))
+
+
+def all_gather_rows(x_local: torch.Tensor, part: RowPartition, group=None) -> torch.Tensor:
+    """Assemble the full n x k operand from every rank's row block (padded
+    all_gather_into_tensor, then the padding is dropped)."""
+    k = x_local.shape[1]
+    pad = part.max_rows
+    buf = torch.zeros(pad, k, dtype=x_local.dtype, device=x_local.device)
+    buf[: x_local.shape[0]] = x_local
+    full = torch.empty(part.world * pad, k, dtype=x_local.dtype, device=x_local.device)
+    dist.all_gather_into_tensor(full, buf, group=group)
+    if all(int(part.bounds[p + 1] - part.bounds[p]) == pad for p in range(part.world)):
+        return full
+    pieces = [full[p * pad: p * pad + int(part.bounds[p + 1] - part.bounds[p])]
+              for p in range(part.world)]
+    return torch.cat(pieces, 0)
+
+
+class CudaOps:
+    """The product ops: sm_100a kernels through the C ABI."""
+
+    @staticmethod
+    def gemm(a, w, row_scale=None, relu=False):
+        from .sparse import gemm
+
+        return gemm(a, w, row_scale=row_scale, relu=relu)
+
+    @staticmethod
+    def spmm(a: CsrMatrix, b, d_row=None, d_col=None, relu=False, weighted=True):
+        from .sparse import spmm, spmm_unweighted
+
+        f = spmm if weighted else spmm_unweighted
+        return f(a, b, d_row=d_row, d_col=d_col, relu=relu)
+
+
+def dist_gcn_layer(part: RowPartition, h_local: torch.Tensor, w: torch.Tensor, *,
+                   composition: str, order: str, d: torch.Tensor | None = None,
+                   ops=CudaOps, group=None) -> torch.Tensor:
+    """One GCN layer on this rank's rows.  ``part.local`` is Ñ's block for
+    precompute or Ã's block for dynamic; ``d`` is the FULL D^-1/2 vector
+    (needed for dynamic).  Returns this rank's output rows."""
+    dyn = composition == "dynamic"
+    if dyn and d is None:
+        raise ValueError("dynamic composition needs the degree vector")
+    d_loc = d[part.lo:part.hi] if dyn else None
+    weighted = not (dyn and part.local.has_unit_values)
+    if order == "update_first":
+        hw_loc = ops.gemm(h_local, w)
+        hw = all_gather_rows(hw_loc, part, group)
+        return ops.spmm(part.local, hw, d_row=d_loc, d_col=d if dyn else None, relu=True,
+                        weighted=weighted)
+    h = all_gather_rows(h_local, part, group)
+    x = ops.spmm(part.local, h, d_row=d_loc, d_col=d if dyn else None, relu=False, weighted=weighted)
+    return ops.gemm(x, w, relu=True)

@@ -81,25 +81,31 @@ def dense_matrix(data) -> torch.Tensor:
 
 
 class _Operand:
-    """A dense 2-D float32 CUDA operand plus where it came from (numpy in ->
-    numpy out, mirroring the reference's ndarray return type)."""
+    """A dense 2-D float32 CUDA operand plus where it came from.
 
-    __slots__ = ("t", "host")
+    numpy in -> numpy out (the reference's ndarray return type); a CPU torch
+    tensor in (ideally pinned) -> a pinned CPU tensor out; a CUDA tensor in ->
+    CUDA tensor out with no host traffic."""
+
+    __slots__ = ("t", "host", "kind")
 
     def __init__(self, b, device: torch.device, what: str = "dense operand"):
-        self.host = not isinstance(b, torch.Tensor)
-        if self.host:
-            arr = np.asarray(b)
-            t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32))
-            if t.dim() == 2 and t.numel():
-                t = t.pin_memory() if device.type == "cuda" else t
-            t = t.to(device, non_blocking=True)
-        else:
-            t = b
-            if t.dtype != torch.float32:
-                t = t.float()
+        if isinstance(b, torch.Tensor) and (b.is_cuda or device.type != "cuda"):
+            self.host, self.kind = False, "device"
+            t = b if b.dtype == torch.float32 else b.float()
             if t.device != device:
                 t = t.to(device)
+        else:
+            self.host = True
+            if isinstance(b, torch.Tensor):
+                self.kind = "torch"
+                t = b if b.dtype == torch.float32 else b.float()
+            else:
+                self.kind = "numpy"
+                t = torch.from_numpy(np.ascontiguousarray(np.asarray(b), dtype=np.float32))
+            if t.dim() == 2 and t.stride(1) != 1:
+                t = t.contiguous()
+            t = t.to(device, non_blocking=t.is_pinned())
         if t.dim() != 2:
             raise ShapeError(f"{what} must be 2-D, got ndim={t.dim()}")
         if t.stride(1) != 1 or (t.size(0) > 1 and t.stride(0) < t.size(1)):
@@ -107,7 +113,53 @@ class _Operand:
         self.t = t
 
     def wrap(self, out: torch.Tensor):
-        return out.cpu().numpy() if self.host else out
+        if not self.host:
+            return out
+        if self.kind == "numpy":
+            return out.cpu().numpy()
+        dst = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+        dst.copy_(out, non_blocking=True)
+        torch.cuda.current_stream(out.device).synchronize()
+        return dst
+
+
+# ---- optional CUDA-event timing of individual kernel calls (bench.py) -------
+_TIMERS: dict[str, list] | None = None
+
+
+class kernel_timing:
+    """Context manager: record a CUDA event pair around every call of the named
+    primitives ("spmm", "gemm", "sddmm_norm", "attention") on the stream the
+    kernel is launched on.  ``durations_ms(name)`` after a synchronize."""
+
+    def __init__(self, *names: str):
+        self.names = names
+        self.events: dict[str, list] = {n: [] for n in names}
+
+    def __enter__(self):
+        global _TIMERS
+        _TIMERS = self.events
+        return self
+
+    def __exit__(self, *exc):
+        global _TIMERS
+        _TIMERS = None
+
+    def durations_ms(self, name: str) -> list[float]:
+        return [a.elapsed_time(b) for a, b in self.events[name]]
+
+
+def _timed_call(name: str, dev: torch.device, fn):
+    ev = _TIMERS.get(name) if _TIMERS is not None else None
+    if ev is None:
+        return fn()
+    st = torch.cuda.current_stream(dev)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    rc = fn()
+    b.record(st)
+    ev.append((a, b))
+    return rc
 
 
 def _ld(t: torch.Tensor) -> int:
@@ -368,11 +420,11 @@ def _spmm(a: CsrMatrix, b, *, weighted: bool, d_row=None, d_col=None, relu=False
         if n_slots:
             ws = torch.empty(n_slots * K, dtype=torch.float32, device=dev)
     lib = nat.load()
-    rc = lib.gc_spmm_f32(a.row_ptr.data_ptr(), a.col_idx.data_ptr(),
-                         a.values.data_ptr() if weighted else None, _ptr(d_row), _ptr(d_col),
-                         bt.data_ptr(), _ld(bt), a.n_rows, a.n_cols, K, out.data_ptr(), _ld(out),
-                         flags, code, _ptr(items), n_items, _ptr(split), n_split, _ptr(ws),
-                         0 if ws is None else ws.numel() * 4, _stream(dev))
+    rc = _timed_call("spmm", dev, lambda: lib.gc_spmm_f32(
+        a.row_ptr.data_ptr(), a.col_idx.data_ptr(), a.values.data_ptr() if weighted else None,
+        _ptr(d_row), _ptr(d_col), bt.data_ptr(), _ld(bt), a.n_rows, a.n_cols, K, out.data_ptr(),
+        _ld(out), flags, code, _ptr(items), n_items, _ptr(split), n_split, _ptr(ws),
+        0 if ws is None else ws.numel() * 4, _stream(dev)))
     nat.check(rc, what)
     return op.wrap(out)
 
@@ -477,9 +529,9 @@ def gemm(a, b, *, row_scale=None, relu=False, precision: str | None = None, out=
         flags |= nat.GC_GEMM_FP32
     if row_scale is not None and tuple(row_scale.shape) != (M,):
         raise ShapeError("gemm: row_scale must have one entry per row")
-    rc = lib.gc_gemm_f32(at.data_ptr(), _ld(at), bt.data_ptr(), _ld(bt), M, K, N, out.data_ptr(),
-                         _ld(out), _ptr(row_scale), flags, _ptr(ws),
-                         0 if ws is None else ws.numel(), _stream(dev))
+    rc = _timed_call("gemm", dev, lambda: lib.gc_gemm_f32(
+        at.data_ptr(), _ld(at), bt.data_ptr(), _ld(bt), M, K, N, out.data_ptr(), _ld(out),
+        _ptr(row_scale), flags, _ptr(ws), 0 if ws is None else ws.numel(), _stream(dev)))
     nat.check(rc, "gemm")
     return oa.wrap(out) if (oa.host and ob.host) else out
 
