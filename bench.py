@@ -57,6 +57,9 @@ def parse():
     p.add_argument("--cpu-sample-edges", type=float, default=0.08,
                    help="fraction of the edges in the CPU-oracle row sample")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-extra", action="store_true",
+                   help="skip the GAT-on-arxiv and products configs (BASELINE configs[2], [3])")
+    p.add_argument("--backend", default="nccl", help="process-group backend for N > 1")
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--out", default=None, help="also write the JSON line to this file")
     return p.parse_args()
@@ -240,10 +243,14 @@ def main():
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:  # e.g. gloo: lets the N > 1 path be exercised with several ranks on one GPU
+            dist.init_process_group(args.backend)
 
     import paper_2306_15155_b200 as gc
     from paper_2306_15155_b200 import _native, graphs, profiling, sparse
@@ -369,6 +376,8 @@ def main():
         # ---- composition sweep -------------------------------------------------
         if not args.no_sweep:
             result["sweep"] = sweep(gc, g, feats, args, dev, pk)
+        if not args.no_extra:
+            result["extra_configs"] = extra_configs(gc, args, dev, pk)
         # ---- CPU baseline --------------------------------------------------------
         if not args.no_cpu:
             result["cpu_baseline"] = cpu_baseline(g, h_host32, inp["w"].astype(np.float32), args)
@@ -481,6 +490,89 @@ def sweep(gc, g, feats, args, dev, pk) -> list[dict]:
         rows.append(entry)
         del h, w
     return rows
+
+
+def _time_layer(fn, reps: int) -> float:
+    from paper_2306_15155_b200 import profiling
+
+    med, _ = profiling.time_iterations(fn, 2, reps)
+    return med
+
+
+def extra_configs(gc, args, dev, pk) -> dict:
+    """BASELINE configs[2] (single/4-head GAT on arxiv, SDDMM vs reassociated
+    attention, reuse vs recompute) and configs[3] (GCN + GAT on products, 1
+    GPU), every composition timed; ms and edges/s = m / layer time."""
+    import torch
+
+    from paper_2306_15155_b200 import graphs, selector
+
+    res = {}
+    # ---- GAT on ogbn-arxiv-shaped RMAT ---------------------------------------
+    A = graphs.shape_graph("arxiv", seed=args.seed, device=dev)
+    at = gc.add_self_loops(A)
+    del A
+    n, m = at.n_rows, at.nnz
+    gat = []
+    for heads, ks in ((1, (32, 256, 1024)), (4, (32, 256))):
+        for K in ks:
+            gen = torch.Generator(device=dev)
+            gen.manual_seed(K + heads)
+            h = torch.rand(n, K, device=dev, generator=gen) - 0.5
+            w = torch.rand(K, K * heads, device=dev, generator=gen) - 0.5
+            a_s = torch.rand(K * heads, device=dev, generator=gen) - 0.5
+            a_d = torch.rand(K * heads, device=dev, generator=gen) - 0.5
+            row = {"heads": heads, "k1": K, "k2": K, "compositions": {}}
+            for comp in selector.B200_COMPOSITIONS["gat"]:
+                base, form = comp.split(":")
+                spec = gc.GatLayerSpec(K, K, w, a_s, a_d, composition=base, heads=heads,
+                                       attention=form)
+                t = _time_layer(lambda: gc.gat_layer(at, h, spec), args.sweep_reps)
+                row["compositions"][comp] = {"ms": round(t * 1e3, 4), "edges_per_s": round(m / t, 1)}
+            best = min(row["compositions"], key=lambda c: row["compositions"][c]["ms"])
+            row["fastest"] = best
+            gat.append(row)
+            del h, w
+    res["gat_arxiv"] = {"n": n, "m_tilde": m, "rows": gat}
+    del at
+    torch.cuda.empty_cache()
+    # ---- products-shaped: GCN (4 compositions) + GAT -------------------------
+    A = graphs.shape_graph("products", seed=args.seed, device=dev)
+    g = gc.NormalizedGraph.from_adjacency(A).with_precomputed()
+    del A
+    n, m = g.a_tilde.n_rows, g.a_tilde.nnz
+    rows = []
+    for K in (32, 256):
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(K)
+        h = torch.rand(n, K, device=dev, generator=gen) - 0.5
+        w = torch.rand(K, K, device=dev, generator=gen) - 0.5
+        row = {"K": K, "gcn": {}, "gat": {}}
+        for comp in selector.B200_COMPOSITIONS["gcn"]:
+            base, order = comp.split(":")
+            spec = gc.GcnLayerSpec(K, K, w, composition=base, order=order)
+            with __import__("paper_2306_15155_b200").sparse.kernel_timing("spmm") as kt:
+                t = _time_layer(lambda: gc.gcn_layer(g, h, spec), 3)
+            torch.cuda.synchronize()
+            sp = float(np.median(kt.durations_ms("spmm")))
+            dyn = base == "dynamic"
+            b = spmm_alg_bytes(n, m, K, not dyn, dyn, dyn)
+            row["gcn"][comp] = {"ms": round(t * 1e3, 4), "edges_per_s": round(m / t, 1),
+                                "spmm_ms": round(sp, 4),
+                                "spmm_hbm_frac": round(b / (sp * 1e-3) / 1e9 / pk["hbm_gbs"], 3)}
+        a_s = torch.rand(K, device=dev, generator=gen) - 0.5
+        a_d = torch.rand(K, device=dev, generator=gen) - 0.5
+        for comp in ("reuse:reassoc", "recompute:reassoc"):
+            base, form = comp.split(":")
+            spec = gc.GatLayerSpec(K, K, w, a_s, a_d, composition=base, attention=form)
+            t = _time_layer(lambda: gc.gat_layer(g.a_tilde, h, spec), 3)
+            row["gat"][comp] = {"ms": round(t * 1e3, 4), "edges_per_s": round(m / t, 1)}
+        rows.append(row)
+        del h, w
+    res["products"] = {"n": n, "m_tilde": m, "rows": rows}
+    del g
+    torch.cuda.empty_cache()
+    return res
 
 
 def cpu_baseline(g, h32, w32, args) -> dict:

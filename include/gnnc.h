@@ -90,11 +90,18 @@ GNNC_API int gc_spmm_f32(const int32_t *row_ptr, const int32_t *col_idx, const f
  * items whose partial sums land in consecutive workspace slots; every other
  * row is one item writing C directly.  items: int32[4*n_items] =
  * {row, begin, end, slot|-1}; split_rows: int32[4*n_split_rows] =
- * {row, first_slot, n_slots, 0}. */
+ * {row, first_slot, n_slots, 0}.  With GC_PLAN_LENGTH_CLASSES the items are
+ * stably ordered by floor(log2(length)), longest class first: lane groups
+ * sharing a warp get similar trip counts and the longest items start first
+ * (the order of work only; every output keeps its fixed accumulation order).
+ * gc_spmm_default_chunk: chunk that bounds the longest item to ~2x the mean
+ * work of one resident lane group for this K on `sm_count` SMs. */
+#define GC_PLAN_LENGTH_CLASSES 1u
+GNNC_API int32_t gc_spmm_default_chunk(int64_t n_rows, int64_t nnz, int64_t K, int sm_count);
 GNNC_API int gc_spmm_plan_count(const int32_t *row_ptr_host, int64_t n_rows, int32_t chunk,
                        int64_t *n_items, int64_t *n_slots, int64_t *n_split_rows);
 GNNC_API int gc_spmm_plan_fill(const int32_t *row_ptr_host, int64_t n_rows, int32_t chunk,
-                      int32_t *items_host, int32_t *split_rows_host);
+                      uint32_t plan_flags, int32_t *items_host, int32_t *split_rows_host);
 
 /* ---- SDDMM --------------------------------------------------------------
  * out[p] = (a_vals ? a_vals[p] : 1) * sum_t B[i,t] * Cm[col_idx[p],t]

@@ -19,6 +19,7 @@ GC_GEMM_TF32 = 1 << 4
 GC_GEMM_FP32 = 1 << 5
 GC_SPMM_ROW = 1
 GC_SPMM_NNZ_SPLIT = 2
+GC_PLAN_LENGTH_CLASSES = 1
 
 GC_OK = 0
 GC_ERR_SHAPE = -1
@@ -47,7 +48,8 @@ _SIGNATURES = {
     "gc_spmm_f32": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _I64, _U32,
                                    ctypes.c_int, _P, _I64, _P, _I64, _P, _SZ, _P]),
     "gc_spmm_plan_count": (ctypes.c_int, [_P, _I64, _I32, _i64p, _i64p, _i64p]),
-    "gc_spmm_plan_fill": (ctypes.c_int, [_P, _I64, _I32, _P, _P]),
+    "gc_spmm_plan_fill": (ctypes.c_int, [_P, _I64, _I32, _U32, _P, _P]),
+    "gc_spmm_default_chunk": (ctypes.c_int32, [_I64, _I64, _I64, ctypes.c_int]),
     "gc_sddmm_f32": (ctypes.c_int, [_P, _P, _P, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _P]),
     "gc_sddmm_norm_f32": (ctypes.c_int, [_P, _P, _P, _P, _I64, _P, _P]),
     "gc_gemm_workspace_bytes": (_SZ, [_I64, _I64]),

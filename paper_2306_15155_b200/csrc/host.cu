@@ -89,11 +89,26 @@ int gc_spmm_plan_count(const int32_t *row_ptr_host, int64_t n_rows, int32_t chun
   return GC_OK;
 }
 
+int32_t gc_spmm_default_chunk(int64_t n_rows, int64_t nnz, int64_t K, int sm_count) {
+  (void)n_rows;
+  // lanes per row group, as chosen by gc_spmm_f32's vector path
+  const int lpr = K <= 8 ? 2 : K <= 16 ? 4 : K <= 32 ? 8 : K <= 64 ? 16 : 32;
+  const int64_t groups = (int64_t)(sm_count > 0 ? sm_count : 148) * 48 * (32 / lpr);
+  const int64_t target = 2 * (nnz / (groups > 0 ? groups : 1));
+  int64_t c = 128;
+  while (c < target && c < 4096) c <<= 1;
+  return (int32_t)c;
+}
+
 int gc_spmm_plan_fill(const int32_t *row_ptr_host, int64_t n_rows, int32_t chunk,
-                      int32_t *items_host, int32_t *split_rows_host) {
+                      uint32_t plan_flags, int32_t *items_host, int32_t *split_rows_host) {
   GC_REQUIRE(row_ptr_host && items_host, GC_ERR_VALUE, "gc_spmm_plan_fill: null pointer");
   GC_REQUIRE(chunk >= 1, GC_ERR_VALUE, "gc_spmm_plan_fill: chunk must be >= 1");
-  int64_t it = 0, slot = 0, sr = 0;
+  GC_REQUIRE((plan_flags & ~GC_PLAN_LENGTH_CLASSES) == 0, GC_ERR_VALUE,
+             "gc_spmm_plan_fill: unknown flags");
+  std::vector<int32_t> nat;  // items in natural (row) order
+  nat.reserve((size_t)n_rows * 4);
+  int64_t slot = 0, sr = 0;
   for (int64_t i = 0; i < n_rows; ++i) {
     const int32_t b = row_ptr_host[i], e = row_ptr_host[i + 1];
     const int64_t deg = (int64_t)e - b;
@@ -108,19 +123,35 @@ int gc_spmm_plan_fill(const int32_t *row_ptr_host, int64_t n_rows, int32_t chunk
       for (int64_t q = 0; q < c; ++q) {
         const int32_t lo = b + (int32_t)(q * chunk);
         const int32_t hi = (int32_t)std::min<int64_t>((int64_t)lo + chunk, e);
-        items_host[4 * it + 0] = (int32_t)i;
-        items_host[4 * it + 1] = lo;
-        items_host[4 * it + 2] = hi;
-        items_host[4 * it + 3] = (int32_t)slot++;
-        ++it;
+        nat.insert(nat.end(), {(int32_t)i, lo, hi, (int32_t)slot++});
       }
     } else {
-      items_host[4 * it + 0] = (int32_t)i;
-      items_host[4 * it + 1] = b;
-      items_host[4 * it + 2] = e;
-      items_host[4 * it + 3] = -1;
-      ++it;
+      nat.insert(nat.end(), {(int32_t)i, b, e, -1});
     }
+  }
+  const size_t n_items = nat.size() / 4;
+  if (!(plan_flags & GC_PLAN_LENGTH_CLASSES)) {
+    std::copy(nat.begin(), nat.end(), items_host);
+    return GC_OK;
+  }
+  // stable counting sort by length class, longest class first
+  auto cls = [&](size_t k) {
+    const int32_t len = nat[4 * k + 2] - nat[4 * k + 1];
+    int c = 0;
+    while ((1 << (c + 1)) <= len && c < 30) ++c;
+    return len == 0 ? 0 : c + 1;
+  };
+  size_t start[33] = {0};
+  for (size_t k = 0; k < n_items; ++k) ++start[cls(k)];
+  size_t acc = 0;
+  for (int c = 32; c >= 0; --c) {
+    const size_t cnt = start[c];
+    start[c] = acc;
+    acc += cnt;
+  }
+  for (size_t k = 0; k < n_items; ++k) {
+    const size_t dst = start[cls(k)]++;
+    std::copy(nat.begin() + 4 * k, nat.begin() + 4 * k + 4, items_host + 4 * dst);
   }
   return GC_OK;
 }

@@ -146,38 +146,47 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
 
   const int len = end - beg;
   const int wmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)len);
+  // software pipeline: the (col, value) batch for the next LPR edges is in
+  // flight while the B rows of the current batch are gathered.
+  int jn = 0;
+  float vn = 1.0f;
+  if (gl < len) {
+    jn = ldg_stream_i32(a.col_idx + beg + gl);
+    if (HAS_VAL) vn = ldg_stream_f32(a.values + beg + gl);
+  }
   for (int base = 0; base < wmax; base += LPR) {
-    int j = 0;
-    float w = 0.0f;
-    if (base + gl < len) {
-      const int p = beg + base + gl;
-      j = ldg_stream_i32(a.col_idx + p);
-      w = HAS_VAL ? ldg_stream_f32(a.values + p) : 1.0f;
-      if (HAS_DCOL) w *= __ldg(a.d_col + j);
+    const int j = jn;
+    const float v = vn;
+    const bool mine = base + gl < len;
+    if (base + LPR + gl < len) {
+      jn = ldg_stream_i32(a.col_idx + beg + base + LPR + gl);
+      if (HAS_VAL) vn = ldg_stream_f32(a.values + beg + base + LPR + gl);
     }
+    float dj = 1.0f;
+    if (HAS_DCOL && mine) dj = __ldg(a.d_col + j);
     const int cnt = len - base;  // edges left for this group (may be <= 0)
     const int cntw = min(LPR, wmax - base);
 #pragma unroll 1
     for (int e0 = 0; e0 < cntw; e0 += U) {
       T bv[U][NV];
-      float we[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int je = __shfl_sync(0xffffffffu, j, e0 + u, LPR);
-        we[u] = __shfl_sync(0xffffffffu, w, e0 + u, LPR);
         const bool ok = (e0 + u) < cnt;
         const float *brow = a.B + (int64_t)je * a.ldb;
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          bv[u][v] = zero_of(T{});
-          if (ok && colok[v]) load_b(bv[u][v], brow + coff[v]);
+        for (int vv = 0; vv < NV; ++vv) {
+          bv[u][vv] = zero_of(T{});
+          if (ok && colok[vv]) load_b(bv[u][vv], brow + coff[vv]);
         }
       }
+      const float w = mine ? v * dj : 0.0f;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
+        const float we = __shfl_sync(0xffffffffu, w, e0 + u, LPR);
         if ((e0 + u) < cnt) {
 #pragma unroll
-          for (int v = 0; v < NV; ++v) fma_into(acc[v], we[u], bv[u][v]);
+          for (int vv = 0; vv < NV; ++vv) fma_into(acc[vv], we, bv[u][vv]);
         }
       }
     }

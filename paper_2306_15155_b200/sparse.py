@@ -348,10 +348,11 @@ class CsrMatrix:
                          validate=False, device=self.device)
 
     # -- nnz-split plan (cached per pattern) ----------------------------------------
-    def spmm_plan(self, chunk: int):
+    def spmm_plan(self, chunk: int, length_classes: bool = True):
         """Work items for GC_SPMM_NNZ_SPLIT: heavy rows (> chunk edges) are cut
-        into chunk-sized pieces whose partial sums are combined in fixed order."""
-        key = ("split", int(chunk))
+        into chunk-sized pieces whose partial sums are combined in fixed order;
+        items are ordered longest-length-class first."""
+        key = ("split", int(chunk), bool(length_classes))
         if key not in self._plans:
             lib = nat.load()
             rp = np.ascontiguousarray(self.row_ptr.cpu().numpy(), dtype=np.int32)
@@ -362,6 +363,7 @@ class CsrMatrix:
             items = np.empty((int(ni[0]), 4), np.int32)
             split = np.empty((max(int(nsr[0]), 1), 4), np.int32)
             nat.check(lib.gc_spmm_plan_fill(rp.ctypes.data, self.n_rows, int(chunk),
+                                            nat.GC_PLAN_LENGTH_CLASSES if length_classes else 0,
                                             items.ctypes.data, split.ctypes.data), "gc_spmm_plan_fill")
             self._plans[key] = (torch.from_numpy(items).to(self.device),
                                 torch.from_numpy(split[: int(nsr[0])]).to(self.device), int(ns[0]))
@@ -387,7 +389,12 @@ def _as_values(x, dev) -> torch.Tensor:
 # SpMM — reference sparse.py:240-264
 # ---------------------------------------------------------------------------
 
-SPLIT_CHUNK = int(os.environ.get("GNNC_SPLIT_CHUNK", "2048"))
+SPLIT_CHUNK = int(os.environ.get("GNNC_SPLIT_CHUNK", "0"))  # 0: per-launch default
+PLAN_MIN_NNZ = 1 << 16  # below this a row-per-group launch needs no plan
+
+
+def _sm_count(dev: torch.device) -> int:
+    return torch.cuda.get_device_properties(dev).multi_processor_count
 
 
 def _spmm(a: CsrMatrix, b, *, weighted: bool, d_row=None, d_col=None, relu=False, out=None,
@@ -409,12 +416,14 @@ def _spmm(a: CsrMatrix, b, *, weighted: bool, d_row=None, d_col=None, relu=False
         if d is not None and tuple(d.shape) != (n,):
             raise ShapeError(f"{what}: {nm} must have {n} entries")
     flags = (nat.GC_RELU if relu else 0) | (nat.GC_ACCUMULATE if accumulate else 0)
-    use_split = algo == "split" or (algo == "auto" and a.nnz and a.max_degree() > SPLIT_CHUNK)
+    chunk = SPLIT_CHUNK or int(nat.load().gc_spmm_default_chunk(a.n_rows, a.nnz, K, _sm_count(dev)))
+    use_split = algo == "split" or (algo == "auto" and a.nnz and (
+        a.nnz >= PLAN_MIN_NNZ or a.max_degree() > chunk))
     items = split = ws = None
     n_items = n_split = 0
     code = nat.GC_SPMM_ROW
     if use_split:
-        items, split, n_slots = a.spmm_plan(SPLIT_CHUNK)
+        items, split, n_slots = a.spmm_plan(chunk)
         n_items, n_split = items.shape[0], split.shape[0]
         code = nat.GC_SPMM_NNZ_SPLIT
         if n_slots:

@@ -66,7 +66,7 @@ def test_error_codes_without_launch(lib):
     assert rc == _native.GC_ERR_VALUE
 
 
-def _plan(lib, rp, chunk):
+def _plan(lib, rp, chunk, flags=0):
     rp = np.ascontiguousarray(rp, dtype=np.int32)
     ni, ns, nsr = (np.zeros(1, np.int64) for _ in range(3))
     assert lib.gc_spmm_plan_count(rp.ctypes.data, rp.size - 1, chunk,
@@ -74,17 +74,27 @@ def _plan(lib, rp, chunk):
                                   nsr.ctypes.data_as(_native._i64p)) == 0
     items = np.zeros((ni[0], 4), np.int32)
     split = np.zeros((max(nsr[0], 1), 4), np.int32)
-    assert lib.gc_spmm_plan_fill(rp.ctypes.data, rp.size - 1, chunk, items.ctypes.data,
+    assert lib.gc_spmm_plan_fill(rp.ctypes.data, rp.size - 1, chunk, flags, items.ctypes.data,
                                  split.ctypes.data) == 0
     return items, split[: nsr[0]], int(ns[0])
 
 
-def test_spmm_plan_covers_every_edge_once(lib):
+@pytest.mark.parametrize("flags", [0, 1])
+def test_spmm_plan_covers_every_edge_once(lib, flags):
     rng = np.random.default_rng(0)
     deg = rng.integers(0, 50, size=200)
     deg[[3, 77]] = [500, 1000]
     rp = np.concatenate(([0], np.cumsum(deg)))
-    items, split, n_slots = _plan(lib, rp, 64)
+    items, split, n_slots = _plan(lib, rp, 64, flags)
+    lens = items[:, 2] - items[:, 1]
+    if flags:  # longest length class first, stable within a class
+        cls = np.where(lens == 0, 0, np.floor(np.log2(np.maximum(lens, 1))).astype(int) + 1)
+        assert np.all(np.diff(cls) <= 0)
+        for c in np.unique(cls):
+            r = items[cls == c, 0]
+            assert np.all(np.diff(r) >= 0)
+    else:
+        assert np.all(np.diff(items[:, 0]) >= 0)
     covered = np.zeros(rp[-1], np.int32)
     for r, b, e, s in items:
         assert rp[r] <= b <= e <= rp[r + 1] and e - b <= 64
@@ -104,6 +114,13 @@ def test_partition_bit_exact_with_oracle(lib, oracle, parts):
     out = np.zeros(parts + 1, np.int64)
     assert lib.gc_partition_rows(rp.ctypes.data, rp.size - 1, parts, out.ctypes.data) == 0
     assert np.array_equal(out, oracle.partition_rows(rp, parts))
+
+
+def test_default_chunk(lib):
+    assert lib.gc_spmm_default_chunk(100, 1000, 256, 148) == 128
+    assert lib.gc_spmm_default_chunk(233_000, 115_000_000, 256, 148) == 4096
+    c = lib.gc_spmm_default_chunk(169_343, 2_500_000, 32, 148)
+    assert 128 <= c <= 512 and c & (c - 1) == 0
 
 
 def test_partition_edge_cases(lib, oracle):
