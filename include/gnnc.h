@@ -52,6 +52,9 @@ extern "C" {
 /* epilogue / mode flags */
 #define GC_RELU (1u << 0)       /* out = max(out, 0) (gcn.py:115-116, gat.py:117-118) */
 #define GC_ACCUMULATE (1u << 1) /* out += result instead of out = result */
+#define GC_HUB_TAGGED (1u << 2) /* col_idx entries carry a hub tag in bit 31 (gc_tag_hub_columns):
+                                   tagged rows of B are gathered with L1::evict_last, the rest
+                                   with L1::no_allocate (SpMM / GAT aggregation only) */
 #define GC_GEMM_TF32 (1u << 4)  /* tcgen05.mma kind::tf32, TMEM accumulators, TMA operands */
 #define GC_GEMM_FP32 (1u << 5)  /* exact fp32 CUDA-core path (rtol 1e-4 parity mode) */
 
@@ -103,6 +106,29 @@ GNNC_API int gc_spmm_plan_count(const int32_t *row_ptr_host, int64_t n_rows, int
 GNNC_API int gc_spmm_plan_fill(const int32_t *row_ptr_host, int64_t n_rows, int32_t chunk,
                       uint32_t plan_flags, int32_t *items_host, int32_t *split_rows_host);
 
+/* Fused GAT aggregation: for each row i
+ *   C[i,:] = epi( sum_p alpha_p * B[col_idx[p],:] ),
+ *   alpha_p = exp(e_p - max_row) / sum_row,  e_p = LeakyReLU(s[i] + t[col_idx[p]])
+ * i.e. gat.py:72-95 (_edge_scores_softmax) followed by the aggregation
+ * spmm(alpha, B) of gat_layer_reuse/recompute (gat.py:121-145), computed with
+ * an online softmax so alpha is never materialised.  Rows without edges give 0.
+ * Same plan/workspace protocol as gc_spmm_f32; NNZ_SPLIT needs
+ * n_slots*(4*K + 8) + 8 bytes of workspace (partial rows, then 8-byte aligned
+ * (max, sum) pairs). */
+GNNC_API int gc_gat_aggregate_f32(const int32_t *row_ptr, const int32_t *col_idx, const float *s,
+                                  const float *t, float slope, const float *B, int64_t ldb,
+                                  int64_t n_rows, int64_t n_cols, int64_t K, float *C, int64_t ldc,
+                                  uint32_t flags, int algo, const int32_t *items, int64_t n_items,
+                                  const int32_t *split_rows, int64_t n_split_rows, void *workspace,
+                                  size_t ws_bytes, void *stream);
+
+/* col_tagged[p] = col_idx[p] | (hot[col_idx[p]] ? 1<<31 : 0): a copy of the
+ * pattern whose hub columns (hot: uint8 per column) are tagged for
+ * GC_HUB_TAGGED launches.  The untagged col_idx stays valid for every other
+ * kernel. */
+GNNC_API int gc_tag_hub_columns(const int32_t *col_idx, int64_t nnz, const uint8_t *hot,
+                                int32_t *col_tagged, void *stream);
+
 /* ---- SDDMM --------------------------------------------------------------
  * out[p] = (a_vals ? a_vals[p] : 1) * sum_t B[i,t] * Cm[col_idx[p],t]
  * Replaces sparse.sddmm (sparse.py:267-282 -> _sddmm_kernel 222-232).
@@ -136,10 +162,14 @@ GNNC_API int gc_scale_rows_f32(const float *d, const float *B, int64_t ldb, int6
 
 /* ---- GAT attention -------------------------------------------------------
  * Node projections (the reassociated attention of gat.py:110-111):
- *   s[h*n + i] = sum_c HW[i, h*k2 + c] * a_src[h*k2 + c],  likewise t/a_dst,
- * for heads h = 0..heads-1 (heads = 1 is the reference's single head). */
-GNNC_API int gc_node_proj_f32(const float *HW, int64_t ld, int64_t n_rows, int64_t k2, int32_t heads,
-                     const float *a_src, const float *a_dst, float *s, float *t, void *stream);
+ *   s[h*n + i] = sum_c X[i, h*head_stride + c] * a_src[h*k2 + c],  likewise t/a_dst,
+ * for heads h = 0..heads-1 (heads = 1 is the reference's single head).
+ * X = HW with head_stride = k2 is the reference's form; X = H with
+ * head_stride = 0 and a = W_h a_h (k1-vectors) gives the same s, t without
+ * forming HW (used by the recompute composition). */
+GNNC_API int gc_node_proj_f32(const float *X, int64_t ld, int64_t n_rows, int64_t k2, int32_t heads,
+                     int64_t head_stride, const float *a_src, const float *a_dst, float *s,
+                     float *t, void *stream);
 
 /* Fused LeakyReLU + edge softmax over each CSR row (gat.py:72-95):
  *   e = s[h,i] + t[h,j]; e = e < 0 ? e * slope : e;

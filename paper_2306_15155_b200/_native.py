@@ -15,6 +15,7 @@ from ._build import LIB, ROOT
 
 GC_RELU = 1 << 0
 GC_ACCUMULATE = 1 << 1
+GC_HUB_TAGGED = 1 << 2
 GC_GEMM_TF32 = 1 << 4
 GC_GEMM_FP32 = 1 << 5
 GC_SPMM_ROW = 1
@@ -56,11 +57,14 @@ _SIGNATURES = {
     "gc_gemm_f32": (ctypes.c_int, [_P, _I64, _P, _I64, _I64, _I64, _I64, _P, _I64, _P, _U32, _P,
                                    _SZ, _P]),
     "gc_scale_rows_f32": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _P, _I64, _U32, _P]),
-    "gc_node_proj_f32": (ctypes.c_int, [_P, _I64, _I64, _I64, _I32, _P, _P, _P, _P, _P]),
+    "gc_node_proj_f32": (ctypes.c_int, [_P, _I64, _I64, _I64, _I32, _I64, _P, _P, _P, _P, _P]),
+    "gc_gat_aggregate_f32": (ctypes.c_int, [_P, _P, _P, _P, _F, _P, _I64, _I64, _I64, _I64, _P, _I64,
+                                            _U32, ctypes.c_int, _P, _I64, _P, _I64, _P, _SZ, _P]),
     "gc_edge_softmax_f32": (ctypes.c_int, [_P, _P, _P, _P, _I32, _F, _I64, _I64, _P, _P]),
     "gc_attn_sddmm_f32": (ctypes.c_int, [_P, _P, _P, _I64, _I64, _I32, _P, _P, _F, _I64, _I64, _P,
                                          _P]),
     "gc_partition_rows": (ctypes.c_int, [_P, _I64, _I32, _P]),
+    "gc_tag_hub_columns": (ctypes.c_int, [_P, _I64, _P, _P, _P]),
 }
 
 

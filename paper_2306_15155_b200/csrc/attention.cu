@@ -61,14 +61,15 @@ __global__ void __launch_bounds__(kThreads)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads)
     node_proj_kernel(const float *__restrict__ HW, int64_t ld, int64_t n_rows, int64_t k2,
-                     int heads, const float *__restrict__ a_src, const float *__restrict__ a_dst,
-                     float *__restrict__ s, float *__restrict__ t, bool vec) {
+                     int heads, int64_t head_stride, const float *__restrict__ a_src,
+                     const float *__restrict__ a_dst, float *__restrict__ s,
+                     float *__restrict__ t, bool vec) {
   const int64_t row = (int64_t)blockIdx.x * (kThreads / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   if (row >= n_rows) return;
   const float *hr = HW + row * ld;
   for (int h = 0; h < heads; ++h) {
-    const float *x = hr + (int64_t)h * k2;
+    const float *x = hr + (int64_t)h * head_stride;
     const float *al = a_src + (int64_t)h * k2;
     const float *ar = a_dst + (int64_t)h * k2;
     float ss = 0.f, tt = 0.f;
@@ -274,19 +275,20 @@ extern "C" int gc_sddmm_norm_f32(const int32_t *row_ptr, const int32_t *col_idx,
 }
 
 extern "C" int gc_node_proj_f32(const float *HW, int64_t ld, int64_t n_rows, int64_t k2,
-                                int32_t heads, const float *a_src, const float *a_dst, float *s,
-                                float *t, void *stream) {
-  GC_REQUIRE(n_rows >= 0 && k2 >= 1 && heads >= 1 && ld >= k2 * heads, GC_ERR_SHAPE,
-             "gc_node_proj_f32: bad shape");
+                                int32_t heads, int64_t head_stride, const float *a_src,
+                                const float *a_dst, float *s, float *t, void *stream) {
+  GC_REQUIRE(n_rows >= 0 && k2 >= 1 && heads >= 1 && head_stride >= 0 &&
+                 ld >= k2 + head_stride * (heads - 1),
+             GC_ERR_SHAPE, "gc_node_proj_f32: bad shape");
   if (n_rows == 0) return GC_OK;
   GC_REQUIRE(HW && a_src && a_dst && s && t, GC_ERR_VALUE, "gc_node_proj_f32: null operand");
-  const bool vec = (k2 % 4 == 0) && (ld % 4 == 0) && aligned16(HW) && aligned16(a_src) &&
-                   aligned16(a_dst);
+  const bool vec = (k2 % 4 == 0) && (ld % 4 == 0) && (head_stride % 4 == 0) && aligned16(HW) &&
+                   aligned16(a_src) && aligned16(a_dst);
   unsigned grid;
   int rc = rows_grid(n_rows, 32, &grid);
   if (rc) return rc;
-  node_proj_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(HW, ld, n_rows, k2, heads, a_src,
-                                                             a_dst, s, t, vec);
+  node_proj_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(HW, ld, n_rows, k2, heads,
+                                                             head_stride, a_src, a_dst, s, t, vec);
   return check_launch("node_proj_kernel");
 }
 

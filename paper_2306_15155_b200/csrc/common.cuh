@@ -52,6 +52,23 @@ __device__ __forceinline__ float4 ldg_f4(const float *p) {
   return r;
 }
 
+// Gathers with explicit L1 policy: hub rows stay resident (evict_last), the
+// long tail streams through without allocating (no_allocate).
+__device__ __forceinline__ float4 ldg_f4_keep(const float *p) {
+  float4 r;
+  asm("ld.global.nc.L1::evict_last.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+      : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float4 ldg_f4_stream(const float *p) {
+  float4 r;
+  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+      : "l"(p));
+  return r;
+}
+
 // Streaming loads (cache-streaming policy: evict-first in L1 and L2) for
 // data read exactly once per kernel (col_idx, values).
 __device__ __forceinline__ int ldg_stream_i32(const int32_t *p) { return __ldcs(p); }

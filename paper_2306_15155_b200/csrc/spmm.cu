@@ -1,18 +1,24 @@
-// CSR SpMM for sm_100a: C = epi( D_row * (A ∘ d_col) * B ).
+// CSR SpMM for sm_100a: C = epi( D_row * (A ∘ d_col) * B ), and its GAT form
+// C = epi( softmax_row(LeakyReLU(s_i + t_j)) * B ) with the edge softmax
+// computed online inside the aggregation (α is never written).
 //
 // Reference semantics: gnncompose/sparse.py:196-219 (_spmm_kernel,
-// _spmm_unweighted_kernel) — every output row owns its accumulation and
-// visits edges in ascending storage order.  Here a row is owned by a group of
-// LPR lanes; each lane owns NV float4 (or scalar) column slots of the row and
-// accumulates the row's edges sequentially with FMA, so the order is fixed
-// and `values == nullptr` is bit-identical to unit values.
+// _spmm_unweighted_kernel) and gat.py:72-95 + sparse.py:196-205 for the GAT
+// form.  A row is owned by a group of LPR lanes; each lane owns NV float4 (or
+// scalar) column slots of the row and accumulates the row's edges in storage
+// order with FMA, so the order is fixed and `values == nullptr` is
+// bit-identical to unit values.
 //
-// Memory plan (HBM-bound): col_idx/values are streamed once
-// (evict-first), the gathered rows of B go through the read-only path as
-// 128-bit loads, U edges are unrolled so each lane keeps U*NV independent
-// 16-byte loads in flight.  The D^-1/2 factors of the dynamic composition are
-// folded in (d_col into the edge weight, d_row into the epilogue) instead of
-// materialising D^-1/2 H.
+// Memory plan: col_idx/values stream once (evict-first),
+// the gathered rows of B go through the read-only path as 128-bit loads, the
+// next batch of column indices is in flight while the current batch's rows are
+// gathered, and U edges are unrolled per step.  The D^-1/2 factors of the
+// dynamic composition are folded in (d_col into the edge weight, d_row into
+// the epilogue) instead of materialising D^-1/2 H.  Heavy rows are cut into
+// plan items whose partial sums (and, for GAT, partial (max, sum) pairs) are
+// merged in slot order by the fixup kernel.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace gnnc {
@@ -33,8 +39,13 @@ struct SpmmArgs {
   int64_t ldc;
   const int4 *items;  // nullptr: one item per row
   int64_t n_items;
-  float *partial;  // [n_slots][K] for split items
+  float *partial;     // [n_slots][K] for split items
+  float2 *partial_mz; // GAT: [n_slots] running (max, sum) of each split item
+  const float *s;     // GAT: per-row source score (s = HW a_src)
+  const float *t;     // GAT: per-column target score (t = HW a_dst)
+  float slope;        // GAT: LeakyReLU slope
   uint32_t flags;
+  bool hints;         // col_idx carries hub tags in bit 31 (gc_tag_hub_columns)
 };
 
 template <bool VEC>
@@ -59,8 +70,17 @@ __device__ __forceinline__ void fma_into(float4 &acc, float w, float4 b) {
   acc.w = fmaf(w, b.w, acc.w);
 }
 __device__ __forceinline__ void fma_into(float &acc, float w, float b) { acc = fmaf(w, b, acc); }
+__device__ __forceinline__ void scale_into(float4 &acc, float sc) {
+  acc.x *= sc, acc.y *= sc, acc.z *= sc, acc.w *= sc;
+}
+__device__ __forceinline__ void scale_into(float &acc, float sc) { acc *= sc; }
 __device__ __forceinline__ void load_b(float4 &dst, const float *p) { dst = ldg_f4(p); }
 __device__ __forceinline__ void load_b(float &dst, const float *p) { dst = __ldg(p); }
+// hot-column hint (bit 31 of a tagged col_idx entry): hub rows are kept in L1
+__device__ __forceinline__ void load_b_hint(float4 &dst, const float *p, bool hot) {
+  dst = hot ? ldg_f4_keep(p) : ldg_f4_stream(p);
+}
+__device__ __forceinline__ void load_b_hint(float &dst, const float *p, bool) { dst = __ldg(p); }
 
 __device__ __forceinline__ float epi1(float v, float ds, float old, uint32_t flags) {
   v *= ds;
@@ -76,10 +96,9 @@ __device__ __forceinline__ int64_t col_of(int64_t c0, int v, int gl) {
 
 template <int LPR, int NV, bool VEC>
 __device__ __forceinline__ void store_row(const SpmmArgs &a, int row, int slot, int gl,
-                                          int64_t c0,
+                                          int64_t c0, float ds,
                                           const typename Lanes<VEC>::T (&acc)[NV]) {
   const uint32_t flags = a.flags;
-  const float ds = (slot < 0 && a.d_row) ? __ldg(a.d_row + row) : 1.0f;
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
     const int64_t c = col_of<LPR, NV, VEC>(c0, v, gl);
@@ -108,7 +127,7 @@ __device__ __forceinline__ void store_row(const SpmmArgs &a, int row, int slot, 
 }
 
 // One group of LPR lanes per work item (a row, or a chunk of a heavy row).
-template <int LPR, int NV, bool VEC, bool HAS_VAL, bool HAS_DCOL>
+template <int LPR, int NV, bool VEC, bool HAS_VAL, bool HAS_DCOL, bool GAT, bool HINT>
 __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
   using T = typename Lanes<VEC>::T;
   constexpr int GPB = kThreads / LPR;
@@ -146,6 +165,10 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
 
   const int len = end - beg;
   const int wmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)len);
+  // GAT: online softmax state; m is identical on every lane of the group,
+  // zl sums this lane's own edge weights relative to m.
+  const float si = (GAT && live) ? __ldg(a.s + row) : 0.0f;
+  float m = -INFINITY, zl = 0.0f;
   // software pipeline: the (col, value) batch for the next LPR edges is in
   // flight while the B rows of the current batch are gathered.
   int jn = 0;
@@ -155,7 +178,8 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
     if (HAS_VAL) vn = ldg_stream_f32(a.values + beg + gl);
   }
   for (int base = 0; base < wmax; base += LPR) {
-    const int j = jn;
+    const int j = HINT ? (jn & 0x7FFFFFFF) : jn;  // HINT: bit 31 tags a hub column
+    const bool hot = HINT && jn < 0;
     const float v = vn;
     const bool mine = base + gl < len;
     if (base + LPR + gl < len) {
@@ -164,6 +188,21 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
     }
     float dj = 1.0f;
     if (HAS_DCOL && mine) dj = __ldg(a.d_col + j);
+    float e = -INFINITY;
+    if (GAT) {
+      if (mine) e = leaky(si + __ldg(a.t + j), a.slope);
+      const float mb = group_max<LPR>(e);
+      const float mn = fmaxf(m, mb);
+      if (mn > m) {  // group-uniform: rescale the running sums to the new max
+        const float sc = __expf(m - mn);
+#pragma unroll
+        for (int vv = 0; vv < NV; ++vv) scale_into(acc[vv], sc);
+        zl *= sc;
+        m = mn;
+      }
+      dj = mine ? __expf(e - m) : 0.0f;
+      zl += dj;
+    }
     const int cnt = len - base;  // edges left for this group (may be <= 0)
     const int cntw = min(LPR, wmax - base);
 #pragma unroll 1
@@ -174,10 +213,15 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
         const int je = __shfl_sync(0xffffffffu, j, e0 + u, LPR);
         const bool ok = (e0 + u) < cnt;
         const float *brow = a.B + (int64_t)je * a.ldb;
+        bool hote = false;
+        if (HINT) hote = __shfl_sync(0xffffffffu, (int)hot, e0 + u, LPR) != 0;
 #pragma unroll
         for (int vv = 0; vv < NV; ++vv) {
           bv[u][vv] = zero_of(T{});
-          if (ok && colok[vv]) load_b(bv[u][vv], brow + coff[vv]);
+          if (ok && colok[vv]) {
+            if (HINT) load_b_hint(bv[u][vv], brow + coff[vv], hote);
+            else load_b(bv[u][vv], brow + coff[vv]);
+          }
         }
       }
       const float w = mine ? v * dj : 0.0f;
@@ -191,11 +235,22 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
       }
     }
   }
-  if (live) store_row<LPR, NV, VEC>(a, row, slot, gl, c0, acc);
+  float ds = 1.0f;
+  if (GAT) {
+    const float z = group_sum<LPR>(zl);
+    if (slot >= 0) {
+      if (live && gl == 0 && blockIdx.y == 0) a.partial_mz[slot] = make_float2(m, z);
+    } else {
+      ds = z > 0.0f ? 1.0f / z : 0.0f;  // rows without edges aggregate to 0
+    }
+  } else if (slot < 0 && live && a.d_row) {
+    ds = __ldg(a.d_row + row);
+  }
+  if (live) store_row<LPR, NV, VEC>(a, row, slot, gl, c0, ds, acc);
 }
 
 // Combine the partial sums of split rows in slot order, then the epilogue.
-template <int LPR, int NV, bool VEC>
+template <int LPR, int NV, bool VEC, bool GAT>
 __global__ void __launch_bounds__(kThreads)
     spmm_fixup_kernel(const SpmmArgs a, const int4 *split_rows, int64_t n_split) {
   using T = typename Lanes<VEC>::T;
@@ -210,22 +265,34 @@ __global__ void __launch_bounds__(kThreads)
   T acc[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) acc[v] = zero_of(T{});
+  float mx = -INFINITY, z = 0.0f;
+  if (GAT)
+    for (int q = 0; q < sr.z; ++q) mx = fmaxf(mx, a.partial_mz[sr.y + q].x);
   for (int q = 0; q < sr.z; ++q) {
     const float *src = a.partial + (int64_t)(sr.y + q) * a.K;
+    float w = 1.0f;
+    if (GAT) {
+      const float2 mz = a.partial_mz[sr.y + q];
+      w = mz.x == -INFINITY ? 0.0f : __expf(mz.x - mx);
+      z = fmaf(w, mz.y, z);
+    }
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       const int64_t c = col_of<LPR, NV, VEC>(c0, v, gl);
       if (c < a.K) {
         T t;
         load_b(t, src + c);
-        fma_into(acc[v], 1.0f, t);
+        fma_into(acc[v], w, t);
       }
     }
   }
-  store_row<LPR, NV, VEC>(a, sr.x, -1, gl, c0, acc);
+  float ds = 1.0f;
+  if (GAT) ds = z > 0.0f ? 1.0f / z : 0.0f;
+  else if (a.d_row) ds = __ldg(a.d_row + sr.x);
+  store_row<LPR, NV, VEC>(a, sr.x, -1, gl, c0, ds, acc);
 }
 
-template <int LPR, int NV, bool VEC>
+template <int LPR, int NV, bool VEC, bool GAT>
 int launch_cfg(const SpmmArgs &a, const int4 *split_rows, int64_t n_split, cudaStream_t st) {
   constexpr int GPB = kThreads / LPR;
   constexpr int64_t kColsPerPass = (int64_t)LPR * NV * Lanes<VEC>::W;
@@ -237,25 +304,109 @@ int launch_cfg(const SpmmArgs &a, const int4 *split_rows, int64_t n_split, cudaS
   if (a.n_items > 0) {
     dim3 grid((unsigned)((a.n_items + GPB - 1) / GPB), (unsigned)ychunks);
     const bool hv = a.values != nullptr, hd = a.d_col != nullptr;
-    if (hv && hd) spmm_kernel<LPR, NV, VEC, true, true><<<grid, kThreads, 0, st>>>(a);
-    else if (hv) spmm_kernel<LPR, NV, VEC, true, false><<<grid, kThreads, 0, st>>>(a);
-    else if (hd) spmm_kernel<LPR, NV, VEC, false, true><<<grid, kThreads, 0, st>>>(a);
-    else spmm_kernel<LPR, NV, VEC, false, false><<<grid, kThreads, 0, st>>>(a);
-    int rc = check_launch("spmm_kernel");
+    if (a.hints) {
+      if (GAT) spmm_kernel<LPR, NV, VEC, false, false, true, true><<<grid, kThreads, 0, st>>>(a);
+      else if (hv && hd) spmm_kernel<LPR, NV, VEC, true, true, false, true><<<grid, kThreads, 0, st>>>(a);
+      else if (hv) spmm_kernel<LPR, NV, VEC, true, false, false, true><<<grid, kThreads, 0, st>>>(a);
+      else if (hd) spmm_kernel<LPR, NV, VEC, false, true, false, true><<<grid, kThreads, 0, st>>>(a);
+      else spmm_kernel<LPR, NV, VEC, false, false, false, true><<<grid, kThreads, 0, st>>>(a);
+    } else {
+      if (GAT) spmm_kernel<LPR, NV, VEC, false, false, true, false><<<grid, kThreads, 0, st>>>(a);
+      else if (hv && hd) spmm_kernel<LPR, NV, VEC, true, true, false, false><<<grid, kThreads, 0, st>>>(a);
+      else if (hv) spmm_kernel<LPR, NV, VEC, true, false, false, false><<<grid, kThreads, 0, st>>>(a);
+      else if (hd) spmm_kernel<LPR, NV, VEC, false, true, false, false><<<grid, kThreads, 0, st>>>(a);
+      else spmm_kernel<LPR, NV, VEC, false, false, false, false><<<grid, kThreads, 0, st>>>(a);
+    }
+    int rc = check_launch(GAT ? "gat_aggregate_kernel" : "spmm_kernel");
     if (rc) return rc;
   }
   if (n_split > 0) {
     dim3 grid((unsigned)((n_split + GPB - 1) / GPB), (unsigned)ychunks);
-    spmm_fixup_kernel<LPR, NV, VEC><<<grid, kThreads, 0, st>>>(a, split_rows, n_split);
+    spmm_fixup_kernel<LPR, NV, VEC, GAT><<<grid, kThreads, 0, st>>>(a, split_rows, n_split);
     return check_launch("spmm_fixup_kernel");
   }
   return GC_OK;
 }
 
 }  // namespace
+
+namespace {
+
+template <bool GAT>
+int dispatch(SpmmArgs &a, int64_t n_rows, int algo, const int32_t *items, int64_t n_items,
+             const int32_t *split_rows, int64_t n_split_rows, void *workspace, size_t ws_bytes,
+             void *stream, const char *who) {
+  const int4 *sr = nullptr;
+  int64_t n_split = 0;
+  if (algo == GC_SPMM_NNZ_SPLIT) {
+    GC_REQUIRE(items && n_items >= n_rows, GC_ERR_VALUE, "%s: NNZ_SPLIT needs a plan", who);
+    GC_REQUIRE(n_split_rows == 0 || split_rows, GC_ERR_VALUE, "%s: split_rows null", who);
+    a.items = reinterpret_cast<const int4 *>(items);
+    a.n_items = n_items;
+    sr = reinterpret_cast<const int4 *>(split_rows);
+    n_split = n_split_rows;
+    if (n_split > 0) {
+      GC_REQUIRE(workspace != nullptr && aligned16(workspace), GC_ERR_WORKSPACE,
+                 "%s: 16-byte aligned workspace required", who);
+      a.partial = static_cast<float *>(workspace);
+      if (GAT) {
+        // (max, sum) pairs follow the [n_slots][K] partial rows; the host
+        // wrapper sized the workspace from the plan it owns.
+        GC_REQUIRE(ws_bytes > 0, GC_ERR_WORKSPACE, "%s: bad workspace", who);
+        const size_t n_slots = ws_bytes / (size_t)(4 * a.K + 8);
+        const size_t off = (n_slots * (size_t)a.K * 4 + 7) & ~(size_t)7;
+        a.partial_mz = reinterpret_cast<float2 *>(static_cast<char *>(workspace) + off);
+      }
+    }
+  } else if (algo == GC_SPMM_ROW || algo == 0) {
+    a.items = nullptr;
+    a.n_items = n_rows;
+  } else {
+    set_error("%s: unknown algo %d", who, algo);
+    return GC_ERR_VALUE;
+  }
+  const int64_t K = a.K;
+  const bool vec = (K % 4 == 0) && (a.ldb % 4 == 0) && (a.ldc % 4 == 0) && aligned16(a.B) &&
+                   aligned16(a.C) && (a.partial == nullptr || aligned16(a.partial));
+  cudaStream_t st = as_stream(stream);
+  if (vec) {
+    if (K <= 8) return launch_cfg<2, 1, true, GAT>(a, sr, n_split, st);
+    if (K <= 16) return launch_cfg<4, 1, true, GAT>(a, sr, n_split, st);
+    if (K <= 32) return launch_cfg<8, 1, true, GAT>(a, sr, n_split, st);
+    if (K <= 64) return launch_cfg<16, 1, true, GAT>(a, sr, n_split, st);
+    if (K <= 128) return launch_cfg<32, 1, true, GAT>(a, sr, n_split, st);
+    return launch_cfg<32, 2, true, GAT>(a, sr, n_split, st);
+  }
+  if (K <= 8) return launch_cfg<8, 1, false, GAT>(a, sr, n_split, st);
+  if (K <= 16) return launch_cfg<16, 1, false, GAT>(a, sr, n_split, st);
+  if (K <= 32) return launch_cfg<32, 1, false, GAT>(a, sr, n_split, st);
+  if (K <= 64) return launch_cfg<32, 2, false, GAT>(a, sr, n_split, st);
+  return launch_cfg<32, 4, false, GAT>(a, sr, n_split, st);
+}
+
+__global__ void tag_hub_kernel(const int32_t *__restrict__ col, int64_t nnz,
+                               const uint8_t *__restrict__ hot, int32_t *__restrict__ out) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = __ldg(col + p);
+    out[p] = __ldg(hot + c) ? (int32_t)((uint32_t)c | 0x80000000u) : c;
+  }
+}
+
+}  // namespace
 }  // namespace gnnc
 
 using namespace gnnc;
+
+extern "C" int gc_tag_hub_columns(const int32_t *col_idx, int64_t nnz, const uint8_t *hot,
+                                  int32_t *col_tagged, void *stream) {
+  GC_REQUIRE(nnz >= 0, GC_ERR_SHAPE, "gc_tag_hub_columns: nnz < 0");
+  if (nnz == 0) return GC_OK;
+  GC_REQUIRE(col_idx && hot && col_tagged, GC_ERR_VALUE, "gc_tag_hub_columns: null operand");
+  const int64_t blocks = std::min<int64_t>((nnz + 255) / 256, (int64_t)sm_count() * 32);
+  tag_hub_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(col_idx, nnz, hot, col_tagged);
+  return check_launch("tag_hub_kernel");
+}
 
 extern "C" int gc_spmm_f32(const int32_t *row_ptr, const int32_t *col_idx, const float *values,
                            const float *d_row, const float *d_col, const float *B, int64_t ldb,
@@ -265,13 +416,12 @@ extern "C" int gc_spmm_f32(const int32_t *row_ptr, const int32_t *col_idx, const
                            size_t ws_bytes, void *stream) {
   GC_REQUIRE(n_rows >= 0 && n_cols >= 0 && K >= 0, GC_ERR_SHAPE, "gc_spmm_f32: negative size");
   GC_REQUIRE(ldb >= K && ldc >= K, GC_ERR_SHAPE, "gc_spmm_f32: leading dimension < K");
-  GC_REQUIRE((flags & ~(GC_RELU | GC_ACCUMULATE)) == 0, GC_ERR_VALUE,
+  GC_REQUIRE((flags & ~(GC_RELU | GC_ACCUMULATE | GC_HUB_TAGGED)) == 0, GC_ERR_VALUE,
              "gc_spmm_f32: unknown flags 0x%x", flags);
   if (n_rows == 0 || K == 0) return GC_OK;
   GC_REQUIRE(row_ptr && C && (B || n_cols == 0), GC_ERR_VALUE, "gc_spmm_f32: null operand");
   GC_REQUIRE(n_rows < INT32_MAX && n_cols < INT32_MAX, GC_ERR_SHAPE,
              "gc_spmm_f32: int32 index range exceeded");
-
   SpmmArgs a{};
   a.row_ptr = row_ptr;
   a.col_idx = col_idx;
@@ -284,43 +434,43 @@ extern "C" int gc_spmm_f32(const int32_t *row_ptr, const int32_t *col_idx, const
   a.C = C;
   a.ldc = ldc;
   a.flags = flags;
-  const int4 *sr = nullptr;
-  int64_t n_split = 0;
-  if (algo == GC_SPMM_NNZ_SPLIT) {
-    GC_REQUIRE(items && n_items >= n_rows, GC_ERR_VALUE, "gc_spmm_f32: NNZ_SPLIT needs a plan");
-    GC_REQUIRE(n_split_rows == 0 || split_rows, GC_ERR_VALUE, "gc_spmm_f32: split_rows null");
-    a.items = reinterpret_cast<const int4 *>(items);
-    a.n_items = n_items;
-    sr = reinterpret_cast<const int4 *>(split_rows);
-    n_split = n_split_rows;
-    if (n_split > 0) {
-      // slots are numbered densely; the last split row tells how many exist
-      GC_REQUIRE(workspace != nullptr, GC_ERR_WORKSPACE, "gc_spmm_f32: workspace required");
-      a.partial = static_cast<float *>(workspace);
-      (void)ws_bytes;  // size validated by the host wrapper (it owns the plan)
-    }
-  } else if (algo == GC_SPMM_ROW || algo == 0) {
-    a.items = nullptr;
-    a.n_items = n_rows;
-  } else {
-    set_error("gc_spmm_f32: unknown algo %d", algo);
-    return GC_ERR_VALUE;
-  }
+  a.hints = (flags & GC_HUB_TAGGED) != 0;
+  return dispatch<false>(a, n_rows, algo, items, n_items, split_rows, n_split_rows, workspace,
+                         ws_bytes, stream, "gc_spmm_f32");
+}
 
-  const bool vec = (K % 4 == 0) && (ldb % 4 == 0) && (ldc % 4 == 0) && aligned16(B) &&
-                   aligned16(C) && (a.partial == nullptr || aligned16(a.partial));
-  cudaStream_t st = as_stream(stream);
-  if (vec) {
-    if (K <= 8) return launch_cfg<2, 1, true>(a, sr, n_split, st);
-    if (K <= 16) return launch_cfg<4, 1, true>(a, sr, n_split, st);
-    if (K <= 32) return launch_cfg<8, 1, true>(a, sr, n_split, st);
-    if (K <= 64) return launch_cfg<16, 1, true>(a, sr, n_split, st);
-    if (K <= 128) return launch_cfg<32, 1, true>(a, sr, n_split, st);
-    return launch_cfg<32, 2, true>(a, sr, n_split, st);
-  }
-  if (K <= 8) return launch_cfg<8, 1, false>(a, sr, n_split, st);
-  if (K <= 16) return launch_cfg<16, 1, false>(a, sr, n_split, st);
-  if (K <= 32) return launch_cfg<32, 1, false>(a, sr, n_split, st);
-  if (K <= 64) return launch_cfg<32, 2, false>(a, sr, n_split, st);
-  return launch_cfg<32, 4, false>(a, sr, n_split, st);
+extern "C" int gc_gat_aggregate_f32(const int32_t *row_ptr, const int32_t *col_idx,
+                                    const float *s, const float *t, float slope, const float *B,
+                                    int64_t ldb, int64_t n_rows, int64_t n_cols, int64_t K,
+                                    float *C, int64_t ldc, uint32_t flags, int algo,
+                                    const int32_t *items, int64_t n_items,
+                                    const int32_t *split_rows, int64_t n_split_rows,
+                                    void *workspace, size_t ws_bytes, void *stream) {
+  GC_REQUIRE(n_rows >= 0 && n_cols >= 0 && K >= 0, GC_ERR_SHAPE,
+             "gc_gat_aggregate_f32: negative size");
+  GC_REQUIRE(ldb >= K && ldc >= K, GC_ERR_SHAPE, "gc_gat_aggregate_f32: leading dimension < K");
+  GC_REQUIRE((flags & ~(GC_RELU | GC_HUB_TAGGED)) == 0, GC_ERR_VALUE,
+             "gc_gat_aggregate_f32: unknown flags 0x%x", flags);
+  GC_REQUIRE(slope > 0.0f && slope < 1.0f, GC_ERR_VALUE,
+             "gc_gat_aggregate_f32: leaky_slope must lie in (0, 1)");
+  if (n_rows == 0 || K == 0) return GC_OK;
+  GC_REQUIRE(row_ptr && C && s && t && (B || n_cols == 0), GC_ERR_VALUE,
+             "gc_gat_aggregate_f32: null operand");
+  GC_REQUIRE(n_rows < INT32_MAX && n_cols < INT32_MAX, GC_ERR_SHAPE,
+             "gc_gat_aggregate_f32: int32 index range exceeded");
+  SpmmArgs a{};
+  a.row_ptr = row_ptr;
+  a.col_idx = col_idx;
+  a.B = B;
+  a.ldb = ldb;
+  a.K = K;
+  a.C = C;
+  a.ldc = ldc;
+  a.flags = flags;
+  a.hints = (flags & GC_HUB_TAGGED) != 0;
+  a.s = s;
+  a.t = t;
+  a.slope = slope;
+  return dispatch<true>(a, n_rows, algo, items, n_items, split_rows, n_split_rows, workspace,
+                        ws_bytes, stream, "gc_gat_aggregate_f32");
 }

@@ -15,6 +15,12 @@ The attention itself has two B200 forms (``GatLayerSpec.attention``):
 * "sddmm": the score of every edge as a k2-wide SDDMM over HW rows
   (a_src·HW_i + a_dst·HW_j), fused with the same LeakyReLU + softmax.
 
+On the layer path (``gat_layer*``) the reassociated form never materialises
+α: one kernel computes the edge softmax online inside the aggregation
+(SURVEY.md §8(f) N1).  The recompute composition also skips HW entirely:
+s = H (W a_src), t = H (W a_dst) needs only two k1-vectors (gat.py:140 forms
+HW just for the scores).
+
 Multi-head (``heads`` > 1, not in the reference): W is
 k1 x (heads*k2) and attn vectors have heads*k2 entries; head h uses the column
 block h, and outputs are concatenated — identical to ``heads`` independent
@@ -30,7 +36,18 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .sparse import CsrMatrix, ShapeError, _Operand, _ld, _require_cuda, _stream, gemm, relu_, spmm
+from .sparse import (
+    CsrMatrix,
+    ShapeError,
+    _Operand,
+    _ld,
+    _require_cuda,
+    _stream,
+    gat_aggregate,
+    gemm,
+    relu_,
+    spmm,
+)
 
 
 class GatComposition(str, Enum):
@@ -140,12 +157,47 @@ def atten_calc(a_tilde: CsrMatrix, hw, spec: GatLayerSpec) -> AttentionMatrix:
     else:
         s = torch.empty(H, n, dtype=torch.float32, device=dev)
         t = torch.empty(H, n, dtype=torch.float32, device=dev)
-        nat.check(lib.gc_node_proj_f32(hwt.data_ptr(), _ld(hwt), n, k2, H, a_src.data_ptr(),
+        nat.check(lib.gc_node_proj_f32(hwt.data_ptr(), _ld(hwt), n, k2, H, k2, a_src.data_ptr(),
                                        a_dst.data_ptr(), s.data_ptr(), t.data_ptr(), st), "node_proj")
         nat.check(lib.gc_edge_softmax_f32(a_tilde.row_ptr.data_ptr(), a_tilde.col_idx.data_ptr(),
                                           s.data_ptr(), t.data_ptr(), H, float(spec.leaky_slope), n, m,
                                           alpha.data_ptr(), st), "edge_softmax")
     return AttentionMatrix(alpha=a_tilde.with_values(alpha[0]), values=alpha if H > 1 else None)
+
+
+def _projections(x: torch.Tensor, spec: GatLayerSpec, a_src: torch.Tensor, a_dst: torch.Tensor,
+                 width: int, head_stride: int) -> tuple[torch.Tensor, torch.Tensor]:
+    """s[h], t[h] = X[:, h-block] · a_src[h], · a_dst[h] for every head."""
+    dev = x.device
+    n, H = x.shape[0], spec.heads
+    s = torch.empty(H, n, dtype=torch.float32, device=dev)
+    t = torch.empty(H, n, dtype=torch.float32, device=dev)
+    nat.check(nat.load().gc_node_proj_f32(x.data_ptr(), _ld(x), n, width, H, head_stride,
+                                          a_src.data_ptr(), a_dst.data_ptr(), s.data_ptr(),
+                                          t.data_ptr(), _stream(dev)), "node_proj")
+    return s, t
+
+
+def _folded_attention_vectors(spec: GatLayerSpec) -> tuple[torch.Tensor, torch.Tensor]:
+    """u_h = W_h a_src_h, v_h = W_h a_dst_h (k1-vectors, heads concatenated),
+    cached on the spec; exact-fp32 GEMVs through the library."""
+    w = spec.weights
+    key = (w.data_ptr(), w._version, spec.attn_src.data_ptr(), spec.attn_src._version,
+           spec.attn_dst.data_ptr(), spec.attn_dst._version)
+    cache = getattr(spec, "_uv_cache", None)
+    if cache is not None and cache[0] == key:
+        return cache[1], cache[2]
+    k1, k2, H = spec.k1, spec.k2, spec.heads
+    u = torch.empty(H * k1, dtype=torch.float32, device=w.device)
+    v = torch.empty(H * k1, dtype=torch.float32, device=w.device)
+    for i in range(H):
+        wi = w[:, i * k2:(i + 1) * k2]
+        ab = torch.stack([spec.attn_src[i * k2:(i + 1) * k2], spec.attn_dst[i * k2:(i + 1) * k2]], 1)
+        uv = gemm(wi, ab.contiguous(), precision="fp32")
+        u[i * k1:(i + 1) * k1] = uv[:, 0]
+        v[i * k1:(i + 1) * k1] = uv[:, 1]
+    spec._uv_cache = (key, u, v)
+    return u, v
 
 
 def _check_h(a_tilde: CsrMatrix, h, spec: GatLayerSpec) -> None:
@@ -160,32 +212,53 @@ def gat_layer_reuse(a_tilde: CsrMatrix, h, spec: GatLayerSpec, *, spmm_fn=None):
     op = _Operand(h, a_tilde.device)
     relu = spec.activation == "relu"
     hw = gemm(op.t, spec.weights)
-    att = atten_calc(a_tilde, hw, spec)
-    k2 = spec.k2
+    k2, H = spec.k2, spec.heads
     if spmm_fn is not None:
-        outs = [spmm_fn(att.head(i), hw[:, i * k2:(i + 1) * k2]) for i in range(spec.heads)]
+        att = atten_calc(a_tilde, hw, spec)
+        outs = [spmm_fn(att.head(i), hw[:, i * k2:(i + 1) * k2]) for i in range(H)]
         out = torch.cat([torch.as_tensor(o, device=hw.device).float() for o in outs], 1).contiguous()
         return op.wrap(relu_(out) if relu else out)
-    out = torch.empty(a_tilde.n_rows, k2 * spec.heads, dtype=torch.float32, device=hw.device)
-    for i in range(spec.heads):
-        spmm(att.head(i), hw[:, i * k2:(i + 1) * k2], relu=relu, out=out[:, i * k2:(i + 1) * k2])
+    out = torch.empty(a_tilde.n_rows, k2 * H, dtype=torch.float32, device=hw.device)
+    if spec.attention is AttentionForm.SDDMM:
+        att = atten_calc(a_tilde, hw, spec)
+        for i in range(H):
+            spmm(att.head(i), hw[:, i * k2:(i + 1) * k2], relu=relu, out=out[:, i * k2:(i + 1) * k2])
+        return op.wrap(out)
+    if a_tilde.n_rows != a_tilde.n_cols:
+        raise ShapeError("attention expects a square adjacency")
+    s, t = _projections(hw, spec, spec.attn_src.to(hw.device), spec.attn_dst.to(hw.device), k2, k2)
+    for i in range(H):
+        gat_aggregate(a_tilde, s[i], t[i], spec.leaky_slope, hw[:, i * k2:(i + 1) * k2], relu=relu,
+                      out=out[:, i * k2:(i + 1) * k2])
     return op.wrap(out)
 
 
 def gat_layer_recompute(a_tilde: CsrMatrix, h, spec: GatLayerSpec, *, spmm_fn=None):
     """Aggregate the raw H (SpMM at k1) then update with one more GEMM —
-    gat.py:132-145.  HW is still computed once for the attention."""
+    gat.py:132-145.  In the reassociated form the scores come from H and the
+    folded vectors W a (no HW GEMM); the "sddmm" form needs HW for its
+    per-edge dot products, as the reference's recompute does."""
     _check_h(a_tilde, h, spec)
     op = _Operand(h, a_tilde.device)
     relu = spec.activation == "relu"
-    hw = gemm(op.t, spec.weights)
-    att = atten_calc(a_tilde, hw, spec)
-    k2 = spec.k2
-    out = torch.empty(a_tilde.n_rows, k2 * spec.heads, dtype=torch.float32, device=hw.device)
-    agg = spmm_fn if spmm_fn is not None else spmm
-    for i in range(spec.heads):
-        ah = agg(att.head(i), op.t)
-        ah = ah if isinstance(ah, torch.Tensor) else torch.as_tensor(ah, device=hw.device).float()
+    k1, k2, H = spec.k1, spec.k2, spec.heads
+    dev = op.t.device
+    out = torch.empty(a_tilde.n_rows, k2 * H, dtype=torch.float32, device=dev)
+    if spmm_fn is not None or spec.attention is AttentionForm.SDDMM:
+        hw = gemm(op.t, spec.weights)
+        att = atten_calc(a_tilde, hw, spec)
+        agg = spmm_fn if spmm_fn is not None else spmm
+        for i in range(H):
+            ah = agg(att.head(i), op.t)
+            ah = ah if isinstance(ah, torch.Tensor) else torch.as_tensor(ah, device=dev).float()
+            gemm(ah, spec.weights[:, i * k2:(i + 1) * k2], relu=relu, out=out[:, i * k2:(i + 1) * k2])
+        return op.wrap(out)
+    if a_tilde.n_rows != a_tilde.n_cols:
+        raise ShapeError("attention expects a square adjacency")
+    u, v = _folded_attention_vectors(spec)
+    s, t = _projections(op.t, spec, u, v, k1, 0)
+    for i in range(H):
+        ah = gat_aggregate(a_tilde, s[i], t[i], spec.leaky_slope, op.t)
         gemm(ah, spec.weights[:, i * k2:(i + 1) * k2], relu=relu, out=out[:, i * k2:(i + 1) * k2])
     return op.wrap(out)
 

@@ -369,6 +369,23 @@ class CsrMatrix:
                                 torch.from_numpy(split[: int(nsr[0])]).to(self.device), int(ns[0]))
         return self._plans[key]
 
+    def hub_tagged_cols(self, K: int, budget_bytes: int | None = None) -> torch.Tensor:
+        """col_idx with the most-referenced columns tagged in bit 31, sized so
+        the tagged rows of a K-wide operand fit one SM's L1 (cached)."""
+        budget = budget_bytes or HUB_L1_BUDGET
+        n_hot = max(1, min(self.n_cols, budget // (4 * max(K, 1))))
+        key = ("hub", n_hot)
+        if key not in self._plans:
+            counts = torch.bincount(self.col_idx.long(), minlength=self.n_cols)
+            hot = torch.zeros(self.n_cols, dtype=torch.uint8, device=self.device)
+            hot[torch.topk(counts, n_hot).indices] = 1
+            tagged = torch.empty_like(self.col_idx)
+            nat.check(nat.load().gc_tag_hub_columns(self.col_idx.data_ptr(), self.nnz, hot.data_ptr(),
+                                                    tagged.data_ptr(), _stream(self.device)),
+                      "tag_hub_columns")
+            self._plans[key] = tagged
+        return self._plans[key]
+
     def __repr__(self):
         return f"CsrMatrix({self.n_rows}x{self.n_cols}, nnz={self.nnz}, device={self.device})"
 
@@ -391,10 +408,27 @@ def _as_values(x, dev) -> torch.Tensor:
 
 SPLIT_CHUNK = int(os.environ.get("GNNC_SPLIT_CHUNK", "0"))  # 0: per-launch default
 PLAN_MIN_NNZ = 1 << 16  # below this a row-per-group launch needs no plan
+HUB_HINTS = os.environ.get("GNNC_HUB_HINTS", "0") == "1"  # L1 policy tags on hub columns
+HUB_L1_BUDGET = int(os.environ.get("GNNC_HUB_L1_BUDGET", str(160 * 1024)))
 
 
 def _sm_count(dev: torch.device) -> int:
     return torch.cuda.get_device_properties(dev).multi_processor_count
+
+
+def _plan_args(a: CsrMatrix, K: int, algo: str, dev, gat: bool = False):
+    """(code, items, n_items, split, n_split, workspace) for one launch."""
+    chunk = SPLIT_CHUNK or int(nat.load().gc_spmm_default_chunk(a.n_rows, a.nnz, K, _sm_count(dev)))
+    use_split = algo == "split" or (algo == "auto" and a.nnz and (
+        a.nnz >= PLAN_MIN_NNZ or a.max_degree() > chunk))
+    if not use_split:
+        return nat.GC_SPMM_ROW, None, 0, None, 0, None
+    items, split, n_slots = a.spmm_plan(chunk)
+    ws = None
+    if n_slots:
+        per_slot = K + (2 if gat else 0)  # partial row (+ (max, sum) pair for GAT)
+        ws = torch.empty(n_slots * per_slot + (2 if gat else 0), dtype=torch.float32, device=dev)
+    return nat.GC_SPMM_NNZ_SPLIT, items, items.shape[0], split, split.shape[0], ws
 
 
 def _spmm(a: CsrMatrix, b, *, weighted: bool, d_row=None, d_col=None, relu=False, out=None,
@@ -416,25 +450,51 @@ def _spmm(a: CsrMatrix, b, *, weighted: bool, d_row=None, d_col=None, relu=False
         if d is not None and tuple(d.shape) != (n,):
             raise ShapeError(f"{what}: {nm} must have {n} entries")
     flags = (nat.GC_RELU if relu else 0) | (nat.GC_ACCUMULATE if accumulate else 0)
-    chunk = SPLIT_CHUNK or int(nat.load().gc_spmm_default_chunk(a.n_rows, a.nnz, K, _sm_count(dev)))
-    use_split = algo == "split" or (algo == "auto" and a.nnz and (
-        a.nnz >= PLAN_MIN_NNZ or a.max_degree() > chunk))
-    items = split = ws = None
-    n_items = n_split = 0
-    code = nat.GC_SPMM_ROW
-    if use_split:
-        items, split, n_slots = a.spmm_plan(chunk)
-        n_items, n_split = items.shape[0], split.shape[0]
-        code = nat.GC_SPMM_NNZ_SPLIT
-        if n_slots:
-            ws = torch.empty(n_slots * K, dtype=torch.float32, device=dev)
+    code, items, n_items, split, n_split, ws = _plan_args(a, K, algo, dev)
+    cols = a.col_idx
+    if HUB_HINTS and a.nnz >= PLAN_MIN_NNZ:
+        cols = a.hub_tagged_cols(K)
+        flags |= nat.GC_HUB_TAGGED
     lib = nat.load()
     rc = _timed_call("spmm", dev, lambda: lib.gc_spmm_f32(
-        a.row_ptr.data_ptr(), a.col_idx.data_ptr(), a.values.data_ptr() if weighted else None,
+        a.row_ptr.data_ptr(), cols.data_ptr(), a.values.data_ptr() if weighted else None,
         _ptr(d_row), _ptr(d_col), bt.data_ptr(), _ld(bt), a.n_rows, a.n_cols, K, out.data_ptr(),
         _ld(out), flags, code, _ptr(items), n_items, _ptr(split), n_split, _ptr(ws),
         0 if ws is None else ws.numel() * 4, _stream(dev)))
     nat.check(rc, what)
+    return op.wrap(out)
+
+
+def gat_aggregate(a: CsrMatrix, s: torch.Tensor, t: torch.Tensor, slope: float, b, *,
+                  relu: bool = False, out=None, algo: str = "auto"):
+    """Fused GAT aggregation: C = epi(softmax_row(LeakyReLU(s_i + t_j)) B) with
+    the softmax computed online inside the SpMM (α never written) —
+    gat.py:72-95 followed by spmm(α, B) (gat.py:127-143) in one kernel."""
+    dev = a.device
+    op = _Operand(b, dev)
+    bt = op.t
+    if a.n_cols != bt.shape[0]:
+        raise ShapeError(f"gat_aggregate: a is {a.n_rows}x{a.n_cols}, b has {bt.shape[0]} rows")
+    if tuple(s.shape) != (a.n_rows,) or tuple(t.shape) != (a.n_cols,):
+        raise ShapeError("gat_aggregate: s/t must have one entry per row/column")
+    K = bt.shape[1]
+    _require_cuda(a.col_idx, bt, s, t)
+    if out is None:
+        out = torch.empty(a.n_rows, K, dtype=torch.float32, device=dev)
+    elif tuple(out.shape) != (a.n_rows, K) or out.stride(1) != 1:
+        raise ShapeError(f"gat_aggregate: out must be a row-major {a.n_rows}x{K} tensor")
+    code, items, n_items, split, n_split, ws = _plan_args(a, K, algo, dev, gat=True)
+    cols, flags = a.col_idx, nat.GC_RELU if relu else 0
+    if HUB_HINTS and a.nnz >= PLAN_MIN_NNZ:
+        cols = a.hub_tagged_cols(K)
+        flags |= nat.GC_HUB_TAGGED
+    lib = nat.load()
+    rc = _timed_call("spmm", dev, lambda: lib.gc_gat_aggregate_f32(
+        a.row_ptr.data_ptr(), cols.data_ptr(), s.data_ptr(), t.data_ptr(), float(slope),
+        bt.data_ptr(), _ld(bt), a.n_rows, a.n_cols, K, out.data_ptr(), _ld(out),
+        flags, code, _ptr(items), n_items, _ptr(split), n_split, _ptr(ws),
+        0 if ws is None else ws.numel() * 4, _stream(dev)))
+    nat.check(rc, "gat_aggregate")
     return op.wrap(out)
 
 

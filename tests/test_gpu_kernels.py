@@ -352,3 +352,55 @@ def test_spmm_fn_hook_is_used(golden):
         out = gc.gcn_layer(g, h, gc.GcnLayerSpec(5, 5, w, composition=comp), spmm_fn=my_spmm)
         assert _rel(out, golden[f"{key}/gcn/{comp}/heuristic"]) <= 1e-2
     assert len(calls) == 2
+
+
+@pytest.mark.parametrize("K", [1, 7, 32, 64, 256])
+@pytest.mark.parametrize("algo", ["row", "split"])
+def test_fused_gat_aggregate_matches_oracle(oracle, plgraph, K, algo, monkeypatch):
+    """gc_gat_aggregate_f32 == edge softmax (gat.py:72-95) then spmm(alpha, B)."""
+    if algo == "split":
+        monkeypatch.setattr(sparse, "SPLIT_CHUNK", 16)
+    rng = np.random.default_rng(K + 100)
+    n = plgraph.n_rows
+    s = f32(rng.standard_normal(n) * 3)
+    t = f32(rng.standard_normal(n) * 3)
+    b = f32(rng.standard_normal((n, K)))
+    dev = lambda x: torch.from_numpy(x).to(DEV)  # noqa: E731
+    for relu, slope in ((False, 0.2), (True, 0.05)):
+        out = sparse.gat_aggregate(plgraph, dev(s), dev(t), slope, dev(b), relu=relu,
+                                   algo=algo).cpu().numpy()
+        oa = to_oracle(oracle, plgraph)
+        alpha = oracle.edge_softmax(oa, s, t, slope)
+        ref = oracle.spmm(oa.with_values(alpha), b)
+        if relu:
+            ref = np.maximum(ref, 0)
+        assert oracle.rel_err(out, ref) < 2e-5, (K, algo, relu)
+
+
+def test_fused_gat_aggregate_empty_rows(oracle):
+    rng = np.random.default_rng(7)
+    a = rand_csr(rng, 60, 60, 0.1, unit=True, empty_rows=(0, 13, 59))
+    s, t = f32(rng.standard_normal(60)), f32(rng.standard_normal(60))
+    b = f32(rng.standard_normal((60, 8)))
+    out = sparse.gat_aggregate(a, torch.from_numpy(s).to(DEV), torch.from_numpy(t).to(DEV), 0.2,
+                               torch.from_numpy(b).to(DEV)).cpu().numpy()
+    assert np.all(out[[0, 13, 59]] == 0) and np.isfinite(out).all()
+    oa = to_oracle(oracle, a)
+    ref = oracle.spmm(oa.with_values(oracle.edge_softmax(oa, s, t, 0.2)), b)
+    assert oracle.rel_err(out, ref) < 2e-5
+
+
+@pytest.mark.parametrize("comp", ["precompute", "dynamic"])
+@pytest.mark.parametrize("order", ["aggregate_first", "update_first"])
+def test_host_pipelined_layer_matches_device_path(plgraph, comp, order):
+    """Pinned host H in -> pinned host out (row-blocked, D2H overlapped) must
+    equal the device-resident path."""
+    rng = np.random.default_rng(21)
+    g = gc.NormalizedGraph(plgraph, gc.inv_sqrt_degrees(plgraph)).with_precomputed()
+    h = torch.from_numpy(f32(rng.uniform(-0.5, 0.5, (plgraph.n_rows, 48)))).pin_memory()
+    spec = gc.GcnLayerSpec(48, 40, f32(rng.uniform(-0.5, 0.5, (48, 40))), composition=comp,
+                           order=order)
+    out = gc.gcn_layer(g, h, spec)
+    assert not out.is_cuda and out.is_pinned()
+    ref = gc.gcn_layer(g, h.to(DEV), spec).cpu()
+    assert torch.allclose(out, ref, rtol=1e-5, atol=1e-6)
