@@ -60,6 +60,8 @@ def parse():
     p.add_argument("--no-extra", action="store_true",
                    help="skip the GAT-on-arxiv and products configs (BASELINE configs[2], [3])")
     p.add_argument("--backend", default="nccl", help="process-group backend for N > 1")
+    p.add_argument("--no-overlap", action="store_true",
+                   help="N > 1: all-gather, then SpMM (default: owned-column edges overlap the gather)")
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--out", default=None, help="also write the JSON line to this file")
     return p.parse_args()
@@ -293,7 +295,7 @@ def main():
 
         def step():
             return dist_gcn_layer(part, h_dev, spec.weights, composition=base, order=order,
-                                  d=d_full)
+                                  d=d_full, overlap=not args.no_overlap)
     else:
         h_dev = torch.from_numpy(h_host32).to(dev)
 
@@ -359,7 +361,9 @@ def main():
                    "nnz_A": shape.nnz, "m_tilde": m, "K": K, "composition": comp,
                    "selected_by": selected_by, "gemm_precision": gc.get_gemm_precision(),
                    "l2": "inputs larger than L2 (CSR 0.9 GB, H 0.24 GB at K=256); no flush",
-                   "parallelism": f"row-partition x{world}" if world > 1 else "single GPU"},
+                   "parallelism": (f"row-partition x{world}, 1 all-gather/layer"
+                                   f"{'' if args.no_overlap else ' overlapped with the owned-column SpMM'}")
+                   if world > 1 else "single GPU"},
         "gpu_launches": int(launches),
         "kernel_ms": {"spmm": spmm_ms, "gemm": gemm_ms},
         "roofline": roof,

@@ -15,6 +15,13 @@ all-gather assembles the operand the local SpMM gathers:
 Output rows stay partitioned and feed the next layer.  Blocks are padded to
 the largest block for ``all_gather_into_tensor``.
 
+Overlap (``overlap=True``): the local block of the
+pattern is split by column into the edges whose source row this rank owns
+(aggregated straight from its own operand block, while the all-gather is in
+flight) and the remote edges (column ids remapped into the padded gather
+buffer, so no unpad copy).  The remote pass accumulates into the local one
+(``out += d_i * acc``; ReLU on the total).
+
 The compute ops are injectable (``ops``) so the host logic — partition,
 padding, gather, unpad, assembly — is testable on CPU with gloo and the
 oracle standing in for the CUDA kernels.
@@ -71,16 +78,50 @@ class RowPartition:
         b = partition_rows(a.row_ptr, world)
         return cls(rank, world, b, a.take_rows(int(b[rank]), int(b[rank + 1])))
 
+    def split_local_remote(self) -> tuple[CsrMatrix, CsrMatrix]:
+        """(edges from owned rows, columns rebased to the local block;
+        remaining edges, columns remapped into the padded gather buffer)."""
+        if getattr(self, "_lr", None) is None:
+            a = self.local
+            col = a.col_idx.long()
+            rows = a.row_of_nnz()
+            own = (col >= self.lo) & (col < self.hi)
+            bounds = torch.as_tensor(self.bounds, device=col.device)
+            owner = torch.searchsorted(bounds[1:], col, right=True)
+            padded = owner * self.max_rows + (col - bounds[owner])
+
+            def sub(mask, cols, n_cols):
+                cnt = torch.bincount(rows[mask], minlength=a.n_rows)
+                rp = torch.cat([cnt.new_zeros(1), torch.cumsum(cnt, 0)])
+                return CsrMatrix(a.n_rows, n_cols, rp, cols[mask], a.values[mask], validate=False,
+                                 device=a.device)
+
+            loc = sub(own, col - self.lo, max(self.rows, 1))
+            rem = sub(~own, padded, self.world * self.max_rows)
+            loc._unit = rem._unit = a._unit
+            self._lr = (loc, rem)
+        return self._lr
+
+
+def all_gather_padded(x_local: torch.Tensor, part: RowPartition, group=None, async_op=False):
+    """Padded all-gather: returns (buffer of world*max_rows rows, work handle)."""
+    k = x_local.shape[1]
+    pad = part.max_rows
+    if x_local.shape[0] == pad:
+        buf = x_local.contiguous()
+    else:
+        buf = torch.zeros(pad, k, dtype=x_local.dtype, device=x_local.device)
+        buf[: x_local.shape[0]] = x_local
+    full = torch.empty(part.world * pad, k, dtype=x_local.dtype, device=x_local.device)
+    work = dist.all_gather_into_tensor(full, buf, group=group, async_op=async_op)
+    return full, work
+
 
 def all_gather_rows(x_local: torch.Tensor, part: RowPartition, group=None) -> torch.Tensor:
     """Assemble the full n x k operand from every rank's row block (padded
     all_gather_into_tensor, then the padding is dropped)."""
-    k = x_local.shape[1]
     pad = part.max_rows
-    buf = torch.zeros(pad, k, dtype=x_local.dtype, device=x_local.device)
-    buf[: x_local.shape[0]] = x_local
-    full = torch.empty(part.world * pad, k, dtype=x_local.dtype, device=x_local.device)
-    dist.all_gather_into_tensor(full, buf, group=group)
+    full, _ = all_gather_padded(x_local, part, group)
     if all(int(part.bounds[p + 1] - part.bounds[p]) == pad for p in range(part.world)):
         return full
     pieces = [full[p * pad: p * pad + int(part.bounds[p + 1] - part.bounds[p])]
@@ -98,16 +139,17 @@ class CudaOps:
         return gemm(a, w, row_scale=row_scale, relu=relu)
 
     @staticmethod
-    def spmm(a: CsrMatrix, b, d_row=None, d_col=None, relu=False, weighted=True):
+    def spmm(a: CsrMatrix, b, d_row=None, d_col=None, relu=False, weighted=True, out=None,
+             accumulate=False):
         from .sparse import spmm, spmm_unweighted
 
         f = spmm if weighted else spmm_unweighted
-        return f(a, b, d_row=d_row, d_col=d_col, relu=relu)
+        return f(a, b, d_row=d_row, d_col=d_col, relu=relu, out=out, accumulate=accumulate)
 
 
 def dist_gcn_layer(part: RowPartition, h_local: torch.Tensor, w: torch.Tensor, *,
                    composition: str, order: str, d: torch.Tensor | None = None,
-                   ops=CudaOps, group=None) -> torch.Tensor:
+                   ops=CudaOps, group=None, overlap: bool = False) -> torch.Tensor:
     """One GCN layer on this rank's rows.  ``part.local`` is Ñ's block for
     precompute or Ã's block for dynamic; ``d`` is the FULL D^-1/2 vector
     (needed for dynamic).  Returns this rank's output rows."""
@@ -116,6 +158,23 @@ def dist_gcn_layer(part: RowPartition, h_local: torch.Tensor, w: torch.Tensor, *
         raise ValueError("dynamic composition needs the degree vector")
     d_loc = d[part.lo:part.hi] if dyn else None
     weighted = not (dyn and part.local.has_unit_values)
+    if overlap:
+        loc, rem = part.split_local_remote()
+        d_pad = None
+        if dyn:
+            d_pad = torch.zeros(part.world * part.max_rows, dtype=d.dtype, device=d.device)
+            for p in range(part.world):
+                lo, hi = int(part.bounds[p]), int(part.bounds[p + 1])
+                d_pad[p * part.max_rows: p * part.max_rows + hi - lo] = d[lo:hi]
+        src = ops.gemm(h_local, w) if order == "update_first" else h_local
+        full, work = all_gather_padded(src, part, group, async_op=True)
+        # owned-column edges while the gather is in flight
+        y = ops.spmm(loc, src, d_row=d_loc, d_col=d_loc, relu=False, weighted=weighted)
+        work.wait()
+        last = order == "update_first"
+        y = ops.spmm(rem, full, d_row=d_loc, d_col=d_pad, relu=last, weighted=weighted, out=y,
+                     accumulate=True)
+        return y if last else ops.gemm(y, w, relu=True)
     if order == "update_first":
         hw_loc = ops.gemm(h_local, w)
         hw = all_gather_rows(hw_loc, part, group)

@@ -37,7 +37,7 @@ class OracleOps:
         return torch.from_numpy(out)
 
     @staticmethod
-    def spmm(a, b, d_row=None, d_col=None, relu=False, weighted=True):
+    def spmm(a, b, d_row=None, d_col=None, relu=False, weighted=True, out=None, accumulate=False):
         from oracle import gnn_oracle as orc
 
         rp, ci, v = a.numpy()
@@ -45,15 +45,17 @@ class OracleOps:
         bb = b.double().numpy()
         if d_col is not None:
             bb = orc.scale_rows(d_col.double().numpy(), bb)
-        out = orc.spmm(oa, bb) if weighted else orc.spmm_unweighted(oa, bb)
+        res = orc.spmm(oa, bb) if weighted else orc.spmm_unweighted(oa, bb)
         if d_row is not None:
-            out = orc.scale_rows(d_row.double().numpy(), out)
+            res = orc.scale_rows(d_row.double().numpy(), res)
+        if accumulate:
+            res = res + out.double().numpy()
         if relu:
-            out = np.maximum(out, 0)
-        return torch.from_numpy(out)
+            res = np.maximum(res, 0)
+        return torch.from_numpy(res)
 
 
-def _worker(rank, world, port, comp, order, q):
+def _worker(rank, world, port, comp, order, q, overlap=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -81,7 +83,7 @@ def _worker(rank, world, port, comp, order, q):
             base = at
         part = RowPartition.of(base, rank, world)
         out = dist_gcn_layer(part, h[part.lo:part.hi], w, composition=comp, order=order,
-                             d=d, ops=OracleOps)
+                             d=d, ops=OracleOps, overlap=overlap)
         full = all_gather_rows(out, part)
         if rank == 0:
             q.put((part.bounds.tolist(), full.numpy()))
@@ -89,15 +91,16 @@ def _worker(rank, world, port, comp, order, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world,overlap", [(2, False), (3, False), (2, True), (3, True)])
 @pytest.mark.parametrize("comp,order", [("dynamic", "aggregate_first"), ("dynamic", "update_first"),
                                         ("precompute", "aggregate_first"),
                                         ("precompute", "update_first")])
-def test_partitioned_layer_matches_single_process(oracle, world, comp, order):
+def test_partitioned_layer_matches_single_process(oracle, world, overlap, comp, order):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, comp, order, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, comp, order, q, overlap))
+             for r in range(world)]
     for p in procs:
         p.start()
     bounds, full = q.get(timeout=240)
