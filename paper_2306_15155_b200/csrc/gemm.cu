@@ -125,7 +125,9 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 constexpr int BM = 128;             // UMMA_M (cta_group::1)
 constexpr int BK = 32;              // fp32 elements per 128-byte swizzle row
 constexpr int UMMA_K = 8;           // K per tcgen05.mma for kind::tf32
-constexpr int kGemmThreads = 128;   // 4 warps: TMA / MMA / TMEM-alloc roles, all do the epilogue
+// 6 warps: 0 = TMA producer (+ TMEM alloc), 1 = MMA issuer, 2..5 = epilogue.
+// Epilogue warp w reads TMEM lanes 32*(w%4) .. +31, so warps 2..5 cover all 128.
+constexpr int kGemmThreads = 192;
 
 struct GemmEpi {
   float *C;
@@ -135,42 +137,54 @@ struct GemmEpi {
   uint32_t flags;
 };
 
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+// Persistent warp-specialised TF32 GEMM.  Tiles (BM x BN) are walked
+// n-fastest (consecutive tiles of a CTA reuse the same A rows from L2); the
+// smem ring streams k-blocks across tile boundaries, and the accumulator is
+// double-buffered in TMEM (2 x BN columns) so the epilogue of tile i overlaps
+// the mainloop of tile i+1.
 template <int BN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tf32_tcgen05(const __grid_constant__ CUtensorMap map_a,
                       const __grid_constant__ CUtensorMap map_b, const GemmEpi ep, int num_kb,
-                      int stages) {
+                      int stages, int m_tiles, int n_tiles) {
   constexpr uint32_t A_BYTES = BM * BK * 4;
   constexpr uint32_t B_BYTES = BN * BK * 4;
   constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;  // power of two >= 32
+  constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // power of two >= 32
 
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;  // SWIZZLE_128B needs 1024-B alignment
   uint8_t *gbase = smem_raw + (base - raw);
-  const uint32_t bar0 = base + (uint32_t)stages * STAGE_BYTES;  // full[s], empty[s], accum
+  const uint32_t bar0 = base + (uint32_t)stages * STAGE_BYTES;
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
   auto empty_bar = [&](int s) { return bar0 + 8u * (stages + s); };
-  const uint32_t accum_bar = bar0 + 8u * (2 * stages);
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + (bar0 - base) + 8u * (2 * stages + 1));
+  auto tfull_bar = [&](int b) { return bar0 + 8u * (2 * stages + b); };
+  auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * stages + 2 + b); };
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + (bar0 - base) + 8u * (2 * stages + 4));
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const int m0 = blockIdx.x * BM;
-  const int n0 = blockIdx.y * BN;
+  const int n_tiles_total = m_tiles * n_tiles;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 1 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
     for (int s = 0; s < stages; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);
     }
-    mbar_init(accum_bar, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull_bar(b), 1);
+      mbar_init(tempty_bar(b), 4);  // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 2) {
+  if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
                  "n"(TMEM_COLS)
@@ -180,74 +194,95 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_d = *tmem_slot;
+  const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer ----------------
-    for (int kb = 0; kb < num_kb; ++kb) {
-      const int s = kb % stages;
-      if (kb >= stages) mbar_wait(empty_bar(s), ((kb / stages) & 1) ^ 1);
-      const uint32_t sa = base + (uint32_t)s * STAGE_BYTES;
-      mbar_expect_tx(full_bar(s), STAGE_BYTES);
-      tma_load_2d(sa, &map_a, full_bar(s), kb * BK, m0);
-      tma_load_2d(sa + A_BYTES, &map_b, full_bar(s), kb * BK, n0);
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer (single thread) ----------------
-    constexpr uint32_t idesc = idesc_tf32(BN);
-    for (int kb = 0; kb < num_kb; ++kb) {
-      const int s = kb % stages;
-      mbar_wait(full_bar(s), (kb / stages) & 1);
-      tc_fence_after();
-      const uint32_t sa = base + (uint32_t)s * STAGE_BYTES;
-#pragma unroll
-      for (int k = 0; k < BK / UMMA_K; ++k) {
-        const uint64_t ad = umma_desc_sw128(sa + k * UMMA_K * 4);
-        const uint64_t bd = umma_desc_sw128(sa + A_BYTES + k * UMMA_K * 4);
-        mma_tf32(tmem_d, ad, bd, idesc, (kb | k) != 0);
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer ----------------
+      int it = 0;
+      for (int tile = blockIdx.x; tile < n_tiles_total; tile += gridDim.x) {
+        const int m0 = (tile / n_tiles) * BM, n0 = (tile % n_tiles) * BN;
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int s = it % stages;
+          mbar_wait(empty_bar(s), ((it / stages) & 1) ^ 1);
+          const uint32_t sa = base + (uint32_t)s * STAGE_BYTES;
+          mbar_expect_tx(full_bar(s), STAGE_BYTES);
+          tma_load_2d(sa, &map_a, full_bar(s), kb * BK, m0);
+          tma_load_2d(sa + A_BYTES, &map_b, full_bar(s), kb * BK, n0);
+        }
       }
-      mma_commit(empty_bar(s));  // frees the smem slot once these MMAs retire
     }
-    mma_commit(accum_bar);  // accumulator complete
-  }
-  __syncwarp();
-
-  // ---------------- epilogue: TMEM -> registers -> global ----------------
-  mbar_wait(accum_bar, 0);
-  tc_fence_after();
-  const int row = m0 + warp * 32 + lane;  // TMEM lane == tile row
-  const bool row_ok = row < ep.M;
-  const float rs = (row_ok && ep.row_scale) ? __ldg(ep.row_scale + row) : 1.0f;
-  const bool relu = (ep.flags & GC_RELU) != 0;
-  const bool vec = ((ep.ldc & 3) == 0) && aligned16(ep.C);
-  float *crow = ep.C + (int64_t)row * ep.ldc;
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer (one thread) ----------------
+      constexpr uint32_t idesc = idesc_tf32(BN);
+      int it = 0, lt = 0;
+      for (int tile = blockIdx.x; tile < n_tiles_total; tile += gridDim.x, ++lt) {
+        const int acc = lt & 1;
+        mbar_wait(tempty_bar(acc), ((lt >> 1) & 1) ^ 1);  // epilogue drained this buffer
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int s = it % stages;
+          mbar_wait(full_bar(s), (it / stages) & 1);
+          tc_fence_after();
+          const uint32_t sa = base + (uint32_t)s * STAGE_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / UMMA_K; ++k) {
+            const uint64_t ad = umma_desc_sw128(sa + k * UMMA_K * 4);
+            const uint64_t bd = umma_desc_sw128(sa + A_BYTES + k * UMMA_K * 4);
+            mma_tf32(tmem_d, ad, bd, idesc, (kb | k) != 0);
+          }
+          mma_commit(empty_bar(s));  // frees the smem slot once these MMAs retire
+        }
+        mma_commit(tfull_bar(acc));  // accumulator of this tile complete
+      }
+    }
+  } else {  // ---------------- epilogue warps 2..5 ----------------
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const bool relu = (ep.flags & GC_RELU) != 0;
+    const bool vec = ((ep.ldc & 3) == 0) && aligned16(ep.C);
+    int lt = 0;
+    for (int tile = blockIdx.x; tile < n_tiles_total; tile += gridDim.x, ++lt) {
+      const int acc = lt & 1;
+      const int m0 = (tile / n_tiles) * BM, n0 = (tile % n_tiles) * BN;
+      mbar_wait(tfull_bar(acc), (lt >> 1) & 1);
+      tc_fence_after();
+      const int row = m0 + q * 32 + lane;
+      const bool row_ok = row < ep.M;
+      const float rs = (row_ok && ep.row_scale) ? __ldg(ep.row_scale + row) : 1.0f;
+      float *crow = ep.C + (int64_t)row * ep.ldc;
+      const uint32_t taddr = tmem_base + (uint32_t)(acc * BN) + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
-  for (int c = 0; c < BN; c += 16) {
-    if (n0 + c >= ep.N) break;  // warp-uniform
-    float v[16];
-    tmem_ld16(tmem_d + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, v);
+      for (int c = 0; c < BN; c += 16) {
+        if (n0 + c >= ep.N) break;  // warp-uniform
+        float v[16];
+        tmem_ld16(taddr + (uint32_t)c, v);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      v[i] *= rs;
-      if (relu) v[i] = fmaxf(v[i], 0.0f);
-    }
-    if (!row_ok) continue;
-    const int64_t col = n0 + c;
-    if (vec && col + 16 <= ep.N) {
+        for (int i = 0; i < 16; ++i) {
+          v[i] *= rs;
+          if (relu) v[i] = fmaxf(v[i], 0.0f);
+        }
+        if (!row_ok) continue;
+        const int64_t col = n0 + c;
+        if (vec && col + 16 <= ep.N) {
 #pragma unroll
-      for (int i = 0; i < 16; i += 4)
-        stg_f4(crow + col + i, make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
-    } else {
+          for (int i = 0; i < 16; i += 4)
+            stg_f4(crow + col + i, make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+        } else {
 #pragma unroll
-      for (int i = 0; i < 16; ++i)
-        if (col + i < ep.N) crow[col + i] = v[i];
+          for (int i = 0; i < 16; ++i)
+            if (col + i < ep.N) crow[col + i] = v[i];
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty_bar(acc));
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 0) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d),
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "n"(TMEM_COLS)
                  : "memory");
   }
@@ -399,8 +434,11 @@ template <int BN>
 int launch_tf32(const CUtensorMap &ma, const CUtensorMap &mb, const GemmEpi &ep, int64_t K,
                 cudaStream_t st) {
   const int num_kb = (int)((K + BK - 1) / BK);
-  const int stages = num_kb < 4 ? num_kb : 4;
-  const size_t smem = (size_t)stages * (BM * BK * 4 + BN * BK * 4) + 8 * (2 * stages + 1) + 16 + 1024;
+  constexpr int stage_bytes = BM * BK * 4 + BN * BK * 4;
+  // deepest ring that fits next to the barriers (<= 8 stages, <= ~200 KB)
+  int stages = (200 * 1024) / stage_bytes;
+  stages = stages > 8 ? 8 : (stages < 2 ? 2 : stages);
+  const size_t smem = (size_t)stages * stage_bytes + 8 * (2 * stages + 4) + 16 + 1024;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
@@ -411,8 +449,12 @@ int launch_tf32(const CUtensorMap &ma, const CUtensorMap &mb, const GemmEpi &ep,
     set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
     return GC_ERR_CUDA;
   }
-  dim3 grid((unsigned)((ep.M + BM - 1) / BM), (unsigned)((ep.N + BN - 1) / BN));
-  gemm_tf32_tcgen05<BN><<<grid, kGemmThreads, smem, st>>>(ma, mb, ep, num_kb, stages);
+  const int m_tiles = (int)((ep.M + BM - 1) / BM);
+  const int n_tiles = (int)((ep.N + BN - 1) / BN);
+  const int64_t tiles = (int64_t)m_tiles * n_tiles;
+  const int grid = (int)(tiles < sm_count() ? tiles : sm_count());  // persistent: one CTA per SM
+  gemm_tf32_tcgen05<BN><<<grid, kGemmThreads, smem, st>>>(ma, mb, ep, num_kb, stages, m_tiles,
+                                                          n_tiles);
   return check_launch("gemm_tf32_tcgen05");
 }
 
