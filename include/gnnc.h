@@ -141,7 +141,7 @@ GNNC_API int gc_sddmm_f32(const int32_t *row_ptr, const int32_t *col_idx, const 
  * out[p] = (a_vals ? a_vals[p] : 1) * (d[i] * d[col_idx[p]])
  * Replaces gcn.precompute_normalized (gcn.py:103-112). */
 GNNC_API int gc_sddmm_norm_f32(const int32_t *row_ptr, const int32_t *col_idx, const float *a_vals,
-                      const float *d, int64_t n_rows, float *out_vals, void *stream);
+                      const float *d, int64_t n_rows, int64_t nnz, float *out_vals, void *stream);
 
 /* ---- dense --------------------------------------------------------------
  * C = epi( diag(row_scale) * A * W ), A: M x K (lda), W: K x N (ldw),

@@ -52,7 +52,7 @@ _SIGNATURES = {
     "gc_spmm_plan_fill": (ctypes.c_int, [_P, _I64, _I32, _U32, _P, _P]),
     "gc_spmm_default_chunk": (ctypes.c_int32, [_I64, _I64, _I64, ctypes.c_int]),
     "gc_sddmm_f32": (ctypes.c_int, [_P, _P, _P, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _P]),
-    "gc_sddmm_norm_f32": (ctypes.c_int, [_P, _P, _P, _P, _I64, _P, _P]),
+    "gc_sddmm_norm_f32": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I64, _P, _P]),
     "gc_gemm_workspace_bytes": (_SZ, [_I64, _I64]),
     "gc_gemm_f32": (ctypes.c_int, [_P, _I64, _P, _I64, _I64, _I64, _I64, _P, _I64, _P, _U32, _P,
                                    _SZ, _P]),

@@ -261,16 +261,22 @@ extern "C" int gc_sddmm_f32(const int32_t *row_ptr, const int32_t *col_idx, cons
 }
 
 extern "C" int gc_sddmm_norm_f32(const int32_t *row_ptr, const int32_t *col_idx,
-                                 const float *a_vals, const float *d, int64_t n_rows,
+                                 const float *a_vals, const float *d, int64_t n_rows, int64_t nnz,
                                  float *out_vals, void *stream) {
-  GC_REQUIRE(n_rows >= 0, GC_ERR_SHAPE, "gc_sddmm_norm_f32: n_rows < 0");
+  GC_REQUIRE(n_rows >= 0 && nnz >= 0, GC_ERR_SHAPE, "gc_sddmm_norm_f32: negative size");
   if (n_rows == 0) return GC_OK;
   GC_REQUIRE(row_ptr && d, GC_ERR_VALUE, "gc_sddmm_norm_f32: null operand");
+  // lanes per row follow the mean degree: short rows share a warp, long rows
+  // get the whole warp (the per-edge d_j gather is latency-bound otherwise)
+  const bool wide = nnz > 12 * n_rows;
   unsigned grid;
-  int rc = rows_grid(n_rows, 8, &grid);
+  cudaStream_t st = as_stream(stream);
+  int rc = rows_grid(n_rows, wide ? 32 : 8, &grid);
   if (rc) return rc;
-  sddmm_norm_kernel<8><<<grid, kThreads, 0, as_stream(stream)>>>(row_ptr, col_idx, a_vals, d,
-                                                                 n_rows, out_vals);
+  if (wide)
+    sddmm_norm_kernel<32><<<grid, kThreads, 0, st>>>(row_ptr, col_idx, a_vals, d, n_rows, out_vals);
+  else
+    sddmm_norm_kernel<8><<<grid, kThreads, 0, st>>>(row_ptr, col_idx, a_vals, d, n_rows, out_vals);
   return check_launch("sddmm_norm_kernel");
 }
 

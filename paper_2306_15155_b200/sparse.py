@@ -408,7 +408,12 @@ def _as_values(x, dev) -> torch.Tensor:
 
 SPLIT_CHUNK = int(os.environ.get("GNNC_SPLIT_CHUNK", "0"))  # 0: per-launch default
 PLAN_MIN_NNZ = 1 << 16  # below this a row-per-group launch needs no plan
-HUB_HINTS = os.environ.get("GNNC_HUB_HINTS", "0") == "1"  # L1 policy tags on hub columns
+# L1 policy tags on hub columns: "0" off, "1" on, "auto" (default): measured
+# once per (pattern, K) on the first large launch and cached — the tags win on
+# graphs whose hubs fit L1 (arxiv-like) and lose where L2 reuse already
+# dominates (Reddit-like), see profiles/spmm_variants.py.
+HUB_HINTS = os.environ.get("GNNC_HUB_HINTS", "auto")
+HUB_AUTOTUNE_MIN_NNZ = 1 << 20
 HUB_L1_BUDGET = int(os.environ.get("GNNC_HUB_L1_BUDGET", str(160 * 1024)))
 
 
@@ -431,6 +436,35 @@ def _plan_args(a: CsrMatrix, K: int, algo: str, dev, gat: bool = False):
     return nat.GC_SPMM_NNZ_SPLIT, items, items.shape[0], split, split.shape[0], ws
 
 
+def _use_hints(a: CsrMatrix, K: int, launch) -> bool:
+    """Decide the hub-tag variant for (pattern, K); ``launch(cols, flag, out)``
+    runs the kernel into a scratch output.  "auto" times both variants once
+    (CUDA events, median of 3) and caches the faster."""
+    mode = HUB_HINTS if isinstance(HUB_HINTS, str) else ("1" if HUB_HINTS else "0")
+    if mode == "0" or a.nnz < PLAN_MIN_NNZ:
+        return False
+    if mode == "1":
+        return True
+    if a.nnz < HUB_AUTOTUNE_MIN_NNZ:
+        return False
+    key = ("hint-choice", int(K))
+    if key not in a._plans:
+        tagged = a.hub_tagged_cols(K)
+        times = {}
+        for variant, cols, flag in ((False, a.col_idx, 0), (True, tagged, nat.GC_HUB_TAGGED)):
+            launch(cols, flag)  # warm
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(3)]
+            for e0, e1 in ev:
+                e0.record()
+                launch(cols, flag)
+                e1.record()
+            torch.cuda.synchronize()
+            times[variant] = sorted(e0.elapsed_time(e1) for e0, e1 in ev)[1]
+        a._plans[key] = times[True] < 0.97 * times[False]
+    return a._plans[key]
+
+
 def _spmm(a: CsrMatrix, b, *, weighted: bool, d_row=None, d_col=None, relu=False, out=None,
           accumulate=False, algo: str = "auto", what="spmm"):
     dev = a.device
@@ -451,16 +485,26 @@ def _spmm(a: CsrMatrix, b, *, weighted: bool, d_row=None, d_col=None, relu=False
             raise ShapeError(f"{what}: {nm} must have {n} entries")
     flags = (nat.GC_RELU if relu else 0) | (nat.GC_ACCUMULATE if accumulate else 0)
     code, items, n_items, split, n_split, ws = _plan_args(a, K, algo, dev)
-    cols = a.col_idx
-    if HUB_HINTS and a.nnz >= PLAN_MIN_NNZ:
-        cols = a.hub_tagged_cols(K)
-        flags |= nat.GC_HUB_TAGGED
     lib = nat.load()
-    rc = _timed_call("spmm", dev, lambda: lib.gc_spmm_f32(
-        a.row_ptr.data_ptr(), cols.data_ptr(), a.values.data_ptr() if weighted else None,
-        _ptr(d_row), _ptr(d_col), bt.data_ptr(), _ld(bt), a.n_rows, a.n_cols, K, out.data_ptr(),
-        _ld(out), flags, code, _ptr(items), n_items, _ptr(split), n_split, _ptr(ws),
-        0 if ws is None else ws.numel() * 4, _stream(dev)))
+
+    def launch(cols, extra, dst=out, fl=flags):
+        return lib.gc_spmm_f32(
+            a.row_ptr.data_ptr(), cols.data_ptr(), a.values.data_ptr() if weighted else None,
+            _ptr(d_row), _ptr(d_col), bt.data_ptr(), _ld(bt), a.n_rows, a.n_cols, K, dst.data_ptr(),
+            _ld(dst), fl | extra, code, _ptr(items), n_items, _ptr(split), n_split, _ptr(ws),
+            0 if ws is None else ws.numel() * 4, _stream(dev))
+
+    scratch = None
+
+    def probe(cols, extra):
+        nonlocal scratch
+        if scratch is None:
+            scratch = torch.empty(a.n_rows, K, dtype=torch.float32, device=dev)
+        nat.check(launch(cols, extra, scratch, flags & ~nat.GC_ACCUMULATE), what)
+
+    hints = _use_hints(a, K, probe)
+    cols = a.hub_tagged_cols(K) if hints else a.col_idx
+    rc = _timed_call("spmm", dev, lambda: launch(cols, nat.GC_HUB_TAGGED if hints else 0))
     nat.check(rc, what)
     return op.wrap(out)
 
@@ -484,16 +528,22 @@ def gat_aggregate(a: CsrMatrix, s: torch.Tensor, t: torch.Tensor, slope: float, 
     elif tuple(out.shape) != (a.n_rows, K) or out.stride(1) != 1:
         raise ShapeError(f"gat_aggregate: out must be a row-major {a.n_rows}x{K} tensor")
     code, items, n_items, split, n_split, ws = _plan_args(a, K, algo, dev, gat=True)
-    cols, flags = a.col_idx, nat.GC_RELU if relu else 0
-    if HUB_HINTS and a.nnz >= PLAN_MIN_NNZ:
-        cols = a.hub_tagged_cols(K)
-        flags |= nat.GC_HUB_TAGGED
     lib = nat.load()
-    rc = _timed_call("spmm", dev, lambda: lib.gc_gat_aggregate_f32(
-        a.row_ptr.data_ptr(), cols.data_ptr(), s.data_ptr(), t.data_ptr(), float(slope),
-        bt.data_ptr(), _ld(bt), a.n_rows, a.n_cols, K, out.data_ptr(), _ld(out),
-        flags, code, _ptr(items), n_items, _ptr(split), n_split, _ptr(ws),
-        0 if ws is None else ws.numel() * 4, _stream(dev)))
+    flags = nat.GC_RELU if relu else 0
+
+    def launch(cols, extra, dst=out):
+        return lib.gc_gat_aggregate_f32(
+            a.row_ptr.data_ptr(), cols.data_ptr(), s.data_ptr(), t.data_ptr(), float(slope),
+            bt.data_ptr(), _ld(bt), a.n_rows, a.n_cols, K, dst.data_ptr(), _ld(dst), flags | extra,
+            code, _ptr(items), n_items, _ptr(split), n_split, _ptr(ws),
+            0 if ws is None else ws.numel() * 4, _stream(dev))
+
+    def probe(cols, extra):
+        nat.check(launch(cols, extra), "gat_aggregate")  # writes `out`; the real launch follows
+
+    hints = _use_hints(a, K, probe)
+    cols = a.hub_tagged_cols(K) if hints else a.col_idx
+    rc = _timed_call("spmm", dev, lambda: launch(cols, nat.GC_HUB_TAGGED if hints else 0))
     nat.check(rc, "gat_aggregate")
     return op.wrap(out)
 
@@ -548,7 +598,7 @@ def sddmm_norm(a: CsrMatrix, d: torch.Tensor, *, weighted: bool = True) -> CsrMa
     if a.nnz:
         nat.check(nat.load().gc_sddmm_norm_f32(a.row_ptr.data_ptr(), a.col_idx.data_ptr(),
                                                a.values.data_ptr() if weighted else None,
-                                               d.data_ptr(), a.n_rows, out.data_ptr(),
+                                               d.data_ptr(), a.n_rows, a.nnz, out.data_ptr(),
                                                _stream(dev)), "sddmm_norm")
     return a.with_values(out)
 

@@ -49,10 +49,10 @@ def main():
             h = torch.rand(n, K, device=dev) - 0.5
             row = {"shape": shape, "K": K, "m": m}
             for hints in (False, True):
-                sparse.HUB_HINTS = hints
+                sparse.HUB_HINTS = "1" if hints else "0"
                 ms = timed(lambda: gc.spmm_unweighted(at, h, d_row=d, d_col=d))
                 row["hints" if hints else "plain"] = ms
-            sparse.HUB_HINTS = False
+            sparse.HUB_HINTS = "auto"
             row["gain"] = row["plain"] / row["hints"]
             out["spmm"].append(row)
             print(json.dumps(row), file=sys.stderr, flush=True)
