@@ -169,28 +169,40 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
   // zl sums this lane's own edge weights relative to m.
   const float si = (GAT && live) ? __ldg(a.s + row) : 0.0f;
   float m = -INFINITY, zl = 0.0f;
-  // software pipeline: the (col, value) batch for the next LPR edges is in
-  // flight while the B rows of the current batch are gathered.
-  int jn = 0;
-  float vn = 1.0f;
+  // Two-deep software pipeline over batches of LPR edges: while batch i's rows
+  // of B are gathered, batch i+1's per-node gather (d_j or t_j) and batch
+  // i+2's (col, value) loads are already in flight.
+  constexpr bool NEEDG = HAS_DCOL || GAT;
+  int j1 = 0, j2 = 0;
+  float v1 = 1.0f, v2 = 1.0f, g1 = 0.0f;
   if (gl < len) {
-    jn = ldg_stream_i32(a.col_idx + beg + gl);
-    if (HAS_VAL) vn = ldg_stream_f32(a.values + beg + gl);
+    j1 = ldg_stream_i32(a.col_idx + beg + gl);
+    if (HAS_VAL) v1 = ldg_stream_f32(a.values + beg + gl);
+    if (NEEDG) g1 = __ldg((GAT ? a.t : a.d_col) + (HINT ? (j1 & 0x7FFFFFFF) : j1));
+  }
+  if (LPR + gl < len) {
+    j2 = ldg_stream_i32(a.col_idx + beg + LPR + gl);
+    if (HAS_VAL) v2 = ldg_stream_f32(a.values + beg + LPR + gl);
   }
   for (int base = 0; base < wmax; base += LPR) {
-    const int j = HINT ? (jn & 0x7FFFFFFF) : jn;  // HINT: bit 31 tags a hub column
-    const bool hot = HINT && jn < 0;
-    const float v = vn;
+    const int j = HINT ? (j1 & 0x7FFFFFFF) : j1;  // HINT: bit 31 tags a hub column
+    const bool hot = HINT && j1 < 0;
+    const float v = v1;
+    const float g = g1;
     const bool mine = base + gl < len;
-    if (base + LPR + gl < len) {
-      jn = ldg_stream_i32(a.col_idx + beg + base + LPR + gl);
-      if (HAS_VAL) vn = ldg_stream_f32(a.values + beg + base + LPR + gl);
+    j1 = j2;
+    v1 = v2;
+    if (NEEDG && base + LPR + gl < len)
+      g1 = __ldg((GAT ? a.t : a.d_col) + (HINT ? (j1 & 0x7FFFFFFF) : j1));
+    if (base + 2 * LPR + gl < len) {
+      j2 = ldg_stream_i32(a.col_idx + beg + base + 2 * LPR + gl);
+      if (HAS_VAL) v2 = ldg_stream_f32(a.values + beg + base + 2 * LPR + gl);
     }
     float dj = 1.0f;
-    if (HAS_DCOL && mine) dj = __ldg(a.d_col + j);
+    if (HAS_DCOL && mine) dj = g;
     float e = -INFINITY;
     if (GAT) {
-      if (mine) e = leaky(si + __ldg(a.t + j), a.slope);
+      if (mine) e = leaky(si + g, a.slope);
       const float mb = group_max<LPR>(e);
       const float mn = fmaxf(m, mb);
       if (mn > m) {  // group-uniform: rescale the running sums to the new max

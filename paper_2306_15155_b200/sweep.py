@@ -27,6 +27,7 @@ SIZES = [(32, 32), (128, 128), (512, 512), (1024, 1024), (32, 256), (256, 32), (
 NS = [2 ** 14, 2 ** 16, 2 ** 18, 2 ** 20, 2 ** 21]
 DEGREES = [2, 8, 32, 128, 512]
 MAX_NNZ = 200_000_000
+NAMED = ("arxiv", "reddit", "products")  # benchmark shapes: train-only, never in the held-out split
 
 
 def graph_plan(quick: bool = False) -> list[tuple[str, str, int, int]]:
@@ -42,6 +43,13 @@ def graph_plan(quick: bool = False) -> list[tuple[str, str, int, int]]:
     return plan
 
 
+def named_plan() -> list[tuple[str, str, int, int]]:
+    """The BASELINE graph shapes themselves (arxiv, reddit, products)."""
+    from .graphs import SHAPES
+
+    return [(s.name, s.kind, s.n, s.nnz) for k, s in SHAPES.items() if k != "cora"]
+
+
 def cmd_profile(args) -> None:
     import torch
 
@@ -52,10 +60,11 @@ def cmd_profile(args) -> None:
     out.parent.mkdir(parents=True, exist_ok=True)
     fh = out.open("a")
     t_start = time.time()
-    for gid, kind, n, nnz in graph_plan(args.quick):
+    plan = named_plan() if args.graphs == "named" else graph_plan(args.quick)
+    for gid, kind, n, nnz in plan:
         try:
-            a = graphs.synthetic_graph(kind, n, nnz, seed=1, device=dev,
-                                       max_candidates=1 << 33)
+            a = graphs.synthetic_graph(kind, n, nnz, seed=1 if args.graphs != "named" else 0,
+                                       device=dev, max_candidates=1 << 33)
         except RuntimeError as e:  # RMAT cannot reach this density
             print(f"skip {gid}: {e}", file=sys.stderr, flush=True)
             continue
@@ -116,7 +125,7 @@ def cmd_train(args) -> None:
         mine = [r for r in recs if r.model == model_tag and r.composition in comps]
         if not mine:
             continue
-        graphs_ = sorted({r.graph_id for r in mine})
+        graphs_ = sorted({r.graph_id for r in mine if r.graph_id not in NAMED})
         rng = np.random.default_rng(0)
         test_g = set(rng.choice(graphs_, size=max(1, len(graphs_) // 5), replace=False).tolist())
         tr = [r for r in mine if r.graph_id not in test_g]
@@ -126,7 +135,7 @@ def cmd_train(args) -> None:
         with warnings.catch_warnings():
             warnings.simplefilter("ignore")
             m = train(tr, model_tag, hyper, compositions=comps)
-        rep = {"train_graphs": len(graphs_) - len(test_g), "test_graphs": sorted(test_g),
+        rep = {"train_graphs": len({r.graph_id for r in tr}), "test_graphs": sorted(test_g),
                "hyper": vars(hyper), "train": evaluate(m, tr, comps), "test": evaluate(m, te, comps)}
         with warnings.catch_warnings():
             warnings.simplefilter("ignore")
@@ -149,6 +158,8 @@ def main(argv=None):
     pp.add_argument("--reps", type=int, default=3)
     pp.add_argument("--warmup", type=int, default=1)
     pp.add_argument("--quick", action="store_true")
+    pp.add_argument("--graphs", choices=("sweep", "named"), default="sweep",
+                    help="sweep: configs[4] uniform/RMAT grid; named: the arxiv/reddit/products shapes")
     pt = sub.add_parser("train")
     pt.add_argument("--records", required=True)
     pt.add_argument("--trees", type=int, default=300)
