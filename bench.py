@@ -345,6 +345,7 @@ def main():
         tf = ROOT / "profiles" / "traffic.json"
         if tf.exists():
             traffic = json.loads(tf.read_text()).get(f"{args.shape}/K{K}/{comp}")
+            traffic = traffic if isinstance(traffic, int) else None
         roof = {"kernel": "spmm_kernel", "bound": "hbm", "achieved": round(ach, 1),
                 "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(ach / pk["hbm_gbs"], 3),
                 "traffic": traffic, "alg_bytes_per_launch": spmm_bytes,
@@ -519,6 +520,52 @@ def _time_layer(fn, reps: int) -> float:
     return med
 
 
+def cora_config(gc, args, dev) -> dict:
+    """BASELINE configs[0]: 2-layer GCN 1433 -> 16 -> 7 on a Cora-shaped
+    uniform graph, every composition: GPU eager, GPU CUDA-graph replay, and
+    the CPU oracle (reference algorithm, float64) on all host cores and on 1."""
+    import torch
+
+    from oracle import gnn_oracle as orc
+    from paper_2306_15155_b200 import graphs, profiling, selector
+    from paper_2306_15155_b200.capture import GraphedForward
+
+    A = graphs.shape_graph("cora", seed=args.seed, device=dev)
+    g = gc.NormalizedGraph.from_adjacency(A).with_precomputed()
+    host = host_graph(A)
+    og = orc.GcnGraph.from_adjacency(host)
+    n = A.n_rows
+    rng = profiling.config_rng(args.seed, "cora", 1433, 16)
+    inp = profiling.draw_inputs(rng, n, 1433, 16, "gcn")
+    w2 = profiling.draw_inputs(profiling.config_rng(args.seed, "cora", 16, 7), n, 16, 7, "gcn")["w"]
+    h32 = inp["h"].astype(np.float32)
+    w1_32, w2_32 = inp["w"].astype(np.float32), w2.astype(np.float32)
+    h = torch.from_numpy(h32).to(dev)
+    out = {"n": n, "m_tilde": g.a_tilde.nnz, "layers": "1433->16->7", "compositions": {}}
+    for comp in selector.B200_COMPOSITIONS["gcn"]:
+        base, order = comp.split(":")
+        specs = [gc.GcnLayerSpec(1433, 16, w1_32, composition=base, order=order),
+                 gc.GcnLayerSpec(16, 7, w2_32, composition=base, order=order)]
+        fwd = lambda x: gc.gcn_forward(g, x, specs)  # noqa: E731
+        eager = _time_layer(lambda: fwd(h), 20)
+        gf = GraphedForward(fwd, h)
+        graphed = _time_layer(lambda: gf(h), 20)
+        y = gf(h).cpu().numpy()
+        ref = orc.gcn_layer(og, orc.gcn_layer(og, h32.astype(np.float64), w1_32.astype(np.float64),
+                                               base, order), w2_32.astype(np.float64), base, order)
+        out["compositions"][comp] = {"gpu_eager_ms": round(eager * 1e3, 4),
+                                     "gpu_graph_ms": round(graphed * 1e3, 4),
+                                     "rel_err": orc.rel_err(y, ref)}
+    # the reference's own CPU path (oracle port), default composition, 1 and all threads
+    for threads in (1, os.cpu_count()):
+        orc.set_threads(threads)
+        t = time_cpu(lambda: orc.gcn_layer(og, orc.gcn_layer(og, h32.astype(np.float64),
+                                                              w1_32.astype(np.float64), "dynamic"),
+                                           w2_32.astype(np.float64), "dynamic"), 3, 10)
+        out[f"cpu_oracle_{threads}t_ms"] = round(t * 1e3, 3)
+    return out
+
+
 def extra_configs(gc, args, dev, pk) -> dict:
     """BASELINE configs[2] (single/4-head GAT on arxiv, SDDMM vs reassociated
     attention, reuse vs recompute) and configs[3] (GCN + GAT on products, 1
@@ -527,7 +574,7 @@ def extra_configs(gc, args, dev, pk) -> dict:
 
     from paper_2306_15155_b200 import graphs, selector
 
-    res = {}
+    res = {"cora": cora_config(gc, args, dev)}
     # ---- GAT on ogbn-arxiv-shaped RMAT ---------------------------------------
     A = graphs.shape_graph("arxiv", seed=args.seed, device=dev)
     at = gc.add_self_loops(A)

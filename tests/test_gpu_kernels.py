@@ -404,3 +404,18 @@ def test_host_pipelined_layer_matches_device_path(plgraph, comp, order):
     assert not out.is_cuda and out.is_pinned()
     ref = gc.gcn_layer(g, h.to(DEV), spec).cpu()
     assert torch.allclose(out, ref, rtol=1e-5, atol=1e-6)
+
+
+def test_cuda_graph_captured_forward_matches_eager(plgraph):
+    from paper_2306_15155_b200.capture import GraphedForward
+
+    rng = np.random.default_rng(31)
+    g = gc.NormalizedGraph(plgraph, gc.inv_sqrt_degrees(plgraph)).with_precomputed()
+    specs = [gc.GcnLayerSpec(40, 16, f32(rng.uniform(-0.5, 0.5, (40, 16))), composition="dynamic"),
+             gc.GcnLayerSpec(16, 7, f32(rng.uniform(-0.5, 0.5, (16, 7))), composition="precompute")]
+    h = torch.from_numpy(f32(rng.uniform(-0.5, 0.5, (plgraph.n_rows, 40)))).to(DEV)
+    eager = gc.gcn_forward(g, h, specs)
+    fwd = GraphedForward(lambda x: gc.gcn_forward(g, x, specs), h)
+    assert torch.equal(fwd(h), eager)
+    h2 = h * 0.5
+    assert torch.equal(fwd(h2), gc.gcn_forward(g, h2, specs))
