@@ -262,3 +262,32 @@ def test_hash_matches_python_reference():
     got = graphs.splitmix64(x).tolist()
     exp = [graphs._s64(graphs._splitmix64_int(v & graphs._M64)) for v in (0, 1, 12345, -7)]
     assert got == exp
+
+
+def test_sweep_plan_and_train_roundtrip(tmp_path, sel_golden, monkeypatch):
+    from paper_2306_15155_b200 import sweep
+
+    plan = sweep.graph_plan()
+    assert len(plan) > 30 and {k for _, k, _, _ in plan} == {"uniform", "rmat"}
+    assert all(nnz <= sweep.MAX_NNZ and nnz % 2 == 0 for _, _, _, nnz in plan)
+    assert [p[0] for p in sweep.named_plan()] == ["arxiv", "reddit", "products"]
+    # synthetic 4-composition records -> train/evaluate/save through the CLI
+    base = [profiling.ProfileRecord.from_dict(d) for d in sel_golden["records"] if d["model"] == "gcn"]
+    comps = selector.B200_COMPOSITIONS["gcn"]
+    recs = []
+    for r in base:
+        if r.composition != "precompute":
+            continue
+        for i, c in enumerate(comps):
+            fast = (i == 3) if r.features.nnz_mean > 20 else (i == 0)
+            recs.append(profiling.ProfileRecord.from_dict(
+                {**r.to_dict(), "composition": c, "median_time_s": r.median_time_s * (1 if fast else 1.5)}))
+    path = tmp_path / "r.ndjson"
+    profiling.write_records(path, recs)
+    monkeypatch.setattr(selector, "MODEL_DIR", tmp_path / "models")
+    rep = tmp_path / "rep.json"
+    sweep.main(["train", "--records", str(path), "--trees", "20", "--lr", "0.3", "--depth", "3",
+                "--report", str(rep)])
+    report = json.loads(rep.read_text())
+    assert report["gcn"]["train"]["selected_over_oracle_geomean"] < 1.05
+    assert (tmp_path / "models" / "gcn_b200.json").exists()
