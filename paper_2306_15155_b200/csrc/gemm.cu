@@ -137,12 +137,6 @@ struct GemmEpi {
   uint32_t flags;
 };
 
-// byte offset (from the 1024-aligned smem base) of the epilogue staging area
-__host__ __device__ constexpr uint32_t kStageOffFor(int stages, uint32_t stage_bytes) {
-  return ((uint32_t)stages * stage_bytes + 8u * (2 * stages + 4) + 16u + 127u) & ~127u;
-}
-constexpr uint32_t kEpiStageBytes = 4 * 32 * 33 * 4;  // 4 warps x 32 rows x (32+1) floats
-
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -176,7 +170,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const int n_tiles_total = m_tiles * n_tiles;
-  auto kStageOff = [&](int st) { return kStageOffFor(st, STAGE_BYTES); };
 
   if (warp == 1 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
@@ -244,43 +237,45 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else {  // ---------------- epilogue warps 2..5 ----------------
-    // TMEM -> registers (thread = row) -> padded smem transpose -> row-wise
-    // coalesced stores (one 128-B line per store instruction).
-    constexpr int CW = BN < 32 ? BN : 32;  // columns per chunk
-    const int q = warp & 3;                // TMEM lane quarter this warp may access
-    float *stage = reinterpret_cast<float *>(gbase + kStageOff(stages)) + (warp - 2) * 32 * (CW + 1);
+    // TMEM -> registers (thread = row, 16 consecutive columns per tcgen05.ld)
+    // -> fused row scale / ReLU -> 4 x 16-byte stores per row segment.  (A
+    // shared-memory transpose for line-coalesced stores measured slower: it
+    // triples the epilogue's instruction count; profiles/r01_ncu_summary.md.)
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
     const bool relu = (ep.flags & GC_RELU) != 0;
+    const bool vec = ((ep.ldc & 3) == 0) && aligned16(ep.C);
     int lt = 0;
     for (int tile = blockIdx.x; tile < n_tiles_total; tile += gridDim.x, ++lt) {
       const int acc = lt & 1;
       const int m0 = (tile / n_tiles) * BM, n0 = (tile % n_tiles) * BN;
       mbar_wait(tfull_bar(acc), (lt >> 1) & 1);
       tc_fence_after();
-      const int row0 = m0 + q * 32;
-      const int row = row0 + lane;
-      const float rs = (row < ep.M && ep.row_scale) ? __ldg(ep.row_scale + row) : 1.0f;
+      const int row = m0 + q * 32 + lane;
+      const bool row_ok = row < ep.M;
+      const float rs = (row_ok && ep.row_scale) ? __ldg(ep.row_scale + row) : 1.0f;
+      float *crow = ep.C + (int64_t)row * ep.ldc;
       const uint32_t taddr = tmem_base + (uint32_t)(acc * BN) + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
-      for (int c = 0; c < BN; c += CW) {
+      for (int c = 0; c < BN; c += 16) {
         if (n0 + c >= ep.N) break;  // warp-uniform
-        float v[CW];
-        tmem_ld16(taddr + (uint32_t)c, *reinterpret_cast<float(*)[16]>(&v[0]));
-        if constexpr (CW == 32) tmem_ld16(taddr + (uint32_t)(c + 16), *reinterpret_cast<float(*)[16]>(&v[16]));
+        float v[16];
+        tmem_ld16(taddr + (uint32_t)c, v);
 #pragma unroll
-        for (int i = 0; i < CW; ++i) {
-          float x = v[i] * rs;
-          if (relu) x = fmaxf(x, 0.0f);
-          stage[lane * (CW + 1) + i] = x;
+        for (int i = 0; i < 16; ++i) {
+          v[i] *= rs;
+          if (relu) v[i] = fmaxf(v[i], 0.0f);
         }
-        __syncwarp();
-        const int64_t col = n0 + c + (lane % CW);
-        const int rstep = 32 / CW;  // rows written per instruction
-#pragma unroll 4
-        for (int r = lane / CW; r < 32; r += rstep) {
-          const int64_t gr = row0 + r;
-          if (gr < ep.M && col < ep.N) ep.C[gr * ep.ldc + col] = stage[r * (CW + 1) + (lane % CW)];
+        if (!row_ok) continue;
+        const int64_t col = n0 + c;
+        if (vec && col + 16 <= ep.N) {
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            stg_f4(crow + col + i, make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (col + i < ep.N) crow[col + i] = v[i];
         }
-        __syncwarp();
       }
       tc_fence_before();
       __syncwarp();
@@ -444,11 +439,10 @@ int launch_tf32(const CUtensorMap &ma, const CUtensorMap &mb, const GemmEpi &ep,
                 cudaStream_t st) {
   const int num_kb = (int)((K + BK - 1) / BK);
   constexpr int stage_bytes = BM * BK * 4 + BN * BK * 4;
-  // deepest ring that fits next to the barriers and the epilogue staging
-  // area (<= 8 stages, ring <= ~190 KB)
-  int stages = (190 * 1024) / stage_bytes;
+  // deepest ring that fits next to the barriers (<= 8 stages, <= ~200 KB)
+  int stages = (200 * 1024) / stage_bytes;
   stages = stages > 8 ? 8 : (stages < 2 ? 2 : stages);
-  const size_t smem = kStageOffFor(stages, stage_bytes) + kEpiStageBytes + 1024;
+  const size_t smem = (size_t)stages * stage_bytes + 8 * (2 * stages + 4) + 16 + 1024;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
