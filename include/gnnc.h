@@ -55,6 +55,10 @@ extern "C" {
 #define GC_HUB_TAGGED (1u << 2) /* col_idx entries carry a hub tag in bit 31 (gc_tag_hub_columns):
                                    tagged rows of B are gathered with L1::evict_last, the rest
                                    with L1::no_allocate (SpMM / GAT aggregation only) */
+#define GC_SPMM_SHRINK(s) ((uint32_t)(s) << 8) /* SpMM/GAT lane-group variant s in {0,1,2}:
+                                                 (K/4 >> s) lanes per row, each owning 4<<s
+                                                 columns; more rows per warp for short rows */
+#define GC_SPMM_SHRINK_MASK (3u << 8)
 #define GC_GEMM_TF32 (1u << 4)  /* tcgen05.mma kind::tf32, TMEM accumulators, TMA operands */
 #define GC_GEMM_FP32 (1u << 5)  /* exact fp32 CUDA-core path (rtol 1e-4 parity mode) */
 

@@ -16,6 +16,10 @@ from ._build import LIB, ROOT
 GC_RELU = 1 << 0
 GC_ACCUMULATE = 1 << 1
 GC_HUB_TAGGED = 1 << 2
+
+
+def GC_SPMM_SHRINK(s: int) -> int:  # noqa: N802 - mirrors the C macro
+    return (int(s) & 3) << 8
 GC_GEMM_TF32 = 1 << 4
 GC_GEMM_FP32 = 1 << 5
 GC_SPMM_ROW = 1

@@ -131,7 +131,8 @@ template <int LPR, int NV, bool VEC, bool HAS_VAL, bool HAS_DCOL, bool GAT, bool
 __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
   using T = typename Lanes<VEC>::T;
   constexpr int GPB = kThreads / LPR;
-  constexpr int U = (NV >= 2) ? 4 : (LPR < 8 ? LPR : 8);  // edges unrolled per step
+  // edges unrolled per step: ~8 independent 16-byte gathers in flight per lane
+  constexpr int U = NV >= 8 ? 1 : NV >= 4 ? 2 : NV >= 2 ? 4 : (LPR < 8 ? LPR : 8);
   const int g = threadIdx.x / LPR;
   const int gl = threadIdx.x % LPR;
   const int64_t item = (int64_t)blockIdx.x * GPB + g;
@@ -382,12 +383,24 @@ int dispatch(SpmmArgs &a, int64_t n_rows, int algo, const int32_t *items, int64_
                    aligned16(a.C) && (a.partial == nullptr || aligned16(a.partial));
   cudaStream_t st = as_stream(stream);
   if (vec) {
+    // lane-shrink s: LPR >> s lanes per row, each owning NV << s float4
+    // columns (same columns per pass; more rows per warp for short rows)
+    const int sh = (int)((a.flags >> 8) & 3u);
     if (K <= 8) return launch_cfg<2, 1, true, GAT>(a, sr, n_split, st);
-    if (K <= 16) return launch_cfg<4, 1, true, GAT>(a, sr, n_split, st);
-    if (K <= 32) return launch_cfg<8, 1, true, GAT>(a, sr, n_split, st);
-    if (K <= 64) return launch_cfg<16, 1, true, GAT>(a, sr, n_split, st);
-    if (K <= 128) return launch_cfg<32, 1, true, GAT>(a, sr, n_split, st);
-    return launch_cfg<32, 2, true, GAT>(a, sr, n_split, st);
+    if (K <= 16) return sh ? launch_cfg<2, 2, true, GAT>(a, sr, n_split, st)
+                           : launch_cfg<4, 1, true, GAT>(a, sr, n_split, st);
+    if (K <= 32) return sh == 2 ? launch_cfg<2, 4, true, GAT>(a, sr, n_split, st)
+                      : sh == 1 ? launch_cfg<4, 2, true, GAT>(a, sr, n_split, st)
+                                : launch_cfg<8, 1, true, GAT>(a, sr, n_split, st);
+    if (K <= 64) return sh == 2 ? launch_cfg<4, 4, true, GAT>(a, sr, n_split, st)
+                      : sh == 1 ? launch_cfg<8, 2, true, GAT>(a, sr, n_split, st)
+                                : launch_cfg<16, 1, true, GAT>(a, sr, n_split, st);
+    if (K <= 128) return sh == 2 ? launch_cfg<8, 4, true, GAT>(a, sr, n_split, st)
+                       : sh == 1 ? launch_cfg<16, 2, true, GAT>(a, sr, n_split, st)
+                                 : launch_cfg<32, 1, true, GAT>(a, sr, n_split, st);
+    return sh == 2 ? launch_cfg<8, 8, true, GAT>(a, sr, n_split, st)
+         : sh == 1 ? launch_cfg<16, 4, true, GAT>(a, sr, n_split, st)
+                   : launch_cfg<32, 2, true, GAT>(a, sr, n_split, st);
   }
   if (K <= 8) return launch_cfg<8, 1, false, GAT>(a, sr, n_split, st);
   if (K <= 16) return launch_cfg<16, 1, false, GAT>(a, sr, n_split, st);
@@ -428,8 +441,8 @@ extern "C" int gc_spmm_f32(const int32_t *row_ptr, const int32_t *col_idx, const
                            size_t ws_bytes, void *stream) {
   GC_REQUIRE(n_rows >= 0 && n_cols >= 0 && K >= 0, GC_ERR_SHAPE, "gc_spmm_f32: negative size");
   GC_REQUIRE(ldb >= K && ldc >= K, GC_ERR_SHAPE, "gc_spmm_f32: leading dimension < K");
-  GC_REQUIRE((flags & ~(GC_RELU | GC_ACCUMULATE | GC_HUB_TAGGED)) == 0, GC_ERR_VALUE,
-             "gc_spmm_f32: unknown flags 0x%x", flags);
+  GC_REQUIRE((flags & ~(GC_RELU | GC_ACCUMULATE | GC_HUB_TAGGED | GC_SPMM_SHRINK_MASK)) == 0,
+             GC_ERR_VALUE, "gc_spmm_f32: unknown flags 0x%x", flags);
   if (n_rows == 0 || K == 0) return GC_OK;
   GC_REQUIRE(row_ptr && C && (B || n_cols == 0), GC_ERR_VALUE, "gc_spmm_f32: null operand");
   GC_REQUIRE(n_rows < INT32_MAX && n_cols < INT32_MAX, GC_ERR_SHAPE,
@@ -461,7 +474,7 @@ extern "C" int gc_gat_aggregate_f32(const int32_t *row_ptr, const int32_t *col_i
   GC_REQUIRE(n_rows >= 0 && n_cols >= 0 && K >= 0, GC_ERR_SHAPE,
              "gc_gat_aggregate_f32: negative size");
   GC_REQUIRE(ldb >= K && ldc >= K, GC_ERR_SHAPE, "gc_gat_aggregate_f32: leading dimension < K");
-  GC_REQUIRE((flags & ~(GC_RELU | GC_HUB_TAGGED)) == 0, GC_ERR_VALUE,
+  GC_REQUIRE((flags & ~(GC_RELU | GC_HUB_TAGGED | GC_SPMM_SHRINK_MASK)) == 0, GC_ERR_VALUE,
              "gc_gat_aggregate_f32: unknown flags 0x%x", flags);
   GC_REQUIRE(slope > 0.0f && slope < 1.0f, GC_ERR_VALUE,
              "gc_gat_aggregate_f32: leaky_slope must lie in (0, 1)");

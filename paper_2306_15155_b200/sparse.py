@@ -436,32 +436,51 @@ def _plan_args(a: CsrMatrix, K: int, algo: str, dev, gat: bool = False):
     return nat.GC_SPMM_NNZ_SPLIT, items, items.shape[0], split, split.shape[0], ws
 
 
-def _use_hints(a: CsrMatrix, K: int, launch) -> bool:
-    """Decide the hub-tag variant for (pattern, K); ``launch(cols, flag, out)``
-    runs the kernel into a scratch output.  "auto" times both variants once
-    (CUDA events, median of 3) and caches the faster."""
-    mode = HUB_HINTS if isinstance(HUB_HINTS, str) else ("1" if HUB_HINTS else "0")
-    if mode == "0" or a.nnz < PLAN_MIN_NNZ:
-        return False
-    if mode == "1":
-        return True
+SPMM_SHRINK = os.environ.get("GNNC_SPMM_SHRINK", "auto")  # lane-group variant: auto | 0 | 1 | 2
+
+
+def _shrink_candidates(K: int) -> list[int]:
+    return [0] if K <= 8 else ([0, 1] if K <= 16 else [0, 1, 2])
+
+
+def _variant(a: CsrMatrix, K: int, mode: str, probe) -> tuple[bool, int]:
+    """Kernel variant for (pattern, K, mode): hub-column L1 tags on/off and the
+    lane-group shape.  ``probe(cols, extra_flags)`` runs the kernel into a
+    scratch output.  In "auto" mode every candidate is timed once (CUDA
+    events, median of 3 after a warm launch) on the first large launch and the
+    fastest is cached — the GPU counterpart of the reference's OPT autotuner
+    (tiling.py:311-364), over kernel variants instead of CPU tile sizes."""
+    hint_mode = HUB_HINTS if isinstance(HUB_HINTS, str) else ("1" if HUB_HINTS else "0")
+    shrink_mode = str(SPMM_SHRINK)
+    if a.nnz < PLAN_MIN_NNZ:
+        return False, 0
+    hints = [False, True] if hint_mode == "auto" else [hint_mode == "1"]
+    shrinks = _shrink_candidates(K) if shrink_mode == "auto" else [int(shrink_mode)]
+    if len(hints) * len(shrinks) == 1:
+        return hints[0], shrinks[0]
     if a.nnz < HUB_AUTOTUNE_MIN_NNZ:
-        return False
-    key = ("hint-choice", int(K))
+        return (False if hint_mode == "auto" else hints[0]), (0 if shrink_mode == "auto" else shrinks[0])
+    key = ("variant", mode, int(K))
     if key not in a._plans:
-        tagged = a.hub_tagged_cols(K)
         times = {}
-        for variant, cols, flag in ((False, a.col_idx, 0), (True, tagged, nat.GC_HUB_TAGGED)):
-            launch(cols, flag)  # warm
-            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                  for _ in range(3)]
-            for e0, e1 in ev:
-                e0.record()
-                launch(cols, flag)
-                e1.record()
-            torch.cuda.synchronize()
-            times[variant] = sorted(e0.elapsed_time(e1) for e0, e1 in ev)[1]
-        a._plans[key] = times[True] < 0.97 * times[False]
+        for hv in hints:
+            cols = a.hub_tagged_cols(K) if hv else a.col_idx
+            for sv in shrinks:
+                extra = (nat.GC_HUB_TAGGED if hv else 0) | nat.GC_SPMM_SHRINK(sv)
+                probe(cols, extra)  # warm
+                ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                      for _ in range(3)]
+                for e0, e1 in ev:
+                    e0.record()
+                    probe(cols, extra)
+                    e1.record()
+                torch.cuda.synchronize()
+                times[(hv, sv)] = sorted(e0.elapsed_time(e1) for e0, e1 in ev)[1]
+        base = times.get((False, 0), min(times.values()))
+        best = min(times, key=times.get)
+        # keep the default unless a variant is clearly (>3%) faster
+        a._plans[key] = best if times[best] < 0.97 * base else (False, 0)
+        a._plans[key + ("times",)] = {f"hints={h},shrink={v}": round(t, 4) for (h, v), t in times.items()}
     return a._plans[key]
 
 
@@ -502,9 +521,10 @@ def _spmm(a: CsrMatrix, b, *, weighted: bool, d_row=None, d_col=None, relu=False
             scratch = torch.empty(a.n_rows, K, dtype=torch.float32, device=dev)
         nat.check(launch(cols, extra, scratch, flags & ~nat.GC_ACCUMULATE), what)
 
-    hints = _use_hints(a, K, probe)
+    hints, shrink = _variant(a, K, "spmm", probe)
     cols = a.hub_tagged_cols(K) if hints else a.col_idx
-    rc = _timed_call("spmm", dev, lambda: launch(cols, nat.GC_HUB_TAGGED if hints else 0))
+    extra = (nat.GC_HUB_TAGGED if hints else 0) | nat.GC_SPMM_SHRINK(shrink)
+    rc = _timed_call("spmm", dev, lambda: launch(cols, extra))
     nat.check(rc, what)
     return op.wrap(out)
 
@@ -541,9 +561,10 @@ def gat_aggregate(a: CsrMatrix, s: torch.Tensor, t: torch.Tensor, slope: float, 
     def probe(cols, extra):
         nat.check(launch(cols, extra), "gat_aggregate")  # writes `out`; the real launch follows
 
-    hints = _use_hints(a, K, probe)
+    hints, shrink = _variant(a, K, "gat", probe)
     cols = a.hub_tagged_cols(K) if hints else a.col_idx
-    rc = _timed_call("spmm", dev, lambda: launch(cols, nat.GC_HUB_TAGGED if hints else 0))
+    extra = (nat.GC_HUB_TAGGED if hints else 0) | nat.GC_SPMM_SHRINK(shrink)
+    rc = _timed_call("spmm", dev, lambda: launch(cols, extra))
     nat.check(rc, "gat_aggregate")
     return op.wrap(out)
 

@@ -419,3 +419,40 @@ def test_cuda_graph_captured_forward_matches_eager(plgraph):
     assert torch.equal(fwd(h), eager)
     h2 = h * 0.5
     assert torch.equal(fwd(h2), gc.gcn_forward(g, h2, specs))
+
+
+@pytest.mark.parametrize("K", [16, 32, 64, 128, 256])
+@pytest.mark.parametrize("shrink", ["0", "1", "2"])
+@pytest.mark.parametrize("hints", ["0", "1"])
+def test_spmm_and_gat_kernel_variants(oracle, plgraph, K, shrink, hints, monkeypatch):
+    """Every lane-group shape x hub-tag variant the autotuner can pick is exact."""
+    if K <= 16 and shrink == "2":
+        pytest.skip("no such variant")
+    monkeypatch.setattr(sparse, "PLAN_MIN_NNZ", 0)
+    monkeypatch.setattr(sparse, "SPMM_SHRINK", shrink)
+    monkeypatch.setattr(sparse, "HUB_HINTS", hints)
+    monkeypatch.setattr(sparse, "HUB_L1_BUDGET", 64 * K)  # tag ~16 hub columns
+    rng = np.random.default_rng(K)
+    a = plgraph.with_values(torch.from_numpy(f32(rng.uniform(0.5, 2, plgraph.nnz))).to(DEV))
+    oa = to_oracle(oracle, a)
+    b = f32(rng.standard_normal((a.n_cols, K)))
+    d = f32(rng.uniform(0.1, 1.0, a.n_rows))
+    bt, dt = torch.from_numpy(b).to(DEV), torch.from_numpy(d).to(DEV)
+    out = gc.spmm(a, bt, d_row=dt, d_col=dt).cpu().numpy()
+    ref = oracle.scale_rows(d, oracle.spmm(oa, oracle.scale_rows(d, b)))
+    assert oracle.rel_err(out, ref) < SP_TOL
+    s, t = f32(rng.standard_normal(a.n_rows)), f32(rng.standard_normal(a.n_rows))
+    outg = sparse.gat_aggregate(a, torch.from_numpy(s).to(DEV), torch.from_numpy(t).to(DEV), 0.2,
+                                bt).cpu().numpy()
+    refg = oracle.spmm(oa.with_values(oracle.edge_softmax(oa, s, t, 0.2)), b)
+    assert oracle.rel_err(outg, refg) < 2e-5
+
+
+def test_variant_autotune_caches_a_choice(monkeypatch):
+    monkeypatch.setattr(sparse, "HUB_AUTOTUNE_MIN_NNZ", 0)
+    monkeypatch.setattr(sparse, "PLAN_MIN_NNZ", 0)
+    a = gc.add_self_loops(graphs.synthetic_graph("rmat", 4096, 60000, seed=2, device=DEV))
+    b = torch.rand(a.n_cols, 64, device=DEV)
+    r1 = gc.spmm(a, b)
+    assert ("variant", "spmm", 64) in a._plans
+    assert torch.equal(gc.spmm(a, b), r1)  # cached variant, deterministic
