@@ -372,6 +372,9 @@ def main():
                   "normalize_sddmm_ms": round(norm_ms, 3)},
     }
     result["clocks"] = clocks.summary()
+    pl = a_used._plans
+    result["spmm_variant"] = {"chosen": pl.get(("variant", "spmm", K)),
+                              "autotune_ms": pl.get(("variant", "spmm", K, "times"))}
 
     if rank == 0 and world == 1:
         # ---- e2e through the public API with host buffers ----------------------

@@ -133,6 +133,21 @@ GNNC_API int gc_gat_aggregate_f32(const int32_t *row_ptr, const int32_t *col_idx
 GNNC_API int gc_tag_hub_columns(const int32_t *col_idx, int64_t nnz, const uint8_t *hot,
                                 int32_t *col_tagged, void *stream);
 
+/* Fused GAT aggregation with the attention as an SDDMM over edges (SURVEY.md
+ * §8(a) A17 fused with N1): e_p = LeakyReLU(a_src.B[i,:] + a_dst.B[j,:]),
+ * alpha = row softmax, C[i,:] = epi(sum_p alpha_p B[j,:]).  Each gathered row
+ * B[j,:] feeds both its score and the aggregation (one gather per edge); the
+ * reuse composition (B = HW, gat.py:121-129).  Needs a square pattern,
+ * K % 4 == 0, K <= 256, 16-byte aligned B/C/a_src/a_dst (else
+ * GC_ERR_UNSUPPORTED).  Plan/workspace protocol as gc_gat_aggregate_f32. */
+GNNC_API int gc_gat_sddmm_aggregate_f32(const int32_t *row_ptr, const int32_t *col_idx,
+                                        const float *a_src, const float *a_dst, float slope,
+                                        const float *B, int64_t ldb, int64_t n_rows, int64_t K,
+                                        float *C, int64_t ldc, uint32_t flags, int algo,
+                                        const int32_t *items, int64_t n_items,
+                                        const int32_t *split_rows, int64_t n_split_rows,
+                                        void *workspace, size_t ws_bytes, void *stream);
+
 /* ---- SDDMM --------------------------------------------------------------
  * out[p] = (a_vals ? a_vals[p] : 1) * sum_t B[i,t] * Cm[col_idx[p],t]
  * Replaces sparse.sddmm (sparse.py:267-282 -> _sddmm_kernel 222-232).

@@ -44,6 +44,8 @@ struct SpmmArgs {
   const float *s;     // GAT: per-row source score (s = HW a_src)
   const float *t;     // GAT: per-column target score (t = HW a_dst)
   float slope;        // GAT: LeakyReLU slope
+  const float *a_src; // GAT-SDDMM: attention vectors (length K): e = a_src.B_i + a_dst.B_j
+  const float *a_dst;
   uint32_t flags;
   bool hints;         // col_idx carries hub tags in bit 31 (gc_tag_hub_columns)
 };
@@ -70,6 +72,10 @@ __device__ __forceinline__ void fma_into(float4 &acc, float w, float4 b) {
   acc.w = fmaf(w, b.w, acc.w);
 }
 __device__ __forceinline__ void fma_into(float &acc, float w, float b) { acc = fmaf(w, b, acc); }
+__device__ __forceinline__ float dot_of(float4 x, float4 w) {
+  return fmaf(x.x, w.x, fmaf(x.y, w.y, fmaf(x.z, w.z, x.w * w.w)));
+}
+__device__ __forceinline__ float dot_of(float x, float w) { return x * w; }
 __device__ __forceinline__ void scale_into(float4 &acc, float sc) {
   acc.x *= sc, acc.y *= sc, acc.z *= sc, acc.w *= sc;
 }
@@ -127,9 +133,15 @@ __device__ __forceinline__ void store_row(const SpmmArgs &a, int row, int slot, 
 }
 
 // One group of LPR lanes per work item (a row, or a chunk of a heavy row).
-template <int LPR, int NV, bool VEC, bool HAS_VAL, bool HAS_DCOL, bool GAT, bool HINT>
+// MODE 0: SpMM.  MODE 1: GAT, e = LeakyReLU(s_i + t_j) with t_j gathered.
+// MODE 2: GAT whose score is an SDDMM over the gathered rows themselves,
+// e = LeakyReLU(a_src.B_i + a_dst.B_j): one gather of B_j feeds both the
+// score and the aggregation (needs the whole row in one column pass).
+template <int LPR, int NV, bool VEC, bool HAS_VAL, bool HAS_DCOL, int MODE, bool HINT>
 __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
   using T = typename Lanes<VEC>::T;
+  constexpr bool GAT = MODE != 0;
+  constexpr bool SD = MODE == 2;
   constexpr int GPB = kThreads / LPR;
   // edges unrolled per step: ~8 independent 16-byte gathers in flight per lane
   constexpr int U = NV >= 8 ? 1 : NV >= 4 ? 2 : NV >= 2 ? 4 : (LPR < 8 ? LPR : 8);
@@ -168,18 +180,37 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
   const int wmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)len);
   // GAT: online softmax state; m is identical on every lane of the group,
   // zl sums this lane's own edge weights relative to m.
-  const float si = (GAT && live) ? __ldg(a.s + row) : 0.0f;
+  float si = (MODE == 1 && live) ? __ldg(a.s + row) : 0.0f;
   float m = -INFINITY, zl = 0.0f;
+  T adst[NV];
+  if constexpr (SD) {  // source term a_src.B_i and this lane's slice of a_dst
+    float part = 0.0f;
+    const float *bi = a.B + (int64_t)row * a.ldb;
+#pragma unroll
+    for (int vv = 0; vv < NV; ++vv) {
+      adst[vv] = zero_of(T{});
+      if (colok[vv]) {
+        T x, w;
+        load_b(w, a.a_src + coff[vv]);
+        if (live) {
+          load_b(x, bi + coff[vv]);
+          part += dot_of(x, w);
+        }
+        load_b(adst[vv], a.a_dst + coff[vv]);
+      }
+    }
+    si = group_sum<LPR>(part);
+  }
   // Two-deep software pipeline over batches of LPR edges: while batch i's rows
   // of B are gathered, batch i+1's per-node gather (d_j or t_j) and batch
   // i+2's (col, value) loads are already in flight.
-  constexpr bool NEEDG = HAS_DCOL || GAT;
+  constexpr bool NEEDG = HAS_DCOL || MODE == 1;
   int j1 = 0, j2 = 0;
   float v1 = 1.0f, v2 = 1.0f, g1 = 0.0f;
   if (gl < len) {
     j1 = ldg_stream_i32(a.col_idx + beg + gl);
     if (HAS_VAL) v1 = ldg_stream_f32(a.values + beg + gl);
-    if (NEEDG) g1 = __ldg((GAT ? a.t : a.d_col) + (HINT ? (j1 & 0x7FFFFFFF) : j1));
+    if (NEEDG) g1 = __ldg((MODE == 1 ? a.t : a.d_col) + (HINT ? (j1 & 0x7FFFFFFF) : j1));
   }
   if (LPR + gl < len) {
     j2 = ldg_stream_i32(a.col_idx + beg + LPR + gl);
@@ -194,7 +225,7 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
     j1 = j2;
     v1 = v2;
     if (NEEDG && base + LPR + gl < len)
-      g1 = __ldg((GAT ? a.t : a.d_col) + (HINT ? (j1 & 0x7FFFFFFF) : j1));
+      g1 = __ldg((MODE == 1 ? a.t : a.d_col) + (HINT ? (j1 & 0x7FFFFFFF) : j1));
     if (base + 2 * LPR + gl < len) {
       j2 = ldg_stream_i32(a.col_idx + beg + base + 2 * LPR + gl);
       if (HAS_VAL) v2 = ldg_stream_f32(a.values + beg + base + 2 * LPR + gl);
@@ -202,7 +233,7 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
     float dj = 1.0f;
     if (HAS_DCOL && mine) dj = g;
     float e = -INFINITY;
-    if (GAT) {
+    if (MODE == 1) {
       if (mine) e = leaky(si + g, a.slope);
       const float mb = group_max<LPR>(e);
       const float mn = fmaxf(m, mb);
@@ -237,20 +268,50 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
           }
         }
       }
-      const float w = mine ? v * dj : 0.0f;
+      if constexpr (SD) {
+        // per-edge score from the row just gathered, then an online-softmax
+        // update in edge order (m, zl identical on every lane of the group)
+        float eu[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const float we = __shfl_sync(0xffffffffu, w, e0 + u, LPR);
-        if ((e0 + u) < cnt) {
+        for (int u = 0; u < U; ++u) {
+          float part = 0.0f;
 #pragma unroll
-          for (int vv = 0; vv < NV; ++vv) fma_into(acc[vv], we, bv[u][vv]);
+          for (int vv = 0; vv < NV; ++vv) part += dot_of(bv[u][vv], adst[vv]);
+          part = group_sum<LPR>(part);
+          eu[u] = (e0 + u) < cnt ? leaky(si + part, a.slope) : -INFINITY;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if ((e0 + u) < cnt) {
+            if (eu[u] > m) {
+              const float sc = __expf(m - eu[u]);
+#pragma unroll
+              for (int vv = 0; vv < NV; ++vv) scale_into(acc[vv], sc);
+              zl *= sc;
+              m = eu[u];
+            }
+            const float w = __expf(eu[u] - m);
+            zl += w;
+#pragma unroll
+            for (int vv = 0; vv < NV; ++vv) fma_into(acc[vv], w, bv[u][vv]);
+          }
+        }
+      } else {
+        const float w = mine ? v * dj : 0.0f;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const float we = __shfl_sync(0xffffffffu, w, e0 + u, LPR);
+          if ((e0 + u) < cnt) {
+#pragma unroll
+            for (int vv = 0; vv < NV; ++vv) fma_into(acc[vv], we, bv[u][vv]);
+          }
         }
       }
     }
   }
   float ds = 1.0f;
   if (GAT) {
-    const float z = group_sum<LPR>(zl);
+    const float z = SD ? zl : group_sum<LPR>(zl);  // SD: every lane already holds the row sum
     if (slot >= 0) {
       if (live && gl == 0 && blockIdx.y == 0) a.partial_mz[slot] = make_float2(m, z);
     } else {
@@ -263,10 +324,11 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
 }
 
 // Combine the partial sums of split rows in slot order, then the epilogue.
-template <int LPR, int NV, bool VEC, bool GAT>
+template <int LPR, int NV, bool VEC, int MODE>
 __global__ void __launch_bounds__(kThreads)
     spmm_fixup_kernel(const SpmmArgs a, const int4 *split_rows, int64_t n_split) {
   using T = typename Lanes<VEC>::T;
+  constexpr bool GAT = MODE != 0;
   constexpr int GPB = kThreads / LPR;
   const int g = threadIdx.x / LPR;
   const int gl = threadIdx.x % LPR;
@@ -305,7 +367,7 @@ __global__ void __launch_bounds__(kThreads)
   store_row<LPR, NV, VEC>(a, sr.x, -1, gl, c0, ds, acc);
 }
 
-template <int LPR, int NV, bool VEC, bool GAT>
+template <int LPR, int NV, bool VEC, int MODE>
 int launch_cfg(const SpmmArgs &a, const int4 *split_rows, int64_t n_split, cudaStream_t st) {
   constexpr int GPB = kThreads / LPR;
   constexpr int64_t kColsPerPass = (int64_t)LPR * NV * Lanes<VEC>::W;
@@ -317,25 +379,27 @@ int launch_cfg(const SpmmArgs &a, const int4 *split_rows, int64_t n_split, cudaS
   if (a.n_items > 0) {
     dim3 grid((unsigned)((a.n_items + GPB - 1) / GPB), (unsigned)ychunks);
     const bool hv = a.values != nullptr, hd = a.d_col != nullptr;
-    if (a.hints) {
-      if (GAT) spmm_kernel<LPR, NV, VEC, false, false, true, true><<<grid, kThreads, 0, st>>>(a);
-      else if (hv && hd) spmm_kernel<LPR, NV, VEC, true, true, false, true><<<grid, kThreads, 0, st>>>(a);
-      else if (hv) spmm_kernel<LPR, NV, VEC, true, false, false, true><<<grid, kThreads, 0, st>>>(a);
-      else if (hd) spmm_kernel<LPR, NV, VEC, false, true, false, true><<<grid, kThreads, 0, st>>>(a);
-      else spmm_kernel<LPR, NV, VEC, false, false, false, true><<<grid, kThreads, 0, st>>>(a);
+    if constexpr (MODE != 0) {
+      if (a.hints) spmm_kernel<LPR, NV, VEC, false, false, MODE, true><<<grid, kThreads, 0, st>>>(a);
+      else spmm_kernel<LPR, NV, VEC, false, false, MODE, false><<<grid, kThreads, 0, st>>>(a);
+    } else if (a.hints) {
+      if (hv && hd) spmm_kernel<LPR, NV, VEC, true, true, 0, true><<<grid, kThreads, 0, st>>>(a);
+      else if (hv) spmm_kernel<LPR, NV, VEC, true, false, 0, true><<<grid, kThreads, 0, st>>>(a);
+      else if (hd) spmm_kernel<LPR, NV, VEC, false, true, 0, true><<<grid, kThreads, 0, st>>>(a);
+      else spmm_kernel<LPR, NV, VEC, false, false, 0, true><<<grid, kThreads, 0, st>>>(a);
     } else {
-      if (GAT) spmm_kernel<LPR, NV, VEC, false, false, true, false><<<grid, kThreads, 0, st>>>(a);
-      else if (hv && hd) spmm_kernel<LPR, NV, VEC, true, true, false, false><<<grid, kThreads, 0, st>>>(a);
-      else if (hv) spmm_kernel<LPR, NV, VEC, true, false, false, false><<<grid, kThreads, 0, st>>>(a);
-      else if (hd) spmm_kernel<LPR, NV, VEC, false, true, false, false><<<grid, kThreads, 0, st>>>(a);
-      else spmm_kernel<LPR, NV, VEC, false, false, false, false><<<grid, kThreads, 0, st>>>(a);
+      if (hv && hd) spmm_kernel<LPR, NV, VEC, true, true, 0, false><<<grid, kThreads, 0, st>>>(a);
+      else if (hv) spmm_kernel<LPR, NV, VEC, true, false, 0, false><<<grid, kThreads, 0, st>>>(a);
+      else if (hd) spmm_kernel<LPR, NV, VEC, false, true, 0, false><<<grid, kThreads, 0, st>>>(a);
+      else spmm_kernel<LPR, NV, VEC, false, false, 0, false><<<grid, kThreads, 0, st>>>(a);
     }
-    int rc = check_launch(GAT ? "gat_aggregate_kernel" : "spmm_kernel");
+    int rc = check_launch(MODE == 0 ? "spmm_kernel" : MODE == 1 ? "gat_aggregate_kernel"
+                                                                : "gat_sddmm_aggregate_kernel");
     if (rc) return rc;
   }
   if (n_split > 0) {
     dim3 grid((unsigned)((n_split + GPB - 1) / GPB), (unsigned)ychunks);
-    spmm_fixup_kernel<LPR, NV, VEC, GAT><<<grid, kThreads, 0, st>>>(a, split_rows, n_split);
+    spmm_fixup_kernel<LPR, NV, VEC, MODE><<<grid, kThreads, 0, st>>>(a, split_rows, n_split);
     return check_launch("spmm_fixup_kernel");
   }
   return GC_OK;
@@ -345,7 +409,7 @@ int launch_cfg(const SpmmArgs &a, const int4 *split_rows, int64_t n_split, cudaS
 
 namespace {
 
-template <bool GAT>
+template <int MODE>
 int dispatch(SpmmArgs &a, int64_t n_rows, int algo, const int32_t *items, int64_t n_items,
              const int32_t *split_rows, int64_t n_split_rows, void *workspace, size_t ws_bytes,
              void *stream, const char *who) {
@@ -362,7 +426,7 @@ int dispatch(SpmmArgs &a, int64_t n_rows, int algo, const int32_t *items, int64_
       GC_REQUIRE(workspace != nullptr && aligned16(workspace), GC_ERR_WORKSPACE,
                  "%s: 16-byte aligned workspace required", who);
       a.partial = static_cast<float *>(workspace);
-      if (GAT) {
+      if (MODE != 0) {
         // (max, sum) pairs follow the [n_slots][K] partial rows; the host
         // wrapper sized the workspace from the plan it owns.
         GC_REQUIRE(ws_bytes > 0, GC_ERR_WORKSPACE, "%s: bad workspace", who);
@@ -381,32 +445,36 @@ int dispatch(SpmmArgs &a, int64_t n_rows, int algo, const int32_t *items, int64_
   const int64_t K = a.K;
   const bool vec = (K % 4 == 0) && (a.ldb % 4 == 0) && (a.ldc % 4 == 0) && aligned16(a.B) &&
                    aligned16(a.C) && (a.partial == nullptr || aligned16(a.partial));
+  if (MODE == 2) {
+    GC_REQUIRE(vec && K <= 256 && aligned16(a.a_src) && aligned16(a.a_dst), GC_ERR_UNSUPPORTED,
+               "%s: needs K %% 4 == 0, K <= 256 and 16-byte aligned operands", who);
+  }
   cudaStream_t st = as_stream(stream);
   if (vec) {
     // lane-shrink s: LPR >> s lanes per row, each owning NV << s float4
     // columns (same columns per pass; more rows per warp for short rows)
     const int sh = (int)((a.flags >> 8) & 3u);
-    if (K <= 8) return launch_cfg<2, 1, true, GAT>(a, sr, n_split, st);
-    if (K <= 16) return sh ? launch_cfg<2, 2, true, GAT>(a, sr, n_split, st)
-                           : launch_cfg<4, 1, true, GAT>(a, sr, n_split, st);
-    if (K <= 32) return sh == 2 ? launch_cfg<2, 4, true, GAT>(a, sr, n_split, st)
-                      : sh == 1 ? launch_cfg<4, 2, true, GAT>(a, sr, n_split, st)
-                                : launch_cfg<8, 1, true, GAT>(a, sr, n_split, st);
-    if (K <= 64) return sh == 2 ? launch_cfg<4, 4, true, GAT>(a, sr, n_split, st)
-                      : sh == 1 ? launch_cfg<8, 2, true, GAT>(a, sr, n_split, st)
-                                : launch_cfg<16, 1, true, GAT>(a, sr, n_split, st);
-    if (K <= 128) return sh == 2 ? launch_cfg<8, 4, true, GAT>(a, sr, n_split, st)
-                       : sh == 1 ? launch_cfg<16, 2, true, GAT>(a, sr, n_split, st)
-                                 : launch_cfg<32, 1, true, GAT>(a, sr, n_split, st);
-    return sh == 2 ? launch_cfg<8, 8, true, GAT>(a, sr, n_split, st)
-         : sh == 1 ? launch_cfg<16, 4, true, GAT>(a, sr, n_split, st)
-                   : launch_cfg<32, 2, true, GAT>(a, sr, n_split, st);
+    if (K <= 8) return launch_cfg<2, 1, true, MODE>(a, sr, n_split, st);
+    if (K <= 16) return sh ? launch_cfg<2, 2, true, MODE>(a, sr, n_split, st)
+                           : launch_cfg<4, 1, true, MODE>(a, sr, n_split, st);
+    if (K <= 32) return sh == 2 ? launch_cfg<2, 4, true, MODE>(a, sr, n_split, st)
+                      : sh == 1 ? launch_cfg<4, 2, true, MODE>(a, sr, n_split, st)
+                                : launch_cfg<8, 1, true, MODE>(a, sr, n_split, st);
+    if (K <= 64) return sh == 2 ? launch_cfg<4, 4, true, MODE>(a, sr, n_split, st)
+                      : sh == 1 ? launch_cfg<8, 2, true, MODE>(a, sr, n_split, st)
+                                : launch_cfg<16, 1, true, MODE>(a, sr, n_split, st);
+    if (K <= 128) return sh == 2 ? launch_cfg<8, 4, true, MODE>(a, sr, n_split, st)
+                       : sh == 1 ? launch_cfg<16, 2, true, MODE>(a, sr, n_split, st)
+                                 : launch_cfg<32, 1, true, MODE>(a, sr, n_split, st);
+    return sh == 2 ? launch_cfg<8, 8, true, MODE>(a, sr, n_split, st)
+         : sh == 1 ? launch_cfg<16, 4, true, MODE>(a, sr, n_split, st)
+                   : launch_cfg<32, 2, true, MODE>(a, sr, n_split, st);
   }
-  if (K <= 8) return launch_cfg<8, 1, false, GAT>(a, sr, n_split, st);
-  if (K <= 16) return launch_cfg<16, 1, false, GAT>(a, sr, n_split, st);
-  if (K <= 32) return launch_cfg<32, 1, false, GAT>(a, sr, n_split, st);
-  if (K <= 64) return launch_cfg<32, 2, false, GAT>(a, sr, n_split, st);
-  return launch_cfg<32, 4, false, GAT>(a, sr, n_split, st);
+  if (K <= 8) return launch_cfg<8, 1, false, MODE>(a, sr, n_split, st);
+  if (K <= 16) return launch_cfg<16, 1, false, MODE>(a, sr, n_split, st);
+  if (K <= 32) return launch_cfg<32, 1, false, MODE>(a, sr, n_split, st);
+  if (K <= 64) return launch_cfg<32, 2, false, MODE>(a, sr, n_split, st);
+  return launch_cfg<32, 4, false, MODE>(a, sr, n_split, st);
 }
 
 __global__ void tag_hub_kernel(const int32_t *__restrict__ col, int64_t nnz,
@@ -460,8 +528,43 @@ extern "C" int gc_spmm_f32(const int32_t *row_ptr, const int32_t *col_idx, const
   a.ldc = ldc;
   a.flags = flags;
   a.hints = (flags & GC_HUB_TAGGED) != 0;
-  return dispatch<false>(a, n_rows, algo, items, n_items, split_rows, n_split_rows, workspace,
+  return dispatch<0>(a, n_rows, algo, items, n_items, split_rows, n_split_rows, workspace,
                          ws_bytes, stream, "gc_spmm_f32");
+}
+
+extern "C" int gc_gat_sddmm_aggregate_f32(const int32_t *row_ptr, const int32_t *col_idx,
+                                          const float *a_src, const float *a_dst, float slope,
+                                          const float *B, int64_t ldb, int64_t n_rows, int64_t K,
+                                          float *C, int64_t ldc, uint32_t flags, int algo,
+                                          const int32_t *items, int64_t n_items,
+                                          const int32_t *split_rows, int64_t n_split_rows,
+                                          void *workspace, size_t ws_bytes, void *stream) {
+  GC_REQUIRE(n_rows >= 0 && K >= 1, GC_ERR_SHAPE, "gc_gat_sddmm_aggregate_f32: bad size");
+  GC_REQUIRE(ldb >= K && ldc >= K, GC_ERR_SHAPE,
+             "gc_gat_sddmm_aggregate_f32: leading dimension < K");
+  GC_REQUIRE((flags & ~(GC_RELU | GC_HUB_TAGGED | GC_SPMM_SHRINK_MASK)) == 0, GC_ERR_VALUE,
+             "gc_gat_sddmm_aggregate_f32: unknown flags 0x%x", flags);
+  GC_REQUIRE(slope > 0.0f && slope < 1.0f, GC_ERR_VALUE,
+             "gc_gat_sddmm_aggregate_f32: leaky_slope must lie in (0, 1)");
+  if (n_rows == 0) return GC_OK;
+  GC_REQUIRE(row_ptr && C && B && a_src && a_dst, GC_ERR_VALUE,
+             "gc_gat_sddmm_aggregate_f32: null operand");
+  GC_REQUIRE(n_rows < INT32_MAX, GC_ERR_SHAPE, "gc_gat_sddmm_aggregate_f32: int32 range");
+  SpmmArgs a{};
+  a.row_ptr = row_ptr;
+  a.col_idx = col_idx;
+  a.B = B;
+  a.ldb = ldb;
+  a.K = K;
+  a.C = C;
+  a.ldc = ldc;
+  a.flags = flags;
+  a.hints = (flags & GC_HUB_TAGGED) != 0;
+  a.a_src = a_src;
+  a.a_dst = a_dst;
+  a.slope = slope;
+  return dispatch<2>(a, n_rows, algo, items, n_items, split_rows, n_split_rows, workspace,
+                     ws_bytes, stream, "gc_gat_sddmm_aggregate_f32");
 }
 
 extern "C" int gc_gat_aggregate_f32(const int32_t *row_ptr, const int32_t *col_idx,
@@ -496,6 +599,6 @@ extern "C" int gc_gat_aggregate_f32(const int32_t *row_ptr, const int32_t *col_i
   a.s = s;
   a.t = t;
   a.slope = slope;
-  return dispatch<true>(a, n_rows, algo, items, n_items, split_rows, n_split_rows, workspace,
+  return dispatch<1>(a, n_rows, algo, items, n_items, split_rows, n_split_rows, workspace,
                         ws_bytes, stream, "gc_gat_aggregate_f32");
 }

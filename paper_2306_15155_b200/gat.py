@@ -38,6 +38,7 @@ import torch
 from . import _native as nat
 from .sparse import (
     CsrMatrix,
+    gat_sddmm_aggregate,
     ShapeError,
     _Operand,
     _ld,
@@ -220,6 +221,16 @@ def gat_layer_reuse(a_tilde: CsrMatrix, h, spec: GatLayerSpec, *, spmm_fn=None):
         return op.wrap(relu_(out) if relu else out)
     out = torch.empty(a_tilde.n_rows, k2 * H, dtype=torch.float32, device=hw.device)
     if spec.attention is AttentionForm.SDDMM:
+        if a_tilde.n_rows == a_tilde.n_cols:
+            # fused: the gathered HW_j row gives its score and its aggregated term
+            a_src, a_dst = spec.attn_src.to(hw.device), spec.attn_dst.to(hw.device)
+            done = all(gat_sddmm_aggregate(a_tilde, a_src[i * k2:(i + 1) * k2],
+                                           a_dst[i * k2:(i + 1) * k2], spec.leaky_slope,
+                                           hw[:, i * k2:(i + 1) * k2], relu=relu,
+                                           out=out[:, i * k2:(i + 1) * k2]) is not None
+                       for i in range(H))
+            if done:
+                return op.wrap(out)
         att = atten_calc(a_tilde, hw, spec)
         for i in range(H):
             spmm(att.head(i), hw[:, i * k2:(i + 1) * k2], relu=relu, out=out[:, i * k2:(i + 1) * k2])

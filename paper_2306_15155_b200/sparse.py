@@ -484,6 +484,47 @@ def _variant(a: CsrMatrix, K: int, mode: str, probe) -> tuple[bool, int]:
     return a._plans[key]
 
 
+def gat_sddmm_aggregate(a: CsrMatrix, a_src: torch.Tensor, a_dst: torch.Tensor, slope: float, b,
+                        *, relu: bool = False, out=None, algo: str = "auto"):
+    """GAT reuse aggregation with SDDMM attention fused in: per edge the
+    gathered row B_j gives both e = LeakyReLU(a_src.B_i + a_dst.B_j) and the
+    aggregated term (one gather per edge; α never written).  Returns None when
+    the operand shape is outside the kernel's range (K > 256, unaligned)."""
+    dev = a.device
+    bt = b
+    K = bt.shape[1]
+    if a.n_rows != a.n_cols or bt.shape[0] != a.n_rows:
+        raise ShapeError("gat_sddmm_aggregate: square pattern and one B row per node required")
+    if (K > 256 or K % 4 or _ld(bt) % 4 or bt.data_ptr() % 16 or a_src.data_ptr() % 16
+            or a_dst.data_ptr() % 16):
+        return None
+    _require_cuda(a.col_idx, bt, a_src, a_dst)
+    if out is None:
+        out = torch.empty(a.n_rows, K, dtype=torch.float32, device=dev)
+    if _ld(out) % 4 or out.data_ptr() % 16:
+        return None
+    code, items, n_items, split, n_split, ws = _plan_args(a, K, algo, dev, gat=True)
+    lib = nat.load()
+    flags = nat.GC_RELU if relu else 0
+
+    def launch(cols, extra):
+        return lib.gc_gat_sddmm_aggregate_f32(
+            a.row_ptr.data_ptr(), cols.data_ptr(), a_src.data_ptr(), a_dst.data_ptr(), float(slope),
+            bt.data_ptr(), _ld(bt), a.n_rows, K, out.data_ptr(), _ld(out), flags | extra, code,
+            _ptr(items), n_items, _ptr(split), n_split, _ptr(ws), 0 if ws is None else ws.numel() * 4,
+            _stream(dev))
+
+    def probe(cols, extra):
+        nat.check(launch(cols, extra), "gat_sddmm_aggregate")
+
+    hints, shrink = _variant(a, K, "gatsd", probe)
+    cols = a.hub_tagged_cols(K) if hints else a.col_idx
+    extra = (nat.GC_HUB_TAGGED if hints else 0) | nat.GC_SPMM_SHRINK(shrink)
+    rc = _timed_call("spmm", dev, lambda: launch(cols, extra))
+    nat.check(rc, "gat_sddmm_aggregate")
+    return out
+
+
 def _spmm(a: CsrMatrix, b, *, weighted: bool, d_row=None, d_col=None, relu=False, out=None,
           accumulate=False, algo: str = "auto", what="spmm"):
     dev = a.device

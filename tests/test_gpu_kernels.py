@@ -456,3 +456,35 @@ def test_variant_autotune_caches_a_choice(monkeypatch):
     r1 = gc.spmm(a, b)
     assert ("variant", "spmm", 64) in a._plans
     assert torch.equal(gc.spmm(a, b), r1)  # cached variant, deterministic
+
+
+@pytest.mark.parametrize("K", [4, 16, 64, 256])
+@pytest.mark.parametrize("algo", ["row", "split"])
+@pytest.mark.parametrize("shrink", ["0", "2"])
+def test_fused_sddmm_attention_aggregate(oracle, plgraph, K, algo, shrink, monkeypatch):
+    """gc_gat_sddmm_aggregate_f32 == SDDMM-form attention (gat.py:98-114) then
+    spmm(alpha, HW) (gat.py:127)."""
+    if algo == "split":
+        monkeypatch.setattr(sparse, "SPLIT_CHUNK", 16)
+    monkeypatch.setattr(sparse, "SPMM_SHRINK", shrink)
+    rng = np.random.default_rng(K + 7)
+    n = plgraph.n_rows
+    hw = f32(rng.uniform(-1, 1, (n, K)))
+    a_s, a_d = f32(rng.uniform(-0.5, 0.5, K)), f32(rng.uniform(-0.5, 0.5, K))
+    dev = lambda x: torch.from_numpy(x).to(DEV)  # noqa: E731
+    for relu in (False, True):
+        out = sparse.gat_sddmm_aggregate(plgraph, dev(a_s), dev(a_d), 0.2, dev(hw), relu=relu,
+                                         algo=algo)
+        assert out is not None
+        oa = to_oracle(oracle, plgraph)
+        alpha = oracle.atten_calc(oa, hw, a_s, a_d, 0.2)
+        ref = oracle.spmm(alpha, hw)
+        if relu:
+            ref = np.maximum(ref, 0)
+        assert oracle.rel_err(out.cpu().numpy(), ref) < 2e-5, (K, algo, relu)
+
+
+def test_fused_sddmm_attention_falls_back_outside_range(plgraph):
+    hw = torch.rand(plgraph.n_rows, 6, device=DEV)
+    assert sparse.gat_sddmm_aggregate(plgraph, torch.rand(8, device=DEV)[:6],
+                                      torch.rand(8, device=DEV)[:6], 0.2, hw) is None
