@@ -144,7 +144,9 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
   constexpr bool SD = MODE == 2;
   constexpr int GPB = kThreads / LPR;
   // edges unrolled per step: ~8 independent 16-byte gathers in flight per lane
-  constexpr int U = NV >= 8 ? 1 : NV >= 4 ? 2 : NV >= 2 ? 4 : (LPR < 8 ? LPR : 8);
+  // (never more than LPR: the edge batch is shuffled within the lane group)
+  constexpr int U0 = NV >= 8 ? 1 : NV >= 4 ? 2 : NV >= 2 ? 4 : 8;
+  constexpr int U = U0 < LPR ? U0 : LPR;
   const int g = threadIdx.x / LPR;
   const int gl = threadIdx.x % LPR;
   const int64_t item = (int64_t)blockIdx.x * GPB + g;
