@@ -702,6 +702,14 @@ def gemm(a, b, *, row_scale=None, relu=False, precision: str | None = None, out=
     flags = nat.GC_RELU if relu else 0
     lib = nat.load()
     ws = None
+    if prec == "tf32" and K >= 8 and (_ld(at) % 4 or at.data_ptr() % 16) and M * K <= (1 << 28):
+        # TMA needs 16-byte row pitch: stage A with a padded leading dimension
+        # (e.g. Cora's k1 = 1433 -> 1436) through the row-copy kernel
+        ldp = (K + 3) // 4 * 4
+        ap = torch.empty(M, ldp, dtype=torch.float32, device=dev)
+        nat.check(lib.gc_scale_rows_f32(None, at.data_ptr(), _ld(at), M, K, ap.data_ptr(), ldp, 0,
+                                        _stream(dev)), "gemm(pad)")
+        at = ap[:, :K]
     if prec == "tf32" and (_ld(at) % 4 == 0) and at.data_ptr() % 16 == 0 and K > 0:
         flags |= nat.GC_GEMM_TF32
         ws = torch.empty(max(int(lib.gc_gemm_workspace_bytes(K, N)), 16), dtype=torch.uint8,
