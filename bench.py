@@ -82,8 +82,10 @@ def peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the
-    timed region (the profiling recipe's clocks line)."""
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms around and
+    during the timed region (the profiling recipe's clocks line).  The first
+    sample is taken before the region starts and one more after it ends, so a
+    region shorter than the sampling period is still bracketed."""
 
     Q = ("index,clocks.sm,clocks.max.sm,utilization.gpu,power.draw,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -92,26 +94,36 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.lines: list[str] = []
+        self.lines: list[tuple[float, str]] = []
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            deadline = time.time() + 3.0
+            while not self.lines and time.time() < deadline:
+                time.sleep(0.01)
         except (FileNotFoundError, OSError):
             self.proc = None
+        self.t0 = time.time()
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
     def __exit__(self, *exc):
+        self.t1 = time.time()
         if self.proc is not None:
+            n = len(self.lines)
+            deadline = time.time() + 1.0
+            while len(self.lines) <= n and time.time() < deadline:
+                time.sleep(0.01)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -120,21 +132,30 @@ class ClockSampler:
 
     def summary(self) -> dict:
         rows = []
-        for ln in self.lines:
+        inside = 0
+        for ts, ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
             try:
-                rows.append((float(f[1]), float(f[2]), float(f[3]), f[5:9]))
+                rows.append((float(f[1]), float(f[2]), float(f[3]), f[5:9], ts))
             except ValueError:
                 continue
+            if self.t0 is not None and self.t1 is not None and self.t0 <= ts <= self.t1:
+                inside += 1
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        load = [r for r in rows if r[2] >= 50] or rows
+        # samples inside the region plus the ones bracketing it
+        lo = max([r for r in rows if r[4] < (self.t0 or 0)], key=lambda r: r[4], default=None)
+        hi = min([r for r in rows if r[4] > (self.t1 or 0)], key=lambda r: r[4], default=None)
+        win = [r for r in rows if self.t0 <= r[4] <= self.t1] + [r for r in (lo, hi) if r is not None]
+        win = win or rows
+        load = [r for r in win if r[2] >= 50] or win
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
         reasons = sorted({names[i] for r in load for i, v in enumerate(r[3]) if v == "Active"})
         return {"sm_mhz": float(np.median([r[0] for r in load])), "sm_max_mhz": rows[0][1],
-                "reasons": reasons, "samples": len(rows), "samples_under_load": len(load)}
+                "reasons": reasons, "samples": len(win), "samples_inside_region": inside,
+                "samples_under_load": len(load), "interval_ms": 50}
 
 
 def spmm_alg_bytes(n_rows: int, m: int, K: int, weighted: bool, dcol: bool, drow: bool) -> int:

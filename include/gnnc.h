@@ -138,7 +138,7 @@ GNNC_API int gc_tag_hub_columns(const int32_t *col_idx, int64_t nnz, const uint8
  * alpha = row softmax, C[i,:] = epi(sum_p alpha_p B[j,:]).  Each gathered row
  * B[j,:] feeds both its score and the aggregation (one gather per edge); the
  * reuse composition (B = HW, gat.py:121-129).  Needs a square pattern,
- * K % 4 == 0, K <= 256, 16-byte aligned B/C/a_src/a_dst (else
+ * K % 4 == 0, K <= 1024, 16-byte aligned B/C/a_src/a_dst (else
  * GC_ERR_UNSUPPORTED).  Plan/workspace protocol as gc_gat_aggregate_f32. */
 GNNC_API int gc_gat_sddmm_aggregate_f32(const int32_t *row_ptr, const int32_t *col_idx,
                                         const float *a_src, const float *a_dst, float slope,

@@ -447,9 +447,13 @@ int dispatch(SpmmArgs &a, int64_t n_rows, int algo, const int32_t *items, int64_
   const int64_t K = a.K;
   const bool vec = (K % 4 == 0) && (a.ldb % 4 == 0) && (a.ldc % 4 == 0) && aligned16(a.B) &&
                    aligned16(a.C) && (a.partial == nullptr || aligned16(a.partial));
-  if (MODE == 2) {
-    GC_REQUIRE(vec && K <= 256 && aligned16(a.a_src) && aligned16(a.a_dst), GC_ERR_UNSUPPORTED,
-               "%s: needs K %% 4 == 0, K <= 256 and 16-byte aligned operands", who);
+  if constexpr (MODE == 2) {
+    GC_REQUIRE(vec && K <= 1024 && aligned16(a.a_src) && aligned16(a.a_dst), GC_ERR_UNSUPPORTED,
+               "%s: needs K %% 4 == 0, K <= 1024 and 16-byte aligned operands", who);
+    // the score needs the whole gathered row in one pass: wide rows get
+    // 4 or 8 float4 slots per lane
+    if (K > 512) return launch_cfg<32, 8, true, MODE>(a, sr, n_split, cudaStream_t(stream));
+    if (K > 256) return launch_cfg<32, 4, true, MODE>(a, sr, n_split, cudaStream_t(stream));
   }
   cudaStream_t st = as_stream(stream);
   if (vec) {

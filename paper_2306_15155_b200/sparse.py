@@ -439,7 +439,9 @@ def _plan_args(a: CsrMatrix, K: int, algo: str, dev, gat: bool = False):
 SPMM_SHRINK = os.environ.get("GNNC_SPMM_SHRINK", "auto")  # lane-group variant: auto | 0 | 1 | 2
 
 
-def _shrink_candidates(K: int) -> list[int]:
+def _shrink_candidates(K: int, mode: str = "spmm") -> list[int]:
+    if mode == "gatsd" and K > 256:
+        return [0]  # one wide lane-group shape only (whole row per pass)
     return [0] if K <= 8 else ([0, 1] if K <= 16 else [0, 1, 2])
 
 
@@ -455,7 +457,7 @@ def _variant(a: CsrMatrix, K: int, mode: str, probe) -> tuple[bool, int]:
     if a.nnz < PLAN_MIN_NNZ:
         return False, 0
     hints = [False, True] if hint_mode == "auto" else [hint_mode == "1"]
-    shrinks = _shrink_candidates(K) if shrink_mode == "auto" else [int(shrink_mode)]
+    shrinks = _shrink_candidates(K, mode) if shrink_mode == "auto" else [int(shrink_mode)]
     if len(hints) * len(shrinks) == 1:
         return hints[0], shrinks[0]
     if a.nnz < HUB_AUTOTUNE_MIN_NNZ:
@@ -495,7 +497,7 @@ def gat_sddmm_aggregate(a: CsrMatrix, a_src: torch.Tensor, a_dst: torch.Tensor, 
     K = bt.shape[1]
     if a.n_rows != a.n_cols or bt.shape[0] != a.n_rows:
         raise ShapeError("gat_sddmm_aggregate: square pattern and one B row per node required")
-    if (K > 256 or K % 4 or _ld(bt) % 4 or bt.data_ptr() % 16 or a_src.data_ptr() % 16
+    if (K > 1024 or K % 4 or _ld(bt) % 4 or bt.data_ptr() % 16 or a_src.data_ptr() % 16
             or a_dst.data_ptr() % 16):
         return None
     _require_cuda(a.col_idx, bt, a_src, a_dst)
