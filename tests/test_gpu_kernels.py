@@ -493,3 +493,14 @@ def test_fused_sddmm_attention_falls_back_outside_range(plgraph):
     hw = torch.rand(plgraph.n_rows, 1028, device=DEV)
     assert sparse.gat_sddmm_aggregate(plgraph, torch.rand(1028, device=DEV),
                                       torch.rand(1028, device=DEV), 0.2, hw) is None
+
+
+def test_reference_side_binding(oracle, plgraph):
+    """INTEGRATION.md's reference-side ctypes stub, fed a reference-style CSR."""
+    from paper_2306_15155_b200.refbind import b200_spmm
+
+    oa = to_oracle(oracle, plgraph.with_values(torch.rand(plgraph.nnz, device=DEV)))
+    b = np.random.default_rng(5).standard_normal((oa.n_cols, 24))
+    out = b200_spmm(oa, b)
+    assert out.dtype == np.float64
+    assert oracle.rel_err(out, oracle.spmm(oa, b.astype(np.float32))) < SP_TOL
