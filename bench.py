@@ -364,7 +364,7 @@ def main():
         ach = spmm_bytes / (spmm_ms * 1e-3) / 1e9
         traffic = None
         tf = ROOT / "profiles" / "traffic.json"
-        if tf.exists():
+        if tf.exists() and world == 1:
             traffic = json.loads(tf.read_text()).get(f"{args.shape}/K{K}/{comp}")
             traffic = traffic if isinstance(traffic, int) else None
         roof = {"kernel": "spmm_kernel", "bound": "hbm", "achieved": round(ach, 1),
