@@ -166,17 +166,22 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
   constexpr int64_t kColsPerPass = (int64_t)LPR * NV * Lanes<VEC>::W;
   const int64_t c0 = (int64_t)blockIdx.y * kColsPerPass;
 
+  // column slots of this lane (32-bit: K is a feature width, far below 2^31)
   bool colok[NV];
-  int64_t coff[NV];
+  int coff[NV];
+  const int kcols = (int)a.K;
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
-    coff[v] = col_of<LPR, NV, VEC>(c0, v, gl);
-    colok[v] = coff[v] < a.K;
+    coff[v] = (int)col_of<LPR, NV, VEC>(c0, v, gl);
+    colok[v] = coff[v] < kcols;
   }
 
   T acc[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) acc[v] = zero_of(T{});
+  constexpr int kSlotStride = LPR * Lanes<VEC>::W;  // floats between a lane's column slots
+  const char *bbase = reinterpret_cast<const char *>(a.B + coff[0]);
+  const uint32_t ldb_bytes = (uint32_t)(a.ldb * 4);
 
   const int len = end - beg;
   const int wmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)len);
@@ -253,20 +258,24 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
     const int cntw = min(LPR, wmax - base);
 #pragma unroll 1
     for (int e0 = 0; e0 < cntw; e0 += U) {
+      // bv slots of edges past the row end (or columns past K) are never
+      // loaded and never consumed: loads and FMAs share one predicate.
+      // Row address = lane base + je * ldb (one 32x32->64 IMAD.WIDE per
+      // edge); the NV slots of a row sit at compile-time offsets.
       T bv[U][NV];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int je = __shfl_sync(0xffffffffu, j, e0 + u, LPR);
         const bool ok = (e0 + u) < cnt;
-        const float *brow = a.B + (int64_t)je * a.ldb;
+        const float *brow = reinterpret_cast<const float *>(
+            bbase + (uint64_t)(uint32_t)je * ldb_bytes);
         bool hote = false;
         if (HINT) hote = __shfl_sync(0xffffffffu, (int)hot, e0 + u, LPR) != 0;
 #pragma unroll
         for (int vv = 0; vv < NV; ++vv) {
-          bv[u][vv] = zero_of(T{});
           if (ok && colok[vv]) {
-            if (HINT) load_b_hint(bv[u][vv], brow + coff[vv], hote);
-            else load_b(bv[u][vv], brow + coff[vv]);
+            if (HINT) load_b_hint(bv[u][vv], brow + vv * kSlotStride, hote);
+            else load_b(bv[u][vv], brow + vv * kSlotStride);
           }
         }
       }
@@ -278,7 +287,8 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
         for (int u = 0; u < U; ++u) {
           float part = 0.0f;
 #pragma unroll
-          for (int vv = 0; vv < NV; ++vv) part += dot_of(bv[u][vv], adst[vv]);
+          for (int vv = 0; vv < NV; ++vv)
+            if ((e0 + u) < cnt && colok[vv]) part += dot_of(bv[u][vv], adst[vv]);
           part = group_sum<LPR>(part);
           eu[u] = (e0 + u) < cnt ? leaky(si + part, a.slope) : -INFINITY;
         }
@@ -295,17 +305,22 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
             const float w = __expf(eu[u] - m);
             zl += w;
 #pragma unroll
-            for (int vv = 0; vv < NV; ++vv) fma_into(acc[vv], w, bv[u][vv]);
+            for (int vv = 0; vv < NV; ++vv)
+              if (colok[vv]) fma_into(acc[vv], w, bv[u][vv]);
           }
         }
       } else {
+        // unit weights (value-blind, no d_j): no weight shuffle; fma(1, b, acc)
+        // rounds exactly like the weighted kernel with unit values
+        constexpr bool UNIT = !HAS_VAL && !HAS_DCOL && MODE == 0;
         const float w = mine ? v * dj : 0.0f;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const float we = __shfl_sync(0xffffffffu, w, e0 + u, LPR);
+          const float we = UNIT ? 1.0f : __shfl_sync(0xffffffffu, w, e0 + u, LPR);
           if ((e0 + u) < cnt) {
 #pragma unroll
-            for (int vv = 0; vv < NV; ++vv) fma_into(acc[vv], we, bv[u][vv]);
+            for (int vv = 0; vv < NV; ++vv)
+              if (colok[vv]) fma_into(acc[vv], we, bv[u][vv]);
           }
         }
       }
@@ -444,6 +459,7 @@ int dispatch(SpmmArgs &a, int64_t n_rows, int algo, const int32_t *items, int64_
     set_error("%s: unknown algo %d", who, algo);
     return GC_ERR_VALUE;
   }
+  GC_REQUIRE(a.ldb < (int64_t(1) << 30), GC_ERR_SHAPE, "%s: leading dimension too large", who);
   const int64_t K = a.K;
   const bool vec = (K % 4 == 0) && (a.ldb % 4 == 0) && (a.ldc % 4 == 0) && aligned16(a.B) &&
                    aligned16(a.C) && (a.partial == nullptr || aligned16(a.partial));
