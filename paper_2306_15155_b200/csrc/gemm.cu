@@ -13,6 +13,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstring>
 #include <mutex>
 
 #include "common.cuh"
@@ -63,6 +64,28 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
       : "memory");
+}
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, uint32_t src, int32_t c0,
+                                             int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(src), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 __device__ __forceinline__ void tc_fence_before() {
@@ -149,8 +172,9 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 template <int BN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tf32_tcgen05(const __grid_constant__ CUtensorMap map_a,
-                      const __grid_constant__ CUtensorMap map_b, const GemmEpi ep, int num_kb,
-                      int stages, int m_tiles, int n_tiles) {
+                      const __grid_constant__ CUtensorMap map_b,
+                      const __grid_constant__ CUtensorMap map_c, const GemmEpi ep, int num_kb,
+                      int stages, int m_tiles, int n_tiles, int tma_store) {
   constexpr uint32_t A_BYTES = BM * BK * 4;
   constexpr uint32_t B_BYTES = BN * BK * 4;
   constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
@@ -166,6 +190,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   auto tfull_bar = [&](int b) { return bar0 + 8u * (2 * stages + b); };
   auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * stages + 2 + b); };
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + (bar0 - base) + 8u * (2 * stages + 4));
+  // epilogue staging: per epilogue warp 2 x (32 rows x 16 fp32) boxes, 64-B swizzled
+  const uint32_t stage_c = (bar0 + 8u * (2 * stages + 4) + 16u + 1023u) & ~1023u;
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -244,7 +270,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const bool relu = (ep.flags & GC_RELU) != 0;
     const bool vec = ((ep.ldc & 3) == 0) && aligned16(ep.C);
-    int lt = 0;
+    const uint32_t my_stage = stage_c + (uint32_t)(warp - 2) * 2u * 2048u;
+    int lt = 0, sbuf = 0;
     for (int tile = blockIdx.x; tile < n_tiles_total; tile += gridDim.x, ++lt) {
       const int acc = lt & 1;
       const int m0 = (tile / n_tiles) * BM, n0 = (tile % n_tiles) * BN;
@@ -265,6 +292,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           v[i] *= rs;
           if (relu) v[i] = fmaxf(v[i], 0.0f);
         }
+        if (tma_store) {
+          // row `lane` of a 32 x 16 box: four 16-B chunks, 64-B swizzle
+          // (chunk ^ ((row >> 1) & 3)) -> conflict-free st.shared.v4
+          const uint32_t buf = my_stage + (uint32_t)sbuf * 2048u;
+          if (lane == 0) bulk_wait_read<1>();  // this buffer's previous store has been read
+          __syncwarp();
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            const uint32_t dst = buf + (uint32_t)lane * 64u + (uint32_t)((ch ^ ((lane >> 1) & 3)) * 16);
+            asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(dst), "f"(v[4 * ch]),
+                         "f"(v[4 * ch + 1]), "f"(v[4 * ch + 2]), "f"(v[4 * ch + 3])
+                         : "memory");
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&map_c, buf, n0 + c, m0 + q * 32);  // TMA clips rows >= M, cols >= N
+            bulk_commit();
+          }
+          sbuf ^= 1;
+          continue;
+        }
         if (!row_ok) continue;
         const int64_t col = n0 + c;
         if (vec && col + 16 <= ep.N) {
@@ -281,6 +330,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty_bar(acc));
     }
+    if (tma_store && lane == 0) bulk_wait_all();  // stores complete before the CTA exits
   }
   tc_fence_before();
   __syncthreads();
@@ -414,7 +464,8 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 // 2-D fp32 row-major matrix (rows x cols, ld elements) as a K-major TMA map
 // with a (BK x box_rows) box and 128-byte swizzle; OOB elements read as 0.
 int make_map(CUtensorMap *map, const float *ptr, int64_t rows, int64_t cols, int64_t ld,
-             int box_rows) {
+             int box_rows, int box_cols = BK,
+             CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto enc = get_encode_fn();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -422,10 +473,10 @@ int make_map(CUtensorMap *map, const float *ptr, int64_t rows, int64_t cols, int
   }
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
-  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims,
-                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -435,14 +486,16 @@ int make_map(CUtensorMap *map, const float *ptr, int64_t rows, int64_t cols, int
 }
 
 template <int BN>
-int launch_tf32(const CUtensorMap &ma, const CUtensorMap &mb, const GemmEpi &ep, int64_t K,
-                cudaStream_t st) {
+int launch_tf32(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mc, int tma_store,
+                const GemmEpi &ep, int64_t K, cudaStream_t st) {
   const int num_kb = (int)((K + BK - 1) / BK);
   constexpr int stage_bytes = BM * BK * 4 + BN * BK * 4;
-  // deepest ring that fits next to the barriers (<= 8 stages, <= ~200 KB)
-  int stages = (200 * 1024) / stage_bytes;
+  // deepest ring that fits next to the barriers and the 16 KB epilogue
+  // staging (<= 8 stages, ring <= ~190 KB)
+  int stages = (190 * 1024) / stage_bytes;
   stages = stages > 8 ? 8 : (stages < 2 ? 2 : stages);
-  const size_t smem = (size_t)stages * stage_bytes + 8 * (2 * stages + 4) + 16 + 1024;
+  const size_t smem = (((size_t)stages * stage_bytes + 8 * (2 * stages + 4) + 16 + 1023) & ~(size_t)1023) +
+                      4 * 2 * 2048 + 1024;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
@@ -457,8 +510,8 @@ int launch_tf32(const CUtensorMap &ma, const CUtensorMap &mb, const GemmEpi &ep,
   const int n_tiles = (int)((ep.N + BN - 1) / BN);
   const int64_t tiles = (int64_t)m_tiles * n_tiles;
   const int grid = (int)(tiles < sm_count() ? tiles : sm_count());  // persistent: one CTA per SM
-  gemm_tf32_tcgen05<BN><<<grid, kGemmThreads, smem, st>>>(ma, mb, ep, num_kb, stages, m_tiles,
-                                                          n_tiles);
+  gemm_tf32_tcgen05<BN><<<grid, kGemmThreads, smem, st>>>(ma, mb, mc, ep, num_kb, stages, m_tiles,
+                                                          n_tiles, tma_store);
   return check_launch("gemm_tf32_tcgen05");
 }
 
@@ -519,17 +572,24 @@ extern "C" int gc_gemm_f32(const float *A, int64_t lda, const float *W, int64_t 
   else if (N <= 32) bn = 32;
   else if (N <= 64) bn = 64;
   else if (N <= 128) bn = 128;
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mc;
   int rc = make_map(&ma, A, M, K, lda, BM);
   if (rc) return rc;
   rc = make_map(&mb, wt, N, K, ldt, bn);
   if (rc) return rc;
+  // output through TMA stores when C's pitch allows it (16-B aligned rows)
+  int tma_store = ((ldc % 4) == 0 && aligned16(C)) ? 1 : 0;
+  memset(&mc, 0, sizeof(mc));
+  if (tma_store) {
+    rc = make_map(&mc, C, M, N, ldc, 32, 16, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (rc) return rc;
+  }
   switch (bn) {
-    case 16: return launch_tf32<16>(ma, mb, ep, K, st);
-    case 32: return launch_tf32<32>(ma, mb, ep, K, st);
-    case 64: return launch_tf32<64>(ma, mb, ep, K, st);
-    case 128: return launch_tf32<128>(ma, mb, ep, K, st);
-    default: return launch_tf32<256>(ma, mb, ep, K, st);
+    case 16: return launch_tf32<16>(ma, mb, mc, tma_store, ep, K, st);
+    case 32: return launch_tf32<32>(ma, mb, mc, tma_store, ep, K, st);
+    case 64: return launch_tf32<64>(ma, mb, mc, tma_store, ep, K, st);
+    case 128: return launch_tf32<128>(ma, mb, mc, tma_store, ep, K, st);
+    default: return launch_tf32<256>(ma, mb, mc, tma_store, ep, K, st);
   }
 }
 
