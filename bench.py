@@ -336,11 +336,15 @@ def main():
     launches0 = _native.launch_count()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks, sparse.kernel_timing("spmm", "gemm") as kt:
+        # cudaProfilerStart/Stop bracket the timed region so that
+        # `ncu --profile-from-start off` captures exactly its launches
+        torch.cuda.profiler.start()
         t_start.record()
         for _ in range(args.steps):
             out = step()
         t_end.record()
         torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
         barrier()
         torch.cuda.synchronize()
     launches = _native.launch_count() - launches0

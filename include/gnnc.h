@@ -193,17 +193,27 @@ GNNC_API int gc_node_proj_f32(const float *X, int64_t ld, int64_t n_rows, int64_
 /* Fused LeakyReLU + edge softmax over each CSR row (gat.py:72-95):
  *   e = s[h,i] + t[h,j]; e = e < 0 ? e * slope : e;
  *   alpha[h*nnz + p] = exp(e - max_row) / sum_row
- * Rows without edges produce nothing.  Requires a square pattern. */
+ * Rows without edges produce nothing.  Requires a square pattern.
+ * heavy_rows (optional, device int32[n_heavy]): the rows longer than
+ * gc_edge_softmax_heavy_threshold(n_rows, nnz) — each gets a whole CTA
+ * instead of a lane group, so power-law hub rows do not serialise the launch.
+ * NULL: every row goes to a lane group (same results). */
+GNNC_API int gc_edge_softmax_heavy_threshold(int64_t n_rows, int64_t nnz);
 GNNC_API int gc_edge_softmax_f32(const int32_t *row_ptr, const int32_t *col_idx, const float *s,
                         const float *t, int32_t heads, float slope, int64_t n_rows,
-                        int64_t nnz, float *alpha, void *stream);
+                        int64_t nnz, const int32_t *heavy_rows, int64_t n_heavy,
+                        float *alpha, void *stream);
 
 /* Attention as an SDDMM over edges: per edge
  *   e = a_src[h]·HW[i, h] + a_dst[h]·HW[j, h]   (k2-wide dot products),
- * then the same LeakyReLU + edge softmax as gc_edge_softmax_f32. */
+ * then the same LeakyReLU + edge softmax as gc_edge_softmax_f32 (same
+ * heavy_rows convention).  The a_dst·HW_j term is gathered per edge
+ * (edge-parallel, uniform chunks); the a_src·HW_i term is one dot per node,
+ * staged in the caller-owned s_work[heads * n_rows]. */
 GNNC_API int gc_attn_sddmm_f32(const int32_t *row_ptr, const int32_t *col_idx, const float *HW,
                       int64_t ld, int64_t k2, int32_t heads, const float *a_src,
                       const float *a_dst, float slope, int64_t n_rows, int64_t nnz,
+                      const int32_t *heavy_rows, int64_t n_heavy, float *s_work,
                       float *alpha, void *stream);
 
 /* ---- multi-GPU row partition -----------------

@@ -8,6 +8,8 @@
 // use a fixed shuffle tree, so results are deterministic.
 #include <math.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace gnnc {
@@ -39,18 +41,41 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// k = 1 normalisation: out[p] = a[p] * (d[i] * d[j])
-template <int LPR>
+// k = 1 normalisation: out[p] = a[p] * (d[i] * d[j]).  Edge-parallel: each
+// warp owns a fixed chunk of edges (uniform work on power-law graphs, whose
+// hub rows would otherwise serialise one warp each), finds the chunk's first
+// row by binary search in row_ptr, and each lane walks rows as it strides.
+__device__ __forceinline__ int64_t row_of_edge(const int32_t *__restrict__ row_ptr,
+                                               int64_t n_rows, int64_t p) {
+  int64_t lo = 0, hi = n_rows;  // last r with row_ptr[r] <= p (skips empty rows)
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)__ldg(row_ptr + mid) <= p) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
 __global__ void __launch_bounds__(kThreads)
     sddmm_norm_kernel(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col_idx,
                       const float *__restrict__ a_vals, const float *__restrict__ d,
-                      int64_t n_rows, float *__restrict__ out) {
-  const int64_t row = (int64_t)blockIdx.x * (kThreads / LPR) + threadIdx.x / LPR;
-  const int gl = threadIdx.x % LPR;
-  if (row >= n_rows) return;
-  const int beg = row_ptr[row], end = row_ptr[row + 1];
-  const float di = __ldg(d + row);
-  for (int p = beg + gl; p < end; p += LPR) {
+                      int64_t n_rows, int64_t nnz, int64_t chunk, float *__restrict__ out) {
+  const int64_t w = ((int64_t)blockIdx.x * kThreads + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  const int64_t p0 = w * chunk;
+  if (p0 >= nnz) return;
+  const int64_t p1 = min(nnz, p0 + chunk);
+  int64_t row = row_of_edge(row_ptr, n_rows, p0);  // warp-uniform search
+  int64_t rend = __ldg(row_ptr + row + 1);
+  int64_t p = p0 + lane;
+  while (p < p1 && p >= rend) rend = __ldg(row_ptr + (++row) + 1);
+  float di = __ldg(d + row);
+  for (; p < p1; p += 32) {
+    if (p >= rend) {
+      do rend = __ldg(row_ptr + (++row) + 1);
+      while (p >= rend);
+      di = __ldg(d + row);
+    }
     const float prod = di * __ldg(d + ldg_stream_i32(col_idx + p));
     out[p] = (a_vals ? ldg_stream_f32(a_vals + p) : 1.0f) * prod;
   }
@@ -90,7 +115,7 @@ __global__ void __launch_bounds__(kThreads)
     tt = group_sum<32>(tt);
     if (lane == 0) {
       s[(int64_t)h * n_rows + row] = ss;
-      t[(int64_t)h * n_rows + row] = tt;
+      if (t) t[(int64_t)h * n_rows + row] = tt;
     }
   }
 }
@@ -98,29 +123,111 @@ __global__ void __launch_bounds__(kThreads)
 // ---------------------------------------------------------------------------
 // fused LeakyReLU + edge softmax (reassociated attention), multi-head.
 // Pass 1: per-lane online (max, sum); group merge.  Pass 2: normalised write.
+// EGIVEN: the scores were staged in `alpha` by attn_score_kernel (SDDMM form)
+// and are normalised in place.
 // ---------------------------------------------------------------------------
-template <int LPR>
-__global__ void __launch_bounds__(kThreads)
-    edge_softmax_kernel(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col_idx,
-                        const float *__restrict__ s, const float *__restrict__ t, int heads,
-                        float slope, int64_t n_rows, int64_t nnz, float *__restrict__ alpha) {
-  const int64_t row = (int64_t)blockIdx.x * (kThreads / LPR) + threadIdx.x / LPR;
-  const int gl = threadIdx.x % LPR;
-  const bool live = row < n_rows;
-  const int beg = live ? row_ptr[row] : 0, end = live ? row_ptr[row + 1] : 0;
+// One heavy row per CTA (power-law hubs): kThreads lanes stride the row, the
+// (max, sum) pairs merge through a fixed shuffle tree and then across warps in
+// warp order, so the result stays deterministic.
+template <bool EGIVEN>
+__device__ __forceinline__ void softmax_row_cta(int64_t row, const int32_t *__restrict__ row_ptr,
+                                                const int32_t *__restrict__ col_idx,
+                                                const float *__restrict__ s,
+                                                const float *__restrict__ t, int heads,
+                                                float slope, int64_t n_rows, int64_t nnz,
+                                                float *__restrict__ alpha) {
+  __shared__ float red_m[kThreads / 32][kMaxHeads], red_z[kThreads / 32][kMaxHeads];
+  __shared__ float fin_m[kMaxHeads], fin_z[kMaxHeads];
+  const int beg = row_ptr[row], end = row_ptr[row + 1];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   float si[kMaxHeads], m[kMaxHeads], z[kMaxHeads];
 #pragma unroll
   for (int h = 0; h < kMaxHeads; ++h) {
-    si[h] = (live && h < heads) ? __ldg(s + (int64_t)h * n_rows + row) : 0.f;
+    si[h] = (!EGIVEN && h < heads) ? __ldg(s + (int64_t)h * n_rows + row) : 0.f;
+    m[h] = -INFINITY;
+    z[h] = 0.f;
+  }
+  for (int p = beg + threadIdx.x; p < end; p += kThreads) {
+    const int j = EGIVEN ? 0 : __ldg(col_idx + p);
+#pragma unroll
+    for (int h = 0; h < kMaxHeads; ++h) {
+      if (h >= heads) break;
+      const float e = EGIVEN ? alpha[(int64_t)h * nnz + p]
+                             : leaky(si[h] + __ldg(t + (int64_t)h * n_rows + j), slope);
+      if (e > m[h]) {
+        z[h] = z[h] * expf(m[h] - e) + 1.0f;
+        m[h] = e;
+      } else {
+        z[h] += expf(e - m[h]);
+      }
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < kMaxHeads; ++h) {
+    if (h >= heads) break;
+    const float mg = group_max<32>(m[h]);
+    const float zl = (m[h] == -INFINITY) ? 0.f : z[h] * expf(m[h] - mg);
+    const float zg = group_sum<32>(zl);
+    if (lane == 0) red_m[warp][h] = mg, red_z[warp][h] = zg;
+  }
+  __syncthreads();
+  if (threadIdx.x < heads) {
+    const int h = threadIdx.x;
+    float mm = -INFINITY;
+    for (int w = 0; w < kThreads / 32; ++w) mm = fmaxf(mm, red_m[w][h]);
+    float zz = 0.f;
+    for (int w = 0; w < kThreads / 32; ++w)
+      if (red_m[w][h] != -INFINITY) zz += red_z[w][h] * expf(red_m[w][h] - mm);
+    fin_m[h] = mm;
+    fin_z[h] = zz;
+  }
+  __syncthreads();
+  for (int p = beg + threadIdx.x; p < end; p += kThreads) {
+    const int j = EGIVEN ? 0 : __ldg(col_idx + p);
+#pragma unroll
+    for (int h = 0; h < kMaxHeads; ++h) {
+      if (h >= heads) break;
+      const float e = EGIVEN ? alpha[(int64_t)h * nnz + p]
+                             : leaky(si[h] + __ldg(t + (int64_t)h * n_rows + j), slope);
+      alpha[(int64_t)h * nnz + p] = expf(e - fin_m[h]) / fin_z[h];
+    }
+  }
+}
+
+// Blocks [0, n_heavy) take one heavy row each (rows longer than `th`, listed
+// by the caller); the remaining blocks give every other row a group of LPR
+// lanes.  Without a heavy list every row goes to the lane groups.
+template <int LPR, bool EGIVEN>
+__global__ void __launch_bounds__(kThreads)
+    edge_softmax_kernel(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col_idx,
+                        const float *__restrict__ s, const float *__restrict__ t, int heads,
+                        float slope, int64_t n_rows, int64_t nnz,
+                        const int32_t *__restrict__ heavy, int64_t n_heavy, int th,
+                        float *__restrict__ alpha) {
+  if ((int64_t)blockIdx.x < n_heavy) {
+    softmax_row_cta<EGIVEN>(heavy[blockIdx.x], row_ptr, col_idx, s, t, heads, slope, n_rows, nnz,
+                            alpha);
+    return;
+  }
+  const int64_t row = ((int64_t)blockIdx.x - n_heavy) * (kThreads / LPR) + threadIdx.x / LPR;
+  const int gl = threadIdx.x % LPR;
+  bool live = row < n_rows;
+  int beg = live ? row_ptr[row] : 0, end = live ? row_ptr[row + 1] : 0;
+  if (heavy && end - beg > th) live = false, beg = end = 0;  // owned by a CTA above
+  float si[kMaxHeads], m[kMaxHeads], z[kMaxHeads];
+#pragma unroll
+  for (int h = 0; h < kMaxHeads; ++h) {
+    si[h] = (!EGIVEN && live && h < heads) ? __ldg(s + (int64_t)h * n_rows + row) : 0.f;
     m[h] = -INFINITY;
     z[h] = 0.f;
   }
   for (int p = beg + gl; p < end; p += LPR) {
-    const int j = __ldg(col_idx + p);
+    const int j = EGIVEN ? 0 : __ldg(col_idx + p);
 #pragma unroll
     for (int h = 0; h < kMaxHeads; ++h) {
       if (h >= heads) break;
-      const float e = leaky(si[h] + __ldg(t + (int64_t)h * n_rows + j), slope);
+      const float e = EGIVEN ? alpha[(int64_t)h * nnz + p]
+                             : leaky(si[h] + __ldg(t + (int64_t)h * n_rows + j), slope);
       if (e > m[h]) {
         z[h] = z[h] * expf(m[h] - e) + 1.0f;
         m[h] = e;
@@ -139,93 +246,160 @@ __global__ void __launch_bounds__(kThreads)
   }
   if (!live || end == beg) return;
   for (int p = beg + gl; p < end; p += LPR) {
-    const int j = __ldg(col_idx + p);
+    const int j = EGIVEN ? 0 : __ldg(col_idx + p);
 #pragma unroll
     for (int h = 0; h < kMaxHeads; ++h) {
       if (h >= heads) break;
-      const float e = leaky(si[h] + __ldg(t + (int64_t)h * n_rows + j), slope);
+      const float e = EGIVEN ? alpha[(int64_t)h * nnz + p]
+                             : leaky(si[h] + __ldg(t + (int64_t)h * n_rows + j), slope);
       alpha[(int64_t)h * nnz + p] = expf(e - m[h]) / z[h];
     }
   }
 }
 
+// lanes per row and the heavy-row threshold, both from the mean degree
+// (exported as gc_edge_softmax_heavy_threshold so the caller can list the
+// heavy rows once per pattern)
+inline int softmax_lpr(int64_t n_rows, int64_t nnz) {
+  const double avg = (double)nnz / (double)(n_rows > 0 ? n_rows : 1);
+  return avg <= 12.0 ? 8 : avg <= 64.0 ? 16 : 32;
+}
+inline int softmax_th(int64_t n_rows, int64_t nnz) { return 16 * softmax_lpr(n_rows, nnz); }
+
+template <bool EGIVEN>
+int launch_softmax(const int32_t *row_ptr, const int32_t *col_idx, const float *s, const float *t,
+                   int heads, float slope, int64_t n_rows, int64_t nnz, const int32_t *heavy,
+                   int64_t n_heavy, float *alpha, cudaStream_t st) {
+  const int lpr = softmax_lpr(n_rows, nnz);
+  const int th = softmax_th(n_rows, nnz);
+  if (!heavy) n_heavy = 0;
+  const int64_t light = (n_rows + (kThreads / lpr) - 1) / (kThreads / lpr);
+  const int64_t blocks = light + n_heavy;
+  if (blocks >= INT32_MAX) {
+    set_error("edge softmax: row count %lld too large", (long long)n_rows);
+    return GC_ERR_SHAPE;
+  }
+  if (lpr == 8)
+    edge_softmax_kernel<8, EGIVEN><<<(unsigned)blocks, kThreads, 0, st>>>(
+        row_ptr, col_idx, s, t, heads, slope, n_rows, nnz, heavy, n_heavy, th, alpha);
+  else if (lpr == 16)
+    edge_softmax_kernel<16, EGIVEN><<<(unsigned)blocks, kThreads, 0, st>>>(
+        row_ptr, col_idx, s, t, heads, slope, n_rows, nnz, heavy, n_heavy, th, alpha);
+  else
+    edge_softmax_kernel<32, EGIVEN><<<(unsigned)blocks, kThreads, 0, st>>>(
+        row_ptr, col_idx, s, t, heads, slope, n_rows, nnz, heavy, n_heavy, th, alpha);
+  return check_launch("edge_softmax_kernel");
+}
+
 // ---------------------------------------------------------------------------
-// attention as an SDDMM over edges: e = a_src·HW_i + a_dst·HW_j per edge
-// (k2-wide dot products, warp per row, lanes across the k2 columns), then
-// the same LeakyReLU + softmax.  Raw scores are staged in `alpha`.
+// attention as an SDDMM over edges:
+//   e_p = LeakyReLU(a_src·HW_i + a_dst·HW_j)  for every edge p = (i, j),
+// the k2-wide target dot product gathered per edge (cost m·2k2), then the
+// same max-shifted row softmax as the reassociated form.
+// Stage 1 (attn_score_kernel) is edge-parallel: each lane group owns a fixed
+// chunk of edges (uniform work whatever the row lengths — power-law rows no
+// longer serialise one warp), finds its first row by binary search in
+// row_ptr and walks rows as the chunk advances; U edges are gathered at once.
+// The source term a_src·HW_i is one k2-wide dot per node (node_proj_kernel).
+// Stage 2 (edge_softmax_kernel<.., true>) normalises the staged scores in
+// place, row by row.
 // ---------------------------------------------------------------------------
-template <bool VEC>
+template <int LPR, int NV, int U, bool VEC>
 __global__ void __launch_bounds__(kThreads)
-    attn_sddmm_kernel(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col_idx,
+    attn_score_kernel(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col_idx,
                       const float *__restrict__ HW, int64_t ld, int64_t k2, int heads,
-                      const float *__restrict__ a_src, const float *__restrict__ a_dst,
-                      float slope, int64_t n_rows, int64_t nnz, float *__restrict__ alpha) {
-  const int64_t row = (int64_t)blockIdx.x * (kThreads / 32) + threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  if (row >= n_rows) return;
-  const int beg = row_ptr[row], end = row_ptr[row + 1];
-  if (beg == end) return;
-  const float *hi = HW + row * ld;
-  for (int h = 0; h < heads; ++h) {
-    const int64_t off = (int64_t)h * k2;
-    const float *al = a_src + off;
-    const float *ar = a_dst + off;
-    // per-row source term
-    float ss = 0.f;
-    if (VEC) {
-      for (int64_t c = 4 * lane; c < k2; c += 128) ss = fma4_dot(ldg_f4(hi + off + c), ldg_f4(al + c), ss);
-    } else {
-      for (int64_t c = lane; c < k2; c += 32) ss = fmaf(__ldg(hi + off + c), __ldg(al + c), ss);
-    }
-    ss = group_sum<32>(ss);
-    float m = -INFINITY, z = 0.f;
-    float *ah = alpha + (int64_t)h * nnz;
-    int p = beg;
-    // 4 edges per step keeps 4 independent row gathers in flight per lane
-    for (; p + 4 <= end; p += 4) {
-      float tt[4] = {0.f, 0.f, 0.f, 0.f};
-      const float *hj[4];
+                      const float *__restrict__ s, const float *__restrict__ a_dst, float slope,
+                      int64_t n_rows, int64_t nnz, int64_t chunk, float *__restrict__ e_out) {
+  // Edges are taken in batches of LPR: lane gl loads batch edge gl's column
+  // (coalesced) and walks its own row index forward; the next batch's
+  // columns are in flight while the current batch is gathered U edges at a
+  // time.  Lane gl owns column slots c0 + W*(gl + LPR*v), v < NV (W = 4
+  // floats when VEC), so all U*NV gathers of a step are issued before the
+  // first FMA and each per-edge dot is reduced over only LPR lanes.
+  constexpr int W = VEC ? 4 : 1;
+  constexpr int PASS = W * LPR * NV;
+  const int gl = threadIdx.x % LPR;
+  const int64_t grp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) / LPR;
+  const int64_t p0 = grp * chunk;
+  if (p0 >= nnz) return;  // group-uniform
+  const int64_t p1 = min(nnz, p0 + chunk);
+  int64_t row = row_of_edge(row_ptr, n_rows, p0);  // this lane's row, walked forward
+  int64_t rend = __ldg(row_ptr + row + 1);
+  int jc = (p0 + gl < p1) ? ldg_stream_i32(col_idx + p0 + gl) : 0;
+  for (int64_t b = p0; b < p1; b += LPR) {
+    const int jn = (b + LPR + gl < p1) ? ldg_stream_i32(col_idx + b + LPR + gl) : 0;
+    const int64_t pe = b + gl;
+    if (pe < p1)
+      while (pe >= rend) rend = __ldg(row_ptr + (++row) + 1);
+    const int rc = (int)row;
+    const int cnt = (int)min((int64_t)LPR, p1 - b);
+#pragma unroll 1
+    for (int e0 = 0; e0 < cnt; e0 += U) {
+      const float *hj[U];
+      int ru[U];
+      bool ok[U];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) hj[u] = HW + (int64_t)__ldg(col_idx + p + u) * ld + off;
-      if (VEC) {
-        for (int64_t c = 4 * lane; c < k2; c += 128) {
-          const float4 a = ldg_f4(ar + c);
+      for (int u = 0; u < U; ++u) {
+        const int src = (e0 + u) & (LPR - 1);
+        ok[u] = e0 + u < cnt;
+        hj[u] = HW + (int64_t)__shfl_sync(0xffffffffu, jc, src, LPR) * ld;
+        ru[u] = __shfl_sync(0xffffffffu, rc, src, LPR);
+      }
+      for (int h = 0; h < heads; ++h) {
+        const int64_t off = (int64_t)h * k2;
+        float tt[U];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) tt[u] = fma4_dot(ldg_f4(hj[u] + c), a, tt[u]);
+        for (int u = 0; u < U; ++u) tt[u] = 0.f;
+        for (int64_t c0 = 0; c0 < k2; c0 += PASS) {
+          if constexpr (VEC) {
+            float4 bv[U][NV], av[NV];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+              for (int v = 0; v < NV; ++v) {
+                const int64_t c = c0 + 4 * (gl + LPR * v);
+                bv[u][v] = (ok[u] && c < k2) ? ldg_f4(hj[u] + off + c)
+                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+              }
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+              const int64_t c = c0 + 4 * (gl + LPR * v);
+              av[v] = c < k2 ? ldg_f4(a_dst + off + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+              for (int v = 0; v < NV; ++v) tt[u] = fma4_dot(bv[u][v], av[v], tt[u]);
+          } else {
+            float bv[U][NV], av[NV];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+              for (int v = 0; v < NV; ++v) {
+                const int64_t c = c0 + gl + LPR * v;
+                bv[u][v] = (ok[u] && c < k2) ? __ldg(hj[u] + off + c) : 0.f;
+              }
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+              const int64_t c = c0 + gl + LPR * v;
+              av[v] = c < k2 ? __ldg(a_dst + off + c) : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+              for (int v = 0; v < NV; ++v) tt[u] = fmaf(bv[u][v], av[v], tt[u]);
+          }
         }
-      } else {
-        for (int64_t c = lane; c < k2; c += 32) {
-          const float a = __ldg(ar + c);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) tt[u] = fmaf(__ldg(hj[u] + c), a, tt[u]);
+        for (int u = 0; u < U; ++u) {
+          const float dot = group_sum<LPR>(tt[u]);
+          if (ok[u] && gl == 0)
+            e_out[(int64_t)h * nnz + b + e0 + u] =
+                leaky(__ldg(s + (int64_t)h * n_rows + ru[u]) + dot, slope);
         }
       }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float e = leaky(ss + group_sum<32>(tt[u]), slope);
-        if (lane == u) ah[p + u] = e;
-        const float mn = fmaxf(m, e);
-        z = z * expf(m - mn) + expf(e - mn);
-        m = mn;
-      }
     }
-    for (; p < end; ++p) {
-      const float *hj = HW + (int64_t)__ldg(col_idx + p) * ld + off;
-      float tt = 0.f;
-      if (VEC) {
-        for (int64_t c = 4 * lane; c < k2; c += 128) tt = fma4_dot(ldg_f4(hj + c), ldg_f4(ar + c), tt);
-      } else {
-        for (int64_t c = lane; c < k2; c += 32) tt = fmaf(__ldg(hj + c), __ldg(ar + c), tt);
-      }
-      const float e = leaky(ss + group_sum<32>(tt), slope);
-      if (lane == 0) ah[p] = e;
-      const float mn = fmaxf(m, e);
-      z = z * expf(m - mn) + expf(e - mn);
-      m = mn;
-    }
-    __syncwarp();
-    for (int q = beg + lane; q < end; q += 32) ah[q] = expf(ah[q] - m) / z;
-    __syncwarp();
+    jc = jn;
   }
 }
 
@@ -264,19 +438,17 @@ extern "C" int gc_sddmm_norm_f32(const int32_t *row_ptr, const int32_t *col_idx,
                                  const float *a_vals, const float *d, int64_t n_rows, int64_t nnz,
                                  float *out_vals, void *stream) {
   GC_REQUIRE(n_rows >= 0 && nnz >= 0, GC_ERR_SHAPE, "gc_sddmm_norm_f32: negative size");
-  if (n_rows == 0) return GC_OK;
-  GC_REQUIRE(row_ptr && d, GC_ERR_VALUE, "gc_sddmm_norm_f32: null operand");
-  // lanes per row follow the mean degree: short rows share a warp, long rows
-  // get the whole warp (the per-edge d_j gather is latency-bound otherwise)
-  const bool wide = nnz > 12 * n_rows;
-  unsigned grid;
-  cudaStream_t st = as_stream(stream);
-  int rc = rows_grid(n_rows, wide ? 32 : 8, &grid);
-  if (rc) return rc;
-  if (wide)
-    sddmm_norm_kernel<32><<<grid, kThreads, 0, st>>>(row_ptr, col_idx, a_vals, d, n_rows, out_vals);
-  else
-    sddmm_norm_kernel<8><<<grid, kThreads, 0, st>>>(row_ptr, col_idx, a_vals, d, n_rows, out_vals);
+  if (n_rows == 0 || nnz == 0) return GC_OK;
+  GC_REQUIRE(row_ptr && col_idx && d && out_vals, GC_ERR_VALUE, "gc_sddmm_norm_f32: null operand");
+  // ~8 resident waves of warps, >= 256 edges (8 per lane) per warp
+  const int64_t warps_target = (int64_t)sm_count() * 8 * (kThreads / 32);
+  int64_t chunk = std::max<int64_t>(256, (nnz + warps_target - 1) / warps_target);
+  chunk = (chunk + 31) / 32 * 32;
+  const int64_t warps = (nnz + chunk - 1) / chunk;
+  const int64_t blocks = (warps + (kThreads / 32) - 1) / (kThreads / 32);
+  GC_REQUIRE(blocks < INT32_MAX, GC_ERR_SHAPE, "gc_sddmm_norm_f32: too many edges");
+  sddmm_norm_kernel<<<(unsigned)blocks, kThreads, 0, as_stream(stream)>>>(
+      row_ptr, col_idx, a_vals, d, n_rows, nnz, chunk, out_vals);
   return check_launch("sddmm_norm_kernel");
 }
 
@@ -298,37 +470,31 @@ extern "C" int gc_node_proj_f32(const float *HW, int64_t ld, int64_t n_rows, int
   return check_launch("node_proj_kernel");
 }
 
+extern "C" int gc_edge_softmax_heavy_threshold(int64_t n_rows, int64_t nnz) {
+  return softmax_th(n_rows, nnz);
+}
+
 extern "C" int gc_edge_softmax_f32(const int32_t *row_ptr, const int32_t *col_idx, const float *s,
                                    const float *t, int32_t heads, float slope, int64_t n_rows,
-                                   int64_t nnz, float *alpha, void *stream) {
-  GC_REQUIRE(n_rows >= 0 && nnz >= 0, GC_ERR_SHAPE, "gc_edge_softmax_f32: bad shape");
+                                   int64_t nnz, const int32_t *heavy_rows, int64_t n_heavy,
+                                   float *alpha, void *stream) {
+  GC_REQUIRE(n_rows >= 0 && nnz >= 0 && n_heavy >= 0, GC_ERR_SHAPE,
+             "gc_edge_softmax_f32: bad shape");
   GC_REQUIRE(heads >= 1 && heads <= kMaxHeads, GC_ERR_VALUE,
              "gc_edge_softmax_f32: heads must be in [1, %d]", kMaxHeads);
   GC_REQUIRE(slope > 0.0f && slope < 1.0f, GC_ERR_VALUE,
              "gc_edge_softmax_f32: leaky_slope must lie in (0, 1)");
   if (n_rows == 0 || nnz == 0) return GC_OK;
-  GC_REQUIRE(row_ptr && col_idx && s && t && alpha, GC_ERR_VALUE,
+  GC_REQUIRE(row_ptr && col_idx && s && t && alpha && (n_heavy == 0 || heavy_rows), GC_ERR_VALUE,
              "gc_edge_softmax_f32: null operand");
-  cudaStream_t st = as_stream(stream);
-  unsigned grid;
-  const double avg = (double)nnz / (double)n_rows;
-  if (avg <= 12.0) {
-    int rc = rows_grid(n_rows, 8, &grid);
-    if (rc) return rc;
-    edge_softmax_kernel<8><<<grid, kThreads, 0, st>>>(row_ptr, col_idx, s, t, heads, slope,
-                                                      n_rows, nnz, alpha);
-  } else {
-    int rc = rows_grid(n_rows, 32, &grid);
-    if (rc) return rc;
-    edge_softmax_kernel<32><<<grid, kThreads, 0, st>>>(row_ptr, col_idx, s, t, heads, slope,
-                                                       n_rows, nnz, alpha);
-  }
-  return check_launch("edge_softmax_kernel");
+  return launch_softmax<false>(row_ptr, col_idx, s, t, heads, slope, n_rows, nnz, heavy_rows,
+                               n_heavy, alpha, as_stream(stream));
 }
 
 extern "C" int gc_attn_sddmm_f32(const int32_t *row_ptr, const int32_t *col_idx, const float *HW,
                                  int64_t ld, int64_t k2, int32_t heads, const float *a_src,
                                  const float *a_dst, float slope, int64_t n_rows, int64_t nnz,
+                                 const int32_t *heavy_rows, int64_t n_heavy, float *s_work,
                                  float *alpha, void *stream) {
   GC_REQUIRE(n_rows >= 0 && nnz >= 0 && k2 >= 1 && ld >= k2 * heads, GC_ERR_SHAPE,
              "gc_attn_sddmm_f32: bad shape");
@@ -337,19 +503,52 @@ extern "C" int gc_attn_sddmm_f32(const int32_t *row_ptr, const int32_t *col_idx,
   GC_REQUIRE(slope > 0.0f && slope < 1.0f, GC_ERR_VALUE,
              "gc_attn_sddmm_f32: leaky_slope must lie in (0, 1)");
   if (n_rows == 0 || nnz == 0) return GC_OK;
-  GC_REQUIRE(row_ptr && col_idx && HW && a_src && a_dst && alpha, GC_ERR_VALUE,
-             "gc_attn_sddmm_f32: null operand");
-  unsigned grid;
-  int rc = rows_grid(n_rows, 32, &grid);
-  if (rc) return rc;
+  GC_REQUIRE(row_ptr && col_idx && HW && a_src && a_dst && s_work && alpha &&
+                 n_heavy >= 0 && (n_heavy == 0 || heavy_rows),
+             GC_ERR_VALUE, "gc_attn_sddmm_f32: null operand");
   const bool vec = (k2 % 4 == 0) && (ld % 4 == 0) && aligned16(HW) && aligned16(a_src) &&
                    aligned16(a_dst);
   cudaStream_t st = as_stream(stream);
-  if (vec)
-    attn_sddmm_kernel<true><<<grid, kThreads, 0, st>>>(row_ptr, col_idx, HW, ld, k2, heads, a_src,
-                                                       a_dst, slope, n_rows, nnz, alpha);
-  else
-    attn_sddmm_kernel<false><<<grid, kThreads, 0, st>>>(row_ptr, col_idx, HW, ld, k2, heads,
-                                                        a_src, a_dst, slope, n_rows, nnz, alpha);
-  return check_launch("attn_sddmm_kernel");
+  // source term a_src·HW_i once per node
+  unsigned grid;
+  int rc = rows_grid(n_rows, 32, &grid);
+  if (rc) return rc;
+  node_proj_kernel<<<grid, kThreads, 0, st>>>(HW, ld, n_rows, k2, heads, k2, a_src, a_src, s_work,
+                                              nullptr, vec);
+  rc = check_launch("node_proj_kernel");
+  if (rc) return rc;
+  // edge-parallel target dot products: lane groups of 8 lanes (32 for rows
+  // wider than 256 floats), a fixed chunk of edges per group sized for ~8
+  // waves of 148 SMs
+  int lpr = 8, nv = 1, u = 8;
+  if (vec) {
+    if (k2 <= 32) nv = 1, u = 8;
+    else if (k2 <= 64) nv = 2, u = 8;
+    else if (k2 <= 128) nv = 4, u = 4;
+    else if (k2 <= 256) nv = 8, u = 2;
+    else lpr = 32, nv = 4, u = 2;  // 512 floats per pass
+  } else {
+    lpr = 32, nv = 2, u = 4;
+  }
+  const int64_t groups_per_block = kThreads / lpr;
+  const int64_t target_groups = (int64_t)sm_count() * 8 * groups_per_block;
+  int64_t chunk = std::max<int64_t>(64, (nnz + target_groups - 1) / target_groups);
+  chunk = (chunk + 7) / 8 * 8;
+  const int64_t n_groups = (nnz + chunk - 1) / chunk;
+  const int64_t blocks = (n_groups + groups_per_block - 1) / groups_per_block;
+  GC_REQUIRE(blocks < INT32_MAX, GC_ERR_SHAPE, "gc_attn_sddmm_f32: too many edges");
+#define GC_SCORE(L, N, UU, V)                                                           \
+  attn_score_kernel<L, N, UU, V><<<(unsigned)blocks, kThreads, 0, st>>>(                \
+      row_ptr, col_idx, HW, ld, k2, heads, s_work, a_dst, slope, n_rows, nnz, chunk, alpha)
+  if (!vec) GC_SCORE(32, 2, 4, false);
+  else if (lpr == 32) GC_SCORE(32, 4, 2, true);
+  else if (nv == 1) GC_SCORE(8, 1, 8, true);
+  else if (nv == 2) GC_SCORE(8, 2, 8, true);
+  else if (nv == 4) GC_SCORE(8, 4, 4, true);
+  else GC_SCORE(8, 8, 2, true);
+#undef GC_SCORE
+  rc = check_launch("attn_score_kernel");
+  if (rc) return rc;
+  return launch_softmax<true>(row_ptr, col_idx, nullptr, nullptr, heads, slope, n_rows, nnz,
+                              heavy_rows, n_heavy, alpha, st);
 }

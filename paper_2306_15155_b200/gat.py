@@ -149,10 +149,13 @@ def atten_calc(a_tilde: CsrMatrix, hw, spec: GatLayerSpec) -> AttentionMatrix:
     alpha = torch.empty(H, m, dtype=torch.float32, device=dev)
     lib = nat.load()
     st = _stream(dev)
+    heavy = a_tilde.softmax_heavy_rows()
     if spec.attention is AttentionForm.SDDMM:
+        s_work = torch.empty(H, n, dtype=torch.float32, device=dev)
         rc = lib.gc_attn_sddmm_f32(a_tilde.row_ptr.data_ptr(), a_tilde.col_idx.data_ptr(),
                                    hwt.data_ptr(), _ld(hwt), k2, H, a_src.data_ptr(),
                                    a_dst.data_ptr(), float(spec.leaky_slope), n, m,
+                                   heavy.data_ptr(), heavy.numel(), s_work.data_ptr(),
                                    alpha.data_ptr(), st)
         nat.check(rc, "attn_sddmm")
     else:
@@ -162,7 +165,8 @@ def atten_calc(a_tilde: CsrMatrix, hw, spec: GatLayerSpec) -> AttentionMatrix:
                                        a_dst.data_ptr(), s.data_ptr(), t.data_ptr(), st), "node_proj")
         nat.check(lib.gc_edge_softmax_f32(a_tilde.row_ptr.data_ptr(), a_tilde.col_idx.data_ptr(),
                                           s.data_ptr(), t.data_ptr(), H, float(spec.leaky_slope), n, m,
-                                          alpha.data_ptr(), st), "edge_softmax")
+                                          heavy.data_ptr(), heavy.numel(), alpha.data_ptr(), st),
+                  "edge_softmax")
     return AttentionMatrix(alpha=a_tilde.with_values(alpha[0]), values=alpha if H > 1 else None)
 
 

@@ -369,6 +369,16 @@ class CsrMatrix:
                                 torch.from_numpy(split[: int(nsr[0])]).to(self.device), int(ns[0]))
         return self._plans[key]
 
+    def softmax_heavy_rows(self) -> torch.Tensor:
+        """Rows longer than the edge-softmax lane-group threshold (int32, on the
+        device, cached per pattern): each gets a whole CTA in the softmax."""
+        key = ("softmax_heavy",)
+        if key not in self._plans:
+            th = nat.load().gc_edge_softmax_heavy_threshold(self.n_rows, self.nnz)
+            deg = self.row_ptr[1:] - self.row_ptr[:-1]
+            self._plans[key] = torch.nonzero(deg > th).flatten().to(torch.int32).contiguous()
+        return self._plans[key]
+
     def hub_tagged_cols(self, K: int, budget_bytes: int | None = None) -> torch.Tensor:
         """col_idx with the most-referenced columns tagged in bit 31, sized so
         the tagged rows of a K-wide operand fit one SM's L1 (cached)."""

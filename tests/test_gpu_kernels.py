@@ -232,6 +232,49 @@ def test_attention_matches_oracle(oracle, plgraph, k2, form):
     np.testing.assert_allclose(sums, 1.0, atol=1e-5)
 
 
+@pytest.fixture(scope="module")
+def hubgraph():
+    """Power-law graph plus two hub rows far above the softmax lane-group
+    threshold (and an empty-row-free Ã), so the CTA-per-heavy-row path runs."""
+    n = 3000
+    rng = np.random.default_rng(5)
+    src = [0] * (n - 1) + [7] * 1500 + list(rng.integers(0, n, 6000))
+    dst = list(range(1, n)) + list(rng.choice(np.arange(8, n), 1500, replace=False)) + \
+        list(rng.integers(0, n, 6000))
+    rows, cols = np.array(src + dst), np.array(dst + src)
+    keep = rows != cols
+    a = gc.CsrMatrix.from_coo(n, n, rows[keep], cols[keep], np.ones(int(keep.sum())), device=DEV)
+    a = gc.CsrMatrix(n, n, a.row_ptr, a.col_idx, torch.ones_like(a.values), device=DEV)
+    return gc.add_self_loops(a)
+
+
+@pytest.mark.parametrize("heads", [1, 3])
+@pytest.mark.parametrize("form", ["reassoc", "sddmm"])
+@pytest.mark.parametrize("k2", [8, 64])
+def test_attention_heavy_rows(oracle, hubgraph, heads, form, k2):
+    assert hubgraph.softmax_heavy_rows().numel() >= 2
+    rng = np.random.default_rng(heads * 100 + k2)
+    hw = f32(rng.standard_normal((hubgraph.n_rows, heads * k2)))
+    a_s, a_d = f32(rng.uniform(-0.5, 0.5, heads * k2)), f32(rng.uniform(-0.5, 0.5, heads * k2))
+    spec = gc.GatLayerSpec(3, k2, np.zeros((3, heads * k2)), a_s, a_d, heads=heads, attention=form)
+    att = gc.atten_calc(hubgraph, torch.from_numpy(hw).to(DEV), spec)
+    oa = to_oracle(oracle, hubgraph)
+    for h in range(heads):
+        ref = oracle.atten_calc(oa, hw[:, h * k2:(h + 1) * k2], a_s[h * k2:(h + 1) * k2],
+                                a_d[h * k2:(h + 1) * k2], 0.2).values
+        assert oracle.rel_err(att.head(h).values.cpu().numpy(), ref) < 1e-5
+    np.testing.assert_allclose(att.row_sums().cpu().numpy(), 1.0, atol=1e-5)
+    # the heavy-row CTAs and the lane groups agree with the unsplit launch
+    again = gc.atten_calc(hubgraph, torch.from_numpy(hw).to(DEV), spec)
+    assert torch.equal(att.alpha.values, again.alpha.values)
+
+
+def test_normalized_adjacency_heavy_rows(oracle, hubgraph):
+    g = gc.NormalizedGraph.from_adjacency(hubgraph, precompute=True)
+    og = oracle.GcnGraph.from_adjacency(to_oracle(oracle, hubgraph))
+    np.testing.assert_allclose(g.n_tilde.values.cpu().numpy(), og.n_tilde.values, rtol=2e-7)
+
+
 def test_attention_singleton_and_ties():
     a = gc.CsrMatrix(1, 1, np.array([0, 1]), np.array([0]), np.ones(1), device=DEV)
     spec = gc.GatLayerSpec(1, 1, np.ones((1, 1)), np.ones(1), np.ones(1))
