@@ -216,6 +216,30 @@ GNNC_API int gc_attn_sddmm_f32(const int32_t *row_ptr, const int32_t *col_idx, c
                       const int32_t *heavy_rows, int64_t n_heavy, float *s_work,
                       float *alpha, void *stream);
 
+/* ---- hybrid aggregation: dense hub block on tcgen05 ----
+ * For a unit-valued pattern Ã and D = diag(d), the aggregation
+ *   C = D Ã D X   (both GCN compositions: dynamic directly, precompute as Ñ = DÃD)
+ * is split by columns into the T most-referenced ("hub") columns and the
+ * rest.  The hub part is a dense product on the 5th-gen tensor cores:
+ *   C_hub = D · A_hub · (B0 + B1 + B2),  A_hub[i, t] = Ã[i, hub_cols[t]] in {0, 1}
+ * with B_q the hi/mid/lo bf16 terms of (D X)[hub_cols] — exact in bf16, so
+ * the result carries fp32 precision.  The tail (remaining columns) is the
+ * ordinary SpMM launched with GC_ACCUMULATE on top of C_hub.
+ *
+ * gc_hub_terms_rows(K): rows per term in the packed operand (K rounded up to
+ *   the kernel's N tile); the packed operand is bf16[3 * rows * T].
+ * gc_hub_pack_bf16x3: Bt[q][f][t] = term_q( X[hub_cols[t], f] * d_col[hub_cols[t]] )
+ *   (d_col may be NULL), zero for f >= K.
+ * gc_hub_gemm_bf16x3: C[i, f] = d_row[i] * sum_t A_hub[i, t] * (B0 + B1 + B2)[f, t]
+ *   (d_row may be NULL; flags: GC_RELU).  A_hub bf16 row-major [n_rows x lda],
+ *   T % 64 == 0, 16-byte aligned operands.                                  */
+GNNC_API int64_t gc_hub_terms_rows(int64_t K);
+GNNC_API int gc_hub_pack_bf16x3(const float *X, int64_t ldx, int64_t K, const int32_t *hub_cols,
+                       int64_t T, const float *d_col, void *Bt, void *stream);
+GNNC_API int gc_hub_gemm_bf16x3(const void *A_hub, int64_t lda, int64_t n_rows, int64_t T,
+                       const void *Bt, int64_t K, float *C, int64_t ldc, const float *d_row,
+                       uint32_t flags, void *stream);
+
 /* ---- multi-GPU row partition -----------------
  * nnz-balanced contiguous row blocks over a HOST copy of row_ptr (int64):
  *   bounds[0] = 0, bounds[P] = n, bounds[p] = first r with row_ptr[r] >=

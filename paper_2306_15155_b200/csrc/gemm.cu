@@ -13,8 +13,11 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
+
+#include <cuda_bf16.h>
 
 #include "common.cuh"
 
@@ -112,12 +115,27 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int n) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((128u >> 4) << 24);
 }
 
+// Instruction descriptor: D = F32, A = B = BF16 (kind::f16), both K-major.
+__host__ __device__ constexpr uint32_t idesc_bf16(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((128u >> 4) << 24);
+}
+
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                          uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
@@ -148,6 +166,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 constexpr int BM = 128;             // UMMA_M (cta_group::1)
 constexpr int BK = 32;              // fp32 elements per 128-byte swizzle row
 constexpr int UMMA_K = 8;           // K per tcgen05.mma for kind::tf32
+// Both element types use the same byte geometry: a k-block is one 128-byte
+// swizzle row (32 fp32 or 64 bf16) and one MMA consumes 32 bytes of it
+// (8 tf32 or 16 bf16), so the descriptors, TMA boxes and ring are shared.
+constexpr int KB_BYTES = 128;
+constexpr int MMA_K_BYTES = 32;
 // 6 warps: 0 = TMA producer (+ TMEM alloc), 1 = MMA issuer, 2..5 = epilogue.
 // Epilogue warp w reads TMEM lanes 32*(w%4) .. +31, so warps 2..5 cover all 128.
 constexpr int kGemmThreads = 192;
@@ -169,15 +192,21 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 // smem ring streams k-blocks across tile boundaries, and the accumulator is
 // double-buffered in TMEM (2 x BN columns) so the epilogue of tile i overlaps
 // the mainloop of tile i+1.
-template <int BN>
-__global__ void __launch_bounds__(kGemmThreads, 1)
-    gemm_tf32_tcgen05(const __grid_constant__ CUtensorMap map_a,
-                      const __grid_constant__ CUtensorMap map_b,
-                      const __grid_constant__ CUtensorMap map_c, const GemmEpi ep, int num_kb,
-                      int stages, int m_tiles, int n_tiles, int tma_store) {
-  constexpr uint32_t A_BYTES = BM * BK * 4;
-  constexpr uint32_t B_BYTES = BN * BK * 4;
-  constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+//
+// TERMS > 1 (the dense hub block of the hybrid aggregation, BF16): the B
+// operand is TERMS stacked [b_rows_per_term x K] slices (hi/mid/lo bf16 terms
+// of one fp32 operand); each k-block stages one A tile and TERMS B tiles and
+// issues TERMS MMAs per 32-byte step into the same accumulator, so
+// D = A·(B0 + B1 + B2) with the A tile read once.
+template <int BN, int TERMS, bool BF16>
+__device__ __forceinline__ void gemm_tc_body(const CUtensorMap &map_a, const CUtensorMap &map_b,
+                                             const CUtensorMap &map_c, const GemmEpi &ep,
+                                             int num_kb, int stages, int m_tiles, int n_tiles,
+                                             int tma_store, int b_rows_per_term) {
+  constexpr uint32_t A_BYTES = BM * KB_BYTES;
+  constexpr uint32_t B_BYTES = BN * KB_BYTES;
+  constexpr uint32_t STAGE_BYTES = A_BYTES + TERMS * B_BYTES;
+  constexpr int KB_ELEMS = BF16 ? 64 : 32;
   constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // power of two >= 32
 
   extern __shared__ uint8_t smem_raw[];
@@ -232,14 +261,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           mbar_wait(empty_bar(s), ((it / stages) & 1) ^ 1);
           const uint32_t sa = base + (uint32_t)s * STAGE_BYTES;
           mbar_expect_tx(full_bar(s), STAGE_BYTES);
-          tma_load_2d(sa, &map_a, full_bar(s), kb * BK, m0);
-          tma_load_2d(sa + A_BYTES, &map_b, full_bar(s), kb * BK, n0);
+          tma_load_2d(sa, &map_a, full_bar(s), kb * KB_ELEMS, m0);
+#pragma unroll
+          for (int q = 0; q < TERMS; ++q)
+            tma_load_2d(sa + A_BYTES + q * B_BYTES, &map_b, full_bar(s), kb * KB_ELEMS,
+                        q * b_rows_per_term + n0);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer (one thread) ----------------
-      constexpr uint32_t idesc = idesc_tf32(BN);
+      constexpr uint32_t idesc = BF16 ? idesc_bf16(BN) : idesc_tf32(BN);
       int it = 0, lt = 0;
       for (int tile = blockIdx.x; tile < n_tiles_total; tile += gridDim.x, ++lt) {
         const int acc = lt & 1;
@@ -252,10 +284,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tc_fence_after();
           const uint32_t sa = base + (uint32_t)s * STAGE_BYTES;
 #pragma unroll
-          for (int k = 0; k < BK / UMMA_K; ++k) {
-            const uint64_t ad = umma_desc_sw128(sa + k * UMMA_K * 4);
-            const uint64_t bd = umma_desc_sw128(sa + A_BYTES + k * UMMA_K * 4);
-            mma_tf32(tmem_d, ad, bd, idesc, (kb | k) != 0);
+          for (int k = 0; k < KB_BYTES / MMA_K_BYTES; ++k) {
+            const uint64_t ad = umma_desc_sw128(sa + k * MMA_K_BYTES);
+#pragma unroll
+            for (int q = 0; q < TERMS; ++q) {
+              const uint64_t bd = umma_desc_sw128(sa + A_BYTES + q * B_BYTES + k * MMA_K_BYTES);
+              if constexpr (BF16) mma_bf16(tmem_d, ad, bd, idesc, (kb | k | q) != 0);
+              else mma_tf32(tmem_d, ad, bd, idesc, (kb | k | q) != 0);
+            }
           }
           mma_commit(empty_bar(s));  // frees the smem slot once these MMAs retire
         }
@@ -340,6 +376,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                  "n"(TMEM_COLS)
                  : "memory");
   }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_tf32_tcgen05(const __grid_constant__ CUtensorMap map_a,
+                      const __grid_constant__ CUtensorMap map_b,
+                      const __grid_constant__ CUtensorMap map_c, const GemmEpi ep, int num_kb,
+                      int stages, int m_tiles, int n_tiles, int tma_store) {
+  gemm_tc_body<BN, 1, false>(map_a, map_b, map_c, ep, num_kb, stages, m_tiles, n_tiles, tma_store,
+                             0);
+}
+
+// Dense hub block of the hybrid aggregation: C = D_row · A_hub · (B0 + B1 + B2)
+// with A_hub the 0/1 adjacency restricted to the hub columns (exact in bf16)
+// and B_q the three bf16 terms of D_col·X[hub rows] (together exact fp32).
+template <int BN>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_hub_bf16x3_tcgen05(const __grid_constant__ CUtensorMap map_a,
+                            const __grid_constant__ CUtensorMap map_b,
+                            const __grid_constant__ CUtensorMap map_c, const GemmEpi ep,
+                            int num_kb, int stages, int m_tiles, int n_tiles, int tma_store,
+                            int b_rows_per_term) {
+  gemm_tc_body<BN, 3, true>(map_a, map_b, map_c, ep, num_kb, stages, m_tiles, n_tiles, tma_store,
+                            b_rows_per_term);
 }
 
 // W (K x N, ldw) -> Wt (N x K, ldt): the K-major B operand.
@@ -463,19 +523,20 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 
 // 2-D fp32 row-major matrix (rows x cols, ld elements) as a K-major TMA map
 // with a (BK x box_rows) box and 128-byte swizzle; OOB elements read as 0.
-int make_map(CUtensorMap *map, const float *ptr, int64_t rows, int64_t cols, int64_t ld,
+int make_map(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
              int box_rows, int box_cols = BK,
-             CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+             CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B, bool bf16 = false) {
   auto enc = get_encode_fn();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled unavailable");
     return GC_ERR_CUDA;
   }
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * (bf16 ? 2 : 4))};
   cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims,
+  CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                   2, const_cast<void *>(ptr), dims,
                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -485,17 +546,30 @@ int make_map(CUtensorMap *map, const float *ptr, int64_t rows, int64_t cols, int
   return GC_OK;
 }
 
+// smem: the stage ring, its barriers and (when it fits) the 16 KB epilogue
+// staging for TMA stores; returns the stage count (0: does not fit)
+inline int ring_stages(size_t stage_bytes, bool staging, size_t *smem,
+                       size_t max_ring = 227 * 1024) {
+  const size_t cap = 227 * 1024;
+  for (int st = 8; st >= 2; --st) {
+    if ((size_t)st * stage_bytes > max_ring && st > 2) continue;
+    const size_t need = (((size_t)st * stage_bytes + 8 * (2 * st + 4) + 16 + 1023) & ~(size_t)1023) +
+                        (staging ? 4 * 2 * 2048 : 0) + 1024;
+    if (need <= cap) {
+      *smem = need;
+      return st;
+    }
+  }
+  return 0;
+}
+
 template <int BN>
 int launch_tf32(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mc, int tma_store,
                 const GemmEpi &ep, int64_t K, cudaStream_t st) {
   const int num_kb = (int)((K + BK - 1) / BK);
-  constexpr int stage_bytes = BM * BK * 4 + BN * BK * 4;
-  // deepest ring that fits next to the barriers and the 16 KB epilogue
-  // staging (<= 8 stages, ring <= ~190 KB)
-  int stages = (190 * 1024) / stage_bytes;
-  stages = stages > 8 ? 8 : (stages < 2 ? 2 : stages);
-  const size_t smem = (((size_t)stages * stage_bytes + 8 * (2 * stages + 4) + 16 + 1023) & ~(size_t)1023) +
-                      4 * 2 * 2048 + 1024;
+  constexpr int stage_bytes = BM * KB_BYTES + BN * KB_BYTES;
+  size_t smem = 0;
+  const int stages = ring_stages(stage_bytes, true, &smem, 190 * 1024);
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
@@ -513,6 +587,85 @@ int launch_tf32(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap 
   gemm_tf32_tcgen05<BN><<<grid, kGemmThreads, smem, st>>>(ma, mb, mc, ep, num_kb, stages, m_tiles,
                                                           n_tiles, tma_store);
   return check_launch("gemm_tf32_tcgen05");
+}
+
+template <int BN>
+int launch_hub(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mc, int tma_store,
+               const GemmEpi &ep, int64_t T, int64_t kp, cudaStream_t st) {
+  const int num_kb = (int)((T + 63) / 64);
+  constexpr int stage_bytes = BM * KB_BYTES + 3 * BN * KB_BYTES;
+  size_t smem = 0;
+  int stages = tma_store ? ring_stages(stage_bytes, true, &smem) : 0;
+  if (stages == 0) {  // no room for the staging buffers: direct stores
+    tma_store = 0;
+    stages = ring_stages(stage_bytes, false, &smem);
+  }
+  if (stages == 0) {
+    set_error("gc_hub_gemm: tile does not fit shared memory");
+    return GC_ERR_UNSUPPORTED;
+  }
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(gemm_hub_bf16x3_tcgen05<BN>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  });
+  if (attr_err != cudaSuccess) {
+    set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
+    return GC_ERR_CUDA;
+  }
+  const int m_tiles = (int)((ep.M + BM - 1) / BM);
+  const int n_tiles = (int)((ep.N + BN - 1) / BN);
+  const int64_t tiles = (int64_t)m_tiles * n_tiles;
+  const int grid = (int)(tiles < sm_count() ? tiles : sm_count());
+  gemm_hub_bf16x3_tcgen05<BN><<<grid, kGemmThreads, smem, st>>>(
+      ma, mb, mc, ep, num_kb, stages, m_tiles, n_tiles, tma_store, (int)kp);
+  return check_launch("gemm_hub_bf16x3_tcgen05");
+}
+
+// X[hub_cols[t], f] * d[hub_cols[t]] -> three bf16 terms, transposed to the
+// K-major B operand Bt[q][f][t] (f < kp; rows f >= K are zero).  hi = bf16(x),
+// mid = bf16(x - hi), lo = bf16(x - hi - mid): hi + mid + lo carries x's full
+// 24-bit mantissa, so A_hub (0/1) · B is an fp32-exact product.
+__global__ void hub_pack_kernel(const float *__restrict__ X, int64_t ldx, int64_t K,
+                                const int32_t *__restrict__ hub_cols, int64_t T,
+                                const float *__restrict__ d, int64_t kp,
+                                __nv_bfloat16 *__restrict__ Bt) {
+  __shared__ float tile[32][33];
+  const int64_t t0 = (int64_t)blockIdx.x * 32, f0 = (int64_t)blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t t = t0 + i, f = f0 + threadIdx.x;
+    float x = 0.0f;
+    if (t < T && f < K) {
+      const int64_t j = hub_cols[t];
+      x = X[j * ldx + f];
+      if (d) x *= __ldg(d + j);
+    }
+    tile[i][threadIdx.x] = x;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t f = f0 + i, t = t0 + threadIdx.x;
+    if (f >= kp || t >= T) continue;
+    const float x = tile[threadIdx.x][i];
+    const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+    const float r1 = x - __bfloat162float(hi);
+    const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+    Bt[f * T + t] = hi;
+    Bt[(kp + f) * T + t] = mid;
+    Bt[(2 * kp + f) * T + t] = lo;
+  }
+}
+
+inline int hub_bn(int64_t K) {
+  static const int cap = [] {  // GNNC_HUB_BN caps the N tile (experiments)
+    const char *e = getenv("GNNC_HUB_BN");
+    const int v = e ? atoi(e) : 128;  // 128: 3-stage ring (measured faster than 256 x 2 stages)
+    return (v == 16 || v == 32 || v == 64 || v == 128) ? v : 256;
+  }();
+  const int bn = K <= 16 ? 16 : K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256;
+  return bn < cap ? bn : cap;
 }
 
 }  // namespace
@@ -607,4 +760,61 @@ extern "C" int gc_scale_rows_f32(const float *d, const float *B, int64_t ldb, in
   scale_rows_kernel<<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, as_stream(stream)>>>(
       d, B, ldb, n_rows, K, C, ldc, flags, vec);
   return check_launch("scale_rows_kernel");
+}
+
+extern "C" int64_t gc_hub_terms_rows(int64_t K) {
+  if (K <= 0) return 0;
+  const int bn = hub_bn(K);
+  return (K + bn - 1) / bn * bn;
+}
+
+extern "C" int gc_hub_pack_bf16x3(const float *X, int64_t ldx, int64_t K, const int32_t *hub_cols,
+                                  int64_t T, const float *d_col, void *Bt, void *stream) {
+  GC_REQUIRE(K >= 1 && T >= 0 && ldx >= K, GC_ERR_SHAPE, "gc_hub_pack_bf16x3: bad shape");
+  if (T == 0) return GC_OK;
+  GC_REQUIRE(X && hub_cols && Bt, GC_ERR_VALUE, "gc_hub_pack_bf16x3: null operand");
+  const int64_t kp = gc_hub_terms_rows(K);
+  dim3 grid((unsigned)((T + 31) / 32), (unsigned)((kp + 31) / 32));
+  GC_REQUIRE(grid.y < 65536, GC_ERR_SHAPE, "gc_hub_pack_bf16x3: K too large");
+  hub_pack_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(
+      X, ldx, K, hub_cols, T, d_col, kp, static_cast<__nv_bfloat16 *>(Bt));
+  return check_launch("hub_pack_kernel");
+}
+
+extern "C" int gc_hub_gemm_bf16x3(const void *A_hub, int64_t lda, int64_t n_rows, int64_t T,
+                                  const void *Bt, int64_t K, float *C, int64_t ldc,
+                                  const float *d_row, uint32_t flags, void *stream) {
+  GC_REQUIRE(n_rows >= 0 && T >= 0 && K >= 1 && lda >= T && ldc >= K, GC_ERR_SHAPE,
+             "gc_hub_gemm_bf16x3: bad shape");
+  GC_REQUIRE((flags & ~GC_RELU) == 0, GC_ERR_VALUE, "gc_hub_gemm_bf16x3: unknown flags 0x%x",
+             flags);
+  if (n_rows == 0) return GC_OK;
+  GC_REQUIRE(A_hub && Bt && C, GC_ERR_VALUE, "gc_hub_gemm_bf16x3: null operand");
+  GC_REQUIRE(T % 64 == 0 && T > 0 && lda % 8 == 0 && aligned16(A_hub) && aligned16(Bt),
+             GC_ERR_UNSUPPORTED,
+             "gc_hub_gemm_bf16x3: needs T %% 64 == 0, lda %% 8 == 0, 16-byte aligned operands");
+  GC_REQUIRE(n_rows < (int64_t)INT32_MAX && T < (int64_t)INT32_MAX, GC_ERR_SHAPE,
+             "gc_hub_gemm_bf16x3: dimension exceeds TMA range");
+  cudaStream_t st = as_stream(stream);
+  const int bn = hub_bn(K);
+  const int64_t kp = gc_hub_terms_rows(K);
+  CUtensorMap ma, mb, mc;
+  int rc = make_map(&ma, A_hub, n_rows, T, lda, BM, 64, CU_TENSOR_MAP_SWIZZLE_128B, true);
+  if (rc) return rc;
+  rc = make_map(&mb, Bt, 3 * kp, T, T, bn, 64, CU_TENSOR_MAP_SWIZZLE_128B, true);
+  if (rc) return rc;
+  GemmEpi ep{C, ldc, d_row, n_rows, K, flags};
+  int tma_store = ((ldc % 4) == 0 && aligned16(C)) ? 1 : 0;
+  memset(&mc, 0, sizeof(mc));
+  if (tma_store) {
+    rc = make_map(&mc, C, n_rows, K, ldc, 32, 16, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (rc) return rc;
+  }
+  switch (bn) {
+    case 16: return launch_hub<16>(ma, mb, mc, tma_store, ep, T, kp, st);
+    case 32: return launch_hub<32>(ma, mb, mc, tma_store, ep, T, kp, st);
+    case 64: return launch_hub<64>(ma, mb, mc, tma_store, ep, T, kp, st);
+    case 128: return launch_hub<128>(ma, mb, mc, tma_store, ep, T, kp, st);
+    default: return launch_hub<256>(ma, mb, mc, tma_store, ep, T, kp, st);
+  }
 }

@@ -538,7 +538,7 @@ def gat_sddmm_aggregate(a: CsrMatrix, a_src: torch.Tensor, a_dst: torch.Tensor, 
 
 
 def _spmm(a: CsrMatrix, b, *, weighted: bool, d_row=None, d_col=None, relu=False, out=None,
-          accumulate=False, algo: str = "auto", what="spmm"):
+          accumulate=False, algo: str = "auto", what="spmm", timer: str | None = "spmm"):
     dev = a.device
     op = _Operand(b, dev)
     bt = op.t
@@ -577,7 +577,7 @@ def _spmm(a: CsrMatrix, b, *, weighted: bool, d_row=None, d_col=None, relu=False
     hints, shrink = _variant(a, K, "spmm", probe)
     cols = a.hub_tagged_cols(K) if hints else a.col_idx
     extra = (nat.GC_HUB_TAGGED if hints else 0) | nat.GC_SPMM_SHRINK(shrink)
-    rc = _timed_call("spmm", dev, lambda: launch(cols, extra))
+    rc = _timed_call(timer, dev, lambda: launch(cols, extra)) if timer else launch(cols, extra)
     nat.check(rc, what)
     return op.wrap(out)
 

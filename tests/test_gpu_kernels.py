@@ -547,3 +547,114 @@ def test_reference_side_binding(oracle, plgraph):
     out = b200_spmm(oa, b)
     assert out.dtype == np.float64
     assert oracle.rel_err(out, oracle.spmm(oa, b.astype(np.float32))) < SP_TOL
+
+
+# ---------------------------------------------------------------------------
+# hybrid aggregation: dense hub block on tcgen05 (BF16 x3) + sparse tail
+# ---------------------------------------------------------------------------
+
+
+@pytest.fixture(scope="module")
+def hub_pl():
+    """Power-law graph dense enough for a 64/128-column hub block."""
+    a = graphs.powerlaw_graph(2500, 40, seed=11, device=DEV)
+    return gc.add_self_loops(a)
+
+
+@pytest.mark.parametrize("K", [1, 7, 16, 32, 100, 256, 300, 512])
+@pytest.mark.parametrize("T", [64, 128])
+def test_hub_gemm_is_fp32_exact(oracle, K, T):
+    from paper_2306_15155_b200 import _native as nat
+    rng = np.random.default_rng(K * 7 + T)
+    n, ncols = 777, 3000
+    a_hub = (rng.random((n, T)) < 0.3).astype(np.float32)
+    x = f32(rng.standard_normal((ncols, K)) * 10.0 ** rng.integers(-3, 3, (ncols, 1)))
+    hub_cols = np.sort(rng.choice(ncols, T, replace=False)).astype(np.int32)
+    d = f32(rng.uniform(0.05, 1.0, ncols))
+    dr = f32(rng.uniform(0.05, 1.0, n))
+    lib = nat.load()
+    kp = lib.gc_hub_terms_rows(K)
+    bt = torch.empty(3 * kp * T, dtype=torch.bfloat16, device=DEV)
+    xt, ht, dt = (torch.from_numpy(v).to(DEV) for v in (x, hub_cols, d))
+    drt = torch.from_numpy(dr).to(DEV)
+    at = torch.from_numpy(a_hub).to(DEV).to(torch.bfloat16)
+    out = torch.full((n, K), float("nan"), device=DEV)
+    st = torch.cuda.current_stream().cuda_stream
+    nat.check(lib.gc_hub_pack_bf16x3(xt.data_ptr(), K, K, ht.data_ptr(), T, dt.data_ptr(),
+                                     bt.data_ptr(), st), "pack")
+    nat.check(lib.gc_hub_gemm_bf16x3(at.data_ptr(), T, n, T, bt.data_ptr(), K, out.data_ptr(), K,
+                                     drt.data_ptr(), 0, st), "gemm")
+    ref = dr.astype(np.float64)[:, None] * (a_hub.astype(np.float64) @ (
+        x.astype(np.float64)[hub_cols] * d.astype(np.float64)[hub_cols][:, None]))
+    assert oracle.rel_err(out.cpu().numpy(), ref) < 1e-6
+
+
+@pytest.mark.parametrize("K", [3, 32, 256])
+@pytest.mark.parametrize("T", [64, 128])
+@pytest.mark.parametrize("precompute", [False, True])
+def test_hybrid_aggregate_matches_oracle(oracle, hub_pl, K, T, precompute):
+    from paper_2306_15155_b200 import hub
+    g = gc.NormalizedGraph.from_adjacency(hub_pl).with_precomputed()
+    og = oracle.GcnGraph.from_adjacency(to_oracle(oracle, hub_pl))
+    rng = np.random.default_rng(K + T)
+    x = f32(rng.uniform(-0.5, 0.5, (hub_pl.n_rows, K)))
+    d = g.d_inv_sqrt.to(DEV)
+    vals = g.n_tilde.values if precompute else None
+    out = hub.hybrid_aggregate(g.a_tilde, torch.from_numpy(x).to(DEV), d, T, values=vals,
+                               relu=True)
+    ref = np.maximum(oracle.spmm(og.n_tilde, x), 0)
+    assert oracle.rel_err(out.cpu().numpy(), ref) < SP_TOL
+    plan = hub.hub_plan(g.a_tilde, T)
+    assert plan.hub_edges + plan.tail.nnz == g.a_tilde.nnz
+    assert plan.hub_edges == int(plan.a_hub.float().sum())
+
+
+@pytest.mark.parametrize("comp", ["precompute", "dynamic"])
+@pytest.mark.parametrize("order", ["aggregate_first", "update_first"])
+def test_gcn_layer_with_hub_split(oracle, hub_pl, comp, order, monkeypatch):
+    from paper_2306_15155_b200 import hub
+    monkeypatch.setattr(hub, "HUB_SPLIT", "128")
+    g = gc.NormalizedGraph.from_adjacency(hub_pl).with_precomputed()
+    og = oracle.GcnGraph.from_adjacency(to_oracle(oracle, hub_pl))
+    rng = np.random.default_rng(3)
+    k1, k2 = 48, 32
+    h = f32(rng.uniform(-0.5, 0.5, (hub_pl.n_rows, k1)))
+    w = f32(rng.uniform(-0.5, 0.5, (k1, k2)))
+    spec = gc.GcnLayerSpec(k1, k2, w, composition=comp, order=order)
+    gc.set_gemm_precision("fp32")
+    try:
+        launches = sparse.kernel_timing("spmm")
+        with launches:
+            out = gc.gcn_layer(g, torch.from_numpy(h).to(DEV), spec).cpu().numpy()
+        torch.cuda.synchronize()
+    finally:
+        gc.set_gemm_precision("tf32")
+    assert ("hubsplit", 128) in g.a_tilde._plans
+    ref = oracle.gcn_layer(og, h.astype(np.float64), w.astype(np.float64), comp, order)
+    assert oracle.rel_err(out, ref) <= 1e-4
+
+
+@pytest.mark.parametrize("comp", ["precompute", "dynamic"])
+@pytest.mark.parametrize("order", ["aggregate_first", "update_first"])
+def test_host_pipelined_layer_with_hub_split(oracle, hub_pl, comp, order, monkeypatch):
+    """Pinned host H through the row-block pipeline with the hub split on
+    every block (the e2e path of bench.py)."""
+    from paper_2306_15155_b200 import gcn as gcn_mod
+    from paper_2306_15155_b200 import hub
+    monkeypatch.setattr(hub, "HUB_SPLIT", "64")
+    monkeypatch.setattr(gcn_mod, "HOST_PIPELINE_BLOCKS", 3)
+    g = gc.NormalizedGraph.from_adjacency(hub_pl).with_precomputed()
+    og = oracle.GcnGraph.from_adjacency(to_oracle(oracle, hub_pl))
+    rng = np.random.default_rng(4)
+    k1, k2 = 40, 24
+    h = f32(rng.uniform(-0.5, 0.5, (hub_pl.n_rows, k1)))
+    w = f32(rng.uniform(-0.5, 0.5, (k1, k2)))
+    spec = gc.GcnLayerSpec(k1, k2, w, composition=comp, order=order)
+    gc.set_gemm_precision("fp32")
+    try:
+        out = gc.gcn_layer(g, torch.from_numpy(h).pin_memory(), spec)
+    finally:
+        gc.set_gemm_precision("tf32")
+    assert not out.is_cuda and ("hubsplit", 64) in g.a_tilde._plans
+    ref = oracle.gcn_layer(og, h.astype(np.float64), w.astype(np.float64), comp, order)
+    assert oracle.rel_err(out.numpy(), ref) <= 1e-4
