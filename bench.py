@@ -291,8 +291,9 @@ def main():
     g = gc.NormalizedGraph.from_adjacency(A)
     torch.cuda.synchronize()
     prep_s = time.perf_counter() - t0
+    g.with_precomputed()  # first call allocates Ñ's values
     e0.record()
-    g.with_precomputed()
+    gc.precompute_normalized(g)
     e1.record()
     torch.cuda.synchronize()
     norm_ms = e0.elapsed_time(e1)
@@ -335,7 +336,8 @@ def main():
     torch.cuda.synchronize()
     launches0 = _native.launch_count()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks, sparse.kernel_timing("spmm", "gemm") as kt:
+    with ClockSampler(local) as clocks, \
+            sparse.kernel_timing("spmm", "gemm", "hub_gemm", "spmm_tail") as kt:
         # cudaProfilerStart/Stop bracket the timed region so that
         # `ncu --profile-from-start off` captures exactly its launches
         torch.cuda.profiler.start()
@@ -353,18 +355,51 @@ def main():
         tt = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-    spmm_ms = float(np.mean(kt.durations_ms("spmm"))) if kt.durations_ms("spmm") else None
-    gemm_ms = float(np.mean(kt.durations_ms("gemm"))) if kt.durations_ms("gemm") else None
+    def kms(name):
+        v = kt.durations_ms(name)
+        return float(np.mean(v)) if v else None
+
+    spmm_ms, gemm_ms = kms("spmm"), kms("gemm")
+    hub_ms, tail_ms = kms("hub_gemm"), kms("spmm_tail")
     value = m / (ms * 1e-3)
 
-    # ---- roofline of the dominant kernel (SpMM) ------------------------------
+    # ---- roofline of the dominant kernel -------------------------------------
     pk = peaks()
     dyn = base == "dynamic"
     a_used = part.local if part is not None else (g.a_tilde if dyn else g.n_tilde)
     weighted = not (dyn and g.a_tilde.has_unit_values)
-    spmm_bytes = spmm_alg_bytes(a_used.n_rows, a_used.nnz, K, weighted, dyn, dyn)
-    roof = None
-    if spmm_ms:
+    T = g.a_tilde._plans.get(("hubsplit-choice", K, not dyn), 0) if part is None else 0
+    roof, hub_roof = None, None
+    if T and tail_ms:
+        # hybrid aggregation: the tail SpMM is the dominant kernel (HBM/L2
+        # roofline over its own edges, + the read-modify-write of C); the hub
+        # block is a tensor-core GEMM (bf16 roofline, 3 terms)
+        from paper_2306_15155_b200 import hub as hubmod
+
+        plan = hubmod.hub_plan(g.a_tilde, T)
+        mt = plan.tail.nnz
+        tail_bytes = spmm_alg_bytes(n, mt, K, weighted, dyn, dyn) + 4 * n * K
+        ach = tail_bytes / (tail_ms * 1e-3) / 1e9
+        traffic = None
+        tfj = ROOT / "profiles" / "traffic.json"
+        if tfj.exists():
+            traffic = json.loads(tfj.read_text()).get(f"{args.shape}/K{K}/{comp}/tail")
+            traffic = traffic if isinstance(traffic, int) else None
+        roof = {"kernel": "spmm_kernel (tail of the hub split)", "bound": "hbm", "achieved": round(ach, 1),
+                "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(ach / pk["hbm_gbs"], 3),
+                "traffic": traffic, "alg_bytes_per_launch": tail_bytes, "kernel_ms": round(tail_ms, 4),
+                "share_of_step": round(tail_ms / ms, 3), "peak_source": pk["source"],
+                "model": "edge-gather over the tail edges: 4(n+1)+4m_t[+4m_t values][+4m_t d_j]+4m_tK+4nK(+4nK C read)[+4n]",
+                "tail_edges": mt}
+        flops = 2 * n * T * K * 3
+        tf = flops / (hub_ms * 1e-3) / 1e12
+        hub_roof = {"kernel": "gemm_hub_bf16x3_tcgen05", "bound": "tensor", "achieved": round(tf, 1),
+                    "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": round(tf / pk["bf16_tflops"], 3),
+                    "kernel_ms": round(hub_ms, 4), "share_of_step": round(hub_ms / ms, 3), "T": T,
+                    "hub_edges": plan.hub_edges, "flops_per_launch": flops,
+                    "model": "2·n·T·K per bf16 term, 3 terms (exact fp32 split)"}
+    elif spmm_ms:
+        spmm_bytes = spmm_alg_bytes(a_used.n_rows, a_used.nnz, K, weighted, dyn, dyn)
         ach = spmm_bytes / (spmm_ms * 1e-3) / 1e9
         traffic = None
         tf = ROOT / "profiles" / "traffic.json"
@@ -391,8 +426,11 @@ def main():
                                    f"{'' if args.no_overlap else ' overlapped with the owned-column SpMM'}")
                    if world > 1 else "single GPU"},
         "gpu_launches": int(launches),
-        "kernel_ms": {"spmm": spmm_ms, "gemm": gemm_ms},
+        "kernel_ms": {"aggregation": spmm_ms, "gemm": gemm_ms, "hub_gemm": hub_ms,
+                      "spmm_tail": tail_ms},
         "roofline": roof,
+        "roofline_hub_gemm": hub_roof,
+        "hub_split": {"T": T, "autotune_ms": g.a_tilde._plans.get(("hubsplit-choice", K, not dyn, "times"))},
         "setup": {"graph_gen_s": round(gen_s, 2), "prep_s": round(prep_s, 3),
                   "normalize_sddmm_ms": round(norm_ms, 3)},
     }

@@ -137,13 +137,14 @@ def hybrid_aggregate(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, T: int, *,
 
     def run():
         bt = packed if packed is not None else pack(a, x, d, T)
-        nat.check(lib.gc_hub_gemm_bf16x3(a_hub.data_ptr(), T, hi - lo, T, bt.data_ptr(), K,
-                                         out.data_ptr(), _ld(out), dr.data_ptr(), 0, st), "hub_gemm")
+        nat.check(_timed_call("hub_gemm", dev, lambda: lib.gc_hub_gemm_bf16x3(
+            a_hub.data_ptr(), T, hi - lo, T, bt.data_ptr(), K, out.data_ptr(), _ld(out),
+            dr.data_ptr(), 0, st)), "hub_gemm")
         if values is None:
             _spmm(tail, x, weighted=False, d_row=dr, d_col=d, relu=relu, out=out,
-                  accumulate=True, timer=None)
+                  accumulate=True, timer="spmm_tail")
         else:
-            _spmm(tail, x, weighted=True, relu=relu, out=out, accumulate=True, timer=None)
+            _spmm(tail, x, weighted=True, relu=relu, out=out, accumulate=True, timer="spmm_tail")
         return 0
 
     _timed_call("spmm", dev, run)

@@ -291,3 +291,27 @@ def test_sweep_plan_and_train_roundtrip(tmp_path, sel_golden, monkeypatch):
     report = json.loads(rep.read_text())
     assert report["gcn"]["train"]["selected_over_oracle_geomean"] < 1.05
     assert (tmp_path / "models" / "gcn_b200.json").exists()
+
+
+def test_hub_plan_partitions_the_pattern():
+    """Host-side structure of the hub split (hub.py): the hub block and the
+    tail partition the edges of Ã; the hub columns are the T most referenced."""
+    from paper_2306_15155_b200 import hub
+
+    a = graphs.synthetic_graph("rmat", 1500, 40000, seed=2, device="cpu")
+    T = 128
+    plan = hub.HubPlan(a, T)
+    counts = torch.bincount(a.col_idx.long(), minlength=a.n_cols)
+    assert plan.hub_cols.numel() == T and bool((plan.hub_cols[1:] > plan.hub_cols[:-1]).all())
+    assert int(counts[plan.hub_cols.long()].min()) >= int(
+        counts[torch.ones(a.n_cols, dtype=torch.bool).index_fill_(0, plan.hub_cols.long(), False)].max())
+    assert plan.hub_edges + plan.tail.nnz == a.nnz
+    assert int(plan.a_hub.float().sum()) == plan.hub_edges
+    dense = a.to_dense()
+    hub_dense = torch.zeros_like(dense)
+    hub_dense[:, plan.hub_cols.long()] = plan.a_hub.float()
+    assert torch.equal(hub_dense + plan.tail.to_dense(), dense)
+    rows = plan.tail_block(None, 100, 700)
+    assert torch.equal(rows.to_dense(), plan.tail.to_dense()[100:700])
+    with pytest.raises(gc.ShapeError):
+        hub.HubPlan(a, 100)
