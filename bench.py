@@ -317,7 +317,8 @@ def main():
 
         def step():
             return dist_gcn_layer(part, h_dev, spec.weights, composition=base, order=order,
-                                  d=d_full, overlap=not args.no_overlap)
+                                  d=d_full, overlap=not args.no_overlap,
+                                  hub_unit=g.a_tilde.has_unit_values)
     else:
         h_dev = torch.from_numpy(h_host32).to(dev)
 

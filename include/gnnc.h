@@ -231,7 +231,7 @@ GNNC_API int gc_attn_sddmm_f32(const int32_t *row_ptr, const int32_t *col_idx, c
  * gc_hub_pack_bf16x3: Bt[q][f][t] = term_q( X[hub_cols[t], f] * d_col[hub_cols[t]] )
  *   (d_col may be NULL), zero for f >= K.
  * gc_hub_gemm_bf16x3: C[i, f] = d_row[i] * sum_t A_hub[i, t] * (B0 + B1 + B2)[f, t]
- *   (d_row may be NULL; flags: GC_RELU).  A_hub bf16 row-major [n_rows x lda],
+ *   (d_row may be NULL; flags: GC_RELU, GC_ACCUMULATE — C = relu?(C + ...)).  A_hub bf16 row-major [n_rows x lda],
  *   T % 64 == 0, 16-byte aligned operands.                                  */
 GNNC_API int64_t gc_hub_terms_rows(int64_t K);
 GNNC_API int gc_hub_pack_bf16x3(const float *X, int64_t ldx, int64_t K, const int32_t *hub_cols,

@@ -305,6 +305,7 @@ __device__ __forceinline__ void gemm_tc_body(const CUtensorMap &map_a, const CUt
     // triples the epilogue's instruction count; profiles/r01_ncu_summary.md.)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const bool relu = (ep.flags & GC_RELU) != 0;
+    const bool accum = (ep.flags & GC_ACCUMULATE) != 0;
     const bool vec = ((ep.ldc & 3) == 0) && aligned16(ep.C);
     const uint32_t my_stage = stage_c + (uint32_t)(warp - 2) * 2u * 2048u;
     int lt = 0, sbuf = 0;
@@ -326,9 +327,9 @@ __device__ __forceinline__ void gemm_tc_body(const CUtensorMap &map_a, const CUt
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           v[i] *= rs;
-          if (relu) v[i] = fmaxf(v[i], 0.0f);
+          if (relu && !accum) v[i] = fmaxf(v[i], 0.0f);
         }
-        if (tma_store) {
+        if (tma_store) {  // (never with GC_ACCUMULATE: the host forces direct stores)
           // row `lane` of a 32 x 16 box: four 16-B chunks, 64-B swizzle
           // (chunk ^ ((row >> 1) & 3)) -> conflict-free st.shared.v4
           const uint32_t buf = my_stage + (uint32_t)sbuf * 2048u;
@@ -352,6 +353,16 @@ __device__ __forceinline__ void gemm_tc_body(const CUtensorMap &map_a, const CUt
         }
         if (!row_ok) continue;
         const int64_t col = n0 + c;
+        if (accum) {  // C = relu?(old + rs * acc), the SpMM epilogue's order
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (col + i < ep.N) {
+              float o = crow[col + i] + v[i];
+              if (relu) o = fmaxf(o, 0.0f);
+              crow[col + i] = o;
+            }
+          continue;
+        }
         if (vec && col + 16 <= ep.N) {
 #pragma unroll
           for (int i = 0; i < 16; i += 4)
@@ -786,8 +797,8 @@ extern "C" int gc_hub_gemm_bf16x3(const void *A_hub, int64_t lda, int64_t n_rows
                                   const float *d_row, uint32_t flags, void *stream) {
   GC_REQUIRE(n_rows >= 0 && T >= 0 && K >= 1 && lda >= T && ldc >= K, GC_ERR_SHAPE,
              "gc_hub_gemm_bf16x3: bad shape");
-  GC_REQUIRE((flags & ~GC_RELU) == 0, GC_ERR_VALUE, "gc_hub_gemm_bf16x3: unknown flags 0x%x",
-             flags);
+  GC_REQUIRE((flags & ~(GC_RELU | GC_ACCUMULATE)) == 0, GC_ERR_VALUE,
+             "gc_hub_gemm_bf16x3: unknown flags 0x%x", flags);
   if (n_rows == 0) return GC_OK;
   GC_REQUIRE(A_hub && Bt && C, GC_ERR_VALUE, "gc_hub_gemm_bf16x3: null operand");
   GC_REQUIRE(T % 64 == 0 && T > 0 && lda % 8 == 0 && aligned16(A_hub) && aligned16(Bt),
@@ -804,7 +815,8 @@ extern "C" int gc_hub_gemm_bf16x3(const void *A_hub, int64_t lda, int64_t n_rows
   rc = make_map(&mb, Bt, 3 * kp, T, T, bn, 64, CU_TENSOR_MAP_SWIZZLE_128B, true);
   if (rc) return rc;
   GemmEpi ep{C, ldc, d_row, n_rows, K, flags};
-  int tma_store = ((ldc % 4) == 0 && aligned16(C)) ? 1 : 0;
+  // accumulating epilogues read C back: direct stores
+  int tma_store = ((ldc % 4) == 0 && aligned16(C) && !(flags & GC_ACCUMULATE)) ? 1 : 0;
   memset(&mc, 0, sizeof(mc));
   if (tma_store) {
     rc = make_map(&mc, C, n_rows, K, ldc, 32, 16, CU_TENSOR_MAP_SWIZZLE_64B);

@@ -140,28 +140,50 @@ class CudaOps:
 
     @staticmethod
     def spmm(a: CsrMatrix, b, d_row=None, d_col=None, relu=False, weighted=True, out=None,
-             accumulate=False):
+             accumulate=False, hub_d=None):
+        """``hub_d = (d_row, d_col)``: ``a`` is a unit Ã block or an Ñ = DÃD
+        block of a unit Ã, so the hub split (hub.py) may take the dense hub
+        columns to the tensor cores (chosen by measurement, cached)."""
+        from . import hub
         from .sparse import spmm, spmm_unweighted
 
+        if hub_d is not None:
+            pat = a
+            vals = a.values if weighted else None
+            if weighted:  # Ñ block: the split runs on the unit pattern twin
+                key = ("unit_twin",)
+                if key not in a._plans:
+                    twin = a.with_values(torch.ones_like(a.values))
+                    twin._unit = True
+                    a._plans[key] = twin
+                pat = a._plans[key]
+            T = hub.choose_split(pat, b, hub_d[1], d_row=hub_d[0], values=vals)
+            if T:
+                return hub.hybrid_aggregate(pat, b, hub_d[1], T, d_row=hub_d[0], values=vals,
+                                            relu=relu, out=out, accumulate=accumulate)
         f = spmm if weighted else spmm_unweighted
         return f(a, b, d_row=d_row, d_col=d_col, relu=relu, out=out, accumulate=accumulate)
 
 
 def dist_gcn_layer(part: RowPartition, h_local: torch.Tensor, w: torch.Tensor, *,
                    composition: str, order: str, d: torch.Tensor | None = None,
-                   ops=CudaOps, group=None, overlap: bool = False) -> torch.Tensor:
+                   ops=CudaOps, group=None, overlap: bool = False,
+                   hub_unit: bool = False) -> torch.Tensor:
     """One GCN layer on this rank's rows.  ``part.local`` is Ñ's block for
     precompute or Ã's block for dynamic; ``d`` is the FULL D^-1/2 vector
-    (needed for dynamic).  Returns this rank's output rows."""
+    (needed for dynamic, and for the hub split).  ``hub_unit``: Ã is
+    unit-valued, so the aggregation may use the hub split (hub.py) on this
+    rank's block.  Returns this rank's output rows."""
     dyn = composition == "dynamic"
     if dyn and d is None:
         raise ValueError("dynamic composition needs the degree vector")
-    d_loc = d[part.lo:part.hi] if dyn else None
+    hub_unit = hub_unit and d is not None
+    d_loc = d[part.lo:part.hi] if (dyn or hub_unit) else None
     weighted = not (dyn and part.local.has_unit_values)
     if overlap:
         loc, rem = part.split_local_remote()
         d_pad = None
-        if dyn:
+        if dyn or hub_unit:
             d_pad = torch.zeros(part.world * part.max_rows, dtype=d.dtype, device=d.device)
             for p in range(part.world):
                 lo, hi = int(part.bounds[p]), int(part.bounds[p + 1])
@@ -169,17 +191,22 @@ def dist_gcn_layer(part: RowPartition, h_local: torch.Tensor, w: torch.Tensor, *
         src = ops.gemm(h_local, w) if order == "update_first" else h_local
         full, work = all_gather_padded(src, part, group, async_op=True)
         # owned-column edges while the gather is in flight
-        y = ops.spmm(loc, src, d_row=d_loc, d_col=d_loc, relu=False, weighted=weighted)
+        dl = d_loc if dyn else None
+        y = ops.spmm(loc, src, d_row=dl, d_col=dl, relu=False, weighted=weighted)
         work.wait()
         last = order == "update_first"
-        y = ops.spmm(rem, full, d_row=d_loc, d_col=d_pad, relu=last, weighted=weighted, out=y,
-                     accumulate=True)
+        hub_kw = {"hub_d": (d_loc, d_pad)} if hub_unit else {}
+        y = ops.spmm(rem, full, d_row=dl, d_col=d_pad if dyn else None, relu=last,
+                     weighted=weighted, out=y, accumulate=True, **hub_kw)
         return y if last else ops.gemm(y, w, relu=True)
+    hub_kw = {"hub_d": (d_loc, d)} if hub_unit else {}
+    dl = d_loc if dyn else None
     if order == "update_first":
         hw_loc = ops.gemm(h_local, w)
         hw = all_gather_rows(hw_loc, part, group)
-        return ops.spmm(part.local, hw, d_row=d_loc, d_col=d if dyn else None, relu=True,
-                        weighted=weighted)
+        return ops.spmm(part.local, hw, d_row=dl, d_col=d if dyn else None, relu=True,
+                        weighted=weighted, **hub_kw)
     h = all_gather_rows(h_local, part, group)
-    x = ops.spmm(part.local, h, d_row=d_loc, d_col=d if dyn else None, relu=False, weighted=weighted)
+    x = ops.spmm(part.local, h, d_row=dl, d_col=d if dyn else None, relu=False, weighted=weighted,
+                 **hub_kw)
     return ops.gemm(x, w, relu=True)

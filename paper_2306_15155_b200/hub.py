@@ -111,21 +111,30 @@ def pack(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, T: int) -> torch.Tensor
 
 
 def hybrid_aggregate(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, T: int, *,
-                     values: torch.Tensor | None = None, relu: bool = False,
-                     out: torch.Tensor | None = None, rows: tuple[int, int] | None = None,
+                     d_row: torch.Tensor | None = None, values: torch.Tensor | None = None,
+                     relu: bool = False, out: torch.Tensor | None = None,
+                     accumulate: bool = False, rows: tuple[int, int] | None = None,
                      packed: torch.Tensor | None = None) -> torch.Tensor:
-    """C = epi(D Ã D X) for a unit-valued pattern ``a`` via the hub split.
-    ``values`` (optional) are a same-pattern matrix's values used for the tail
-    instead of d_i·d_j (the precompute composition streams Ñ's values).
-    ``rows=(lo, hi)`` computes that row block only (``out`` then has hi-lo
-    rows); ``packed`` reuses one ``pack`` across row blocks."""
+    """C = epi(D_row Ã D X) for a unit-valued pattern ``a`` via the hub split
+    (``d`` scales the columns; ``d_row`` the rows, default ``d`` itself for a
+    square pattern).  ``values`` (optional) are a same-pattern matrix's values
+    used for the tail instead of d_i·d_j (the precompute composition streams
+    Ñ's values).  ``accumulate``: C += ... (ReLU on the total).  ``rows=(lo,
+    hi)`` computes that row block only (``out`` then has hi-lo rows);
+    ``packed`` reuses one ``pack`` across row blocks."""
     dev = _require_cuda(a.col_idx, x, d)
     if x.dim() != 2 or x.shape[0] != a.n_cols or x.stride(1) != 1:
         raise ShapeError("hybrid_aggregate: x must be a row-major n_cols x K tensor")
+    if d_row is None:
+        if a.n_rows != a.n_cols:
+            raise ShapeError("hybrid_aggregate: d_row is required for a rectangular pattern")
+        d_row = d
     K = x.shape[1]
     lo, hi = rows if rows is not None else (0, a.n_rows)
     plan = hub_plan(a, T)
     if out is None:
+        if accumulate:
+            raise ValueError("hybrid_aggregate: accumulate needs an output")
         out = torch.empty(hi - lo, K, dtype=torch.float32, device=dev)
     elif tuple(out.shape) != (hi - lo, K) or out.stride(1) != 1:
         raise ShapeError(f"hybrid_aggregate: out must be a row-major {hi - lo}x{K} tensor")
@@ -133,13 +142,14 @@ def hybrid_aggregate(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, T: int, *,
     st = _stream(dev)
     tail = plan.tail_block(values, lo, hi)
     a_hub = plan.a_hub[lo:hi]
-    dr = d[lo:hi]
+    dr = d_row[lo:hi]
+    flags = nat.GC_ACCUMULATE if accumulate else 0
 
     def run():
         bt = packed if packed is not None else pack(a, x, d, T)
         nat.check(_timed_call("hub_gemm", dev, lambda: lib.gc_hub_gemm_bf16x3(
             a_hub.data_ptr(), T, hi - lo, T, bt.data_ptr(), K, out.data_ptr(), _ld(out),
-            dr.data_ptr(), 0, st)), "hub_gemm")
+            dr.data_ptr(), flags, st)), "hub_gemm")
         if values is None:
             _spmm(tail, x, weighted=False, d_row=dr, d_col=d, relu=relu, out=out,
                   accumulate=True, timer="spmm_tail")
@@ -164,13 +174,17 @@ def _candidates(a: CsrMatrix) -> list[int]:
 
 
 def choose_split(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, *,
-                 values: torch.Tensor | None = None) -> int:
+                 d_row: torch.Tensor | None = None, values: torch.Tensor | None = None) -> int:
     """T for (pattern, K): 0 (plain SpMM) unless a hub split is measurably
     faster.  Every candidate is timed once (median of 3 after a warm launch)
     on the first call and the choice is cached on the pattern."""
     mode = str(HUB_SPLIT)
-    if mode == "0" or not a.has_unit_values or a.n_rows != a.n_cols:
+    if mode == "0" or not a.has_unit_values:
         return 0
+    if d_row is None:
+        if a.n_rows != a.n_cols:
+            return 0
+        d_row = d
     if mode != "auto":
         return int(mode)
     K = x.shape[1]
@@ -188,7 +202,7 @@ def choose_split(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, *,
     src = a if values is None else a.with_values(values)
 
     def plain():
-        _spmm(src, x, weighted=values is not None, d_row=None if values is not None else d,
+        _spmm(src, x, weighted=values is not None, d_row=None if values is not None else d_row,
               d_col=None if values is not None else d, out=scratch, timer=None)
 
     def timed(fn) -> float:
@@ -204,7 +218,8 @@ def choose_split(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, *,
 
     times = {0: timed(plain)}
     for T in cands:
-        times[T] = timed(lambda T=T: hybrid_aggregate(a, x, d, T, values=values, out=scratch))
+        times[T] = timed(lambda T=T: hybrid_aggregate(a, x, d, T, d_row=d_row, values=values,
+                                                      out=scratch))
     best = min(times, key=times.get)
     if best and times[best] >= 0.97 * times[0]:
         best = 0

@@ -37,7 +37,8 @@ class OracleOps:
         return torch.from_numpy(out)
 
     @staticmethod
-    def spmm(a, b, d_row=None, d_col=None, relu=False, weighted=True, out=None, accumulate=False):
+    def spmm(a, b, d_row=None, d_col=None, relu=False, weighted=True, out=None, accumulate=False,
+             hub_d=None):  # hub split = same product (GPU-only kernel choice)
         from oracle import gnn_oracle as orc
 
         rp, ci, v = a.numpy()
@@ -82,8 +83,10 @@ def _worker(rank, world, port, comp, order, q, overlap=False):
         else:
             base = at
         part = RowPartition.of(base, rank, world)
+        # hub_unit: the hub-split plumbing (d_row/d_col of each pass); the
+        # oracle ops compute the same product either way
         out = dist_gcn_layer(part, h[part.lo:part.hi], w, composition=comp, order=order,
-                             d=d, ops=OracleOps, overlap=overlap)
+                             d=d, ops=OracleOps, overlap=overlap, hub_unit=world == 2)
         full = all_gather_rows(out, part)
         if rank == 0:
             q.put((part.bounds.tolist(), full.numpy()))

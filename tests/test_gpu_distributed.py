@@ -1,0 +1,85 @@
+"""The row-partitioned layer with the real kernels (and the hub split) on one
+GPU: 2 ranks of a gloo group share cuda:0, so the multi-GPU host path —
+partition, padded all-gather, owned/remote split, per-rank hub block — runs
+through libgnnc; outputs are compared with the single-process oracle."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, comp, order, overlap, q):
+    import sys
+    from pathlib import Path
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2306_15155_b200 as gc
+        from paper_2306_15155_b200 import graphs, hub
+        from paper_2306_15155_b200.distributed import RowPartition, all_gather_rows, dist_gcn_layer
+
+        hub.HUB_SPLIT = "64"
+        dev = torch.device("cuda", 0)
+        a = graphs.powerlaw_graph(2500, 40, seed=11, device=dev)
+        g = gc.NormalizedGraph.from_adjacency(a).with_precomputed()
+        rng = np.random.default_rng(8)
+        h = torch.from_numpy(rng.uniform(-0.5, 0.5, (2500, 40)).astype(np.float32)).to(dev)
+        w = torch.from_numpy(rng.uniform(-0.5, 0.5, (40, 24)).astype(np.float32)).to(dev)
+        gc.set_gemm_precision("fp32")
+        part = RowPartition.of(g.n_tilde if comp == "precompute" else g.a_tilde, rank, world)
+        out = dist_gcn_layer(part, h[part.lo:part.hi], w, composition=comp, order=order,
+                             d=g.d_inv_sqrt.to(dev), overlap=overlap, hub_unit=True)
+        used = any(k[0] == "hubsplit" for k in part.local._plans) or \
+            any(k[0] == "hubsplit" for k in part.split_local_remote()[1]._plans)
+        full = all_gather_rows(out.cpu(), part)
+        if rank == 0:
+            q.put((full.numpy(), used))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("overlap", [False, True])
+@pytest.mark.parametrize("comp,order", [("dynamic", "update_first"), ("precompute", "aggregate_first")])
+def test_partitioned_layer_with_hub_split_on_gpu(oracle, comp, order, overlap):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, comp, order, overlap, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    full, used = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert used
+    import paper_2306_15155_b200 as gc
+    from paper_2306_15155_b200 import graphs
+
+    a = graphs.powerlaw_graph(2500, 40, seed=11, device="cuda")
+    rp, ci, v = a.numpy()
+    og = oracle.GcnGraph.from_adjacency(oracle.Csr(2500, 2500, rp, ci, v))
+    rng = np.random.default_rng(8)
+    h = rng.uniform(-0.5, 0.5, (2500, 40)).astype(np.float32)
+    w = rng.uniform(-0.5, 0.5, (40, 24)).astype(np.float32)
+    ref = oracle.gcn_layer(og, h.astype(np.float64), w.astype(np.float64), comp, order)
+    assert oracle.rel_err(full, ref) <= 1e-4
+    _ = gc
