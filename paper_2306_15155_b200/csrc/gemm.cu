@@ -389,6 +389,259 @@ __device__ __forceinline__ void gemm_tc_body(const CUtensorMap &map_a, const CUt
   }
 }
 
+// ============================================================================
+// CTA-pair (cta_group::2) variant of the hub GEMM
+// ============================================================================
+// Two CTAs of a cluster (one TPC) share every MMA: M = 256 (each CTA stages
+// its own 128 rows of A_hub) and N = BN (each CTA stages BN/2 rows of each B
+// term), so per SM the B operand traffic through shared memory and L2 is
+// halved — the single-CTA kernel is shared-memory-bandwidth bound (operand
+// reads of N = 128 tiles plus the TMA writes exceed 128 B/clk).  Protocol:
+//  * both CTAs' TMA loads complete_tx on the LEADER's full barrier (count 2:
+//    leader arrive.expect_tx(both stages' bytes) + peer remote arrive);
+//  * the leader's single MMA thread issues tcgen05.mma.cta_group::2 and
+//    commits with a 0b11 multicast to both CTAs' empty / tmem-full barriers;
+//  * the 8 epilogue warps (4 per CTA) arrive on the leader's tmem-empty barrier.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(addr), "r"(rank));
+  return out;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap *map,
+                                                 uint32_t leader_bar, int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+// D = F32, A = B = BF16, K-major, M = 256 (cta pair), N = n
+__host__ __device__ constexpr uint32_t idesc_bf16_m256(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((256u >> 4) << 24);
+}
+
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+    gemm_hub_pair_tcgen05(const __grid_constant__ CUtensorMap map_a,
+                          const __grid_constant__ CUtensorMap map_b,
+                          const __grid_constant__ CUtensorMap map_c, const GemmEpi ep, int num_kb,
+                          int stages, int m_pairs, int n_tiles, int tma_store,
+                          int b_rows_per_term) {
+  constexpr int TERMS = 3;
+  constexpr int BH = BN / 2;  // B rows per CTA per term
+  constexpr uint32_t A_BYTES = BM * KB_BYTES;
+  constexpr uint32_t B_BYTES = BH * KB_BYTES;
+  constexpr uint32_t STAGE_BYTES = A_BYTES + TERMS * B_BYTES;
+  constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t *gbase = smem_raw + (base - raw);
+  const uint32_t bar0 = base + (uint32_t)stages * STAGE_BYTES;
+  auto full_bar = [&](int s) { return bar0 + 8u * s; };
+  auto empty_bar = [&](int s) { return bar0 + 8u * (stages + s); };
+  auto tfull_bar = [&](int b) { return bar0 + 8u * (2 * stages + b); };
+  auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * stages + 2 + b); };
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + (bar0 - base) + 8u * (2 * stages + 4));
+  const uint32_t stage_c = (bar0 + 8u * (2 * stages + 4) + 16u + 1023u) & ~1023u;
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x / 2, n_clusters = gridDim.x / 2;
+  const int n_tiles_total = m_pairs * n_tiles;
+
+  if (warp == 1 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(full_bar(s), 2);   // leader expect_tx + peer arrive (leader's copy is used)
+      mbar_init(empty_bar(s), 1);  // multicast MMA commit
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull_bar(b), 1);
+      mbar_init(tempty_bar(b), 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs) ----------------
+      int it = 0;
+      for (int tile = cluster_id; tile < n_tiles_total; tile += n_clusters) {
+        const int m0 = (tile / n_tiles) * (2 * BM) + (int)rank * BM;
+        const int n0 = (tile % n_tiles) * BN + (int)rank * BH;
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int s = it % stages;
+          mbar_wait(empty_bar(s), ((it / stages) & 1) ^ 1);
+          const uint32_t sa = base + (uint32_t)s * STAGE_BYTES;
+          const uint32_t lbar = mapa_shared(full_bar(s), 0);
+          if (leader) mbar_expect_tx(full_bar(s), 2 * STAGE_BYTES);
+          else mbar_arrive_cluster(lbar);
+          tma_load_2d_pair(sa, &map_a, lbar, kb * 64, m0);
+#pragma unroll
+          for (int q = 0; q < TERMS; ++q)
+            tma_load_2d_pair(sa + A_BYTES + q * B_BYTES, &map_b, lbar, kb * 64,
+                             q * b_rows_per_term + n0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {  // ---------------- MMA issuer (leader only) ----------------
+      constexpr uint32_t idesc = idesc_bf16_m256(BN);
+      int it = 0, lt = 0;
+      for (int tile = cluster_id; tile < n_tiles_total; tile += n_clusters, ++lt) {
+        const int acc = lt & 1;
+        mbar_wait(tempty_bar(acc), ((lt >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int s = it % stages;
+          mbar_wait(full_bar(s), (it / stages) & 1);
+          tc_fence_after();
+          const uint32_t sa = base + (uint32_t)s * STAGE_BYTES;
+#pragma unroll
+          for (int k = 0; k < KB_BYTES / MMA_K_BYTES; ++k) {
+            const uint64_t ad = umma_desc_sw128(sa + k * MMA_K_BYTES);
+#pragma unroll
+            for (int q = 0; q < TERMS; ++q) {
+              const uint64_t bd = umma_desc_sw128(sa + A_BYTES + q * B_BYTES + k * MMA_K_BYTES);
+              mma_bf16_pair(tmem_d, ad, bd, idesc, (kb | k | q) != 0);
+            }
+          }
+          mma_commit_pair(empty_bar(s));  // frees slot s in both CTAs
+        }
+        mma_commit_pair(tfull_bar(acc));  // accumulators of both CTAs complete
+      }
+    }
+  } else {  // ---------------- epilogue warps 2..5 (both CTAs) ----------------
+    const int q = warp & 3;
+    const bool relu = (ep.flags & GC_RELU) != 0;
+    const bool accum = (ep.flags & GC_ACCUMULATE) != 0;
+    const bool vec = ((ep.ldc & 3) == 0) && aligned16(ep.C);
+    const uint32_t my_stage = stage_c + (uint32_t)(warp - 2) * 2u * 2048u;
+    int lt = 0, sbuf = 0;
+    for (int tile = cluster_id; tile < n_tiles_total; tile += n_clusters, ++lt) {
+      const int acc = lt & 1;
+      const int m0 = (tile / n_tiles) * (2 * BM) + (int)rank * BM;
+      const int n0 = (tile % n_tiles) * BN;
+      mbar_wait(tfull_bar(acc), (lt >> 1) & 1);
+      tc_fence_after();
+      const int row = m0 + q * 32 + lane;
+      const bool row_ok = row < ep.M;
+      const float rs = (row_ok && ep.row_scale) ? __ldg(ep.row_scale + row) : 1.0f;
+      float *crow = ep.C + (int64_t)row * ep.ldc;
+      const uint32_t taddr = tmem_base + (uint32_t)(acc * BN) + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        if (n0 + c >= ep.N) break;
+        float v[16];
+        tmem_ld16(taddr + (uint32_t)c, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          v[i] *= rs;
+          if (relu && !accum) v[i] = fmaxf(v[i], 0.0f);
+        }
+        if (tma_store) {
+          const uint32_t buf = my_stage + (uint32_t)sbuf * 2048u;
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            const uint32_t dst = buf + (uint32_t)lane * 64u + (uint32_t)((ch ^ ((lane >> 1) & 3)) * 16);
+            asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(dst), "f"(v[4 * ch]),
+                         "f"(v[4 * ch + 1]), "f"(v[4 * ch + 2]), "f"(v[4 * ch + 3])
+                         : "memory");
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&map_c, buf, n0 + c, m0 + q * 32);
+            bulk_commit();
+          }
+          sbuf ^= 1;
+          continue;
+        }
+        if (!row_ok) continue;
+        const int64_t col = n0 + c;
+        if (accum) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (col + i < ep.N) {
+              float o = crow[col + i] + v[i];
+              if (relu) o = fmaxf(o, 0.0f);
+              crow[col + i] = o;
+            }
+          continue;
+        }
+        if (vec && col + 16 <= ep.N) {
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            stg_f4(crow + col + i, make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (col + i < ep.N) crow[col + i] = v[i];
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mapa_shared(tempty_bar(acc), 0));
+    }
+    if (tma_store && lane == 0) bulk_wait_all();
+  }
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs done (MMAs retired, epilogues drained)
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "n"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tf32_tcgen05(const __grid_constant__ CUtensorMap map_a,
@@ -634,6 +887,48 @@ int launch_hub(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &
   return check_launch("gemm_hub_bf16x3_tcgen05");
 }
 
+template <int BN>
+int launch_hub_pair(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mc,
+                    int tma_store, const GemmEpi &ep, int64_t T, int64_t kp, cudaStream_t st) {
+  const int num_kb = (int)((T + 63) / 64);
+  constexpr int stage_bytes = BM * KB_BYTES + 3 * (BN / 2) * KB_BYTES;
+  size_t smem = 0;
+  int stages = tma_store ? ring_stages(stage_bytes, true, &smem) : 0;
+  if (stages == 0) {
+    tma_store = 0;
+    stages = ring_stages(stage_bytes, false, &smem);
+  }
+  if (stages == 0) {
+    set_error("gc_hub_gemm: pair tile does not fit shared memory");
+    return GC_ERR_UNSUPPORTED;
+  }
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(gemm_hub_pair_tcgen05<BN>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  });
+  if (attr_err != cudaSuccess) {
+    set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
+    return GC_ERR_CUDA;
+  }
+  const int m_pairs = (int)((ep.M + 2 * BM - 1) / (2 * BM));
+  const int n_tiles = (int)((ep.N + BN - 1) / BN);
+  const int64_t tiles = (int64_t)m_pairs * n_tiles;
+  const int clusters = (int)(tiles < sm_count() / 2 ? tiles : sm_count() / 2);
+  gemm_hub_pair_tcgen05<BN><<<2 * clusters, kGemmThreads, smem, st>>>(
+      ma, mb, mc, ep, num_kb, stages, m_pairs, n_tiles, tma_store, (int)kp);
+  return check_launch("gemm_hub_pair_tcgen05");
+}
+
+inline bool hub_pair_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("GNNC_HUB_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // X[hub_cols[t], f] * d[hub_cols[t]] -> three bf16 terms, transposed to the
 // K-major B operand Bt[q][f][t] (f < kp; rows f >= K are zero).  hi = bf16(x),
 // mid = bf16(x - hi), lo = bf16(x - hi - mid): hi + mid + lo carries x's full
@@ -821,6 +1116,21 @@ extern "C" int gc_hub_gemm_bf16x3(const void *A_hub, int64_t lda, int64_t n_rows
   if (tma_store) {
     rc = make_map(&mc, C, n_rows, K, ldc, 32, 16, CU_TENSOR_MAP_SWIZZLE_64B);
     if (rc) return rc;
+  }
+  if (hub_pair_enabled() && K > 16) {
+    // CTA pairs: N = pair_bn, each CTA stages pair_bn/2 rows of each B term
+    const int pbn = K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256;
+    if (kp % pbn == 0) {
+      CUtensorMap mbp;
+      rc = make_map(&mbp, Bt, 3 * kp, T, T, pbn / 2, 64, CU_TENSOR_MAP_SWIZZLE_128B, true);
+      if (rc) return rc;
+      switch (pbn) {
+        case 32: return launch_hub_pair<32>(ma, mbp, mc, tma_store, ep, T, kp, st);
+        case 64: return launch_hub_pair<64>(ma, mbp, mc, tma_store, ep, T, kp, st);
+        case 128: return launch_hub_pair<128>(ma, mbp, mc, tma_store, ep, T, kp, st);
+        default: return launch_hub_pair<256>(ma, mbp, mc, tma_store, ep, T, kp, st);
+      }
+    }
   }
   switch (bn) {
     case 16: return launch_hub<16>(ma, mb, mc, tma_store, ep, T, kp, st);
