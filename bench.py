@@ -369,36 +369,39 @@ def main():
     dyn = base == "dynamic"
     a_used = part.local if part is not None else (g.a_tilde if dyn else g.n_tilde)
     weighted = not (dyn and g.a_tilde.has_unit_values)
-    T = g.a_tilde._plans.get(("hubsplit-choice", K, not dyn), 0) if part is None else 0
+    split = g.a_tilde._plans.get(("hubsplit-choice", K, not dyn), 0) if part is None else 0
     roof, hub_roof = None, None
-    if T and tail_ms:
+    if split and tail_ms:
         # hybrid aggregation: the tail SpMM is the dominant kernel (HBM/L2
-        # roofline over its own edges, + the read-modify-write of C); the hub
-        # block is a tensor-core GEMM (bf16 roofline, 3 terms)
+        # roofline over its own edges, + the read-modify-write of C); the
+        # dense part is a tensor-core GEMM (bf16 roofline, 3 terms)
         from paper_2306_15155_b200 import hub as hubmod
 
-        plan = hubmod.hub_plan(g.a_tilde, T)
+        plan = hubmod.hub_plan(g.a_tilde, split)
         mt = plan.tail.nnz
         tail_bytes = spmm_alg_bytes(n, mt, K, weighted, dyn, dyn) + 4 * n * K
         ach = tail_bytes / (tail_ms * 1e-3) / 1e9
         traffic = None
         tfj = ROOT / "profiles" / "traffic.json"
         if tfj.exists():
-            traffic = json.loads(tfj.read_text()).get(f"{args.shape}/K{K}/{comp}/tail")
+            traffic = json.loads(tfj.read_text()).get(
+                f"{args.shape}/K{K}/{comp}/tail/{hubmod.spec_label(split)}")
             traffic = traffic if isinstance(traffic, int) else None
-        roof = {"kernel": "spmm_kernel (tail of the hub split)", "bound": "hbm", "achieved": round(ach, 1),
+        roof = {"kernel": "spmm_kernel (tail of the dense split)", "bound": "hbm", "achieved": round(ach, 1),
                 "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(ach / pk["hbm_gbs"], 3),
                 "traffic": traffic, "alg_bytes_per_launch": tail_bytes, "kernel_ms": round(tail_ms, 4),
                 "share_of_step": round(tail_ms / ms, 3), "peak_source": pk["source"],
                 "model": "edge-gather over the tail edges: 4(n+1)+4m_t[+4m_t values][+4m_t d_j]+4m_tK+4nK(+4nK C read)[+4n]",
                 "tail_edges": mt}
-        flops = 2 * n * T * K * 3
+        flops = 2 * plan.cells * K * 3
         tf = flops / (hub_ms * 1e-3) / 1e12
-        hub_roof = {"kernel": "gemm_hub_bf16x3_tcgen05", "bound": "tensor", "achieved": round(tf, 1),
+        hub_roof = {"kernel": "gemm_hub_pair_tcgen05 (dense part)", "bound": "tensor", "achieved": round(tf, 1),
                     "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": round(tf / pk["bf16_tflops"], 3),
-                    "kernel_ms": round(hub_ms, 4), "share_of_step": round(hub_ms / ms, 3), "T": T,
-                    "hub_edges": plan.hub_edges, "flops_per_launch": flops,
-                    "model": "2·n·T·K per bf16 term, 3 terms (exact fp32 split)"}
+                    "kernel_ms": round(hub_ms, 4), "share_of_step": round(hub_ms / ms, 3),
+                    "split": hubmod.spec_label(split), "dense_cells": plan.cells,
+                    "dense_edges": plan.hub_edges, "flops_per_launch": flops,
+                    "steps": getattr(plan, "steps", None),
+                    "model": "2·cells·K per bf16 term, 3 terms (exact fp32 split)"}
     elif spmm_ms:
         spmm_bytes = spmm_alg_bytes(a_used.n_rows, a_used.nnz, K, weighted, dyn, dyn)
         ach = spmm_bytes / (spmm_ms * 1e-3) / 1e9
@@ -431,7 +434,8 @@ def main():
                       "spmm_tail": tail_ms},
         "roofline": roof,
         "roofline_hub_gemm": hub_roof,
-        "hub_split": {"T": T, "autotune_ms": g.a_tilde._plans.get(("hubsplit-choice", K, not dyn, "times"))},
+        "dense_split": {"chosen": __import__("paper_2306_15155_b200.hub", fromlist=["spec_label"]).spec_label(split),
+                        "autotune_ms": g.a_tilde._plans.get(("hubsplit-choice", K, not dyn, "times"))},
         "setup": {"graph_gen_s": round(gen_s, 2), "prep_s": round(prep_s, 3),
                   "normalize_sddmm_ms": round(norm_ms, 3)},
     }

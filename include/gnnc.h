@@ -240,6 +240,22 @@ GNNC_API int gc_hub_gemm_bf16x3(const void *A_hub, int64_t lda, int64_t n_rows, 
                        const void *Bt, int64_t K, float *C, int64_t ldc, const float *d_row,
                        uint32_t flags, void *stream);
 
+/* Staircase of dense blocks (degree-rank order).  Step s (0 <= s < n_steps
+ * <= 8) is A_steps[s]: bf16 row-major [step_rows[s] x step_width[s]], the
+ * 0/1 adjacency of the step_rows[s] highest-degree rows (rank order) against
+ * the hub columns at positions [step_c0[s], step_c0[s] + step_width[s]) of
+ * the packed operand Bt (gc_hub_pack_bf16x3 over T hub columns in rank
+ * order).  Rows shrink and column ranges are consecutive across steps.  Rank
+ * row r of the result goes to C row row_map[r] (NULL: r):
+ *   C[row_map[r], f] = d_row[row_map[r]] * sum_{s: r < rows[s]} A_s[r, :] · B[.., c0_s ..]
+ * One CTA-pair tcgen05 launch; flags GC_RELU / GC_ACCUMULATE.  Requires
+ * gc_hub_stair_supported(K).                                               */
+GNNC_API int gc_hub_stair_supported(int64_t K);
+GNNC_API int gc_hub_stair_gemm_bf16x3(const void *const *A_steps, const int64_t *step_rows,
+                       const int64_t *step_c0, const int64_t *step_width, int32_t n_steps,
+                       const int32_t *row_map, const void *Bt, int64_t T, int64_t K, float *C,
+                       int64_t ldc, const float *d_row, uint32_t flags, void *stream);
+
 /* ---- multi-GPU row partition -----------------
  * nnz-balanced contiguous row blocks over a HOST copy of row_ptr (int64):
  *   bounds[0] = 0, bounds[P] = n, bounds[p] = first r with row_ptr[r] >=

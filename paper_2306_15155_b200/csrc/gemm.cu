@@ -449,13 +449,39 @@ __host__ __device__ constexpr uint32_t idesc_bf16_m256(int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((256u >> 4) << 24);
 }
 
+// Staircase of dense blocks (hub.py): step s is the 0/1 block of rows
+// [0, rows[s]) (rows in degree-rank order) x columns [c0[s], c0[s] + 64*nkb[s])
+// (column-degree-rank order, i.e. positions in the packed B operand).  Rows
+// shrink as columns grow, so the columns a rank-ordered M-tile reduces over
+// are a prefix of the steps; one accumulator per tile covers all of them and
+// the epilogue scatters row r to row_map[r] (nullptr: identity).  One step
+// with rows = n is the plain hub block.
+constexpr int kMaxSteps = 8;
+struct StairMaps {
+  CUtensorMap a[kMaxSteps];
+};
+struct StairArgs {
+  int n_steps;
+  int rows[kMaxSteps];
+  int c0[kMaxSteps];
+  int nkb[kMaxSteps];
+  const int32_t *row_map;
+};
+
+__device__ __forceinline__ int stair_kblocks(const StairArgs &sa, int m0) {
+  int t = 0;
+  for (int s = 0; s < sa.n_steps; ++s)
+    if (sa.rows[s] > m0) t += sa.nkb[s];
+  return t;
+}
+
 template <int BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
-    gemm_hub_pair_tcgen05(const __grid_constant__ CUtensorMap map_a,
+    gemm_hub_pair_tcgen05(const __grid_constant__ StairMaps maps,
                           const __grid_constant__ CUtensorMap map_b,
-                          const __grid_constant__ CUtensorMap map_c, const GemmEpi ep, int num_kb,
-                          int stages, int m_pairs, int n_tiles, int tma_store,
-                          int b_rows_per_term) {
+                          const __grid_constant__ CUtensorMap map_c, const GemmEpi ep,
+                          const StairArgs sarg, int stages, int m_pairs, int n_tiles,
+                          int tma_store, int b_rows_per_term) {
   constexpr int TERMS = 3;
   constexpr int BH = BN / 2;  // B rows per CTA per term
   constexpr uint32_t A_BYTES = BM * KB_BYTES;
@@ -483,7 +509,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const int n_tiles_total = m_pairs * n_tiles;
 
   if (warp == 1 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    for (int s = 0; s < sarg.n_steps; ++s)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.a[s]))
+                   : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
     for (int s = 0; s < stages; ++s) {
       mbar_init(full_bar(s), 2);   // leader expect_tx + peer arrive (leader's copy is used)
@@ -511,20 +539,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {  // ---------------- TMA producer (both CTAs) ----------------
       int it = 0;
       for (int tile = cluster_id; tile < n_tiles_total; tile += n_clusters) {
-        const int m0 = (tile / n_tiles) * (2 * BM) + (int)rank * BM;
+        const int mp = (tile / n_tiles) * (2 * BM);
+        const int m0 = mp + (int)rank * BM;
         const int n0 = (tile % n_tiles) * BN + (int)rank * BH;
-        for (int kb = 0; kb < num_kb; ++kb, ++it) {
-          const int s = it % stages;
-          mbar_wait(empty_bar(s), ((it / stages) & 1) ^ 1);
-          const uint32_t sa = base + (uint32_t)s * STAGE_BYTES;
-          const uint32_t lbar = mapa_shared(full_bar(s), 0);
-          if (leader) mbar_expect_tx(full_bar(s), 2 * STAGE_BYTES);
-          else mbar_arrive_cluster(lbar);
-          tma_load_2d_pair(sa, &map_a, lbar, kb * 64, m0);
+        for (int st = 0; st < sarg.n_steps; ++st) {
+          if (sarg.rows[st] <= mp) continue;  // pair-uniform: both CTAs load the same steps
+          for (int kb = 0; kb < sarg.nkb[st]; ++kb, ++it) {
+            const int s = it % stages;
+            mbar_wait(empty_bar(s), ((it / stages) & 1) ^ 1);
+            const uint32_t sa = base + (uint32_t)s * STAGE_BYTES;
+            const uint32_t lbar = mapa_shared(full_bar(s), 0);
+            if (leader) mbar_expect_tx(full_bar(s), 2 * STAGE_BYTES);
+            else mbar_arrive_cluster(lbar);
+            tma_load_2d_pair(sa, &maps.a[st], lbar, kb * 64, m0);  // rows >= rows[st]: zero fill
 #pragma unroll
-          for (int q = 0; q < TERMS; ++q)
-            tma_load_2d_pair(sa + A_BYTES + q * B_BYTES, &map_b, lbar, kb * 64,
-                             q * b_rows_per_term + n0);
+            for (int q = 0; q < TERMS; ++q)
+              tma_load_2d_pair(sa + A_BYTES + q * B_BYTES, &map_b, lbar, sarg.c0[st] + kb * 64,
+                               q * b_rows_per_term + n0);
+          }
         }
       }
     }
@@ -537,6 +569,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         mbar_wait(tempty_bar(acc), ((lt >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + (uint32_t)(acc * BN);
+        const int num_kb = stair_kblocks(sarg, (tile / n_tiles) * (2 * BM));
         for (int kb = 0; kb < num_kb; ++kb, ++it) {
           const int s = it % stages;
           mbar_wait(full_bar(s), (it / stages) & 1);
@@ -569,8 +602,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const int n0 = (tile % n_tiles) * BN;
       mbar_wait(tfull_bar(acc), (lt >> 1) & 1);
       tc_fence_after();
-      const int row = m0 + q * 32 + lane;
-      const bool row_ok = row < ep.M;
+      const int rrow = m0 + q * 32 + lane;  // rank-ordered row
+      const bool row_ok = rrow < ep.M;
+      const int row = (row_ok && sarg.row_map) ? __ldg(sarg.row_map + rrow) : rrow;
       const float rs = (row_ok && ep.row_scale) ? __ldg(ep.row_scale + row) : 1.0f;
       float *crow = ep.C + (int64_t)row * ep.ldc;
       const uint32_t taddr = tmem_base + (uint32_t)(acc * BN) + ((uint32_t)(q * 32) << 16);
@@ -888,9 +922,9 @@ int launch_hub(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &
 }
 
 template <int BN>
-int launch_hub_pair(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mc,
-                    int tma_store, const GemmEpi &ep, int64_t T, int64_t kp, cudaStream_t st) {
-  const int num_kb = (int)((T + 63) / 64);
+int launch_hub_pair(const StairMaps &maps, const StairArgs &sarg, const CUtensorMap &mb,
+                    const CUtensorMap &mc, int tma_store, const GemmEpi &ep, int64_t kp,
+                    cudaStream_t st) {
   constexpr int stage_bytes = BM * KB_BYTES + 3 * (BN / 2) * KB_BYTES;
   size_t smem = 0;
   int stages = tma_store ? ring_stages(stage_bytes, true, &smem) : 0;
@@ -916,9 +950,23 @@ int launch_hub_pair(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensor
   const int n_tiles = (int)((ep.N + BN - 1) / BN);
   const int64_t tiles = (int64_t)m_pairs * n_tiles;
   const int clusters = (int)(tiles < sm_count() / 2 ? tiles : sm_count() / 2);
+  // tiles are walked in rank order = descending reduction length, round-robin
+  // over the clusters (longest-first keeps the staircase balanced)
   gemm_hub_pair_tcgen05<BN><<<2 * clusters, kGemmThreads, smem, st>>>(
-      ma, mb, mc, ep, num_kb, stages, m_pairs, n_tiles, tma_store, (int)kp);
+      maps, mb, mc, ep, sarg, stages, m_pairs, n_tiles, tma_store, (int)kp);
   return check_launch("gemm_hub_pair_tcgen05");
+}
+
+inline int pair_bn(int64_t K) { return K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256; }
+
+template <typename... Args>
+int launch_hub_pair_bn(int pbn, Args &&...args) {
+  switch (pbn) {
+    case 32: return launch_hub_pair<32>(args...);
+    case 64: return launch_hub_pair<64>(args...);
+    case 128: return launch_hub_pair<128>(args...);
+    default: return launch_hub_pair<256>(args...);
+  }
 }
 
 inline bool hub_pair_enabled() {
@@ -1117,20 +1165,23 @@ extern "C" int gc_hub_gemm_bf16x3(const void *A_hub, int64_t lda, int64_t n_rows
     rc = make_map(&mc, C, n_rows, K, ldc, 32, 16, CU_TENSOR_MAP_SWIZZLE_64B);
     if (rc) return rc;
   }
-  if (hub_pair_enabled() && K > 16) {
-    // CTA pairs: N = pair_bn, each CTA stages pair_bn/2 rows of each B term
-    const int pbn = K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256;
-    if (kp % pbn == 0) {
-      CUtensorMap mbp;
-      rc = make_map(&mbp, Bt, 3 * kp, T, T, pbn / 2, 64, CU_TENSOR_MAP_SWIZZLE_128B, true);
-      if (rc) return rc;
-      switch (pbn) {
-        case 32: return launch_hub_pair<32>(ma, mbp, mc, tma_store, ep, T, kp, st);
-        case 64: return launch_hub_pair<64>(ma, mbp, mc, tma_store, ep, T, kp, st);
-        case 128: return launch_hub_pair<128>(ma, mbp, mc, tma_store, ep, T, kp, st);
-        default: return launch_hub_pair<256>(ma, mbp, mc, tma_store, ep, T, kp, st);
-      }
-    }
+  if (hub_pair_enabled() && K > 16 && kp % pair_bn(K) == 0) {
+    // CTA pairs: N = pair_bn, each CTA stages pair_bn/2 rows of each B term;
+    // the plain hub block is a one-step staircase
+    const int pbn = pair_bn(K);
+    CUtensorMap mbp;
+    rc = make_map(&mbp, Bt, 3 * kp, T, T, pbn / 2, 64, CU_TENSOR_MAP_SWIZZLE_128B, true);
+    if (rc) return rc;
+    StairMaps maps;
+    memset(&maps, 0, sizeof(maps));
+    maps.a[0] = ma;
+    StairArgs sarg{};
+    sarg.n_steps = 1;
+    sarg.rows[0] = (int)n_rows;
+    sarg.c0[0] = 0;
+    sarg.nkb[0] = (int)(T / 64);
+    sarg.row_map = nullptr;
+    return launch_hub_pair_bn(pbn, maps, sarg, mbp, mc, tma_store, ep, kp, st);
   }
   switch (bn) {
     case 16: return launch_hub<16>(ma, mb, mc, tma_store, ep, T, kp, st);
@@ -1139,4 +1190,60 @@ extern "C" int gc_hub_gemm_bf16x3(const void *A_hub, int64_t lda, int64_t n_rows
     case 128: return launch_hub<128>(ma, mb, mc, tma_store, ep, T, kp, st);
     default: return launch_hub<256>(ma, mb, mc, tma_store, ep, T, kp, st);
   }
+}
+
+extern "C" int gc_hub_stair_supported(int64_t K) {
+  return (hub_pair_enabled() && K > 16 && gc_hub_terms_rows(K) % pair_bn(K) == 0) ? 1 : 0;
+}
+
+extern "C" int gc_hub_stair_gemm_bf16x3(const void *const *A_steps, const int64_t *step_rows,
+                                        const int64_t *step_c0, const int64_t *step_width,
+                                        int32_t n_steps, const int32_t *row_map, const void *Bt,
+                                        int64_t T, int64_t K, float *C, int64_t ldc,
+                                        const float *d_row, uint32_t flags, void *stream) {
+  GC_REQUIRE(n_steps >= 1 && n_steps <= kMaxSteps, GC_ERR_VALUE,
+             "gc_hub_stair_gemm_bf16x3: 1..%d steps", kMaxSteps);
+  GC_REQUIRE(K >= 1 && T > 0 && T % 64 == 0 && ldc >= K, GC_ERR_SHAPE,
+             "gc_hub_stair_gemm_bf16x3: bad shape");
+  GC_REQUIRE((flags & ~(GC_RELU | GC_ACCUMULATE)) == 0, GC_ERR_VALUE,
+             "gc_hub_stair_gemm_bf16x3: unknown flags 0x%x", flags);
+  GC_REQUIRE(A_steps && step_rows && step_c0 && step_width && Bt && C, GC_ERR_VALUE,
+             "gc_hub_stair_gemm_bf16x3: null operand");
+  GC_REQUIRE(gc_hub_stair_supported(K), GC_ERR_UNSUPPORTED,
+             "gc_hub_stair_gemm_bf16x3: K=%lld has no CTA-pair tile", (long long)K);
+  GC_REQUIRE(aligned16(Bt), GC_ERR_UNSUPPORTED, "gc_hub_stair_gemm_bf16x3: Bt alignment");
+  StairMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  StairArgs sarg{};
+  sarg.n_steps = n_steps;
+  sarg.row_map = row_map;
+  for (int s = 0; s < n_steps; ++s) {
+    const int64_t r = step_rows[s], c0 = step_c0[s], w = step_width[s];
+    GC_REQUIRE(r >= 1 && r < INT32_MAX && w > 0 && w % 64 == 0 && c0 % 64 == 0 && c0 + w <= T,
+               GC_ERR_SHAPE, "gc_hub_stair_gemm_bf16x3: bad step %d", s);
+    GC_REQUIRE(s == 0 || (r <= step_rows[s - 1] && c0 == step_c0[s - 1] + step_width[s - 1]),
+               GC_ERR_SHAPE, "gc_hub_stair_gemm_bf16x3: steps must be a staircase");
+    GC_REQUIRE(A_steps[s] && aligned16(A_steps[s]), GC_ERR_VALUE,
+               "gc_hub_stair_gemm_bf16x3: step %d operand", s);
+    int rc = make_map(&maps.a[s], A_steps[s], r, w, w, BM, 64, CU_TENSOR_MAP_SWIZZLE_128B, true);
+    if (rc) return rc;
+    sarg.rows[s] = (int)r;
+    sarg.c0[s] = (int)c0;
+    sarg.nkb[s] = (int)(w / 64);
+  }
+  const int64_t kp = gc_hub_terms_rows(K);
+  const int pbn = pair_bn(K);
+  CUtensorMap mbp, mc;
+  int rc = make_map(&mbp, Bt, 3 * kp, T, T, pbn / 2, 64, CU_TENSOR_MAP_SWIZZLE_128B, true);
+  if (rc) return rc;
+  memset(&mc, 0, sizeof(mc));
+  // rank-ordered rows scatter through row_map: direct stores
+  const int tma_store = (row_map == nullptr && (ldc % 4) == 0 && aligned16(C) &&
+                         !(flags & GC_ACCUMULATE)) ? 1 : 0;
+  if (tma_store) {
+    rc = make_map(&mc, C, step_rows[0], K, ldc, 32, 16, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (rc) return rc;
+  }
+  GemmEpi ep{C, ldc, d_row, step_rows[0], K, flags};
+  return launch_hub_pair_bn(pbn, maps, sarg, mbp, mc, tma_store, ep, kp, as_stream(stream));
 }

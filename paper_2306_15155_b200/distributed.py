@@ -157,9 +157,9 @@ class CudaOps:
                     twin._unit = True
                     a._plans[key] = twin
                 pat = a._plans[key]
-            T = hub.choose_split(pat, b, hub_d[1], d_row=hub_d[0], values=vals)
-            if T:
-                return hub.hybrid_aggregate(pat, b, hub_d[1], T, d_row=hub_d[0], values=vals,
+            spec = hub.choose_split(pat, b, hub_d[1], d_row=hub_d[0], values=vals)
+            if spec:
+                return hub.hybrid_aggregate(pat, b, hub_d[1], spec, d_row=hub_d[0], values=vals,
                                             relu=relu, out=out, accumulate=accumulate)
         f = spmm if weighted else spmm_unweighted
         return f(a, b, d_row=d_row, d_col=d_col, relu=relu, out=out, accumulate=accumulate)

@@ -1,50 +1,107 @@
-"""Hybrid aggregation for power-law graphs: the dense hub block on the tensor
-cores, the sparse tail on the SpMM kernel.
+"""Hybrid aggregation for power-law graphs: dense blocks of the adjacency on
+the tensor cores, the sparse remainder on the SpMM kernel.
 
 On a dense power-law graph (Reddit-shaped: mean degree ~490) the SpMM is
 bound by L2 bandwidth, not HBM: every edge gathers a K-wide row of X and the
-most-referenced columns are gathered again and again.  Splitting the columns
-into the T most-referenced ("hub") columns and the rest turns the hub part of
+most-referenced columns are gathered again and again.  Ordering rows and
+columns by degree exposes dense regions of
 
     C = D Ã D X          (the reference's dynamic form, gcn.py:137-155;
                           precompute's Ñ = D Ã D, gcn.py:103-112)
 
-into a dense product whose operand tiles are reused from shared memory:
+that are cheaper as dense products whose operand tiles are reused from
+shared memory:
 
-    C_hub = D · A_hub · (D X)[hub_cols],   A_hub ∈ {0,1}^{n × T}
+    C_dense = D · A_dense · (D X)[dense columns],   A_dense ∈ {0,1}
 
-computed by ``gc_hub_gemm_bf16x3`` (tcgen05 kind::f16): A_hub is exact in
-bf16 and (D X)[hub_cols] is split into three bf16 terms that together carry
-its fp32 mantissa, so the hub part keeps fp32 precision.  The tail SpMM then
-accumulates the remaining columns on top (GC_ACCUMULATE).  Only the
-summation order differs from the plain SpMM.
+computed by tcgen05 kind::f16 GEMMs: the 0/1 blocks are exact in bf16 and
+(D X)[columns] is split into three bf16 terms that together carry its fp32
+mantissa (``gc_hub_pack_bf16x3``), so the dense part keeps fp32 precision.
+The SpMM then accumulates the remaining edges on top (GC_ACCUMULATE).  Only
+the summation order differs from the plain SpMM.
+
+Two plans:
+
+* ``HubPlan`` (block, T): every row against the T most-referenced columns
+  (one dense n × T block; supports row ranges, any K).
+* ``StairPlan`` ("stair", δ): rows and columns in degree-rank order; step s
+  is the block rows [0, R_s) × columns [C_s, C_{s+1}) with R_s the last row
+  band whose density in that column band is ≥ δ — a staircase hugging the
+  dense corner (the high-degree rows are dense far beyond the top columns).
+  All steps run in ONE CTA-pair GEMM whose rank-ordered tiles reduce over a
+  prefix of the steps (``gc_hub_stair_gemm_bf16x3``), scattering rows back
+  through the rank permutation.
 
 The split applies to a unit-valued Ã (the reference's own generated graphs and
-``has_unit_values`` case); T is chosen per (pattern, K) by timing the
+``has_unit_values`` case); the plan is chosen per (pattern, K) by timing the
 candidates once, like the SpMM variant autotuner (reference tiling.py:311-364
-is the CPU analogue).  "0" in GNNC_HUB_SPLIT disables it; a number forces T.
+is the CPU analogue).  GNNC_HUB_SPLIT: "auto" (default), "0" (off), "<T>"
+(block plan), "stair:<δ in permille>".
 """
 
 from __future__ import annotations
 
 import os
 
+import numpy as np
 import torch
 
 from . import _native as nat
 from .sparse import CsrMatrix, ShapeError, _ld, _require_cuda, _spmm, _stream, _timed_call
 
-HUB_SPLIT = os.environ.get("GNNC_HUB_SPLIT", "auto")  # auto | 0 | <T>
+HUB_SPLIT = os.environ.get("GNNC_HUB_SPLIT", "auto")
 HUB_T_CANDIDATES = (1024, 2048, 4096, 8192)
+STAIR_DELTAS = (0.015, 0.03, 0.06)  # density thresholds tried by the autotuner
 HUB_MIN_NNZ = 1 << 24            # smaller graphs stay on the SpMM alone
-HUB_MIN_DENSITY = 0.02           # mean density of the hub block worth a dense product
-HUB_MEM_BUDGET = 8 << 30         # bytes of A_hub per pattern
+HUB_MIN_DENSITY = 0.02           # mean density of a block worth a dense product
+HUB_MEM_BUDGET = 8 << 30         # bytes of dense blocks per pattern
+STAIR_MAX_STEPS = 8
+STAIR_CLUSTERS = 74              # CTA pairs of a B200 (balance bound of the top tile)
 
 
-class HubPlan:
+def _unit_tail(a: CsrMatrix, keep: torch.Tensor, rows: torch.Tensor) -> CsrMatrix:
+    cnt = torch.bincount(rows[keep], minlength=a.n_rows)
+    rp = torch.zeros(a.n_rows + 1, dtype=torch.int32, device=a.device)
+    rp[1:] = torch.cumsum(cnt, 0).to(torch.int32)
+    tail = CsrMatrix(a.n_rows, a.n_cols, rp, a.col_idx[keep].contiguous(),
+                     torch.ones(keep.numel(), dtype=torch.float32, device=a.device),
+                     validate=False, device=a.device)
+    tail._unit = True
+    return tail
+
+
+class _TailMixin:
+    """The remainder pattern and its row blocks, carrying unit values or a
+    same-pattern matrix's values (e.g. Ñ's) gathered at the tail positions."""
+
+    def _init_tail(self, a: CsrMatrix, keep_mask: torch.Tensor, rows: torch.Tensor):
+        keep = torch.nonzero(keep_mask).flatten()
+        self.keep = keep
+        self.tail = _unit_tail(a, keep, rows)
+        self.hub_edges = a.nnz - keep.numel()
+        self._tail_vals: dict = {}
+
+    def tail_block(self, values: torch.Tensor | None, lo: int, hi: int) -> CsrMatrix:
+        vkey = None if values is None else (values.data_ptr(), values._version)
+        if vkey not in self._tail_vals:
+            self._tail_vals = {k: v for k, v in self._tail_vals.items() if k is None}
+            self._tail_vals[vkey] = ({}, self.tail if values is None
+                                     else self.tail.with_values(values[self.keep].contiguous()))
+        blocks, full = self._tail_vals[vkey]
+        if (lo, hi) == (0, full.n_rows):
+            return full
+        if (lo, hi) not in blocks:
+            blocks[(lo, hi)] = full.take_rows(lo, hi)
+            blocks[(lo, hi)]._unit = values is None
+        return blocks[(lo, hi)]
+
+
+class HubPlan(_TailMixin):
     """Column split of one pattern: hub columns, the dense 0/1 hub block
     (bf16, row-major n × T) and the tail pattern (CSR without the hub
     columns; ``keep`` maps tail positions back to the full pattern)."""
+
+    kind = "block"
 
     def __init__(self, a: CsrMatrix, T: int):
         if T % 64 or T <= 0 or T > a.n_cols:
@@ -61,67 +118,199 @@ class HubPlan:
         self.hub_cols = hub.to(torch.int32).contiguous()
         self.a_hub = torch.zeros(a.n_rows, T, dtype=torch.bfloat16, device=dev)
         self.a_hub[rows[is_hub], colpos[is_hub]] = 1.0
-        keep = torch.nonzero(~is_hub).flatten()
-        cnt = torch.bincount(rows[keep], minlength=a.n_rows)
-        rp = torch.zeros(a.n_rows + 1, dtype=torch.int32, device=dev)
-        rp[1:] = torch.cumsum(cnt, 0).to(torch.int32)
-        self.keep = keep
-        self.hub_edges = int(is_hub.sum())
-        self.tail = CsrMatrix(a.n_rows, a.n_cols, rp, a.col_idx[keep].contiguous(),
-                              torch.ones(keep.numel(), dtype=torch.float32, device=dev),
-                              validate=False, device=dev)
-        self.tail._unit = True
-        self._tail_vals: dict = {}
-
-    def tail_block(self, values: torch.Tensor | None, lo: int, hi: int) -> CsrMatrix:
-        """Rows [lo, hi) of the tail pattern, carrying ``values`` (a
-        same-pattern matrix's values, e.g. Ñ's, gathered at the tail positions)
-        or unit values; cached per (values tensor, row range)."""
-        vkey = None if values is None else (values.data_ptr(), values._version)
-        if vkey not in self._tail_vals:
-            self._tail_vals = {k: v for k, v in self._tail_vals.items() if k is None}
-            self._tail_vals[vkey] = ({}, self.tail if values is None
-                                     else self.tail.with_values(values[self.keep].contiguous()))
-        blocks, full = self._tail_vals[vkey]
-        if (lo, hi) == (0, full.n_rows):
-            return full
-        if (lo, hi) not in blocks:
-            blocks[(lo, hi)] = full.take_rows(lo, hi)
-            blocks[(lo, hi)]._unit = values is None
-        return blocks[(lo, hi)]
+        self.cells = a.n_rows * T
+        self._init_tail(a, ~is_hub, rows)
 
 
-def hub_plan(a: CsrMatrix, T: int) -> HubPlan:
-    key = ("hubsplit", int(T))
+class StairPlan(_TailMixin):
+    """Degree-rank staircase of dense blocks (see the module docstring)."""
+
+    kind = "stair"
+
+    def __init__(self, a: CsrMatrix, delta: float, *, n_clusters: int = STAIR_CLUSTERS,
+                 first_band: int = 1024):
+        dev = a.device
+        col = a.col_idx.long()
+        ccount = torch.bincount(col, minlength=a.n_cols)
+        corder = torch.argsort(ccount, descending=True, stable=True)
+        crank = torch.empty_like(corder)
+        crank[corder] = torch.arange(a.n_cols, device=dev)
+        rdeg = a.degrees()
+        rorder = torch.argsort(rdeg, descending=True, stable=True)
+        rrank = torch.empty_like(rorder)
+        rrank[rorder] = torch.arange(a.n_rows, device=dev)
+        rows = a.row_of_nnz()
+        er, ec = rrank[rows], crank[col]
+        self.steps = self._staircase(a, er, ec, delta, n_clusters, first_band)
+        if not self.steps:
+            raise ValueError("stair split: no block reaches the density threshold")
+        C = self.steps[-1][1] + self.steps[-1][2]
+        self.T = C
+        self.delta = delta
+        self.hub_cols = corder[:C].to(torch.int32).contiguous()
+        self.row_map = rorder.to(torch.int32).contiguous()
+        self.rows0 = self.steps[0][0]
+        # step of each covered edge: column rank band, then the row limit
+        c_starts = torch.tensor([s[1] for s in self.steps], device=dev)
+        r_limits = torch.tensor([s[0] for s in self.steps], device=dev)
+        in_cols = ec < C
+        step = torch.bucketize(ec.clamp(max=C - 1), c_starts, right=True) - 1
+        covered = in_cols & (er < r_limits[step])
+        self.blocks = []
+        for s, (R, c0, W) in enumerate(self.steps):
+            blk = torch.zeros(R, W, dtype=torch.bfloat16, device=dev)
+            sel = covered & (step == s)
+            blk[er[sel], ec[sel] - c0] = 1.0
+            self.blocks.append(blk)
+        self.cells = sum(R * W for R, _, W in self.steps)
+        self._np_rows = np.array([s[0] for s in self.steps], np.int64)
+        self._np_c0 = np.array([s[1] for s in self.steps], np.int64)
+        self._np_w = np.array([s[2] for s in self.steps], np.int64)
+        self._np_ptrs = np.array([b.data_ptr() for b in self.blocks], np.uint64)
+        self._init_tail(a, ~covered, rows)
+
+    @staticmethod
+    def _bands(n: int, first: int = 1024) -> list[int]:
+        b, x = [0], first
+        while x < n:
+            b.append(x)
+            x *= 2
+        b.append(n)
+        return b
+
+    @classmethod
+    def _staircase(cls, a: CsrMatrix, er, ec, delta, n_clusters,
+                   first_band: int = 1024) -> list[tuple[int, int, int]]:
+        """[(R_s, C_s, W_s)]: column bands of doubling width in rank order
+        (multiples of 64), each taking the leading row bands whose density is
+        >= delta; rows never grow; stop when a step would make the longest
+        (top) tile's reduction exceed the mean per-cluster load."""
+        rb = cls._bands(a.n_rows, first_band)
+        cmax = a.n_cols // 64 * 64
+        if cmax < 64:
+            return []
+        cb = [c for c in cls._bands(cmax, first_band) if c <= cmax]
+        if cb[-1] != cmax:
+            cb.append(cmax)
+        dev = er.device
+        ri = torch.bucketize(er, torch.tensor(rb[1:-1], device=dev), right=True)
+        ci = torch.bucketize(ec, torch.tensor(cb[1:-1], device=dev), right=True)
+        valid = ec < cmax
+        H = torch.zeros((len(rb) - 1) * (len(cb) - 1), dtype=torch.int64, device=dev)
+        H.index_add_(0, (ri * (len(cb) - 1) + ci)[valid], torch.ones_like(ri[valid]))
+        H = H.view(len(rb) - 1, len(cb) - 1).cpu().numpy()
+        steps: list[tuple[int, int, int]] = []
+        prev_r = a.n_rows
+        work = 0.0  # pair k-blocks of the steps taken
+        for s in range(len(cb) - 1):
+            W = cb[s + 1] - cb[s]
+            R = 0
+            for b in range(len(rb) - 1):
+                if H[b, s] / ((rb[b + 1] - rb[b]) * W) < delta:
+                    break
+                R = rb[b + 1]
+            R = min(R, prev_r)
+            if R < first_band or len(steps) == STAIR_MAX_STEPS:
+                break
+            w_new = work + R * W / (256.0 * 64.0)
+            if steps and cb[s + 1] / 64.0 > w_new / n_clusters:
+                break  # the top tile would outlast the average cluster
+            steps.append((R, cb[s], W))
+            work, prev_r = w_new, R
+        return steps
+
+
+def _parse_spec(spec):
+    """0 | T (block plan) | ("stair", permille) | "stair:<permille>" | "<T>"."""
+    if isinstance(spec, tuple):
+        return spec
+    if isinstance(spec, str) and spec.startswith("stair:"):
+        return ("stair", int(spec.split(":")[1]))
+    return int(spec)
+
+
+def spec_label(spec) -> str:
+    spec = _parse_spec(spec)
+    return f"stair:{spec[1]}" if isinstance(spec, tuple) else str(spec)
+
+
+def hub_plan(a: CsrMatrix, spec):
+    spec = _parse_spec(spec)
+    key = ("hubsplit", spec)
     if key not in a._plans:
-        a._plans[key] = HubPlan(a, T)
+        if isinstance(spec, tuple):
+            a._plans[key] = StairPlan(a, spec[1] / 1000.0)
+        else:
+            a._plans[key] = HubPlan(a, spec)
     return a._plans[key]
 
 
-def pack(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, T: int) -> torch.Tensor:
-    """The hub operand (D X)[hub_cols] as three bf16 terms, K-major."""
-    plan = hub_plan(a, T)
+def pack(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec) -> torch.Tensor:
+    """The dense-part operand (D X)[hub_cols] as three bf16 terms, K-major."""
+    plan = hub_plan(a, spec)
     lib = nat.load()
     K = x.shape[1]
     kp = int(lib.gc_hub_terms_rows(K))
-    bt = torch.empty(3 * kp * T, dtype=torch.bfloat16, device=x.device)
-    nat.check(lib.gc_hub_pack_bf16x3(x.data_ptr(), _ld(x), K, plan.hub_cols.data_ptr(), T,
+    bt = torch.empty(3 * kp * plan.T, dtype=torch.bfloat16, device=x.device)
+    nat.check(lib.gc_hub_pack_bf16x3(x.data_ptr(), _ld(x), K, plan.hub_cols.data_ptr(), plan.T,
                                      d.data_ptr(), bt.data_ptr(), _stream(x.device)), "hub_pack")
     return bt
 
 
-def hybrid_aggregate(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, T: int, *,
+def dense_part(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, out: torch.Tensor, *,
+               d_row: torch.Tensor, accumulate: bool = False, packed=None,
+               rows: tuple[int, int] | None = None) -> None:
+    """out (rows [lo, hi) of C, or all of C) = / += D_row · A_dense · (D X)[...]."""
+    plan = hub_plan(a, spec)
+    dev = x.device
+    lib = nat.load()
+    st = _stream(dev)
+    K = x.shape[1]
+    bt = packed if packed is not None else pack(a, x, d, spec)
+    flags = nat.GC_ACCUMULATE if accumulate else 0
+    if plan.kind == "block":
+        lo, hi = rows if rows is not None else (0, a.n_rows)
+        a_hub = plan.a_hub[lo:hi]
+        dr = d_row[lo:hi]
+        nat.check(_timed_call("hub_gemm", dev, lambda: lib.gc_hub_gemm_bf16x3(
+            a_hub.data_ptr(), plan.T, hi - lo, plan.T, bt.data_ptr(), K, out.data_ptr(), _ld(out),
+            dr.data_ptr(), flags, st)), "hub_gemm")
+        return
+    if rows is not None and tuple(rows) != (0, a.n_rows):
+        raise ShapeError("stair split: the dense part covers all rows (rank-ordered tiles)")
+    if plan.rows0 < a.n_rows and not accumulate:
+        out.zero_()  # rows outside every step receive only the tail
+    nat.check(_timed_call("hub_gemm", dev, lambda: lib.gc_hub_stair_gemm_bf16x3(
+        plan._np_ptrs.ctypes.data, plan._np_rows.ctypes.data, plan._np_c0.ctypes.data,
+        plan._np_w.ctypes.data, len(plan.steps), plan.row_map.data_ptr(), bt.data_ptr(), plan.T,
+        K, out.data_ptr(), _ld(out), d_row.data_ptr(), flags, st)), "hub_stair_gemm")
+
+
+def tail_part(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, out: torch.Tensor, *,
+              d_row: torch.Tensor, values=None, relu=False, rows: tuple[int, int] | None = None):
+    """out (rows [lo, hi)) += the remaining edges (ReLU on the total)."""
+    plan = hub_plan(a, spec)
+    lo, hi = rows if rows is not None else (0, a.n_rows)
+    tail = plan.tail_block(values, lo, hi)
+    if values is None:
+        _spmm(tail, x, weighted=False, d_row=d_row[lo:hi], d_col=d, relu=relu, out=out,
+              accumulate=True, timer="spmm_tail")
+    else:
+        _spmm(tail, x, weighted=True, relu=relu, out=out, accumulate=True, timer="spmm_tail")
+
+
+def hybrid_aggregate(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, *,
                      d_row: torch.Tensor | None = None, values: torch.Tensor | None = None,
                      relu: bool = False, out: torch.Tensor | None = None,
                      accumulate: bool = False, rows: tuple[int, int] | None = None,
                      packed: torch.Tensor | None = None) -> torch.Tensor:
-    """C = epi(D_row Ã D X) for a unit-valued pattern ``a`` via the hub split
-    (``d`` scales the columns; ``d_row`` the rows, default ``d`` itself for a
-    square pattern).  ``values`` (optional) are a same-pattern matrix's values
-    used for the tail instead of d_i·d_j (the precompute composition streams
-    Ñ's values).  ``accumulate``: C += ... (ReLU on the total).  ``rows=(lo,
-    hi)`` computes that row block only (``out`` then has hi-lo rows);
-    ``packed`` reuses one ``pack`` across row blocks."""
+    """C = epi(D_row Ã D X) for a unit-valued pattern ``a`` via the dense/tail
+    split ``spec`` (``d`` scales the columns; ``d_row`` the rows, default
+    ``d`` itself for a square pattern).  ``values`` (optional) are a
+    same-pattern matrix's values used for the tail instead of d_i·d_j (the
+    precompute composition streams Ñ's values).  ``accumulate``: C += ...
+    (ReLU on the total).  ``rows=(lo, hi)`` (block plans only) computes that
+    row block (``out`` then has hi-lo rows); ``packed`` reuses one ``pack``."""
     dev = _require_cuda(a.col_idx, x, d)
     if x.dim() != 2 or x.shape[0] != a.n_cols or x.stride(1) != 1:
         raise ShapeError("hybrid_aggregate: x must be a row-major n_cols x K tensor")
@@ -131,37 +320,24 @@ def hybrid_aggregate(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, T: int, *,
         d_row = d
     K = x.shape[1]
     lo, hi = rows if rows is not None else (0, a.n_rows)
-    plan = hub_plan(a, T)
     if out is None:
         if accumulate:
             raise ValueError("hybrid_aggregate: accumulate needs an output")
         out = torch.empty(hi - lo, K, dtype=torch.float32, device=dev)
     elif tuple(out.shape) != (hi - lo, K) or out.stride(1) != 1:
         raise ShapeError(f"hybrid_aggregate: out must be a row-major {hi - lo}x{K} tensor")
-    lib = nat.load()
-    st = _stream(dev)
-    tail = plan.tail_block(values, lo, hi)
-    a_hub = plan.a_hub[lo:hi]
-    dr = d_row[lo:hi]
-    flags = nat.GC_ACCUMULATE if accumulate else 0
 
     def run():
-        bt = packed if packed is not None else pack(a, x, d, T)
-        nat.check(_timed_call("hub_gemm", dev, lambda: lib.gc_hub_gemm_bf16x3(
-            a_hub.data_ptr(), T, hi - lo, T, bt.data_ptr(), K, out.data_ptr(), _ld(out),
-            dr.data_ptr(), flags, st)), "hub_gemm")
-        if values is None:
-            _spmm(tail, x, weighted=False, d_row=dr, d_col=d, relu=relu, out=out,
-                  accumulate=True, timer="spmm_tail")
-        else:
-            _spmm(tail, x, weighted=True, relu=relu, out=out, accumulate=True, timer="spmm_tail")
+        dense_part(a, x, d, spec, out, d_row=d_row, accumulate=accumulate, packed=packed,
+                   rows=rows)
+        tail_part(a, x, d, spec, out, d_row=d_row, values=values, relu=relu, rows=rows)
         return 0
 
     _timed_call("spmm", dev, run)
     return out
 
 
-def _candidates(a: CsrMatrix) -> list[int]:
+def _block_candidates(a: CsrMatrix) -> list[int]:
     counts = torch.bincount(a.col_idx.long(), minlength=a.n_cols)
     top = torch.sort(counts, descending=True).values.double().cumsum(0)
     out = []
@@ -173,11 +349,27 @@ def _candidates(a: CsrMatrix) -> list[int]:
     return out
 
 
+def _candidates(a: CsrMatrix, K: int) -> list:
+    cands: list = list(_block_candidates(a))
+    if nat.load().gc_hub_stair_supported(K):
+        for dl in STAIR_DELTAS:
+            spec = ("stair", int(round(dl * 1000)))
+            try:
+                plan = hub_plan(a, spec)
+            except ValueError:
+                continue
+            if plan.cells * 2 <= HUB_MEM_BUDGET:
+                cands.append(spec)
+            else:
+                a._plans.pop(("hubsplit", spec), None)
+    return cands
+
+
 def choose_split(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, *,
-                 d_row: torch.Tensor | None = None, values: torch.Tensor | None = None) -> int:
-    """T for (pattern, K): 0 (plain SpMM) unless a hub split is measurably
-    faster.  Every candidate is timed once (median of 3 after a warm launch)
-    on the first call and the choice is cached on the pattern."""
+                 d_row: torch.Tensor | None = None, values: torch.Tensor | None = None):
+    """Split spec for (pattern, K): 0 (plain SpMM) unless a dense split is
+    measurably faster.  Every candidate is timed once (median of 3 after a
+    warm launch) on the first call and the choice is cached on the pattern."""
     mode = str(HUB_SPLIT)
     if mode == "0" or not a.has_unit_values:
         return 0
@@ -186,7 +378,7 @@ def choose_split(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, *,
             return 0
         d_row = d
     if mode != "auto":
-        return int(mode)
+        return _parse_spec(mode)
     K = x.shape[1]
     key = ("hubsplit-choice", int(K), values is not None)
     if key in a._plans:
@@ -194,7 +386,7 @@ def choose_split(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, *,
     if a.nnz < HUB_MIN_NNZ or x.stride(1) != 1:
         a._plans[key] = 0
         return 0
-    cands = _candidates(a)
+    cands = _candidates(a, K)
     if not cands:
         a._plans[key] = 0
         return 0
@@ -217,15 +409,15 @@ def choose_split(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, *,
         return sorted(e0.elapsed_time(e1) for e0, e1 in ev)[1]
 
     times = {0: timed(plain)}
-    for T in cands:
-        times[T] = timed(lambda T=T: hybrid_aggregate(a, x, d, T, d_row=d_row, values=values,
-                                                      out=scratch))
+    for spec in cands:
+        times[spec] = timed(lambda spec=spec: hybrid_aggregate(a, x, d, spec, d_row=d_row,
+                                                               values=values, out=scratch))
     best = min(times, key=times.get)
-    if best and times[best] >= 0.97 * times[0]:
+    if best != 0 and times[best] >= 0.97 * times[0]:
         best = 0
-    for T in cands:  # keep only the chosen block resident
-        if T != best:
-            a._plans.pop(("hubsplit", T), None)
+    for spec in cands:  # keep only the chosen plan resident
+        if spec != best:
+            a._plans.pop(("hubsplit", spec), None)
     a._plans[key] = best
-    a._plans[key + ("times",)] = {str(T): round(t, 4) for T, t in times.items()}
+    a._plans[key + ("times",)] = {spec_label(s): round(t, 4) for s, t in times.items()}
     return best

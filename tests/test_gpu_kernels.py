@@ -658,3 +658,67 @@ def test_host_pipelined_layer_with_hub_split(oracle, hub_pl, comp, order, monkey
     assert not out.is_cuda and ("hubsplit", 64) in g.a_tilde._plans
     ref = oracle.gcn_layer(og, h.astype(np.float64), w.astype(np.float64), comp, order)
     assert oracle.rel_err(out.numpy(), ref) <= 1e-4
+
+
+@pytest.fixture(scope="module")
+def stair_pl():
+    a = graphs.synthetic_graph("rmat", 6000, 300000, seed=5, device=DEV)
+    return gc.add_self_loops(a)
+
+
+@pytest.mark.parametrize("K", [24, 32, 64, 96, 128, 256, 512])
+@pytest.mark.parametrize("precompute", [False, True])
+def test_stair_split_matches_oracle(oracle, stair_pl, K, precompute):
+    """Multi-step staircase (rank-ordered rows scattered by row_map, rows
+    outside every step zero-filled before the tail) vs the oracle."""
+    from paper_2306_15155_b200 import _native as nat
+    from paper_2306_15155_b200 import hub
+    if not nat.load().gc_hub_stair_supported(K):
+        pytest.skip("no CTA-pair tile for this K")
+    g = gc.NormalizedGraph.from_adjacency(stair_pl).with_precomputed()
+    a = g.a_tilde
+    spec = ("stair", 50)
+    a._plans[("hubsplit", spec)] = hub.StairPlan(a, 0.05, n_clusters=1, first_band=256)
+    plan = hub.hub_plan(a, spec)
+    assert len(plan.steps) >= 2 and plan.rows0 < a.n_rows
+    og = oracle.GcnGraph.from_adjacency(to_oracle(oracle, stair_pl))
+    rng = np.random.default_rng(K)
+    x = f32(rng.uniform(-0.5, 0.5, (a.n_rows, K)))
+    d = g.d_inv_sqrt.to(DEV)
+    vals = g.n_tilde.values if precompute else None
+    out = hub.hybrid_aggregate(a, torch.from_numpy(x).to(DEV), d, spec, values=vals, relu=True)
+    ref = np.maximum(oracle.spmm(og.n_tilde, x), 0)
+    assert oracle.rel_err(out.cpu().numpy(), ref) < SP_TOL
+    # accumulate form (used by the multi-GPU remote pass)
+    base = torch.from_numpy(f32(rng.uniform(-1, 1, (a.n_rows, K)))).to(DEV)
+    acc = base.clone()
+    hub.hybrid_aggregate(a, torch.from_numpy(x).to(DEV), d, spec, values=vals, out=acc,
+                         accumulate=True)
+    ref2 = base.cpu().numpy().astype(np.float64) + oracle.spmm(og.n_tilde, x)
+    assert oracle.rel_err(acc.cpu().numpy(), ref2) < SP_TOL
+
+
+def test_host_pipelined_layer_with_stair_split(oracle, stair_pl, monkeypatch):
+    from paper_2306_15155_b200 import gcn as gcn_mod
+    from paper_2306_15155_b200 import hub
+    g = gc.NormalizedGraph.from_adjacency(stair_pl).with_precomputed()
+    a = g.a_tilde
+    spec = ("stair", 50)
+    a._plans[("hubsplit", spec)] = hub.StairPlan(a, 0.05, n_clusters=1, first_band=256)
+    monkeypatch.setattr(hub, "HUB_SPLIT", "stair:50")
+    monkeypatch.setattr(gcn_mod, "HOST_PIPELINE_BLOCKS", 3)
+    og = oracle.GcnGraph.from_adjacency(to_oracle(oracle, stair_pl))
+    rng = np.random.default_rng(9)
+    h = f32(rng.uniform(-0.5, 0.5, (a.n_rows, 64)))
+    w = f32(rng.uniform(-0.5, 0.5, (64, 32)))
+    for comp, order in (("precompute", "update_first"), ("dynamic", "aggregate_first")):
+        spec_l = gc.GcnLayerSpec(64, 32, w, composition=comp, order=order)
+        gc.set_gemm_precision("fp32")
+        try:
+            out = gc.gcn_layer(g, torch.from_numpy(h).pin_memory(), spec_l)
+            dev_out = gc.gcn_layer(g, torch.from_numpy(h).to(DEV), spec_l).cpu()
+        finally:
+            gc.set_gemm_precision("tf32")
+        ref = oracle.gcn_layer(og, h.astype(np.float64), w.astype(np.float64), comp, order)
+        assert oracle.rel_err(out.numpy(), ref) <= 1e-4
+        assert oracle.rel_err(dev_out.numpy(), ref) <= 1e-4

@@ -315,3 +315,28 @@ def test_hub_plan_partitions_the_pattern():
     assert torch.equal(rows.to_dense(), plan.tail.to_dense()[100:700])
     with pytest.raises(gc.ShapeError):
         hub.HubPlan(a, 100)
+
+
+def test_stair_plan_partitions_the_pattern():
+    """The degree-rank staircase (hub.StairPlan): blocks + tail partition the
+    edges, rows shrink along the staircase, block cells are the adjacency of
+    the rank-ordered rows/columns."""
+    from paper_2306_15155_b200 import hub
+
+    a = graphs.synthetic_graph("rmat", 6000, 300000, seed=5, device="cpu")
+    plan = hub.StairPlan(a, 0.05, n_clusters=1, first_band=256)
+    assert len(plan.steps) >= 2
+    rows_seq = [r for r, _, _ in plan.steps]
+    assert rows_seq == sorted(rows_seq, reverse=True)
+    for (_, c0, w), (_, c1, _) in zip(plan.steps, plan.steps[1:]):
+        assert c1 == c0 + w and w % 64 == 0
+    dense = a.to_dense()
+    cover = torch.zeros_like(dense)
+    for (R, c0, W), blk in zip(plan.steps, plan.blocks):
+        r_ids = plan.row_map[:R].long()
+        c_ids = plan.hub_cols[c0:c0 + W].long()
+        assert torch.equal(blk.float(), dense[r_ids][:, c_ids])
+        cover[r_ids.unsqueeze(1), c_ids.unsqueeze(0)] = blk.float()
+    assert torch.equal(cover + plan.tail.to_dense(), dense)
+    assert plan.hub_edges + plan.tail.nnz == a.nnz
+    assert plan.hub_edges == int(sum(b.float().sum() for b in plan.blocks))
