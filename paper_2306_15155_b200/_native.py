@@ -8,6 +8,7 @@ raises if the library or the device is missing.  Host-only entry points
 from __future__ import annotations
 
 import ctypes
+import os
 import re
 from pathlib import Path
 
@@ -102,7 +103,8 @@ def load(build_if_missing: bool = True):
         from ._build import build
 
         build()
-    lib = ctypes.CDLL(str(LIB))
+    # GNNC_LIB_PATH: load another build of the same ABI (A/B experiments)
+    lib = ctypes.CDLL(os.environ.get("GNNC_LIB_PATH", str(LIB)))
     for name, (res, args) in _SIGNATURES.items():
         fn = getattr(lib, name)
         fn.restype = res
