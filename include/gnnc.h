@@ -241,7 +241,7 @@ GNNC_API int gc_hub_gemm_bf16x3(const void *A_hub, int64_t lda, int64_t n_rows, 
                        uint32_t flags, void *stream);
 
 /* Staircase of dense blocks (degree-rank order).  Step s (0 <= s < n_steps
- * <= 8) is A_steps[s]: bf16 row-major [step_rows[s] x step_width[s]], the
+ * <= 16) is A_steps[s]: bf16 row-major [step_rows[s] x step_width[s]], the
  * 0/1 adjacency of the step_rows[s] highest-degree rows (rank order) against
  * the hub columns at positions [step_c0[s], step_c0[s] + step_width[s]) of
  * the packed operand Bt (gc_hub_pack_bf16x3 over T hub columns in rank
@@ -249,12 +249,24 @@ GNNC_API int gc_hub_gemm_bf16x3(const void *A_hub, int64_t lda, int64_t n_rows, 
  * row r of the result goes to C row row_map[r] (NULL: r):
  *   C[row_map[r], f] = d_row[row_map[r]] * sum_{s: r < rows[s]} A_s[r, :] · B[.., c0_s ..]
  * One CTA-pair tcgen05 launch; flags GC_RELU / GC_ACCUMULATE.  Requires
- * gc_hub_stair_supported(K).                                               */
+ * gc_hub_stair_supported(K).  Optional static schedule (device int32):
+ * n_clusters CTA pairs, pair c runs work items items[cluster_start[c] ..
+ * cluster_start[c+1]), item = {tile, first k-block, end k-block (-1: to the
+ * end), workspace slot (-1: write C)}, tile = m_pair * n_tiles + n_tile
+ * (m_pair: 256 rank-ordered rows, n_tile: gc_hub_stair_pair_bn(K) columns);
+ * NULL: round-robin whole tiles.  Split-K: items with a slot write their
+ * (row-scaled) partial tile to workspace[slot][256][pair_bn]; fixups
+ * {tile, first slot, slot count, 0} then add the partials to C in slot
+ * order (deterministic; no GC_RELU with split items).                      */
 GNNC_API int gc_hub_stair_supported(int64_t K);
+GNNC_API int gc_hub_stair_pair_bn(int64_t K);
 GNNC_API int gc_hub_stair_gemm_bf16x3(const void *const *A_steps, const int64_t *step_rows,
                        const int64_t *step_c0, const int64_t *step_width, int32_t n_steps,
-                       const int32_t *row_map, const void *Bt, int64_t T, int64_t K, float *C,
-                       int64_t ldc, const float *d_row, uint32_t flags, void *stream);
+                       const int32_t *row_map, const int32_t *items,
+                       const int32_t *cluster_start, int32_t n_clusters, float *workspace,
+                       const int32_t *fixups, int32_t n_fixups, const void *Bt, int64_t T,
+                       int64_t K, float *C, int64_t ldc, const float *d_row, uint32_t flags,
+                       void *stream);
 
 /* ---- multi-GPU row partition -----------------
  * nnz-balanced contiguous row blocks over a HOST copy of row_ptr (int64):

@@ -76,8 +76,9 @@ _SIGNATURES = {
     "gc_hub_pack_bf16x3": (ctypes.c_int, [_P, _I64, _I64, _P, _I64, _P, _P, _P]),
     "gc_hub_gemm_bf16x3": (ctypes.c_int, [_P, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _U32, _P]),
     "gc_hub_stair_supported": (ctypes.c_int, [_I64]),
-    "gc_hub_stair_gemm_bf16x3": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P, _P, _I64, _I64, _P, _I64,
-                                                _P, _U32, _P]),
+    "gc_hub_stair_pair_bn": (ctypes.c_int, [_I64]),
+    "gc_hub_stair_gemm_bf16x3": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P, _P, _P, _I32, _P, _P,
+                                                _I32, _P, _I64, _I64, _P, _I64, _P, _U32, _P]),
     "gc_tag_hub_columns": (ctypes.c_int, [_P, _I64, _P, _P, _P]),
 }
 

@@ -456,7 +456,7 @@ __host__ __device__ constexpr uint32_t idesc_bf16_m256(int n) {
 // are a prefix of the steps; one accumulator per tile covers all of them and
 // the epilogue scatters row r to row_map[r] (nullptr: identity).  One step
 // with rows = n is the plain hub block.
-constexpr int kMaxSteps = 8;
+constexpr int kMaxSteps = 16;
 struct StairMaps {
   CUtensorMap a[kMaxSteps];
 };
@@ -466,6 +466,13 @@ struct StairArgs {
   int c0[kMaxSteps];
   int nkb[kMaxSteps];
   const int32_t *row_map;
+  // optional static schedule (longest-processing-time first, built by the
+  // caller): cluster c runs work items items[cluster_start[c] ..
+  // cluster_start[c+1]); item = {tile, first k-block, end k-block (-1: all),
+  // workspace slot (-1: write C)} — split-K for the longest tiles
+  const int4 *items;
+  const int32_t *cluster_start;
+  float *ws;  // [slot][256 rank rows][BN] partial products (rows pre-scaled)
 };
 
 __device__ __forceinline__ int stair_kblocks(const StairArgs &sa, int m0) {
@@ -507,6 +514,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const bool leader = rank == 0;
   const int cluster_id = blockIdx.x / 2, n_clusters = gridDim.x / 2;
   const int n_tiles_total = m_pairs * n_tiles;
+  // this cluster's work items: the caller's LPT list, or round-robin tiles
+  const bool sched = sarg.items != nullptr;
+  const int t_begin = sched ? __ldg(sarg.cluster_start + cluster_id) : cluster_id;
+  const int t_end = sched ? __ldg(sarg.cluster_start + cluster_id + 1) : n_tiles_total;
+  const int t_step = sched ? 1 : n_clusters;
+  auto item_at = [&](int i) {
+    return sched ? __ldg(sarg.items + i) : make_int4(i, 0, -1, -1);
+  };
 
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < sarg.n_steps; ++s)
@@ -538,15 +553,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs) ----------------
       int it = 0;
-      for (int tile = cluster_id; tile < n_tiles_total; tile += n_clusters) {
+      for (int ti = t_begin; ti < t_end; ti += t_step) {
+        const int4 item = item_at(ti);
+        const int tile = item.x;
         const int mp = (tile / n_tiles) * (2 * BM);
         const int m0 = mp + (int)rank * BM;
         const int n0 = (tile % n_tiles) * BN + (int)rank * BH;
-        for (int st = 0; st < sarg.n_steps; ++st) {
+        const int g_lo = item.y, g_hi = item.z < 0 ? INT32_MAX : item.z;
+        int g = 0;  // k-block index along the tile's step prefix
+        for (int st = 0; st < sarg.n_steps && g < g_hi; ++st) {
           if (sarg.rows[st] <= mp) continue;  // pair-uniform: both CTAs load the same steps
-          for (int kb = 0; kb < sarg.nkb[st]; ++kb, ++it) {
+          for (int kb = 0; kb < sarg.nkb[st]; ++kb, ++g) {
+            if (g < g_lo) continue;
+            if (g >= g_hi) break;
             const int s = it % stages;
-            mbar_wait(empty_bar(s), ((it / stages) & 1) ^ 1);
+            const int ph = ((it / stages) & 1) ^ 1;
+            ++it;
+            mbar_wait(empty_bar(s), ph);
             const uint32_t sa = base + (uint32_t)s * STAGE_BYTES;
             const uint32_t lbar = mapa_shared(full_bar(s), 0);
             if (leader) mbar_expect_tx(full_bar(s), 2 * STAGE_BYTES);
@@ -564,12 +587,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     if (lane == 0 && leader) {  // ---------------- MMA issuer (leader only) ----------------
       constexpr uint32_t idesc = idesc_bf16_m256(BN);
       int it = 0, lt = 0;
-      for (int tile = cluster_id; tile < n_tiles_total; tile += n_clusters, ++lt) {
+      for (int ti = t_begin; ti < t_end; ti += t_step, ++lt) {
+        const int4 item = item_at(ti);
+        const int tile = item.x;
         const int acc = lt & 1;
         mbar_wait(tempty_bar(acc), ((lt >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + (uint32_t)(acc * BN);
-        const int num_kb = stair_kblocks(sarg, (tile / n_tiles) * (2 * BM));
+        const int kb_all = stair_kblocks(sarg, (tile / n_tiles) * (2 * BM));
+        const int num_kb = (item.z < 0 ? kb_all : min(item.z, kb_all)) - item.y;
         for (int kb = 0; kb < num_kb; ++kb, ++it) {
           const int s = it % stages;
           mbar_wait(full_bar(s), (it / stages) & 1);
@@ -596,7 +622,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     const bool vec = ((ep.ldc & 3) == 0) && aligned16(ep.C);
     const uint32_t my_stage = stage_c + (uint32_t)(warp - 2) * 2u * 2048u;
     int lt = 0, sbuf = 0;
-    for (int tile = cluster_id; tile < n_tiles_total; tile += n_clusters, ++lt) {
+    for (int ti = t_begin; ti < t_end; ti += t_step, ++lt) {
+      const int4 item = item_at(ti);
+      const int tile = item.x;
+      const int slot = item.w;
       const int acc = lt & 1;
       const int m0 = (tile / n_tiles) * (2 * BM) + (int)rank * BM;
       const int n0 = (tile % n_tiles) * BN;
@@ -617,6 +646,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         for (int i = 0; i < 16; ++i) {
           v[i] *= rs;
           if (relu && !accum) v[i] = fmaxf(v[i], 0.0f);
+        }
+        if (slot >= 0) {  // split-K partial: rank-row-major workspace tile, fixed up later
+          if (row_ok) {
+            float *w = sarg.ws + ((int64_t)slot * (2 * BM) + (int)rank * BM + q * 32 + lane) * BN + c;
+#pragma unroll
+            for (int i = 0; i < 16; i += 4) stg_f4(w + i, make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+          }
+          continue;
         }
         if (tma_store) {
           const uint32_t buf = my_stage + (uint32_t)sbuf * 2048u;
@@ -921,10 +958,28 @@ int launch_hub(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &
   return check_launch("gemm_hub_bf16x3_tcgen05");
 }
 
+// Split-K fixup: per split tile, sum its workspace partials in slot order and
+// add them to C through the rank permutation (deterministic).
+__global__ void hub_splitk_fixup_kernel(const float *__restrict__ ws, const int4 *__restrict__ fix,
+                                        const int32_t *__restrict__ row_map, float *__restrict__ C,
+                                        int64_t ldc, int64_t M, int64_t N, int n_tiles, int bn) {
+  const int4 f = fix[blockIdx.x];
+  const int64_t m0 = (int64_t)(f.x / n_tiles) * 256, n0 = (int64_t)(f.x % n_tiles) * bn;
+  for (int idx = threadIdx.x; idx < 256 * bn; idx += blockDim.x) {
+    const int r = idx / bn, c = idx % bn;
+    const int64_t rrow = m0 + r, col = n0 + c;
+    if (rrow >= M || col >= N) continue;
+    float sum = 0.0f;
+    for (int k = 0; k < f.z; ++k) sum += ws[((int64_t)(f.y + k) * 256 + r) * bn + c];
+    const int64_t row = row_map ? row_map[rrow] : rrow;
+    C[row * ldc + col] += sum;
+  }
+}
+
 template <int BN>
 int launch_hub_pair(const StairMaps &maps, const StairArgs &sarg, const CUtensorMap &mb,
                     const CUtensorMap &mc, int tma_store, const GemmEpi &ep, int64_t kp,
-                    cudaStream_t st) {
+                    cudaStream_t st, int sched_clusters = 0) {
   constexpr int stage_bytes = BM * KB_BYTES + 3 * (BN / 2) * KB_BYTES;
   size_t smem = 0;
   int stages = tma_store ? ring_stages(stage_bytes, true, &smem) : 0;
@@ -949,9 +1004,10 @@ int launch_hub_pair(const StairMaps &maps, const StairArgs &sarg, const CUtensor
   const int m_pairs = (int)((ep.M + 2 * BM - 1) / (2 * BM));
   const int n_tiles = (int)((ep.N + BN - 1) / BN);
   const int64_t tiles = (int64_t)m_pairs * n_tiles;
-  const int clusters = (int)(tiles < sm_count() / 2 ? tiles : sm_count() / 2);
   // tiles are walked in rank order = descending reduction length, round-robin
-  // over the clusters (longest-first keeps the staircase balanced)
+  // over the clusters, unless the caller passed an LPT schedule
+  const int clusters = sched_clusters > 0 ? sched_clusters
+                                          : (int)(tiles < sm_count() / 2 ? tiles : sm_count() / 2);
   gemm_hub_pair_tcgen05<BN><<<2 * clusters, kGemmThreads, smem, st>>>(
       maps, mb, mc, ep, sarg, stages, m_pairs, n_tiles, tma_store, (int)kp);
   return check_launch("gemm_hub_pair_tcgen05");
@@ -1192,13 +1248,18 @@ extern "C" int gc_hub_gemm_bf16x3(const void *A_hub, int64_t lda, int64_t n_rows
   }
 }
 
+extern "C" int gc_hub_stair_pair_bn(int64_t K) { return K > 0 ? pair_bn(K) : 0; }
+
 extern "C" int gc_hub_stair_supported(int64_t K) {
   return (hub_pair_enabled() && K > 16 && gc_hub_terms_rows(K) % pair_bn(K) == 0) ? 1 : 0;
 }
 
 extern "C" int gc_hub_stair_gemm_bf16x3(const void *const *A_steps, const int64_t *step_rows,
                                         const int64_t *step_c0, const int64_t *step_width,
-                                        int32_t n_steps, const int32_t *row_map, const void *Bt,
+                                        int32_t n_steps, const int32_t *row_map,
+                                        const int32_t *items, const int32_t *cluster_start,
+                                        int32_t n_clusters, float *workspace,
+                                        const int32_t *fixups, int32_t n_fixups, const void *Bt,
                                         int64_t T, int64_t K, float *C, int64_t ldc,
                                         const float *d_row, uint32_t flags, void *stream) {
   GC_REQUIRE(n_steps >= 1 && n_steps <= kMaxSteps, GC_ERR_VALUE,
@@ -1214,9 +1275,22 @@ extern "C" int gc_hub_stair_gemm_bf16x3(const void *const *A_steps, const int64_
   GC_REQUIRE(aligned16(Bt), GC_ERR_UNSUPPORTED, "gc_hub_stair_gemm_bf16x3: Bt alignment");
   StairMaps maps;
   memset(&maps, 0, sizeof(maps));
+  GC_REQUIRE((items == nullptr) == (cluster_start == nullptr), GC_ERR_VALUE,
+             "gc_hub_stair_gemm_bf16x3: items and cluster_start go together");
+  GC_REQUIRE(items == nullptr || (n_clusters >= 1 && n_clusters <= sm_count() / 2),
+             GC_ERR_VALUE, "gc_hub_stair_gemm_bf16x3: 1..%d clusters", sm_count() / 2);
+  GC_REQUIRE(n_fixups >= 0 && (n_fixups == 0 || (fixups && workspace && items)), GC_ERR_VALUE,
+             "gc_hub_stair_gemm_bf16x3: split-K needs items, workspace and fixups");
+  GC_REQUIRE(n_fixups == 0 || !(flags & GC_RELU), GC_ERR_VALUE,
+             "gc_hub_stair_gemm_bf16x3: ReLU cannot follow split-K partials");
+  GC_REQUIRE(workspace == nullptr || aligned16(workspace), GC_ERR_WORKSPACE,
+             "gc_hub_stair_gemm_bf16x3: 16-byte aligned workspace required");
   StairArgs sarg{};
   sarg.n_steps = n_steps;
   sarg.row_map = row_map;
+  sarg.items = reinterpret_cast<const int4 *>(items);
+  sarg.cluster_start = cluster_start;
+  sarg.ws = workspace;
   for (int s = 0; s < n_steps; ++s) {
     const int64_t r = step_rows[s], c0 = step_c0[s], w = step_width[s];
     GC_REQUIRE(r >= 1 && r < INT32_MAX && w > 0 && w % 64 == 0 && c0 % 64 == 0 && c0 + w <= T,
@@ -1245,5 +1319,13 @@ extern "C" int gc_hub_stair_gemm_bf16x3(const void *const *A_steps, const int64_
     if (rc) return rc;
   }
   GemmEpi ep{C, ldc, d_row, step_rows[0], K, flags};
-  return launch_hub_pair_bn(pbn, maps, sarg, mbp, mc, tma_store, ep, kp, as_stream(stream));
+  cudaStream_t st = as_stream(stream);
+  rc = launch_hub_pair_bn(pbn, maps, sarg, mbp, mc, tma_store, ep, kp, st,
+                          items ? (int)n_clusters : 0);
+  if (rc || n_fixups == 0) return rc;
+  const int n_tiles = (int)((K + pbn - 1) / pbn);
+  hub_splitk_fixup_kernel<<<(unsigned)n_fixups, 256, 0, st>>>(
+      workspace, reinterpret_cast<const int4 *>(fixups), row_map, C, ldc, step_rows[0], K,
+      n_tiles, pbn);
+  return check_launch("hub_splitk_fixup_kernel");
 }

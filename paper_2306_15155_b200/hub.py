@@ -51,11 +51,15 @@ from .sparse import CsrMatrix, ShapeError, _ld, _require_cuda, _spmm, _stream, _
 
 HUB_SPLIT = os.environ.get("GNNC_HUB_SPLIT", "auto")
 HUB_T_CANDIDATES = (1024, 2048, 4096, 8192)
-STAIR_DELTAS = (0.015, 0.03, 0.06)  # density thresholds tried by the autotuner
+# (cell/edge cost ratio δ, balance slack) pairs tried by the autotuner
+# (slack > 1 reaches further right, but short-wide steps stream their B
+# operand from DRAM once per pair tile and lose to the tail: measured 2.73 ms
+# at (0.012, 1.0) vs 2.99 ms at (0.018, 3.0) on Reddit K=256)
+STAIR_CANDIDATES = ((0.012, 1.0), (0.018, 1.0), (0.018, 1.5))
 HUB_MIN_NNZ = 1 << 24            # smaller graphs stay on the SpMM alone
 HUB_MIN_DENSITY = 0.02           # mean density of a block worth a dense product
 HUB_MEM_BUDGET = 8 << 30         # bytes of dense blocks per pattern
-STAIR_MAX_STEPS = 8
+STAIR_MAX_STEPS = 16
 STAIR_CLUSTERS = 74              # CTA pairs of a B200 (balance bound of the top tile)
 
 
@@ -127,8 +131,8 @@ class StairPlan(_TailMixin):
 
     kind = "stair"
 
-    def __init__(self, a: CsrMatrix, delta: float, *, n_clusters: int = STAIR_CLUSTERS,
-                 first_band: int = 1024):
+    def __init__(self, a: CsrMatrix, delta: float, *, slack: float = 1.0,
+                 n_clusters: int = STAIR_CLUSTERS, first_band: int = 1024):
         dev = a.device
         col = a.col_idx.long()
         ccount = torch.bincount(col, minlength=a.n_cols)
@@ -141,9 +145,9 @@ class StairPlan(_TailMixin):
         rrank[rorder] = torch.arange(a.n_rows, device=dev)
         rows = a.row_of_nnz()
         er, ec = rrank[rows], crank[col]
-        self.steps = self._staircase(a, er, ec, delta, n_clusters, first_band)
+        self.steps = self._staircase(a, er, ec, delta, slack, n_clusters, first_band)
         if not self.steps:
-            raise ValueError("stair split: no block reaches the density threshold")
+            raise ValueError("stair split: no block pays for its cells")
         C = self.steps[-1][1] + self.steps[-1][2]
         self.T = C
         self.delta = delta
@@ -167,71 +171,136 @@ class StairPlan(_TailMixin):
         self._np_c0 = np.array([s[1] for s in self.steps], np.int64)
         self._np_w = np.array([s[2] for s in self.steps], np.int64)
         self._np_ptrs = np.array([b.data_ptr() for b in self.blocks], np.uint64)
+        self._sched: dict = {}
         self._init_tail(a, ~covered, rows)
 
+    def schedule(self, K: int, device):
+        """Work items for the staircase GEMM, longest-processing-time first
+        over the CTA pairs.  Pair tiles (256 rank-ordered rows x one N tile)
+        reduce over different step prefixes; a tile longer than the mean
+        per-pair load is cut into split-K chunks (the first writes C, the rest
+        write workspace slots that a fixup adds in slot order).  Returns
+        (items int32[n][4], cluster_start, n_clusters, workspace | None,
+        fixups int32[f][4] | None)."""
+        if K not in self._sched:
+            import heapq
+
+            pbn = int(nat.load().gc_hub_stair_pair_bn(K))
+            n_tiles = -(-K // pbn)
+            m_pairs = -(-self.rows0 // 256)
+            kb = [sum(w // 64 for r, _, w in self.steps if r > mp * 256) for mp in range(m_pairs)]
+            sms = torch.cuda.get_device_properties(device).multi_processor_count
+            total = sum(kb) * n_tiles
+            n_cl = max(1, min(m_pairs * n_tiles, sms // 2))
+            target = max(16, -(-total // n_cl))
+            items, fixups, slot = [], [], 0
+            for mp in range(m_pairs):
+                for nt in range(n_tiles):
+                    t = mp * n_tiles + nt
+                    parts = -(-kb[mp] // target) if kb[mp] > target else 1
+                    if parts == 1:
+                        items.append((kb[mp], (t, 0, -1, -1)))
+                        continue
+                    bounds = [kb[mp] * i // parts for i in range(parts + 1)]
+                    items.append((bounds[1], (t, 0, bounds[1], -1)))
+                    fixups.append((t, slot, parts - 1, 0))
+                    for i in range(1, parts):
+                        items.append((bounds[i + 1] - bounds[i], (t, bounds[i], bounds[i + 1], slot)))
+                        slot += 1
+            items.sort(key=lambda x: -x[0])
+            heap = [(0, c) for c in range(n_cl)]
+            lists: list[list] = [[] for _ in range(n_cl)]
+            for w, it in items:
+                load, c = heapq.heappop(heap)
+                lists[c].append(it)
+                heapq.heappush(heap, (load + w + 4, c))  # + per-item epilogue cost
+            starts = np.zeros(n_cl + 1, np.int32)
+            starts[1:] = np.cumsum([len(x) for x in lists])
+            flat = np.array([v for x in lists for it in x for v in it], np.int32)
+            ws = torch.empty(max(slot, 1) * 256 * pbn, dtype=torch.float32, device=device) \
+                if slot else None
+            fx = torch.from_numpy(np.array(fixups, np.int32).reshape(-1, 4)).to(device) \
+                if fixups else None
+            self._sched[K] = (torch.from_numpy(flat).to(device), torch.from_numpy(starts).to(device),
+                              n_cl, ws, fx)
+        return self._sched[K]
+
     @staticmethod
-    def _bands(n: int, first: int = 1024) -> list[int]:
-        b, x = [0], first
-        while x < n:
-            b.append(x)
-            x *= 2
-        b.append(n)
+    def _bands(n: int, first: int, align: int) -> list[int]:
+        """0, first, then ratio-sqrt(2) boundaries (multiples of ``align``), n."""
+        b, x = [0], float(first)
+        while int(x) // align * align < n:
+            v = int(x) // align * align
+            if v > b[-1]:
+                b.append(v)
+            x *= 2 ** 0.5
+        if b[-1] != n:
+            b.append(n)
         return b
 
     @classmethod
-    def _staircase(cls, a: CsrMatrix, er, ec, delta, n_clusters,
+    def _staircase(cls, a: CsrMatrix, er, ec, delta, slack, n_clusters,
                    first_band: int = 1024) -> list[tuple[int, int, int]]:
-        """[(R_s, C_s, W_s)]: column bands of doubling width in rank order
-        (multiples of 64), each taking the leading row bands whose density is
-        >= delta; rows never grow; stop when a step would make the longest
-        (top) tile's reduction exceed the mean per-cluster load."""
-        rb = cls._bands(a.n_rows, first_band)
+        """[(R_s, C_s, W_s)]: per column band (rank order, multiples of 64),
+        the row prefix R maximising edges − δ·cells (δ = cell cost / edge
+        cost), never growing from one band to the next; adjacent bands with
+        the same R merge into one step (<= STAIR_MAX_STEPS).  Stops when the
+        top tile's reduction would exceed slack × the mean per-cluster load."""
         cmax = a.n_cols // 64 * 64
         if cmax < 64:
             return []
-        cb = [c for c in cls._bands(cmax, first_band) if c <= cmax]
-        if cb[-1] != cmax:
-            cb.append(cmax)
+        rb = cls._bands(a.n_rows, first_band, 128)
+        cb = cls._bands(cmax, first_band, 64)
         dev = er.device
         ri = torch.bucketize(er, torch.tensor(rb[1:-1], device=dev), right=True)
         ci = torch.bucketize(ec, torch.tensor(cb[1:-1], device=dev), right=True)
         valid = ec < cmax
-        H = torch.zeros((len(rb) - 1) * (len(cb) - 1), dtype=torch.int64, device=dev)
-        H.index_add_(0, (ri * (len(cb) - 1) + ci)[valid], torch.ones_like(ri[valid]))
-        H = H.view(len(rb) - 1, len(cb) - 1).cpu().numpy()
-        steps: list[tuple[int, int, int]] = []
+        nr, nc = len(rb) - 1, len(cb) - 1
+        H = torch.zeros(nr * nc, dtype=torch.int64, device=dev)
+        H.index_add_(0, (ri * nc + ci)[valid], torch.ones_like(ri[valid]))
+        H = H.view(nr, nc).cpu().numpy()
+        steps: list[list[int]] = []
         prev_r = a.n_rows
-        work = 0.0  # pair k-blocks of the steps taken
-        for s in range(len(cb) - 1):
+        work = 0.0  # pair k-blocks of the bands taken
+        for s in range(nc):
             W = cb[s + 1] - cb[s]
-            R = 0
-            for b in range(len(rb) - 1):
-                if H[b, s] / ((rb[b + 1] - rb[b]) * W) < delta:
+            best_r, best_gain, cum = 0, 0.0, 0
+            for b in range(nr):
+                if rb[b + 1] > prev_r:
                     break
-                R = rb[b + 1]
-            R = min(R, prev_r)
-            if R < first_band or len(steps) == STAIR_MAX_STEPS:
+                cum += int(H[b, s])
+                gain = cum - delta * rb[b + 1] * W
+                if gain > best_gain:
+                    best_gain, best_r = gain, rb[b + 1]
+            if best_r < first_band:
                 break
-            w_new = work + R * W / (256.0 * 64.0)
-            if steps and cb[s + 1] / 64.0 > w_new / n_clusters:
+            w_new = work + best_r * W / (256.0 * 64.0)
+            if steps and cb[s + 1] / 64.0 > slack * w_new / n_clusters:
                 break  # the top tile would outlast the average cluster
-            steps.append((R, cb[s], W))
-            work, prev_r = w_new, R
-        return steps
+            if steps and steps[-1][0] == best_r:
+                steps[-1][2] += W  # same rows: widen the previous step
+            elif len(steps) == STAIR_MAX_STEPS:
+                break
+            else:
+                steps.append([best_r, cb[s], W])
+            work, prev_r = w_new, best_r
+        return [tuple(x) for x in steps]
 
 
 def _parse_spec(spec):
-    """0 | T (block plan) | ("stair", permille) | "stair:<permille>" | "<T>"."""
+    """0 | T (block plan) | ("stair", δ permille, slack tenths) |
+    "stair:<permille>[:<slack tenths>]" | "<T>"."""
     if isinstance(spec, tuple):
-        return spec
+        return spec if len(spec) == 3 else (spec[0], spec[1], 10)
     if isinstance(spec, str) and spec.startswith("stair:"):
-        return ("stair", int(spec.split(":")[1]))
+        parts = spec.split(":")
+        return ("stair", int(parts[1]), int(parts[2]) if len(parts) > 2 else 10)
     return int(spec)
 
 
 def spec_label(spec) -> str:
     spec = _parse_spec(spec)
-    return f"stair:{spec[1]}" if isinstance(spec, tuple) else str(spec)
+    return f"stair:{spec[1]}:{spec[2]}" if isinstance(spec, tuple) else str(spec)
 
 
 def hub_plan(a: CsrMatrix, spec):
@@ -239,7 +308,7 @@ def hub_plan(a: CsrMatrix, spec):
     key = ("hubsplit", spec)
     if key not in a._plans:
         if isinstance(spec, tuple):
-            a._plans[key] = StairPlan(a, spec[1] / 1000.0)
+            a._plans[key] = StairPlan(a, spec[1] / 1000.0, slack=spec[2] / 10.0)
         else:
             a._plans[key] = HubPlan(a, spec)
     return a._plans[key]
@@ -280,10 +349,13 @@ def dense_part(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, out: torch.
         raise ShapeError("stair split: the dense part covers all rows (rank-ordered tiles)")
     if plan.rows0 < a.n_rows and not accumulate:
         out.zero_()  # rows outside every step receive only the tail
+    items, starts, n_cl, ws, fx = plan.schedule(K, dev)
     nat.check(_timed_call("hub_gemm", dev, lambda: lib.gc_hub_stair_gemm_bf16x3(
         plan._np_ptrs.ctypes.data, plan._np_rows.ctypes.data, plan._np_c0.ctypes.data,
-        plan._np_w.ctypes.data, len(plan.steps), plan.row_map.data_ptr(), bt.data_ptr(), plan.T,
-        K, out.data_ptr(), _ld(out), d_row.data_ptr(), flags, st)), "hub_stair_gemm")
+        plan._np_w.ctypes.data, len(plan.steps), plan.row_map.data_ptr(), items.data_ptr(),
+        starts.data_ptr(), n_cl, None if ws is None else ws.data_ptr(),
+        None if fx is None else fx.data_ptr(), 0 if fx is None else fx.shape[0], bt.data_ptr(),
+        plan.T, K, out.data_ptr(), _ld(out), d_row.data_ptr(), flags, st)), "hub_stair_gemm")
 
 
 def tail_part(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, out: torch.Tensor, *,
@@ -352,8 +424,8 @@ def _block_candidates(a: CsrMatrix) -> list[int]:
 def _candidates(a: CsrMatrix, K: int) -> list:
     cands: list = list(_block_candidates(a))
     if nat.load().gc_hub_stair_supported(K):
-        for dl in STAIR_DELTAS:
-            spec = ("stair", int(round(dl * 1000)))
+        for dl, sl in STAIR_CANDIDATES:
+            spec = ("stair", int(round(dl * 1000)), int(round(sl * 10)))
             try:
                 plan = hub_plan(a, spec)
             except ValueError:

@@ -22,7 +22,9 @@ def t_ms(fn, reps=7):
     return sorted(ts)[reps // 2]
 ref = sparse.spmm_unweighted(a, x, d_col=d, d_row=d)
 print(json.dumps({"plain_ms": t_ms(lambda: sparse.spmm_unweighted(a, x, d_col=d, d_row=d, out=out))}), flush=True)
-for spec in [4096, ("stair", 10), ("stair", 15), ("stair", 20), ("stair", 30), ("stair", 60)]:
+specs = [hub._parse_spec(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else \
+    [4096, ("stair", 12, 10), ("stair", 18, 10), ("stair", 18, 15), ("stair", 18, 20), ("stair", 12, 20)]
+for spec in specs:
     try:
         plan = hub.hub_plan(a, spec)
     except ValueError as e:

@@ -677,10 +677,13 @@ def test_stair_split_matches_oracle(oracle, stair_pl, K, precompute):
         pytest.skip("no CTA-pair tile for this K")
     g = gc.NormalizedGraph.from_adjacency(stair_pl).with_precomputed()
     a = g.a_tilde
-    spec = ("stair", 50)
+    spec = ("stair", 50, 10)
     a._plans[("hubsplit", spec)] = hub.StairPlan(a, 0.05, n_clusters=1, first_band=256)
     plan = hub.hub_plan(a, spec)
     assert len(plan.steps) >= 2 and plan.rows0 < a.n_rows
+    _, _, _, ws, fx = plan.schedule(K, torch.device(DEV))
+    if K <= 256:  # the top tile outlasts the mean pair load: split-K items + fixups
+        assert fx is not None and ws is not None
     og = oracle.GcnGraph.from_adjacency(to_oracle(oracle, stair_pl))
     rng = np.random.default_rng(K)
     x = f32(rng.uniform(-0.5, 0.5, (a.n_rows, K)))
@@ -703,9 +706,9 @@ def test_host_pipelined_layer_with_stair_split(oracle, stair_pl, monkeypatch):
     from paper_2306_15155_b200 import hub
     g = gc.NormalizedGraph.from_adjacency(stair_pl).with_precomputed()
     a = g.a_tilde
-    spec = ("stair", 50)
+    spec = ("stair", 50, 10)
     a._plans[("hubsplit", spec)] = hub.StairPlan(a, 0.05, n_clusters=1, first_band=256)
-    monkeypatch.setattr(hub, "HUB_SPLIT", "stair:50")
+    monkeypatch.setattr(hub, "HUB_SPLIT", "stair:50:10")
     monkeypatch.setattr(gcn_mod, "HOST_PIPELINE_BLOCKS", 3)
     og = oracle.GcnGraph.from_adjacency(to_oracle(oracle, stair_pl))
     rng = np.random.default_rng(9)
