@@ -192,7 +192,10 @@ def dist_gcn_layer(part: RowPartition, h_local: torch.Tensor, w: torch.Tensor, *
         full, work = all_gather_padded(src, part, group, async_op=True)
         # owned-column edges while the gather is in flight
         dl = d_loc if dyn else None
-        y = ops.spmm(loc, src, d_row=dl, d_col=dl, relu=False, weighted=weighted)
+        # (on power-law graphs the owned columns of the first ranks are the
+        # hubs: the owned pass may take the dense split as well)
+        loc_kw = {"hub_d": (d_loc, d_loc)} if hub_unit else {}
+        y = ops.spmm(loc, src, d_row=dl, d_col=dl, relu=False, weighted=weighted, **loc_kw)
         work.wait()
         last = order == "update_first"
         hub_kw = {"hub_d": (d_loc, d_pad)} if hub_unit else {}
