@@ -494,7 +494,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   constexpr uint32_t A_BYTES = BM * KB_BYTES;
   constexpr uint32_t B_BYTES = BH * KB_BYTES;
   constexpr uint32_t STAGE_BYTES = A_BYTES + TERMS * B_BYTES;
-  constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  // Narrow tiles (BN <= 64): the three staged term tiles are one contiguous
+  // K-major [3*BH rows] operand, so ONE MMA with N = 3*BN covers all terms
+  // (A is read once per k-step instead of three times) and the epilogue adds
+  // the three term column groups.  Accumulator columns per tile:
+  constexpr bool TSTACK = BN <= 64;
+  constexpr int ACC_N = TSTACK ? 3 * BN : BN;
+  constexpr uint32_t TMEM_COLS = 2 * ACC_N <= 32 ? 32 : 2 * ACC_N <= 64 ? 64 : 2 * ACC_N <= 128 ? 128
+                                 : 2 * ACC_N <= 256 ? 256 : 512;
 
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -585,7 +592,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {  // ---------------- MMA issuer (leader only) ----------------
-      constexpr uint32_t idesc = idesc_bf16_m256(BN);
+      constexpr uint32_t idesc = idesc_bf16_m256(ACC_N);
       int it = 0, lt = 0;
       for (int ti = t_begin; ti < t_end; ti += t_step, ++lt) {
         const int4 item = item_at(ti);
@@ -593,7 +600,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         const int acc = lt & 1;
         mbar_wait(tempty_bar(acc), ((lt >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t tmem_d = tmem_base + (uint32_t)(acc * BN);
+        const uint32_t tmem_d = tmem_base + (uint32_t)(acc * ACC_N);
         const int kb_all = stair_kblocks(sarg, (tile / n_tiles) * (2 * BM));
         const int num_kb = (item.z < 0 ? kb_all : min(item.z, kb_all)) - item.y;
         for (int kb = 0; kb < num_kb; ++kb, ++it) {
@@ -604,10 +611,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int k = 0; k < KB_BYTES / MMA_K_BYTES; ++k) {
             const uint64_t ad = umma_desc_sw128(sa + k * MMA_K_BYTES);
+            if constexpr (TSTACK) {
+              const uint64_t bd = umma_desc_sw128(sa + A_BYTES + k * MMA_K_BYTES);
+              mma_bf16_pair(tmem_d, ad, bd, idesc, (kb | k) != 0);
+            } else {
 #pragma unroll
-            for (int q = 0; q < TERMS; ++q) {
-              const uint64_t bd = umma_desc_sw128(sa + A_BYTES + q * B_BYTES + k * MMA_K_BYTES);
-              mma_bf16_pair(tmem_d, ad, bd, idesc, (kb | k | q) != 0);
+              for (int q = 0; q < TERMS; ++q) {
+                const uint64_t bd = umma_desc_sw128(sa + A_BYTES + q * B_BYTES + k * MMA_K_BYTES);
+                mma_bf16_pair(tmem_d, ad, bd, idesc, (kb | k | q) != 0);
+              }
             }
           }
           mma_commit_pair(empty_bar(s));  // frees slot s in both CTAs
@@ -636,12 +648,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const int row = (row_ok && sarg.row_map) ? __ldg(sarg.row_map + rrow) : rrow;
       const float rs = (row_ok && ep.row_scale) ? __ldg(ep.row_scale + row) : 1.0f;
       float *crow = ep.C + (int64_t)row * ep.ldc;
-      const uint32_t taddr = tmem_base + (uint32_t)(acc * BN) + ((uint32_t)(q * 32) << 16);
+      const uint32_t taddr = tmem_base + (uint32_t)(acc * ACC_N) + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
       for (int c = 0; c < BN; c += 16) {
         if (n0 + c >= ep.N) break;
         float v[16];
-        tmem_ld16(taddr + (uint32_t)c, v);
+        if constexpr (TSTACK) {
+          // feature chunk c lives in CTA half h at column j of each term group
+          const int h = c / BH, jj = c % BH;
+          float t1[16], t2[16];
+          tmem_ld16(taddr + (uint32_t)(h * 3 * BH + jj), v);
+          tmem_ld16(taddr + (uint32_t)(h * 3 * BH + BH + jj), t1);
+          tmem_ld16(taddr + (uint32_t)(h * 3 * BH + 2 * BH + jj), t2);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = (v[i] + t1[i]) + t2[i];
+        } else {
+          tmem_ld16(taddr + (uint32_t)c, v);
+        }
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           v[i] *= rs;

@@ -56,6 +56,18 @@ HUB_T_CANDIDATES = (1024, 2048, 4096, 8192)
 # operand from DRAM once per pair tile and lose to the tail: measured 2.73 ms
 # at (0.012, 1.0) vs 2.99 ms at (0.018, 3.0) on Reddit K=256)
 STAIR_CANDIDATES = ((0.012, 1.0), (0.018, 1.0), (0.018, 1.5))
+# narrower feature rows make a dense cell relatively dearer (the tensor tile
+# is N = K wide: A-operand bound), so small K tries sparser staircases
+STAIR_CANDIDATES_SMALL_K = {128: ((0.018, 1.0), (0.03, 1.0), (0.06, 1.0)),
+                            64: ((0.03, 1.0), (0.06, 1.0), (0.12, 1.0)),
+                            32: ((0.03, 1.0), (0.06, 1.0), (0.12, 1.0))}
+
+
+def _stair_candidates(K: int):
+    for k, c in sorted(STAIR_CANDIDATES_SMALL_K.items()):
+        if K <= k:
+            return c
+    return STAIR_CANDIDATES
 HUB_MIN_NNZ = 1 << 24            # smaller graphs stay on the SpMM alone
 HUB_MIN_DENSITY = 0.02           # mean density of a block worth a dense product
 HUB_MEM_BUDGET = 8 << 30         # bytes of dense blocks per pattern
@@ -424,7 +436,7 @@ def _block_candidates(a: CsrMatrix) -> list[int]:
 def _candidates(a: CsrMatrix, K: int) -> list:
     cands: list = list(_block_candidates(a))
     if nat.load().gc_hub_stair_supported(K):
-        for dl, sl in STAIR_CANDIDATES:
+        for dl, sl in _stair_candidates(K):
             spec = ("stair", int(round(dl * 1000)), int(round(sl * 10)))
             try:
                 plan = hub_plan(a, spec)
