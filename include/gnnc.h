@@ -216,37 +216,47 @@ GNNC_API int gc_attn_sddmm_f32(const int32_t *row_ptr, const int32_t *col_idx, c
                       const int32_t *heavy_rows, int64_t n_heavy, float *s_work,
                       float *alpha, void *stream);
 
-/* ---- hybrid aggregation: dense hub block on tcgen05 ----
+/* ---- hybrid aggregation: dense blocks on tcgen05 ------
  * For a unit-valued pattern Ã and D = diag(d), the aggregation
  *   C = D Ã D X   (both GCN compositions: dynamic directly, precompute as Ñ = DÃD)
- * is split by columns into the T most-referenced ("hub") columns and the
- * rest.  The hub part is a dense product on the 5th-gen tensor cores:
- *   C_hub = D · A_hub · (B0 + B1 + B2),  A_hub[i, t] = Ã[i, hub_cols[t]] in {0, 1}
- * with B_q the hi/mid/lo bf16 terms of (D X)[hub_cols] — exact in bf16, so
- * the result carries fp32 precision.  The tail (remaining columns) is the
- * ordinary SpMM launched with GC_ACCUMULATE on top of C_hub.
+ * is split into dense 0/1 blocks of Ã (degree-sorted corners, or all rows x
+ * the T most-referenced "hub" columns) and the remaining edges.  The dense
+ * part is a tensor-core product  C_dense = D · A_dense · (D X)[hub_cols]
+ * over terms of (D X)[hub_cols]:
+ *   GC_HUB_BF16X3: hi/mid/lo bf16 terms — an exact fp32 split;
+ *   GC_HUB_F16X2:  hi/lo fp16 terms of s·D·X, s = 2^(13 - floor(log2 max|D X|))
+ *                  — 22 significant bits above 2^-10·max, absolute error
+ *                  <= 2^-23·max|D X| per element; 2/3 of the MMAs.
+ * The 0/1 blocks are bf16 (BF16X3) or fp16 (F16X2) — exact either way.  The
+ * remaining edges are the ordinary SpMM launched with GC_ACCUMULATE on top.
  *
- * gc_hub_terms_rows(K): rows per term in the packed operand (K rounded up to
- *   the kernel's N tile); the packed operand is bf16[3 * rows * T].
- * gc_hub_pack_bf16x3: Bt[q][f][t] = term_q( X[hub_cols[t], f] * d_col[hub_cols[t]] )
- *   (d_col may be NULL), zero for f >= K.
- * gc_hub_gemm_bf16x3: C[i, f] = d_row[i] * sum_t A_hub[i, t] * (B0 + B1 + B2)[f, t]
- *   (d_row may be NULL; flags: GC_RELU, GC_ACCUMULATE — C = relu?(C + ...)).  A_hub bf16 row-major [n_rows x lda],
- *   T % 64 == 0, 16-byte aligned operands.                                  */
+ * gc_hub_terms_rows(K): rows per term of the packed operand (K rounded up to
+ *   the kernel's N tile); the packed operand is {terms * rows * T} 16-bit
+ *   elements (terms = 3 for BF16X3, 2 for F16X2).
+ * gc_hub_pack: Bt[q][f][t] = term_q(X[hub_cols[t], f] * d_col[hub_cols[t]])
+ *   (d_col may be NULL), zero for f >= K; T % 64 == 0.  F16X2 also needs
+ *   scale_ws (float[2], caller-owned): the max and 1/s for the GEMM.
+ * gc_hub_gemm: C[i, f] = d_row[i] * sum_t A_hub[i, t] * (sum_q B_q)[f, t]
+ *   (d_row may be NULL; flags: GC_RELU, GC_ACCUMULATE — C = relu?(C + ...)).
+ *   A_hub row-major [n_rows x lda], T % 64 == 0, 16-byte aligned operands.
+ *   CTA pairs (tcgen05.mma.cta_group::2) when K > 16.                      */
+#define GC_HUB_BF16X3 0
+#define GC_HUB_F16X2 1
 GNNC_API int64_t gc_hub_terms_rows(int64_t K);
-GNNC_API int gc_hub_pack_bf16x3(const float *X, int64_t ldx, int64_t K, const int32_t *hub_cols,
-                       int64_t T, const float *d_col, void *Bt, void *stream);
-GNNC_API int gc_hub_gemm_bf16x3(const void *A_hub, int64_t lda, int64_t n_rows, int64_t T,
-                       const void *Bt, int64_t K, float *C, int64_t ldc, const float *d_row,
-                       uint32_t flags, void *stream);
+GNNC_API int gc_hub_pack(const float *X, int64_t ldx, int64_t K, const int32_t *hub_cols,
+                int64_t T, const float *d_col, int32_t fmt, void *Bt, float *scale_ws,
+                void *stream);
+GNNC_API int gc_hub_gemm(const void *A_hub, int64_t lda, int64_t n_rows, int64_t T,
+                const void *Bt, int64_t K, int32_t fmt, const float *scale_ws, float *C,
+                int64_t ldc, const float *d_row, uint32_t flags, void *stream);
 
 /* Staircase of dense blocks (degree-rank order).  Step s (0 <= s < n_steps
- * <= 16) is A_steps[s]: bf16 row-major [step_rows[s] x step_width[s]], the
- * 0/1 adjacency of the step_rows[s] highest-degree rows (rank order) against
- * the hub columns at positions [step_c0[s], step_c0[s] + step_width[s]) of
- * the packed operand Bt (gc_hub_pack_bf16x3 over T hub columns in rank
- * order).  Rows shrink and column ranges are consecutive across steps.  Rank
- * row r of the result goes to C row row_map[r] (NULL: r):
+ * <= 16) is A_steps[s]: row-major [step_rows[s] x step_width[s]], the 0/1
+ * adjacency of the step_rows[s] highest-degree rows (rank order) against the
+ * hub columns at positions [step_c0[s], step_c0[s] + step_width[s]) of the
+ * packed operand Bt (gc_hub_pack over T hub columns in rank order).  Rows
+ * shrink and column ranges are consecutive across steps.  Rank row r of the
+ * result goes to C row row_map[r] (NULL: r):
  *   C[row_map[r], f] = d_row[row_map[r]] * sum_{s: r < rows[s]} A_s[r, :] · B[.., c0_s ..]
  * One CTA-pair tcgen05 launch; flags GC_RELU / GC_ACCUMULATE.  Requires
  * gc_hub_stair_supported(K).  Optional static schedule (device int32):
@@ -260,13 +270,12 @@ GNNC_API int gc_hub_gemm_bf16x3(const void *A_hub, int64_t lda, int64_t n_rows, 
  * order (deterministic; no GC_RELU with split items).                      */
 GNNC_API int gc_hub_stair_supported(int64_t K);
 GNNC_API int gc_hub_stair_pair_bn(int64_t K);
-GNNC_API int gc_hub_stair_gemm_bf16x3(const void *const *A_steps, const int64_t *step_rows,
-                       const int64_t *step_c0, const int64_t *step_width, int32_t n_steps,
-                       const int32_t *row_map, const int32_t *items,
-                       const int32_t *cluster_start, int32_t n_clusters, float *workspace,
-                       const int32_t *fixups, int32_t n_fixups, const void *Bt, int64_t T,
-                       int64_t K, float *C, int64_t ldc, const float *d_row, uint32_t flags,
-                       void *stream);
+GNNC_API int gc_hub_stair_gemm(const void *const *A_steps, const int64_t *step_rows,
+                const int64_t *step_c0, const int64_t *step_width, int32_t n_steps,
+                const int32_t *row_map, const int32_t *items, const int32_t *cluster_start,
+                int32_t n_clusters, float *workspace, const int32_t *fixups, int32_t n_fixups,
+                const void *Bt, int64_t T, int64_t K, int32_t fmt, const float *scale_ws,
+                float *C, int64_t ldc, const float *d_row, uint32_t flags, void *stream);
 
 /* ---- multi-GPU row partition -----------------
  * nnz-balanced contiguous row blocks over a HOST copy of row_ptr (int64):

@@ -16,6 +16,8 @@ from ._build import LIB, ROOT
 
 GC_RELU = 1 << 0
 GC_ACCUMULATE = 1 << 1
+GC_HUB_BF16X3 = 0
+GC_HUB_F16X2 = 1
 GC_HUB_TAGGED = 1 << 2
 
 
@@ -73,12 +75,13 @@ _SIGNATURES = {
                                          _I64, _P, _P, _P]),
     "gc_partition_rows": (ctypes.c_int, [_P, _I64, _I32, _P]),
     "gc_hub_terms_rows": (_I64, [_I64]),
-    "gc_hub_pack_bf16x3": (ctypes.c_int, [_P, _I64, _I64, _P, _I64, _P, _P, _P]),
-    "gc_hub_gemm_bf16x3": (ctypes.c_int, [_P, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _U32, _P]),
+    "gc_hub_pack": (ctypes.c_int, [_P, _I64, _I64, _P, _I64, _P, _I32, _P, _P, _P]),
+    "gc_hub_gemm": (ctypes.c_int, [_P, _I64, _I64, _I64, _P, _I64, _I32, _P, _P, _I64, _P, _U32,
+                                   _P]),
     "gc_hub_stair_supported": (ctypes.c_int, [_I64]),
     "gc_hub_stair_pair_bn": (ctypes.c_int, [_I64]),
-    "gc_hub_stair_gemm_bf16x3": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P, _P, _P, _I32, _P, _P,
-                                                _I32, _P, _I64, _I64, _P, _I64, _P, _U32, _P]),
+    "gc_hub_stair_gemm": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P, _P, _P, _I32, _P, _P, _I32, _P,
+                                         _I64, _I64, _I32, _P, _P, _I64, _P, _U32, _P]),
     "gc_tag_hub_columns": (ctypes.c_int, [_P, _I64, _P, _P, _P]),
 }
 

@@ -18,6 +18,7 @@
 #include <mutex>
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "common.cuh"
 
@@ -119,6 +120,10 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int n) {
 __host__ __device__ constexpr uint32_t idesc_bf16(int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((128u >> 4) << 24);
 }
+// D = F32, A = B = F16 (kind::f16, format 0), both K-major, M = 128.
+__host__ __device__ constexpr uint32_t idesc_f16(int n) {
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((128u >> 4) << 24);
+}
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                          uint32_t idesc, uint32_t accumulate) {
@@ -181,6 +186,7 @@ struct GemmEpi {
   const float *row_scale;
   int64_t M, N;
   uint32_t flags;
+  const float *scale;  // optional device scalar multiplied into every row (f16x2 unscale)
 };
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
@@ -198,7 +204,8 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 // of one fp32 operand); each k-block stages one A tile and TERMS B tiles and
 // issues TERMS MMAs per 32-byte step into the same accumulator, so
 // D = A·(B0 + B1 + B2) with the A tile read once.
-template <int BN, int TERMS, bool BF16>
+// ELEM: 0 = TF32 (kind::tf32), 1 = BF16, 2 = FP16 (kind::f16)
+template <int BN, int TERMS, int ELEM>
 __device__ __forceinline__ void gemm_tc_body(const CUtensorMap &map_a, const CUtensorMap &map_b,
                                              const CUtensorMap &map_c, const GemmEpi &ep,
                                              int num_kb, int stages, int m_tiles, int n_tiles,
@@ -206,6 +213,7 @@ __device__ __forceinline__ void gemm_tc_body(const CUtensorMap &map_a, const CUt
   constexpr uint32_t A_BYTES = BM * KB_BYTES;
   constexpr uint32_t B_BYTES = BN * KB_BYTES;
   constexpr uint32_t STAGE_BYTES = A_BYTES + TERMS * B_BYTES;
+  constexpr bool BF16 = ELEM != 0;  // 16-bit elements (kind::f16)
   constexpr int KB_ELEMS = BF16 ? 64 : 32;
   constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // power of two >= 32
 
@@ -271,7 +279,7 @@ __device__ __forceinline__ void gemm_tc_body(const CUtensorMap &map_a, const CUt
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer (one thread) ----------------
-      constexpr uint32_t idesc = BF16 ? idesc_bf16(BN) : idesc_tf32(BN);
+      constexpr uint32_t idesc = ELEM == 2 ? idesc_f16(BN) : ELEM == 1 ? idesc_bf16(BN) : idesc_tf32(BN);
       int it = 0, lt = 0;
       for (int tile = blockIdx.x; tile < n_tiles_total; tile += gridDim.x, ++lt) {
         const int acc = lt & 1;
@@ -316,7 +324,8 @@ __device__ __forceinline__ void gemm_tc_body(const CUtensorMap &map_a, const CUt
       tc_fence_after();
       const int row = m0 + q * 32 + lane;
       const bool row_ok = row < ep.M;
-      const float rs = (row_ok && ep.row_scale) ? __ldg(ep.row_scale + row) : 1.0f;
+      float rs = (row_ok && ep.row_scale) ? __ldg(ep.row_scale + row) : 1.0f;
+      if (ep.scale) rs *= __ldg(ep.scale);
       float *crow = ep.C + (int64_t)row * ep.ldc;
       const uint32_t taddr = tmem_base + (uint32_t)(acc * BN) + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
@@ -448,6 +457,10 @@ __device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
 __host__ __device__ constexpr uint32_t idesc_bf16_m256(int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((256u >> 4) << 24);
 }
+// D = F32, A = B = F16, K-major, M = 256 (cta pair), N = n
+__host__ __device__ constexpr uint32_t idesc_f16_m256(int n) {
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((256u >> 4) << 24);
+}
 
 // Staircase of dense blocks (hub.py): step s is the 0/1 block of rows
 // [0, rows[s]) (rows in degree-rank order) x columns [c0[s], c0[s] + 64*nkb[s])
@@ -482,14 +495,16 @@ __device__ __forceinline__ int stair_kblocks(const StairArgs &sa, int m0) {
   return t;
 }
 
-template <int BN>
+// FMT 0: three bf16 terms (exact fp32 split); 1: two fp16 terms of s·D·X
+// (22 significant bits, absolute error <= 2^-23 max|D·X|), 2/3 of the MMAs.
+template <int BN, int FMT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     gemm_hub_pair_tcgen05(const __grid_constant__ StairMaps maps,
                           const __grid_constant__ CUtensorMap map_b,
                           const __grid_constant__ CUtensorMap map_c, const GemmEpi ep,
                           const StairArgs sarg, int stages, int m_pairs, int n_tiles,
                           int tma_store, int b_rows_per_term) {
-  constexpr int TERMS = 3;
+  constexpr int TERMS = FMT ? 2 : 3;
   constexpr int BH = BN / 2;  // B rows per CTA per term
   constexpr uint32_t A_BYTES = BM * KB_BYTES;
   constexpr uint32_t B_BYTES = BH * KB_BYTES;
@@ -498,7 +513,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   // K-major [3*BH rows] operand, so ONE MMA with N = 3*BN covers all terms
   // (A is read once per k-step instead of three times) and the epilogue adds
   // the three term column groups.  Accumulator columns per tile:
-  constexpr bool TSTACK = BN <= 64;
+  constexpr bool TSTACK = TERMS * BN <= 256;
   constexpr int ACC_N = TSTACK ? 3 * BN : BN;
   constexpr uint32_t TMEM_COLS = 2 * ACC_N <= 32 ? 32 : 2 * ACC_N <= 64 ? 64 : 2 * ACC_N <= 128 ? 128
                                  : 2 * ACC_N <= 256 ? 256 : 512;
@@ -592,7 +607,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {  // ---------------- MMA issuer (leader only) ----------------
-      constexpr uint32_t idesc = idesc_bf16_m256(ACC_N);
+      constexpr uint32_t idesc = FMT ? idesc_f16_m256(ACC_N) : idesc_bf16_m256(ACC_N);
       int it = 0, lt = 0;
       for (int ti = t_begin; ti < t_end; ti += t_step, ++lt) {
         const int4 item = item_at(ti);
@@ -646,7 +661,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const int rrow = m0 + q * 32 + lane;  // rank-ordered row
       const bool row_ok = rrow < ep.M;
       const int row = (row_ok && sarg.row_map) ? __ldg(sarg.row_map + rrow) : rrow;
-      const float rs = (row_ok && ep.row_scale) ? __ldg(ep.row_scale + row) : 1.0f;
+      float rs = (row_ok && ep.row_scale) ? __ldg(ep.row_scale + row) : 1.0f;
+      if (ep.scale) rs *= __ldg(ep.scale);
       float *crow = ep.C + (int64_t)row * ep.ldc;
       const uint32_t taddr = tmem_base + (uint32_t)(acc * ACC_N) + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
@@ -656,12 +672,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         if constexpr (TSTACK) {
           // feature chunk c lives in CTA half h at column j of each term group
           const int h = c / BH, jj = c % BH;
-          float t1[16], t2[16];
-          tmem_ld16(taddr + (uint32_t)(h * 3 * BH + jj), v);
-          tmem_ld16(taddr + (uint32_t)(h * 3 * BH + BH + jj), t1);
-          tmem_ld16(taddr + (uint32_t)(h * 3 * BH + 2 * BH + jj), t2);
+          float t1[16];
+          tmem_ld16(taddr + (uint32_t)(h * TERMS * BH + jj), v);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = (v[i] + t1[i]) + t2[i];
+          for (int q = 1; q < TERMS; ++q) {
+            tmem_ld16(taddr + (uint32_t)(h * TERMS * BH + q * BH + jj), t1);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] += t1[i];
+          }
         } else {
           tmem_ld16(taddr + (uint32_t)c, v);
         }
@@ -742,8 +760,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                       const __grid_constant__ CUtensorMap map_b,
                       const __grid_constant__ CUtensorMap map_c, const GemmEpi ep, int num_kb,
                       int stages, int m_tiles, int n_tiles, int tma_store) {
-  gemm_tc_body<BN, 1, false>(map_a, map_b, map_c, ep, num_kb, stages, m_tiles, n_tiles, tma_store,
-                             0);
+  gemm_tc_body<BN, 1, 0>(map_a, map_b, map_c, ep, num_kb, stages, m_tiles, n_tiles, tma_store, 0);
 }
 
 // Dense hub block of the hybrid aggregation: C = D_row · A_hub · (B0 + B1 + B2)
@@ -756,8 +773,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                             const __grid_constant__ CUtensorMap map_c, const GemmEpi ep,
                             int num_kb, int stages, int m_tiles, int n_tiles, int tma_store,
                             int b_rows_per_term) {
-  gemm_tc_body<BN, 3, true>(map_a, map_b, map_c, ep, num_kb, stages, m_tiles, n_tiles, tma_store,
-                            b_rows_per_term);
+  gemm_tc_body<BN, 3, 1>(map_a, map_b, map_c, ep, num_kb, stages, m_tiles, n_tiles, tma_store,
+                         b_rows_per_term);
+}
+
+// The same with the two-term FP16 split (hi/lo fp16 of s·D·X, s a power of two)
+template <int BN>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_hub_f16x2_tcgen05(const __grid_constant__ CUtensorMap map_a,
+                           const __grid_constant__ CUtensorMap map_b,
+                           const __grid_constant__ CUtensorMap map_c, const GemmEpi ep,
+                           int num_kb, int stages, int m_tiles, int n_tiles, int tma_store,
+                           int b_rows_per_term) {
+  gemm_tc_body<BN, 2, 2>(map_a, map_b, map_c, ep, num_kb, stages, m_tiles, n_tiles, tma_store,
+                         b_rows_per_term);
 }
 
 // W (K x N, ldw) -> Wt (N x K, ldt): the K-major B operand.
@@ -883,7 +912,8 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 // with a (BK x box_rows) box and 128-byte swizzle; OOB elements read as 0.
 int make_map(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
              int box_rows, int box_cols = BK,
-             CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B, bool bf16 = false) {
+             CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B, bool bf16 = false,
+             bool f16 = false) {
   auto enc = get_encode_fn();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -893,7 +923,8 @@ int make_map(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int6
   cuuint64_t strides[1] = {(cuuint64_t)(ld * (bf16 ? 2 : 4))};
   cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+  CUresult r = enc(map, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                        : bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                    2, const_cast<void *>(ptr), dims,
                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -947,11 +978,12 @@ int launch_tf32(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap 
   return check_launch("gemm_tf32_tcgen05");
 }
 
-template <int BN>
+template <int BN, int FMT>
 int launch_hub(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mc, int tma_store,
                const GemmEpi &ep, int64_t T, int64_t kp, cudaStream_t st) {
+  constexpr int TERMS = FMT ? 2 : 3;
   const int num_kb = (int)((T + 63) / 64);
-  constexpr int stage_bytes = BM * KB_BYTES + 3 * BN * KB_BYTES;
+  constexpr int stage_bytes = BM * KB_BYTES + TERMS * BN * KB_BYTES;
   size_t smem = 0;
   int stages = tma_store ? ring_stages(stage_bytes, true, &smem) : 0;
   if (stages == 0) {  // no room for the staging buffers: direct stores
@@ -962,11 +994,11 @@ int launch_hub(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &
     set_error("gc_hub_gemm: tile does not fit shared memory");
     return GC_ERR_UNSUPPORTED;
   }
+  auto kern = FMT ? gemm_hub_f16x2_tcgen05<BN> : gemm_hub_bf16x3_tcgen05<BN>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(gemm_hub_bf16x3_tcgen05<BN>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   });
   if (attr_err != cudaSuccess) {
     set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
@@ -976,9 +1008,9 @@ int launch_hub(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &
   const int n_tiles = (int)((ep.N + BN - 1) / BN);
   const int64_t tiles = (int64_t)m_tiles * n_tiles;
   const int grid = (int)(tiles < sm_count() ? tiles : sm_count());
-  gemm_hub_bf16x3_tcgen05<BN><<<grid, kGemmThreads, smem, st>>>(
-      ma, mb, mc, ep, num_kb, stages, m_tiles, n_tiles, tma_store, (int)kp);
-  return check_launch("gemm_hub_bf16x3_tcgen05");
+  kern<<<grid, kGemmThreads, smem, st>>>(ma, mb, mc, ep, num_kb, stages, m_tiles, n_tiles,
+                                         tma_store, (int)kp);
+  return check_launch(FMT ? "gemm_hub_f16x2_tcgen05" : "gemm_hub_bf16x3_tcgen05");
 }
 
 // Split-K fixup: per split tile, sum its workspace partials in slot order and
@@ -999,11 +1031,11 @@ __global__ void hub_splitk_fixup_kernel(const float *__restrict__ ws, const int4
   }
 }
 
-template <int BN>
+template <int BN, int FMT>
 int launch_hub_pair(const StairMaps &maps, const StairArgs &sarg, const CUtensorMap &mb,
                     const CUtensorMap &mc, int tma_store, const GemmEpi &ep, int64_t kp,
                     cudaStream_t st, int sched_clusters = 0) {
-  constexpr int stage_bytes = BM * KB_BYTES + 3 * (BN / 2) * KB_BYTES;
+  constexpr int stage_bytes = BM * KB_BYTES + (FMT ? 2 : 3) * (BN / 2) * KB_BYTES;
   size_t smem = 0;
   int stages = tma_store ? ring_stages(stage_bytes, true, &smem) : 0;
   if (stages == 0) {
@@ -1017,7 +1049,7 @@ int launch_hub_pair(const StairMaps &maps, const StairArgs &sarg, const CUtensor
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(gemm_hub_pair_tcgen05<BN>,
+    attr_err = cudaFuncSetAttribute(gemm_hub_pair_tcgen05<BN, FMT>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   });
   if (attr_err != cudaSuccess) {
@@ -1031,20 +1063,34 @@ int launch_hub_pair(const StairMaps &maps, const StairArgs &sarg, const CUtensor
   // over the clusters, unless the caller passed an LPT schedule
   const int clusters = sched_clusters > 0 ? sched_clusters
                                           : (int)(tiles < sm_count() / 2 ? tiles : sm_count() / 2);
-  gemm_hub_pair_tcgen05<BN><<<2 * clusters, kGemmThreads, smem, st>>>(
+  gemm_hub_pair_tcgen05<BN, FMT><<<2 * clusters, kGemmThreads, smem, st>>>(
       maps, mb, mc, ep, sarg, stages, m_pairs, n_tiles, tma_store, (int)kp);
   return check_launch("gemm_hub_pair_tcgen05");
 }
 
 inline int pair_bn(int64_t K) { return K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256; }
 
-template <typename... Args>
-int launch_hub_pair_bn(int pbn, Args &&...args) {
+template <int FMT, typename... Args>
+int launch_hub_pair_bn_f(int pbn, Args &&...args) {
   switch (pbn) {
-    case 32: return launch_hub_pair<32>(args...);
-    case 64: return launch_hub_pair<64>(args...);
-    case 128: return launch_hub_pair<128>(args...);
-    default: return launch_hub_pair<256>(args...);
+    case 32: return launch_hub_pair<32, FMT>(args...);
+    case 64: return launch_hub_pair<64, FMT>(args...);
+    case 128: return launch_hub_pair<128, FMT>(args...);
+    default: return launch_hub_pair<256, FMT>(args...);
+  }
+}
+template <typename... Args>
+int launch_hub_pair_bn(int fmt, int pbn, Args &&...args) {
+  return fmt ? launch_hub_pair_bn_f<1>(pbn, args...) : launch_hub_pair_bn_f<0>(pbn, args...);
+}
+template <int FMT, typename... Args>
+int launch_hub_bn_f(int bn, Args &&...args) {
+  switch (bn) {
+    case 16: return launch_hub<16, FMT>(args...);
+    case 32: return launch_hub<32, FMT>(args...);
+    case 64: return launch_hub<64, FMT>(args...);
+    case 128: return launch_hub<128, FMT>(args...);
+    default: return launch_hub<256, FMT>(args...);
   }
 }
 
@@ -1060,34 +1106,102 @@ inline bool hub_pair_enabled() {
 // K-major B operand Bt[q][f][t] (f < kp; rows f >= K are zero).  hi = bf16(x),
 // mid = bf16(x - hi), lo = bf16(x - hi - mid): hi + mid + lo carries x's full
 // 24-bit mantissa, so A_hub (0/1) · B is an fp32-exact product.
-__global__ void hub_pack_kernel(const float *__restrict__ X, int64_t ldx, int64_t K,
-                                const int32_t *__restrict__ hub_cols, int64_t T,
-                                const float *__restrict__ d, int64_t kp,
-                                __nv_bfloat16 *__restrict__ Bt) {
-  __shared__ float tile[32][33];
-  const int64_t t0 = (int64_t)blockIdx.x * 32, f0 = (int64_t)blockIdx.y * 32;
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+__device__ __forceinline__ void split3(float x, __nv_bfloat16 &hi, __nv_bfloat16 &mid,
+                                       __nv_bfloat16 &lo) {
+  hi = __float2bfloat16_rn(x);
+  const float r1 = x - __bfloat162float(hi);
+  mid = __float2bfloat16_rn(r1);
+  lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+}
+
+// 64 hub rows x 32 features per block: coalesced 128-byte reads of the
+// gathered rows, then each thread writes a bf16x2 pair of hub positions for
+// each of the three terms (128-byte rows of the K-major operand per warp).
+__global__ void __launch_bounds__(256)
+    hub_pack_kernel(const float *__restrict__ X, int64_t ldx, int64_t K,
+                    const int32_t *__restrict__ hub_cols, int64_t T,
+                    const float *__restrict__ d, int64_t kp, __nv_bfloat16 *__restrict__ Bt) {
+  __shared__ float tile[64][33];
+  const int64_t t0 = (int64_t)blockIdx.x * 64, f0 = (int64_t)blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 64; i += blockDim.y) {
     const int64_t t = t0 + i, f = f0 + threadIdx.x;
     float x = 0.0f;
     if (t < T && f < K) {
-      const int64_t j = hub_cols[t];
-      x = X[j * ldx + f];
+      const int64_t j = __ldg(hub_cols + t);
+      x = __ldg(X + j * ldx + f);
       if (d) x *= __ldg(d + j);
     }
     tile[i][threadIdx.x] = x;
   }
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int64_t f = f0 + i, t = t0 + threadIdx.x;
+    const int64_t f = f0 + i, t = t0 + 2 * threadIdx.x;
     if (f >= kp || t >= T) continue;
-    const float x = tile[threadIdx.x][i];
-    const __nv_bfloat16 hi = __float2bfloat16_rn(x);
-    const float r1 = x - __bfloat162float(hi);
-    const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
-    const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
-    Bt[f * T + t] = hi;
-    Bt[(kp + f) * T + t] = mid;
-    Bt[(2 * kp + f) * T + t] = lo;
+    __nv_bfloat16 h0, m0, l0, h1, m1, l1;
+    split3(tile[2 * threadIdx.x][i], h0, m0, l0);
+    split3(tile[2 * threadIdx.x + 1][i], h1, m1, l1);
+    // T is a multiple of 64, so (t, t + 1) are both in range and 4-byte aligned
+    *reinterpret_cast<__nv_bfloat162 *>(Bt + f * T + t) = __halves2bfloat162(h0, h1);
+    *reinterpret_cast<__nv_bfloat162 *>(Bt + (kp + f) * T + t) = __halves2bfloat162(m0, m1);
+    *reinterpret_cast<__nv_bfloat162 *>(Bt + (2 * kp + f) * T + t) = __halves2bfloat162(l0, l1);
+  }
+}
+
+// |(D X)[hub_cols]| maximum (as float bits; non-negative floats order like ints)
+__global__ void __launch_bounds__(256)
+    hub_absmax_kernel(const float *__restrict__ X, int64_t ldx, int64_t K,
+                      const int32_t *__restrict__ hub_cols, int64_t T,
+                      const float *__restrict__ d, unsigned *__restrict__ out) {
+  float m = 0.0f;
+  const int64_t total = T * K;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / K, f = i % K;
+    const int64_t j = __ldg(hub_cols + t);
+    float x = __ldg(X + j * ldx + f);
+    if (d) x *= __ldg(d + j);
+    m = fmaxf(m, fabsf(x));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+}
+
+// Two fp16 terms of s·x, s = 2^(13 - floor(log2 max|x|)) so max|s·x| < 2^14:
+// hi = fp16(s x), lo = fp16(s x - hi) carry 22 significant bits of every
+// element above 2^-10 max|x| (absolute error <= 2^-23 max|x| for all).
+// Block (0, 0) publishes 1/s in scale[1] for the GEMM epilogue.
+__global__ void __launch_bounds__(256)
+    hub_pack_f16_kernel(const float *__restrict__ X, int64_t ldx, int64_t K,
+                        const int32_t *__restrict__ hub_cols, int64_t T,
+                        const float *__restrict__ d, int64_t kp, const unsigned *__restrict__ amax,
+                        float *__restrict__ inv_scale, __half *__restrict__ Bt) {
+  __shared__ float tile[64][33];
+  const float mx = __uint_as_float(*amax);
+  const int e = mx > 0.0f ? ilogbf(mx) : 0;
+  const float sc = ldexpf(1.0f, 13 - e);
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && threadIdx.y == 0)
+    *inv_scale = ldexpf(1.0f, e - 13);
+  const int64_t t0 = (int64_t)blockIdx.x * 64, f0 = (int64_t)blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 64; i += blockDim.y) {
+    const int64_t t = t0 + i, f = f0 + threadIdx.x;
+    float x = 0.0f;
+    if (t < T && f < K) {
+      const int64_t j = __ldg(hub_cols + t);
+      x = __ldg(X + j * ldx + f);
+      if (d) x *= __ldg(d + j);
+    }
+    tile[i][threadIdx.x] = x * sc;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t f = f0 + i, t = t0 + 2 * threadIdx.x;
+    if (f >= kp || t >= T) continue;
+    const float y0 = tile[2 * threadIdx.x][i], y1 = tile[2 * threadIdx.x + 1][i];
+    const __half h0 = __float2half_rn(y0), h1 = __float2half_rn(y1);
+    const __half l0 = __float2half_rn(y0 - __half2float(h0));
+    const __half l1 = __float2half_rn(y1 - __half2float(h1));
+    *reinterpret_cast<__half2 *>(Bt + f * T + t) = __halves2half2(h0, h1);
+    *reinterpret_cast<__half2 *>(Bt + (kp + f) * T + t) = __halves2half2(l0, l1);
   }
 }
 
@@ -1201,42 +1315,67 @@ extern "C" int64_t gc_hub_terms_rows(int64_t K) {
   return (K + bn - 1) / bn * bn;
 }
 
-extern "C" int gc_hub_pack_bf16x3(const float *X, int64_t ldx, int64_t K, const int32_t *hub_cols,
-                                  int64_t T, const float *d_col, void *Bt, void *stream) {
-  GC_REQUIRE(K >= 1 && T >= 0 && ldx >= K, GC_ERR_SHAPE, "gc_hub_pack_bf16x3: bad shape");
+extern "C" int gc_hub_pack(const float *X, int64_t ldx, int64_t K, const int32_t *hub_cols,
+                           int64_t T, const float *d_col, int32_t fmt, void *Bt, float *scale_ws,
+                           void *stream) {
+  GC_REQUIRE(K >= 1 && T >= 0 && ldx >= K, GC_ERR_SHAPE, "gc_hub_pack: bad shape");
+  GC_REQUIRE(fmt == GC_HUB_BF16X3 || fmt == GC_HUB_F16X2, GC_ERR_VALUE, "gc_hub_pack: format %d",
+             fmt);
   if (T == 0) return GC_OK;
-  GC_REQUIRE(X && hub_cols && Bt, GC_ERR_VALUE, "gc_hub_pack_bf16x3: null operand");
+  GC_REQUIRE(X && hub_cols && Bt && (fmt == GC_HUB_BF16X3 || scale_ws), GC_ERR_VALUE,
+             "gc_hub_pack: null operand");
   const int64_t kp = gc_hub_terms_rows(K);
-  dim3 grid((unsigned)((T + 31) / 32), (unsigned)((kp + 31) / 32));
-  GC_REQUIRE(grid.y < 65536, GC_ERR_SHAPE, "gc_hub_pack_bf16x3: K too large");
-  hub_pack_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(
-      X, ldx, K, hub_cols, T, d_col, kp, static_cast<__nv_bfloat16 *>(Bt));
-  return check_launch("hub_pack_kernel");
+  GC_REQUIRE(T % 64 == 0, GC_ERR_SHAPE, "gc_hub_pack: T must be a multiple of 64");
+  dim3 grid((unsigned)((T + 63) / 64), (unsigned)((kp + 31) / 32));
+  GC_REQUIRE(grid.y < 65536, GC_ERR_SHAPE, "gc_hub_pack: K too large");
+  cudaStream_t st = as_stream(stream);
+  if (fmt == GC_HUB_BF16X3) {
+    hub_pack_kernel<<<grid, dim3(32, 8), 0, st>>>(X, ldx, K, hub_cols, T, d_col, kp,
+                                                  static_cast<__nv_bfloat16 *>(Bt));
+    return check_launch("hub_pack_kernel");
+  }
+  unsigned *amax = reinterpret_cast<unsigned *>(scale_ws);
+  if (cudaMemsetAsync(amax, 0, sizeof(unsigned), st) != cudaSuccess) {
+    set_error("gc_hub_pack: %s", cudaGetErrorString(cudaGetLastError()));
+    return GC_ERR_CUDA;
+  }
+  const int64_t work = T * K;
+  const int64_t blocks = std::min<int64_t>((work + 255) / 256, (int64_t)sm_count() * 8);
+  hub_absmax_kernel<<<(unsigned)blocks, 256, 0, st>>>(X, ldx, K, hub_cols, T, d_col, amax);
+  int rc = check_launch("hub_absmax_kernel");
+  if (rc) return rc;
+  hub_pack_f16_kernel<<<grid, dim3(32, 8), 0, st>>>(X, ldx, K, hub_cols, T, d_col, kp, amax,
+                                                    scale_ws + 1, static_cast<__half *>(Bt));
+  return check_launch("hub_pack_f16_kernel");
 }
 
-extern "C" int gc_hub_gemm_bf16x3(const void *A_hub, int64_t lda, int64_t n_rows, int64_t T,
-                                  const void *Bt, int64_t K, float *C, int64_t ldc,
-                                  const float *d_row, uint32_t flags, void *stream) {
+extern "C" int gc_hub_gemm(const void *A_hub, int64_t lda, int64_t n_rows, int64_t T,
+                           const void *Bt, int64_t K, int32_t fmt, const float *scale_ws,
+                           float *C, int64_t ldc, const float *d_row, uint32_t flags,
+                           void *stream) {
   GC_REQUIRE(n_rows >= 0 && T >= 0 && K >= 1 && lda >= T && ldc >= K, GC_ERR_SHAPE,
-             "gc_hub_gemm_bf16x3: bad shape");
+             "gc_hub_gemm: bad shape");
+  GC_REQUIRE(fmt == GC_HUB_BF16X3 || fmt == GC_HUB_F16X2, GC_ERR_VALUE, "gc_hub_gemm: format %d",
+             fmt);
   GC_REQUIRE((flags & ~(GC_RELU | GC_ACCUMULATE)) == 0, GC_ERR_VALUE,
-             "gc_hub_gemm_bf16x3: unknown flags 0x%x", flags);
+             "gc_hub_gemm: unknown flags 0x%x", flags);
   if (n_rows == 0) return GC_OK;
-  GC_REQUIRE(A_hub && Bt && C, GC_ERR_VALUE, "gc_hub_gemm_bf16x3: null operand");
+  GC_REQUIRE(A_hub && Bt && C && (fmt == GC_HUB_BF16X3 || scale_ws), GC_ERR_VALUE,
+             "gc_hub_gemm: null operand");
   GC_REQUIRE(T % 64 == 0 && T > 0 && lda % 8 == 0 && aligned16(A_hub) && aligned16(Bt),
              GC_ERR_UNSUPPORTED,
-             "gc_hub_gemm_bf16x3: needs T %% 64 == 0, lda %% 8 == 0, 16-byte aligned operands");
+             "gc_hub_gemm: needs T %% 64 == 0, lda %% 8 == 0, 16-byte aligned operands");
   GC_REQUIRE(n_rows < (int64_t)INT32_MAX && T < (int64_t)INT32_MAX, GC_ERR_SHAPE,
-             "gc_hub_gemm_bf16x3: dimension exceeds TMA range");
+             "gc_hub_gemm: dimension exceeds TMA range");
   cudaStream_t st = as_stream(stream);
+  const int terms = fmt == GC_HUB_F16X2 ? 2 : 3;
   const int bn = hub_bn(K);
   const int64_t kp = gc_hub_terms_rows(K);
   CUtensorMap ma, mb, mc;
-  int rc = make_map(&ma, A_hub, n_rows, T, lda, BM, 64, CU_TENSOR_MAP_SWIZZLE_128B, true);
+  int rc = make_map(&ma, A_hub, n_rows, T, lda, BM, 64, CU_TENSOR_MAP_SWIZZLE_128B, true,
+                    fmt == GC_HUB_F16X2);
   if (rc) return rc;
-  rc = make_map(&mb, Bt, 3 * kp, T, T, bn, 64, CU_TENSOR_MAP_SWIZZLE_128B, true);
-  if (rc) return rc;
-  GemmEpi ep{C, ldc, d_row, n_rows, K, flags};
+  GemmEpi ep{C, ldc, d_row, n_rows, K, flags, fmt == GC_HUB_F16X2 ? scale_ws + 1 : nullptr};
   // accumulating epilogues read C back: direct stores
   int tma_store = ((ldc % 4) == 0 && aligned16(C) && !(flags & GC_ACCUMULATE)) ? 1 : 0;
   memset(&mc, 0, sizeof(mc));
@@ -1249,7 +1388,8 @@ extern "C" int gc_hub_gemm_bf16x3(const void *A_hub, int64_t lda, int64_t n_rows
     // the plain hub block is a one-step staircase
     const int pbn = pair_bn(K);
     CUtensorMap mbp;
-    rc = make_map(&mbp, Bt, 3 * kp, T, T, pbn / 2, 64, CU_TENSOR_MAP_SWIZZLE_128B, true);
+    rc = make_map(&mbp, Bt, terms * kp, T, T, pbn / 2, 64, CU_TENSOR_MAP_SWIZZLE_128B, true,
+                  fmt == GC_HUB_F16X2);
     if (rc) return rc;
     StairMaps maps;
     memset(&maps, 0, sizeof(maps));
@@ -1260,15 +1400,13 @@ extern "C" int gc_hub_gemm_bf16x3(const void *A_hub, int64_t lda, int64_t n_rows
     sarg.c0[0] = 0;
     sarg.nkb[0] = (int)(T / 64);
     sarg.row_map = nullptr;
-    return launch_hub_pair_bn(pbn, maps, sarg, mbp, mc, tma_store, ep, kp, st);
+    return launch_hub_pair_bn(fmt, pbn, maps, sarg, mbp, mc, tma_store, ep, kp, st, 0);
   }
-  switch (bn) {
-    case 16: return launch_hub<16>(ma, mb, mc, tma_store, ep, T, kp, st);
-    case 32: return launch_hub<32>(ma, mb, mc, tma_store, ep, T, kp, st);
-    case 64: return launch_hub<64>(ma, mb, mc, tma_store, ep, T, kp, st);
-    case 128: return launch_hub<128>(ma, mb, mc, tma_store, ep, T, kp, st);
-    default: return launch_hub<256>(ma, mb, mc, tma_store, ep, T, kp, st);
-  }
+  rc = make_map(&mb, Bt, terms * kp, T, T, bn, 64, CU_TENSOR_MAP_SWIZZLE_128B, true,
+                fmt == GC_HUB_F16X2);
+  if (rc) return rc;
+  return fmt == GC_HUB_F16X2 ? launch_hub_bn_f<1>(bn, ma, mb, mc, tma_store, ep, T, kp, st)
+                             : launch_hub_bn_f<0>(bn, ma, mb, mc, tma_store, ep, T, kp, st);
 }
 
 extern "C" int gc_hub_stair_pair_bn(int64_t K) { return K > 0 ? pair_bn(K) : 0; }
@@ -1277,37 +1415,39 @@ extern "C" int gc_hub_stair_supported(int64_t K) {
   return (hub_pair_enabled() && K > 16 && gc_hub_terms_rows(K) % pair_bn(K) == 0) ? 1 : 0;
 }
 
-extern "C" int gc_hub_stair_gemm_bf16x3(const void *const *A_steps, const int64_t *step_rows,
-                                        const int64_t *step_c0, const int64_t *step_width,
-                                        int32_t n_steps, const int32_t *row_map,
-                                        const int32_t *items, const int32_t *cluster_start,
-                                        int32_t n_clusters, float *workspace,
-                                        const int32_t *fixups, int32_t n_fixups, const void *Bt,
-                                        int64_t T, int64_t K, float *C, int64_t ldc,
-                                        const float *d_row, uint32_t flags, void *stream) {
+extern "C" int gc_hub_stair_gemm(const void *const *A_steps, const int64_t *step_rows,
+                                 const int64_t *step_c0, const int64_t *step_width,
+                                 int32_t n_steps, const int32_t *row_map, const int32_t *items,
+                                 const int32_t *cluster_start, int32_t n_clusters,
+                                 float *workspace, const int32_t *fixups, int32_t n_fixups,
+                                 const void *Bt, int64_t T, int64_t K, int32_t fmt,
+                                 const float *scale_ws, float *C, int64_t ldc, const float *d_row,
+                                 uint32_t flags, void *stream) {
+  GC_REQUIRE(fmt == GC_HUB_BF16X3 || (fmt == GC_HUB_F16X2 && scale_ws), GC_ERR_VALUE,
+             "gc_hub_stair_gemm: format %d", fmt);
   GC_REQUIRE(n_steps >= 1 && n_steps <= kMaxSteps, GC_ERR_VALUE,
-             "gc_hub_stair_gemm_bf16x3: 1..%d steps", kMaxSteps);
+             "gc_hub_stair_gemm: 1..%d steps", kMaxSteps);
   GC_REQUIRE(K >= 1 && T > 0 && T % 64 == 0 && ldc >= K, GC_ERR_SHAPE,
-             "gc_hub_stair_gemm_bf16x3: bad shape");
+             "gc_hub_stair_gemm: bad shape");
   GC_REQUIRE((flags & ~(GC_RELU | GC_ACCUMULATE)) == 0, GC_ERR_VALUE,
-             "gc_hub_stair_gemm_bf16x3: unknown flags 0x%x", flags);
+             "gc_hub_stair_gemm: unknown flags 0x%x", flags);
   GC_REQUIRE(A_steps && step_rows && step_c0 && step_width && Bt && C, GC_ERR_VALUE,
-             "gc_hub_stair_gemm_bf16x3: null operand");
+             "gc_hub_stair_gemm: null operand");
   GC_REQUIRE(gc_hub_stair_supported(K), GC_ERR_UNSUPPORTED,
-             "gc_hub_stair_gemm_bf16x3: K=%lld has no CTA-pair tile", (long long)K);
-  GC_REQUIRE(aligned16(Bt), GC_ERR_UNSUPPORTED, "gc_hub_stair_gemm_bf16x3: Bt alignment");
+             "gc_hub_stair_gemm: K=%lld has no CTA-pair tile", (long long)K);
+  GC_REQUIRE(aligned16(Bt), GC_ERR_UNSUPPORTED, "gc_hub_stair_gemm: Bt alignment");
   StairMaps maps;
   memset(&maps, 0, sizeof(maps));
   GC_REQUIRE((items == nullptr) == (cluster_start == nullptr), GC_ERR_VALUE,
-             "gc_hub_stair_gemm_bf16x3: items and cluster_start go together");
+             "gc_hub_stair_gemm: items and cluster_start go together");
   GC_REQUIRE(items == nullptr || (n_clusters >= 1 && n_clusters <= sm_count() / 2),
-             GC_ERR_VALUE, "gc_hub_stair_gemm_bf16x3: 1..%d clusters", sm_count() / 2);
+             GC_ERR_VALUE, "gc_hub_stair_gemm: 1..%d clusters", sm_count() / 2);
   GC_REQUIRE(n_fixups >= 0 && (n_fixups == 0 || (fixups && workspace && items)), GC_ERR_VALUE,
-             "gc_hub_stair_gemm_bf16x3: split-K needs items, workspace and fixups");
+             "gc_hub_stair_gemm: split-K needs items, workspace and fixups");
   GC_REQUIRE(n_fixups == 0 || !(flags & GC_RELU), GC_ERR_VALUE,
-             "gc_hub_stair_gemm_bf16x3: ReLU cannot follow split-K partials");
+             "gc_hub_stair_gemm: ReLU cannot follow split-K partials");
   GC_REQUIRE(workspace == nullptr || aligned16(workspace), GC_ERR_WORKSPACE,
-             "gc_hub_stair_gemm_bf16x3: 16-byte aligned workspace required");
+             "gc_hub_stair_gemm: 16-byte aligned workspace required");
   StairArgs sarg{};
   sarg.n_steps = n_steps;
   sarg.row_map = row_map;
@@ -1317,12 +1457,13 @@ extern "C" int gc_hub_stair_gemm_bf16x3(const void *const *A_steps, const int64_
   for (int s = 0; s < n_steps; ++s) {
     const int64_t r = step_rows[s], c0 = step_c0[s], w = step_width[s];
     GC_REQUIRE(r >= 1 && r < INT32_MAX && w > 0 && w % 64 == 0 && c0 % 64 == 0 && c0 + w <= T,
-               GC_ERR_SHAPE, "gc_hub_stair_gemm_bf16x3: bad step %d", s);
+               GC_ERR_SHAPE, "gc_hub_stair_gemm: bad step %d", s);
     GC_REQUIRE(s == 0 || (r <= step_rows[s - 1] && c0 == step_c0[s - 1] + step_width[s - 1]),
-               GC_ERR_SHAPE, "gc_hub_stair_gemm_bf16x3: steps must be a staircase");
+               GC_ERR_SHAPE, "gc_hub_stair_gemm: steps must be a staircase");
     GC_REQUIRE(A_steps[s] && aligned16(A_steps[s]), GC_ERR_VALUE,
-               "gc_hub_stair_gemm_bf16x3: step %d operand", s);
-    int rc = make_map(&maps.a[s], A_steps[s], r, w, w, BM, 64, CU_TENSOR_MAP_SWIZZLE_128B, true);
+               "gc_hub_stair_gemm: step %d operand", s);
+    int rc = make_map(&maps.a[s], A_steps[s], r, w, w, BM, 64, CU_TENSOR_MAP_SWIZZLE_128B, true,
+                      fmt == GC_HUB_F16X2);
     if (rc) return rc;
     sarg.rows[s] = (int)r;
     sarg.c0[s] = (int)c0;
@@ -1331,7 +1472,8 @@ extern "C" int gc_hub_stair_gemm_bf16x3(const void *const *A_steps, const int64_
   const int64_t kp = gc_hub_terms_rows(K);
   const int pbn = pair_bn(K);
   CUtensorMap mbp, mc;
-  int rc = make_map(&mbp, Bt, 3 * kp, T, T, pbn / 2, 64, CU_TENSOR_MAP_SWIZZLE_128B, true);
+  int rc = make_map(&mbp, Bt, (fmt == GC_HUB_F16X2 ? 2 : 3) * kp, T, T, pbn / 2, 64,
+                    CU_TENSOR_MAP_SWIZZLE_128B, true, fmt == GC_HUB_F16X2);
   if (rc) return rc;
   memset(&mc, 0, sizeof(mc));
   // rank-ordered rows scatter through row_map: direct stores
@@ -1341,9 +1483,10 @@ extern "C" int gc_hub_stair_gemm_bf16x3(const void *const *A_steps, const int64_
     rc = make_map(&mc, C, step_rows[0], K, ldc, 32, 16, CU_TENSOR_MAP_SWIZZLE_64B);
     if (rc) return rc;
   }
-  GemmEpi ep{C, ldc, d_row, step_rows[0], K, flags};
+  GemmEpi ep{C, ldc, d_row, step_rows[0], K, flags,
+             fmt == GC_HUB_F16X2 ? scale_ws + 1 : nullptr};
   cudaStream_t st = as_stream(stream);
-  rc = launch_hub_pair_bn(pbn, maps, sarg, mbp, mc, tma_store, ep, kp, st,
+  rc = launch_hub_pair_bn(fmt, pbn, maps, sarg, mbp, mc, tma_store, ep, kp, st,
                           items ? (int)n_clusters : 0);
   if (rc || n_fixups == 0) return rc;
   const int n_tiles = (int)((K + pbn - 1) / pbn);

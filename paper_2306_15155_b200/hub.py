@@ -14,11 +14,14 @@ shared memory:
 
     C_dense = D · A_dense · (D X)[dense columns],   A_dense ∈ {0,1}
 
-computed by tcgen05 kind::f16 GEMMs: the 0/1 blocks are exact in bf16 and
-(D X)[columns] is split into three bf16 terms that together carry its fp32
-mantissa (``gc_hub_pack_bf16x3``), so the dense part keeps fp32 precision.
-The SpMM then accumulates the remaining edges on top (GC_ACCUMULATE).  Only
-the summation order differs from the plain SpMM.
+computed by tcgen05 kind::f16 GEMMs: the 0/1 blocks are exact in fp16/bf16
+and (D X)[columns] is split into 16-bit terms (``gc_hub_pack``): by default
+two fp16 terms of s·D·X with a power-of-two scale s (22 significant bits:
+absolute error <= 2^-23·max|D X| per element, normwise ~1e-7), or three bf16
+terms that carry its exact fp32 mantissa (GNNC_HUB_FORMAT=bf16x3, 1.5x the
+MMAs).  The SpMM then accumulates the remaining edges on top
+(GC_ACCUMULATE); apart from the term split only the summation order differs
+from the plain SpMM.
 
 Two plans:
 
@@ -29,7 +32,7 @@ Two plans:
   band whose density in that column band is ≥ δ — a staircase hugging the
   dense corner (the high-degree rows are dense far beyond the top columns).
   All steps run in ONE CTA-pair GEMM whose rank-ordered tiles reduce over a
-  prefix of the steps (``gc_hub_stair_gemm_bf16x3``), scattering rows back
+  prefix of the steps (``gc_hub_stair_gemm``), scattering rows back
   through the rank permutation.
 
 The split applies to a unit-valued Ã (the reference's own generated graphs and
@@ -50,6 +53,17 @@ from . import _native as nat
 from .sparse import CsrMatrix, ShapeError, _ld, _require_cuda, _spmm, _stream, _timed_call
 
 HUB_SPLIT = os.environ.get("GNNC_HUB_SPLIT", "auto")
+# term format of the dense operand: "f16x2" (default: two fp16 terms of s·D·X,
+# 22 significant bits, 2/3 of the MMAs) or "bf16x3" (exact fp32 split)
+HUB_FORMAT = os.environ.get("GNNC_HUB_FORMAT", "f16x2")
+
+
+def _fmt() -> int:
+    return nat.GC_HUB_F16X2 if HUB_FORMAT == "f16x2" else nat.GC_HUB_BF16X3
+
+
+def _block_dtype(fmt: int):
+    return torch.float16 if fmt == nat.GC_HUB_F16X2 else torch.bfloat16
 HUB_T_CANDIDATES = (1024, 2048, 4096, 8192)
 # (cell/edge cost ratio δ, balance slack) pairs tried by the autotuner
 # (slack > 1 reaches further right, but short-wide steps stream their B
@@ -72,6 +86,7 @@ HUB_MIN_NNZ = 1 << 24            # smaller graphs stay on the SpMM alone
 HUB_MIN_DENSITY = 0.02           # mean density of a block worth a dense product
 HUB_MEM_BUDGET = 8 << 30         # bytes of dense blocks per pattern
 STAIR_MAX_STEPS = 16
+STAIR_FIRST_BAND = 1024          # rows / columns of the first histogram band
 STAIR_CLUSTERS = 74              # CTA pairs of a B200 (balance bound of the top tile)
 
 
@@ -131,8 +146,9 @@ class HubPlan(_TailMixin):
         is_hub = colpos >= 0
         rows = a.row_of_nnz()
         self.T = T
+        self.fmt = _fmt()
         self.hub_cols = hub.to(torch.int32).contiguous()
-        self.a_hub = torch.zeros(a.n_rows, T, dtype=torch.bfloat16, device=dev)
+        self.a_hub = torch.zeros(a.n_rows, T, dtype=_block_dtype(self.fmt), device=dev)
         self.a_hub[rows[is_hub], colpos[is_hub]] = 1.0
         self.cells = a.n_rows * T
         self._init_tail(a, ~is_hub, rows)
@@ -173,8 +189,9 @@ class StairPlan(_TailMixin):
         step = torch.bucketize(ec.clamp(max=C - 1), c_starts, right=True) - 1
         covered = in_cols & (er < r_limits[step])
         self.blocks = []
+        self.fmt = _fmt()
         for s, (R, c0, W) in enumerate(self.steps):
-            blk = torch.zeros(R, W, dtype=torch.bfloat16, device=dev)
+            blk = torch.zeros(R, W, dtype=_block_dtype(self.fmt), device=dev)
             sel = covered & (step == s)
             blk[er[sel], ec[sel] - c0] = 1.0
             self.blocks.append(blk)
@@ -320,22 +337,27 @@ def hub_plan(a: CsrMatrix, spec):
     key = ("hubsplit", spec)
     if key not in a._plans:
         if isinstance(spec, tuple):
-            a._plans[key] = StairPlan(a, spec[1] / 1000.0, slack=spec[2] / 10.0)
+            a._plans[key] = StairPlan(a, spec[1] / 1000.0, slack=spec[2] / 10.0,
+                                      first_band=STAIR_FIRST_BAND)
         else:
             a._plans[key] = HubPlan(a, spec)
     return a._plans[key]
 
 
-def pack(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec) -> torch.Tensor:
-    """The dense-part operand (D X)[hub_cols] as three bf16 terms, K-major."""
+def pack(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec):
+    """The dense-part operand (D X)[hub_cols] as bf16/fp16 terms, K-major, and
+    the fp16 format's scale workspace (float[2]: max, 1/s)."""
     plan = hub_plan(a, spec)
     lib = nat.load()
     K = x.shape[1]
     kp = int(lib.gc_hub_terms_rows(K))
-    bt = torch.empty(3 * kp * plan.T, dtype=torch.bfloat16, device=x.device)
-    nat.check(lib.gc_hub_pack_bf16x3(x.data_ptr(), _ld(x), K, plan.hub_cols.data_ptr(), plan.T,
-                                     d.data_ptr(), bt.data_ptr(), _stream(x.device)), "hub_pack")
-    return bt
+    terms = 2 if plan.fmt == nat.GC_HUB_F16X2 else 3
+    bt = torch.empty(terms * kp * plan.T, dtype=_block_dtype(plan.fmt), device=x.device)
+    sc = torch.empty(2, dtype=torch.float32, device=x.device)
+    nat.check(lib.gc_hub_pack(x.data_ptr(), _ld(x), K, plan.hub_cols.data_ptr(), plan.T,
+                              d.data_ptr(), plan.fmt, bt.data_ptr(), sc.data_ptr(),
+                              _stream(x.device)), "hub_pack")
+    return bt, sc
 
 
 def dense_part(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, out: torch.Tensor, *,
@@ -347,27 +369,28 @@ def dense_part(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, out: torch.
     lib = nat.load()
     st = _stream(dev)
     K = x.shape[1]
-    bt = packed if packed is not None else pack(a, x, d, spec)
+    bt, sc = packed if packed is not None else pack(a, x, d, spec)
     flags = nat.GC_ACCUMULATE if accumulate else 0
     if plan.kind == "block":
         lo, hi = rows if rows is not None else (0, a.n_rows)
         a_hub = plan.a_hub[lo:hi]
         dr = d_row[lo:hi]
-        nat.check(_timed_call("hub_gemm", dev, lambda: lib.gc_hub_gemm_bf16x3(
-            a_hub.data_ptr(), plan.T, hi - lo, plan.T, bt.data_ptr(), K, out.data_ptr(), _ld(out),
-            dr.data_ptr(), flags, st)), "hub_gemm")
+        nat.check(_timed_call("hub_gemm", dev, lambda: lib.gc_hub_gemm(
+            a_hub.data_ptr(), plan.T, hi - lo, plan.T, bt.data_ptr(), K, plan.fmt, sc.data_ptr(),
+            out.data_ptr(), _ld(out), dr.data_ptr(), flags, st)), "hub_gemm")
         return
     if rows is not None and tuple(rows) != (0, a.n_rows):
         raise ShapeError("stair split: the dense part covers all rows (rank-ordered tiles)")
     if plan.rows0 < a.n_rows and not accumulate:
         out.zero_()  # rows outside every step receive only the tail
     items, starts, n_cl, ws, fx = plan.schedule(K, dev)
-    nat.check(_timed_call("hub_gemm", dev, lambda: lib.gc_hub_stair_gemm_bf16x3(
+    nat.check(_timed_call("hub_gemm", dev, lambda: lib.gc_hub_stair_gemm(
         plan._np_ptrs.ctypes.data, plan._np_rows.ctypes.data, plan._np_c0.ctypes.data,
         plan._np_w.ctypes.data, len(plan.steps), plan.row_map.data_ptr(), items.data_ptr(),
         starts.data_ptr(), n_cl, None if ws is None else ws.data_ptr(),
         None if fx is None else fx.data_ptr(), 0 if fx is None else fx.shape[0], bt.data_ptr(),
-        plan.T, K, out.data_ptr(), _ld(out), d_row.data_ptr(), flags, st)), "hub_stair_gemm")
+        plan.T, K, plan.fmt, sc.data_ptr(), out.data_ptr(), _ld(out), d_row.data_ptr(), flags,
+        st)), "hub_stair_gemm")
 
 
 def tail_part(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, out: torch.Tensor, *,
@@ -462,7 +485,12 @@ def choose_split(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, *,
             return 0
         d_row = d
     if mode != "auto":
-        return _parse_spec(mode)
+        spec = _parse_spec(mode)
+        try:
+            hub_plan(a, spec)
+        except (ValueError, ShapeError):
+            return 0  # the forced split does not fit this pattern
+        return spec
     K = x.shape[1]
     key = ("hubsplit-choice", int(K), values is not None)
     if key in a._plans:

@@ -1,7 +1,8 @@
 """Does the hub GEMM overlap the tail SpMM on a side stream?  Times
 sequential (GEMM then tail with ACCUMULATE) against concurrent (GEMM on a
 side stream into its own buffer, tail on the main stream, then a combine)."""
-import sys, json
+import sys, json, os
+os.environ.setdefault("GNNC_HUB_FORMAT", "bf16x3")  # the probe packs bf16x3 terms
 import torch
 sys.path.insert(0, ".")
 import paper_2306_15155_b200 as gc
@@ -15,6 +16,7 @@ plan = hub.hub_plan(a, T)
 lib = nat.load()
 kp = lib.gc_hub_terms_rows(K)
 bt = torch.empty(3 * kp * T, dtype=torch.bfloat16, device=dev)
+sc = torch.empty(2, device=dev)
 out = torch.empty(a.n_rows, K, device=dev); ch = torch.empty_like(out)
 side = torch.cuda.Stream(dev)
 def t_ms(fn, reps=10):
@@ -26,8 +28,8 @@ def t_ms(fn, reps=10):
         e0.record(); fn(); e1.record(); torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
     return sorted(ts)[reps // 2]
 def pg(dst, st):
-    nat.check(lib.gc_hub_pack_bf16x3(x.data_ptr(), K, K, plan.hub_cols.data_ptr(), T, d.data_ptr(), bt.data_ptr(), st), "p")
-    nat.check(lib.gc_hub_gemm_bf16x3(plan.a_hub.data_ptr(), T, a.n_rows, T, bt.data_ptr(), K, dst.data_ptr(), K, d.data_ptr(), 0, st), "g")
+    nat.check(lib.gc_hub_pack(x.data_ptr(), K, K, plan.hub_cols.data_ptr(), T, d.data_ptr(), 0, bt.data_ptr(), sc.data_ptr(), st), "p")
+    nat.check(lib.gc_hub_gemm(plan.a_hub.data_ptr(), T, a.n_rows, T, bt.data_ptr(), K, 0, sc.data_ptr(), dst.data_ptr(), K, d.data_ptr(), 0, st), "g")
 def seq():
     pg(out, torch.cuda.current_stream().cuda_stream)
     sparse._spmm(plan.tail, x, weighted=False, d_row=d, d_col=d, out=out, accumulate=True, relu=True, timer=None)

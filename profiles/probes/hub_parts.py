@@ -1,6 +1,7 @@
 """Component times of the hybrid aggregation on a named shape at one K and T:
 pack, hub GEMM (TFLOP/s over the 3-term product), tail SpMM."""
-import sys, json
+import sys, json, os
+os.environ.setdefault("GNNC_HUB_FORMAT", "bf16x3")  # the probe packs bf16x3 terms
 import torch
 sys.path.insert(0, ".")
 import paper_2306_15155_b200 as gc
@@ -14,6 +15,7 @@ plan = hub.hub_plan(a, T)
 lib = nat.load(); st = torch.cuda.current_stream().cuda_stream
 kp = lib.gc_hub_terms_rows(K)
 bt = torch.empty(3 * kp * T, dtype=torch.bfloat16, device=dev)
+sc = torch.empty(2, device=dev)
 out = torch.empty(a.n_rows, K, device=dev)
 def t_ms(fn, reps=10):
     for _ in range(3): fn()
@@ -23,8 +25,8 @@ def t_ms(fn, reps=10):
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
         e0.record(); fn(); e1.record(); torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
     return sorted(ts)[reps // 2]
-pack = lambda: nat.check(lib.gc_hub_pack_bf16x3(x.data_ptr(), K, K, plan.hub_cols.data_ptr(), T, d.data_ptr(), bt.data_ptr(), st), "p")
-gemm = lambda: nat.check(lib.gc_hub_gemm_bf16x3(plan.a_hub.data_ptr(), T, a.n_rows, T, bt.data_ptr(), K, out.data_ptr(), K, d.data_ptr(), 0, st), "g")
+pack = lambda: nat.check(lib.gc_hub_pack(x.data_ptr(), K, K, plan.hub_cols.data_ptr(), T, d.data_ptr(), 0, bt.data_ptr(), sc.data_ptr(), st), "p")
+gemm = lambda: nat.check(lib.gc_hub_gemm(plan.a_hub.data_ptr(), T, a.n_rows, T, bt.data_ptr(), K, 0, sc.data_ptr(), out.data_ptr(), K, d.data_ptr(), 0, st), "g")
 tail = lambda: sparse._spmm(plan.tail, x, weighted=False, d_row=d, d_col=d, out=out, accumulate=True, timer=None)
 r = {"shape": shape, "K": K, "T": T, "hub_edges_frac": plan.hub_edges / a.nnz}
 r["pack_ms"] = t_ms(pack); r["gemm_ms"] = t_ms(gemm); r["tail_ms"] = t_ms(tail)

@@ -563,8 +563,15 @@ def hub_pl():
 
 @pytest.mark.parametrize("K", [1, 7, 16, 32, 100, 256, 300, 512])
 @pytest.mark.parametrize("T", [64, 128])
-def test_hub_gemm_is_fp32_exact(oracle, K, T):
+@pytest.mark.parametrize("fmt", ["bf16x3", "f16x2"])
+def test_hub_gemm_term_split(oracle, K, T, fmt):
+    """Dense 0/1 block times the packed terms of D·X: bf16x3 is the exact fp32
+    split (1e-6 normwise with rows spanning six decades), f16x2 carries 22
+    significant bits relative to max|D·X| (absolute error <= 2^-23 max)."""
     from paper_2306_15155_b200 import _native as nat
+    f = nat.GC_HUB_F16X2 if fmt == "f16x2" else nat.GC_HUB_BF16X3
+    dt = torch.float16 if fmt == "f16x2" else torch.bfloat16
+    terms = 2 if fmt == "f16x2" else 3
     rng = np.random.default_rng(K * 7 + T)
     n, ncols = 777, 3000
     a_hub = (rng.random((n, T)) < 0.3).astype(np.float32)
@@ -574,19 +581,24 @@ def test_hub_gemm_is_fp32_exact(oracle, K, T):
     dr = f32(rng.uniform(0.05, 1.0, n))
     lib = nat.load()
     kp = lib.gc_hub_terms_rows(K)
-    bt = torch.empty(3 * kp * T, dtype=torch.bfloat16, device=DEV)
-    xt, ht, dt = (torch.from_numpy(v).to(DEV) for v in (x, hub_cols, d))
+    bt = torch.empty(terms * kp * T, dtype=dt, device=DEV)
+    sc = torch.empty(2, dtype=torch.float32, device=DEV)
+    xt, ht, dtt = (torch.from_numpy(v).to(DEV) for v in (x, hub_cols, d))
     drt = torch.from_numpy(dr).to(DEV)
-    at = torch.from_numpy(a_hub).to(DEV).to(torch.bfloat16)
+    at = torch.from_numpy(a_hub).to(DEV).to(dt)
     out = torch.full((n, K), float("nan"), device=DEV)
     st = torch.cuda.current_stream().cuda_stream
-    nat.check(lib.gc_hub_pack_bf16x3(xt.data_ptr(), K, K, ht.data_ptr(), T, dt.data_ptr(),
-                                     bt.data_ptr(), st), "pack")
-    nat.check(lib.gc_hub_gemm_bf16x3(at.data_ptr(), T, n, T, bt.data_ptr(), K, out.data_ptr(), K,
-                                     drt.data_ptr(), 0, st), "gemm")
+    nat.check(lib.gc_hub_pack(xt.data_ptr(), K, K, ht.data_ptr(), T, dtt.data_ptr(), f,
+                              bt.data_ptr(), sc.data_ptr(), st), "pack")
+    nat.check(lib.gc_hub_gemm(at.data_ptr(), T, n, T, bt.data_ptr(), K, f, sc.data_ptr(),
+                              out.data_ptr(), K, drt.data_ptr(), 0, st), "gemm")
     ref = dr.astype(np.float64)[:, None] * (a_hub.astype(np.float64) @ (
         x.astype(np.float64)[hub_cols] * d.astype(np.float64)[hub_cols][:, None]))
     assert oracle.rel_err(out.cpu().numpy(), ref) < 1e-6
+    if fmt == "bf16x3":  # exact split: every row to fp32 accuracy, not just normwise
+        big = np.abs(ref).max(axis=1) > 0
+        rel = np.abs(out.cpu().numpy() - ref).max(axis=1)[big] / np.abs(ref).max(axis=1)[big]
+        assert rel.max() < 1e-5
 
 
 @pytest.mark.parametrize("K", [3, 32, 256])
@@ -709,6 +721,7 @@ def test_host_pipelined_layer_with_stair_split(oracle, stair_pl, monkeypatch):
     spec = ("stair", 50, 10)
     a._plans[("hubsplit", spec)] = hub.StairPlan(a, 0.05, n_clusters=1, first_band=256)
     monkeypatch.setattr(hub, "HUB_SPLIT", "stair:50:10")
+    monkeypatch.setattr(hub, "STAIR_FIRST_BAND", 256)
     monkeypatch.setattr(gcn_mod, "HOST_PIPELINE_BLOCKS", 3)
     og = oracle.GcnGraph.from_adjacency(to_oracle(oracle, stair_pl))
     rng = np.random.default_rng(9)
@@ -725,3 +738,6 @@ def test_host_pipelined_layer_with_stair_split(oracle, stair_pl, monkeypatch):
         ref = oracle.gcn_layer(og, h.astype(np.float64), w.astype(np.float64), comp, order)
         assert oracle.rel_err(out.numpy(), ref) <= 1e-4
         assert oracle.rel_err(dev_out.numpy(), ref) <= 1e-4
+    blocks = list(g.__dict__.get("_unit_block_cache", {}).values()) + \
+        [b for (_, _, b) in sum(g.__dict__.get("_row_block_cache", {}).values(), [])]
+    assert any(("hubsplit", ("stair", 50, 10)) in b._plans for b in blocks)
