@@ -23,7 +23,8 @@ def test_header_declares_the_boundary():
     syms = _native.header_symbols()
     for s in ("gc_spmm_f32", "gc_sddmm_f32", "gc_sddmm_norm_f32", "gc_gemm_f32",
               "gc_edge_softmax_f32", "gc_attn_sddmm_f32", "gc_node_proj_f32",
-              "gc_partition_rows", "gc_spmm_plan_count", "gc_spmm_plan_fill"):
+              "gc_partition_rows", "gc_spmm_plan_count", "gc_spmm_plan_fill", "gc_hub_pack",
+              "gc_hub_gemm", "gc_hub_stair_gemm"):
         assert s in syms
 
 
@@ -64,6 +65,18 @@ def test_error_codes_without_launch(lib):
     assert b"negative" in lib.gc_last_error()
     rc = lib.gc_gemm_f32(None, 4, None, 4, 4, 4, 4, None, 4, None, 0, None, 0, None)
     assert rc == _native.GC_ERR_VALUE
+    # dense-split entry points: unknown term format, bad shapes, bad staircase
+    rc = lib.gc_hub_pack(None, 8, 8, None, 64, None, 7, None, None, None)
+    assert rc == _native.GC_ERR_VALUE and b"format" in lib.gc_last_error()
+    rc = lib.gc_hub_pack(None, 8, 8, None, 64, None, _native.GC_HUB_F16X2, None, None, None)
+    assert rc == _native.GC_ERR_VALUE  # null operands (f16x2 also needs the scale workspace)
+    rc = lib.gc_hub_gemm(None, 63, 10, 64, None, 8, _native.GC_HUB_BF16X3, None, None, 8, None,
+                         0, None)
+    assert rc == _native.GC_ERR_SHAPE  # lda < T
+    rc = lib.gc_hub_stair_gemm(None, None, None, None, 0, None, None, None, 0, None, None, 0, None,
+                               64, 32, 0, None, None, 32, None, 0, None)
+    assert rc == _native.GC_ERR_VALUE  # no steps
+    assert lib.gc_hub_terms_rows(256) % 128 == 0 and lib.gc_hub_terms_rows(0) == 0
 
 
 def _plan(lib, rp, chunk, flags=0):
