@@ -513,7 +513,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   // K-major [3*BH rows] operand, so ONE MMA with N = 3*BN covers all terms
   // (A is read once per k-step instead of three times) and the epilogue adds
   // the three term column groups.  Accumulator columns per tile:
-  constexpr bool TSTACK = TERMS * BN <= 256;
+  // (verified for the 3-term bf16 stack, N = 96 / 192; the 2-term fp16 stack
+  // at N = 64 / 256 lost the second term on B200 and stays one MMA per term)
+  constexpr bool TSTACK = TERMS == 3 && BN <= 64;
   constexpr int ACC_N = TSTACK ? 3 * BN : BN;
   constexpr uint32_t TMEM_COLS = 2 * ACC_N <= 32 ? 32 : 2 * ACC_N <= 64 ? 64 : 2 * ACC_N <= 128 ? 128
                                  : 2 * ACC_N <= 256 ? 256 : 512;

