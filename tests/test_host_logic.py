@@ -340,3 +340,18 @@ def test_stair_plan_partitions_the_pattern():
     assert torch.equal(cover + plan.tail.to_dense(), dense)
     assert plan.hub_edges + plan.tail.nnz == a.nnz
     assert plan.hub_edges == int(sum(b.float().sum() for b in plan.blocks))
+
+
+def test_host_pipeline_spans_cover_rows_in_order():
+    """The e2e row-block schedule (gcn._pipeline_spans): contiguous blocks
+    covering every row once, processed from the last rows to the first, never
+    slower than one block under the pipeline model."""
+    from paper_2306_15155_b200 import gcn
+
+    a = graphs.synthetic_graph("rmat", 20000, 2_000_000, seed=1, device="cpu")
+    rp = a.row_ptr.numpy().astype(np.float64)
+    spans = gcn._pipeline_spans(rp)
+    assert spans[0][1] == a.n_rows and spans[-1][0] == 0
+    for (lo, hi), (lo2, hi2) in zip(spans, spans[1:]):
+        assert hi2 == lo and lo2 < hi2
+    assert gcn._simulate_pipeline(rp, spans) <= gcn._simulate_pipeline(rp, [(0, a.n_rows)])
