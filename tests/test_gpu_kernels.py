@@ -737,3 +737,23 @@ def test_host_pipelined_layer_with_stair_split(oracle, stair_pl, monkeypatch):
     blocks = list(g.__dict__.get("_unit_block_cache", {}).values()) + \
         [b for (_, _, b) in sum(g.__dict__.get("_row_block_cache", {}).values(), [])]
     assert any(("hubsplit", ("stair", 50, 10)) in b._plans for b in blocks)
+
+
+def test_stair_split_on_rectangular_block(oracle, stair_pl):
+    """A row block of Ã (local rows x all columns, as a rank's remote pass or an
+    e2e row block sees it) through the staircase with separate d_row / d_col."""
+    from paper_2306_15155_b200 import hub
+    g = gc.NormalizedGraph.from_adjacency(stair_pl).with_precomputed()
+    d = g.d_inv_sqrt.to(DEV)
+    lo, hi = 0, 3000  # the high-degree half of the RMAT rows
+    blk = g.a_tilde.take_rows(lo, hi)
+    blk._unit = True
+    spec = ("stair", 40, 10)
+    blk._plans[("hubsplit", spec)] = hub.StairPlan(blk, 0.04, n_clusters=4, first_band=256)
+    plan = hub.hub_plan(blk, spec)
+    assert len(plan.steps) >= 2
+    rng = np.random.default_rng(2)
+    x = torch.from_numpy(f32(rng.uniform(-0.5, 0.5, (blk.n_cols, 128)))).to(DEV)
+    out = hub.hybrid_aggregate(blk, x, d, spec, d_row=d[lo:hi], relu=True)
+    ref = gc.spmm_unweighted(blk, x, d_row=d[lo:hi], d_col=d, relu=True)
+    assert oracle.rel_err(out.cpu().numpy(), ref.cpu().numpy().astype(np.float64)) < SP_TOL
