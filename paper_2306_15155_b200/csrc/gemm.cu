@@ -486,6 +486,7 @@ struct StairArgs {
   const int4 *items;
   const int32_t *cluster_start;
   float *ws;  // [slot][256 rank rows][BN] partial products (rows pre-scaled)
+  int dbg;    // experiments only (GNNC_HUB_DBG): 1 = A once per step, 2 = B once, 4 = no MMA
 };
 
 __device__ __forceinline__ int stair_kblocks(const StairArgs &sa, int m0) {
@@ -553,7 +554,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                    : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
     for (int s = 0; s < stages; ++s) {
-      mbar_init(full_bar(s), 2);   // leader expect_tx + peer arrive (leader's copy is used)
+      // leader's arrive.expect_tx (both CTAs' bytes) is the only arrival: the
+      // peer's TMA bytes complete_tx on the leader's barrier, and the peer
+      // cannot refill slot s before the MMA that freed it has consumed this
+      // phase, so its bytes never land in the wrong phase
+      mbar_init(full_bar(s), 1);
       mbar_init(empty_bar(s), 1);  // multicast MMA commit
     }
     for (int b = 0; b < 2; ++b) {
@@ -596,13 +601,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             mbar_wait(empty_bar(s), ph);
             const uint32_t sa = base + (uint32_t)s * STAGE_BYTES;
             const uint32_t lbar = mapa_shared(full_bar(s), 0);
-            if (leader) mbar_expect_tx(full_bar(s), 2 * STAGE_BYTES);
-            else mbar_arrive_cluster(lbar);
-            tma_load_2d_pair(sa, &maps.a[st], lbar, kb * 64, m0);  // rows >= rows[st]: zero fill
+            const bool la = !(sarg.dbg & 1) || kb == 0, lb = !(sarg.dbg & 2) || kb == 0;
+            if (leader)
+              mbar_expect_tx(full_bar(s), 2 * ((la ? A_BYTES : 0) + (lb ? TERMS * B_BYTES : 0)));
+            if (la) tma_load_2d_pair(sa, &maps.a[st], lbar, kb * 64, m0);  // rows >= rows[st]: zero fill
 #pragma unroll
             for (int q = 0; q < TERMS; ++q)
-              tma_load_2d_pair(sa + A_BYTES + q * B_BYTES, &map_b, lbar, sarg.c0[st] + kb * 64,
-                               q * b_rows_per_term + n0);
+              if (lb)
+                tma_load_2d_pair(sa + A_BYTES + q * B_BYTES, &map_b, lbar, sarg.c0[st] + kb * 64,
+                                 q * b_rows_per_term + n0);
           }
         }
       }
@@ -627,6 +634,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           const uint32_t sa = base + (uint32_t)s * STAGE_BYTES;
 #pragma unroll
           for (int k = 0; k < KB_BYTES / MMA_K_BYTES; ++k) {
+            if (sarg.dbg & 4) break;
             const uint64_t ad = umma_desc_sw128(sa + k * MMA_K_BYTES);
             if constexpr (TSTACK) {
               const uint64_t bd = umma_desc_sw128(sa + A_BYTES + k * MMA_K_BYTES);
@@ -1456,6 +1464,11 @@ extern "C" int gc_hub_stair_gemm(const void *const *A_steps, const int64_t *step
   sarg.items = reinterpret_cast<const int4 *>(items);
   sarg.cluster_start = cluster_start;
   sarg.ws = workspace;
+  static const int dbg = [] {
+    const char *e = getenv("GNNC_HUB_DBG");
+    return e ? atoi(e) : 0;
+  }();
+  sarg.dbg = dbg;
   for (int s = 0; s < n_steps; ++s) {
     const int64_t r = step_rows[s], c0 = step_c0[s], w = step_width[s];
     GC_REQUIRE(r >= 1 && r < INT32_MAX && w > 0 && w % 64 == 0 && c0 % 64 == 0 && c0 + w <= T,

@@ -663,7 +663,10 @@ def test_host_pipelined_layer_with_hub_split(oracle, hub_pl, comp, order, monkey
         out = gc.gcn_layer(g, torch.from_numpy(h).pin_memory(), spec)
     finally:
         gc.set_gemm_precision("tf32")
-    assert not out.is_cuda and ("hubsplit", 64) in g.a_tilde._plans
+    assert not out.is_cuda
+    blocks = list(g.__dict__.get("_unit_block_cache", {}).values()) + \
+        [b for (_, _, b) in sum(g.__dict__.get("_row_block_cache", {}).values(), [])]
+    assert any(("hubsplit", 64) in b._plans for b in blocks)  # each row block splits
     ref = oracle.gcn_layer(og, h.astype(np.float64), w.astype(np.float64), comp, order)
     assert oracle.rel_err(out.numpy(), ref) <= 1e-4
 
