@@ -393,7 +393,7 @@ def main():
                 "share_of_step": round(tail_ms / ms, 3), "peak_source": pk["source"],
                 "model": "edge-gather over the tail edges: 4(n+1)+4m_t[+4m_t values][+4m_t d_j]+4m_tK+4nK(+4nK C read)[+4n]",
                 "tail_edges": mt}
-        flops = 2 * plan.cells * K * 3
+        flops = 2 * plan.cells * K * (2 if hubmod.HUB_FORMAT == "f16x2" else 3)
         tf = flops / (hub_ms * 1e-3) / 1e12
         hub_roof = {"kernel": "gemm_hub_pair_tcgen05 (dense part)", "bound": "tensor", "achieved": round(tf, 1),
                     "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": round(tf / pk["bf16_tflops"], 3),
@@ -401,7 +401,8 @@ def main():
                     "split": hubmod.spec_label(split), "dense_cells": plan.cells,
                     "dense_edges": plan.hub_edges, "flops_per_launch": flops,
                     "steps": getattr(plan, "steps", None),
-                    "model": "2·cells·K per bf16 term, 3 terms (exact fp32 split)"}
+                    "terms": hubmod.HUB_FORMAT,
+                    "model": "2·cells·K per 16-bit term (f16x2: 2 terms, 22-bit split of D·X; bf16x3: 3 terms, exact)"}
     elif spmm_ms:
         spmm_bytes = spmm_alg_bytes(a_used.n_rows, a_used.nnz, K, weighted, dyn, dyn)
         ach = spmm_bytes / (spmm_ms * 1e-3) / 1e9
@@ -435,6 +436,7 @@ def main():
         "roofline": roof,
         "roofline_hub_gemm": hub_roof,
         "dense_split": {"chosen": __import__("paper_2306_15155_b200.hub", fromlist=["spec_label"]).spec_label(split),
+                        "terms": __import__("paper_2306_15155_b200.hub", fromlist=["HUB_FORMAT"]).HUB_FORMAT,
                         "autotune_ms": g.a_tilde._plans.get(("hubsplit-choice", K, not dyn, "times"))},
         "setup": {"graph_gen_s": round(gen_s, 2), "prep_s": round(prep_s, 3),
                   "normalize_sddmm_ms": round(norm_ms, 3)},

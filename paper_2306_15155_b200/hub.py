@@ -16,9 +16,9 @@ shared memory:
 
 computed by tcgen05 kind::f16 GEMMs: the 0/1 blocks are exact in fp16/bf16
 and (D X)[columns] is split into 16-bit terms (``gc_hub_pack``): by default
-three bf16 terms that carry its exact fp32 mantissa, or (GNNC_HUB_FORMAT=
-f16x2) two fp16 terms of s·D·X with a power-of-two scale s (22 significant
-bits: absolute error <= 2^-23·max|D X| per element), 2/3 of the MMAs.  The SpMM then accumulates the remaining edges on top
+two fp16 terms of s·D·X with a power-of-two scale s (22 significant bits:
+absolute error <= 2^-23·max|D X| per element, 2/3 of the MMAs), or
+(GNNC_HUB_FORMAT=bf16x3) three bf16 terms that carry its exact fp32 mantissa.  The SpMM then accumulates the remaining edges on top
 (GC_ACCUMULATE); apart from the term split only the summation order differs
 from the plain SpMM.
 
@@ -52,11 +52,12 @@ from . import _native as nat
 from .sparse import CsrMatrix, ShapeError, _ld, _require_cuda, _spmm, _stream, _timed_call
 
 HUB_SPLIT = os.environ.get("GNNC_HUB_SPLIT", "auto")
-# term format of the dense operand: "bf16x3" (default: exact fp32 split) or
-# "f16x2" (two fp16 terms of s·D·X, 22 significant bits, 2/3 of the MMAs —
-# measured no faster on the staircase, which is not MMA-bound: Reddit K=256
-# 0.88 vs 0.89 ms)
-HUB_FORMAT = os.environ.get("GNNC_HUB_FORMAT", "bf16x3")
+# term format of the dense operand: "f16x2" (default: two fp16 terms of s·D·X
+# with a power-of-two s — 22 significant bits, absolute error <= 2^-23
+# max|D·X| per element, 2/3 of the MMAs; Reddit K=256 staircase 0.58 vs 0.80
+# ms, normwise difference from the plain SpMM 2.8e-6 either way) or "bf16x3"
+# (exact fp32 split)
+HUB_FORMAT = os.environ.get("GNNC_HUB_FORMAT", "f16x2")
 
 
 def _fmt() -> int:
