@@ -71,7 +71,7 @@ HUB_T_CANDIDATES = (1024, 2048, 4096, 8192)
 # (slack > 1 reaches further right, but short-wide steps stream their B
 # operand from DRAM once per pair tile and lose to the tail: measured 2.73 ms
 # at (0.012, 1.0) vs 2.99 ms at (0.018, 3.0) on Reddit K=256)
-STAIR_CANDIDATES = ((0.012, 1.0), (0.018, 1.0), (0.018, 1.5))
+STAIR_CANDIDATES = ((0.008, 1.0), (0.012, 1.0), (0.018, 1.0))
 # narrower feature rows make a dense cell relatively dearer (the tensor tile
 # is N = K wide: A-operand bound), so small K tries sparser staircases
 STAIR_CANDIDATES_SMALL_K = {128: ((0.018, 1.0), (0.03, 1.0), (0.06, 1.0)),
