@@ -1157,23 +1157,25 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// |(D X)[hub_cols]| maximum (as float bits; non-negative floats order like ints)
+// |(D X)[hub_cols]| maximum (as float bits; non-negative floats order like
+// ints): a warp per gathered row, lanes across its K floats.
 __global__ void __launch_bounds__(256)
     hub_absmax_kernel(const float *__restrict__ X, int64_t ldx, int64_t K,
                       const int32_t *__restrict__ hub_cols, int64_t T,
                       const float *__restrict__ d, unsigned *__restrict__ out) {
+  const int lane = threadIdx.x % 32;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int64_t n_warps = (int64_t)gridDim.x * blockDim.x / 32;
   float m = 0.0f;
-  const int64_t total = T * K;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = i / K, f = i % K;
+  for (int64_t t = warp; t < T; t += n_warps) {
     const int64_t j = __ldg(hub_cols + t);
-    float x = __ldg(X + j * ldx + f);
-    if (d) x *= __ldg(d + j);
-    m = fmaxf(m, fabsf(x));
+    const float *row = X + j * ldx;
+    float mr = 0.0f;
+    for (int64_t f = lane; f < K; f += 32) mr = fmaxf(mr, fabsf(__ldg(row + f)));
+    m = fmaxf(m, d ? mr * fabsf(__ldg(d + j)) : mr);
   }
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+  if (lane == 0) atomicMax(out, __float_as_uint(m));
 }
 
 // Two fp16 terms of s·x, s = 2^(13 - floor(log2 max|x|)) so max|s·x| < 2^14:
@@ -1349,8 +1351,7 @@ extern "C" int gc_hub_pack(const float *X, int64_t ldx, int64_t K, const int32_t
     set_error("gc_hub_pack: %s", cudaGetErrorString(cudaGetLastError()));
     return GC_ERR_CUDA;
   }
-  const int64_t work = T * K;
-  const int64_t blocks = std::min<int64_t>((work + 255) / 256, (int64_t)sm_count() * 8);
+  const int64_t blocks = std::min<int64_t>((T + 7) / 8, (int64_t)sm_count() * 8);
   hub_absmax_kernel<<<(unsigned)blocks, 256, 0, st>>>(X, ldx, K, hub_cols, T, d_col, amax);
   int rc = check_launch("hub_absmax_kernel");
   if (rc) return rc;
