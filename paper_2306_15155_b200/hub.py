@@ -89,6 +89,7 @@ HUB_MIN_DENSITY = 0.02           # mean density of a block worth a dense product
 HUB_MEM_BUDGET = 8 << 30         # bytes of dense blocks per pattern
 STAIR_MAX_STEPS = 16
 STAIR_FIRST_BAND = 1024          # rows / columns of the first histogram band
+STAIR_BAND_RATIO = 2 ** 0.5      # growth of the histogram bands
 STAIR_CLUSTERS = 74              # CTA pairs of a B200 (balance bound of the top tile)
 
 
@@ -258,13 +259,14 @@ class StairPlan(_TailMixin):
 
     @staticmethod
     def _bands(n: int, first: int, align: int) -> list[int]:
-        """0, first, then ratio-sqrt(2) boundaries (multiples of ``align``), n."""
+        """0, first, then geometric boundaries (STAIR_BAND_RATIO, multiples of
+        ``align``), n."""
         b, x = [0], float(first)
         while int(x) // align * align < n:
             v = int(x) // align * align
             if v > b[-1]:
                 b.append(v)
-            x *= 2 ** 0.5
+            x *= STAIR_BAND_RATIO
         if b[-1] != n:
             b.append(n)
         return b
