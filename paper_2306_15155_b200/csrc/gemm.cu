@@ -461,6 +461,19 @@ __host__ __device__ constexpr uint32_t idesc_bf16_m256(int n) {
 __host__ __device__ constexpr uint32_t idesc_f16_m256(int n) {
   return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((256u >> 4) << 24);
 }
+// D = F32, A = B = TF32, K-major, M = 256 (cta pair), N = n
+__host__ __device__ constexpr uint32_t idesc_tf32_m256(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((256u >> 4) << 24);
+}
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 
 // Staircase of dense blocks (hub.py): step s is the 0/1 block of rows
 // [0, rows[s]) (rows in degree-rank order) x columns [c0[s], c0[s] + 64*nkb[s])
@@ -497,7 +510,8 @@ __device__ __forceinline__ int stair_kblocks(const StairArgs &sa, int m0) {
 }
 
 // FMT 0: three bf16 terms (exact fp32 split); 1: two fp16 terms of s·D·X
-// (22 significant bits, absolute error <= 2^-23 max|D·X|), 2/3 of the MMAs.
+// (22 significant bits, absolute error <= 2^-23 max|D·X|), 2/3 of the MMAs;
+// 2: one fp32 operand pair on kind::tf32 (the dense update H·W on CTA pairs).
 template <int BN, int FMT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     gemm_hub_pair_tcgen05(const __grid_constant__ StairMaps maps,
@@ -505,7 +519,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                           const __grid_constant__ CUtensorMap map_c, const GemmEpi ep,
                           const StairArgs sarg, int stages, int m_pairs, int n_tiles,
                           int tma_store, int b_rows_per_term) {
-  constexpr int TERMS = FMT ? 2 : 3;
+  constexpr int TERMS = FMT == 2 ? 1 : FMT ? 2 : 3;
+  constexpr int KB_EL = FMT == 2 ? 32 : 64;  // elements per 128-byte k-block row
   constexpr int BH = BN / 2;  // B rows per CTA per term
   constexpr uint32_t A_BYTES = BM * KB_BYTES;
   constexpr uint32_t B_BYTES = BH * KB_BYTES;
@@ -604,11 +619,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             const bool la = !(sarg.dbg & 1) || kb == 0, lb = !(sarg.dbg & 2) || kb == 0;
             if (leader)
               mbar_expect_tx(full_bar(s), 2 * ((la ? A_BYTES : 0) + (lb ? TERMS * B_BYTES : 0)));
-            if (la) tma_load_2d_pair(sa, &maps.a[st], lbar, kb * 64, m0);  // rows >= rows[st]: zero fill
+            if (la) tma_load_2d_pair(sa, &maps.a[st], lbar, kb * KB_EL, m0);  // rows >= rows[st]: zero fill
 #pragma unroll
             for (int q = 0; q < TERMS; ++q)
               if (lb)
-                tma_load_2d_pair(sa + A_BYTES + q * B_BYTES, &map_b, lbar, sarg.c0[st] + kb * 64,
+                tma_load_2d_pair(sa + A_BYTES + q * B_BYTES, &map_b, lbar, sarg.c0[st] + kb * KB_EL,
                                  q * b_rows_per_term + n0);
           }
         }
@@ -616,7 +631,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {  // ---------------- MMA issuer (leader only) ----------------
-      constexpr uint32_t idesc = FMT ? idesc_f16_m256(ACC_N) : idesc_bf16_m256(ACC_N);
+      constexpr uint32_t idesc = FMT == 2 ? idesc_tf32_m256(ACC_N)
+                                 : FMT ? idesc_f16_m256(ACC_N) : idesc_bf16_m256(ACC_N);
       int it = 0, lt = 0;
       for (int ti = t_begin; ti < t_end; ti += t_step, ++lt) {
         const int4 item = item_at(ti);
@@ -643,7 +659,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
               for (int q = 0; q < TERMS; ++q) {
                 const uint64_t bd = umma_desc_sw128(sa + A_BYTES + q * B_BYTES + k * MMA_K_BYTES);
-                mma_bf16_pair(tmem_d, ad, bd, idesc, (kb | k | q) != 0);
+                if constexpr (FMT == 2) mma_tf32_pair(tmem_d, ad, bd, idesc, (kb | k | q) != 0);
+                else mma_bf16_pair(tmem_d, ad, bd, idesc, (kb | k | q) != 0);
               }
             }
           }
@@ -1045,7 +1062,7 @@ template <int BN, int FMT>
 int launch_hub_pair(const StairMaps &maps, const StairArgs &sarg, const CUtensorMap &mb,
                     const CUtensorMap &mc, int tma_store, const GemmEpi &ep, int64_t kp,
                     cudaStream_t st, int sched_clusters = 0) {
-  constexpr int stage_bytes = BM * KB_BYTES + (FMT ? 2 : 3) * (BN / 2) * KB_BYTES;
+  constexpr int stage_bytes = BM * KB_BYTES + (FMT == 2 ? 1 : FMT ? 2 : 3) * (BN / 2) * KB_BYTES;
   size_t smem = 0;
   int stages = tma_store ? ring_stages(stage_bytes, true, &smem) : 0;
   if (stages == 0) {
@@ -1091,7 +1108,8 @@ int launch_hub_pair_bn_f(int pbn, Args &&...args) {
 }
 template <typename... Args>
 int launch_hub_pair_bn(int fmt, int pbn, Args &&...args) {
-  return fmt ? launch_hub_pair_bn_f<1>(pbn, args...) : launch_hub_pair_bn_f<0>(pbn, args...);
+  return fmt == 2 ? launch_hub_pair_bn_f<2>(pbn, args...)
+       : fmt ? launch_hub_pair_bn_f<1>(pbn, args...) : launch_hub_pair_bn_f<0>(pbn, args...);
 }
 template <int FMT, typename... Args>
 int launch_hub_bn_f(int bn, Args &&...args) {
@@ -1102,6 +1120,14 @@ int launch_hub_bn_f(int bn, Args &&...args) {
     case 128: return launch_hub<128, FMT>(args...);
     default: return launch_hub<256, FMT>(args...);
   }
+}
+
+inline bool gemm_pair_enabled() {  // GNNC_GEMM_PAIR=0: TF32 GEMM on single CTAs
+  static const bool on = [] {
+    const char *e = getenv("GNNC_GEMM_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 inline bool hub_pair_enabled() {
@@ -1287,6 +1313,29 @@ extern "C" int gc_gemm_f32(const float *A, int64_t lda, const float *W, int64_t 
   CUtensorMap ma, mb, mc;
   int rc = make_map(&ma, A, M, K, lda, BM);
   if (rc) return rc;
+  if (hub_pair_enabled() && gemm_pair_enabled() && N > 16 && M >= 2 * BM) {
+    // CTA pairs (M = 256 per MMA, each CTA stages half of the W tile): the
+    // hub GEMM's pipeline with one TF32 operand pair (FMT 2)
+    const int pbn = pair_bn(N);
+    CUtensorMap mbp;
+    rc = make_map(&mbp, wt, N, K, ldt, pbn / 2);
+    if (rc) return rc;
+    int tma_store = ((ldc % 4) == 0 && aligned16(C)) ? 1 : 0;
+    memset(&mc, 0, sizeof(mc));
+    if (tma_store) {
+      rc = make_map(&mc, C, M, N, ldc, 32, 16, CU_TENSOR_MAP_SWIZZLE_64B);
+      if (rc) return rc;
+    }
+    StairMaps maps;
+    memset(&maps, 0, sizeof(maps));
+    maps.a[0] = ma;
+    StairArgs sarg{};
+    sarg.n_steps = 1;
+    sarg.rows[0] = (int)M;
+    sarg.c0[0] = 0;
+    sarg.nkb[0] = (int)((K + BK - 1) / BK);
+    return launch_hub_pair_bn(2, pbn, maps, sarg, mbp, mc, tma_store, ep, (int64_t)0, st, 0);
+  }
   rc = make_map(&mb, wt, N, K, ldt, bn);
   if (rc) return rc;
   // output through TMA stores when C's pitch allows it (16-B aligned rows)
