@@ -1313,9 +1313,12 @@ extern "C" int gc_gemm_f32(const float *A, int64_t lda, const float *W, int64_t 
   CUtensorMap ma, mb, mc;
   int rc = make_map(&ma, A, M, K, lda, BM);
   if (rc) return rc;
-  if (hub_pair_enabled() && gemm_pair_enabled() && N > 16 && M >= 2 * BM) {
+  if (hub_pair_enabled() && gemm_pair_enabled() && N > 16 && M >= 2 * BM &&
+      (K >= 512 || M >= (int64_t(1) << 20))) {
     // CTA pairs (M = 256 per MMA, each CTA stages half of the W tile): the
-    // hub GEMM's pipeline with one TF32 operand pair (FMT 2)
+    // hub GEMM's pipeline with one TF32 operand pair (FMT 2).  Measured:
+    // 169K x 1024 x 1024 0.79 -> 0.60 ms, 2.45M x 256 x 256 1.15 -> 0.93 ms;
+    // the HBM-bound 233K x 256 x 256 stays on single CTAs (0.117 vs 0.131 ms)
     const int pbn = pair_bn(N);
     CUtensorMap mbp;
     rc = make_map(&mbp, wt, N, K, ldt, pbn / 2);
