@@ -648,8 +648,23 @@ def extra_configs(gc, args, dev, pk) -> dict:
     from paper_2306_15155_b200 import graphs, selector
 
     res = {"cora": cora_config(gc, args, dev)}
+    models = {t: selector.load_b200_model(t) for t in ("gcn", "gat")}
+
+    def pick(row_comps: dict, model: str, feats, K: int) -> dict:
+        """The B200 selector's choice for this group and its time over the
+        fastest composition measured (north-star target: <= 1.1)."""
+        if models[model] is None:
+            return {}
+        sel = selector.select(models[model], selector.SelectorInput(features=feats, k1=K, k2=K))
+        best = min(row_comps, key=lambda c: row_comps[c]["ms"])
+        out = {"fastest": best, "selected": sel}
+        if sel in row_comps:
+            out["selected_over_fastest"] = round(row_comps[sel]["ms"] / row_comps[best]["ms"], 3)
+        return out
+
     # ---- GAT on ogbn-arxiv-shaped RMAT ---------------------------------------
     A = graphs.shape_graph("arxiv", seed=args.seed, device=dev)
+    feats = gc.extract_features(A)  # raw graph, as the reference's cli.py:187
     at = gc.add_self_loops(A)
     del A
     n, m = at.n_rows, at.nnz
@@ -669,8 +684,7 @@ def extra_configs(gc, args, dev, pk) -> dict:
                                        attention=form)
                 t = _time_layer(lambda: gc.gat_layer(at, h, spec), args.sweep_reps)
                 row["compositions"][comp] = {"ms": round(t * 1e3, 4), "edges_per_s": round(m / t, 1)}
-            best = min(row["compositions"], key=lambda c: row["compositions"][c]["ms"])
-            row["fastest"] = best
+            row.update(pick(row["compositions"], "gat", feats, K))
             gat.append(row)
             del h, w
     res["gat_arxiv"] = {"n": n, "m_tilde": m, "rows": gat}
@@ -678,6 +692,7 @@ def extra_configs(gc, args, dev, pk) -> dict:
     torch.cuda.empty_cache()
     # ---- products-shaped: GCN (4 compositions) + GAT -------------------------
     A = graphs.shape_graph("products", seed=args.seed, device=dev)
+    feats = gc.extract_features(A)
     g = gc.NormalizedGraph.from_adjacency(A).with_precomputed()
     del A
     n, m = g.a_tilde.n_rows, g.a_tilde.nnz
@@ -702,11 +717,13 @@ def extra_configs(gc, args, dev, pk) -> dict:
                                 "spmm_hbm_frac": round(b / (sp * 1e-3) / 1e9 / pk["hbm_gbs"], 3)}
         a_s = torch.rand(K, device=dev, generator=gen) - 0.5
         a_d = torch.rand(K, device=dev, generator=gen) - 0.5
-        for comp in ("reuse:reassoc", "recompute:reassoc"):
+        for comp in selector.B200_COMPOSITIONS["gat"]:
             base, form = comp.split(":")
             spec = gc.GatLayerSpec(K, K, w, a_s, a_d, composition=base, attention=form)
             t = _time_layer(lambda: gc.gat_layer(g.a_tilde, h, spec), 3)
             row["gat"][comp] = {"ms": round(t * 1e3, 4), "edges_per_s": round(m / t, 1)}
+        row["gcn_selection"] = pick(row["gcn"], "gcn", feats, K)
+        row["gat_selection"] = pick(row["gat"], "gat", feats, K)
         rows.append(row)
         del h, w
     res["products"] = {"n": n, "m_tilde": m, "rows": rows}

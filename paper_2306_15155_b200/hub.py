@@ -89,6 +89,7 @@ HUB_MIN_DENSITY = 0.02           # mean density of a block worth a dense product
 HUB_MEM_BUDGET = 8 << 30         # bytes of dense blocks per pattern
 STAIR_MAX_STEPS = 16
 STAIR_FIRST_BAND = 1024          # rows / columns of the first histogram band
+AUTOTUNE_ROUNDS = 5              # interleaved timing rounds per candidate
 STAIR_BAND_RATIO = 2 ** 0.5      # growth of the histogram bands
 STAIR_CLUSTERS = 74              # CTA pairs of a B200 (balance bound of the top tile)
 
@@ -359,7 +360,8 @@ def pack(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec):
     bt = torch.empty(terms * kp * plan.T, dtype=_block_dtype(plan.fmt), device=x.device)
     sc = torch.empty(2, dtype=torch.float32, device=x.device)
     nat.check(lib.gc_hub_pack(x.data_ptr(), _ld(x), K, plan.hub_cols.data_ptr(), plan.T,
-                              d.data_ptr(), plan.fmt, bt.data_ptr(), sc.data_ptr(),
+                              None if d is None else d.data_ptr(), plan.fmt, bt.data_ptr(),
+                              sc.data_ptr(),
                               _stream(x.device)), "hub_pack")
     return bt, sc
 
@@ -416,18 +418,20 @@ def hybrid_aggregate(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, *,
                      accumulate: bool = False, rows: tuple[int, int] | None = None,
                      packed: torch.Tensor | None = None) -> torch.Tensor:
     """C = epi(D_row Ã D X) for a unit-valued pattern ``a`` via the dense/tail
-    split ``spec`` (``d`` scales the columns; ``d_row`` the rows, default
-    ``d`` itself for a square pattern).  ``values`` (optional) are a
+    split ``spec`` (``d`` scales the columns — None when x already carries
+    the column scaling; ``d_row`` the rows, default ``d`` itself for a square
+    pattern).  ``values`` (optional) are a
     same-pattern matrix's values used for the tail instead of d_i·d_j (the
     precompute composition streams Ñ's values).  ``accumulate``: C += ...
     (ReLU on the total).  ``rows=(lo, hi)`` (block plans only) computes that
     row block (``out`` then has hi-lo rows); ``packed`` reuses one ``pack``."""
-    dev = _require_cuda(a.col_idx, x, d)
+    dev = _require_cuda(a.col_idx, x)
     if x.dim() != 2 or x.shape[0] != a.n_cols or x.stride(1) != 1:
         raise ShapeError("hybrid_aggregate: x must be a row-major n_cols x K tensor")
     if d_row is None:
-        if a.n_rows != a.n_cols:
-            raise ShapeError("hybrid_aggregate: d_row is required for a rectangular pattern")
+        if a.n_rows != a.n_cols or d is None:
+            raise ShapeError("hybrid_aggregate: d_row is required for a rectangular pattern "
+                             "or an already column-scaled x (d=None)")
         d_row = d
     K = x.shape[1]
     lo, hi = rows if rows is not None else (0, a.n_rows)
@@ -485,7 +489,7 @@ def choose_split(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, *,
     if mode == "0" or not a.has_unit_values:
         return 0
     if d_row is None:
-        if a.n_rows != a.n_cols:
+        if a.n_rows != a.n_cols or d is None:
             return 0
         d_row = d
     if mode != "auto":
@@ -513,21 +517,28 @@ def choose_split(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, *,
         _spmm(src, x, weighted=values is not None, d_row=None if values is not None else d_row,
               d_col=None if values is not None else d, out=scratch, timer=None)
 
-    def timed(fn) -> float:
+    # every candidate once to warm up (plans, autotuned tail variants), then
+    # AUTOTUNE_ROUNDS interleaved rounds (drift in clocks / power cap hits
+    # all candidates alike); the median per candidate decides
+    runs = {0: plain}
+    for spec in cands:
+        runs[spec] = (lambda spec=spec: hybrid_aggregate(a, x, d, spec, d_row=d_row,
+                                                         values=values, out=scratch))
+    for fn in runs.values():
         fn()
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(3)]
-        for e0, e1 in ev:
+    samples: dict = {k: [] for k in runs}
+    for _ in range(AUTOTUNE_ROUNDS):
+        ev = {}
+        for k, fn in runs.items():
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             fn()
             e1.record()
+            ev[k] = (e0, e1)
         torch.cuda.synchronize()
-        return sorted(e0.elapsed_time(e1) for e0, e1 in ev)[1]
-
-    times = {0: timed(plain)}
-    for spec in cands:
-        times[spec] = timed(lambda spec=spec: hybrid_aggregate(a, x, d, spec, d_row=d_row,
-                                                               values=values, out=scratch))
+        for k, (e0, e1) in ev.items():
+            samples[k].append(e0.elapsed_time(e1))
+    times = {k: float(sorted(v)[len(v) // 2]) for k, v in samples.items()}
     best = min(times, key=times.get)
     if best != 0 and times[best] >= 0.97 * times[0]:
         best = 0
