@@ -41,12 +41,35 @@ from .sparse import CsrMatrix
 
 def partition_rows(row_ptr, parts: int) -> np.ndarray:
     """nnz-balanced contiguous row blocks: bounds[p] = first r with
-    row_ptr[r] >= ceil(p*nnz/P) (C ABI gc_partition_rows)."""
+    row_ptr[r] >= ceil(p*nnz/P) (C ABI gc_partition_rows).  A device-resident
+    row_ptr is partitioned in place (:func:`partition_rows_device`)."""
+    if isinstance(row_ptr, torch.Tensor) and row_ptr.is_cuda:
+        return partition_rows_device(row_ptr, parts)
     rp = np.ascontiguousarray(
         row_ptr.cpu().numpy() if isinstance(row_ptr, torch.Tensor) else row_ptr, dtype=np.int64)
     out = np.zeros(parts + 1, dtype=np.int64)
     nat.check(nat.load().gc_partition_rows(rp.ctypes.data, rp.size - 1, int(parts), out.ctypes.data),
               "partition_rows")
+    return out
+
+
+def partition_rows_device(row_ptr: torch.Tensor, parts: int) -> np.ndarray:
+    """:func:`partition_rows` computed where ``row_ptr`` lives: one scalar
+    read (nnz), P-1 lower-bound searches on the device, P+1 bounds back —
+    row_ptr itself never crosses to the host.  Bit-identical to the C ABI
+    (``searchsorted(left)`` is ``std::lower_bound``)."""
+    if parts < 1:
+        raise ValueError("partition_rows: parts must be >= 1")
+    n = row_ptr.numel() - 1
+    if n < 0:
+        raise ValueError("partition_rows: empty row_ptr")
+    m = int(row_ptr[-1])
+    p = torch.arange(1, parts, dtype=torch.int64)
+    target = ((p * m + parts - 1) // parts).to(row_ptr.device, row_ptr.dtype)
+    hit = torch.searchsorted(row_ptr.contiguous(), target, right=False).clamp_(max=n)
+    out = np.empty(parts + 1, dtype=np.int64)
+    out[0], out[parts] = 0, n
+    out[1:parts] = hit.cpu().numpy()
     return out
 
 

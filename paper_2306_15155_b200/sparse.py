@@ -287,6 +287,76 @@ class CsrMatrix:
             out._check()
         return out
 
+    # -- binary CSR file ----------------------------------
+    # The reference ingests graphs only through MatrixMarket text
+    # (mtxio.py), which parses at a few M entries/s; a graph the size of
+    # Reddit takes minutes.  ``.gcsr`` stores the device layout verbatim so a
+    # load is a memory map + one host->device copy per array:
+    #   bytes 0..63   header: b"GCSR" + u32 version, i64 n_rows, i64 n_cols,
+    #                 i64 nnz, u32 flags (bit 0: unit values, not stored),
+    #                 zero padding
+    #   then          row_ptr int32[n_rows+1], col_idx int32[nnz],
+    #                 values float32[nnz] (absent if unit), each section
+    #                 starting on a 64-byte boundary, little-endian.
+    GCSR_MAGIC = b"GCSR"
+    GCSR_VERSION = 1
+
+    def save(self, path) -> None:
+        """Write the matrix as a ``.gcsr`` file (layout above)."""
+        unit = self.has_unit_values
+        head = np.zeros(64, dtype=np.uint8)
+        hdr = (self.GCSR_MAGIC + np.array([self.GCSR_VERSION], "<u4").tobytes()
+               + np.array([self.n_rows, self.n_cols, self.nnz], "<i8").tobytes()
+               + np.array([1 if unit else 0], "<u4").tobytes())
+        head[:len(hdr)] = np.frombuffer(hdr, np.uint8)
+        sections = [self.row_ptr.cpu().numpy().astype("<i4", copy=False),
+                    self.col_idx.cpu().numpy().astype("<i4", copy=False)]
+        if not unit:
+            sections.append(self.values.cpu().numpy().astype("<f4", copy=False))
+        with open(path, "wb") as f:
+            f.write(head.tobytes())
+            for arr in sections:
+                f.write(arr.tobytes())
+                pad = (-arr.nbytes) % 64
+                if pad:
+                    f.write(b"\0" * pad)
+
+    @classmethod
+    def load(cls, path, device=None, validate: bool = True) -> "CsrMatrix":
+        """Read a ``.gcsr`` file written by :meth:`save` onto ``device``.
+        Truncated or foreign files raise ``ShapeError``; the CSR invariants
+        are checked on the device unless ``validate=False``."""
+        dev = torch.device(device) if device is not None else default_device()
+        raw = np.memmap(path, dtype=np.uint8, mode="r")
+        if raw.size < 64 or bytes(raw[:4]) != cls.GCSR_MAGIC:
+            raise ShapeError(f"{path}: not a .gcsr file")
+        version = int(raw[4:8].view("<u4")[0])
+        if version != cls.GCSR_VERSION:
+            raise ShapeError(f"{path}: unsupported .gcsr version {version}")
+        n_rows, n_cols, nnz = (int(x) for x in raw[8:32].view("<i8"))
+        flags = int(raw[32:36].view("<u4")[0])
+        if min(n_rows, n_cols, nnz) < 0:
+            raise ShapeError(f"{path}: negative dimension in header")
+        unit = bool(flags & 1)
+        off = 64
+
+        def section(count: int, dt: str) -> torch.Tensor:
+            nonlocal off
+            nbytes = count * 4
+            if off + nbytes > raw.size:
+                raise ShapeError(f"{path}: truncated .gcsr file")
+            host = torch.from_numpy(np.array(raw[off:off + nbytes].view(dt), copy=True))
+            off += nbytes + (-nbytes) % 64
+            return host.to(dev, non_blocking=False)
+
+        rp = section(n_rows + 1, "<i4")
+        ci = section(nnz, "<i4")
+        va = torch.ones(nnz, dtype=torch.float32, device=dev) if unit else section(nnz, "<f4")
+        out = cls(n_rows, n_cols, rp, ci, va, validate=validate, device=dev)
+        if unit:
+            out._unit = True
+        return out
+
     def to(self, device) -> "CsrMatrix":
         dev = torch.device(device)
         out = CsrMatrix(self.n_rows, self.n_cols, self.row_ptr.to(dev), self.col_idx.to(dev),

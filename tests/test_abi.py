@@ -9,6 +9,7 @@ import subprocess
 
 import numpy as np
 import pytest
+import torch
 
 from paper_2306_15155_b200 import _build, _native
 
@@ -142,3 +143,17 @@ def test_partition_edge_cases(lib, oracle):
         assert lib.gc_partition_rows(rp.ctypes.data, rp.size - 1, 4, out.ctypes.data) == 0
         assert np.array_equal(out, oracle.partition_rows(rp, 4))
     assert lib.gc_partition_rows(ctypes.c_void_p(0), 0, 2, ctypes.c_void_p(0)) == _native.GC_ERR_VALUE
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3, 4, 8])
+def test_partition_device_form_matches_abi(oracle, parts):
+    """partition_rows_device (searchsorted where row_ptr lives) gives the
+    same bounds as the C ABI / oracle; run here on a CPU tensor."""
+    from paper_2306_15155_b200.distributed import partition_rows_device
+
+    rng = np.random.default_rng(10 + parts)
+    for deg in (rng.zipf(1.7, size=3000).clip(max=5000), np.zeros(7, np.int64), np.array([10])):
+        rp = np.concatenate(([0], np.cumsum(deg))).astype(np.int64)
+        want = oracle.partition_rows(rp, parts)
+        got = partition_rows_device(torch.from_numpy(rp.astype(np.int32)), parts)
+        assert np.array_equal(got, want)

@@ -760,3 +760,18 @@ def test_stair_split_on_rectangular_block(oracle, stair_pl):
     out = hub.hybrid_aggregate(blk, x, d, spec, d_row=d[lo:hi], relu=True)
     ref = gc.spmm_unweighted(blk, x, d_row=d[lo:hi], d_col=d, relu=True)
     assert oracle.rel_err(out.cpu().numpy(), ref.cpu().numpy().astype(np.float64)) < SP_TOL
+
+
+def test_gcsr_load_to_device_and_partition(tmp_path, oracle):
+    """.gcsr file -> device CSR (same arrays), then the on-device partition
+    equals the C-ABI/oracle bounds."""
+    from paper_2306_15155_b200.distributed import partition_rows_device
+
+    a = graphs.synthetic_graph("rmat", 20000, 400000, seed=3, device=DEV)
+    p = tmp_path / "g.gcsr"
+    a.save(p)
+    b = gc.CsrMatrix.load(p, device=DEV)
+    assert b.device.type == "cuda" and b.same_pattern(a) and b.has_unit_values
+    rp = a.row_ptr.cpu().numpy().astype(np.int64)
+    for parts in (2, 3, 8):
+        assert np.array_equal(partition_rows_device(b.row_ptr, parts), oracle.partition_rows(rp, parts))

@@ -355,3 +355,60 @@ def test_host_pipeline_spans_cover_rows_in_order():
     for (lo, hi), (lo2, hi2) in zip(spans, spans[1:]):
         assert hi2 == lo and lo2 < hi2
     assert gcn._simulate_pipeline(rp, spans) <= gcn._simulate_pipeline(rp, [(0, a.n_rows)])
+
+
+# ---- .gcsr binary CSR files -----------------------------
+
+
+@pytest.mark.parametrize("name", ["weighted40", "powerlaw200", "diag30"])
+def test_gcsr_round_trip(golden, tmp_path, name):
+    a = gcsr(golden, f"{name}/A")
+    p = tmp_path / f"{name}.gcsr"
+    a.save(p)
+    b = gc.CsrMatrix.load(p, device=CPU)
+    assert (b.n_rows, b.n_cols, b.nnz) == (a.n_rows, a.n_cols, a.nnz)
+    assert torch.equal(b.row_ptr, a.row_ptr) and torch.equal(b.col_idx, a.col_idx)
+    assert torch.equal(b.values, a.values)
+    assert b.has_unit_values == a.has_unit_values
+
+
+def test_gcsr_unit_values_not_stored(tmp_path):
+    a = graphs.powerlaw_graph(300, 3, seed=1, device=CPU)
+    assert a.has_unit_values
+    p = tmp_path / "u.gcsr"
+    a.save(p)
+    size = p.stat().st_size
+    rp_bytes = (a.n_rows + 1) * 4 + (-(a.n_rows + 1) * 4) % 64
+    ci_bytes = a.nnz * 4 + (-a.nnz * 4) % 64
+    assert size == 64 + rp_bytes + ci_bytes
+    b = gc.CsrMatrix.load(p, device=CPU)
+    assert b.has_unit_values and torch.equal(b.values, torch.ones(a.nnz))
+    assert b.same_pattern(a)
+
+
+def test_gcsr_empty_and_rectangular(tmp_path):
+    for a in (gc.CsrMatrix(0, 0, [0], [], [], device=CPU),
+              gc.CsrMatrix(3, 5, [0, 0, 2, 2], [1, 4], [0.5, -2.0], device=CPU)):
+        p = tmp_path / "m.gcsr"
+        a.save(p)
+        b = gc.CsrMatrix.load(p, device=CPU)
+        assert torch.equal(b.to_dense(), a.to_dense()) and b.n_cols == a.n_cols
+
+
+def test_gcsr_rejects_bad_files(tmp_path):
+    a = gc.CsrMatrix(2, 2, [0, 1, 2], [1, 0], [3.0, 4.0], device=CPU)
+    p = tmp_path / "m.gcsr"
+    a.save(p)
+    raw = p.read_bytes()
+    (tmp_path / "trunc.gcsr").write_bytes(raw[:-70])
+    with pytest.raises(gc.ShapeError):
+        gc.CsrMatrix.load(tmp_path / "trunc.gcsr", device=CPU)
+    (tmp_path / "foreign.gcsr").write_bytes(b"%%MatrixMarket" + raw[14:])
+    with pytest.raises(gc.ShapeError):
+        gc.CsrMatrix.load(tmp_path / "foreign.gcsr", device=CPU)
+    bad = bytearray(raw)
+    bad[64 + 4] = 7  # row_ptr[1] = 7 > nnz: invariant check on load
+    (tmp_path / "bad.gcsr").write_bytes(bytes(bad))
+    with pytest.raises(gc.ShapeError):
+        gc.CsrMatrix.load(tmp_path / "bad.gcsr", device=CPU)
+    assert gc.CsrMatrix.load(tmp_path / "bad.gcsr", device=CPU, validate=False).nnz == 2
