@@ -255,6 +255,18 @@ def cpu_model() -> str:
 # ---------------------------------------------------------------------------
 
 
+def _dram_side(traffic, kernel_ms, pk, alg_bytes) -> dict:
+    """The DRAM-side rate of a gather kernel: its ncu-measured DRAM bytes per
+    launch over the live launch time.  The algorithmic model counts every
+    K-wide row gather; most of those hit the 126 MB L2, so ``frac`` (model
+    bytes / HBM peak) can exceed 1 while the DRAM side stays below peak."""
+    if not traffic or not kernel_ms:
+        return {}
+    gbs = traffic / (kernel_ms * 1e-3) / 1e9
+    return {"dram_gbs": round(gbs, 1), "dram_frac": round(gbs / pk["hbm_gbs"], 3),
+            "dram_over_model": round(traffic / alg_bytes, 3)}
+
+
 def main():
     args = parse()
     import torch
@@ -393,7 +405,8 @@ def main():
                 "share_of_step": round(tail_ms / ms, 3), "peak_source": pk["source"],
                 "model": "edge-gather over the tail edges: 4(n+1)+4m_t[+4m_t values][+4m_t d_j]+4m_tK+4nK(+4nK C read)[+4n]",
                 "tail_edges": mt}
-        flops = 2 * plan.cells * K * (2 if hubmod.HUB_FORMAT == "f16x2" else 3)
+        roof.update(_dram_side(traffic, tail_ms, pk, tail_bytes))
+        flops = 2 * plan.cells * K * hubmod.term_count()
         tf = flops / (hub_ms * 1e-3) / 1e12
         hub_roof = {"kernel": "gemm_hub_pair_tcgen05 (dense part)", "bound": "tensor", "achieved": round(tf, 1),
                     "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": round(tf / pk["bf16_tflops"], 3),
@@ -401,8 +414,9 @@ def main():
                     "split": hubmod.spec_label(split), "dense_cells": plan.cells,
                     "dense_edges": plan.hub_edges, "flops_per_launch": flops,
                     "steps": getattr(plan, "steps", None),
-                    "terms": hubmod.HUB_FORMAT,
-                    "model": "2·cells·K per 16-bit term (f16x2: 2 terms, 22-bit split of D·X; bf16x3: 3 terms, exact)"}
+                    "terms": hubmod.FORMAT_NAMES[hubmod.term_format()],
+                    "model": "2·cells·K per 16-bit term (f16: 1 term, TF32-equivalent 11-bit rounding of D·X; "
+                             "f16x2: 2 terms, 22-bit split; bf16x3: 3 terms, exact)"}
     elif spmm_ms:
         spmm_bytes = spmm_alg_bytes(a_used.n_rows, a_used.nnz, K, weighted, dyn, dyn)
         ach = spmm_bytes / (spmm_ms * 1e-3) / 1e9
@@ -417,6 +431,7 @@ def main():
                 "kernel_ms": round(spmm_ms, 4), "share_of_step": round(spmm_ms / ms, 3),
                 "peak_source": pk["source"],
                 "model": "edge-gather: 4(n+1)+4m[+4m values][+4m d_j]+4mK+4nK[+4n]"}
+        roof.update(_dram_side(traffic, spmm_ms, pk, spmm_bytes))
     result = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
@@ -436,7 +451,8 @@ def main():
         "roofline": roof,
         "roofline_hub_gemm": hub_roof,
         "dense_split": {"chosen": __import__("paper_2306_15155_b200.hub", fromlist=["spec_label"]).spec_label(split),
-                        "terms": __import__("paper_2306_15155_b200.hub", fromlist=["HUB_FORMAT"]).HUB_FORMAT,
+                        "terms": (lambda h: h.FORMAT_NAMES[h.term_format()])(
+                            __import__("paper_2306_15155_b200.hub", fromlist=["term_format"])),
                         "autotune_ms": g.a_tilde._plans.get(("hubsplit-choice", K, not dyn, "times"))},
         "setup": {"graph_gen_s": round(gen_s, 2), "prep_s": round(prep_s, 3),
                   "normalize_sddmm_ms": round(norm_ms, 3)},

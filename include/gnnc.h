@@ -227,14 +227,17 @@ GNNC_API int gc_attn_sddmm_f32(const int32_t *row_ptr, const int32_t *col_idx, c
  *   GC_HUB_F16X2:  hi/lo fp16 terms of s·D·X, s = 2^(13 - floor(log2 max|D X|))
  *                  — 22 significant bits above 2^-10·max, absolute error
  *                  <= 2^-23·max|D X| per element; 2/3 of the MMAs.
- * The 0/1 blocks are bf16 (BF16X3) or fp16 (F16X2) — exact either way.  The
+ *   GC_HUB_F16:    the hi fp16 term alone — 11 significant bits, the same
+ *                  input rounding as a TF32 GEMM (for the 1e-2 parity mode
+ *                  the TF32 update already runs in); 1/3 of the MMAs.
+ * The 0/1 blocks are bf16 (BF16X3) or fp16 (F16X2, F16) — exact either way.  The
  * remaining edges are the ordinary SpMM launched with GC_ACCUMULATE on top.
  *
  * gc_hub_terms_rows(K): rows per term of the packed operand (K rounded up to
  *   the kernel's N tile); the packed operand is {terms * rows * T} 16-bit
- *   elements (terms = 3 for BF16X3, 2 for F16X2).
+ *   elements (terms = 3 for BF16X3, 2 for F16X2, 1 for F16).
  * gc_hub_pack: Bt[q][f][t] = term_q(X[hub_cols[t], f] * d_col[hub_cols[t]])
- *   (d_col may be NULL), zero for f >= K; T % 64 == 0.  F16X2 also needs
+ *   (d_col may be NULL), zero for f >= K; T % 64 == 0.  F16X2 / F16 also need
  *   scale_ws (float[2], caller-owned): the max and 1/s for the GEMM.
  * gc_hub_gemm: C[i, f] = d_row[i] * sum_t A_hub[i, t] * (sum_q B_q)[f, t]
  *   (d_row may be NULL; flags: GC_RELU, GC_ACCUMULATE — C = relu?(C + ...)).
@@ -242,6 +245,7 @@ GNNC_API int gc_attn_sddmm_f32(const int32_t *row_ptr, const int32_t *col_idx, c
  *   CTA pairs (tcgen05.mma.cta_group::2) when K > 16.                      */
 #define GC_HUB_BF16X3 0
 #define GC_HUB_F16X2 1
+#define GC_HUB_F16 2
 GNNC_API int64_t gc_hub_terms_rows(int64_t K);
 GNNC_API int gc_hub_pack(const float *X, int64_t ldx, int64_t K, const int32_t *hub_cols,
                 int64_t T, const float *d_col, int32_t fmt, void *Bt, float *scale_ws,

@@ -18,6 +18,7 @@ GC_RELU = 1 << 0
 GC_ACCUMULATE = 1 << 1
 GC_HUB_BF16X3 = 0
 GC_HUB_F16X2 = 1
+GC_HUB_F16 = 2
 GC_HUB_TAGGED = 1 << 2
 
 

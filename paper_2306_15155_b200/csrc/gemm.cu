@@ -511,7 +511,10 @@ __device__ __forceinline__ int stair_kblocks(const StairArgs &sa, int m0) {
 
 // FMT 0: three bf16 terms (exact fp32 split); 1: two fp16 terms of s·D·X
 // (22 significant bits, absolute error <= 2^-23 max|D·X|), 2/3 of the MMAs;
-// 2: one fp32 operand pair on kind::tf32 (the dense update H·W on CTA pairs).
+// 2: one fp32 operand pair on kind::tf32 (the dense update H·W on CTA pairs);
+// 3: one fp16 term of s·D·X (11 significant bits: TF32's input rounding).
+constexpr int fmt_terms(int fmt) { return fmt == 2 || fmt == 3 ? 1 : fmt == 1 ? 2 : 3; }
+
 template <int BN, int FMT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     gemm_hub_pair_tcgen05(const __grid_constant__ StairMaps maps,
@@ -519,7 +522,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
                           const __grid_constant__ CUtensorMap map_c, const GemmEpi ep,
                           const StairArgs sarg, int stages, int m_pairs, int n_tiles,
                           int tma_store, int b_rows_per_term) {
-  constexpr int TERMS = FMT == 2 ? 1 : FMT ? 2 : 3;
+  constexpr int TERMS = fmt_terms(FMT);
   constexpr int KB_EL = FMT == 2 ? 32 : 64;  // elements per 128-byte k-block row
   constexpr int BH = BN / 2;  // B rows per CTA per term
   constexpr uint32_t A_BYTES = BM * KB_BYTES;
@@ -632,7 +635,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   } else if (warp == 1) {
     if (lane == 0 && leader) {  // ---------------- MMA issuer (leader only) ----------------
       constexpr uint32_t idesc = FMT == 2 ? idesc_tf32_m256(ACC_N)
-                                 : FMT ? idesc_f16_m256(ACC_N) : idesc_bf16_m256(ACC_N);
+                                 : FMT ? idesc_f16_m256(ACC_N) : idesc_bf16_m256(ACC_N);  // 1, 3: fp16
       int it = 0, lt = 0;
       for (int ti = t_begin; ti < t_end; ti += t_step, ++lt) {
         const int4 item = item_at(ti);
@@ -801,6 +804,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                             int num_kb, int stages, int m_tiles, int n_tiles, int tma_store,
                             int b_rows_per_term) {
   gemm_tc_body<BN, 3, 1>(map_a, map_b, map_c, ep, num_kb, stages, m_tiles, n_tiles, tma_store,
+                         b_rows_per_term);
+}
+
+// One fp16 term of s·D·X (TF32-equivalent input rounding)
+template <int BN>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_hub_f16_tcgen05(const __grid_constant__ CUtensorMap map_a,
+                         const __grid_constant__ CUtensorMap map_b,
+                         const __grid_constant__ CUtensorMap map_c, const GemmEpi ep, int num_kb,
+                         int stages, int m_tiles, int n_tiles, int tma_store, int b_rows_per_term) {
+  gemm_tc_body<BN, 1, 2>(map_a, map_b, map_c, ep, num_kb, stages, m_tiles, n_tiles, tma_store,
                          b_rows_per_term);
 }
 
@@ -1008,7 +1022,7 @@ int launch_tf32(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap 
 template <int BN, int FMT>
 int launch_hub(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mc, int tma_store,
                const GemmEpi &ep, int64_t T, int64_t kp, cudaStream_t st) {
-  constexpr int TERMS = FMT ? 2 : 3;
+  constexpr int TERMS = fmt_terms(FMT);
   const int num_kb = (int)((T + 63) / 64);
   constexpr int stage_bytes = BM * KB_BYTES + TERMS * BN * KB_BYTES;
   size_t smem = 0;
@@ -1021,7 +1035,8 @@ int launch_hub(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &
     set_error("gc_hub_gemm: tile does not fit shared memory");
     return GC_ERR_UNSUPPORTED;
   }
-  auto kern = FMT ? gemm_hub_f16x2_tcgen05<BN> : gemm_hub_bf16x3_tcgen05<BN>;
+  auto kern = FMT == 3 ? gemm_hub_f16_tcgen05<BN>
+              : FMT ? gemm_hub_f16x2_tcgen05<BN> : gemm_hub_bf16x3_tcgen05<BN>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
@@ -1037,7 +1052,8 @@ int launch_hub(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &
   const int grid = (int)(tiles < sm_count() ? tiles : sm_count());
   kern<<<grid, kGemmThreads, smem, st>>>(ma, mb, mc, ep, num_kb, stages, m_tiles, n_tiles,
                                          tma_store, (int)kp);
-  return check_launch(FMT ? "gemm_hub_f16x2_tcgen05" : "gemm_hub_bf16x3_tcgen05");
+  return check_launch(FMT == 3 ? "gemm_hub_f16_tcgen05"
+                      : FMT ? "gemm_hub_f16x2_tcgen05" : "gemm_hub_bf16x3_tcgen05");
 }
 
 // Split-K fixup: per split tile, sum its workspace partials in slot order and
@@ -1062,7 +1078,7 @@ template <int BN, int FMT>
 int launch_hub_pair(const StairMaps &maps, const StairArgs &sarg, const CUtensorMap &mb,
                     const CUtensorMap &mc, int tma_store, const GemmEpi &ep, int64_t kp,
                     cudaStream_t st, int sched_clusters = 0) {
-  constexpr int stage_bytes = BM * KB_BYTES + (FMT == 2 ? 1 : FMT ? 2 : 3) * (BN / 2) * KB_BYTES;
+  constexpr int stage_bytes = BM * KB_BYTES + fmt_terms(FMT) * (BN / 2) * KB_BYTES;
   size_t smem = 0;
   int stages = tma_store ? ring_stages(stage_bytes, true, &smem) : 0;
   if (stages == 0) {
@@ -1106,10 +1122,15 @@ int launch_hub_pair_bn_f(int pbn, Args &&...args) {
     default: return launch_hub_pair<256, FMT>(args...);
   }
 }
+// kfmt: the kernel's FMT (0 bf16x3, 1 f16x2, 2 tf32, 3 f16) — see kernel_fmt()
 template <typename... Args>
-int launch_hub_pair_bn(int fmt, int pbn, Args &&...args) {
-  return fmt == 2 ? launch_hub_pair_bn_f<2>(pbn, args...)
-       : fmt ? launch_hub_pair_bn_f<1>(pbn, args...) : launch_hub_pair_bn_f<0>(pbn, args...);
+int launch_hub_pair_bn(int kfmt, int pbn, Args &&...args) {
+  switch (kfmt) {
+    case 2: return launch_hub_pair_bn_f<2>(pbn, args...);
+    case 3: return launch_hub_pair_bn_f<3>(pbn, args...);
+    case 1: return launch_hub_pair_bn_f<1>(pbn, args...);
+    default: return launch_hub_pair_bn_f<0>(pbn, args...);
+  }
 }
 template <int FMT, typename... Args>
 int launch_hub_bn_f(int bn, Args &&...args) {
@@ -1120,6 +1141,14 @@ int launch_hub_bn_f(int bn, Args &&...args) {
     case 128: return launch_hub<128, FMT>(args...);
     default: return launch_hub<256, FMT>(args...);
   }
+}
+
+// ABI term format (GC_HUB_*) -> kernel FMT, term count, 16-bit element kind
+inline int kernel_fmt(int32_t fmt) { return fmt == GC_HUB_F16 ? 3 : fmt == GC_HUB_F16X2 ? 1 : 0; }
+inline int hub_terms(int32_t fmt) { return fmt == GC_HUB_F16 ? 1 : fmt == GC_HUB_F16X2 ? 2 : 3; }
+inline bool hub_is_f16(int32_t fmt) { return fmt == GC_HUB_F16 || fmt == GC_HUB_F16X2; }
+inline bool hub_fmt_ok(int32_t fmt) {
+  return fmt == GC_HUB_BF16X3 || fmt == GC_HUB_F16X2 || fmt == GC_HUB_F16;
 }
 
 inline bool gemm_pair_enabled() {  // GNNC_GEMM_PAIR=0: TF32 GEMM on single CTAs
@@ -1207,7 +1236,9 @@ __global__ void __launch_bounds__(256)
 // Two fp16 terms of s·x, s = 2^(13 - floor(log2 max|x|)) so max|s·x| < 2^14:
 // hi = fp16(s x), lo = fp16(s x - hi) carry 22 significant bits of every
 // element above 2^-10 max|x| (absolute error <= 2^-23 max|x| for all).
+// TERMS == 1 writes hi only: 11 significant bits, TF32's input rounding.
 // Block (0, 0) publishes 1/s in scale[1] for the GEMM epilogue.
+template <int TERMS>
 __global__ void __launch_bounds__(256)
     hub_pack_f16_kernel(const float *__restrict__ X, int64_t ldx, int64_t K,
                         const int32_t *__restrict__ hub_cols, int64_t T,
@@ -1236,10 +1267,12 @@ __global__ void __launch_bounds__(256)
     if (f >= kp || t >= T) continue;
     const float y0 = tile[2 * threadIdx.x][i], y1 = tile[2 * threadIdx.x + 1][i];
     const __half h0 = __float2half_rn(y0), h1 = __float2half_rn(y1);
-    const __half l0 = __float2half_rn(y0 - __half2float(h0));
-    const __half l1 = __float2half_rn(y1 - __half2float(h1));
     *reinterpret_cast<__half2 *>(Bt + f * T + t) = __halves2half2(h0, h1);
-    *reinterpret_cast<__half2 *>(Bt + (kp + f) * T + t) = __halves2half2(l0, l1);
+    if constexpr (TERMS == 2) {
+      const __half l0 = __float2half_rn(y0 - __half2float(h0));
+      const __half l1 = __float2half_rn(y1 - __half2float(h1));
+      *reinterpret_cast<__half2 *>(Bt + (kp + f) * T + t) = __halves2half2(l0, l1);
+    }
   }
 }
 
@@ -1383,8 +1416,7 @@ extern "C" int gc_hub_pack(const float *X, int64_t ldx, int64_t K, const int32_t
                            int64_t T, const float *d_col, int32_t fmt, void *Bt, float *scale_ws,
                            void *stream) {
   GC_REQUIRE(K >= 1 && T >= 0 && ldx >= K, GC_ERR_SHAPE, "gc_hub_pack: bad shape");
-  GC_REQUIRE(fmt == GC_HUB_BF16X3 || fmt == GC_HUB_F16X2, GC_ERR_VALUE, "gc_hub_pack: format %d",
-             fmt);
+  GC_REQUIRE(hub_fmt_ok(fmt), GC_ERR_VALUE, "gc_hub_pack: format %d", fmt);
   if (T == 0) return GC_OK;
   GC_REQUIRE(X && hub_cols && Bt && (fmt == GC_HUB_BF16X3 || scale_ws), GC_ERR_VALUE,
              "gc_hub_pack: null operand");
@@ -1407,8 +1439,12 @@ extern "C" int gc_hub_pack(const float *X, int64_t ldx, int64_t K, const int32_t
   hub_absmax_kernel<<<(unsigned)blocks, 256, 0, st>>>(X, ldx, K, hub_cols, T, d_col, amax);
   int rc = check_launch("hub_absmax_kernel");
   if (rc) return rc;
-  hub_pack_f16_kernel<<<grid, dim3(32, 8), 0, st>>>(X, ldx, K, hub_cols, T, d_col, kp, amax,
-                                                    scale_ws + 1, static_cast<__half *>(Bt));
+  if (fmt == GC_HUB_F16)
+    hub_pack_f16_kernel<1><<<grid, dim3(32, 8), 0, st>>>(X, ldx, K, hub_cols, T, d_col, kp, amax,
+                                                         scale_ws + 1, static_cast<__half *>(Bt));
+  else
+    hub_pack_f16_kernel<2><<<grid, dim3(32, 8), 0, st>>>(X, ldx, K, hub_cols, T, d_col, kp, amax,
+                                                         scale_ws + 1, static_cast<__half *>(Bt));
   return check_launch("hub_pack_f16_kernel");
 }
 
@@ -1418,8 +1454,7 @@ extern "C" int gc_hub_gemm(const void *A_hub, int64_t lda, int64_t n_rows, int64
                            void *stream) {
   GC_REQUIRE(n_rows >= 0 && T >= 0 && K >= 1 && lda >= T && ldc >= K, GC_ERR_SHAPE,
              "gc_hub_gemm: bad shape");
-  GC_REQUIRE(fmt == GC_HUB_BF16X3 || fmt == GC_HUB_F16X2, GC_ERR_VALUE, "gc_hub_gemm: format %d",
-             fmt);
+  GC_REQUIRE(hub_fmt_ok(fmt), GC_ERR_VALUE, "gc_hub_gemm: format %d", fmt);
   GC_REQUIRE((flags & ~(GC_RELU | GC_ACCUMULATE)) == 0, GC_ERR_VALUE,
              "gc_hub_gemm: unknown flags 0x%x", flags);
   if (n_rows == 0) return GC_OK;
@@ -1431,14 +1466,14 @@ extern "C" int gc_hub_gemm(const void *A_hub, int64_t lda, int64_t n_rows, int64
   GC_REQUIRE(n_rows < (int64_t)INT32_MAX && T < (int64_t)INT32_MAX, GC_ERR_SHAPE,
              "gc_hub_gemm: dimension exceeds TMA range");
   cudaStream_t st = as_stream(stream);
-  const int terms = fmt == GC_HUB_F16X2 ? 2 : 3;
+  const int terms = hub_terms(fmt);
   const int bn = hub_bn(K);
   const int64_t kp = gc_hub_terms_rows(K);
   CUtensorMap ma, mb, mc;
   int rc = make_map(&ma, A_hub, n_rows, T, lda, BM, 64, CU_TENSOR_MAP_SWIZZLE_128B, true,
-                    fmt == GC_HUB_F16X2);
+                    hub_is_f16(fmt));
   if (rc) return rc;
-  GemmEpi ep{C, ldc, d_row, n_rows, K, flags, fmt == GC_HUB_F16X2 ? scale_ws + 1 : nullptr};
+  GemmEpi ep{C, ldc, d_row, n_rows, K, flags, hub_is_f16(fmt) ? scale_ws + 1 : nullptr};
   // accumulating epilogues read C back: direct stores
   int tma_store = ((ldc % 4) == 0 && aligned16(C) && !(flags & GC_ACCUMULATE)) ? 1 : 0;
   memset(&mc, 0, sizeof(mc));
@@ -1452,7 +1487,7 @@ extern "C" int gc_hub_gemm(const void *A_hub, int64_t lda, int64_t n_rows, int64
     const int pbn = pair_bn(K);
     CUtensorMap mbp;
     rc = make_map(&mbp, Bt, terms * kp, T, T, pbn / 2, 64, CU_TENSOR_MAP_SWIZZLE_128B, true,
-                  fmt == GC_HUB_F16X2);
+                  hub_is_f16(fmt));
     if (rc) return rc;
     StairMaps maps;
     memset(&maps, 0, sizeof(maps));
@@ -1463,13 +1498,16 @@ extern "C" int gc_hub_gemm(const void *A_hub, int64_t lda, int64_t n_rows, int64
     sarg.c0[0] = 0;
     sarg.nkb[0] = (int)(T / 64);
     sarg.row_map = nullptr;
-    return launch_hub_pair_bn(fmt, pbn, maps, sarg, mbp, mc, tma_store, ep, kp, st, 0);
+    return launch_hub_pair_bn(kernel_fmt(fmt), pbn, maps, sarg, mbp, mc, tma_store, ep, kp, st, 0);
   }
   rc = make_map(&mb, Bt, terms * kp, T, T, bn, 64, CU_TENSOR_MAP_SWIZZLE_128B, true,
-                fmt == GC_HUB_F16X2);
+                hub_is_f16(fmt));
   if (rc) return rc;
-  return fmt == GC_HUB_F16X2 ? launch_hub_bn_f<1>(bn, ma, mb, mc, tma_store, ep, T, kp, st)
-                             : launch_hub_bn_f<0>(bn, ma, mb, mc, tma_store, ep, T, kp, st);
+  switch (kernel_fmt(fmt)) {
+    case 3: return launch_hub_bn_f<3>(bn, ma, mb, mc, tma_store, ep, T, kp, st);
+    case 1: return launch_hub_bn_f<1>(bn, ma, mb, mc, tma_store, ep, T, kp, st);
+    default: return launch_hub_bn_f<0>(bn, ma, mb, mc, tma_store, ep, T, kp, st);
+  }
 }
 
 extern "C" int gc_hub_stair_pair_bn(int64_t K) { return K > 0 ? pair_bn(K) : 0; }
@@ -1486,7 +1524,7 @@ extern "C" int gc_hub_stair_gemm(const void *const *A_steps, const int64_t *step
                                  const void *Bt, int64_t T, int64_t K, int32_t fmt,
                                  const float *scale_ws, float *C, int64_t ldc, const float *d_row,
                                  uint32_t flags, void *stream) {
-  GC_REQUIRE(fmt == GC_HUB_BF16X3 || (fmt == GC_HUB_F16X2 && scale_ws), GC_ERR_VALUE,
+  GC_REQUIRE(hub_fmt_ok(fmt) && (fmt == GC_HUB_BF16X3 || scale_ws), GC_ERR_VALUE,
              "gc_hub_stair_gemm: format %d", fmt);
   GC_REQUIRE(n_steps >= 1 && n_steps <= kMaxSteps, GC_ERR_VALUE,
              "gc_hub_stair_gemm: 1..%d steps", kMaxSteps);
@@ -1531,7 +1569,7 @@ extern "C" int gc_hub_stair_gemm(const void *const *A_steps, const int64_t *step
     GC_REQUIRE(A_steps[s] && aligned16(A_steps[s]), GC_ERR_VALUE,
                "gc_hub_stair_gemm: step %d operand", s);
     int rc = make_map(&maps.a[s], A_steps[s], r, w, w, BM, 64, CU_TENSOR_MAP_SWIZZLE_128B, true,
-                      fmt == GC_HUB_F16X2);
+                      hub_is_f16(fmt));
     if (rc) return rc;
     sarg.rows[s] = (int)r;
     sarg.c0[s] = (int)c0;
@@ -1540,8 +1578,8 @@ extern "C" int gc_hub_stair_gemm(const void *const *A_steps, const int64_t *step
   const int64_t kp = gc_hub_terms_rows(K);
   const int pbn = pair_bn(K);
   CUtensorMap mbp, mc;
-  int rc = make_map(&mbp, Bt, (fmt == GC_HUB_F16X2 ? 2 : 3) * kp, T, T, pbn / 2, 64,
-                    CU_TENSOR_MAP_SWIZZLE_128B, true, fmt == GC_HUB_F16X2);
+  int rc = make_map(&mbp, Bt, hub_terms(fmt) * kp, T, T, pbn / 2, 64,
+                    CU_TENSOR_MAP_SWIZZLE_128B, true, hub_is_f16(fmt));
   if (rc) return rc;
   memset(&mc, 0, sizeof(mc));
   // rank-ordered rows scatter through row_map: direct stores
@@ -1551,10 +1589,9 @@ extern "C" int gc_hub_stair_gemm(const void *const *A_steps, const int64_t *step
     rc = make_map(&mc, C, step_rows[0], K, ldc, 32, 16, CU_TENSOR_MAP_SWIZZLE_64B);
     if (rc) return rc;
   }
-  GemmEpi ep{C, ldc, d_row, step_rows[0], K, flags,
-             fmt == GC_HUB_F16X2 ? scale_ws + 1 : nullptr};
+  GemmEpi ep{C, ldc, d_row, step_rows[0], K, flags, hub_is_f16(fmt) ? scale_ws + 1 : nullptr};
   cudaStream_t st = as_stream(stream);
-  rc = launch_hub_pair_bn(fmt, pbn, maps, sarg, mbp, mc, tma_store, ep, kp, st,
+  rc = launch_hub_pair_bn(kernel_fmt(fmt), pbn, maps, sarg, mbp, mc, tma_store, ep, kp, st,
                           items ? (int)n_clusters : 0);
   if (rc || n_fixups == 0) return rc;
   const int n_tiles = (int)((K + pbn - 1) / pbn);

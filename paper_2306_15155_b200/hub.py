@@ -15,10 +15,14 @@ shared memory:
     C_dense = D · A_dense · (D X)[dense columns],   A_dense ∈ {0,1}
 
 computed by tcgen05 kind::f16 GEMMs: the 0/1 blocks are exact in fp16/bf16
-and (D X)[columns] is split into 16-bit terms (``gc_hub_pack``): by default
-two fp16 terms of s·D·X with a power-of-two scale s (22 significant bits:
-absolute error <= 2^-23·max|D X| per element, 2/3 of the MMAs), or
-(GNNC_HUB_FORMAT=bf16x3) three bf16 terms that carry its exact fp32 mantissa.  The SpMM then accumulates the remaining edges on top
+and (D X)[columns] is rounded to 16-bit terms (``gc_hub_pack``) following
+the layer's GEMM precision (``sparse.set_gemm_precision``): in the TF32 mode
+(1e-2 parity, the default) one fp16 term of s·D·X with a power-of-two scale
+s — 11 significant bits, the same input rounding the TF32 update GEMM
+applies to H; in the fp32 mode (1e-4 parity) two fp16 terms (22 significant
+bits: absolute error <= 2^-23·max|D X| per element).  GNNC_HUB_FORMAT pins
+"f16", "f16x2" or "bf16x3" (three bf16 terms carrying the exact fp32
+mantissa).  The SpMM then accumulates the remaining edges on top
 (GC_ACCUMULATE); apart from the term split only the summation order differs
 from the plain SpMM.
 
@@ -52,20 +56,41 @@ from . import _native as nat
 from .sparse import CsrMatrix, ShapeError, _ld, _require_cuda, _spmm, _stream, _timed_call
 
 HUB_SPLIT = os.environ.get("GNNC_HUB_SPLIT", "auto")
-# term format of the dense operand: "f16x2" (default: two fp16 terms of s·D·X
-# with a power-of-two s — 22 significant bits, absolute error <= 2^-23
-# max|D·X| per element, 2/3 of the MMAs; Reddit K=256 staircase 0.58 vs 0.80
-# ms, normwise difference from the plain SpMM 2.8e-6 either way) or "bf16x3"
-# (exact fp32 split)
-HUB_FORMAT = os.environ.get("GNNC_HUB_FORMAT", "f16x2")
+# term format of the dense operand: "auto" (default: one fp16 term in the TF32
+# GEMM mode, two in the fp32 mode), "f16" (one fp16 term of s·D·X, 11
+# significant bits), "f16x2" (two fp16 terms — 22 significant bits, absolute
+# error <= 2^-23 max|D·X| per element, 2/3 of the MMAs of bf16x3; Reddit K=256
+# staircase 0.58 vs 0.80 ms, normwise difference from the plain SpMM 2.8e-6
+# either way) or "bf16x3" (exact fp32 split)
+HUB_FORMAT = os.environ.get("GNNC_HUB_FORMAT", "auto")
+_TERMS = {nat.GC_HUB_F16: 1, nat.GC_HUB_F16X2: 2, nat.GC_HUB_BF16X3: 3}
+FORMAT_NAMES = {nat.GC_HUB_F16: "f16", nat.GC_HUB_F16X2: "f16x2", nat.GC_HUB_BF16X3: "bf16x3"}
 
 
 def _fmt() -> int:
-    return nat.GC_HUB_F16X2 if HUB_FORMAT == "f16x2" else nat.GC_HUB_BF16X3
+    """The 0/1 block family of a plan: bf16 blocks for bf16x3, else fp16."""
+    return nat.GC_HUB_BF16X3 if HUB_FORMAT == "bf16x3" else nat.GC_HUB_F16X2
+
+
+def term_format(block_fmt: int | None = None) -> int:
+    """The term format a pack/GEMM runs in now (see HUB_FORMAT)."""
+    if (block_fmt if block_fmt is not None else _fmt()) == nat.GC_HUB_BF16X3:
+        return nat.GC_HUB_BF16X3
+    if HUB_FORMAT == "f16":
+        return nat.GC_HUB_F16
+    if HUB_FORMAT == "f16x2":
+        return nat.GC_HUB_F16X2
+    from .sparse import get_gemm_precision
+
+    return nat.GC_HUB_F16 if get_gemm_precision() == "tf32" else nat.GC_HUB_F16X2
+
+
+def term_count(fmt: int | None = None) -> int:
+    return _TERMS[term_format() if fmt is None else fmt]
 
 
 def _block_dtype(fmt: int):
-    return torch.float16 if fmt == nat.GC_HUB_F16X2 else torch.bfloat16
+    return torch.bfloat16 if fmt == nat.GC_HUB_BF16X3 else torch.float16
 HUB_T_CANDIDATES = (1024, 2048, 4096, 8192)
 # (cell/edge cost ratio δ, balance slack) pairs tried by the autotuner
 # (slack > 1 reaches further right, but short-wide steps stream their B
@@ -80,10 +105,21 @@ STAIR_CANDIDATES_SMALL_K = {128: ((0.018, 1.0), (0.03, 1.0), (0.06, 1.0)),
 
 
 def _stair_candidates(K: int):
+    """δ candidates for this K, tuned on the two-term format; a dense cell
+    costs MMAs in proportion to the term count, so δ scales with it (the
+    one-term format also keeps the two-term table's smallest δ)."""
+    cands = STAIR_CANDIDATES
     for k, c in sorted(STAIR_CANDIDATES_SMALL_K.items()):
         if K <= k:
-            return c
-    return STAIR_CANDIDATES
+            cands = c
+            break
+    f = term_count() / 2.0
+    if f == 1.0:
+        return cands
+    out = [(max(round(dl * f, 3), 0.001), sl) for dl, sl in cands]
+    if f < 1.0:
+        out.append(cands[0])
+    return tuple(dict.fromkeys(out))
 HUB_MIN_NNZ = 1 << 24            # smaller graphs stay on the SpMM alone
 HUB_MIN_DENSITY = 0.02           # mean density of a block worth a dense product
 HUB_MEM_BUDGET = 8 << 30         # bytes of dense blocks per pattern
@@ -350,20 +386,21 @@ def hub_plan(a: CsrMatrix, spec):
 
 
 def pack(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec):
-    """The dense-part operand (D X)[hub_cols] as bf16/fp16 terms, K-major, and
-    the fp16 format's scale workspace (float[2]: max, 1/s)."""
+    """The dense-part operand (D X)[hub_cols] as bf16/fp16 terms, K-major,
+    the fp16 formats' scale workspace (float[2]: max, 1/s) and the term
+    format used (``term_format``)."""
     plan = hub_plan(a, spec)
     lib = nat.load()
     K = x.shape[1]
     kp = int(lib.gc_hub_terms_rows(K))
-    terms = 2 if plan.fmt == nat.GC_HUB_F16X2 else 3
-    bt = torch.empty(terms * kp * plan.T, dtype=_block_dtype(plan.fmt), device=x.device)
+    fmt = term_format(plan.fmt)
+    bt = torch.empty(_TERMS[fmt] * kp * plan.T, dtype=_block_dtype(fmt), device=x.device)
     sc = torch.empty(2, dtype=torch.float32, device=x.device)
     nat.check(lib.gc_hub_pack(x.data_ptr(), _ld(x), K, plan.hub_cols.data_ptr(), plan.T,
-                              None if d is None else d.data_ptr(), plan.fmt, bt.data_ptr(),
+                              None if d is None else d.data_ptr(), fmt, bt.data_ptr(),
                               sc.data_ptr(),
                               _stream(x.device)), "hub_pack")
-    return bt, sc
+    return bt, sc, fmt
 
 
 def dense_part(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, out: torch.Tensor, *,
@@ -375,14 +412,14 @@ def dense_part(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, out: torch.
     lib = nat.load()
     st = _stream(dev)
     K = x.shape[1]
-    bt, sc = packed if packed is not None else pack(a, x, d, spec)
+    bt, sc, fmt = packed if packed is not None else pack(a, x, d, spec)
     flags = nat.GC_ACCUMULATE if accumulate else 0
     if plan.kind == "block":
         lo, hi = rows if rows is not None else (0, a.n_rows)
         a_hub = plan.a_hub[lo:hi]
         dr = d_row[lo:hi]
         nat.check(_timed_call("hub_gemm", dev, lambda: lib.gc_hub_gemm(
-            a_hub.data_ptr(), plan.T, hi - lo, plan.T, bt.data_ptr(), K, plan.fmt, sc.data_ptr(),
+            a_hub.data_ptr(), plan.T, hi - lo, plan.T, bt.data_ptr(), K, fmt, sc.data_ptr(),
             out.data_ptr(), _ld(out), dr.data_ptr(), flags, st)), "hub_gemm")
         return
     if rows is not None and tuple(rows) != (0, a.n_rows):
@@ -395,7 +432,7 @@ def dense_part(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, out: torch.
         plan._np_w.ctypes.data, len(plan.steps), plan.row_map.data_ptr(), items.data_ptr(),
         starts.data_ptr(), n_cl, None if ws is None else ws.data_ptr(),
         None if fx is None else fx.data_ptr(), 0 if fx is None else fx.shape[0], bt.data_ptr(),
-        plan.T, K, plan.fmt, sc.data_ptr(), out.data_ptr(), _ld(out), d_row.data_ptr(), flags,
+        plan.T, K, fmt, sc.data_ptr(), out.data_ptr(), _ld(out), d_row.data_ptr(), flags,
         st)), "hub_stair_gemm")
 
 
@@ -416,7 +453,7 @@ def hybrid_aggregate(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, *,
                      d_row: torch.Tensor | None = None, values: torch.Tensor | None = None,
                      relu: bool = False, out: torch.Tensor | None = None,
                      accumulate: bool = False, rows: tuple[int, int] | None = None,
-                     packed: torch.Tensor | None = None) -> torch.Tensor:
+                     packed: tuple | None = None) -> torch.Tensor:
     """C = epi(D_row Ã D X) for a unit-valued pattern ``a`` via the dense/tail
     split ``spec`` (``d`` scales the columns — None when x already carries
     the column scaling; ``d_row`` the rows, default ``d`` itself for a square

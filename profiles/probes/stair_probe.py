@@ -38,6 +38,6 @@ for spec in specs:
     r["total_ms"] = t_ms(lambda: hub.hybrid_aggregate(a, x, d, spec, out=out))
     y = hub.hybrid_aggregate(a, x, d, spec)
     r["rel_err_vs_plain"] = float((y - ref).abs().max() / ref.abs().max())
-    r["dense_tflops"] = 2 * plan.cells * K * 3 / r["dense_ms"] / 1e9
+    r["dense_tflops"] = 2 * plan.cells * K * hub.term_count() / r["dense_ms"] / 1e9; r["terms"] = hub.term_count()
     print(json.dumps(r), flush=True)
     a._plans.pop(("hubsplit", hub._parse_spec(spec)), None)

@@ -71,6 +71,12 @@ def test_error_codes_without_launch(lib):
     assert rc == _native.GC_ERR_VALUE and b"format" in lib.gc_last_error()
     rc = lib.gc_hub_pack(None, 8, 8, None, 64, None, _native.GC_HUB_F16X2, None, None, None)
     assert rc == _native.GC_ERR_VALUE  # null operands (f16x2 also needs the scale workspace)
+    rc = lib.gc_hub_pack(None, 8, 8, None, 64, None, _native.GC_HUB_F16, None, None, None)
+    assert rc == _native.GC_ERR_VALUE  # one-term f16: known format, null operands
+    assert b"null" in lib.gc_last_error()
+    rc = lib.gc_hub_stair_gemm(None, None, None, None, 1, None, None, None, 0, None, None, 0, None,
+                               64, 32, _native.GC_HUB_F16, None, None, 32, None, 0, None)
+    assert rc == _native.GC_ERR_VALUE  # f16 needs the scale workspace
     rc = lib.gc_hub_gemm(None, 63, 10, 64, None, 8, _native.GC_HUB_BF16X3, None, None, 8, None,
                          0, None)
     assert rc == _native.GC_ERR_SHAPE  # lda < T

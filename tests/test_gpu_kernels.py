@@ -17,6 +17,16 @@ from paper_2306_15155_b200 import graphs, sparse  # noqa: E402
 
 DEV = "cuda"
 SP_TOL = 1e-5
+# the hybrid aggregation in the default TF32 mode rounds the dense part's
+# operand to one fp16 term (11 significant bits, TF32's input rounding): the
+# layer's stated 1e-2 class; measured ~1e-4 on these graphs
+HUB_F16_TOL = 1e-3
+
+
+def hub_tol() -> float:
+    from paper_2306_15155_b200 import _native as nat
+    from paper_2306_15155_b200 import hub
+    return HUB_F16_TOL if hub.term_format() == nat.GC_HUB_F16 else SP_TOL
 
 
 def to_oracle(oracle, a: gc.CsrMatrix):
@@ -563,15 +573,16 @@ def hub_pl():
 
 @pytest.mark.parametrize("K", [1, 7, 16, 32, 100, 256, 300, 512])
 @pytest.mark.parametrize("T", [64, 128])
-@pytest.mark.parametrize("fmt", ["bf16x3", "f16x2"])
+@pytest.mark.parametrize("fmt", ["bf16x3", "f16x2", "f16"])
 def test_hub_gemm_term_split(oracle, K, T, fmt):
     """Dense 0/1 block times the packed terms of D·X: bf16x3 is the exact fp32
     split (1e-6 normwise with rows spanning six decades), f16x2 carries 22
-    significant bits relative to max|D·X| (absolute error <= 2^-23 max)."""
+    significant bits relative to max|D·X| (absolute error <= 2^-23 max), f16
+    11 (TF32's input rounding: 1e-3 normwise here)."""
     from paper_2306_15155_b200 import _native as nat
-    f = nat.GC_HUB_F16X2 if fmt == "f16x2" else nat.GC_HUB_BF16X3
-    dt = torch.float16 if fmt == "f16x2" else torch.bfloat16
-    terms = 2 if fmt == "f16x2" else 3
+    f = {"f16x2": nat.GC_HUB_F16X2, "f16": nat.GC_HUB_F16, "bf16x3": nat.GC_HUB_BF16X3}[fmt]
+    dt = torch.bfloat16 if fmt == "bf16x3" else torch.float16
+    terms = {"f16x2": 2, "f16": 1, "bf16x3": 3}[fmt]
     rng = np.random.default_rng(K * 7 + T)
     n, ncols = 777, 3000
     a_hub = (rng.random((n, T)) < 0.3).astype(np.float32)
@@ -594,7 +605,7 @@ def test_hub_gemm_term_split(oracle, K, T, fmt):
                               out.data_ptr(), K, drt.data_ptr(), 0, st), "gemm")
     ref = dr.astype(np.float64)[:, None] * (a_hub.astype(np.float64) @ (
         x.astype(np.float64)[hub_cols] * d.astype(np.float64)[hub_cols][:, None]))
-    assert oracle.rel_err(out.cpu().numpy(), ref) < 1e-6
+    assert oracle.rel_err(out.cpu().numpy(), ref) < (1e-3 if fmt == "f16" else 1e-6)
 
 
 @pytest.mark.parametrize("K", [3, 32, 256])
@@ -611,7 +622,7 @@ def test_hybrid_aggregate_matches_oracle(oracle, hub_pl, K, T, precompute):
     out = hub.hybrid_aggregate(g.a_tilde, torch.from_numpy(x).to(DEV), d, T, values=vals,
                                relu=True)
     ref = np.maximum(oracle.spmm(og.n_tilde, x), 0)
-    assert oracle.rel_err(out.cpu().numpy(), ref) < SP_TOL
+    assert oracle.rel_err(out.cpu().numpy(), ref) < hub_tol()
     plan = hub.hub_plan(g.a_tilde, T)
     assert plan.hub_edges + plan.tail.nnz == g.a_tilde.nnz
     assert plan.hub_edges == int(plan.a_hub.float().sum())
@@ -702,14 +713,14 @@ def test_stair_split_matches_oracle(oracle, stair_pl, K, precompute):
     vals = g.n_tilde.values if precompute else None
     out = hub.hybrid_aggregate(a, torch.from_numpy(x).to(DEV), d, spec, values=vals, relu=True)
     ref = np.maximum(oracle.spmm(og.n_tilde, x), 0)
-    assert oracle.rel_err(out.cpu().numpy(), ref) < SP_TOL
+    assert oracle.rel_err(out.cpu().numpy(), ref) < hub_tol()
     # accumulate form (used by the multi-GPU remote pass)
     base = torch.from_numpy(f32(rng.uniform(-1, 1, (a.n_rows, K)))).to(DEV)
     acc = base.clone()
     hub.hybrid_aggregate(a, torch.from_numpy(x).to(DEV), d, spec, values=vals, out=acc,
                          accumulate=True)
     ref2 = base.cpu().numpy().astype(np.float64) + oracle.spmm(og.n_tilde, x)
-    assert oracle.rel_err(acc.cpu().numpy(), ref2) < SP_TOL
+    assert oracle.rel_err(acc.cpu().numpy(), ref2) < hub_tol()
 
 
 def test_host_pipelined_layer_with_stair_split(oracle, stair_pl, monkeypatch):
@@ -759,7 +770,7 @@ def test_stair_split_on_rectangular_block(oracle, stair_pl):
     x = torch.from_numpy(f32(rng.uniform(-0.5, 0.5, (blk.n_cols, 128)))).to(DEV)
     out = hub.hybrid_aggregate(blk, x, d, spec, d_row=d[lo:hi], relu=True)
     ref = gc.spmm_unweighted(blk, x, d_row=d[lo:hi], d_col=d, relu=True)
-    assert oracle.rel_err(out.cpu().numpy(), ref.cpu().numpy().astype(np.float64)) < SP_TOL
+    assert oracle.rel_err(out.cpu().numpy(), ref.cpu().numpy().astype(np.float64)) < hub_tol()
 
 
 def test_gcsr_load_to_device_and_partition(tmp_path, oracle):
