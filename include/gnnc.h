@@ -61,6 +61,7 @@ extern "C" {
 #define GC_SPMM_SHRINK_MASK (3u << 8)
 #define GC_GEMM_TF32 (1u << 4)  /* tcgen05.mma kind::tf32, TMEM accumulators, TMA operands */
 #define GC_GEMM_FP32 (1u << 5)  /* exact fp32 CUDA-core path (rtol 1e-4 parity mode) */
+#define GC_HUB_A_BITS (1u << 6) /* gc_hub_stair_gemm: A_steps are bitmaps (see there) */
 
 /* SpMM work decomposition */
 #define GC_SPMM_ROW 1       /* one lane-group per CSR row                          */
@@ -271,7 +272,11 @@ GNNC_API int gc_hub_gemm(const void *A_hub, int64_t lda, int64_t n_rows, int64_t
  * NULL: round-robin whole tiles.  Split-K: items with a slot write their
  * (row-scaled) partial tile to workspace[slot][256][pair_bn]; fixups
  * {tile, first slot, slot count, 0} then add the partials to C in slot
- * order (deterministic; no GC_RELU with split items).                      */
+ * order (deterministic; no GC_RELU with split items).
+ * GC_HUB_A_BITS: A_steps[s] is instead a bitmap of uint64 words, word
+ * (k, r) at index k * rpad_s + r (rpad_s = step_rows[s] rounded up to 256,
+ * padding rows zero), bit j = A_s[r, 64k + j]; converter warps expand each
+ * 128 x 64 tile into the 16-bit operand in shared memory (16x fewer A bytes). */
 GNNC_API int gc_hub_stair_supported(int64_t K);
 GNNC_API int gc_hub_stair_pair_bn(int64_t K);
 GNNC_API int gc_hub_stair_gemm(const void *const *A_steps, const int64_t *step_rows,

@@ -19,6 +19,7 @@ GC_ACCUMULATE = 1 << 1
 GC_HUB_BF16X3 = 0
 GC_HUB_F16X2 = 1
 GC_HUB_F16 = 2
+GC_HUB_A_BITS = 1 << 6
 GC_HUB_TAGGED = 1 << 2
 
 

@@ -61,12 +61,40 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   }
 }
 
+// The same with cluster-scope acquire: the waiter then observes the
+// (release.cluster) arrivals' prior shared-memory writes of the peer CTA.
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  uint64_t spins = 0;
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (++spins > (1ull << 26)) __trap();
+  }
+}
+
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar,
                                             int32_t c0, int32_t c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// plain bulk copy global -> this CTA's shared memory (16-B aligned, size % 16 == 0)
+__device__ __forceinline__ void bulk_load_1d(uint32_t dst, const void *src, uint32_t bytes,
+                                             uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
       : "memory");
 }
 
@@ -491,6 +519,9 @@ struct StairArgs {
   int rows[kMaxSteps];
   int c0[kMaxSteps];
   int nkb[kMaxSteps];
+  // bit-packed blocks (GC_HUB_A_BITS): step s's words start at bits[s],
+  // word (k, r) at k * rpad(s) + r, rpad = rows rounded up to 256
+  const uint64_t *bits[kMaxSteps];
   const int32_t *row_map;
   // optional static schedule (longest-processing-time first, built by the
   // caller): cluster c runs work items items[cluster_start[c] ..
@@ -499,7 +530,8 @@ struct StairArgs {
   const int4 *items;
   const int32_t *cluster_start;
   float *ws;  // [slot][256 rank rows][BN] partial products (rows pre-scaled)
-  int dbg;    // experiments only (GNNC_HUB_DBG): 1 = A once per step, 2 = B once, 4 = no MMA
+  int dbg;    // experiments only (GNNC_HUB_DBG): 1 = A once per step, 2 = B once, 4 = no MMA,
+              // 8 = converters skip the expansion, 16 = no proxy fence
 };
 
 __device__ __forceinline__ int stair_kblocks(const StairArgs &sa, int m0) {
@@ -515,8 +547,32 @@ __device__ __forceinline__ int stair_kblocks(const StairArgs &sa, int m0) {
 // 3: one fp16 term of s·D·X (11 significant bits: TF32's input rounding).
 constexpr int fmt_terms(int fmt) { return fmt == 2 || fmt == 3 ? 1 : fmt == 1 ? 2 : 3; }
 
-template <int BN, int FMT>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+// ABITS: the 0/1 A blocks arrive as bitmaps (1 KB per 128 x 64 k-block tile
+// instead of 16 KB) and converter warps expand them into the SWIZZLE_128B
+// fp16/bf16 tile the MMA reads — the dense part's DRAM traffic drops to the
+// B operand (L2-resident) plus 1/16 of the A bytes.  Three rings: bitmaps
+// (kBitsSlots deep, streamed by a dedicated producer warp: DRAM latency is
+// hidden by 1 KB slots), converted A tiles (kAStages: produced on chip, so
+// shallow) and B tiles (all remaining shared memory: the B stream from L2 is
+// latency x bytes-in-flight bound).  Converter groups (4 warps = 128 rows
+// each) take alternate k-blocks — one group's per-k-block latency (wait,
+// expand, proxy fence, remote arrive) exceeds the MMA time of a k-block.
+// Group g owns A slot g (kAStages == kConvGroups): every slot's barriers have
+// one sequential waiter, so no waiter can run two phases ahead (parity
+// aliasing), and the bitmap slots map to groups the same way.
+// Measured on Reddit K=256 (stair:8, one fp16 term): 0.86 ms vs 0.62 ms with
+// 16-bit A tiles from HBM — the per-k-block handoff chain (bitmap -> converter
+// -> cluster arrive -> MMA -> commit -> converter) bounds it: more A slots do
+// not help (8 per 4 groups: 0.86), fewer groups hurt (2: 1.12).  Kept as the
+// GC_HUB_A_BITS option for its 16x smaller block storage.
+constexpr int kConvGroups = 4;
+constexpr int kAStages = kConvGroups;
+constexpr int kBitsSlots = 16;
+static_assert(kAStages % kConvGroups == 0 && kBitsSlots % kConvGroups == 0, "bitmap slot -> converter group must be fixed");
+constexpr int kBitsThreads = 32 + 128 * kConvGroups;
+
+template <int BN, int FMT, bool ABITS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ABITS ? kGemmThreads + kBitsThreads : kGemmThreads, 1)
     gemm_hub_pair_tcgen05(const __grid_constant__ StairMaps maps,
                           const __grid_constant__ CUtensorMap map_b,
                           const __grid_constant__ CUtensorMap map_c, const GemmEpi ep,
@@ -527,7 +583,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   constexpr int BH = BN / 2;  // B rows per CTA per term
   constexpr uint32_t A_BYTES = BM * KB_BYTES;
   constexpr uint32_t B_BYTES = BH * KB_BYTES;
+  constexpr uint32_t BITS_BYTES = BM * 8u;  // 128 rows x 64 bits
   constexpr uint32_t STAGE_BYTES = A_BYTES + TERMS * B_BYTES;
+  static_assert(!ABITS || FMT != 2, "bitmap A is a 16-bit operand");
   // Narrow tiles (BN <= 64): the three staged term tiles are one contiguous
   // K-major [3*BH rows] operand, so ONE MMA with N = 3*BN covers all terms
   // (A is read once per k-step instead of three times) and the epilogue adds
@@ -543,13 +601,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t *gbase = smem_raw + (base - raw);
-  const uint32_t bar0 = base + (uint32_t)stages * STAGE_BYTES;
+  // ring addresses: A tile of k-block `it`, B tiles of stage s, bitmap ring
+  constexpr uint32_t B_STRIDE = ABITS ? TERMS * B_BYTES : STAGE_BYTES;
+  const uint32_t b_ring = base + (ABITS ? (uint32_t)kAStages * A_BYTES : A_BYTES);
+  auto a_addr = [&](int it) -> uint32_t {
+    return ABITS ? base + (uint32_t)(it % kAStages) * A_BYTES : base + (uint32_t)(it % stages) * STAGE_BYTES;
+  };
+  auto b_addr = [&](int s) -> uint32_t { return b_ring + (uint32_t)s * B_STRIDE; };
+  const uint32_t bits_base = ABITS ? b_ring + (uint32_t)stages * B_STRIDE : 0u;
+  const uint32_t bar0 = ABITS ? bits_base + (uint32_t)kBitsSlots * BITS_BYTES
+                              : base + (uint32_t)stages * STAGE_BYTES;
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
   auto empty_bar = [&](int s) { return bar0 + 8u * (stages + s); };
   auto tfull_bar = [&](int b) { return bar0 + 8u * (2 * stages + b); };
   auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * stages + 2 + b); };
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + (bar0 - base) + 8u * (2 * stages + 4));
-  const uint32_t stage_c = (bar0 + 8u * (2 * stages + 4) + 16u + 1023u) & ~1023u;
+  const uint32_t xbar0 = bar0 + 8u * (2 * stages + 4) + 16u;
+  auto aready_bar = [&](int a) { return xbar0 + 8u * a; };  // leader: both CTAs' A tiles built
+  auto aempty_bar = [&](int a) { return xbar0 + 8u * (kAStages + a); };  // multicast MMA commit
+  auto bfull_bar = [&](int b) { return xbar0 + 8u * (2 * kAStages + b); };  // own CTA: bitmap landed
+  auto bempty_bar = [&](int b) { return xbar0 + 8u * (2 * kAStages + kBitsSlots + b); };
+  const uint32_t stage_c =
+      (xbar0 + (ABITS ? 8u * (uint32_t)(2 * kAStages + 2 * kBitsSlots) : 0u) + 1023u) & ~1023u;
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -564,6 +637,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const int t_step = sched ? 1 : n_clusters;
   auto item_at = [&](int i) {
     return sched ? __ldg(sarg.items + i) : make_int4(i, 0, -1, -1);
+  };
+  // every (step, k-block) this cluster reduces over, in the order all roles
+  // walk them: fn(mp, st, kb), mp = the pair tile's first rank row
+  auto walk = [&](auto &&fn) {
+    for (int ti = t_begin; ti < t_end; ti += t_step) {
+      const int4 item = item_at(ti);
+      const int mp = (item.x / n_tiles) * (2 * BM);
+      const int g_lo = item.y, g_hi = item.z < 0 ? INT32_MAX : item.z;
+      int g = 0;
+      for (int st = 0; st < sarg.n_steps && g < g_hi; ++st) {
+        if (sarg.rows[st] <= mp) continue;
+        for (int kb = 0; kb < sarg.nkb[st]; ++kb, ++g) {
+          if (g < g_lo) continue;
+          if (g >= g_hi) break;
+          fn(mp, st, kb);
+        }
+      }
+    }
   };
 
   if (warp == 1 && lane == 0) {
@@ -582,6 +673,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull_bar(b), 1);
       mbar_init(tempty_bar(b), 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    }
+    if constexpr (ABITS) {
+      for (int a = 0; a < kAStages; ++a) {
+        mbar_init(aready_bar(a), 8);  // 4 converter warps x 2 CTAs
+        mbar_init(aempty_bar(a), 1);
+      }
+      for (int b = 0; b < kBitsSlots; ++b) {
+        mbar_init(bfull_bar(b), 1);
+        mbar_init(bempty_bar(b), 4);  // the consuming group's 4 warps
+      }
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -617,16 +718,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             const int ph = ((it / stages) & 1) ^ 1;
             ++it;
             mbar_wait(empty_bar(s), ph);
-            const uint32_t sa = base + (uint32_t)s * STAGE_BYTES;
             const uint32_t lbar = mapa_shared(full_bar(s), 0);
             const bool la = !(sarg.dbg & 1) || kb == 0, lb = !(sarg.dbg & 2) || kb == 0;
-            if (leader)
-              mbar_expect_tx(full_bar(s), 2 * ((la ? A_BYTES : 0) + (lb ? TERMS * B_BYTES : 0)));
-            if (la) tma_load_2d_pair(sa, &maps.a[st], lbar, kb * KB_EL, m0);  // rows >= rows[st]: zero fill
+            if constexpr (ABITS) {  // A is built by the converters
+              if (leader) mbar_expect_tx(full_bar(s), 2 * (lb ? TERMS * B_BYTES : 0));
+            } else {
+              if (leader)
+                mbar_expect_tx(full_bar(s), 2 * ((la ? A_BYTES : 0) + (lb ? TERMS * B_BYTES : 0)));
+              if (la) tma_load_2d_pair(a_addr(it - 1), &maps.a[st], lbar, kb * KB_EL, m0);  // rows >= rows[st]: zero fill
+            }
 #pragma unroll
             for (int q = 0; q < TERMS; ++q)
               if (lb)
-                tma_load_2d_pair(sa + A_BYTES + q * B_BYTES, &map_b, lbar, sarg.c0[st] + kb * KB_EL,
+                tma_load_2d_pair(b_addr(s) + q * B_BYTES, &map_b, lbar, sarg.c0[st] + kb * KB_EL,
                                  q * b_rows_per_term + n0);
           }
         }
@@ -649,29 +753,87 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         for (int kb = 0; kb < num_kb; ++kb, ++it) {
           const int s = it % stages;
           mbar_wait(full_bar(s), (it / stages) & 1);
+          // converters of both CTAs wrote A with generic stores: cluster-scope acquire
+          if constexpr (ABITS) mbar_wait_cluster(aready_bar(it % kAStages), (it / kAStages) & 1);
           tc_fence_after();
-          const uint32_t sa = base + (uint32_t)s * STAGE_BYTES;
+          const uint32_t sa = a_addr(it), sb = b_addr(s);
 #pragma unroll
           for (int k = 0; k < KB_BYTES / MMA_K_BYTES; ++k) {
             if (sarg.dbg & 4) break;
             const uint64_t ad = umma_desc_sw128(sa + k * MMA_K_BYTES);
             if constexpr (TSTACK) {
-              const uint64_t bd = umma_desc_sw128(sa + A_BYTES + k * MMA_K_BYTES);
+              const uint64_t bd = umma_desc_sw128(sb + k * MMA_K_BYTES);
               mma_bf16_pair(tmem_d, ad, bd, idesc, (kb | k) != 0);
             } else {
 #pragma unroll
               for (int q = 0; q < TERMS; ++q) {
-                const uint64_t bd = umma_desc_sw128(sa + A_BYTES + q * B_BYTES + k * MMA_K_BYTES);
+                const uint64_t bd = umma_desc_sw128(sb + q * B_BYTES + k * MMA_K_BYTES);
                 if constexpr (FMT == 2) mma_tf32_pair(tmem_d, ad, bd, idesc, (kb | k | q) != 0);
                 else mma_bf16_pair(tmem_d, ad, bd, idesc, (kb | k | q) != 0);
               }
             }
           }
           mma_commit_pair(empty_bar(s));  // frees slot s in both CTAs
+          if constexpr (ABITS) mma_commit_pair(aempty_bar(it % kAStages));
         }
         mma_commit_pair(tfull_bar(acc));  // accumulators of both CTAs complete
       }
     }
+  } else if (ABITS && warp == 6) {  // ---------- bitmap producer (both CTAs) ----------
+    if (lane == 0) {
+      int it = 0;
+      walk([&](int mp, int st, int kb) {
+        const int b = it % kBitsSlots;
+        mbar_wait(bempty_bar(b), ((it / kBitsSlots) & 1) ^ 1);
+        ++it;
+        // this CTA's 128 rows of the k-block's bitmap: 1 KB, contiguous
+        const int rpad = (sarg.rows[st] + 255) & ~255;
+        mbar_expect_tx(bfull_bar(b), BITS_BYTES);
+        bulk_load_1d(bits_base + (uint32_t)b * BITS_BYTES,
+                     sarg.bits[st] + (int64_t)kb * rpad + mp + (int)rank * BM, BITS_BYTES,
+                     bfull_bar(b));
+      });
+    }
+  } else if (ABITS && warp >= 7) {  // ---------- bitmap -> A tile converters (both CTAs) ----------
+    // thread = tile row r: its 64-bit word becomes eight 16-byte chunks of
+    // 16-bit ones/zeros, chunk c stored at (c ^ (r & 7)) — the SWIZZLE_128B
+    // K-major layout TMA would have written
+    const int r = ((warp - 7) & 3) * 32 + lane;
+    const int grp = (warp - 7) >> 2;
+    constexpr uint32_t ONE = FMT == 0 ? 0x3F80u : 0x3C00u;  // bf16 / fp16 1.0
+    int it = 0;
+    walk([&](int, int, int) {
+      const int my = it++;
+      if (my % kConvGroups != grp) return;
+      const int b = my % kBitsSlots, a = my % kAStages;
+      mbar_wait(bfull_bar(b), (my / kBitsSlots) & 1);
+      mbar_wait(aempty_bar(a), ((my / kAStages) & 1) ^ 1);  // the MMA released A slot a
+      const uint32_t sa = a_addr(my);
+      uint64_t w;
+      asm volatile("ld.shared.u64 %0, [%1];"
+                   : "=l"(w)
+                   : "r"(bits_base + (uint32_t)b * BITS_BYTES + (uint32_t)r * 8u)
+                   : "memory");
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (sarg.dbg & 8) break;
+        const uint32_t x = (uint32_t)(w >> (8 * c));
+        uint32_t h[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          h[j] = ((x >> (2 * j)) & 1u) * ONE | ((x >> (2 * j + 1)) & 1u) * (ONE << 16);
+        const uint32_t dst = sa + (uint32_t)r * 128u + (uint32_t)((c ^ (r & 7)) * 16);
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst), "r"(h[0]), "r"(h[1]),
+                     "r"(h[2]), "r"(h[3])
+                     : "memory");
+      }
+      if (!(sarg.dbg & 16)) fence_proxy_async_smem();  // generic-proxy stores -> visible to the MMA
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(bempty_bar(b));
+        mbar_arrive_cluster(mapa_shared(aready_bar(a), 0));
+      }
+    });
   } else {  // ---------------- epilogue warps 2..5 (both CTAs) ----------------
     const int q = warp & 3;
     const bool relu = (ep.flags & GC_RELU) != 0;
@@ -979,12 +1141,13 @@ int make_map(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int6
 // smem: the stage ring, its barriers and (when it fits) the 16 KB epilogue
 // staging for TMA stores; returns the stage count (0: does not fit)
 inline int ring_stages(size_t stage_bytes, bool staging, size_t *smem,
-                       size_t max_ring = 227 * 1024) {
+                       size_t max_ring = 227 * 1024, size_t fixed = 0, int max_st = 8) {
   const size_t cap = 227 * 1024;
-  for (int st = 8; st >= 2; --st) {
+  for (int st = max_st; st >= 2; --st) {
     if ((size_t)st * stage_bytes > max_ring && st > 2) continue;
-    const size_t need = (((size_t)st * stage_bytes + 8 * (2 * st + 4) + 16 + 1023) & ~(size_t)1023) +
-                        (staging ? 4 * 2 * 2048 : 0) + 1024;
+    const size_t need =
+        (((size_t)st * stage_bytes + fixed + 8 * (2 * st + 4) + 16 + 1023) & ~(size_t)1023) +
+        (staging ? 4 * 2 * 2048 : 0) + 1024;
     if (need <= cap) {
       *smem = need;
       return st;
@@ -1074,16 +1237,20 @@ __global__ void hub_splitk_fixup_kernel(const float *__restrict__ ws, const int4
   }
 }
 
-template <int BN, int FMT>
+template <int BN, int FMT, bool ABITS = false>
 int launch_hub_pair(const StairMaps &maps, const StairArgs &sarg, const CUtensorMap &mb,
                     const CUtensorMap &mc, int tma_store, const GemmEpi &ep, int64_t kp,
                     cudaStream_t st, int sched_clusters = 0) {
-  constexpr int stage_bytes = BM * KB_BYTES + fmt_terms(FMT) * (BN / 2) * KB_BYTES;
+  // (bitmap variant: B-only stages + the A and bitmap rings and their barriers)
+  constexpr int stage_bytes = (ABITS ? 0 : BM * KB_BYTES) + fmt_terms(FMT) * (BN / 2) * KB_BYTES;
+  constexpr size_t fixed =
+      ABITS ? (size_t)kAStages * (BM * KB_BYTES + 16) + (size_t)kBitsSlots * (BM * 8 + 16) : 0;
   size_t smem = 0;
-  int stages = tma_store ? ring_stages(stage_bytes, true, &smem) : 0;
+  constexpr int max_st = ABITS ? 12 : 8;
+  int stages = tma_store ? ring_stages(stage_bytes, true, &smem, 227 * 1024, fixed, max_st) : 0;
   if (stages == 0) {
     tma_store = 0;
-    stages = ring_stages(stage_bytes, false, &smem);
+    stages = ring_stages(stage_bytes, false, &smem, 227 * 1024, fixed, max_st);
   }
   if (stages == 0) {
     set_error("gc_hub_gemm: pair tile does not fit shared memory");
@@ -1092,7 +1259,7 @@ int launch_hub_pair(const StairMaps &maps, const StairArgs &sarg, const CUtensor
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(gemm_hub_pair_tcgen05<BN, FMT>,
+    attr_err = cudaFuncSetAttribute(gemm_hub_pair_tcgen05<BN, FMT, ABITS>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   });
   if (attr_err != cudaSuccess) {
@@ -1106,20 +1273,30 @@ int launch_hub_pair(const StairMaps &maps, const StairArgs &sarg, const CUtensor
   // over the clusters, unless the caller passed an LPT schedule
   const int clusters = sched_clusters > 0 ? sched_clusters
                                           : (int)(tiles < sm_count() / 2 ? tiles : sm_count() / 2);
-  gemm_hub_pair_tcgen05<BN, FMT><<<2 * clusters, kGemmThreads, smem, st>>>(
+  gemm_hub_pair_tcgen05<BN, FMT, ABITS><<<2 * clusters, ABITS ? kGemmThreads + kBitsThreads : kGemmThreads,
+                                         smem, st>>>(
       maps, mb, mc, ep, sarg, stages, m_pairs, n_tiles, tma_store, (int)kp);
   return check_launch("gemm_hub_pair_tcgen05");
 }
 
 inline int pair_bn(int64_t K) { return K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256; }
 
-template <int FMT, typename... Args>
+template <int FMT, bool ABITS = false, typename... Args>
 int launch_hub_pair_bn_f(int pbn, Args &&...args) {
   switch (pbn) {
-    case 32: return launch_hub_pair<32, FMT>(args...);
-    case 64: return launch_hub_pair<64, FMT>(args...);
-    case 128: return launch_hub_pair<128, FMT>(args...);
-    default: return launch_hub_pair<256, FMT>(args...);
+    case 32: return launch_hub_pair<32, FMT, ABITS>(args...);
+    case 64: return launch_hub_pair<64, FMT, ABITS>(args...);
+    case 128: return launch_hub_pair<128, FMT, ABITS>(args...);
+    default: return launch_hub_pair<256, FMT, ABITS>(args...);
+  }
+}
+// the staircase with bit-packed A blocks (kind::f16 formats only)
+template <typename... Args>
+int launch_hub_pair_bits(int kfmt, int pbn, Args &&...args) {
+  switch (kfmt) {
+    case 3: return launch_hub_pair_bn_f<3, true>(pbn, args...);
+    case 1: return launch_hub_pair_bn_f<1, true>(pbn, args...);
+    default: return launch_hub_pair_bn_f<0, true>(pbn, args...);
   }
 }
 // kfmt: the kernel's FMT (0 bf16x3, 1 f16x2, 2 tf32, 3 f16) — see kernel_fmt()
@@ -1530,8 +1707,10 @@ extern "C" int gc_hub_stair_gemm(const void *const *A_steps, const int64_t *step
              "gc_hub_stair_gemm: 1..%d steps", kMaxSteps);
   GC_REQUIRE(K >= 1 && T > 0 && T % 64 == 0 && ldc >= K, GC_ERR_SHAPE,
              "gc_hub_stair_gemm: bad shape");
-  GC_REQUIRE((flags & ~(GC_RELU | GC_ACCUMULATE)) == 0, GC_ERR_VALUE,
+  GC_REQUIRE((flags & ~(GC_RELU | GC_ACCUMULATE | GC_HUB_A_BITS)) == 0, GC_ERR_VALUE,
              "gc_hub_stair_gemm: unknown flags 0x%x", flags);
+  const bool abits = (flags & GC_HUB_A_BITS) != 0;
+  flags &= ~GC_HUB_A_BITS;
   GC_REQUIRE(A_steps && step_rows && step_c0 && step_width && Bt && C, GC_ERR_VALUE,
              "gc_hub_stair_gemm: null operand");
   GC_REQUIRE(gc_hub_stair_supported(K), GC_ERR_UNSUPPORTED,
@@ -1568,9 +1747,13 @@ extern "C" int gc_hub_stair_gemm(const void *const *A_steps, const int64_t *step
                GC_ERR_SHAPE, "gc_hub_stair_gemm: steps must be a staircase");
     GC_REQUIRE(A_steps[s] && aligned16(A_steps[s]), GC_ERR_VALUE,
                "gc_hub_stair_gemm: step %d operand", s);
-    int rc = make_map(&maps.a[s], A_steps[s], r, w, w, BM, 64, CU_TENSOR_MAP_SWIZZLE_128B, true,
-                      hub_is_f16(fmt));
-    if (rc) return rc;
+    if (abits) {
+      sarg.bits[s] = static_cast<const uint64_t *>(A_steps[s]);
+    } else {
+      int rc = make_map(&maps.a[s], A_steps[s], r, w, w, BM, 64, CU_TENSOR_MAP_SWIZZLE_128B, true,
+                        hub_is_f16(fmt));
+      if (rc) return rc;
+    }
     sarg.rows[s] = (int)r;
     sarg.c0[s] = (int)c0;
     sarg.nkb[s] = (int)(w / 64);
@@ -1591,8 +1774,10 @@ extern "C" int gc_hub_stair_gemm(const void *const *A_steps, const int64_t *step
   }
   GemmEpi ep{C, ldc, d_row, step_rows[0], K, flags, hub_is_f16(fmt) ? scale_ws + 1 : nullptr};
   cudaStream_t st = as_stream(stream);
-  rc = launch_hub_pair_bn(kernel_fmt(fmt), pbn, maps, sarg, mbp, mc, tma_store, ep, kp, st,
-                          items ? (int)n_clusters : 0);
+  rc = abits ? launch_hub_pair_bits(kernel_fmt(fmt), pbn, maps, sarg, mbp, mc, tma_store, ep, kp,
+                                    st, items ? (int)n_clusters : 0)
+              : launch_hub_pair_bn(kernel_fmt(fmt), pbn, maps, sarg, mbp, mc, tma_store, ep, kp, st,
+                                   items ? (int)n_clusters : 0);
   if (rc || n_fixups == 0) return rc;
   const int n_tiles = (int)((K + pbn - 1) / pbn);
   hub_splitk_fixup_kernel<<<(unsigned)n_fixups, 256, 0, st>>>(

@@ -91,6 +91,10 @@ def term_count(fmt: int | None = None) -> int:
 
 def _block_dtype(fmt: int):
     return torch.bfloat16 if fmt == nat.GC_HUB_BF16X3 else torch.float16
+# staircase blocks as bitmaps (GC_HUB_A_BITS: converter warps expand them in
+# shared memory; 1/16 of the 16-bit blocks' HBM footprint).  Off by default:
+# measured 0.86 vs 0.62 ms on Reddit K=256 — handoff-latency bound (gemm.cu)
+HUB_ABITS = os.environ.get("GNNC_HUB_ABITS", "0") == "1"
 HUB_T_CANDIDATES = (1024, 2048, 4096, 8192)
 # (cell/edge cost ratio δ, balance slack) pairs tried by the autotuner
 # (slack > 1 reaches further right, but short-wide steps stream their B
@@ -230,10 +234,20 @@ class StairPlan(_TailMixin):
         covered = in_cols & (er < r_limits[step])
         self.blocks = []
         self.fmt = _fmt()
+        self.abits = HUB_ABITS
         for s, (R, c0, W) in enumerate(self.steps):
-            blk = torch.zeros(R, W, dtype=_block_dtype(self.fmt), device=dev)
             sel = covered & (step == s)
-            blk[er[sel], ec[sel] - c0] = 1.0
+            if self.abits:
+                # word (k, r) at k * rpad + r; the edges of a row are distinct
+                # columns, so summing their bits is OR-ing them
+                rpad = -(-R // 256) * 256
+                c = ec[sel] - c0
+                blk = torch.zeros((W // 64) * rpad, dtype=torch.int64, device=dev)
+                blk.index_add_(0, (c // 64) * rpad + er[sel],
+                               torch.bitwise_left_shift(torch.ones_like(c), c % 64))
+            else:
+                blk = torch.zeros(R, W, dtype=_block_dtype(self.fmt), device=dev)
+                blk[er[sel], ec[sel] - c0] = 1.0
             self.blocks.append(blk)
         self.cells = sum(R * W for R, _, W in self.steps)
         self._np_rows = np.array([s[0] for s in self.steps], np.int64)
@@ -242,6 +256,18 @@ class StairPlan(_TailMixin):
         self._np_ptrs = np.array([b.data_ptr() for b in self.blocks], np.uint64)
         self._sched: dict = {}
         self._init_tail(a, ~covered, rows)
+
+    def dense_block(self, s: int) -> torch.Tensor:
+        """Step s's 0/1 block as a float [R x W] tensor (either storage)."""
+        R, _, W = self.steps[s]
+        blk = self.blocks[s]
+        if not self.abits:
+            return blk.float()
+        rpad = -(-R // 256) * 256
+        words = blk.view(W // 64, rpad)
+        j = torch.arange(64, device=blk.device)
+        bits = (words.unsqueeze(-1) >> j) & 1  # [k, r, 64]
+        return bits.permute(1, 0, 2).reshape(rpad, W)[:R].float()
 
     def schedule(self, K: int, device):
         """Work items for the staircase GEMM, longest-processing-time first
@@ -427,6 +453,8 @@ def dense_part(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, out: torch.
     if plan.rows0 < a.n_rows and not accumulate:
         out.zero_()  # rows outside every step receive only the tail
     items, starts, n_cl, ws, fx = plan.schedule(K, dev)
+    if plan.abits:
+        flags |= nat.GC_HUB_A_BITS
     nat.check(_timed_call("hub_gemm", dev, lambda: lib.gc_hub_stair_gemm(
         plan._np_ptrs.ctypes.data, plan._np_rows.ctypes.data, plan._np_c0.ctypes.data,
         plan._np_w.ctypes.data, len(plan.steps), plan.row_map.data_ptr(), items.data_ptr(),
@@ -510,7 +538,7 @@ def _candidates(a: CsrMatrix, K: int) -> list:
                 plan = hub_plan(a, spec)
             except ValueError:
                 continue
-            if plan.cells * 2 <= HUB_MEM_BUDGET:
+            if plan.cells * (0.125 if getattr(plan, "abits", False) else 2) <= HUB_MEM_BUDGET:
                 cands.append(spec)
             else:
                 a._plans.pop(("hubsplit", spec), None)

@@ -690,11 +690,14 @@ def stair_pl():
 
 @pytest.mark.parametrize("K", [24, 32, 64, 96, 128, 256, 512])
 @pytest.mark.parametrize("precompute", [False, True])
-def test_stair_split_matches_oracle(oracle, stair_pl, K, precompute):
+@pytest.mark.parametrize("abits", [True, False])
+def test_stair_split_matches_oracle(oracle, stair_pl, K, precompute, abits, monkeypatch):
     """Multi-step staircase (rank-ordered rows scattered by row_map, rows
-    outside every step zero-filled before the tail) vs the oracle."""
+    outside every step zero-filled before the tail) vs the oracle, with the
+    0/1 blocks as bitmaps (expanded in shared memory) or 16-bit tiles."""
     from paper_2306_15155_b200 import _native as nat
     from paper_2306_15155_b200 import hub
+    monkeypatch.setattr(hub, "HUB_ABITS", abits)
     if not nat.load().gc_hub_stair_supported(K):
         pytest.skip("no CTA-pair tile for this K")
     g = gc.NormalizedGraph.from_adjacency(stair_pl).with_precomputed()

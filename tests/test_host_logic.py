@@ -317,12 +317,15 @@ def test_hub_plan_partitions_the_pattern():
         hub.HubPlan(a, 100)
 
 
-def test_stair_plan_partitions_the_pattern():
+@pytest.mark.parametrize("abits", [True, False])
+def test_stair_plan_partitions_the_pattern(abits, monkeypatch):
     """The degree-rank staircase (hub.StairPlan): blocks + tail partition the
     edges, rows shrink along the staircase, block cells are the adjacency of
-    the rank-ordered rows/columns."""
+    the rank-ordered rows/columns — stored as 16-bit blocks or as bitmaps
+    (GC_HUB_A_BITS word layout: word (k, r) at k * rpad + r, zero padding)."""
     from paper_2306_15155_b200 import hub
 
+    monkeypatch.setattr(hub, "HUB_ABITS", abits)
     a = graphs.synthetic_graph("rmat", 6000, 300000, seed=5, device="cpu")
     plan = hub.StairPlan(a, 0.05, n_clusters=1, first_band=256)
     assert len(plan.steps) >= 2
@@ -332,14 +335,21 @@ def test_stair_plan_partitions_the_pattern():
         assert c1 == c0 + w and w % 64 == 0
     dense = a.to_dense()
     cover = torch.zeros_like(dense)
-    for (R, c0, W), blk in zip(plan.steps, plan.blocks):
+    edges = 0
+    for s, (R, c0, W) in enumerate(plan.steps):
+        blk = plan.dense_block(s)
         r_ids = plan.row_map[:R].long()
         c_ids = plan.hub_cols[c0:c0 + W].long()
-        assert torch.equal(blk.float(), dense[r_ids][:, c_ids])
-        cover[r_ids.unsqueeze(1), c_ids.unsqueeze(0)] = blk.float()
+        assert torch.equal(blk, dense[r_ids][:, c_ids])
+        cover[r_ids.unsqueeze(1), c_ids.unsqueeze(0)] = blk
+        edges += int(blk.sum())
+        if abits:  # padding rows R..rpad stay zero
+            rpad = -(-R // 256) * 256
+            words = plan.blocks[s].view(W // 64, rpad)
+            assert plan.blocks[s].dtype == torch.int64 and not bool(words[:, R:].any())
     assert torch.equal(cover + plan.tail.to_dense(), dense)
     assert plan.hub_edges + plan.tail.nnz == a.nnz
-    assert plan.hub_edges == int(sum(b.float().sum() for b in plan.blocks))
+    assert plan.hub_edges == edges
 
 
 def test_host_pipeline_spans_cover_rows_in_order():
