@@ -120,6 +120,15 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// one lane of a converged warp (the same lane every call)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -531,7 +540,9 @@ struct StairArgs {
   const int32_t *cluster_start;
   float *ws;  // [slot][256 rank rows][BN] partial products (rows pre-scaled)
   int dbg;    // experiments only (GNNC_HUB_DBG): 1 = A once per step, 2 = B once, 4 = no MMA,
-              // 8 = converters skip the expansion, 16 = no proxy fence
+              // 8 = converters skip the expansion, 16 = no proxy fence, 32 = no bitmap loads,
+              // 64 = MMA ignores aready, 128 = no A-slot release, 256 = no epilogue stores
+              // (timing only)
 };
 
 __device__ __forceinline__ int stair_kblocks(const StairArgs &sa, int m0) {
@@ -572,7 +583,7 @@ static_assert(kAStages % kConvGroups == 0 && kBitsSlots % kConvGroups == 0, "bit
 constexpr int kBitsThreads = 32 + 128 * kConvGroups;
 
 template <int BN, int FMT, bool ABITS>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ABITS ? kGemmThreads + kBitsThreads : kGemmThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ABITS ? kGemmThreads + kBitsThreads : kGemmThreads + 32, 1)
     gemm_hub_pair_tcgen05(const __grid_constant__ StairMaps maps,
                           const __grid_constant__ CUtensorMap map_b,
                           const __grid_constant__ CUtensorMap map_c, const GemmEpi ep,
@@ -663,11 +674,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ABITS ? kGemmThreads
                    : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
     for (int s = 0; s < stages; ++s) {
-      // leader's arrive.expect_tx (both CTAs' bytes) is the only arrival: the
-      // peer's TMA bytes complete_tx on the leader's barrier, and the peer
-      // cannot refill slot s before the MMA that freed it has consumed this
-      // phase, so its bytes never land in the wrong phase
-      mbar_init(full_bar(s), 1);
+      // the leader's arrive.expect_tx calls (both CTAs' bytes; one per
+      // producer warp) are the only arrivals: the peer's TMA bytes
+      // complete_tx on the leader's barrier, and the peer cannot refill slot
+      // s before the MMA that freed it has consumed this phase, so its bytes
+      // never land in the wrong phase
+      mbar_init(full_bar(s), ABITS ? 1 : 2);  // the leader's A and B producers
       mbar_init(empty_bar(s), 1);  // multicast MMA commit
     }
     for (int b = 0; b < 2; ++b) {
@@ -698,48 +710,71 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ABITS ? kGemmThreads
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer (both CTAs) ----------------
-      int it = 0;
-      for (int ti = t_begin; ti < t_end; ti += t_step) {
-        const int4 item = item_at(ti);
-        const int tile = item.x;
-        const int mp = (tile / n_tiles) * (2 * BM);
-        const int m0 = mp + (int)rank * BM;
-        const int n0 = (tile % n_tiles) * BN + (int)rank * BH;
-        const int g_lo = item.y, g_hi = item.z < 0 ? INT32_MAX : item.z;
-        int g = 0;  // k-block index along the tile's step prefix
-        for (int st = 0; st < sarg.n_steps && g < g_hi; ++st) {
-          if (sarg.rows[st] <= mp) continue;  // pair-uniform: both CTAs load the same steps
-          for (int kb = 0; kb < sarg.nkb[st]; ++kb, ++g) {
-            if (g < g_lo) continue;
-            if (g >= g_hi) break;
-            const int s = it % stages;
-            const int ph = ((it / stages) & 1) ^ 1;
-            ++it;
-            mbar_wait(empty_bar(s), ph);
+  // ---------------- TMA producers (both CTAs, whole warps) ----------------
+  // A tiles (warp 0) and B tiles (warp 6; warp 0 when the converters build A)
+  // stream from separate warps: a producer's per-k-block chain (empty wait,
+  // expect_tx, tensor-map TMA issue) costs several hundred cycles of
+  // mbarrier / TMA latency, and one producer for both operands was the
+  // kernel's pace-setter (profiles/r01n_ncu_summary.md).  The leader's two
+  // arrive.expect_tx are the full barrier's only arrivals (count 2).
+  auto produce = [&](bool doA, bool doB) {
+    const bool issuer = elect_one();
+    int it = 0;
+    for (int ti = t_begin; ti < t_end; ti += t_step) {
+      const int4 item = item_at(ti);
+      const int tile = item.x;
+      const int mp = (tile / n_tiles) * (2 * BM);
+      const int m0 = mp + (int)rank * BM;
+      const int n0 = (tile % n_tiles) * BN + (int)rank * BH;
+      const int g_lo = item.y, g_hi = item.z < 0 ? INT32_MAX : item.z;
+      int g = 0;  // k-block index along the tile's step prefix
+      for (int st = 0; st < sarg.n_steps && g < g_hi; ++st) {
+        if (sarg.rows[st] <= mp) continue;  // pair-uniform: both CTAs load the same steps
+        for (int kb = 0; kb < sarg.nkb[st]; ++kb, ++g) {
+          if (g < g_lo) continue;
+          if (g >= g_hi) break;
+          const int s = it % stages;
+          const int ph = ((it / stages) & 1) ^ 1;
+          ++it;
+          mbar_wait(empty_bar(s), ph);
+          if (issuer) {
             const uint32_t lbar = mapa_shared(full_bar(s), 0);
             const bool la = !(sarg.dbg & 1) || kb == 0, lb = !(sarg.dbg & 2) || kb == 0;
-            if constexpr (ABITS) {  // A is built by the converters
-              if (leader) mbar_expect_tx(full_bar(s), 2 * (lb ? TERMS * B_BYTES : 0));
-            } else {
-              if (leader)
-                mbar_expect_tx(full_bar(s), 2 * ((la ? A_BYTES : 0) + (lb ? TERMS * B_BYTES : 0)));
+            if (doA) {
+              if (leader) mbar_expect_tx(full_bar(s), 2 * (la ? A_BYTES : 0));
               if (la) tma_load_2d_pair(a_addr(it - 1), &maps.a[st], lbar, kb * KB_EL, m0);  // rows >= rows[st]: zero fill
             }
+            if (doB) {
+              if (leader) mbar_expect_tx(full_bar(s), 2 * (lb ? TERMS * B_BYTES : 0));
 #pragma unroll
-            for (int q = 0; q < TERMS; ++q)
-              if (lb)
-                tma_load_2d_pair(b_addr(s) + q * B_BYTES, &map_b, lbar, sarg.c0[st] + kb * KB_EL,
-                                 q * b_rows_per_term + n0);
+              for (int q = 0; q < TERMS; ++q)
+                if (lb)
+                  tma_load_2d_pair(b_addr(s) + q * B_BYTES, &map_b, lbar, sarg.c0[st] + kb * KB_EL,
+                                   q * b_rows_per_term + n0);
+            }
           }
+          __syncwarp();
         }
       }
     }
+  };
+
+  if (warp == 0) {
+    produce(!ABITS, ABITS);
+  } else if (!ABITS && warp == 6) {
+    produce(false, true);
   } else if (warp == 1) {
-    if (lane == 0 && leader) {  // ---------------- MMA issuer (leader only) ----------------
+    // ---------------- MMA issuer (leader CTA, whole warp) ----------------
+    // The loop runs warp-uniform so descriptors and TMEM addresses live in
+    // uniform registers; one elected lane issues the MMAs and their commits
+    // (a commit tracks the MMAs of the thread that issues it).  With a single
+    // divergent lane every MMA cost a waterfall (ELECT / R2UR / BRA.U.ANY,
+    // ~110 instructions per k-block) and the issue loop, not the tensor pipe,
+    // set the pace (ncu: full barrier never waited on, tensor pipe 65 % busy).
+    if (leader) {
       constexpr uint32_t idesc = FMT == 2 ? idesc_tf32_m256(ACC_N)
                                  : FMT ? idesc_f16_m256(ACC_N) : idesc_bf16_m256(ACC_N);  // 1, 3: fp16
+      const bool issuer = elect_one();
       int it = 0, lt = 0;
       for (int ti = t_begin; ti < t_end; ti += t_step, ++lt) {
         const int4 item = item_at(ti);
@@ -754,29 +789,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ABITS ? kGemmThreads
           const int s = it % stages;
           mbar_wait(full_bar(s), (it / stages) & 1);
           // converters of both CTAs wrote A with generic stores: cluster-scope acquire
-          if constexpr (ABITS) mbar_wait_cluster(aready_bar(it % kAStages), (it / kAStages) & 1);
+          if constexpr (ABITS)
+            if (!(sarg.dbg & 64)) mbar_wait_cluster(aready_bar(it % kAStages), (it / kAStages) & 1);
           tc_fence_after();
-          const uint32_t sa = a_addr(it), sb = b_addr(s);
+          // descriptor of k-step k = base + k * (32 B >> 4) in the start-address field
+          const uint64_t ad0 = umma_desc_sw128(a_addr(it)), bd0 = umma_desc_sw128(b_addr(s));
+          if (issuer && !(sarg.dbg & 4)) {
 #pragma unroll
-          for (int k = 0; k < KB_BYTES / MMA_K_BYTES; ++k) {
-            if (sarg.dbg & 4) break;
-            const uint64_t ad = umma_desc_sw128(sa + k * MMA_K_BYTES);
-            if constexpr (TSTACK) {
-              const uint64_t bd = umma_desc_sw128(sb + k * MMA_K_BYTES);
-              mma_bf16_pair(tmem_d, ad, bd, idesc, (kb | k) != 0);
-            } else {
+            for (int k = 0; k < KB_BYTES / MMA_K_BYTES; ++k) {
+              const uint64_t ad = ad0 + (uint64_t)(k * (MMA_K_BYTES >> 4));
+              if constexpr (TSTACK) {
+                mma_bf16_pair(tmem_d, ad, bd0 + (uint64_t)(k * (MMA_K_BYTES >> 4)), idesc, (kb | k) != 0);
+              } else {
 #pragma unroll
-              for (int q = 0; q < TERMS; ++q) {
-                const uint64_t bd = umma_desc_sw128(sb + q * B_BYTES + k * MMA_K_BYTES);
-                if constexpr (FMT == 2) mma_tf32_pair(tmem_d, ad, bd, idesc, (kb | k | q) != 0);
-                else mma_bf16_pair(tmem_d, ad, bd, idesc, (kb | k | q) != 0);
+                for (int q = 0; q < TERMS; ++q) {
+                  const uint64_t bd = bd0 + (uint64_t)((q * B_BYTES + k * MMA_K_BYTES) >> 4);
+                  if constexpr (FMT == 2) mma_tf32_pair(tmem_d, ad, bd, idesc, (kb | k | q) != 0);
+                  else mma_bf16_pair(tmem_d, ad, bd, idesc, (kb | k | q) != 0);
+                }
               }
             }
           }
-          mma_commit_pair(empty_bar(s));  // frees slot s in both CTAs
-          if constexpr (ABITS) mma_commit_pair(aempty_bar(it % kAStages));
+          if (issuer) {
+            mma_commit_pair(empty_bar(s));  // frees slot s in both CTAs
+            if constexpr (ABITS)
+              if (!(sarg.dbg & 128)) mma_commit_pair(aempty_bar(it % kAStages));
+          }
+          __syncwarp();
         }
-        mma_commit_pair(tfull_bar(acc));  // accumulators of both CTAs complete
+        if (issuer) mma_commit_pair(tfull_bar(acc));  // accumulators of both CTAs complete
+        __syncwarp();
       }
     }
   } else if (ABITS && warp == 6) {  // ---------- bitmap producer (both CTAs) ----------
@@ -788,6 +830,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ABITS ? kGemmThreads
         ++it;
         // this CTA's 128 rows of the k-block's bitmap: 1 KB, contiguous
         const int rpad = (sarg.rows[st] + 255) & ~255;
+        if (sarg.dbg & 32) {  // experiment: no bitmap traffic
+          mbar_arrive(bfull_bar(b));
+          return;
+        }
         mbar_expect_tx(bfull_bar(b), BITS_BYTES);
         bulk_load_1d(bits_base + (uint32_t)b * BITS_BYTES,
                      sarg.bits[st] + (int64_t)kb * rpad + mp + (int)rank * BM, BITS_BYTES,
@@ -807,7 +853,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ABITS ? kGemmThreads
       if (my % kConvGroups != grp) return;
       const int b = my % kBitsSlots, a = my % kAStages;
       mbar_wait(bfull_bar(b), (my / kBitsSlots) & 1);
-      mbar_wait(aempty_bar(a), ((my / kAStages) & 1) ^ 1);  // the MMA released A slot a
+      if (!(sarg.dbg & 128)) mbar_wait(aempty_bar(a), ((my / kAStages) & 1) ^ 1);  // the MMA released A slot a
       const uint32_t sa = a_addr(my);
       uint64_t w;
       asm volatile("ld.shared.u64 %0, [%1];"
@@ -879,6 +925,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ABITS ? kGemmThreads
         for (int i = 0; i < 16; ++i) {
           v[i] *= rs;
           if (relu && !accum) v[i] = fmaxf(v[i], 0.0f);
+        }
+        if (sarg.dbg & 256) {  // experiment: no epilogue stores
+          if (v[0] == 12345.678f) crow[0] = v[1];
+          continue;
         }
         if (slot >= 0) {  // split-K partial: rank-row-major workspace tile, fixed up later
           if (row_ok) {
@@ -1246,7 +1296,11 @@ int launch_hub_pair(const StairMaps &maps, const StairArgs &sarg, const CUtensor
   constexpr size_t fixed =
       ABITS ? (size_t)kAStages * (BM * KB_BYTES + 16) + (size_t)kBitsSlots * (BM * 8 + 16) : 0;
   size_t smem = 0;
-  constexpr int max_st = ABITS ? 12 : 8;
+  static const int stage_cap = [] {  // GNNC_HUB_STAGES caps the ring (experiments)
+    const char *e = getenv("GNNC_HUB_STAGES");
+    return e ? atoi(e) : 0;
+  }();
+  const int max_st = stage_cap >= 2 ? stage_cap : ABITS ? 12 : 8;
   int stages = tma_store ? ring_stages(stage_bytes, true, &smem, 227 * 1024, fixed, max_st) : 0;
   if (stages == 0) {
     tma_store = 0;
@@ -1273,7 +1327,7 @@ int launch_hub_pair(const StairMaps &maps, const StairArgs &sarg, const CUtensor
   // over the clusters, unless the caller passed an LPT schedule
   const int clusters = sched_clusters > 0 ? sched_clusters
                                           : (int)(tiles < sm_count() / 2 ? tiles : sm_count() / 2);
-  gemm_hub_pair_tcgen05<BN, FMT, ABITS><<<2 * clusters, ABITS ? kGemmThreads + kBitsThreads : kGemmThreads,
+  gemm_hub_pair_tcgen05<BN, FMT, ABITS><<<2 * clusters, ABITS ? kGemmThreads + kBitsThreads : kGemmThreads + 32,
                                          smem, st>>>(
       maps, mb, mc, ep, sarg, stages, m_pairs, n_tiles, tma_store, (int)kp);
   return check_launch("gemm_hub_pair_tcgen05");
