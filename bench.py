@@ -415,6 +415,10 @@ def main():
                     "dense_edges": plan.hub_edges, "flops_per_launch": flops,
                     "steps": getattr(plan, "steps", None),
                     "terms": hubmod.FORMAT_NAMES[hubmod.term_format()],
+                    # the other roof: the 0/1 blocks stream from HBM once per launch
+                    "block_bytes": int(plan.cells * (0.125 if getattr(plan, "abits", False) else 2)),
+                    "block_hbm_frac": round(plan.cells * (0.125 if getattr(plan, "abits", False) else 2)
+                                            / (hub_ms * 1e-3) / 1e9 / pk["hbm_gbs"], 3),
                     "model": "2·cells·K per 16-bit term (f16: 1 term, TF32-equivalent 11-bit rounding of D·X; "
                              "f16x2: 2 terms, 22-bit split; bf16x3: 3 terms, exact)"}
     elif spmm_ms:

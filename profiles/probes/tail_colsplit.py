@@ -11,7 +11,7 @@ K = int(sys.argv[1]) if len(sys.argv) > 1 else 256
 g = gc.NormalizedGraph.from_adjacency(graphs.shape_graph("reddit", device=dev))
 a, d = g.a_tilde, g.d_inv_sqrt.to(dev)
 x = torch.rand(a.n_rows, K, device=dev) - 0.5
-spec = ("stair", 18, 10)
+spec = hub._parse_spec(sys.argv[2]) if len(sys.argv) > 2 else ("stair", 18, 10)
 plan = hub.hub_plan(a, spec)
 tail = plan.tail
 out = torch.zeros(a.n_rows, K, device=dev)
