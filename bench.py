@@ -445,6 +445,12 @@ def main():
         "config": {"workload": f"gcn_layer/{args.shape}/k1=k2={K}", "shape": args.shape, "n": n,
                    "nnz_A": shape.nnz, "m_tilde": m, "K": K, "composition": comp,
                    "selected_by": selected_by, "gemm_precision": gc.get_gemm_precision(),
+                   "numerics": ("fp32 accumulation everywhere; the update GEMM rounds its inputs to "
+                                "TF32 and the dense part of the aggregation rounds D*X to one fp16 "
+                                "term (the same 11-bit input rounding); the SpMM tail gathers fp32; "
+                                "parity vs the fp64 oracle stated in 'parity' (tol 1e-2)")
+                   if gc.get_gemm_precision() == "tf32" else
+                   "fp32 CUDA-core GEMM, two-term fp16 dense aggregation operand; tol 1e-4",
                    "l2": "inputs larger than L2 (CSR 0.9 GB, H 0.24 GB at K=256); no flush",
                    "parallelism": (f"row-partition x{world}, 1 all-gather/layer"
                                    f"{'' if args.no_overlap else ' overlapped with the owned-column SpMM'}")
