@@ -231,6 +231,10 @@ GNNC_API int gc_attn_sddmm_f32(const int32_t *row_ptr, const int32_t *col_idx, c
  *   GC_HUB_F16:    the hi fp16 term alone — 11 significant bits, the same
  *                  input rounding as a TF32 GEMM (for the 1e-2 parity mode
  *                  the TF32 update already runs in); 1/3 of the MMAs.
+ *   GC_HUB_F16_MN: GC_HUB_F16 packed MN-major: Bt is fp16[T][Kp], the
+ *                  gathered rows as they are (no transpose); requires
+ *                  gc_hub_f16_mn_supported(K) (CTA pairs, K > 64) and
+ *                  16-bit A blocks.
  * The 0/1 blocks are bf16 (BF16X3) or fp16 (F16X2, F16) — exact either way.  The
  * remaining edges are the ordinary SpMM launched with GC_ACCUMULATE on top.
  *
@@ -247,6 +251,7 @@ GNNC_API int gc_attn_sddmm_f32(const int32_t *row_ptr, const int32_t *col_idx, c
 #define GC_HUB_BF16X3 0
 #define GC_HUB_F16X2 1
 #define GC_HUB_F16 2
+#define GC_HUB_F16_MN 3
 GNNC_API int64_t gc_hub_terms_rows(int64_t K);
 GNNC_API int gc_hub_pack(const float *X, int64_t ldx, int64_t K, const int32_t *hub_cols,
                 int64_t T, const float *d_col, int32_t fmt, void *Bt, float *scale_ws,
@@ -278,6 +283,7 @@ GNNC_API int gc_hub_gemm(const void *A_hub, int64_t lda, int64_t n_rows, int64_t
  * padding rows zero), bit j = A_s[r, 64k + j]; converter warps expand each
  * 128 x 64 tile into the 16-bit operand in shared memory (16x fewer A bytes). */
 GNNC_API int gc_hub_stair_supported(int64_t K);
+GNNC_API int gc_hub_f16_mn_supported(int64_t K);
 GNNC_API int gc_hub_stair_pair_bn(int64_t K);
 GNNC_API int gc_hub_stair_gemm(const void *const *A_steps, const int64_t *step_rows,
                 const int64_t *step_c0, const int64_t *step_width, int32_t n_steps,

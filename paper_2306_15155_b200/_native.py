@@ -19,6 +19,7 @@ GC_ACCUMULATE = 1 << 1
 GC_HUB_BF16X3 = 0
 GC_HUB_F16X2 = 1
 GC_HUB_F16 = 2
+GC_HUB_F16_MN = 3
 GC_HUB_A_BITS = 1 << 6
 GC_HUB_TAGGED = 1 << 2
 
@@ -81,6 +82,7 @@ _SIGNATURES = {
     "gc_hub_gemm": (ctypes.c_int, [_P, _I64, _I64, _I64, _P, _I64, _I32, _P, _P, _I64, _P, _U32,
                                    _P]),
     "gc_hub_stair_supported": (ctypes.c_int, [_I64]),
+    "gc_hub_f16_mn_supported": (ctypes.c_int, [_I64]),
     "gc_hub_stair_pair_bn": (ctypes.c_int, [_I64]),
     "gc_hub_stair_gemm": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P, _P, _P, _I32, _P, _P, _I32, _P,
                                          _I64, _I64, _I32, _P, _P, _I64, _P, _U32, _P]),

@@ -148,6 +148,19 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
   return d;
 }
 
+// MN-major SWIZZLE_128B operand (16-bit): 64-element MN rows of 128 B, 8-row
+// (K) atoms of 1 KB at SBO = 1 KB, MN blocks of 64 elements at LBO = lbo bytes
+// (the layout a 2-D TMA box {64 MN, rows K} with SWIZZLE_128B writes).
+__device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t saddr, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
 // Instruction descriptor: D = F32, A = B = TF32, both K-major, M = 128, N = n.
 __host__ __device__ constexpr uint32_t idesc_tf32(int n) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((128u >> 4) << 24);
@@ -474,6 +487,15 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap
       "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap *map,
+                                                 uint32_t leader_bar, int32_t c0, int32_t c1,
+                                                 int32_t c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
 __device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                               uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -556,7 +578,7 @@ __device__ __forceinline__ int stair_kblocks(const StairArgs &sa, int m0) {
 // (22 significant bits, absolute error <= 2^-23 max|D·X|), 2/3 of the MMAs;
 // 2: one fp32 operand pair on kind::tf32 (the dense update H·W on CTA pairs);
 // 3: one fp16 term of s·D·X (11 significant bits: TF32's input rounding).
-constexpr int fmt_terms(int fmt) { return fmt == 2 || fmt == 3 ? 1 : fmt == 1 ? 2 : 3; }
+constexpr int fmt_terms(int fmt) { return fmt >= 2 ? 1 : fmt == 1 ? 2 : 3; }
 
 // ABITS: the 0/1 A blocks arrive as bitmaps (1 KB per 128 x 64 k-block tile
 // instead of 16 KB) and converter warps expand them into the SWIZZLE_128B
@@ -597,6 +619,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ABITS ? kGemmThreads
   constexpr uint32_t BITS_BYTES = BM * 8u;  // 128 rows x 64 bits
   constexpr uint32_t STAGE_BYTES = A_BYTES + TERMS * B_BYTES;
   static_assert(!ABITS || FMT != 2, "bitmap A is a 16-bit operand");
+  // FMT 4: one fp16 term with B MN-major ([T][Kp] rows as packed, no
+  // transpose): BH/64 TMA boxes of 64 features x 64 hub rows per stage
+  constexpr bool MNB = FMT == 4;
+  static_assert(!MNB || BH % 64 == 0, "MN-major B needs 64-element blocks per CTA");
   // Narrow tiles (BN <= 64): the three staged term tiles are one contiguous
   // K-major [3*BH rows] operand, so ONE MMA with N = 3*BN covers all terms
   // (A is read once per k-step instead of three times) and the epilogue adds
@@ -746,11 +772,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ABITS ? kGemmThreads
             }
             if (doB) {
               if (leader) mbar_expect_tx(full_bar(s), 2 * (lb ? TERMS * B_BYTES : 0));
+              if (MNB) {  // one 3-D box: BH/64 feature blocks of 64 hub rows
+                if (lb) tma_load_3d_pair(b_addr(s), &map_b, lbar, 0, sarg.c0[st] + kb * KB_EL, n0 / 64);
+              } else {
 #pragma unroll
-              for (int q = 0; q < TERMS; ++q)
-                if (lb)
-                  tma_load_2d_pair(b_addr(s) + q * B_BYTES, &map_b, lbar, sarg.c0[st] + kb * KB_EL,
-                                   q * b_rows_per_term + n0);
+                for (int q = 0; q < TERMS; ++q)
+                  if (lb)
+                    tma_load_2d_pair(b_addr(s) + q * B_BYTES, &map_b, lbar, sarg.c0[st] + kb * KB_EL,
+                                     q * b_rows_per_term + n0);
+              }
             }
           }
           __syncwarp();
@@ -773,6 +803,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ABITS ? kGemmThreads
     // set the pace (ncu: full barrier never waited on, tensor pipe 65 % busy).
     if (leader) {
       constexpr uint32_t idesc = FMT == 2 ? idesc_tf32_m256(ACC_N)
+                                 : FMT == 4 ? idesc_f16_m256(ACC_N) | (1u << 16)  // B MN-major
                                  : FMT ? idesc_f16_m256(ACC_N) : idesc_bf16_m256(ACC_N);  // 1, 3: fp16
       const bool issuer = elect_one();
       int it = 0, lt = 0;
@@ -793,7 +824,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ABITS ? kGemmThreads
             if (!(sarg.dbg & 64)) mbar_wait_cluster(aready_bar(it % kAStages), (it / kAStages) & 1);
           tc_fence_after();
           // descriptor of k-step k = base + k * (32 B >> 4) in the start-address field
-          const uint64_t ad0 = umma_desc_sw128(a_addr(it)), bd0 = umma_desc_sw128(b_addr(s));
+          const uint64_t ad0 = umma_desc_sw128(a_addr(it));
+          // MN-major B: k-step k starts 16 rows (2 KB) further; K-major: 32 B further
+          const uint64_t bd0 = MNB ? umma_desc_sw128_mn(b_addr(s), 8192) : umma_desc_sw128(b_addr(s));
           if (issuer && !(sarg.dbg & 4)) {
 #pragma unroll
             for (int k = 0; k < KB_BYTES / MMA_K_BYTES; ++k) {
@@ -803,7 +836,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ABITS ? kGemmThreads
               } else {
 #pragma unroll
                 for (int q = 0; q < TERMS; ++q) {
-                  const uint64_t bd = bd0 + (uint64_t)((q * B_BYTES + k * MMA_K_BYTES) >> 4);
+                  const uint64_t bd = MNB ? bd0 + (uint64_t)((k * 16 * 128) >> 4)
+                                          : bd0 + (uint64_t)((q * B_BYTES + k * MMA_K_BYTES) >> 4);
                   if constexpr (FMT == 2) mma_tf32_pair(tmem_d, ad, bd, idesc, (kb | k | q) != 0);
                   else mma_bf16_pair(tmem_d, ad, bd, idesc, (kb | k | q) != 0);
                 }
@@ -1188,6 +1222,30 @@ int make_map(CUtensorMap *map, const void *ptr, int64_t rows, int64_t cols, int6
   return GC_OK;
 }
 
+// MN-major B for the one-term pair GEMM: fp16 Bm[T][kp] viewed as
+// {64 features, T rows, kp/64 feature blocks} so ONE box {64, 64, nblk}
+// lands nblk 8 KB SWIZZLE_128B blocks (the MN blocks of the descriptor, LBO
+// 8 KB apart) per stage
+int make_map_mn(CUtensorMap *map, const void *ptr, int64_t T, int64_t kp, int nblk) {
+  auto enc = get_encode_fn();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return GC_ERR_CUDA;
+  }
+  cuuint64_t dims[3] = {64, (cuuint64_t)T, (cuuint64_t)(kp / 64)};
+  cuuint64_t strides[2] = {(cuuint64_t)(kp * 2), 128};
+  cuuint32_t box[3] = {64, 64, (cuuint32_t)nblk};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void *>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (MN-major B) failed (%d)", (int)r);
+    return GC_ERR_CUDA;
+  }
+  return GC_OK;
+}
+
 // smem: the stage ring, its barriers and (when it fits) the 16 KB epilogue
 // staging for TMA stores; returns the stage count (0: does not fit)
 inline int ring_stages(size_t stage_bytes, bool staging, size_t *smem,
@@ -1359,6 +1417,7 @@ int launch_hub_pair_bn(int kfmt, int pbn, Args &&...args) {
   switch (kfmt) {
     case 2: return launch_hub_pair_bn_f<2>(pbn, args...);
     case 3: return launch_hub_pair_bn_f<3>(pbn, args...);
+    case 4: return pbn >= 256 ? launch_hub_pair<256, 4>(args...) : launch_hub_pair<128, 4>(args...);
     case 1: return launch_hub_pair_bn_f<1>(pbn, args...);
     default: return launch_hub_pair_bn_f<0>(pbn, args...);
   }
@@ -1375,11 +1434,15 @@ int launch_hub_bn_f(int bn, Args &&...args) {
 }
 
 // ABI term format (GC_HUB_*) -> kernel FMT, term count, 16-bit element kind
-inline int kernel_fmt(int32_t fmt) { return fmt == GC_HUB_F16 ? 3 : fmt == GC_HUB_F16X2 ? 1 : 0; }
-inline int hub_terms(int32_t fmt) { return fmt == GC_HUB_F16 ? 1 : fmt == GC_HUB_F16X2 ? 2 : 3; }
-inline bool hub_is_f16(int32_t fmt) { return fmt == GC_HUB_F16 || fmt == GC_HUB_F16X2; }
+inline int kernel_fmt(int32_t fmt) {
+  return fmt == GC_HUB_F16_MN ? 4 : fmt == GC_HUB_F16 ? 3 : fmt == GC_HUB_F16X2 ? 1 : 0;
+}
+inline int hub_terms(int32_t fmt) {
+  return (fmt == GC_HUB_F16 || fmt == GC_HUB_F16_MN) ? 1 : fmt == GC_HUB_F16X2 ? 2 : 3;
+}
+inline bool hub_is_f16(int32_t fmt) { return fmt != GC_HUB_BF16X3; }
 inline bool hub_fmt_ok(int32_t fmt) {
-  return fmt == GC_HUB_BF16X3 || fmt == GC_HUB_F16X2 || fmt == GC_HUB_F16;
+  return fmt == GC_HUB_BF16X3 || fmt == GC_HUB_F16X2 || fmt == GC_HUB_F16 || fmt == GC_HUB_F16_MN;
 }
 
 inline bool gemm_pair_enabled() {  // GNNC_GEMM_PAIR=0: TF32 GEMM on single CTAs
@@ -1503,6 +1566,43 @@ __global__ void __launch_bounds__(256)
       const __half l0 = __float2half_rn(y0 - __half2float(h0));
       const __half l1 = __float2half_rn(y1 - __half2float(h1));
       *reinterpret_cast<__half2 *>(Bt + (kp + f) * T + t) = __halves2half2(l0, l1);
+    }
+  }
+}
+
+// One fp16 term of s·x, rows as gathered ([T][kp], features contiguous: the
+// MN-major B operand, no transpose).  Warp per hub row, 8 features per lane
+// per pass (two float4 loads, one 16-byte store); features >= K are zero.
+__global__ void __launch_bounds__(256)
+    hub_pack_f16_mn_kernel(const float *__restrict__ X, int64_t ldx, int64_t K,
+                           const int32_t *__restrict__ hub_cols, int64_t T,
+                           const float *__restrict__ d, int64_t kp,
+                           const unsigned *__restrict__ amax, float *__restrict__ inv_scale,
+                           __half *__restrict__ Bm, int vec) {
+  const float mx = __uint_as_float(*amax);
+  const int e = mx > 0.0f ? ilogbf(mx) : 0;
+  const float sc = ldexpf(1.0f, 13 - e);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *inv_scale = ldexpf(1.0f, e - 13);
+  const int lane = threadIdx.x % 32;
+  const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; t < T; t += n_warps) {
+    const int64_t j = __ldg(hub_cols + t);
+    const float *row = X + j * ldx;
+    const float s = d ? __ldg(d + j) * sc : sc;
+    for (int64_t f = 8 * lane; f < kp; f += 256) {
+      float v[8];
+      if (vec && f + 8 <= K) {
+        const float4 a = __ldg(reinterpret_cast<const float4 *>(row + f));
+        const float4 b = __ldg(reinterpret_cast<const float4 *>(row + f + 4));
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = f + i < K ? __ldg(row + f + i) : 0.0f;
+      }
+      __half2 h[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(v[2 * i] * s, v[2 * i + 1] * s);
+      *reinterpret_cast<uint4 *>(Bm + t * kp + f) = *reinterpret_cast<const uint4 *>(h);
     }
   }
 }
@@ -1670,6 +1770,14 @@ extern "C" int gc_hub_pack(const float *X, int64_t ldx, int64_t K, const int32_t
   hub_absmax_kernel<<<(unsigned)blocks, 256, 0, st>>>(X, ldx, K, hub_cols, T, d_col, amax);
   int rc = check_launch("hub_absmax_kernel");
   if (rc) return rc;
+  if (fmt == GC_HUB_F16_MN) {
+    GC_REQUIRE(aligned16(Bt) && kp % 8 == 0, GC_ERR_UNSUPPORTED, "gc_hub_pack: Bt alignment");
+    const int vec = (ldx % 4 == 0 && aligned16(X)) ? 1 : 0;
+    const int64_t nb = std::min<int64_t>((T + 7) / 8, (int64_t)sm_count() * 16);
+    hub_pack_f16_mn_kernel<<<(unsigned)nb, 256, 0, st>>>(X, ldx, K, hub_cols, T, d_col, kp, amax,
+                                                         scale_ws + 1, static_cast<__half *>(Bt), vec);
+    return check_launch("hub_pack_f16_mn_kernel");
+  }
   if (fmt == GC_HUB_F16)
     hub_pack_f16_kernel<1><<<grid, dim3(32, 8), 0, st>>>(X, ldx, K, hub_cols, T, d_col, kp, amax,
                                                          scale_ws + 1, static_cast<__half *>(Bt));
@@ -1712,13 +1820,17 @@ extern "C" int gc_hub_gemm(const void *A_hub, int64_t lda, int64_t n_rows, int64
     rc = make_map(&mc, C, n_rows, K, ldc, 32, 16, CU_TENSOR_MAP_SWIZZLE_64B);
     if (rc) return rc;
   }
+  GC_REQUIRE(fmt != GC_HUB_F16_MN || gc_hub_f16_mn_supported(K), GC_ERR_UNSUPPORTED,
+             "gc_hub_gemm: GC_HUB_F16_MN needs gc_hub_f16_mn_supported(K)");
   if (hub_pair_enabled() && K > 16 && kp % pair_bn(K) == 0) {
     // CTA pairs: N = pair_bn, each CTA stages pair_bn/2 rows of each B term;
     // the plain hub block is a one-step staircase
     const int pbn = pair_bn(K);
     CUtensorMap mbp;
-    rc = make_map(&mbp, Bt, terms * kp, T, T, pbn / 2, 64, CU_TENSOR_MAP_SWIZZLE_128B, true,
-                  hub_is_f16(fmt));
+    rc = fmt == GC_HUB_F16_MN
+             ? make_map_mn(&mbp, Bt, T, kp, pbn / 128)
+             : make_map(&mbp, Bt, terms * kp, T, T, pbn / 2, 64, CU_TENSOR_MAP_SWIZZLE_128B, true,
+                        hub_is_f16(fmt));
     if (rc) return rc;
     StairMaps maps;
     memset(&maps, 0, sizeof(maps));
@@ -1742,6 +1854,12 @@ extern "C" int gc_hub_gemm(const void *A_hub, int64_t lda, int64_t n_rows, int64
 }
 
 extern "C" int gc_hub_stair_pair_bn(int64_t K) { return K > 0 ? pair_bn(K) : 0; }
+
+extern "C" int gc_hub_f16_mn_supported(int64_t K) {
+  return (hub_pair_enabled() && K > 64 && gc_hub_terms_rows(K) % pair_bn(K) == 0 &&
+          gc_hub_terms_rows(K) % 8 == 0)
+             ? 1 : 0;
+}
 
 extern "C" int gc_hub_stair_supported(int64_t K) {
   return (hub_pair_enabled() && K > 16 && gc_hub_terms_rows(K) % pair_bn(K) == 0) ? 1 : 0;
@@ -1814,9 +1932,13 @@ extern "C" int gc_hub_stair_gemm(const void *const *A_steps, const int64_t *step
   }
   const int64_t kp = gc_hub_terms_rows(K);
   const int pbn = pair_bn(K);
+  GC_REQUIRE(fmt != GC_HUB_F16_MN || (gc_hub_f16_mn_supported(K) && !abits), GC_ERR_UNSUPPORTED,
+             "gc_hub_stair_gemm: GC_HUB_F16_MN needs gc_hub_f16_mn_supported(K) and 16-bit blocks");
   CUtensorMap mbp, mc;
-  int rc = make_map(&mbp, Bt, hub_terms(fmt) * kp, T, T, pbn / 2, 64,
-                    CU_TENSOR_MAP_SWIZZLE_128B, true, hub_is_f16(fmt));
+  int rc = fmt == GC_HUB_F16_MN
+               ? make_map_mn(&mbp, Bt, T, kp, pbn / 128)
+               : make_map(&mbp, Bt, hub_terms(fmt) * kp, T, T, pbn / 2, 64,
+                          CU_TENSOR_MAP_SWIZZLE_128B, true, hub_is_f16(fmt));
   if (rc) return rc;
   memset(&mc, 0, sizeof(mc));
   // rank-ordered rows scatter through row_map: direct stores

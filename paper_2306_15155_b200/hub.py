@@ -63,8 +63,9 @@ HUB_SPLIT = os.environ.get("GNNC_HUB_SPLIT", "auto")
 # staircase 0.58 vs 0.80 ms, normwise difference from the plain SpMM 2.8e-6
 # either way) or "bf16x3" (exact fp32 split)
 HUB_FORMAT = os.environ.get("GNNC_HUB_FORMAT", "auto")
-_TERMS = {nat.GC_HUB_F16: 1, nat.GC_HUB_F16X2: 2, nat.GC_HUB_BF16X3: 3}
-FORMAT_NAMES = {nat.GC_HUB_F16: "f16", nat.GC_HUB_F16X2: "f16x2", nat.GC_HUB_BF16X3: "bf16x3"}
+_TERMS = {nat.GC_HUB_F16: 1, nat.GC_HUB_F16_MN: 1, nat.GC_HUB_F16X2: 2, nat.GC_HUB_BF16X3: 3}
+FORMAT_NAMES = {nat.GC_HUB_F16: "f16", nat.GC_HUB_F16_MN: "f16", nat.GC_HUB_F16X2: "f16x2",
+                nat.GC_HUB_BF16X3: "bf16x3"}
 
 
 def _fmt() -> int:
@@ -420,6 +421,9 @@ def pack(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec):
     K = x.shape[1]
     kp = int(lib.gc_hub_terms_rows(K))
     fmt = term_format(plan.fmt)
+    if fmt == nat.GC_HUB_F16 and not getattr(plan, "abits", False) \
+            and lib.gc_hub_f16_mn_supported(K):
+        fmt = nat.GC_HUB_F16_MN  # rows as gathered: no transpose in the pack
     bt = torch.empty(_TERMS[fmt] * kp * plan.T, dtype=_block_dtype(fmt), device=x.device)
     sc = torch.empty(2, dtype=torch.float32, device=x.device)
     nat.check(lib.gc_hub_pack(x.data_ptr(), _ld(x), K, plan.hub_cols.data_ptr(), plan.T,

@@ -573,16 +573,19 @@ def hub_pl():
 
 @pytest.mark.parametrize("K", [1, 7, 16, 32, 100, 256, 300, 512])
 @pytest.mark.parametrize("T", [64, 128])
-@pytest.mark.parametrize("fmt", ["bf16x3", "f16x2", "f16"])
+@pytest.mark.parametrize("fmt", ["bf16x3", "f16x2", "f16", "f16mn"])
 def test_hub_gemm_term_split(oracle, K, T, fmt):
     """Dense 0/1 block times the packed terms of D·X: bf16x3 is the exact fp32
     split (1e-6 normwise with rows spanning six decades), f16x2 carries 22
     significant bits relative to max|D·X| (absolute error <= 2^-23 max), f16
     11 (TF32's input rounding: 1e-3 normwise here)."""
     from paper_2306_15155_b200 import _native as nat
-    f = {"f16x2": nat.GC_HUB_F16X2, "f16": nat.GC_HUB_F16, "bf16x3": nat.GC_HUB_BF16X3}[fmt]
+    f = {"f16x2": nat.GC_HUB_F16X2, "f16": nat.GC_HUB_F16, "f16mn": nat.GC_HUB_F16_MN,
+         "bf16x3": nat.GC_HUB_BF16X3}[fmt]
+    if fmt == "f16mn" and not nat.load().gc_hub_f16_mn_supported(K):
+        pytest.skip("MN-major one-term operand needs CTA pairs and K > 64")
     dt = torch.bfloat16 if fmt == "bf16x3" else torch.float16
-    terms = {"f16x2": 2, "f16": 1, "bf16x3": 3}[fmt]
+    terms = {"f16x2": 2, "f16": 1, "f16mn": 1, "bf16x3": 3}[fmt]
     rng = np.random.default_rng(K * 7 + T)
     n, ncols = 777, 3000
     a_hub = (rng.random((n, T)) < 0.3).astype(np.float32)
@@ -605,7 +608,7 @@ def test_hub_gemm_term_split(oracle, K, T, fmt):
                               out.data_ptr(), K, drt.data_ptr(), 0, st), "gemm")
     ref = dr.astype(np.float64)[:, None] * (a_hub.astype(np.float64) @ (
         x.astype(np.float64)[hub_cols] * d.astype(np.float64)[hub_cols][:, None]))
-    assert oracle.rel_err(out.cpu().numpy(), ref) < (1e-3 if fmt == "f16" else 1e-6)
+    assert oracle.rel_err(out.cpu().numpy(), ref) < (1e-3 if fmt in ("f16", "f16mn") else 1e-6)
 
 
 @pytest.mark.parametrize("K", [3, 32, 256])
