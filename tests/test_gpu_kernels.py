@@ -759,6 +759,35 @@ def test_host_pipelined_layer_with_stair_split(oracle, stair_pl, monkeypatch):
     assert any(("hubsplit", ("stair", 50, 10)) in b._plans for b in blocks)
 
 
+def test_host_pipelined_stair_split_tf32_mode(oracle, stair_pl, monkeypatch):
+    """The bench's e2e configuration: TF32 mode (one-term MN-major dense
+    operand on every row block), pinned host H, row-block pipeline; layer
+    parity in the TF32 class (1e-2, measured ~1e-3)."""
+    from paper_2306_15155_b200 import gcn as gcn_mod
+    from paper_2306_15155_b200 import hub
+    g = gc.NormalizedGraph.from_adjacency(stair_pl).with_precomputed()
+    monkeypatch.setattr(hub, "HUB_SPLIT", "stair:50:10")
+    monkeypatch.setattr(hub, "STAIR_FIRST_BAND", 256)
+    monkeypatch.setattr(gcn_mod, "HOST_PIPELINE_BLOCKS", 3)
+    og = oracle.GcnGraph.from_adjacency(to_oracle(oracle, stair_pl))
+    rng = np.random.default_rng(12)
+    h = f32(rng.uniform(-0.5, 0.5, (stair_pl.n_rows, 256)))
+    w = f32(rng.uniform(-0.5, 0.5, (256, 256)))
+    assert gc.get_gemm_precision() == "tf32"
+    for comp, order in (("dynamic", "update_first"), ("precompute", "aggregate_first")):
+        spec_l = gc.GcnLayerSpec(256, 256, w, composition=comp, order=order)
+        out = gc.gcn_layer(g, torch.from_numpy(h).pin_memory(), spec_l)
+        dev_out = gc.gcn_layer(g, torch.from_numpy(h).to(DEV), spec_l).cpu()
+        ref = oracle.gcn_layer(og, h.astype(np.float64), w.astype(np.float64), comp, order)
+        assert oracle.rel_err(out.numpy(), ref) <= 1e-2
+        assert oracle.rel_err(dev_out.numpy(), ref) <= 1e-2
+    blocks = list(g.__dict__.get("_unit_block_cache", {}).values()) + \
+        [b for (_, _, b) in sum(g.__dict__.get("_row_block_cache", {}).values(), [])]
+    assert any(("hubsplit", ("stair", 50, 10)) in b._plans for b in blocks)
+    from paper_2306_15155_b200 import _native as nat
+    assert nat.load().gc_hub_f16_mn_supported(256)
+
+
 def test_stair_split_on_rectangular_block(oracle, stair_pl):
     """A row block of Ã (local rows x all columns, as a rank's remote pass or an
     e2e row block sees it) through the staircase with separate d_row / d_col."""
