@@ -127,6 +127,20 @@ GNNC_API int gc_gat_aggregate_f32(const int32_t *row_ptr, const int32_t *col_idx
                                   const int32_t *split_rows, int64_t n_split_rows, void *workspace,
                                   size_t ws_bytes, void *stream);
 
+/* Multi-head form (A16 in one pass over col_idx): B rows
+ * hold heads * head_dim features, head h owning columns [h*head_dim,
+ * (h+1)*head_dim); s and t are head-major [heads][n_rows] / [heads][n_cols];
+ * each head has its own LeakyReLU score and online softmax.  Equal to heads
+ * gc_gat_aggregate_f32 calls on the column blocks.  heads <= 8.  Split plans
+ * need workspace for [n_slots][K] partials + [n_slots][heads] (max, sum)
+ * pairs.                                                                   */
+GNNC_API int gc_gat_aggregate_mh_f32(const int32_t *row_ptr, const int32_t *col_idx,
+                const float *s, const float *t, int32_t heads, int64_t head_dim, float slope,
+                const float *B, int64_t ldb, int64_t n_rows, int64_t n_cols, float *C,
+                int64_t ldc, uint32_t flags, int algo, const int32_t *items, int64_t n_items,
+                const int32_t *split_rows, int64_t n_split_rows, void *workspace,
+                size_t ws_bytes, void *stream);
+
 /* col_tagged[p] = col_idx[p] | (hot[col_idx[p]] ? 1<<31 : 0): a copy of the
  * pattern whose hub columns (hot: uint8 per column) are tagged for
  * GC_HUB_TAGGED launches.  The untagged col_idx stays valid for every other

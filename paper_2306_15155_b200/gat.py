@@ -45,10 +45,20 @@ from .sparse import (
     _require_cuda,
     _stream,
     gat_aggregate,
+    gat_aggregate_mh,
     gemm,
     relu_,
     spmm,
 )
+
+# reuse/reassoc with heads > 1: one fused pass per head (default) or all heads
+# in one pass over the pattern (GNNC_GAT_MH=1, gat_aggregate_mh).  Measured
+# (profiles/probes/gat_mh.py): one pass is 1.1-1.6x SLOWER on B200 — each
+# per-head pass gathers a k2-wide slice of HW that stays L2-resident, while
+# the one-pass row is heads*k2 wide (4x the L2 working set) and carries
+# per-head softmax state in registers; the shared col_idx read it saves is
+# 4 bytes per edge against 4*k2 gathered
+MULTIHEAD_ONE_PASS = __import__("os").environ.get("GNNC_GAT_MH", "0") == "1"
 
 
 class GatComposition(str, Enum):
@@ -242,6 +252,11 @@ def gat_layer_reuse(a_tilde: CsrMatrix, h, spec: GatLayerSpec, *, spmm_fn=None):
     if a_tilde.n_rows != a_tilde.n_cols:
         raise ShapeError("attention expects a square adjacency")
     s, t = _projections(hw, spec, spec.attn_src.to(hw.device), spec.attn_dst.to(hw.device), k2, k2)
+    if H > 1 and MULTIHEAD_ONE_PASS:
+        # all heads in one pass over the pattern (one col_idx read, per-head
+        # online softmax in the same lane group)
+        gat_aggregate_mh(a_tilde, s, t, spec.leaky_slope, hw, H, relu=relu, out=out)
+        return op.wrap(out)
     for i in range(H):
         gat_aggregate(a_tilde, s[i], t[i], spec.leaky_slope, hw[:, i * k2:(i + 1) * k2], relu=relu,
                       out=out[:, i * k2:(i + 1) * k2])

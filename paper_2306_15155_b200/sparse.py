@@ -501,7 +501,7 @@ def _sm_count(dev: torch.device) -> int:
     return torch.cuda.get_device_properties(dev).multi_processor_count
 
 
-def _plan_args(a: CsrMatrix, K: int, algo: str, dev, gat: bool = False):
+def _plan_args(a: CsrMatrix, K: int, algo: str, dev, gat: bool = False, heads: int = 1):
     """(code, items, n_items, split, n_split, workspace) for one launch."""
     chunk = SPLIT_CHUNK or int(nat.load().gc_spmm_default_chunk(a.n_rows, a.nnz, K, _sm_count(dev)))
     use_split = algo == "split" or (algo == "auto" and a.nnz and (
@@ -511,7 +511,7 @@ def _plan_args(a: CsrMatrix, K: int, algo: str, dev, gat: bool = False):
     items, split, n_slots = a.spmm_plan(chunk)
     ws = None
     if n_slots:
-        per_slot = K + (2 if gat else 0)  # partial row (+ (max, sum) pair for GAT)
+        per_slot = K + (2 * heads if gat else 0)  # partial row (+ (max, sum) per GAT head)
         ws = torch.empty(n_slots * per_slot + (2 if gat else 0), dtype=torch.float32, device=dev)
     return nat.GC_SPMM_NNZ_SPLIT, items, items.shape[0], split, split.shape[0], ws
 
@@ -689,6 +689,50 @@ def gat_aggregate(a: CsrMatrix, s: torch.Tensor, t: torch.Tensor, slope: float, 
     extra = (nat.GC_HUB_TAGGED if hints else 0) | nat.GC_SPMM_SHRINK(shrink)
     rc = _timed_call("spmm", dev, lambda: launch(cols, extra))
     nat.check(rc, "gat_aggregate")
+    return op.wrap(out)
+
+
+def gat_aggregate_mh(a: CsrMatrix, s: torch.Tensor, t: torch.Tensor, slope: float, b, heads: int,
+                     *, relu: bool = False, out=None, algo: str = "auto"):
+    """Multi-head fused GAT aggregation in one pass over the pattern: ``b`` is
+    n_cols x (heads*k2) (head h in column block h), ``s`` / ``t`` are
+    [heads, n_rows] / [heads, n_cols]; equal to ``heads`` ``gat_aggregate``
+    calls on the column blocks (A16 of SURVEY.md §8(a), N1 of §8(f))."""
+    dev = a.device
+    op = _Operand(b, dev)
+    bt = op.t
+    if a.n_cols != bt.shape[0]:
+        raise ShapeError(f"gat_aggregate_mh: a is {a.n_rows}x{a.n_cols}, b has {bt.shape[0]} rows")
+    K = bt.shape[1]
+    if heads < 1 or K % heads:
+        raise ShapeError("gat_aggregate_mh: b's width must be heads * k2")
+    if tuple(s.shape) != (heads, a.n_rows) or tuple(t.shape) != (heads, a.n_cols) \
+            or not (s.is_contiguous() and t.is_contiguous()):
+        raise ShapeError("gat_aggregate_mh: s/t must be contiguous [heads, n] score arrays")
+    _require_cuda(a.col_idx, bt, s, t)
+    if out is None:
+        out = torch.empty(a.n_rows, K, dtype=torch.float32, device=dev)
+    elif tuple(out.shape) != (a.n_rows, K) or out.stride(1) != 1:
+        raise ShapeError(f"gat_aggregate_mh: out must be a row-major {a.n_rows}x{K} tensor")
+    code, items, n_items, split, n_split, ws = _plan_args(a, K, algo, dev, gat=True, heads=heads)
+    lib = nat.load()
+    flags = nat.GC_RELU if relu else 0
+
+    def launch(cols, extra, dst=out):
+        return lib.gc_gat_aggregate_mh_f32(
+            a.row_ptr.data_ptr(), cols.data_ptr(), s.data_ptr(), t.data_ptr(), int(heads),
+            K // heads, float(slope), bt.data_ptr(), _ld(bt), a.n_rows, a.n_cols, dst.data_ptr(),
+            _ld(dst), flags | extra, code, _ptr(items), n_items, _ptr(split), n_split, _ptr(ws),
+            0 if ws is None else ws.numel() * 4, _stream(dev))
+
+    def probe(cols, extra):
+        nat.check(launch(cols, extra), "gat_aggregate_mh")  # writes `out`; the real launch follows
+
+    hints, shrink = _variant(a, K, "gatmh", probe)
+    cols = a.hub_tagged_cols(K) if hints else a.col_idx
+    extra = (nat.GC_HUB_TAGGED if hints else 0) | nat.GC_SPMM_SHRINK(shrink)
+    rc = _timed_call("spmm", dev, lambda: launch(cols, extra))
+    nat.check(rc, "gat_aggregate_mh")
     return op.wrap(out)
 
 

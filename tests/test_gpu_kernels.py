@@ -821,3 +821,23 @@ def test_gcsr_load_to_device_and_partition(tmp_path, oracle):
     rp = a.row_ptr.cpu().numpy().astype(np.int64)
     for parts in (2, 3, 8):
         assert np.array_equal(partition_rows_device(b.row_ptr, parts), oracle.partition_rows(rp, parts))
+
+
+@pytest.mark.parametrize("heads,k2", [(2, 16), (3, 24), (4, 32), (4, 64), (8, 32), (4, 256)])
+@pytest.mark.parametrize("algo", ["row", "split"])
+def test_gat_aggregate_multihead_one_pass(hubgraph, heads, k2, algo):
+    """gat_aggregate_mh (all heads in one pass over the pattern, per-head
+    online softmax; split plans merge per-head (max, sum) pairs) equals one
+    fused aggregation per head on the column blocks."""
+    from paper_2306_15155_b200.sparse import gat_aggregate, gat_aggregate_mh
+    rng = np.random.default_rng(heads * 7 + k2)
+    n = hubgraph.n_rows
+    hw = torch.from_numpy(f32(rng.standard_normal((n, heads * k2)))).to(DEV)
+    s = torch.from_numpy(f32(rng.standard_normal((heads, n)))).to(DEV)
+    t = torch.from_numpy(f32(rng.standard_normal((heads, n)))).to(DEV)
+    out = gat_aggregate_mh(hubgraph, s, t, 0.2, hw, heads, relu=True, algo=algo)
+    for hd in range(heads):
+        ref = gat_aggregate(hubgraph, s[hd], t[hd], 0.2, hw[:, hd * k2:(hd + 1) * k2].contiguous(),
+                            relu=True, algo=algo)
+        got = out[:, hd * k2:(hd + 1) * k2]
+        assert torch.allclose(got, ref, rtol=2e-5, atol=2e-6), (hd, float((got - ref).abs().max()))
