@@ -56,6 +56,26 @@ __device__ __forceinline__ int64_t row_of_edge(const int32_t *__restrict__ row_p
   return lo;
 }
 
+// Rows of a step's 32 consecutive edges: lane k holds the end of row
+// r0 + k (row_ptr[r0 + 1 + k]); an edge's row offset is the number of those
+// ends <= its index, found by a 5-step binary search over the lanes with
+// shuffles — no dependent global loads per row crossing.  Returns 32 when
+// the 32-row window does not reach the edge (runs of empty rows).
+__device__ __forceinline__ int row_offset_in_window(int bk, int p) {
+  int cnt = 0;
+#pragma unroll
+  for (int step = 16; step > 0; step >>= 1) {
+    const int b = __shfl_sync(0xffffffffu, bk, cnt + step - 1);
+    if (b <= p) cnt += step;
+  }
+  const int b31 = __shfl_sync(0xffffffffu, bk, 31);  // (all lanes: full-mask shuffle)
+  if (cnt == 31 && b31 <= p) cnt = 32;  // the window ends before p: caller walks on
+  return cnt;
+}
+
+// LONG (mean degree >= 128): a step that stays inside the current row skips
+// the window (most steps on dense graphs); short rows always search.
+template <bool LONG>
 __global__ void __launch_bounds__(kThreads)
     sddmm_norm_kernel(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col_idx,
                       const float *__restrict__ a_vals, const float *__restrict__ d,
@@ -65,19 +85,30 @@ __global__ void __launch_bounds__(kThreads)
   const int64_t p0 = w * chunk;
   if (p0 >= nnz) return;
   const int64_t p1 = min(nnz, p0 + chunk);
-  int64_t row = row_of_edge(row_ptr, n_rows, p0);  // warp-uniform search
-  int64_t rend = __ldg(row_ptr + row + 1);
-  int64_t p = p0 + lane;
-  while (p < p1 && p >= rend) rend = __ldg(row_ptr + (++row) + 1);
-  float di = __ldg(d + row);
-  for (; p < p1; p += 32) {
-    if (p >= rend) {
-      do rend = __ldg(row_ptr + (++row) + 1);
-      while (p >= rend);
-      di = __ldg(d + row);
+  int64_t r0 = row_of_edge(row_ptr, n_rows, p0);  // warp-uniform search, once per chunk
+  int64_t rend0 = __ldg(row_ptr + r0 + 1);          // end of row r0 (warp-uniform)
+  for (int64_t base = p0; base < p1; base += 32) {
+    const int64_t p = base + lane;
+    const bool ok = p < p1;
+    const int j = ok ? ldg_stream_i32(col_idx + p) : 0;
+    const float av = (a_vals && ok) ? ldg_stream_f32(a_vals + p) : 1.0f;
+    int64_t row = r0;
+    if (!LONG || min(base + 31, p1 - 1) >= rend0) {  // the step crosses a row end (warp-uniform)
+      const int64_t rk = r0 + 1 + lane;
+      const int bk = rk <= n_rows ? __ldg(row_ptr + rk) : INT32_MAX;
+      const int64_t pc = min(p, p1 - 1);  // idle lanes take the last edge's row
+      const int off = row_offset_in_window(bk, (int)pc);
+      row = r0 + off;
+      if (off == 32) {  // > 31 row ends within the step (runs of empty rows): walk
+        int64_t rend = __ldg(row_ptr + row + 1);
+        while (pc >= rend) rend = __ldg(row_ptr + (++row) + 1);
+      }
+      const int off31 = __shfl_sync(0xffffffffu, off, 31);
+      r0 = __shfl_sync(0xffffffffu, row, 31);  // row of the step's last edge
+      const int be = __shfl_sync(0xffffffffu, bk, off31 & 31);
+      rend0 = off31 < 32 ? be : __ldg(row_ptr + r0 + 1);
     }
-    const float prod = di * __ldg(d + ldg_stream_i32(col_idx + p));
-    out[p] = (a_vals ? ldg_stream_f32(a_vals + p) : 1.0f) * prod;
+    if (ok) out[p] = av * (__ldg(d + row) * __ldg(d + j));
   }
 }
 
@@ -447,8 +478,12 @@ extern "C" int gc_sddmm_norm_f32(const int32_t *row_ptr, const int32_t *col_idx,
   const int64_t warps = (nnz + chunk - 1) / chunk;
   const int64_t blocks = (warps + (kThreads / 32) - 1) / (kThreads / 32);
   GC_REQUIRE(blocks < INT32_MAX, GC_ERR_SHAPE, "gc_sddmm_norm_f32: too many edges");
-  sddmm_norm_kernel<<<(unsigned)blocks, kThreads, 0, as_stream(stream)>>>(
-      row_ptr, col_idx, a_vals, d, n_rows, nnz, chunk, out_vals);
+  if (nnz >= 128 * n_rows)
+    sddmm_norm_kernel<true><<<(unsigned)blocks, kThreads, 0, as_stream(stream)>>>(
+        row_ptr, col_idx, a_vals, d, n_rows, nnz, chunk, out_vals);
+  else
+    sddmm_norm_kernel<false><<<(unsigned)blocks, kThreads, 0, as_stream(stream)>>>(
+        row_ptr, col_idx, a_vals, d, n_rows, nnz, chunk, out_vals);
   return check_launch("sddmm_norm_kernel");
 }
 
