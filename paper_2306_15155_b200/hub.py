@@ -433,6 +433,9 @@ def pack(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec):
     return bt, sc, fmt
 
 
+_SIDE_STREAMS: dict = {}
+
+
 def dense_part(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, out: torch.Tensor, *,
                d_row: torch.Tensor, accumulate: bool = False, packed=None,
                rows: tuple[int, int] | None = None) -> None:
@@ -442,6 +445,19 @@ def dense_part(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, out: torch.
     lib = nat.load()
     st = _stream(dev)
     K = x.shape[1]
+    zero_done = None
+    if plan.kind == "stair" and plan.rows0 < a.n_rows and not accumulate \
+            and (rows is None or tuple(rows) == (0, a.n_rows)):
+        # rows outside every step receive only the tail: zero them on a side
+        # stream while the operand is packed (independent memory)
+        main = torch.cuda.current_stream(dev)
+        side = _SIDE_STREAMS.setdefault(dev, torch.cuda.Stream(dev))
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            out.zero_()
+        out.record_stream(side)
+        zero_done = torch.cuda.Event()
+        zero_done.record(side)
     bt, sc, fmt = packed if packed is not None else pack(a, x, d, spec)
     flags = nat.GC_ACCUMULATE if accumulate else 0
     if plan.kind == "block":
@@ -454,8 +470,8 @@ def dense_part(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, out: torch.
         return
     if rows is not None and tuple(rows) != (0, a.n_rows):
         raise ShapeError("stair split: the dense part covers all rows (rank-ordered tiles)")
-    if plan.rows0 < a.n_rows and not accumulate:
-        out.zero_()  # rows outside every step receive only the tail
+    if zero_done is not None:
+        torch.cuda.current_stream(dev).wait_event(zero_done)
     items, starts, n_cl, ws, fx = plan.schedule(K, dev)
     if plan.abits:
         flags |= nat.GC_HUB_A_BITS
