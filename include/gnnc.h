@@ -296,6 +296,12 @@ GNNC_API int gc_hub_gemm(const void *A_hub, int64_t lda, int64_t n_rows, int64_t
  * (k, r) at index k * rpad_s + r (rpad_s = step_rows[s] rounded up to 256,
  * padding rows zero), bit j = A_s[r, 64k + j]; converter warps expand each
  * 128 x 64 tile into the 16-bit operand in shared memory (16x fewer A bytes). */
+/* Join of the concurrent form (hub.py): the staircase GEMM wrote its
+ * rank-ordered rows to G (row_map = NULL, d_row in rank order) while the tail
+ * SpMM wrote C for every row; C[i] = relu?(C[i] + G[rank[i]]) for rank[i] <
+ * rows0, relu?(C[i]) otherwise (flags: GC_RELU).                          */
+GNNC_API int gc_hub_merge_rows(const float *G, int64_t ldg, int64_t rows0, const int32_t *rank,
+                float *C, int64_t ldc, int64_t n_rows, int64_t K, uint32_t flags, void *stream);
 GNNC_API int gc_hub_stair_supported(int64_t K);
 GNNC_API int gc_hub_f16_mn_supported(int64_t K);
 GNNC_API int gc_hub_stair_pair_bn(int64_t K);

@@ -434,6 +434,11 @@ def pack(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec):
 
 
 _SIDE_STREAMS: dict = {}
+# "1": the staircase GEMM on a side stream concurrently with the tail SpMM
+# (joined by gc_hub_merge_rows).  Off by default: measured 2.21 vs 1.94 ms on
+# Reddit K=256 — the persistent GEMM holds every SM (one 220 KB CTA each), so
+# the tail does not overlap it and the join pass is pure overhead
+HUB_CONCURRENT = os.environ.get("GNNC_HUB_CONCURRENT", "0") == "1"
 
 
 def dense_part(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, out: torch.Tensor, *,
@@ -472,16 +477,80 @@ def dense_part(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, out: torch.
         raise ShapeError("stair split: the dense part covers all rows (rank-ordered tiles)")
     if zero_done is not None:
         torch.cuda.current_stream(dev).wait_event(zero_done)
+    _stair_gemm(plan, K, (bt, sc, fmt), out, d_row, flags, rank_order=False)
+
+
+def _stair_gemm(plan, K: int, packed, out: torch.Tensor, d_row: torch.Tensor, flags: int, *,
+                rank_order: bool) -> None:
+    """One staircase launch: rows scattered through the degree permutation into
+    ``out`` (n rows), or with ``rank_order`` written in rank order to ``out``
+    (rows0 rows) with ``d_row`` already in rank order."""
+    bt, sc, fmt = packed
+    dev = out.device
+    lib = nat.load()
+    st = _stream(dev)
     items, starts, n_cl, ws, fx = plan.schedule(K, dev)
     if plan.abits:
         flags |= nat.GC_HUB_A_BITS
+    row_map = None if rank_order else plan.row_map.data_ptr()
     nat.check(_timed_call("hub_gemm", dev, lambda: lib.gc_hub_stair_gemm(
         plan._np_ptrs.ctypes.data, plan._np_rows.ctypes.data, plan._np_c0.ctypes.data,
-        plan._np_w.ctypes.data, len(plan.steps), plan.row_map.data_ptr(), items.data_ptr(),
+        plan._np_w.ctypes.data, len(plan.steps), row_map, items.data_ptr(),
         starts.data_ptr(), n_cl, None if ws is None else ws.data_ptr(),
         None if fx is None else fx.data_ptr(), 0 if fx is None else fx.shape[0], bt.data_ptr(),
         plan.T, K, fmt, sc.data_ptr(), out.data_ptr(), _ld(out), d_row.data_ptr(), flags,
         st)), "hub_stair_gemm")
+
+
+def _rank_tables(plan, d_row: torch.Tensor):
+    """(rank int32[n]: row -> degree rank, d_row in rank order for the first
+    rows0 ranks), cached on the plan per d_row tensor."""
+    if getattr(plan, "_rank", None) is None:
+        rank = torch.empty_like(plan.row_map)
+        rank[plan.row_map.long()] = torch.arange(plan.row_map.numel(), dtype=torch.int32,
+                                                 device=plan.row_map.device)
+        plan._rank = rank
+    key = (d_row.data_ptr(), d_row._version, d_row.numel())
+    cache = getattr(plan, "_d_rank", None)
+    if cache is None or cache[0] != key:
+        plan._d_rank = (key, d_row[plan.row_map[:plan.rows0].long()].contiguous())
+    return plan._rank, plan._d_rank[1]
+
+
+def _concurrent_aggregate(a: CsrMatrix, x: torch.Tensor, d, spec, out: torch.Tensor, *,
+                          d_row: torch.Tensor, values, relu: bool, packed) -> None:
+    """The staircase GEMM (side stream, rank-ordered rows into a scratch G)
+    runs concurrently with the tail SpMM (writing every row of ``out``); a
+    join kernel adds G through the rank table and applies ReLU.  The GEMM
+    streams its 0/1 blocks from HBM while the tail is bound by L2 gathers, so
+    the two overlap; the tail also stops reading ``out`` back."""
+    plan = hub_plan(a, spec)
+    dev = x.device
+    K = x.shape[1]
+    rank, d_rank = _rank_tables(plan, d_row)
+    main = torch.cuda.current_stream(dev)
+    side = _SIDE_STREAMS.setdefault(dev, torch.cuda.Stream(dev))
+    g = torch.empty(plan.rows0, K, dtype=torch.float32, device=dev)
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        pk = packed if packed is not None else pack(a, x, d, spec)
+        _stair_gemm(plan, K, pk, g, d_rank, 0, rank_order=True)
+    g.record_stream(side)
+    for t in pk[:2]:
+        t.record_stream(side)
+    tail = plan.tail_block(values, 0, a.n_rows)
+    if values is None:
+        _spmm(tail, x, weighted=False, d_row=d_row, d_col=d, relu=False, out=out,
+              accumulate=False, timer="spmm_tail")
+    else:
+        _spmm(tail, x, weighted=True, relu=False, out=out, accumulate=False, timer="spmm_tail")
+    done = torch.cuda.Event()
+    done.record(side)
+    main.wait_event(done)
+    nat.check(nat.load().gc_hub_merge_rows(g.data_ptr(), _ld(g), plan.rows0, rank.data_ptr(),
+                                           out.data_ptr(), _ld(out), a.n_rows, K,
+                                           nat.GC_RELU if relu else 0, _stream(dev)),
+              "hub_merge_rows")
 
 
 def tail_part(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, out: torch.Tensor, *,
@@ -527,7 +596,15 @@ def hybrid_aggregate(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, *,
     elif tuple(out.shape) != (hi - lo, K) or out.stride(1) != 1:
         raise ShapeError(f"hybrid_aggregate: out must be a row-major {hi - lo}x{K} tensor")
 
+    plan = hub_plan(a, spec)
+    concurrent = (HUB_CONCURRENT and plan.kind == "stair" and not accumulate
+                  and (rows is None or tuple(rows) == (0, a.n_rows)))
+
     def run():
+        if concurrent:
+            _concurrent_aggregate(a, x, d, spec, out, d_row=d_row, values=values, relu=relu,
+                                  packed=packed)
+            return 0
         dense_part(a, x, d, spec, out, d_row=d_row, accumulate=accumulate, packed=packed,
                    rows=rows)
         tail_part(a, x, d, spec, out, d_row=d_row, values=values, relu=relu, rows=rows)

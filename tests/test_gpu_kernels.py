@@ -759,6 +759,26 @@ def test_host_pipelined_layer_with_stair_split(oracle, stair_pl, monkeypatch):
     assert any(("hubsplit", ("stair", 50, 10)) in b._plans for b in blocks)
 
 
+@pytest.mark.parametrize("relu", [True, False])
+def test_stair_split_concurrent_join(oracle, stair_pl, relu, monkeypatch):
+    """Opt-in concurrent form: staircase GEMM into rank-ordered scratch on a
+    side stream, tail SpMM writing every row, gc_hub_merge_rows join."""
+    from paper_2306_15155_b200 import hub
+    monkeypatch.setattr(hub, "HUB_CONCURRENT", True)
+    g = gc.NormalizedGraph.from_adjacency(stair_pl).with_precomputed()
+    a = g.a_tilde
+    spec = ("stair", 50, 10)
+    a._plans[("hubsplit", spec)] = hub.StairPlan(a, 0.05, n_clusters=1, first_band=256)
+    og = oracle.GcnGraph.from_adjacency(to_oracle(oracle, stair_pl))
+    rng = np.random.default_rng(21)
+    x = f32(rng.uniform(-0.5, 0.5, (a.n_rows, 128)))
+    d = g.d_inv_sqrt.to(DEV)
+    out = hub.hybrid_aggregate(a, torch.from_numpy(x).to(DEV), d, spec, relu=relu)
+    ref = oracle.spmm(og.n_tilde, x)
+    ref = np.maximum(ref, 0) if relu else ref
+    assert oracle.rel_err(out.cpu().numpy(), ref) < hub_tol()
+
+
 def test_host_pipelined_stair_split_tf32_mode(oracle, stair_pl, monkeypatch):
     """The bench's e2e configuration: TF32 mode (one-term MN-major dense
     operand on every row block), pinned host H, row-block pipeline; layer
