@@ -327,8 +327,10 @@ class CsrMatrix:
         Truncated or foreign files raise ``ShapeError``; the CSR invariants
         are checked on the device unless ``validate=False``."""
         dev = torch.device(device) if device is not None else default_device()
+        if os.path.getsize(path) < 64:
+            raise ShapeError(f"{path}: not a .gcsr file (shorter than its header)")
         raw = np.memmap(path, dtype=np.uint8, mode="r")
-        if raw.size < 64 or bytes(raw[:4]) != cls.GCSR_MAGIC:
+        if bytes(raw[:4]) != cls.GCSR_MAGIC:
             raise ShapeError(f"{path}: not a .gcsr file")
         version = int(raw[4:8].view("<u4")[0])
         if version != cls.GCSR_VERSION:

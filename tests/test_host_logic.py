@@ -413,6 +413,9 @@ def test_gcsr_rejects_bad_files(tmp_path):
     (tmp_path / "trunc.gcsr").write_bytes(raw[:-70])
     with pytest.raises(gc.ShapeError):
         gc.CsrMatrix.load(tmp_path / "trunc.gcsr", device=CPU)
+    (tmp_path / "empty.gcsr").write_bytes(b"")
+    with pytest.raises(gc.ShapeError):
+        gc.CsrMatrix.load(tmp_path / "empty.gcsr", device=CPU)
     (tmp_path / "foreign.gcsr").write_bytes(b"%%MatrixMarket" + raw[14:])
     with pytest.raises(gc.ShapeError):
         gc.CsrMatrix.load(tmp_path / "foreign.gcsr", device=CPU)
