@@ -302,6 +302,10 @@ GNNC_API int gc_hub_gemm(const void *A_hub, int64_t lda, int64_t n_rows, int64_t
  * rows0, relu?(C[i]) otherwise (flags: GC_RELU).                          */
 GNNC_API int gc_hub_merge_rows(const float *G, int64_t ldg, int64_t rows0, const int32_t *rank,
                 float *C, int64_t ldc, int64_t n_rows, int64_t K, uint32_t flags, void *stream);
+/* C[rows[i], :K] = 0 for i < n_rows (the rows outside every staircase step,
+ * zeroed before the tail accumulates).                                    */
+GNNC_API int gc_zero_rows(float *C, int64_t ldc, const int32_t *rows, int64_t n_rows, int64_t K,
+                void *stream);
 GNNC_API int gc_hub_stair_supported(int64_t K);
 GNNC_API int gc_hub_f16_mn_supported(int64_t K);
 GNNC_API int gc_hub_stair_pair_bn(int64_t K);

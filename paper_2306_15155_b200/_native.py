@@ -87,6 +87,7 @@ _SIGNATURES = {
     "gc_hub_stair_supported": (ctypes.c_int, [_I64]),
     "gc_hub_f16_mn_supported": (ctypes.c_int, [_I64]),
     "gc_hub_merge_rows": (ctypes.c_int, [_P, _I64, _I64, _P, _P, _I64, _I64, _I64, _U32, _P]),
+    "gc_zero_rows": (ctypes.c_int, [_P, _I64, _P, _I64, _I64, _P]),
     "gc_hub_stair_pair_bn": (ctypes.c_int, [_I64]),
     "gc_hub_stair_gemm": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P, _P, _P, _I32, _P, _P, _I32, _P,
                                          _I64, _I64, _I32, _P, _P, _I64, _P, _U32, _P]),

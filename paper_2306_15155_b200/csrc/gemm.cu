@@ -1761,6 +1761,36 @@ __global__ void __launch_bounds__(256)
 }  // namespace
 }  // namespace gnnc
 
+namespace gnnc {
+namespace {
+__global__ void __launch_bounds__(256)
+    zero_rows_kernel(float *__restrict__ C, int64_t ldc, const int32_t *__restrict__ rows,
+                     int64_t n, int64_t K, bool vec) {
+  const int lane = threadIdx.x % 32;
+  const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; i < n; i += n_warps) {
+    float *c = C + (int64_t)__ldg(rows + i) * ldc;
+    if (vec)
+      for (int64_t f = 4 * lane; f < K; f += 128)
+        *reinterpret_cast<float4 *>(c + f) = make_float4(0.f, 0.f, 0.f, 0.f);
+    else
+      for (int64_t f = lane; f < K; f += 32) c[f] = 0.f;
+  }
+}
+}  // namespace
+}  // namespace gnnc
+
+extern "C" int gc_zero_rows(float *C, int64_t ldc, const int32_t *rows, int64_t n_rows, int64_t K,
+                            void *stream) {
+  GC_REQUIRE(n_rows >= 0 && K >= 0 && ldc >= K, GC_ERR_SHAPE, "gc_zero_rows: bad shape");
+  if (n_rows == 0 || K == 0) return GC_OK;
+  GC_REQUIRE(C && rows, GC_ERR_VALUE, "gc_zero_rows: null operand");
+  const bool vec = (K % 4 == 0) && (ldc % 4 == 0) && aligned16(C);
+  const int64_t blocks = std::min<int64_t>((n_rows + 7) / 8, (int64_t)sm_count() * 16);
+  zero_rows_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(C, ldc, rows, n_rows, K, vec);
+  return check_launch("zero_rows_kernel");
+}
+
 extern "C" int gc_hub_merge_rows(const float *G, int64_t ldg, int64_t rows0, const int32_t *rank,
                                  float *C, int64_t ldc, int64_t n_rows, int64_t K, uint32_t flags,
                                  void *stream) {

@@ -458,8 +458,10 @@ def dense_part(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, out: torch.
         main = torch.cuda.current_stream(dev)
         side = _SIDE_STREAMS.setdefault(dev, torch.cuda.Stream(dev))
         side.wait_stream(main)
+        outside = plan.row_map[plan.rows0:]  # original ids of the rows beyond every step
         with torch.cuda.stream(side):
-            out.zero_()
+            nat.check(lib.gc_zero_rows(out.data_ptr(), _ld(out), outside.data_ptr(),
+                                       outside.numel(), K, _stream(dev)), "zero_rows")
         out.record_stream(side)
         zero_done = torch.cuda.Event()
         zero_done.record(side)
