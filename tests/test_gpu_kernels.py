@@ -861,3 +861,47 @@ def test_gat_aggregate_multihead_one_pass(hubgraph, heads, k2, algo):
                             relu=True, algo=algo)
         got = out[:, hd * k2:(hd + 1) * k2]
         assert torch.allclose(got, ref, rtol=2e-5, atol=2e-6), (hd, float((got - ref).abs().max()))
+
+
+@pytest.fixture(scope="module")
+def reddit_full():
+    """BASELINE configs[1] at full size: Reddit-shaped RMAT (n = 232,965,
+    nnz(A) = 114.6 M) with self loops, on the device."""
+    return gc.NormalizedGraph.from_adjacency(graphs.shape_graph("reddit", device=DEV))
+
+
+def test_full_size_reddit_layer_parity(oracle, reddit_full):
+    """The bench's configuration at full size: the selected dynamic layer with
+    the autotuned dense split vs the fp64 oracle on 512 sampled rows (TF32
+    class, 1e-2), and the size-independent property that the hybrid
+    aggregation equals the plain SpMM (1e-3 of max in the one-term mode)."""
+    from paper_2306_15155_b200 import hub
+    g = reddit_full
+    a = g.a_tilde
+    n, K = a.n_rows, 256
+    rng = np.random.default_rng(1)
+    h = f32(rng.uniform(-0.5, 0.5, (n, K)))
+    w = f32(rng.uniform(-0.5, 0.5, (K, K)))
+    spec = gc.GcnLayerSpec(K, K, w, composition="dynamic", order="update_first")
+    out = gc.gcn_layer(g, torch.from_numpy(h).to(DEV), spec)
+    split = a._plans.get(("hubsplit-choice", K, False), 0)
+    assert split, "the autotuner keeps a dense split on the Reddit shape"
+    # oracle on sampled rows: relu(D Ã D (H W)) restricted to those rows
+    rows = np.sort(rng.choice(n, size=512, replace=False))
+    rp, ci, _ = a.numpy()
+    d = g.d_inv_sqrt.cpu().numpy().astype(np.float64)
+    hw = h.astype(np.float64) @ w.astype(np.float64)
+    ref = np.zeros((rows.size, K))
+    for k, r in enumerate(rows):
+        cols = ci[rp[r]:rp[r + 1]]
+        ref[k] = d[r] * (d[cols][:, None] * hw[cols]).sum(0)
+    ref = np.maximum(ref, 0)
+    got = out[torch.from_numpy(rows).to(DEV)].cpu().numpy()
+    assert oracle.rel_err(got, ref) <= 1e-2
+    # hybrid == plain on the whole output (same HW operand)
+    x = torch.from_numpy(f32(hw)).to(DEV)
+    dd = g.d_inv_sqrt.to(DEV)
+    plain = sparse.spmm_unweighted(a, x, d_row=dd, d_col=dd)
+    hyb = hub.hybrid_aggregate(a, x, dd, split)
+    err = float((hyb - plain).abs().max() / plain.abs().max())
+    assert err <= 1e-3, err
