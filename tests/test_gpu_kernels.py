@@ -905,3 +905,16 @@ def test_full_size_reddit_layer_parity(oracle, reddit_full):
     hyb = hub.hybrid_aggregate(a, x, dd, split)
     err = float((hyb - plain).abs().max() / plain.abs().max())
     assert err <= 1e-3, err
+
+
+@pytest.mark.parametrize("shape", ["products", "reddit", "arxiv"])
+def test_full_size_normalisation_sddmm_exact(shape):
+    """Ñ = D Ã D at the full BASELINE shapes through the edge-parallel window
+    kernel: every value equals fp32(d_i * d_j) bit for bit (rows of every
+    length, including runs of short rows that cross many row ends per step)."""
+    a = gc.add_self_loops(graphs.shape_graph(shape, device=DEV))
+    d = sparse.inv_sqrt_degrees(a).to(DEV)
+    nt = sparse.sddmm_norm(a, d)
+    vals = nt.values if hasattr(nt, "values") else nt
+    ref = d[a.row_of_nnz()] * d[a.col_idx.long()]
+    assert torch.equal(vals, ref)
