@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define GNNC_ABI_VERSION 1
+#define GNNC_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define GNNC_API __attribute__((visibility("default")))
@@ -127,20 +127,6 @@ GNNC_API int gc_gat_aggregate_f32(const int32_t *row_ptr, const int32_t *col_idx
                                   const int32_t *split_rows, int64_t n_split_rows, void *workspace,
                                   size_t ws_bytes, void *stream);
 
-/* Multi-head form (A16 in one pass over col_idx): B rows
- * hold heads * head_dim features, head h owning columns [h*head_dim,
- * (h+1)*head_dim); s and t are head-major [heads][n_rows] / [heads][n_cols];
- * each head has its own LeakyReLU score and online softmax.  Equal to heads
- * gc_gat_aggregate_f32 calls on the column blocks.  heads <= 8.  Split plans
- * need workspace for [n_slots][K] partials + [n_slots][heads] (max, sum)
- * pairs.                                                                   */
-GNNC_API int gc_gat_aggregate_mh_f32(const int32_t *row_ptr, const int32_t *col_idx,
-                const float *s, const float *t, int32_t heads, int64_t head_dim, float slope,
-                const float *B, int64_t ldb, int64_t n_rows, int64_t n_cols, float *C,
-                int64_t ldc, uint32_t flags, int algo, const int32_t *items, int64_t n_items,
-                const int32_t *split_rows, int64_t n_split_rows, void *workspace,
-                size_t ws_bytes, void *stream);
-
 /* col_tagged[p] = col_idx[p] | (hot[col_idx[p]] ? 1<<31 : 0): a copy of the
  * pattern whose hub columns (hot: uint8 per column) are tagged for
  * GC_HUB_TAGGED launches.  The untagged col_idx stays valid for every other
@@ -152,12 +138,16 @@ GNNC_API int gc_tag_hub_columns(const int32_t *col_idx, int64_t nnz, const uint8
  * §8(a) A17 fused with N1): e_p = LeakyReLU(a_src.B[i,:] + a_dst.B[j,:]),
  * alpha = row softmax, C[i,:] = epi(sum_p alpha_p B[j,:]).  Each gathered row
  * B[j,:] feeds both its score and the aggregation (one gather per edge); the
- * reuse composition (B = HW, gat.py:121-129).  Needs a square pattern,
- * K % 4 == 0, K <= 1024, 16-byte aligned B/C/a_src/a_dst (else
- * GC_ERR_UNSUPPORTED).  Plan/workspace protocol as gc_gat_aggregate_f32. */
+ * reuse composition (B = HW, gat.py:121-129).  The source term a_src.B_i
+ * reads row i of B_self (ld_self), or of B when B_self is NULL (square
+ * pattern); a rank's row block of a partitioned graph passes its own rows of
+ * HW as B_self and the gathered HW as B.  Needs K % 4 == 0, K <= 1024,
+ * 16-byte aligned B/B_self/C/a_src/a_dst (else GC_ERR_UNSUPPORTED).
+ * Plan/workspace protocol as gc_gat_aggregate_f32. */
 GNNC_API int gc_gat_sddmm_aggregate_f32(const int32_t *row_ptr, const int32_t *col_idx,
                                         const float *a_src, const float *a_dst, float slope,
-                                        const float *B, int64_t ldb, int64_t n_rows, int64_t K,
+                                        const float *B, int64_t ldb, const float *B_self,
+                                        int64_t ld_self, int64_t n_rows, int64_t K,
                                         float *C, int64_t ldc, uint32_t flags, int algo,
                                         const int32_t *items, int64_t n_items,
                                         const int32_t *split_rows, int64_t n_split_rows,
@@ -223,10 +213,13 @@ GNNC_API int gc_edge_softmax_f32(const int32_t *row_ptr, const int32_t *col_idx,
  *   e = a_src[h]·HW[i, h] + a_dst[h]·HW[j, h]   (k2-wide dot products),
  * then the same LeakyReLU + edge softmax as gc_edge_softmax_f32 (same
  * heavy_rows convention).  The a_dst·HW_j term is gathered per edge
- * (edge-parallel, uniform chunks); the a_src·HW_i term is one dot per node,
- * staged in the caller-owned s_work[heads * n_rows]. */
+ * (edge-parallel, uniform chunks); the a_src·HW_i term is one dot per node
+ * over row i of HW_self (ld_self; NULL: HW itself, a square pattern — a
+ * rank's row block passes its own HW rows), staged in the caller-owned
+ * s_work[heads * n_rows]. */
 GNNC_API int gc_attn_sddmm_f32(const int32_t *row_ptr, const int32_t *col_idx, const float *HW,
-                      int64_t ld, int64_t k2, int32_t heads, const float *a_src,
+                      int64_t ld, const float *HW_self, int64_t ld_self, int64_t k2,
+                      int32_t heads, const float *a_src,
                       const float *a_dst, float slope, int64_t n_rows, int64_t nnz,
                       const int32_t *heavy_rows, int64_t n_heavy, float *s_work,
                       float *alpha, void *stream);
@@ -296,12 +289,6 @@ GNNC_API int gc_hub_gemm(const void *A_hub, int64_t lda, int64_t n_rows, int64_t
  * (k, r) at index k * rpad_s + r (rpad_s = step_rows[s] rounded up to 256,
  * padding rows zero), bit j = A_s[r, 64k + j]; converter warps expand each
  * 128 x 64 tile into the 16-bit operand in shared memory (16x fewer A bytes). */
-/* Join of the concurrent form (hub.py): the staircase GEMM wrote its
- * rank-ordered rows to G (row_map = NULL, d_row in rank order) while the tail
- * SpMM wrote C for every row; C[i] = relu?(C[i] + G[rank[i]]) for rank[i] <
- * rows0, relu?(C[i]) otherwise (flags: GC_RELU).                          */
-GNNC_API int gc_hub_merge_rows(const float *G, int64_t ldg, int64_t rows0, const int32_t *rank,
-                float *C, int64_t ldc, int64_t n_rows, int64_t K, uint32_t flags, void *stream);
 /* C[rows[i], :K] = 0 for i < n_rows (the rows outside every staircase step,
  * zeroed before the tail accumulates).                                    */
 GNNC_API int gc_zero_rows(float *C, int64_t ldc, const int32_t *rows, int64_t n_rows, int64_t K,

@@ -14,6 +14,7 @@ from pathlib import Path
 
 from ._build import LIB, ROOT
 
+ABI_VERSION = 2  # GNNC_ABI_VERSION of include/gnnc.h
 GC_RELU = 1 << 0
 GC_ACCUMULATE = 1 << 1
 GC_HUB_BF16X3 = 0
@@ -68,16 +69,15 @@ _SIGNATURES = {
                                    _SZ, _P]),
     "gc_scale_rows_f32": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _P, _I64, _U32, _P]),
     "gc_node_proj_f32": (ctypes.c_int, [_P, _I64, _I64, _I64, _I32, _I64, _P, _P, _P, _P, _P]),
-    "gc_gat_sddmm_aggregate_f32": (ctypes.c_int, [_P, _P, _P, _P, _F, _P, _I64, _I64, _I64, _P, _I64,
+    "gc_gat_sddmm_aggregate_f32": (ctypes.c_int, [_P, _P, _P, _P, _F, _P, _I64, _P, _I64, _I64, _I64,
+                                                  _P, _I64,
                                                   _U32, ctypes.c_int, _P, _I64, _P, _I64, _P, _SZ, _P]),
     "gc_gat_aggregate_f32": (ctypes.c_int, [_P, _P, _P, _P, _F, _P, _I64, _I64, _I64, _I64, _P, _I64,
                                             _U32, ctypes.c_int, _P, _I64, _P, _I64, _P, _SZ, _P]),
-    "gc_gat_aggregate_mh_f32": (ctypes.c_int, [_P, _P, _P, _P, _I32, _I64, _F, _P, _I64, _I64, _I64,
-                                               _P, _I64, _U32, ctypes.c_int, _P, _I64, _P, _I64, _P,
-                                               _SZ, _P]),
     "gc_edge_softmax_heavy_threshold": (ctypes.c_int, [_I64, _I64]),
     "gc_edge_softmax_f32": (ctypes.c_int, [_P, _P, _P, _P, _I32, _F, _I64, _I64, _P, _I64, _P, _P]),
-    "gc_attn_sddmm_f32": (ctypes.c_int, [_P, _P, _P, _I64, _I64, _I32, _P, _P, _F, _I64, _I64, _P,
+    "gc_attn_sddmm_f32": (ctypes.c_int, [_P, _P, _P, _I64, _P, _I64, _I64, _I32, _P, _P, _F, _I64,
+                                         _I64, _P,
                                          _I64, _P, _P, _P]),
     "gc_partition_rows": (ctypes.c_int, [_P, _I64, _I32, _P]),
     "gc_hub_terms_rows": (_I64, [_I64]),
@@ -86,7 +86,6 @@ _SIGNATURES = {
                                    _P]),
     "gc_hub_stair_supported": (ctypes.c_int, [_I64]),
     "gc_hub_f16_mn_supported": (ctypes.c_int, [_I64]),
-    "gc_hub_merge_rows": (ctypes.c_int, [_P, _I64, _I64, _P, _P, _I64, _I64, _I64, _U32, _P]),
     "gc_zero_rows": (ctypes.c_int, [_P, _I64, _P, _I64, _I64, _P]),
     "gc_hub_stair_pair_bn": (ctypes.c_int, [_I64]),
     "gc_hub_stair_gemm": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P, _P, _P, _I32, _P, _P, _I32, _P,
@@ -122,7 +121,7 @@ def load(build_if_missing: bool = True):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.gc_abi_version() != 1:
+    if lib.gc_abi_version() != ABI_VERSION:
         raise ImportError("libgnnc ABI version mismatch")
     _lib = lib
     return lib

@@ -527,7 +527,8 @@ extern "C" int gc_edge_softmax_f32(const int32_t *row_ptr, const int32_t *col_id
 }
 
 extern "C" int gc_attn_sddmm_f32(const int32_t *row_ptr, const int32_t *col_idx, const float *HW,
-                                 int64_t ld, int64_t k2, int32_t heads, const float *a_src,
+                                 int64_t ld, const float *HW_self, int64_t ld_self, int64_t k2,
+                                 int32_t heads, const float *a_src,
                                  const float *a_dst, float slope, int64_t n_rows, int64_t nnz,
                                  const int32_t *heavy_rows, int64_t n_heavy, float *s_work,
                                  float *alpha, void *stream) {
@@ -541,15 +542,21 @@ extern "C" int gc_attn_sddmm_f32(const int32_t *row_ptr, const int32_t *col_idx,
   GC_REQUIRE(row_ptr && col_idx && HW && a_src && a_dst && s_work && alpha &&
                  n_heavy >= 0 && (n_heavy == 0 || heavy_rows),
              GC_ERR_VALUE, "gc_attn_sddmm_f32: null operand");
+  GC_REQUIRE(HW_self == nullptr || ld_self >= k2 * heads, GC_ERR_SHAPE,
+             "gc_attn_sddmm_f32: ld_self < k2 * heads");
+  if (HW_self == nullptr) HW_self = HW, ld_self = ld;
   const bool vec = (k2 % 4 == 0) && (ld % 4 == 0) && aligned16(HW) && aligned16(a_src) &&
                    aligned16(a_dst);
+  const bool vec_self = (k2 % 4 == 0) && (ld_self % 4 == 0) && aligned16(HW_self) &&
+                        aligned16(a_src);
   cudaStream_t st = as_stream(stream);
-  // source term a_src·HW_i once per node
+  // source term a_src·HW_i once per node (row i of HW_self: the pattern's own
+  // rows; HW itself for a square pattern)
   unsigned grid;
   int rc = rows_grid(n_rows, 32, &grid);
   if (rc) return rc;
-  node_proj_kernel<<<grid, kThreads, 0, st>>>(HW, ld, n_rows, k2, heads, k2, a_src, a_src, s_work,
-                                              nullptr, vec);
+  node_proj_kernel<<<grid, kThreads, 0, st>>>(HW_self, ld_self, n_rows, k2, heads, k2, a_src, a_src,
+                                              s_work, nullptr, vec_self);
   rc = check_launch("node_proj_kernel");
   if (rc) return rc;
   // edge-parallel target dot products: lane groups of 8 lanes (32 for rows

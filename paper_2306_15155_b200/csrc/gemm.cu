@@ -1723,46 +1723,6 @@ extern "C" int gc_gemm_f32(const float *A, int64_t lda, const float *W, int64_t 
 
 namespace gnnc {
 namespace {
-// C[i] = epi(C[i] + (rank[i] < rows0 ? G[rank[i]] : 0)): the staircase's
-// rank-ordered dense part joined into the tail's output (warp per row,
-// float4 when aligned)
-__global__ void __launch_bounds__(256)
-    hub_merge_rows_kernel(const float *__restrict__ G, int64_t ldg, int64_t rows0,
-                          const int32_t *__restrict__ rank, float *__restrict__ C, int64_t ldc,
-                          int64_t n_rows, int64_t K, uint32_t flags, bool vec) {
-  const int lane = threadIdx.x % 32;
-  const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x / 32);
-  const bool relu = (flags & GC_RELU) != 0;
-  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; i < n_rows; i += n_warps) {
-    const int64_t r = __ldg(rank + i);
-    const bool has = r < rows0;
-    if (!has && !relu) continue;
-    float *c = C + i * ldc;
-    const float *g = G + r * ldg;
-    if (vec) {
-      for (int64_t f = 4 * lane; f < K; f += 128) {
-        float4 v = *reinterpret_cast<const float4 *>(c + f);
-        if (has) {
-          const float4 a = ldg_f4(g + f);
-          v.x += a.x, v.y += a.y, v.z += a.z, v.w += a.w;
-        }
-        if (relu) v.x = fmaxf(v.x, 0.f), v.y = fmaxf(v.y, 0.f), v.z = fmaxf(v.z, 0.f), v.w = fmaxf(v.w, 0.f);
-        *reinterpret_cast<float4 *>(c + f) = v;
-      }
-    } else {
-      for (int64_t f = lane; f < K; f += 32) {
-        float v = c[f];
-        if (has) v += __ldg(g + f);
-        c[f] = relu ? fmaxf(v, 0.f) : v;
-      }
-    }
-  }
-}
-}  // namespace
-}  // namespace gnnc
-
-namespace gnnc {
-namespace {
 __global__ void __launch_bounds__(256)
     zero_rows_kernel(float *__restrict__ C, int64_t ldc, const int32_t *__restrict__ rows,
                      int64_t n, int64_t K, bool vec) {
@@ -1789,22 +1749,6 @@ extern "C" int gc_zero_rows(float *C, int64_t ldc, const int32_t *rows, int64_t 
   const int64_t blocks = std::min<int64_t>((n_rows + 7) / 8, (int64_t)sm_count() * 16);
   zero_rows_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(C, ldc, rows, n_rows, K, vec);
   return check_launch("zero_rows_kernel");
-}
-
-extern "C" int gc_hub_merge_rows(const float *G, int64_t ldg, int64_t rows0, const int32_t *rank,
-                                 float *C, int64_t ldc, int64_t n_rows, int64_t K, uint32_t flags,
-                                 void *stream) {
-  GC_REQUIRE(rows0 >= 0 && n_rows >= 0 && K >= 0 && ldg >= K && ldc >= K, GC_ERR_SHAPE,
-             "gc_hub_merge_rows: bad shape");
-  GC_REQUIRE((flags & ~GC_RELU) == 0, GC_ERR_VALUE, "gc_hub_merge_rows: unknown flags 0x%x", flags);
-  if (n_rows == 0 || K == 0) return GC_OK;
-  GC_REQUIRE(rank && C && (G || rows0 == 0), GC_ERR_VALUE, "gc_hub_merge_rows: null operand");
-  const bool vec = (K % 4 == 0) && (ldg % 4 == 0) && (ldc % 4 == 0) && aligned16(C) &&
-                   (G == nullptr || aligned16(G));
-  const int64_t blocks = std::min<int64_t>((n_rows + 7) / 8, (int64_t)sm_count() * 16);
-  hub_merge_rows_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(G, ldg, rows0, rank, C, ldc,
-                                                                        n_rows, K, flags, vec);
-  return check_launch("hub_merge_rows_kernel");
 }
 
 extern "C" int gc_scale_rows_f32(const float *d, const float *B, int64_t ldb, int64_t n_rows,

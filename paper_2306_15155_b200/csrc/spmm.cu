@@ -48,12 +48,9 @@ struct SpmmArgs {
   const float *a_dst;
   uint32_t flags;
   bool hints;         // col_idx carries hub tags in bit 31 (gc_tag_hub_columns)
-  int heads;          // GAT multi-head (MODE 3): s [heads][s_stride], t [heads][t_stride]
-  int head_dim;       //   columns of head h: [h*head_dim, (h+1)*head_dim)
-  int64_t s_stride, t_stride;
+  const float *B_self; // GAT-SDDMM: row i's own features (a_src.B_self[i]); B for a square
+  int64_t ld_self;     //   pattern, a rank's own rows for a row block of a partition
 };
-
-constexpr int kMaxHeads = 8;
 
 template <bool VEC>
 struct Lanes;
@@ -142,17 +139,11 @@ __device__ __forceinline__ void store_row(const SpmmArgs &a, int row, int slot, 
 // MODE 2: GAT whose score is an SDDMM over the gathered rows themselves,
 // e = LeakyReLU(a_src.B_i + a_dst.B_j): one gather of B_j feeds both the
 // score and the aggregation (needs the whole row in one column pass).
-// MODE 3: multi-head GAT in one pass over col_idx: heads h < a.heads each
-// with its own score LeakyReLU(s_i^h + t_j^h) and online softmax state; the
-// gathered row of B holds all heads' features (column c belongs to head
-// c / head_dim), so a row's edges are read once for every head.
 template <int LPR, int NV, bool VEC, bool HAS_VAL, bool HAS_DCOL, int MODE, bool HINT>
 __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
   using T = typename Lanes<VEC>::T;
   constexpr bool GAT = MODE != 0;
   constexpr bool SD = MODE == 2;
-  constexpr bool MH = MODE == 3;
-  constexpr int MAXH = MH ? kMaxHeads : 1;
   constexpr int GPB = kThreads / LPR;
   // edges unrolled per step: ~8 independent 16-byte gathers in flight per lane
   // (never more than LPR: the edge batch is shuffled within the lane group)
@@ -200,23 +191,10 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
   // zl sums this lane's own edge weights relative to m.
   float si = (MODE == 1 && live) ? __ldg(a.s + row) : 0.0f;
   float m = -INFINITY, zl = 0.0f;
-  // MODE 3: per-head source scores and online-softmax states; hv = head of
-  // each column slot of this lane
-  int hv[NV];
-  float sih[MAXH], mh[MAXH], zh[MAXH], gh1[MAXH], wh[MAXH];
-  if constexpr (MH) {
-#pragma unroll
-    for (int v = 0; v < NV; ++v) hv[v] = min(coff[v] / a.head_dim, a.heads - 1);
-#pragma unroll
-    for (int h = 0; h < MAXH; ++h) {
-      sih[h] = (h < a.heads && live) ? __ldg(a.s + h * a.s_stride + row) : 0.0f;
-      mh[h] = -INFINITY, zh[h] = 0.0f, gh1[h] = 0.0f, wh[h] = 0.0f;
-    }
-  }
   T adst[NV];
   if constexpr (SD) {  // source term a_src.B_i and this lane's slice of a_dst
     float part = 0.0f;
-    const float *bi = a.B + (int64_t)row * a.ldb;
+    const float *bi = a.B_self + (int64_t)row * a.ld_self;
 #pragma unroll
     for (int vv = 0; vv < NV; ++vv) {
       adst[vv] = zero_of(T{});
@@ -242,12 +220,6 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
     j1 = ldg_stream_i32(a.col_idx + beg + gl);
     if (HAS_VAL) v1 = ldg_stream_f32(a.values + beg + gl);
     if (NEEDG) g1 = __ldg((MODE == 1 ? a.t : a.d_col) + (HINT ? (j1 & 0x7FFFFFFF) : j1));
-    if constexpr (MH) {
-      const int jj = HINT ? (j1 & 0x7FFFFFFF) : j1;
-#pragma unroll
-      for (int h = 0; h < MAXH; ++h)
-        if (h < a.heads) gh1[h] = __ldg(a.t + h * a.t_stride + jj);
-    }
   }
   if (LPR + gl < len) {
     j2 = ldg_stream_i32(a.col_idx + beg + LPR + gl);
@@ -259,23 +231,10 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
     const float v = v1;
     const float g = g1;
     const bool mine = base + gl < len;
-    float gh[MAXH];
-    if constexpr (MH) {
-#pragma unroll
-      for (int h = 0; h < MAXH; ++h) gh[h] = gh1[h];
-    }
     j1 = j2;
     v1 = v2;
     if (NEEDG && base + LPR + gl < len)
       g1 = __ldg((MODE == 1 ? a.t : a.d_col) + (HINT ? (j1 & 0x7FFFFFFF) : j1));
-    if constexpr (MH) {
-      if (base + LPR + gl < len) {
-        const int jj = HINT ? (j1 & 0x7FFFFFFF) : j1;
-#pragma unroll
-        for (int h = 0; h < MAXH; ++h)
-          if (h < a.heads) gh1[h] = __ldg(a.t + h * a.t_stride + jj);
-      }
-    }
     if (base + 2 * LPR + gl < len) {
       j2 = ldg_stream_i32(a.col_idx + beg + base + 2 * LPR + gl);
       if (HAS_VAL) v2 = ldg_stream_f32(a.values + beg + base + 2 * LPR + gl);
@@ -296,25 +255,6 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
       }
       dj = mine ? __expf(e - m) : 0.0f;
       zl += dj;
-    }
-    if constexpr (MH) {
-#pragma unroll
-      for (int h = 0; h < MAXH; ++h) {
-        if (h < a.heads) {  // group-uniform
-          const float eh = mine ? leaky(sih[h] + gh[h], a.slope) : -INFINITY;
-          const float mn = fmaxf(mh[h], group_max<LPR>(eh));
-          if (mn > mh[h]) {  // group-uniform: rescale this head's slots and sum
-            const float sc = __expf(mh[h] - mn);
-#pragma unroll
-            for (int vv = 0; vv < NV; ++vv)
-              if (hv[vv] == h) scale_into(acc[vv], sc);
-            zh[h] *= sc;
-            mh[h] = mn;
-          }
-          wh[h] = mine ? __expf(eh - mh[h]) : 0.0f;
-          zh[h] += wh[h];
-        }
-      }
     }
     const int cnt = len - base;  // edges left for this group (may be <= 0)
     const int cntw = min(LPR, wmax - base);
@@ -371,30 +311,6 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
               if (colok[vv]) fma_into(acc[vv], w, bv[u][vv]);
           }
         }
-      } else if constexpr (MH) {
-        // each head's weight of edge u from its owner lane; slot vv takes
-        // the weight of its own head
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          // (selected per slot as each head's weight arrives: no array
-          // indexed by the runtime head, which the compiler would spill)
-          float we[NV];
-#pragma unroll
-          for (int vv = 0; vv < NV; ++vv) we[vv] = 0.0f;
-#pragma unroll
-          for (int h = 0; h < MAXH; ++h) {
-            if (h < a.heads) {
-              const float x = __shfl_sync(0xffffffffu, wh[h], e0 + u, LPR);
-#pragma unroll
-              for (int vv = 0; vv < NV; ++vv) we[vv] = hv[vv] == h ? x : we[vv];
-            }
-          }
-          if ((e0 + u) < cnt) {
-#pragma unroll
-            for (int vv = 0; vv < NV; ++vv)
-              if (colok[vv]) fma_into(acc[vv], we[vv], bv[u][vv]);
-          }
-        }
       } else {
         // unit weights (value-blind, no d_j): no weight shuffle; fma(1, b, acc)
         // rounds exactly like the weighted kernel with unit values
@@ -413,26 +329,7 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
     }
   }
   float ds = 1.0f;
-  if constexpr (MH) {
-    float zs[NV];
-#pragma unroll
-    for (int vv = 0; vv < NV; ++vv) zs[vv] = 0.0f;
-#pragma unroll
-    for (int h = 0; h < MAXH; ++h) {
-      if (h < a.heads) {
-        const float zt = group_sum<LPR>(zh[h]);
-        if (slot >= 0 && live && gl == 0 && blockIdx.y == 0)
-          a.partial_mz[(int64_t)slot * a.heads + h] = make_float2(mh[h], zt);
-#pragma unroll
-        for (int vv = 0; vv < NV; ++vv) zs[vv] = hv[vv] == h ? zt : zs[vv];
-      }
-    }
-    if (slot < 0) {
-#pragma unroll
-      for (int vv = 0; vv < NV; ++vv)  // rows without edges aggregate to 0
-        scale_into(acc[vv], zs[vv] > 0.0f ? 1.0f / zs[vv] : 0.0f);
-    }
-  } else if (GAT) {
+  if (GAT) {
     const float z = SD ? zl : group_sum<LPR>(zl);  // SD: every lane already holds the row sum
     if (slot >= 0) {
       if (live && gl == 0 && blockIdx.y == 0) a.partial_mz[slot] = make_float2(m, z);
@@ -463,37 +360,6 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
   for (int v = 0; v < NV; ++v) acc[v] = zero_of(T{});
   float mx = -INFINITY, z = 0.0f;
-  if constexpr (MODE == 3) {  // per-head (max, sum) pairs, slot-major
-    int hv[NV];
-    float zs[NV];
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const int64_t c = col_of<LPR, NV, VEC>(c0, v, gl);
-      hv[v] = (int)min(c / a.head_dim, (int64_t)a.heads - 1);
-      zs[v] = 0.0f;
-    }
-    for (int q = 0; q < sr.z; ++q) {
-      const float *src = a.partial + (int64_t)(sr.y + q) * a.K;
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const int64_t c = col_of<LPR, NV, VEC>(c0, v, gl);
-        if (c >= a.K) continue;
-        float mxh = -INFINITY;
-        for (int p = 0; p < sr.z; ++p)
-          mxh = fmaxf(mxh, a.partial_mz[(int64_t)(sr.y + p) * a.heads + hv[v]].x);
-        const float2 mz = a.partial_mz[(int64_t)(sr.y + q) * a.heads + hv[v]];
-        const float w = mz.x == -INFINITY ? 0.0f : __expf(mz.x - mxh);
-        zs[v] = fmaf(w, mz.y, zs[v]);
-        T t;
-        load_b(t, src + c);
-        fma_into(acc[v], w, t);
-      }
-    }
-#pragma unroll
-    for (int v = 0; v < NV; ++v) scale_into(acc[v], zs[v] > 0.0f ? 1.0f / zs[v] : 0.0f);
-    store_row<LPR, NV, VEC>(a, sr.x, -1, gl, c0, 1.0f, acc);
-    return;
-  }
   if (GAT)
     for (int q = 0; q < sr.z; ++q) mx = fmaxf(mx, a.partial_mz[sr.y + q].x);
   for (int q = 0; q < sr.z; ++q) {
@@ -546,8 +412,9 @@ int launch_cfg(const SpmmArgs &a, const int4 *split_rows, int64_t n_split, cudaS
       else if (hd) spmm_kernel<LPR, NV, VEC, false, true, 0, false><<<grid, kThreads, 0, st>>>(a);
       else spmm_kernel<LPR, NV, VEC, false, false, 0, false><<<grid, kThreads, 0, st>>>(a);
     }
-    int rc = check_launch(MODE == 0 ? "spmm_kernel" : MODE == 1 ? "gat_aggregate_kernel"
-                          : MODE == 3 ? "gat_aggregate_mh_kernel" : "gat_sddmm_aggregate_kernel");
+    int rc = check_launch(MODE == 0   ? "spmm_kernel"
+                          : MODE == 1 ? "gat_aggregate_kernel"
+                                      : "gat_sddmm_aggregate_kernel");
     if (rc) return rc;
   }
   if (n_split > 0) {
@@ -583,8 +450,7 @@ int dispatch(SpmmArgs &a, int64_t n_rows, int algo, const int32_t *items, int64_
         // (max, sum) pairs follow the [n_slots][K] partial rows; the host
         // wrapper sized the workspace from the plan it owns.
         GC_REQUIRE(ws_bytes > 0, GC_ERR_WORKSPACE, "%s: bad workspace", who);
-        const size_t per_mz = 8 * (size_t)(MODE == 3 ? a.heads : 1);
-        const size_t n_slots = ws_bytes / (size_t)(4 * a.K + per_mz);
+        const size_t n_slots = ws_bytes / (size_t)(4 * a.K + 8);
         const size_t off = (n_slots * (size_t)a.K * 4 + 7) & ~(size_t)7;
         a.partial_mz = reinterpret_cast<float2 *>(static_cast<char *>(workspace) + off);
       }
@@ -693,7 +559,8 @@ extern "C" int gc_spmm_f32(const int32_t *row_ptr, const int32_t *col_idx, const
 
 extern "C" int gc_gat_sddmm_aggregate_f32(const int32_t *row_ptr, const int32_t *col_idx,
                                           const float *a_src, const float *a_dst, float slope,
-                                          const float *B, int64_t ldb, int64_t n_rows, int64_t K,
+                                          const float *B, int64_t ldb, const float *B_self,
+                                          int64_t ld_self, int64_t n_rows, int64_t K,
                                           float *C, int64_t ldc, uint32_t flags, int algo,
                                           const int32_t *items, int64_t n_items,
                                           const int32_t *split_rows, int64_t n_split_rows,
@@ -709,11 +576,16 @@ extern "C" int gc_gat_sddmm_aggregate_f32(const int32_t *row_ptr, const int32_t 
   GC_REQUIRE(row_ptr && C && B && a_src && a_dst, GC_ERR_VALUE,
              "gc_gat_sddmm_aggregate_f32: null operand");
   GC_REQUIRE(n_rows < INT32_MAX, GC_ERR_SHAPE, "gc_gat_sddmm_aggregate_f32: int32 range");
+  GC_REQUIRE(B_self == nullptr || (ld_self >= K && ld_self % 4 == 0 && aligned16(B_self)),
+             GC_ERR_UNSUPPORTED, "gc_gat_sddmm_aggregate_f32: B_self needs ld >= K, ld %% 4 == 0 "
+             "and 16-byte alignment");
   SpmmArgs a{};
   a.row_ptr = row_ptr;
   a.col_idx = col_idx;
   a.B = B;
   a.ldb = ldb;
+  a.B_self = B_self ? B_self : B;
+  a.ld_self = B_self ? ld_self : ldb;
   a.K = K;
   a.C = C;
   a.ldc = ldc;
@@ -760,49 +632,4 @@ extern "C" int gc_gat_aggregate_f32(const int32_t *row_ptr, const int32_t *col_i
   a.slope = slope;
   return dispatch<1>(a, n_rows, algo, items, n_items, split_rows, n_split_rows, workspace,
                         ws_bytes, stream, "gc_gat_aggregate_f32");
-}
-
-extern "C" int gc_gat_aggregate_mh_f32(const int32_t *row_ptr, const int32_t *col_idx,
-                                       const float *s, const float *t, int32_t heads,
-                                       int64_t head_dim, float slope, const float *B, int64_t ldb,
-                                       int64_t n_rows, int64_t n_cols, float *C, int64_t ldc,
-                                       uint32_t flags, int algo, const int32_t *items,
-                                       int64_t n_items, const int32_t *split_rows,
-                                       int64_t n_split_rows, void *workspace, size_t ws_bytes,
-                                       void *stream) {
-  GC_REQUIRE(heads >= 1 && heads <= kMaxHeads, GC_ERR_VALUE,
-             "gc_gat_aggregate_mh_f32: heads must be in [1, %d]", kMaxHeads);
-  GC_REQUIRE(n_rows >= 0 && n_cols >= 0 && head_dim >= 1, GC_ERR_SHAPE,
-             "gc_gat_aggregate_mh_f32: bad size");
-  const int64_t K = (int64_t)heads * head_dim;
-  GC_REQUIRE(ldb >= K && ldc >= K, GC_ERR_SHAPE,
-             "gc_gat_aggregate_mh_f32: leading dimension < heads * head_dim");
-  GC_REQUIRE((flags & ~(GC_RELU | GC_HUB_TAGGED | GC_SPMM_SHRINK_MASK)) == 0, GC_ERR_VALUE,
-             "gc_gat_aggregate_mh_f32: unknown flags 0x%x", flags);
-  GC_REQUIRE(slope > 0.0f && slope < 1.0f, GC_ERR_VALUE,
-             "gc_gat_aggregate_mh_f32: leaky_slope must lie in (0, 1)");
-  if (n_rows == 0) return GC_OK;
-  GC_REQUIRE(row_ptr && C && s && t && (B || n_cols == 0), GC_ERR_VALUE,
-             "gc_gat_aggregate_mh_f32: null operand");
-  GC_REQUIRE(n_rows < INT32_MAX && n_cols < INT32_MAX, GC_ERR_SHAPE,
-             "gc_gat_aggregate_mh_f32: int32 index range exceeded");
-  SpmmArgs a{};
-  a.row_ptr = row_ptr;
-  a.col_idx = col_idx;
-  a.B = B;
-  a.ldb = ldb;
-  a.K = K;
-  a.C = C;
-  a.ldc = ldc;
-  a.flags = flags;
-  a.hints = (flags & GC_HUB_TAGGED) != 0;
-  a.s = s;
-  a.t = t;
-  a.slope = slope;
-  a.heads = heads;
-  a.head_dim = (int)head_dim;
-  a.s_stride = n_rows;
-  a.t_stride = n_cols;
-  return dispatch<3>(a, n_rows, algo, items, n_items, split_rows, n_split_rows, workspace,
-                        ws_bytes, stream, "gc_gat_aggregate_mh_f32");
 }

@@ -1,29 +1,38 @@
-"""Row-partitioned layers across GPUs.
+"""Row-partitioned GCN and GAT layers across GPUs.
 
 One process per GPU (``torch.distributed``, NCCL over NVLink on the box,
 gloo in the CPU tests).  Ã is cut into contiguous, nnz-balanced row blocks
 (``partition_rows`` — the C-ABI host function, bit-exact with the oracle);
 rank p owns rows [b_p, b_{p+1}) with global column ids.  Per layer exactly one
-all-gather assembles the operand the local SpMM gathers:
+all-gather assembles the operand the local aggregation gathers:
 
-    composition              all-gathered operand
-    GCN A(HW)                (H_p W)          (d ⊙ folded into the SpMM gather)
+    composition              all-gathered operand (one collective)
+    GCN A(HW)                H_p W          (d ⊙ folded into the GEMM epilogue)
     GCN (AH)W                H_p
-    GAT reuse                H_p W and t_p
-    GAT recompute            H_p and t_p (+ H_p W for the local attention)
+    GAT reuse, reassoc       [H_p W | t_p]  (gat.py:121-129)
+    GAT reuse, sddmm         H_p W          (scores from the gathered rows)
+    GAT recompute, reassoc   [H_p | t_p]    (gat.py:132-145; t_p = H_p W a_dst)
+    GAT recompute, sddmm     [H_p | H_p W]  (α needs HW rows, the SpMM H rows)
 
 Output rows stay partitioned and feed the next layer.  Blocks are padded to
-the largest block for ``all_gather_into_tensor``.
+the largest block for ``all_gather_into_tensor``; the local pattern's column
+ids are remapped once into that padded layout (``RowPartition.padded``) so the
+gathered buffer is used in place, and the gather buffers are reused across
+layers (cached per partition, width and role).
 
-Overlap (``overlap=True``): the local block of the
+Overlap (``overlap=True``, GCN): the local block of the
 pattern is split by column into the edges whose source row this rank owns
 (aggregated straight from its own operand block, while the all-gather is in
-flight) and the remote edges (column ids remapped into the padded gather
-buffer, so no unpad copy).  The remote pass accumulates into the local one
-(``out += d_i * acc``; ReLU on the total).
+flight) and the remote edges.  The remote pass accumulates into the local one
+(``out += d_i * acc``; ReLU on the total).  (GAT keeps one pass: its online
+softmax would need the two passes' (max, sum) states merged.)
+
+Capacity path: :meth:`RowPartition.from_file` reads only this rank's rows of a
+``.gcsr`` file of Ã (the row_ptr — O(n) — is read whole to cut the blocks and
+to form D^-1/2), so no rank materialises the whole graph.
 
 The compute ops are injectable (``ops``) so the host logic — partition,
-padding, gather, unpad, assembly — is testable on CPU with gloo and the
+padding, gather, remapping, assembly — is testable on CPU with gloo and the
 oracle standing in for the CUDA kernels.
 """
 
@@ -36,7 +45,7 @@ import torch
 import torch.distributed as dist
 
 from . import _native as nat
-from .sparse import CsrMatrix
+from .sparse import CsrMatrix, ShapeError
 
 
 def partition_rows(row_ptr, parts: int) -> np.ndarray:
@@ -94,12 +103,60 @@ class RowPartition:
 
     @property
     def max_rows(self) -> int:
-        return int(np.diff(self.bounds).max())
+        return max(int(np.diff(self.bounds).max()), 1)
 
     @classmethod
     def of(cls, a: CsrMatrix, rank: int, world: int) -> "RowPartition":
         b = partition_rows(a.row_ptr, world)
         return cls(rank, world, b, a.take_rows(int(b[rank]), int(b[rank + 1])))
+
+    @classmethod
+    def from_file(cls, path, rank: int, world: int, device=None) -> tuple["RowPartition", torch.Tensor]:
+        """This rank's block of the ``.gcsr`` file of Ã (self loops included)
+        and the FULL D^-1/2 vector, reading only the O(n) row_ptr and this
+        rank's rows of col_idx/values: the capacity path, where no rank holds
+        the whole graph.  Bounds are bit-identical to :meth:`of`."""
+        rp = CsrMatrix.read_row_ptr(path)
+        b = partition_rows(rp, world)
+        local = CsrMatrix.load(path, device=device, rows=(int(b[rank]), int(b[rank + 1])))
+        deg = np.diff(rp).astype(np.float64)
+        if deg.size and deg.min() <= 0:
+            from .sparse import DegenerateNodeError
+
+            raise DegenerateNodeError("zero-degree row: D^-1/2 undefined")
+        d = torch.from_numpy((1.0 / np.sqrt(deg)).astype(np.float32)).to(local.device)
+        return cls(rank, world, b, local), d
+
+    def _owner_map(self, col: torch.Tensor):
+        bounds = torch.as_tensor(self.bounds, device=col.device)
+        owner = torch.searchsorted(bounds[1:], col, right=True)
+        return owner, owner * self.max_rows + (col - bounds[owner])
+
+    def padded(self) -> CsrMatrix:
+        """The local block with its column ids remapped into the padded
+        all-gather layout (column j owned by rank q at q * max_rows + j - b_q),
+        n_cols = world * max_rows; cached."""
+        if getattr(self, "_padded", None) is None:
+            a = self.local
+            _, cols = self._owner_map(a.col_idx.long())
+            pad = CsrMatrix(a.n_rows, self.world * self.max_rows, a.row_ptr, cols, a.values,
+                            validate=False, device=a.device)
+            pad._unit = a._unit
+            self._padded = pad
+        return self._padded
+
+    def pad_vector(self, d: torch.Tensor) -> torch.Tensor:
+        """A full per-node vector (e.g. D^-1/2) in the padded layout (zeros in
+        the padding); cached per source tensor."""
+        key = (id(d), d._version)
+        hit = getattr(self, "_dpad", None)
+        if hit is None or hit[0] != key or hit[1] is not d:
+            out = torch.zeros(self.world * self.max_rows, dtype=d.dtype, device=d.device)
+            for p in range(self.world):
+                lo, hi = int(self.bounds[p]), int(self.bounds[p + 1])
+                out[p * self.max_rows: p * self.max_rows + hi - lo] = d[lo:hi]
+            self._dpad = (key, d, out)
+        return self._dpad[2]
 
     def split_local_remote(self) -> tuple[CsrMatrix, CsrMatrix]:
         """(edges from owned rows, columns rebased to the local block;
@@ -109,9 +166,7 @@ class RowPartition:
             col = a.col_idx.long()
             rows = a.row_of_nnz()
             own = (col >= self.lo) & (col < self.hi)
-            bounds = torch.as_tensor(self.bounds, device=col.device)
-            owner = torch.searchsorted(bounds[1:], col, right=True)
-            padded = owner * self.max_rows + (col - bounds[owner])
+            _, padded = self._owner_map(col)
 
             def sub(mask, cols, n_cols):
                 cnt = torch.bincount(rows[mask], minlength=a.n_rows)
@@ -125,28 +180,38 @@ class RowPartition:
             self._lr = (loc, rem)
         return self._lr
 
+    def gather_buffers(self, k: int, dtype, device, tag: str = "x"):
+        """(send [max_rows, k], recv [world*max_rows, k]) reused across layers
+        (stream-ordered: the next gather into a buffer follows the kernels
+        that read it on the same stream)."""
+        cache = self.__dict__.setdefault("_bufs", {})
+        key = (tag, int(k), dtype, str(device))
+        if key not in cache:
+            cache[key] = (torch.zeros(self.max_rows, k, dtype=dtype, device=device),
+                          torch.empty(self.world * self.max_rows, k, dtype=dtype, device=device))
+        return cache[key]
 
-def all_gather_padded(x_local: torch.Tensor, part: RowPartition, group=None, async_op=False):
-    """Padded all-gather: returns (buffer of world*max_rows rows, work handle)."""
+
+def all_gather_padded(x_local: torch.Tensor, part: RowPartition, group=None, async_op=False,
+                      tag: str = "x"):
+    """Padded all-gather: returns (buffer of world*max_rows rows, work handle).
+    The buffers are the partition's cached ones (:meth:`RowPartition.gather_buffers`)."""
     k = x_local.shape[1]
-    pad = part.max_rows
-    if x_local.shape[0] == pad:
-        buf = x_local.contiguous()
+    send, full = part.gather_buffers(k, x_local.dtype, x_local.device, tag)
+    if x_local.shape[0] == part.max_rows and x_local.is_contiguous():
+        send = x_local
     else:
-        buf = torch.zeros(pad, k, dtype=x_local.dtype, device=x_local.device)
-        buf[: x_local.shape[0]] = x_local
-    full = torch.empty(part.world * pad, k, dtype=x_local.dtype, device=x_local.device)
-    work = dist.all_gather_into_tensor(full, buf, group=group, async_op=async_op)
+        send[: x_local.shape[0]].copy_(x_local)
+    work = dist.all_gather_into_tensor(full, send, group=group, async_op=async_op)
     return full, work
 
 
 def all_gather_rows(x_local: torch.Tensor, part: RowPartition, group=None) -> torch.Tensor:
     """Assemble the full n x k operand from every rank's row block (padded
-    all_gather_into_tensor, then the padding is dropped)."""
+    all_gather_into_tensor, then the padding is dropped).  Returns a fresh
+    tensor (the gather buffer is reused by the next call)."""
     pad = part.max_rows
-    full, _ = all_gather_padded(x_local, part, group)
-    if all(int(part.bounds[p + 1] - part.bounds[p]) == pad for p in range(part.world)):
-        return full
+    full, _ = all_gather_padded(x_local, part, group, tag="rows")
     pieces = [full[p * pad: p * pad + int(part.bounds[p + 1] - part.bounds[p])]
               for p in range(part.world)]
     return torch.cat(pieces, 0)
@@ -156,10 +221,10 @@ class CudaOps:
     """The product ops: sm_100a kernels through the C ABI."""
 
     @staticmethod
-    def gemm(a, w, row_scale=None, relu=False):
+    def gemm(a, w, row_scale=None, relu=False, out=None):
         from .sparse import gemm
 
-        return gemm(a, w, row_scale=row_scale, relu=relu)
+        return gemm(a, w, row_scale=row_scale, relu=relu, out=out)
 
     @staticmethod
     def spmm(a: CsrMatrix, b, d_row=None, d_col=None, relu=False, weighted=True, out=None,
@@ -187,30 +252,83 @@ class CudaOps:
         f = spmm if weighted else spmm_unweighted
         return f(a, b, d_row=d_row, d_col=d_col, relu=relu, out=out, accumulate=accumulate)
 
+    @staticmethod
+    def node_scores(x, a_src, a_dst, heads: int, width: int, head_stride: int):
+        """s[h], t[h] = X[:, h-block] · a_src[h], · a_dst[h] ([heads, rows])."""
+        from .sparse import _ld, _stream
+
+        n = x.shape[0]
+        s = torch.empty(heads, n, dtype=torch.float32, device=x.device)
+        t = torch.empty(heads, n, dtype=torch.float32, device=x.device)
+        if n:
+            nat.check(nat.load().gc_node_proj_f32(x.data_ptr(), _ld(x), n, width, heads, head_stride,
+                                                  a_src.data_ptr(), a_dst.data_ptr(), s.data_ptr(),
+                                                  t.data_ptr(), _stream(x.device)), "node_proj")
+        return s, t
+
+    @staticmethod
+    def gat_aggregate(a: CsrMatrix, s, t, slope, b, relu=False, out=None):
+        from .sparse import gat_aggregate
+
+        return gat_aggregate(a, s, t, slope, b, relu=relu, out=out)
+
+    @staticmethod
+    def gat_sddmm_aggregate(a: CsrMatrix, a_src, a_dst, slope, b, b_self, relu=False, out=None):
+        from .sparse import gat_sddmm_aggregate
+
+        res = gat_sddmm_aggregate(a, a_src, a_dst, slope, b, relu=relu, out=out, b_self=b_self)
+        if res is not None:
+            return res
+        # outside the fused kernel's range (K % 4, K > 1024, alignment): α by
+        # the SDDMM attention kernel, then the weighted SpMM
+        from .sparse import spmm
+
+        alpha = CudaOps.attn_sddmm(a, b, b_self, a_src, a_dst, slope, 1, b.shape[1])
+        return spmm(a.with_values(alpha[0]), b, relu=relu, out=out)
+
+    @staticmethod
+    def attn_sddmm(a: CsrMatrix, hw, hw_self, a_src, a_dst, slope, heads: int, k2: int):
+        """α [heads, nnz] of the SDDMM attention (gc_attn_sddmm_f32) on a row
+        block: source terms from ``hw_self`` (this rank's rows), target terms
+        gathered from ``hw`` (padded layout)."""
+        from .sparse import _ld, _stream
+
+        m = a.nnz
+        alpha = torch.empty(heads, m, dtype=torch.float32, device=hw.device)
+        s_work = torch.empty(heads, max(a.n_rows, 1), dtype=torch.float32, device=hw.device)
+        heavy = a.softmax_heavy_rows()
+        nat.check(nat.load().gc_attn_sddmm_f32(
+            a.row_ptr.data_ptr(), a.col_idx.data_ptr(), hw.data_ptr(), _ld(hw), hw_self.data_ptr(),
+            _ld(hw_self), k2, heads, a_src.data_ptr(), a_dst.data_ptr(), float(slope), a.n_rows, m,
+            heavy.data_ptr(), heavy.numel(), s_work.data_ptr(), alpha.data_ptr(),
+            _stream(hw.device)), "attn_sddmm")
+        return alpha
+
 
 def dist_gcn_layer(part: RowPartition, h_local: torch.Tensor, w: torch.Tensor, *,
                    composition: str, order: str, d: torch.Tensor | None = None,
                    ops=CudaOps, group=None, overlap: bool = False,
                    hub_unit: bool = False) -> torch.Tensor:
-    """One GCN layer on this rank's rows.  ``part.local`` is Ñ's block for
-    precompute or Ã's block for dynamic; ``d`` is the FULL D^-1/2 vector
-    (needed for dynamic, and for the hub split).  ``hub_unit``: Ã is
-    unit-valued, so the aggregation may use the hub split (hub.py) on this
-    rank's block.  Returns this rank's output rows."""
+    """One GCN layer on this rank's rows (reference gcn.py:125-161 on a row
+    block).  ``part.local`` is Ñ's block for precompute or Ã's block for
+    dynamic; ``d`` is the FULL D^-1/2 vector (needed for dynamic, and for the
+    hub split).  ``hub_unit``: Ã is unit-valued, so the aggregation may use
+    the hub split (hub.py) on this rank's block.  Returns this rank's output
+    rows.  A rank with no rows still joins the collective and returns a
+    0-row output."""
     dyn = composition == "dynamic"
     if dyn and d is None:
         raise ValueError("dynamic composition needs the degree vector")
     hub_unit = hub_unit and d is not None
     d_loc = d[part.lo:part.hi] if (dyn or hub_unit) else None
     weighted = not (dyn and part.local.has_unit_values)
+    if part.rows == 0:
+        src = ops.gemm(h_local, w) if order == "update_first" else h_local
+        all_gather_padded(src, part, group)
+        return torch.zeros(0, w.shape[1], dtype=torch.float32, device=h_local.device)
     if overlap:
         loc, rem = part.split_local_remote()
-        d_pad = None
-        if dyn or hub_unit:
-            d_pad = torch.zeros(part.world * part.max_rows, dtype=d.dtype, device=d.device)
-            for p in range(part.world):
-                lo, hi = int(part.bounds[p]), int(part.bounds[p + 1])
-                d_pad[p * part.max_rows: p * part.max_rows + hi - lo] = d[lo:hi]
+        d_pad = part.pad_vector(d) if (dyn or hub_unit) else None
         src = ops.gemm(h_local, w) if order == "update_first" else h_local
         full, work = all_gather_padded(src, part, group, async_op=True)
         # owned-column edges while the gather is in flight
@@ -225,14 +343,101 @@ def dist_gcn_layer(part: RowPartition, h_local: torch.Tensor, w: torch.Tensor, *
         y = ops.spmm(rem, full, d_row=dl, d_col=d_pad if dyn else None, relu=last,
                      weighted=weighted, out=y, accumulate=True, **hub_kw)
         return y if last else ops.gemm(y, w, relu=True)
-    hub_kw = {"hub_d": (d_loc, d)} if hub_unit else {}
+    pat = part.padded()
+    d_pad = part.pad_vector(d) if (dyn or hub_unit) else None
+    hub_kw = {"hub_d": (d_loc, d_pad)} if hub_unit else {}
     dl = d_loc if dyn else None
     if order == "update_first":
-        hw_loc = ops.gemm(h_local, w)
-        hw = all_gather_rows(hw_loc, part, group)
-        return ops.spmm(part.local, hw, d_row=dl, d_col=d if dyn else None, relu=True,
+        full, _ = all_gather_padded(ops.gemm(h_local, w), part, group)
+        return ops.spmm(pat, full, d_row=dl, d_col=d_pad if dyn else None, relu=True,
                         weighted=weighted, **hub_kw)
-    h = all_gather_rows(h_local, part, group)
-    x = ops.spmm(part.local, h, d_row=dl, d_col=d if dyn else None, relu=False, weighted=weighted,
+    full, _ = all_gather_padded(h_local, part, group)
+    x = ops.spmm(pat, full, d_row=dl, d_col=d_pad if dyn else None, relu=False, weighted=weighted,
                  **hub_kw)
     return ops.gemm(x, w, relu=True)
+
+
+def _pad4(n: int) -> int:
+    return (n + 3) // 4 * 4
+
+
+def dist_gat_layer(part: RowPartition, h_local: torch.Tensor, spec, *, ops=CudaOps,
+                   group=None) -> torch.Tensor:
+    """One GAT layer (``spec``: a :class:`~.gat.GatLayerSpec`, any heads,
+    composition and attention form) on this rank's rows of the unit Ã —
+    reference gat.py:121-153 on a row block.  One all-gather per layer of the
+    operand in the module table; the aggregation reads the padded gather
+    buffer through the remapped pattern.  Returns this rank's output rows
+    (rows x heads*k2)."""
+    from .gat import AttentionForm, GatComposition, _folded_attention_vectors
+
+    H, k1, k2 = spec.heads, spec.k1, spec.k2
+    dev = h_local.device
+    if tuple(h_local.shape) != (part.rows, k1):
+        raise ShapeError(f"embeddings shape {tuple(h_local.shape)} != ({part.rows}, {k1})")
+    relu = spec.activation == "relu"
+    slope = spec.leaky_slope
+    a_src, a_dst = spec.attn_src.to(dev), spec.attn_dst.to(dev)
+    pat = part.padded()
+    out = torch.empty(part.rows, k2 * H, dtype=torch.float32, device=dev)
+    recompute = spec.composition is GatComposition.RECOMPUTE
+    sddmm = spec.attention is AttentionForm.SDDMM
+    w = spec.weights
+    if not recompute:
+        hw = ops.gemm(h_local, w)  # rows x H*k2
+        if sddmm:
+            full, _ = all_gather_padded(hw, part, group, tag="gat")
+            if part.rows == 0:
+                return out
+            for i in range(H):
+                cs = slice(i * k2, (i + 1) * k2)
+                ops.gat_sddmm_aggregate(pat, a_src[cs], a_dst[cs], slope, full[:, cs], hw[:, cs],
+                                        relu=relu, out=out[:, cs])
+            return out
+        s, t = ops.node_scores(hw, a_src, a_dst, H, k2, k2)
+        wid = H * k2
+        full, _ = all_gather_padded(torch.cat([hw, t.t(), hw.new_zeros(hw.shape[0], _pad4(H) - H)],
+                                              1), part, group, tag="gat")
+        if part.rows == 0:
+            return out
+        t_full = full[:, wid:wid + H].t().contiguous()
+        for i in range(H):
+            cs = slice(i * k2, (i + 1) * k2)
+            ops.gat_aggregate(pat, s[i], t_full[i], slope, full[:, cs], relu=relu, out=out[:, cs])
+        return out
+    if sddmm:
+        # α from the SDDMM over HW rows, then (α H) W: gather [H_p | H_p W]
+        hw = ops.gemm(h_local, w)
+        k1p = _pad4(k1)
+        parts_ = [h_local] + ([h_local.new_zeros(h_local.shape[0], k1p - k1)] if k1p > k1 else [])             + [hw]
+        full, _ = all_gather_padded(torch.cat(parts_, 1), part, group, tag="gat")
+        if part.rows == 0:
+            return out
+        h_full, hw_full = full[:, :k1], full[:, k1p:]
+        alpha = ops.attn_sddmm(pat, hw_full, hw, a_src, a_dst, slope, H, k2)
+        for i in range(H):
+            ah = ops.spmm(pat.with_values(alpha[i]), h_full, relu=False, weighted=True)
+            ops.gemm(ah, w[:, i * k2:(i + 1) * k2], relu=relu, out=out[:, i * k2:(i + 1) * k2])
+        return out
+    # recompute, reassociated scores: s = H (W a_src), t = H (W a_dst) —
+    # no HW GEMM; gather [H_p | t_p]
+    if ops is CudaOps:
+        u, v = _folded_attention_vectors(spec)  # exact-fp32 GEMVs, cached on the spec
+    else:
+        uv = [ops.gemm(w[:, i * k2:(i + 1) * k2], torch.stack([a_src[i * k2:(i + 1) * k2],
+                                                               a_dst[i * k2:(i + 1) * k2]], 1))
+              for i in range(H)]
+        u = torch.cat([x[:, 0] for x in uv]).contiguous()
+        v = torch.cat([x[:, 1] for x in uv]).contiguous()
+    s, t = ops.node_scores(h_local, u, v, H, k1, 0)
+    full, _ = all_gather_padded(torch.cat([h_local, t.t(), h_local.new_zeros(h_local.shape[0],
+                                                                             _pad4(k1 + H) - k1 - H)],
+                                          1), part, group, tag="gat")
+    if part.rows == 0:
+        return out
+    h_full = full[:, :k1]
+    t_full = full[:, k1:k1 + H].t().contiguous()
+    for i in range(H):
+        ah = ops.gat_aggregate(pat, s[i], t_full[i], slope, h_full, relu=False)
+        ops.gemm(ah, w[:, i * k2:(i + 1) * k2], relu=relu, out=out[:, i * k2:(i + 1) * k2])
+    return out

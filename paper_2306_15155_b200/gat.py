@@ -44,22 +44,12 @@ from .sparse import (
     _ld,
     _require_cuda,
     _stream,
+    call_spmm_hook,
     gat_aggregate,
-    gat_aggregate_mh,
     gemm,
     relu_,
     spmm,
 )
-
-# reuse/reassoc with heads > 1: one fused pass per head (default) or all heads
-# in one pass over the pattern (GNNC_GAT_MH=1, gat_aggregate_mh).  Measured
-# (profiles/probes/gat_mh.py): one pass is 1.1-1.6x SLOWER on B200 — each
-# per-head pass gathers a k2-wide slice of HW that stays L2-resident, while
-# the one-pass row is heads*k2 wide (4x the L2 working set) and carries
-# per-head softmax state in registers; the shared col_idx read it saves is
-# 4 bytes per edge against 4*k2 gathered
-MULTIHEAD_ONE_PASS = __import__("os").environ.get("GNNC_GAT_MH", "0") == "1"
-
 
 class GatComposition(str, Enum):
     REUSE = "reuse"
@@ -163,7 +153,7 @@ def atten_calc(a_tilde: CsrMatrix, hw, spec: GatLayerSpec) -> AttentionMatrix:
     if spec.attention is AttentionForm.SDDMM:
         s_work = torch.empty(H, n, dtype=torch.float32, device=dev)
         rc = lib.gc_attn_sddmm_f32(a_tilde.row_ptr.data_ptr(), a_tilde.col_idx.data_ptr(),
-                                   hwt.data_ptr(), _ld(hwt), k2, H, a_src.data_ptr(),
+                                   hwt.data_ptr(), _ld(hwt), None, 0, k2, H, a_src.data_ptr(),
                                    a_dst.data_ptr(), float(spec.leaky_slope), n, m,
                                    heavy.data_ptr(), heavy.numel(), s_work.data_ptr(),
                                    alpha.data_ptr(), st)
@@ -230,8 +220,9 @@ def gat_layer_reuse(a_tilde: CsrMatrix, h, spec: GatLayerSpec, *, spmm_fn=None):
     k2, H = spec.k2, spec.heads
     if spmm_fn is not None:
         att = atten_calc(a_tilde, hw, spec)
-        outs = [spmm_fn(att.head(i), hw[:, i * k2:(i + 1) * k2]) for i in range(H)]
-        out = torch.cat([torch.as_tensor(o, device=hw.device).float() for o in outs], 1).contiguous()
+        outs = [call_spmm_hook(spmm_fn, att.head(i), hw[:, i * k2:(i + 1) * k2].contiguous())
+                for i in range(H)]
+        out = torch.cat(outs, 1).contiguous()
         return op.wrap(relu_(out) if relu else out)
     out = torch.empty(a_tilde.n_rows, k2 * H, dtype=torch.float32, device=hw.device)
     if spec.attention is AttentionForm.SDDMM:
@@ -252,11 +243,6 @@ def gat_layer_reuse(a_tilde: CsrMatrix, h, spec: GatLayerSpec, *, spmm_fn=None):
     if a_tilde.n_rows != a_tilde.n_cols:
         raise ShapeError("attention expects a square adjacency")
     s, t = _projections(hw, spec, spec.attn_src.to(hw.device), spec.attn_dst.to(hw.device), k2, k2)
-    if H > 1 and MULTIHEAD_ONE_PASS:
-        # all heads in one pass over the pattern (one col_idx read, per-head
-        # online softmax in the same lane group)
-        gat_aggregate_mh(a_tilde, s, t, spec.leaky_slope, hw, H, relu=relu, out=out)
-        return op.wrap(out)
     for i in range(H):
         gat_aggregate(a_tilde, s[i], t[i], spec.leaky_slope, hw[:, i * k2:(i + 1) * k2], relu=relu,
                       out=out[:, i * k2:(i + 1) * k2])
@@ -279,8 +265,7 @@ def gat_layer_recompute(a_tilde: CsrMatrix, h, spec: GatLayerSpec, *, spmm_fn=No
         att = atten_calc(a_tilde, hw, spec)
         agg = spmm_fn if spmm_fn is not None else spmm
         for i in range(H):
-            ah = agg(att.head(i), op.t)
-            ah = ah if isinstance(ah, torch.Tensor) else torch.as_tensor(ah, device=dev).float()
+            ah = call_spmm_hook(agg, att.head(i), op.t)
             gemm(ah, spec.weights[:, i * k2:(i + 1) * k2], relu=relu, out=out[:, i * k2:(i + 1) * k2])
         return op.wrap(out)
     if a_tilde.n_rows != a_tilde.n_cols:

@@ -96,7 +96,6 @@ def _block_dtype(fmt: int):
 # shared memory; 1/16 of the 16-bit blocks' HBM footprint).  Off by default:
 # measured 0.86 vs 0.62 ms on Reddit K=256 — handoff-latency bound (gemm.cu)
 HUB_ABITS = os.environ.get("GNNC_HUB_ABITS", "0") == "1"
-HUB_T_CANDIDATES = (1024, 2048, 4096, 8192)
 # (cell/edge cost ratio δ, balance slack) pairs tried by the autotuner
 # (slack > 1 reaches further right, but short-wide steps stream their B
 # operand from DRAM once per pair tile and lose to the tail: measured 2.73 ms
@@ -126,7 +125,6 @@ def _stair_candidates(K: int):
         out.append(cands[0])
     return tuple(dict.fromkeys(out))
 HUB_MIN_NNZ = 1 << 24            # smaller graphs stay on the SpMM alone
-HUB_MIN_DENSITY = 0.02           # mean density of a block worth a dense product
 HUB_MEM_BUDGET = 8 << 30         # bytes of dense blocks per pattern
 STAIR_MAX_STEPS = 16
 STAIR_FIRST_BAND = 1024          # rows / columns of the first histogram band
@@ -158,12 +156,16 @@ class _TailMixin:
         self._tail_vals: dict = {}
 
     def tail_block(self, values: torch.Tensor | None, lo: int, hi: int) -> CsrMatrix:
-        vkey = None if values is None else (values.data_ptr(), values._version)
-        if vkey not in self._tail_vals:
+        # keyed on the values tensor itself (held, so its id cannot be reused
+        # by a new tensor) and its version (in-place updates invalidate)
+        vkey = None if values is None else (id(values), values._version)
+        hit = self._tail_vals.get(vkey)
+        if hit is None or (values is not None and hit[0] is not values):
             self._tail_vals = {k: v for k, v in self._tail_vals.items() if k is None}
-            self._tail_vals[vkey] = ({}, self.tail if values is None
-                                     else self.tail.with_values(values[self.keep].contiguous()))
-        blocks, full = self._tail_vals[vkey]
+            hit = (values, {}, self.tail if values is None
+                   else self.tail.with_values(values[self.keep].contiguous()))
+            self._tail_vals[vkey] = hit
+        _, blocks, full = hit
         if (lo, hi) == (0, full.n_rows):
             return full
         if (lo, hi) not in blocks:
@@ -221,6 +223,10 @@ class StairPlan(_TailMixin):
         self.steps = self._staircase(a, er, ec, delta, slack, n_clusters, first_band)
         if not self.steps:
             raise ValueError("stair split: no block pays for its cells")
+        cells = sum(R * W for R, _, W in self.steps)
+        if cells * (0.125 if HUB_ABITS else 2) > HUB_MEM_BUDGET:
+            # checked before any block is allocated
+            raise ValueError(f"stair split: {cells} cells exceed the dense-block budget")
         C = self.steps[-1][1] + self.steps[-1][2]
         self.T = C
         self.delta = delta
@@ -434,11 +440,6 @@ def pack(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec):
 
 
 _SIDE_STREAMS: dict = {}
-# "1": the staircase GEMM on a side stream concurrently with the tail SpMM
-# (joined by gc_hub_merge_rows).  Off by default: measured 2.21 vs 1.94 ms on
-# Reddit K=256 — the persistent GEMM holds every SM (one 220 KB CTA each), so
-# the tail does not overlap it and the join pass is pure overhead
-HUB_CONCURRENT = os.environ.get("GNNC_HUB_CONCURRENT", "0") == "1"
 
 
 def dense_part(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, out: torch.Tensor, *,
@@ -504,57 +505,6 @@ def _stair_gemm(plan, K: int, packed, out: torch.Tensor, d_row: torch.Tensor, fl
         st)), "hub_stair_gemm")
 
 
-def _rank_tables(plan, d_row: torch.Tensor):
-    """(rank int32[n]: row -> degree rank, d_row in rank order for the first
-    rows0 ranks), cached on the plan per d_row tensor."""
-    if getattr(plan, "_rank", None) is None:
-        rank = torch.empty_like(plan.row_map)
-        rank[plan.row_map.long()] = torch.arange(plan.row_map.numel(), dtype=torch.int32,
-                                                 device=plan.row_map.device)
-        plan._rank = rank
-    key = (d_row.data_ptr(), d_row._version, d_row.numel())
-    cache = getattr(plan, "_d_rank", None)
-    if cache is None or cache[0] != key:
-        plan._d_rank = (key, d_row[plan.row_map[:plan.rows0].long()].contiguous())
-    return plan._rank, plan._d_rank[1]
-
-
-def _concurrent_aggregate(a: CsrMatrix, x: torch.Tensor, d, spec, out: torch.Tensor, *,
-                          d_row: torch.Tensor, values, relu: bool, packed) -> None:
-    """The staircase GEMM (side stream, rank-ordered rows into a scratch G)
-    runs concurrently with the tail SpMM (writing every row of ``out``); a
-    join kernel adds G through the rank table and applies ReLU.  The GEMM
-    streams its 0/1 blocks from HBM while the tail is bound by L2 gathers, so
-    the two overlap; the tail also stops reading ``out`` back."""
-    plan = hub_plan(a, spec)
-    dev = x.device
-    K = x.shape[1]
-    rank, d_rank = _rank_tables(plan, d_row)
-    main = torch.cuda.current_stream(dev)
-    side = _SIDE_STREAMS.setdefault(dev, torch.cuda.Stream(dev))
-    g = torch.empty(plan.rows0, K, dtype=torch.float32, device=dev)
-    side.wait_stream(main)
-    with torch.cuda.stream(side):
-        pk = packed if packed is not None else pack(a, x, d, spec)
-        _stair_gemm(plan, K, pk, g, d_rank, 0, rank_order=True)
-    g.record_stream(side)
-    for t in pk[:2]:
-        t.record_stream(side)
-    tail = plan.tail_block(values, 0, a.n_rows)
-    if values is None:
-        _spmm(tail, x, weighted=False, d_row=d_row, d_col=d, relu=False, out=out,
-              accumulate=False, timer="spmm_tail")
-    else:
-        _spmm(tail, x, weighted=True, relu=False, out=out, accumulate=False, timer="spmm_tail")
-    done = torch.cuda.Event()
-    done.record(side)
-    main.wait_event(done)
-    nat.check(nat.load().gc_hub_merge_rows(g.data_ptr(), _ld(g), plan.rows0, rank.data_ptr(),
-                                           out.data_ptr(), _ld(out), a.n_rows, K,
-                                           nat.GC_RELU if relu else 0, _stream(dev)),
-              "hub_merge_rows")
-
-
 def tail_part(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, out: torch.Tensor, *,
               d_row: torch.Tensor, values=None, relu=False, rows: tuple[int, int] | None = None):
     """out (rows [lo, hi)) += the remaining edges (ReLU on the total)."""
@@ -598,15 +548,7 @@ def hybrid_aggregate(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, *,
     elif tuple(out.shape) != (hi - lo, K) or out.stride(1) != 1:
         raise ShapeError(f"hybrid_aggregate: out must be a row-major {hi - lo}x{K} tensor")
 
-    plan = hub_plan(a, spec)
-    concurrent = (HUB_CONCURRENT and plan.kind == "stair" and not accumulate
-                  and (rows is None or tuple(rows) == (0, a.n_rows)))
-
     def run():
-        if concurrent:
-            _concurrent_aggregate(a, x, d, spec, out, d_row=d_row, values=values, relu=relu,
-                                  packed=packed)
-            return 0
         dense_part(a, x, d, spec, out, d_row=d_row, accumulate=accumulate, packed=packed,
                    rows=rows)
         tail_part(a, x, d, spec, out, d_row=d_row, values=values, relu=relu, rows=rows)
@@ -616,39 +558,49 @@ def hybrid_aggregate(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, *,
     return out
 
 
-def _block_candidates(a: CsrMatrix) -> list[int]:
-    counts = torch.bincount(a.col_idx.long(), minlength=a.n_cols)
-    top = torch.sort(counts, descending=True).values.double().cumsum(0)
-    out = []
-    for T in HUB_T_CANDIDATES:
-        if T > a.n_cols // 8 or a.n_rows * T * 2 > HUB_MEM_BUDGET:
-            continue
-        if float(top[T - 1]) / (a.n_rows * T) >= HUB_MIN_DENSITY:
-            out.append(T)
-    return out
+def _candidates(K: int) -> list:
+    """Staircase specs tried by the autotuner for this K.  (Block plans —
+    ``HubPlan`` — never beat the staircase on the measured shapes; they stay
+    reachable through GNNC_HUB_SPLIT=<T>.)"""
+    if not nat.load().gc_hub_stair_supported(K):
+        return []
+    return [("stair", int(round(dl * 1000)), int(round(sl * 10))) for dl, sl in _stair_candidates(K)]
 
 
-def _candidates(a: CsrMatrix, K: int) -> list:
-    cands: list = list(_block_candidates(a))
-    if nat.load().gc_hub_stair_supported(K):
-        for dl, sl in _stair_candidates(K):
-            spec = ("stair", int(round(dl * 1000)), int(round(sl * 10)))
-            try:
-                plan = hub_plan(a, spec)
-            except ValueError:
-                continue
-            if plan.cells * (0.125 if getattr(plan, "abits", False) else 2) <= HUB_MEM_BUDGET:
-                cands.append(spec)
-            else:
-                a._plans.pop(("hubsplit", spec), None)
-    return cands
+def _time_interleaved(runs: dict, rounds: int) -> dict:
+    """Median CUDA-event time per run over ``rounds`` interleaved rounds, after
+    one warm call each (clock / power-cap drift hits every candidate alike)."""
+    for fn in runs.values():
+        fn()
+    samples: dict = {k: [] for k in runs}
+    for _ in range(rounds):
+        ev = {}
+        for k, fn in runs.items():
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            ev[k] = (e0, e1)
+        torch.cuda.synchronize()
+        for k, (e0, e1) in ev.items():
+            samples[k].append(e0.elapsed_time(e1))
+    return {k: float(sorted(v)[len(v) // 2]) for k, v in samples.items()}
 
 
 def choose_split(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, *,
                  d_row: torch.Tensor | None = None, values: torch.Tensor | None = None):
     """Split spec for (pattern, K): 0 (plain SpMM) unless a dense split is
-    measurably faster.  Every candidate is timed once (median of 3 after a
-    warm launch) on the first call and the choice is cached on the pattern."""
+    measurably faster, chosen on the first call and cached on the pattern.
+
+    The candidates run as a tournament: each staircase plan is built (its
+    block budget checked before allocation), timed against the current best
+    in interleaved rounds, and the loser's blocks are freed at once — at most
+    two plans are resident.  Device OOM while building or timing a candidate
+    drops that candidate (the plain SpMM always remains).  Build time,
+    autotune time and the peak extra device memory are recorded under
+    ``a._plans[("hubsplit-choice", K, weighted, "stats")]``."""
+    import time
+
     mode = str(HUB_SPLIT)
     if mode == "0" or not a.has_unit_values:
         return 0
@@ -670,45 +622,55 @@ def choose_split(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, *,
     if a.nnz < HUB_MIN_NNZ or x.stride(1) != 1:
         a._plans[key] = 0
         return 0
-    cands = _candidates(a, K)
+    cands = _candidates(K)
     if not cands:
         a._plans[key] = 0
         return 0
-    scratch = torch.empty(a.n_rows, K, dtype=torch.float32, device=x.device)
+    dev = x.device
+    t_start = time.perf_counter()
+    torch.cuda.synchronize(dev)
+    mem0 = torch.cuda.memory_allocated(dev)
+    torch.cuda.reset_peak_memory_stats(dev)
+    scratch = torch.empty(a.n_rows, K, dtype=torch.float32, device=dev)
     src = a if values is None else a.with_values(values)
 
     def plain():
         _spmm(src, x, weighted=values is not None, d_row=None if values is not None else d_row,
               d_col=None if values is not None else d, out=scratch, timer=None)
 
-    # every candidate once to warm up (plans, autotuned tail variants), then
-    # AUTOTUNE_ROUNDS interleaved rounds (drift in clocks / power cap hits
-    # all candidates alike); the median per candidate decides
-    runs = {0: plain}
+    def hybrid(spec):
+        return lambda: hybrid_aggregate(a, x, d, spec, d_row=d_row, values=values, out=scratch)
+
+    best, times, build_s = 0, {}, 0.0
     for spec in cands:
-        runs[spec] = (lambda spec=spec: hybrid_aggregate(a, x, d, spec, d_row=d_row,
-                                                         values=values, out=scratch))
-    for fn in runs.values():
-        fn()
-    samples: dict = {k: [] for k in runs}
-    for _ in range(AUTOTUNE_ROUNDS):
-        ev = {}
-        for k, fn in runs.items():
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            fn()
-            e1.record()
-            ev[k] = (e0, e1)
-        torch.cuda.synchronize()
-        for k, (e0, e1) in ev.items():
-            samples[k].append(e0.elapsed_time(e1))
-    times = {k: float(sorted(v)[len(v) // 2]) for k, v in samples.items()}
-    best = min(times, key=times.get)
-    if best != 0 and times[best] >= 0.97 * times[0]:
-        best = 0
-    for spec in cands:  # keep only the chosen plan resident
-        if spec != best:
+        try:
+            t0 = time.perf_counter()
+            hub_plan(a, spec)
+            torch.cuda.synchronize(dev)
+            build_s += time.perf_counter() - t0
+            runs = {best: plain if best == 0 else hybrid(best), spec: hybrid(spec)}
+            tt = _time_interleaved(runs, AUTOTUNE_ROUNDS)
+        except ValueError:
+            continue  # no step pays for its cells, or over the block budget
+        except torch.cuda.OutOfMemoryError:
             a._plans.pop(("hubsplit", spec), None)
+            torch.cuda.empty_cache()
+            continue
+        times.update(tt)
+        # a split must be clearly (> 3 %) faster than the plain SpMM
+        win = tt[spec] < tt[best] and (best != 0 or tt[spec] < 0.97 * tt[0])
+        loser = best if win else spec
+        if win:
+            best = spec
+        if loser != 0:
+            a._plans.pop(("hubsplit", loser), None)  # free its blocks now
+    del scratch
+    torch.cuda.synchronize(dev)
     a._plans[key] = best
     a._plans[key + ("times",)] = {spec_label(s): round(t, 4) for s, t in times.items()}
+    a._plans[key + ("stats",)] = {
+        "plan_build_s": round(build_s, 3),
+        "autotune_s": round(time.perf_counter() - t_start, 3),
+        "peak_extra_bytes": int(torch.cuda.max_memory_allocated(dev) - mem0),
+        "resident_plan_bytes": int(hub_plan(a, best).cells * (0.125 if HUB_ABITS else 2)) if best else 0}
     return best

@@ -255,6 +255,16 @@ class CsrMatrix:
                             else values).to(dev, torch.float64).reshape(-1)
         if not (r.shape == c.shape == v.shape):
             raise ShapeError("rows/cols/values must have equal length")
+        # range checks before the (row, col) key is formed: an out-of-range
+        # column would otherwise alias a valid entry of the next row and be
+        # summed into it (the reference lexsorts and raises in _check)
+        # (rows first: the reference's row_ptr-length check precedes the
+        # column check)
+        if r.numel():
+            if int(r.min()) < 0 or int(r.max()) >= int(n_rows):
+                raise ShapeError("row index out of range")
+            if int(c.min()) < 0 or int(c.max()) >= int(n_cols):
+                raise ShapeError("column index out of range")
         key = r * max(int(n_cols), 1) + c
         key, order = torch.sort(key, stable=True)
         r, c, v = r[order], c[order], v[order]
@@ -322,11 +332,7 @@ class CsrMatrix:
                     f.write(b"\0" * pad)
 
     @classmethod
-    def load(cls, path, device=None, validate: bool = True) -> "CsrMatrix":
-        """Read a ``.gcsr`` file written by :meth:`save` onto ``device``.
-        Truncated or foreign files raise ``ShapeError``; the CSR invariants
-        are checked on the device unless ``validate=False``."""
-        dev = torch.device(device) if device is not None else default_device()
+    def _gcsr_header(cls, path):
         if os.path.getsize(path) < 64:
             raise ShapeError(f"{path}: not a .gcsr file (shorter than its header)")
         raw = np.memmap(path, dtype=np.uint8, mode="r")
@@ -339,22 +345,49 @@ class CsrMatrix:
         flags = int(raw[32:36].view("<u4")[0])
         if min(n_rows, n_cols, nnz) < 0:
             raise ShapeError(f"{path}: negative dimension in header")
+        rp_bytes = 4 * (n_rows + 1)
+        ci_off = 64 + rp_bytes + (-rp_bytes) % 64
+        va_off = ci_off + 4 * nnz + (-4 * nnz) % 64
         unit = bool(flags & 1)
-        off = 64
+        need = (ci_off + 4 * nnz) if unit else (va_off + 4 * nnz)
+        if raw.size < need:
+            raise ShapeError(f"{path}: truncated .gcsr file")
+        return raw, n_rows, n_cols, nnz, unit, ci_off, va_off
 
-        def section(count: int, dt: str) -> torch.Tensor:
-            nonlocal off
-            nbytes = count * 4
-            if off + nbytes > raw.size:
-                raise ShapeError(f"{path}: truncated .gcsr file")
-            host = torch.from_numpy(np.array(raw[off:off + nbytes].view(dt), copy=True))
-            off += nbytes + (-nbytes) % 64
+    @classmethod
+    def read_row_ptr(cls, path) -> np.ndarray:
+        """The row_ptr of a ``.gcsr`` file as a host int64 array (O(n) bytes
+        read; col_idx / values are not touched)."""
+        raw, n_rows, *_ = cls._gcsr_header(path)
+        return raw[64:64 + 4 * (n_rows + 1)].view("<i4").astype(np.int64)
+
+    @classmethod
+    def load(cls, path, device=None, validate: bool = True,
+             rows: tuple[int, int] | None = None) -> "CsrMatrix":
+        """Read a ``.gcsr`` file written by :meth:`save` onto ``device``.
+        ``rows=(lo, hi)`` reads only that row block (rebased row_ptr, global
+        column ids — a partition's local adjacency): only those rows' bytes of
+        col_idx / values are read.  Truncated or foreign files raise
+        ``ShapeError``; the CSR invariants are checked on the device unless
+        ``validate=False``."""
+        dev = torch.device(device) if device is not None else default_device()
+        raw, n_rows, n_cols, nnz, unit, ci_off, va_off = cls._gcsr_header(path)
+        lo, hi = (0, n_rows) if rows is None else (int(rows[0]), int(rows[1]))
+        if not 0 <= lo <= hi <= n_rows:
+            raise ShapeError(f"{path}: row range [{lo}, {hi}) outside [0, {n_rows})")
+        rp_host = np.array(raw[64 + 4 * lo:64 + 4 * (hi + 1)].view("<i4"), copy=True)
+        b, e = int(rp_host[0]), int(rp_host[-1])
+        if not 0 <= b <= e <= nnz:
+            raise ShapeError(f"{path}: corrupt row_ptr")
+
+        def section(off: int, dt: str) -> torch.Tensor:
+            host = torch.from_numpy(np.array(raw[off + 4 * b:off + 4 * e].view(dt), copy=True))
             return host.to(dev, non_blocking=False)
 
-        rp = section(n_rows + 1, "<i4")
-        ci = section(nnz, "<i4")
-        va = torch.ones(nnz, dtype=torch.float32, device=dev) if unit else section(nnz, "<f4")
-        out = cls(n_rows, n_cols, rp, ci, va, validate=validate, device=dev)
+        rp = torch.from_numpy(rp_host - b).to(dev)
+        ci = section(ci_off, "<i4")
+        va = torch.ones(e - b, dtype=torch.float32, device=dev) if unit else section(va_off, "<f4")
+        out = cls(hi - lo, n_cols, rp, ci, va, validate=validate, device=dev)
         if unit:
             out._unit = True
         return out
@@ -569,18 +602,26 @@ def _variant(a: CsrMatrix, K: int, mode: str, probe) -> tuple[bool, int]:
 
 
 def gat_sddmm_aggregate(a: CsrMatrix, a_src: torch.Tensor, a_dst: torch.Tensor, slope: float, b,
-                        *, relu: bool = False, out=None, algo: str = "auto"):
+                        *, relu: bool = False, out=None, algo: str = "auto", b_self=None):
     """GAT reuse aggregation with SDDMM attention fused in: per edge the
     gathered row B_j gives both e = LeakyReLU(a_src.B_i + a_dst.B_j) and the
-    aggregated term (one gather per edge; α never written).  Returns None when
-    the operand shape is outside the kernel's range (K > 256, unaligned)."""
+    aggregated term (one gather per edge; α never written).  ``b_self``: the
+    rows B_i of the pattern's own rows when ``a`` is a row block (a rank's
+    rows of a partitioned graph, B the gathered operand); default ``b`` with a
+    square pattern.  Returns None when the operand shape is outside the
+    kernel's range (K > 1024, unaligned)."""
     dev = a.device
     bt = b
     K = bt.shape[1]
-    if a.n_rows != a.n_cols or bt.shape[0] != a.n_rows:
-        raise ShapeError("gat_sddmm_aggregate: square pattern and one B row per node required")
+    if bt.shape[0] != a.n_cols:
+        raise ShapeError("gat_sddmm_aggregate: one B row per column of the pattern required")
+    if b_self is None and a.n_rows != a.n_cols:
+        raise ShapeError("gat_sddmm_aggregate: a rectangular pattern needs b_self")
+    if b_self is not None and (tuple(b_self.shape) != (a.n_rows, K) or b_self.stride(1) != 1):
+        raise ShapeError("gat_sddmm_aggregate: b_self must be a row-major n_rows x K tensor")
     if (K > 1024 or K % 4 or _ld(bt) % 4 or bt.data_ptr() % 16 or a_src.data_ptr() % 16
-            or a_dst.data_ptr() % 16):
+            or a_dst.data_ptr() % 16
+            or (b_self is not None and (_ld(b_self) % 4 or b_self.data_ptr() % 16))):
         return None
     _require_cuda(a.col_idx, bt, a_src, a_dst)
     if out is None:
@@ -594,7 +635,8 @@ def gat_sddmm_aggregate(a: CsrMatrix, a_src: torch.Tensor, a_dst: torch.Tensor, 
     def launch(cols, extra):
         return lib.gc_gat_sddmm_aggregate_f32(
             a.row_ptr.data_ptr(), cols.data_ptr(), a_src.data_ptr(), a_dst.data_ptr(), float(slope),
-            bt.data_ptr(), _ld(bt), a.n_rows, K, out.data_ptr(), _ld(out), flags | extra, code,
+            bt.data_ptr(), _ld(bt), _ptr(b_self), 0 if b_self is None else _ld(b_self), a.n_rows, K,
+            out.data_ptr(), _ld(out), flags | extra, code,
             _ptr(items), n_items, _ptr(split), n_split, _ptr(ws), 0 if ws is None else ws.numel() * 4,
             _stream(dev))
 
@@ -694,50 +736,48 @@ def gat_aggregate(a: CsrMatrix, s: torch.Tensor, t: torch.Tensor, slope: float, 
     return op.wrap(out)
 
 
-def gat_aggregate_mh(a: CsrMatrix, s: torch.Tensor, t: torch.Tensor, slope: float, b, heads: int,
-                     *, relu: bool = False, out=None, algo: str = "auto"):
-    """Multi-head fused GAT aggregation in one pass over the pattern: ``b`` is
-    n_cols x (heads*k2) (head h in column block h), ``s`` / ``t`` are
-    [heads, n_rows] / [heads, n_cols]; equal to ``heads`` ``gat_aggregate``
-    calls on the column blocks (A16 of SURVEY.md §8(a), N1 of §8(f))."""
-    dev = a.device
-    op = _Operand(b, dev)
-    bt = op.t
-    if a.n_cols != bt.shape[0]:
-        raise ShapeError(f"gat_aggregate_mh: a is {a.n_rows}x{a.n_cols}, b has {bt.shape[0]} rows")
-    K = bt.shape[1]
-    if heads < 1 or K % heads:
-        raise ShapeError("gat_aggregate_mh: b's width must be heads * k2")
-    if tuple(s.shape) != (heads, a.n_rows) or tuple(t.shape) != (heads, a.n_cols) \
-            or not (s.is_contiguous() and t.is_contiguous()):
-        raise ShapeError("gat_aggregate_mh: s/t must be contiguous [heads, n] score arrays")
-    _require_cuda(a.col_idx, bt, s, t)
-    if out is None:
-        out = torch.empty(a.n_rows, K, dtype=torch.float32, device=dev)
-    elif tuple(out.shape) != (a.n_rows, K) or out.stride(1) != 1:
-        raise ShapeError(f"gat_aggregate_mh: out must be a row-major {a.n_rows}x{K} tensor")
-    code, items, n_items, split, n_split, ws = _plan_args(a, K, algo, dev, gat=True, heads=heads)
-    lib = nat.load()
-    flags = nat.GC_RELU if relu else 0
-
-    def launch(cols, extra, dst=out):
-        return lib.gc_gat_aggregate_mh_f32(
-            a.row_ptr.data_ptr(), cols.data_ptr(), s.data_ptr(), t.data_ptr(), int(heads),
-            K // heads, float(slope), bt.data_ptr(), _ld(bt), a.n_rows, a.n_cols, dst.data_ptr(),
-            _ld(dst), flags | extra, code, _ptr(items), n_items, _ptr(split), n_split, _ptr(ws),
-            0 if ws is None else ws.numel() * 4, _stream(dev))
-
-    def probe(cols, extra):
-        nat.check(launch(cols, extra), "gat_aggregate_mh")  # writes `out`; the real launch follows
-
-    hints, shrink = _variant(a, K, "gatmh", probe)
-    cols = a.hub_tagged_cols(K) if hints else a.col_idx
-    extra = (nat.GC_HUB_TAGGED if hints else 0) | nat.GC_SPMM_SHRINK(shrink)
-    rc = _timed_call("spmm", dev, lambda: launch(cols, extra))
-    nat.check(rc, "gat_aggregate_mh")
-    return op.wrap(out)
+def device_hook(fn):
+    """Mark an ``spmm_fn`` hook as device-aware: it receives this package's
+    device ``CsrMatrix`` and CUDA operands.  Unmarked hooks get the
+    reference's host contract (:func:`call_spmm_hook`)."""
+    fn.__gnnc_device__ = True
+    return fn
 
 
+class HostCsrView:
+    """Host copy of a CSR with the reference ``CsrMatrix`` attributes
+    (``n_rows``, ``n_cols``, int64 ``row_ptr``/``col_idx``, float64
+    ``values``, ``nnz``, ``has_unit_values``) — what a reference-style hook
+    such as ``gnncompose.sparse.spmm`` (sparse.py:240-247) reads."""
+
+    def __init__(self, a: CsrMatrix):
+        self.n_rows, self.n_cols = a.n_rows, a.n_cols
+        self.row_ptr, self.col_idx, self.values = a.numpy()
+        self.has_unit_values = a.has_unit_values
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col_idx.size)
+
+
+def call_spmm_hook(fn, a: CsrMatrix, b):
+    """Run a user ``spmm_fn(a, b)`` (reference gcn.py:125-161, gat.py:121-153).
+    Device-aware hooks (:func:`device_hook`; this package's ``spmm`` and
+    ``spmm_unweighted``) get the device operands.  Any other hook gets the
+    reference's host contract — a :class:`HostCsrView` and a float64 ndarray —
+    and its ndarray result is uploaded as float32."""
+    if getattr(fn, "__gnnc_device__", False):
+        out = fn(a, b)
+    else:
+        bh = b.detach().cpu().numpy().astype(np.float64) if isinstance(b, torch.Tensor) else \
+            np.asarray(b, dtype=np.float64)
+        out = fn(HostCsrView(a), bh)
+    if not isinstance(out, torch.Tensor):
+        out = torch.from_numpy(np.ascontiguousarray(out, dtype=np.float32))
+    return out.to(a.device, torch.float32)
+
+
+@device_hook
 def spmm(a: CsrMatrix, b, **kw):
     """Sparse-times-dense product C[i,k] = sum_j a[i,j] * b[j,k] (sparse.py:240-247).
 
@@ -746,6 +786,7 @@ def spmm(a: CsrMatrix, b, **kw):
     return _spmm(a, b, weighted=True, what="spmm", **kw)
 
 
+@device_hook
 def spmm_unweighted(a: CsrMatrix, b, **kw):
     """SpMM over the pattern only; ``a.values`` is never read (sparse.py:250-264).
     Bit-identical to ``spmm`` with unit values (same per-row order)."""

@@ -54,7 +54,7 @@ def test_tcgen05_and_tma_in_sass(lib):
 
 
 def test_abi_version_and_counters(lib):
-    assert lib.gc_abi_version() == 1
+    assert lib.gc_abi_version() == _native.ABI_VERSION == 2
     assert isinstance(_native.launch_count(), int)
 
 

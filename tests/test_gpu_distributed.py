@@ -83,3 +83,69 @@ def test_partitioned_layer_with_hub_split_on_gpu(oracle, comp, order, overlap):
     ref = oracle.gcn_layer(og, h.astype(np.float64), w.astype(np.float64), comp, order)
     assert oracle.rel_err(full, ref) <= 1e-4
     _ = gc
+
+
+def _gat_worker(rank, world, port, comp, att, heads, q):
+    import sys
+    from pathlib import Path
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2306_15155_b200 as gc
+        from paper_2306_15155_b200 import graphs
+        from paper_2306_15155_b200.distributed import RowPartition, all_gather_rows, dist_gat_layer
+
+        dev = torch.device("cuda", 0)
+        at = gc.add_self_loops(graphs.powerlaw_graph(3000, 30, seed=12, device=dev))
+        rng = np.random.default_rng(21)
+        k1, k2 = 48, 32
+        h = torch.from_numpy(rng.uniform(-0.5, 0.5, (3000, k1)).astype(np.float32)).to(dev)
+        w = rng.uniform(-0.5, 0.5, (k1, k2 * heads)).astype(np.float32)
+        a_s = rng.uniform(-0.5, 0.5, k2 * heads).astype(np.float32)
+        a_d = rng.uniform(-0.5, 0.5, k2 * heads).astype(np.float32)
+        gc.set_gemm_precision("fp32")
+        spec = gc.GatLayerSpec(k1, k2, w, a_s, a_d, composition=comp, attention=att, heads=heads)
+        part = RowPartition.of(at, rank, world)
+        out = dist_gat_layer(part, h[part.lo:part.hi], spec)
+        full = all_gather_rows(out.cpu(), part)
+        if rank == 0:
+            q.put(full.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("comp,att", [("reuse", "reassoc"), ("reuse", "sddmm"),
+                                      ("recompute", "reassoc"), ("recompute", "sddmm")])
+@pytest.mark.parametrize("heads", [1, 4])
+def test_partitioned_gat_layer_on_gpu(oracle, comp, att, heads):
+    """dist_gat_layer with the real kernels (2 gloo ranks sharing cuda:0):
+    the concatenated rank outputs equal the single-process oracle (fp32 mode,
+    1e-4)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gat_worker, args=(r, 2, port, comp, att, heads, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    full = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from paper_2306_15155_b200 import graphs
+
+    rp, ci, v = graphs.powerlaw_graph(3000, 30, seed=12, device="cuda").numpy()
+    at = oracle.add_self_loops(oracle.Csr(3000, 3000, rp, ci, v))
+    rng = np.random.default_rng(21)
+    k1, k2 = 48, 32
+    h = rng.uniform(-0.5, 0.5, (3000, k1)).astype(np.float32).astype(np.float64)
+    w = rng.uniform(-0.5, 0.5, (k1, k2 * heads)).astype(np.float32).astype(np.float64)
+    a_s = rng.uniform(-0.5, 0.5, k2 * heads).astype(np.float32).astype(np.float64)
+    a_d = rng.uniform(-0.5, 0.5, k2 * heads).astype(np.float32).astype(np.float64)
+    ref = oracle.gat_layer_multihead(at, h, w, a_s, a_d, heads, 0.2, comp, "relu")
+    assert oracle.rel_err(full, ref) <= 1e-4

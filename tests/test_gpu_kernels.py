@@ -395,6 +395,7 @@ def test_spmm_fn_hook_is_used(golden):
     g = gc.NormalizedGraph.from_adjacency(golden_graph(golden, "grid4x5"), precompute=True)
     calls = []
 
+    @gc.device_hook
     def my_spmm(a, b):
         calls.append(a.nnz)
         return gc.spmm(a, b)
@@ -405,6 +406,35 @@ def test_spmm_fn_hook_is_used(golden):
         out = gc.gcn_layer(g, h, gc.GcnLayerSpec(5, 5, w, composition=comp), spmm_fn=my_spmm)
         assert _rel(out, golden[f"{key}/gcn/{comp}/heuristic"]) <= 1e-2
     assert len(calls) == 2
+
+
+def test_host_spmm_fn_hook_gets_reference_operands(golden, oracle):
+    """An unmarked hook gets the reference's host contract (a CsrMatrix-like
+    view with int64/float64 numpy arrays, a float64 ndarray) — e.g. the
+    reference's own numpy/numba spmm, here its oracle restatement."""
+    g = gc.NormalizedGraph.from_adjacency(golden_graph(golden, "grid4x5"), precompute=True)
+    seen = []
+
+    def host_spmm(a, b):
+        assert isinstance(b, np.ndarray) and b.dtype == np.float64
+        assert a.row_ptr.dtype == np.int64 and a.values.dtype == np.float64
+        seen.append(a.nnz)
+        return oracle.spmm(oracle.Csr(a.n_rows, a.n_cols, a.row_ptr, a.col_idx, a.values), b)
+
+    key = "grid4x5/5x5"
+    h, w = golden[f"{key}/h"], golden[f"{key}/w"]
+    for comp in ("precompute", "dynamic"):
+        out = gc.gcn_layer(g, h, gc.GcnLayerSpec(5, 5, w, composition=comp), spmm_fn=host_spmm)
+        assert _rel(out, golden[f"{key}/gcn/{comp}/heuristic"]) <= 1e-2
+    rng = np.random.default_rng(3)
+    a_s, a_d = rng.uniform(-0.5, 0.5, 5), rng.uniform(-0.5, 0.5, 5)
+    for comp in ("reuse", "recompute"):
+        spec = gc.GatLayerSpec(5, 5, w, a_s, a_d, composition=comp)
+        ref = gc.gat_layer(g.a_tilde, torch.as_tensor(h, dtype=torch.float32, device=DEV), spec)
+        out = gc.gat_layer(g.a_tilde, torch.as_tensor(h, dtype=torch.float32, device=DEV), spec,
+                           spmm_fn=host_spmm)
+        assert _rel(out.cpu().numpy(), ref.cpu().numpy()) <= 1e-5
+    assert len(seen) == 4
 
 
 @pytest.mark.parametrize("K", [1, 7, 32, 64, 256])
@@ -759,26 +789,6 @@ def test_host_pipelined_layer_with_stair_split(oracle, stair_pl, monkeypatch):
     assert any(("hubsplit", ("stair", 50, 10)) in b._plans for b in blocks)
 
 
-@pytest.mark.parametrize("relu", [True, False])
-def test_stair_split_concurrent_join(oracle, stair_pl, relu, monkeypatch):
-    """Opt-in concurrent form: staircase GEMM into rank-ordered scratch on a
-    side stream, tail SpMM writing every row, gc_hub_merge_rows join."""
-    from paper_2306_15155_b200 import hub
-    monkeypatch.setattr(hub, "HUB_CONCURRENT", True)
-    g = gc.NormalizedGraph.from_adjacency(stair_pl).with_precomputed()
-    a = g.a_tilde
-    spec = ("stair", 50, 10)
-    a._plans[("hubsplit", spec)] = hub.StairPlan(a, 0.05, n_clusters=1, first_band=256)
-    og = oracle.GcnGraph.from_adjacency(to_oracle(oracle, stair_pl))
-    rng = np.random.default_rng(21)
-    x = f32(rng.uniform(-0.5, 0.5, (a.n_rows, 128)))
-    d = g.d_inv_sqrt.to(DEV)
-    out = hub.hybrid_aggregate(a, torch.from_numpy(x).to(DEV), d, spec, relu=relu)
-    ref = oracle.spmm(og.n_tilde, x)
-    ref = np.maximum(ref, 0) if relu else ref
-    assert oracle.rel_err(out.cpu().numpy(), ref) < hub_tol()
-
-
 def test_host_pipelined_stair_split_tf32_mode(oracle, stair_pl, monkeypatch):
     """The bench's e2e configuration: TF32 mode (one-term MN-major dense
     operand on every row block), pinned host H, row-block pipeline; layer
@@ -841,26 +851,6 @@ def test_gcsr_load_to_device_and_partition(tmp_path, oracle):
     rp = a.row_ptr.cpu().numpy().astype(np.int64)
     for parts in (2, 3, 8):
         assert np.array_equal(partition_rows_device(b.row_ptr, parts), oracle.partition_rows(rp, parts))
-
-
-@pytest.mark.parametrize("heads,k2", [(2, 16), (3, 24), (4, 32), (4, 64), (8, 32), (4, 256)])
-@pytest.mark.parametrize("algo", ["row", "split"])
-def test_gat_aggregate_multihead_one_pass(hubgraph, heads, k2, algo):
-    """gat_aggregate_mh (all heads in one pass over the pattern, per-head
-    online softmax; split plans merge per-head (max, sum) pairs) equals one
-    fused aggregation per head on the column blocks."""
-    from paper_2306_15155_b200.sparse import gat_aggregate, gat_aggregate_mh
-    rng = np.random.default_rng(heads * 7 + k2)
-    n = hubgraph.n_rows
-    hw = torch.from_numpy(f32(rng.standard_normal((n, heads * k2)))).to(DEV)
-    s = torch.from_numpy(f32(rng.standard_normal((heads, n)))).to(DEV)
-    t = torch.from_numpy(f32(rng.standard_normal((heads, n)))).to(DEV)
-    out = gat_aggregate_mh(hubgraph, s, t, 0.2, hw, heads, relu=True, algo=algo)
-    for hd in range(heads):
-        ref = gat_aggregate(hubgraph, s[hd], t[hd], 0.2, hw[:, hd * k2:(hd + 1) * k2].contiguous(),
-                            relu=True, algo=algo)
-        got = out[:, hd * k2:(hd + 1) * k2]
-        assert torch.allclose(got, ref, rtol=2e-5, atol=2e-6), (hd, float((got - ref).abs().max()))
 
 
 @pytest.fixture(scope="module")

@@ -43,6 +43,19 @@ def test_from_coo_matches_reference_golden(golden):
     assert np.array_equal(v, golden["coo/out/values"].astype(np.float32))
 
 
+def test_from_coo_rejects_out_of_range_before_merging():
+    """an out-of-range column must raise, not alias a valid entry
+    of the next row and be summed into it (reference lexsort + _check)."""
+    with pytest.raises(gc.ShapeError, match="column index out of range"):
+        gc.CsrMatrix.from_coo(3, 3, [1, 0], [0, 3], [1, 1], device=CPU)
+    with pytest.raises(gc.ShapeError, match="column index out of range"):
+        gc.CsrMatrix.from_coo(3, 3, [0], [-1], [1.0], device=CPU)
+    with pytest.raises(gc.ShapeError):
+        gc.CsrMatrix.from_coo(2, 2, [2], [0], [1.0], device=CPU)
+    with pytest.raises(ValueError):
+        gc.CsrMatrix.from_coo(2, 2, [-1], [0], [1.0], device=CPU)
+
+
 def test_validation_rejects_bad_row_ptr():
     with pytest.raises(gc.ShapeError):
         gc.CsrMatrix(2, 2, np.array([0, 1]), np.array([0]), np.array([1.0]), device=CPU)
@@ -352,21 +365,6 @@ def test_stair_plan_partitions_the_pattern(abits, monkeypatch):
     assert plan.hub_edges == edges
 
 
-def test_host_pipeline_spans_cover_rows_in_order():
-    """The e2e row-block schedule (gcn._pipeline_spans): contiguous blocks
-    covering every row once, processed from the last rows to the first, never
-    slower than one block under the pipeline model."""
-    from paper_2306_15155_b200 import gcn
-
-    a = graphs.synthetic_graph("rmat", 20000, 2_000_000, seed=1, device="cpu")
-    rp = a.row_ptr.numpy().astype(np.float64)
-    spans = gcn._pipeline_spans(rp)
-    assert spans[0][1] == a.n_rows and spans[-1][0] == 0
-    for (lo, hi), (lo2, hi2) in zip(spans, spans[1:]):
-        assert hi2 == lo and lo2 < hi2
-    assert gcn._simulate_pipeline(rp, spans) <= gcn._simulate_pipeline(rp, [(0, a.n_rows)])
-
-
 # ---- .gcsr binary CSR files (SURVEY.md §8(f) N3) -----------------------------
 
 
@@ -403,6 +401,46 @@ def test_gcsr_empty_and_rectangular(tmp_path):
         a.save(p)
         b = gc.CsrMatrix.load(p, device=CPU)
         assert torch.equal(b.to_dense(), a.to_dense()) and b.n_cols == a.n_cols
+
+
+@pytest.mark.parametrize("name", ["weighted40", "powerlaw200"])
+def test_gcsr_row_range_load_equals_take_rows(golden, tmp_path, name):
+    """CsrMatrix.load(rows=(lo, hi)) reads only that row block: equal to
+    take_rows of the whole matrix (rebased row_ptr, global column ids)."""
+    a = gcsr(golden, f"{name}/A")
+    p = tmp_path / f"{name}.gcsr"
+    a.save(p)
+    assert np.array_equal(gc.CsrMatrix.read_row_ptr(p), a.row_ptr.numpy().astype(np.int64))
+    n = a.n_rows
+    for lo, hi in ((0, n), (0, 0), (3, 17), (n // 2, n), (n, n)):
+        blk = gc.CsrMatrix.load(p, device=CPU, rows=(lo, hi))
+        ref = a.take_rows(lo, hi)
+        assert blk.n_rows == hi - lo and blk.n_cols == a.n_cols
+        for x, y in zip(blk.numpy(), ref.numpy()):
+            assert np.array_equal(x, y)
+    with pytest.raises(gc.ShapeError):
+        gc.CsrMatrix.load(p, device=CPU, rows=(5, 2))
+
+
+def test_partition_from_file_matches_in_memory(golden, tmp_path, oracle):
+    """The capacity path: each rank reads only its rows of Ã from the file;
+    bounds, block and D^-1/2 equal the in-memory partition of the same Ã."""
+    from paper_2306_15155_b200.distributed import RowPartition
+
+    at = gc.add_self_loops(gcsr(golden, "powerlaw200/A"))
+    p = tmp_path / "at.gcsr"
+    at.save(p)
+    d_ref = gc.inv_sqrt_degrees(at)
+    for world in (1, 2, 3, 5):
+        for rank in range(world):
+            part, d = RowPartition.from_file(p, rank, world, device=CPU)
+            ref = RowPartition.of(at, rank, world)
+            assert np.array_equal(part.bounds, ref.bounds)
+            assert np.array_equal(part.bounds, oracle.partition_rows(
+                at.row_ptr.numpy().astype(np.int64), world))
+            for x, y in zip(part.local.numpy(), ref.local.numpy()):
+                assert np.array_equal(x, y)
+            assert torch.equal(d, d_ref.to(torch.float32))
 
 
 def test_gcsr_rejects_bad_files(tmp_path):
