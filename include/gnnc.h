@@ -61,6 +61,7 @@ extern "C" {
 #define GC_SPMM_SHRINK_MASK (3u << 8)
 #define GC_GEMM_TF32 (1u << 4)  /* tcgen05.mma kind::tf32, TMEM accumulators, TMA operands */
 #define GC_GEMM_FP32 (1u << 5)  /* exact fp32 CUDA-core path (rtol 1e-4 parity mode) */
+#define GC_GEMM_TF32X3 (1u << 7) /* 3xTF32 on tcgen05: hi·hi + hi·lo + lo·hi, fp32-class (1e-4) */
 #define GC_HUB_A_BITS (1u << 6) /* gc_hub_stair_gemm: A_steps are bitmaps (see there) */
 
 /* SpMM work decomposition */

@@ -1,5 +1,6 @@
 """Row-sampled oracle layers for the full BASELINE shapes (SURVEY.md §8(c)
-step 5).  TEST INFRASTRUCTURE: the checker only.
+step 5).  TEST INFRASTRUCTURE: the checker only (used by tests/ and by
+bench.py's parity checks; never by the product package).
 
 The layer output rows ``rows`` depend on the operand rows of their
 neighbours only, so the reference layer (gcn.py:125-161, gat.py:121-153) is
@@ -14,7 +15,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from oracle import gnn_oracle as orc
+from . import gnn_oracle as orc
 
 
 def _remap(sub: "orc.Csr", rows: np.ndarray):

@@ -29,6 +29,7 @@ def GC_SPMM_SHRINK(s: int) -> int:  # noqa: N802 - mirrors the C macro
     return (int(s) & 3) << 8
 GC_GEMM_TF32 = 1 << 4
 GC_GEMM_FP32 = 1 << 5
+GC_GEMM_TF32X3 = 1 << 7
 GC_SPMM_ROW = 1
 GC_SPMM_NNZ_SPLIT = 2
 GC_PLAN_LENGTH_CLASSES = 1

@@ -255,14 +255,26 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 // issues TERMS MMAs per 32-byte step into the same accumulator, so
 // D = A·(B0 + B1 + B2) with the A tile read once.
 // ELEM: 0 = TF32 (kind::tf32), 1 = BF16, 2 = FP16 (kind::f16)
-template <int BN, int TERMS, int ELEM>
+//
+// SPLITA (TF32 only, TERMS = 2: B = [hi(W^T); lo(W^T)]): the 3xTF32
+// fp32-class product.  Four converter warps (6..9) rewrite each landed A tile
+// in place as hi = A with the 13 low mantissa bits cleared (exact in TF32)
+// and write lo = A - hi (exact in fp32) to a second tile of the stage; the
+// MMA warp then issues hi·hi + hi·lo + lo·hi per 32-byte step.  The dropped
+// lo·lo term and the TF32 rounding of lo are both ~2^-20 of |a·b|, so the
+// result carries ~fp32 accuracy (normwise ~1e-6) at three TF32 MMAs.
+constexpr int kConvThreads = 128;
+template <int BN, int TERMS, int ELEM, bool SPLITA = false>
 __device__ __forceinline__ void gemm_tc_body(const CUtensorMap &map_a, const CUtensorMap &map_b,
                                              const CUtensorMap &map_c, const GemmEpi &ep,
                                              int num_kb, int stages, int m_tiles, int n_tiles,
                                              int tma_store, int b_rows_per_term) {
+  static_assert(!SPLITA || (ELEM == 0 && TERMS == 2), "3xTF32 split: TF32 with B = [hi; lo]");
   constexpr uint32_t A_BYTES = BM * KB_BYTES;
+  constexpr uint32_t ALO_BYTES = SPLITA ? A_BYTES : 0u;  // lo(A) tile written by the converters
   constexpr uint32_t B_BYTES = BN * KB_BYTES;
-  constexpr uint32_t STAGE_BYTES = A_BYTES + TERMS * B_BYTES;
+  constexpr uint32_t B_OFF = A_BYTES + ALO_BYTES;
+  constexpr uint32_t STAGE_BYTES = B_OFF + TERMS * B_BYTES;
   constexpr bool BF16 = ELEM != 0;  // 16-bit elements (kind::f16)
   constexpr int KB_ELEMS = BF16 ? 64 : 32;
   constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // power of two >= 32
@@ -277,8 +289,11 @@ __device__ __forceinline__ void gemm_tc_body(const CUtensorMap &map_a, const CUt
   auto tfull_bar = [&](int b) { return bar0 + 8u * (2 * stages + b); };
   auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * stages + 2 + b); };
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + (bar0 - base) + 8u * (2 * stages + 4));
+  // SPLITA: per-stage "A converted" barriers after the TMEM slot
+  auto conv_bar = [&](int s) { return bar0 + 8u * (2 * stages + 4) + 16u + 8u * s; };
   // epilogue staging: per epilogue warp 2 x (32 rows x 16 fp32) boxes, 64-B swizzled
-  const uint32_t stage_c = (bar0 + 8u * (2 * stages + 4) + 16u + 1023u) & ~1023u;
+  const uint32_t stage_c =
+      (bar0 + 8u * (2 * stages + 4) + 16u + (SPLITA ? 8u * stages : 0u) + 1023u) & ~1023u;
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -295,6 +310,8 @@ __device__ __forceinline__ void gemm_tc_body(const CUtensorMap &map_a, const CUt
       mbar_init(tfull_bar(b), 1);
       mbar_init(tempty_bar(b), 4);  // one arrive per epilogue warp
     }
+    if constexpr (SPLITA)
+      for (int s = 0; s < stages; ++s) mbar_init(conv_bar(s), kConvThreads / 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -318,11 +335,11 @@ __device__ __forceinline__ void gemm_tc_body(const CUtensorMap &map_a, const CUt
           const int s = it % stages;
           mbar_wait(empty_bar(s), ((it / stages) & 1) ^ 1);
           const uint32_t sa = base + (uint32_t)s * STAGE_BYTES;
-          mbar_expect_tx(full_bar(s), STAGE_BYTES);
+          mbar_expect_tx(full_bar(s), STAGE_BYTES - ALO_BYTES);  // TMA bytes (lo(A) is made on chip)
           tma_load_2d(sa, &map_a, full_bar(s), kb * KB_ELEMS, m0);
 #pragma unroll
           for (int q = 0; q < TERMS; ++q)
-            tma_load_2d(sa + A_BYTES + q * B_BYTES, &map_b, full_bar(s), kb * KB_ELEMS,
+            tma_load_2d(sa + B_OFF + q * B_BYTES, &map_b, full_bar(s), kb * KB_ELEMS,
                         q * b_rows_per_term + n0);
         }
       }
@@ -338,15 +355,25 @@ __device__ __forceinline__ void gemm_tc_body(const CUtensorMap &map_a, const CUt
         const uint32_t tmem_d = tmem_base + (uint32_t)(acc * BN);
         for (int kb = 0; kb < num_kb; ++kb, ++it) {
           const int s = it % stages;
-          mbar_wait(full_bar(s), (it / stages) & 1);
+          // SPLITA: the converters' arrival implies the TMA bytes landed
+          mbar_wait(SPLITA ? conv_bar(s) : full_bar(s), (it / stages) & 1);
           tc_fence_after();
           const uint32_t sa = base + (uint32_t)s * STAGE_BYTES;
 #pragma unroll
           for (int k = 0; k < KB_BYTES / MMA_K_BYTES; ++k) {
             const uint64_t ad = umma_desc_sw128(sa + k * MMA_K_BYTES);
+            if constexpr (SPLITA) {
+              const uint64_t alo = umma_desc_sw128(sa + A_BYTES + k * MMA_K_BYTES);
+              const uint64_t bhi = umma_desc_sw128(sa + B_OFF + k * MMA_K_BYTES);
+              const uint64_t blo = umma_desc_sw128(sa + B_OFF + B_BYTES + k * MMA_K_BYTES);
+              mma_tf32(tmem_d, alo, bhi, idesc, (kb | k) != 0);  // small terms first
+              mma_tf32(tmem_d, ad, blo, idesc, 1);
+              mma_tf32(tmem_d, ad, bhi, idesc, 1);
+              continue;
+            }
 #pragma unroll
             for (int q = 0; q < TERMS; ++q) {
-              const uint64_t bd = umma_desc_sw128(sa + A_BYTES + q * B_BYTES + k * MMA_K_BYTES);
+              const uint64_t bd = umma_desc_sw128(sa + B_OFF + q * B_BYTES + k * MMA_K_BYTES);
               if constexpr (BF16) mma_bf16(tmem_d, ad, bd, idesc, (kb | k | q) != 0);
               else mma_tf32(tmem_d, ad, bd, idesc, (kb | k | q) != 0);
             }
@@ -354,6 +381,36 @@ __device__ __forceinline__ void gemm_tc_body(const CUtensorMap &map_a, const CUt
           mma_commit(empty_bar(s));  // frees the smem slot once these MMAs retire
         }
         mma_commit(tfull_bar(acc));  // accumulator of this tile complete
+      }
+    }
+  } else if (SPLITA && warp >= kGemmThreads / 32) {  // -------- A-split converters --------
+    // thread t rewrites 16-byte chunks t, t+128, ... of the landed A tile:
+    // each warp access is 512 contiguous bytes (conflict-free); the swizzle
+    // is irrelevant to an elementwise map as hi / lo keep A's positions
+    const int ct = threadIdx.x - kGemmThreads;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < n_tiles_total; tile += gridDim.x) {
+      for (int kb = 0; kb < num_kb; ++kb, ++it) {
+        const int s = it % stages;
+        mbar_wait(full_bar(s), (it / stages) & 1);
+        uint8_t *ta = gbase + (size_t)s * STAGE_BYTES;
+#pragma unroll
+        for (int i = 0; i < (int)(A_BYTES / 16 / kConvThreads); ++i) {
+          const uint32_t off = (uint32_t)(i * kConvThreads + ct) * 16u;
+          float4 *pa = reinterpret_cast<float4 *>(ta + off);
+          const float4 v = *pa;
+          float4 hi;
+          hi.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+          hi.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+          hi.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+          hi.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+          *pa = hi;
+          *reinterpret_cast<float4 *>(ta + A_BYTES + off) =
+              make_float4(v.x - hi.x, v.y - hi.y, v.z - hi.z, v.w - hi.w);
+        }
+        fence_proxy_async_smem();  // generic-proxy stores -> visible to the MMA (async proxy)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(conv_bar(s));
       }
     }
   } else {  // ---------------- epilogue warps 2..5 ----------------
@@ -1039,6 +1096,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   gemm_tc_body<BN, 1, 0>(map_a, map_b, map_c, ep, num_kb, stages, m_tiles, n_tiles, tma_store, 0);
 }
 
+// 3xTF32 (fp32-class) dense update: B = [hi(W^T); lo(W^T)] (b_rows_per_term
+// rows each), A split into hi / lo on chip (see gemm_tc_body SPLITA).
+template <int BN>
+__global__ void __launch_bounds__(kGemmThreads + kConvThreads, 1)
+    gemm_tf32x3_tcgen05(const __grid_constant__ CUtensorMap map_a,
+                        const __grid_constant__ CUtensorMap map_b,
+                        const __grid_constant__ CUtensorMap map_c, const GemmEpi ep, int num_kb,
+                        int stages, int m_tiles, int n_tiles, int tma_store, int b_rows_per_term) {
+  gemm_tc_body<BN, 2, 0, true>(map_a, map_b, map_c, ep, num_kb, stages, m_tiles, n_tiles,
+                               tma_store, b_rows_per_term);
+}
+
 // Dense hub block of the hybrid aggregation: C = D_row · A_hub · (B0 + B1 + B2)
 // with A_hub the 0/1 adjacency restricted to the hub columns (exact in bf16)
 // and B_q the three bf16 terms of D_col·X[hub rows] (together exact fp32).
@@ -1076,9 +1145,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                          b_rows_per_term);
 }
 
-// W (K x N, ldw) -> Wt (N x K, ldt): the K-major B operand.
+// W (K x N, ldw) -> Wt (N x K, ldt): the K-major B operand.  With Wt_lo
+// (3xTF32): Wt = hi(W^T) (13 low mantissa bits cleared, exact in TF32) and
+// Wt_lo = W^T - hi (exact in fp32).
 __global__ void transpose_kernel(const float *__restrict__ W, int64_t ldw, int64_t K, int64_t N,
-                                 float *__restrict__ Wt, int64_t ldt) {
+                                 float *__restrict__ Wt, int64_t ldt, float *__restrict__ Wt_lo) {
   __shared__ float tile[32][33];
   const int64_t k0 = (int64_t)blockIdx.y * 32, n0 = (int64_t)blockIdx.x * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -1088,7 +1159,16 @@ __global__ void transpose_kernel(const float *__restrict__ W, int64_t ldw, int64
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int64_t n = n0 + i, k = k0 + threadIdx.x;
-    if (n < N && k < ldt) Wt[n * ldt + k] = (k < K) ? tile[threadIdx.x][i] : 0.0f;
+    if (n < N && k < ldt) {
+      const float w = (k < K) ? tile[threadIdx.x][i] : 0.0f;
+      if (Wt_lo) {
+        const float hi = __uint_as_float(__float_as_uint(w) & 0xFFFFE000u);
+        Wt[n * ldt + k] = hi;
+        Wt_lo[n * ldt + k] = w - hi;
+      } else {
+        Wt[n * ldt + k] = w;
+      }
+    }
   }
 }
 
@@ -1288,6 +1368,37 @@ int launch_tf32(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap 
   gemm_tf32_tcgen05<BN><<<grid, kGemmThreads, smem, st>>>(ma, mb, mc, ep, num_kb, stages, m_tiles,
                                                           n_tiles, tma_store);
   return check_launch("gemm_tf32_tcgen05");
+}
+
+template <int BN>
+int launch_tf32x3(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mc,
+                  int tma_store, const GemmEpi &ep, int64_t K, int b_rows_per_term,
+                  cudaStream_t st) {
+  const int num_kb = (int)((K + BK - 1) / BK);
+  constexpr int stage_bytes = 2 * BM * KB_BYTES + 2 * BN * KB_BYTES;
+  size_t smem = 0;
+  const int stages = ring_stages(stage_bytes, true, &smem, 196 * 1024, 8 * 8);
+  if (stages < 2) {
+    set_error("gc_gemm_f32: 3xTF32 ring does not fit shared memory");
+    return GC_ERR_UNSUPPORTED;
+  }
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(gemm_tf32x3_tcgen05<BN>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  });
+  if (attr_err != cudaSuccess) {
+    set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
+    return GC_ERR_CUDA;
+  }
+  const int m_tiles = (int)((ep.M + BM - 1) / BM);
+  const int n_tiles = (int)((ep.N + BN - 1) / BN);
+  const int64_t tiles = (int64_t)m_tiles * n_tiles;
+  const int grid = (int)(tiles < sm_count() ? tiles : sm_count());
+  gemm_tf32x3_tcgen05<BN><<<grid, kGemmThreads + kConvThreads, smem, st>>>(
+      ma, mb, mc, ep, num_kb, stages, m_tiles, n_tiles, tma_store, b_rows_per_term);
+  return check_launch("gemm_tf32x3_tcgen05");
 }
 
 template <int BN, int FMT>
@@ -1625,7 +1736,7 @@ using namespace gnnc;
 extern "C" size_t gc_gemm_workspace_bytes(int64_t K, int64_t N) {
   if (K <= 0 || N <= 0) return 0;
   const int64_t ldt = (K + 3) / 4 * 4;
-  return (size_t)(N * ldt * 4);
+  return (size_t)(2 * N * ldt * 4);  // W^T, and its lo term for 3xTF32
 }
 
 extern "C" int gc_gemm_f32(const float *A, int64_t lda, const float *W, int64_t ldw, int64_t M,
@@ -1634,9 +1745,11 @@ extern "C" int gc_gemm_f32(const float *A, int64_t lda, const float *W, int64_t 
   GC_REQUIRE(M >= 0 && K >= 0 && N >= 0, GC_ERR_SHAPE, "gc_gemm_f32: negative size");
   GC_REQUIRE(lda >= K && ldw >= N && ldc >= N, GC_ERR_SHAPE, "gc_gemm_f32: bad leading dim");
   const bool tf32 = (flags & GC_GEMM_TF32) != 0, fp32 = (flags & GC_GEMM_FP32) != 0;
-  GC_REQUIRE(tf32 != fp32, GC_ERR_VALUE, "gc_gemm_f32: exactly one of TF32 / FP32 required");
-  GC_REQUIRE((flags & ~(GC_RELU | GC_GEMM_TF32 | GC_GEMM_FP32)) == 0, GC_ERR_VALUE,
-             "gc_gemm_f32: unknown flags 0x%x", flags);
+  const bool x3 = (flags & GC_GEMM_TF32X3) != 0;
+  GC_REQUIRE((int)tf32 + (int)fp32 + (int)x3 == 1, GC_ERR_VALUE,
+             "gc_gemm_f32: exactly one of TF32 / TF32X3 / FP32 required");
+  GC_REQUIRE((flags & ~(GC_RELU | GC_GEMM_TF32 | GC_GEMM_FP32 | GC_GEMM_TF32X3)) == 0,
+             GC_ERR_VALUE, "gc_gemm_f32: unknown flags 0x%x", flags);
   if (M == 0 || N == 0) return GC_OK;
   GC_REQUIRE(C && (K == 0 || (A && W)), GC_ERR_VALUE, "gc_gemm_f32: null operand");
   cudaStream_t st = as_stream(stream);
@@ -1653,7 +1766,7 @@ extern "C" int gc_gemm_f32(const float *A, int64_t lda, const float *W, int64_t 
     gemm_fp32_simt<<<grid, 256, 0, st>>>(A, lda, W, ldw, ep, K);
     return check_launch("gemm_fp32_simt");
   }
-  // TF32 tensor-core path
+  // TF32 / 3xTF32 tensor-core path
   GC_REQUIRE((lda % 4) == 0 && aligned16(A), GC_ERR_UNSUPPORTED,
              "gc_gemm_f32: TF32 path needs lda %% 4 == 0 and a 16-byte aligned A");
   GC_REQUIRE(M < (int64_t)INT32_MAX && K < (int64_t)INT32_MAX, GC_ERR_SHAPE,
@@ -1665,7 +1778,8 @@ extern "C" int gc_gemm_f32(const float *A, int64_t lda, const float *W, int64_t 
   float *wt = static_cast<float *>(workspace);
   {
     dim3 grid((unsigned)((N + 31) / 32), (unsigned)((ldt + 31) / 32));
-    transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(W, ldw, K, N, wt, ldt);
+    transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(W, ldw, K, N, wt, ldt,
+                                                     x3 ? wt + N * ldt : nullptr);
     int rc = check_launch("transpose_kernel");
     if (rc) return rc;
   }
@@ -1677,6 +1791,25 @@ extern "C" int gc_gemm_f32(const float *A, int64_t lda, const float *W, int64_t 
   CUtensorMap ma, mb, mc;
   int rc = make_map(&ma, A, M, K, lda, BM);
   if (rc) return rc;
+  if (x3) {
+    // 3xTF32: A split on chip, B = [hi; lo] stacked (N rows per term); N
+    // tiles of at most 128 columns keep three 64 KB stages in shared memory
+    bn = bn > 128 ? 128 : bn;
+    rc = make_map(&mb, wt, 2 * N, K, ldt, bn);
+    if (rc) return rc;
+    int tma_store = ((ldc % 4) == 0 && aligned16(C)) ? 1 : 0;
+    memset(&mc, 0, sizeof(mc));
+    if (tma_store) {
+      rc = make_map(&mc, C, M, N, ldc, 32, 16, CU_TENSOR_MAP_SWIZZLE_64B);
+      if (rc) return rc;
+    }
+    switch (bn) {
+      case 16: return launch_tf32x3<16>(ma, mb, mc, tma_store, ep, K, (int)N, st);
+      case 32: return launch_tf32x3<32>(ma, mb, mc, tma_store, ep, K, (int)N, st);
+      case 64: return launch_tf32x3<64>(ma, mb, mc, tma_store, ep, K, (int)N, st);
+      default: return launch_tf32x3<128>(ma, mb, mc, tma_store, ep, K, (int)N, st);
+    }
+  }
   if (hub_pair_enabled() && gemm_pair_enabled() && N > 16 && M >= 2 * BM &&
       (K >= 512 || M >= (int64_t(1) << 20))) {
     // CTA pairs (M = 256 per MMA, each CTA stages half of the W tile): the

@@ -587,6 +587,13 @@ def _time_interleaved(runs: dict, rounds: int) -> dict:
     return {k: float(sorted(v)[len(v) // 2]) for k, v in samples.items()}
 
 
+def split_key(K: int, weighted: bool) -> tuple:
+    """Cache key of the split choice: per K, weighted (Ñ values) or not, and
+    the operand term format of the current numerics class (a cell costs MMAs
+    in proportion to the term count, so the classes choose separately)."""
+    return ("hubsplit-choice", int(K), bool(weighted), term_format())
+
+
 def choose_split(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, *,
                  d_row: torch.Tensor | None = None, values: torch.Tensor | None = None):
     """Split spec for (pattern, K): 0 (plain SpMM) unless a dense split is
@@ -598,7 +605,7 @@ def choose_split(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, *,
     two plans are resident.  Device OOM while building or timing a candidate
     drops that candidate (the plain SpMM always remains).  Build time,
     autotune time and the peak extra device memory are recorded under
-    ``a._plans[("hubsplit-choice", K, weighted, "stats")]``."""
+    ``a._plans[split_key(K, weighted) + ("stats",)]``."""
     import time
 
     mode = str(HUB_SPLIT)
@@ -616,7 +623,7 @@ def choose_split(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, *,
             return 0  # the forced split does not fit this pattern
         return spec
     K = x.shape[1]
-    key = ("hubsplit-choice", int(K), values is not None)
+    key = split_key(K, values is not None)
     if key in a._plans:
         return a._plans[key]
     if a.nnz < HUB_MIN_NNZ or x.stride(1) != 1:

@@ -842,8 +842,15 @@ _GEMM_PRECISION = os.environ.get("GNNC_GEMM_PRECISION", "tf32")
 
 
 def set_gemm_precision(p: str) -> None:
-    """"tf32" (tcgen05 tensor cores; parity 1e-2) or "fp32" (exact CUDA-core
-    FMA; parity 1e-4)."""
+    """The numerics class of the dense update (and of the dense split's
+    operand terms, hub.py):
+
+    * "tf32" — one tcgen05 kind::tf32 MMA per product (TF32 input rounding,
+      fp32 accumulation); parity class 1e-2;
+    * "fp32" — 3xTF32 on tcgen05 (hi·hi + hi·lo + lo·hi, the fp32 operands
+      split into TF32 hi/lo terms on chip); parity class 1e-4.  Operands TMA
+      cannot describe (row pitch not a multiple of 16 bytes) take the exact
+      CUDA-core kernel."""
     global _GEMM_PRECISION
     if p not in ("tf32", "fp32"):
         raise ValueError("precision must be 'tf32' or 'fp32'")
@@ -856,7 +863,8 @@ def get_gemm_precision() -> str:
 
 def gemm(a, b, *, row_scale=None, relu=False, precision: str | None = None, out=None):
     """Dense product a @ b (sparse.py:285-291) on the tcgen05 tensor cores
-    (TF32) or exact fp32 CUDA cores; optional fused row scale and ReLU."""
+    (TF32, or 3xTF32 in the fp32 class); ``precision="simt"`` forces the
+    exact-fp32 CUDA-core kernel.  Optional fused row scale and ReLU."""
     dev = b.device if isinstance(b, torch.Tensor) else (
         a.device if isinstance(a, torch.Tensor) else default_device())
     oa, ob = _Operand(a, dev), _Operand(b, dev)
@@ -868,10 +876,13 @@ def gemm(a, b, *, row_scale=None, relu=False, precision: str | None = None, out=
     if out is None:
         out = torch.empty(M, N, dtype=torch.float32, device=dev)
     prec = precision or _GEMM_PRECISION
+    if prec not in ("tf32", "fp32", "simt"):
+        raise ValueError("precision must be 'tf32', 'fp32' or 'simt'")
     flags = nat.GC_RELU if relu else 0
     lib = nat.load()
     ws = None
-    if prec == "tf32" and K >= 8 and (_ld(at) % 4 or at.data_ptr() % 16) and M * K <= (1 << 28):
+    tensor = prec in ("tf32", "fp32")
+    if tensor and K >= 8 and (_ld(at) % 4 or at.data_ptr() % 16) and M * K <= (1 << 28):
         # TMA needs 16-byte row pitch: stage A with a padded leading dimension
         # (e.g. Cora's k1 = 1433 -> 1436) through the row-copy kernel
         ldp = (K + 3) // 4 * 4
@@ -879,8 +890,8 @@ def gemm(a, b, *, row_scale=None, relu=False, precision: str | None = None, out=
         nat.check(lib.gc_scale_rows_f32(None, at.data_ptr(), _ld(at), M, K, ap.data_ptr(), ldp, 0,
                                         _stream(dev)), "gemm(pad)")
         at = ap[:, :K]
-    if prec == "tf32" and (_ld(at) % 4 == 0) and at.data_ptr() % 16 == 0 and K > 0:
-        flags |= nat.GC_GEMM_TF32
+    if tensor and (_ld(at) % 4 == 0) and at.data_ptr() % 16 == 0 and K > 0:
+        flags |= nat.GC_GEMM_TF32 if prec == "tf32" else nat.GC_GEMM_TF32X3
         ws = torch.empty(max(int(lib.gc_gemm_workspace_bytes(K, N)), 16), dtype=torch.uint8,
                          device=dev)
     else:

@@ -26,7 +26,7 @@ import torch
 import paper_2306_15155_b200 as gc
 from paper_2306_15155_b200 import graphs, sparse
 
-import sampled_oracle as so
+from oracle import sampled as so
 
 pytestmark = pytest.mark.gpu
 DEV = "cuda"
@@ -174,7 +174,9 @@ def test_reddit_gcn_layer_parity(oracle, precision, K, comp, order):
         pytest.skip("fp32 class at K=1024: covered by the dynamic compositions")
     g = _gcn_case(oracle, "reddit", K, comp, order, precision, seed=K)
     if comp == "dynamic" and order == "update_first" and precision == "tf32" and K == 256:
-        assert g.a_tilde._plans.get(("hubsplit-choice", K, False), 0), \
+        from paper_2306_15155_b200 import hub
+
+        assert g.a_tilde._plans.get(hub.split_key(K, False), 0), \
             "the autotuner keeps a dense split on the Reddit shape"
 
 

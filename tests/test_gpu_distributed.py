@@ -47,7 +47,7 @@ def _worker(rank, world, port, comp, order, overlap, q):
         part = RowPartition.of(g.n_tilde if comp == "precompute" else g.a_tilde, rank, world)
         out = dist_gcn_layer(part, h[part.lo:part.hi], w, composition=comp, order=order,
                              d=g.d_inv_sqrt.to(dev), overlap=overlap, hub_unit=True)
-        used = any(k[0] == "hubsplit" for k in part.local._plans) or \
+        used = any(k[0] == "hubsplit" for k in part.padded()._plans) or \
             any(k[0] == "hubsplit" for k in part.split_local_remote()[1]._plans)
         full = all_gather_rows(out.cpu(), part)
         if rank == 0:

@@ -184,7 +184,7 @@ GEMM_SHAPES = [(1, 1, 1), (5, 3, 7), (130, 33, 16), (300, 32, 32), (1000, 64, 20
 
 
 @pytest.mark.parametrize("M,K,N", GEMM_SHAPES)
-@pytest.mark.parametrize("prec,tol", [("fp32", 1e-4), ("tf32", 1e-2)])
+@pytest.mark.parametrize("prec,tol", [("fp32", 2e-5), ("simt", 1e-5), ("tf32", 1e-2)])
 def test_gemm(oracle, M, K, N, prec, tol):
     rng = np.random.default_rng(M + K + N)
     a, w = f32(rng.uniform(-0.5, 0.5, (M, K))), f32(rng.uniform(-0.5, 0.5, (K, N)))
@@ -205,6 +205,20 @@ def test_gemm_tf32_uses_tensor_cores_accuracy_profile(oracle):
     e32 = oracle.rel_err(gc.gemm(a, w, precision="fp32"), ref)
     etf = oracle.rel_err(gc.gemm(a, w, precision="tf32"), ref)
     assert e32 < 1e-5 < etf < 1e-2
+
+
+def test_gemm_3xtf32_wide_dynamic_range(oracle):
+    """3xTF32 (the fp32 class): operands spanning 2^-20 .. 2^20 keep fp32-class
+    normwise error — the hi/lo split carries 22+ significant bits per operand."""
+    rng = np.random.default_rng(17)
+    a = f32(rng.uniform(-1, 1, (777, 96)) * 2.0 ** rng.integers(-20, 20, (777, 96)))
+    w = f32(rng.uniform(-1, 1, (96, 80)) * 2.0 ** rng.integers(-4, 4, (96, 80)))
+    ref = oracle.gemm(a, w)
+    out = gc.gemm(torch.from_numpy(a).to(DEV), torch.from_numpy(w).to(DEV), precision="fp32")
+    err = float(np.abs(out.cpu().numpy() - ref).max() / np.abs(ref).max())
+    assert err < 4e-6, err
+    tf = gc.gemm(torch.from_numpy(a).to(DEV), torch.from_numpy(w).to(DEV), precision="tf32")
+    assert float(np.abs(tf.cpu().numpy() - ref).max() / np.abs(ref).max()) > 10 * err
 
 
 def test_gemm_known_and_errors():
@@ -874,7 +888,7 @@ def test_full_size_reddit_layer_parity(oracle, reddit_full):
     w = f32(rng.uniform(-0.5, 0.5, (K, K)))
     spec = gc.GcnLayerSpec(K, K, w, composition="dynamic", order="update_first")
     out = gc.gcn_layer(g, torch.from_numpy(h).to(DEV), spec)
-    split = a._plans.get(("hubsplit-choice", K, False), 0)
+    split = a._plans.get(hub.split_key(K, False), 0)
     assert split, "the autotuner keeps a dense split on the Reddit shape"
     # oracle on sampled rows: relu(D Ã D (H W)) restricted to those rows
     rows = np.sort(rng.choice(n, size=512, replace=False))
