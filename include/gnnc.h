@@ -59,6 +59,8 @@ extern "C" {
                                                  (K/4 >> s) lanes per row, each owning 4<<s
                                                  columns; more rows per warp for short rows */
 #define GC_SPMM_SHRINK_MASK (3u << 8)
+#define GC_SPMM_B_F16 (1u << 10) /* gc_spmm_f32: B holds fp16 rows (ldb in elements; K % 4 == 0,
+                                  * ldb % 4 == 0, 8-byte aligned), see gc_pack_rows_f16 */
 #define GC_GEMM_TF32 (1u << 4)  /* tcgen05.mma kind::tf32, TMEM accumulators, TMA operands */
 #define GC_GEMM_FP32 (1u << 5)  /* exact fp32 CUDA-core path (rtol 1e-4 parity mode) */
 #define GC_GEMM_TF32X3 (1u << 7) /* 3xTF32 on tcgen05: hi·hi + hi·lo + lo·hi, fp32-class (1e-4) */
@@ -127,6 +129,15 @@ GNNC_API int gc_gat_aggregate_f32(const int32_t *row_ptr, const int32_t *col_idx
                                   uint32_t flags, int algo, const int32_t *items, int64_t n_items,
                                   const int32_t *split_rows, int64_t n_split_rows, void *workspace,
                                   size_t ws_bytes, void *stream);
+
+/* Half-width gather operand of the TF32 numerics class: per row j,
+ *   Xh[j,:] = fp16_rn(X[j,:] * 2^-e_j)  (max |.| in [2^14, 2^15)),
+ *   sigma[j] = (d ? d[j] : 1) * 2^e_j,
+ * so sigma[j] * Xh[j,:] = d[j] * X[j,:] to fp16's 11 significant bits (the
+ * input rounding TF32 applies).  gc_spmm_f32 with GC_SPMM_B_F16 and
+ * d_col = sigma then gathers 2 bytes per feature instead of 4. */
+GNNC_API int gc_pack_rows_f16(const float *X, int64_t ldx, int64_t n_rows, int64_t K,
+                              const float *d, void *Xh, int64_t ldh, float *sigma, void *stream);
 
 /* col_tagged[p] = col_idx[p] | (hot[col_idx[p]] ? 1<<31 : 0): a copy of the
  * pattern whose hub columns (hot: uint8 per column) are tagged for

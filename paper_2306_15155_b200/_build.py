@@ -52,20 +52,26 @@ def _stale(lib: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = False,
+          defines: tuple[str, ...] = (), out: Path | None = None) -> Path:
+    """Build ``lib/libgnnc.so`` (or, for A/B experiments, a variant with extra
+    ``-D`` ``defines`` written to ``out``; load it with GNNC_LIB_PATH)."""
     deps = sources() + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "gnnc.h", Path(__file__)]
-    if not force and not _stale(LIB, deps):
-        return LIB
-    OBJ.mkdir(exist_ok=True)
-    LIB_DIR.mkdir(exist_ok=True)
+    lib = Path(out) if out is not None else LIB
+    if not force and not defines and not _stale(lib, deps):
+        return lib
+    obj_dir = OBJ if not defines else OBJ / ("v_" + "_".join(d.replace("=", "") for d in defines))
+    obj_dir.mkdir(parents=True, exist_ok=True)
+    lib.parent.mkdir(parents=True, exist_ok=True)
     cc = nvcc()
     # host compiler: /usr/bin/g++ (the image's CC/CXX point at a gcc without all runtimes)
     host = ["-ccbin", "/usr/bin/g++"] if Path("/usr/bin/g++").exists() else []
     extra = ["-Xptxas", "-v"] if ptxas_verbose else []
 
     def compile_one(src: Path) -> Path:
-        obj = OBJ / (src.stem + ".o")
-        cmd = [cc, *host, *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)]
+        obj = obj_dir / (src.stem + ".o")
+        cmd = [cc, *host, *NVCC_FLAGS, *extra, *(f"-D{d}" for d in defines), "-c", str(src),
+               "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -77,13 +83,13 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
 
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, sources()))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [cc, *host, *ARCH, "-shared", "-o", str(tmp), *map(str, objs)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

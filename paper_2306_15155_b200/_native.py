@@ -23,6 +23,7 @@ GC_HUB_F16 = 2
 GC_HUB_F16_MN = 3
 GC_HUB_A_BITS = 1 << 6
 GC_HUB_TAGGED = 1 << 2
+GC_SPMM_B_F16 = 1 << 10
 
 
 def GC_SPMM_SHRINK(s: int) -> int:  # noqa: N802 - mirrors the C macro
@@ -92,6 +93,7 @@ _SIGNATURES = {
     "gc_hub_stair_gemm": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P, _P, _P, _I32, _P, _P, _I32, _P,
                                          _I64, _I64, _I32, _P, _P, _I64, _P, _U32, _P]),
     "gc_tag_hub_columns": (ctypes.c_int, [_P, _I64, _P, _P, _P]),
+    "gc_pack_rows_f16": (ctypes.c_int, [_P, _I64, _I64, _I64, _P, _P, _I64, _P, _P]),
 }
 
 

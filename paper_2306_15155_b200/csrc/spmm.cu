@@ -19,12 +19,20 @@
 // merged in slot order by the fixup kernel.
 #include <algorithm>
 
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace gnnc {
 namespace {
 
 constexpr int kThreads = 256;
+// resident CTAs per SM the SpMM kernel is compiled for (register cap
+// 65536 / (kThreads * GNNC_SPMM_MINB)); the gathers are latency-bound, so
+// warps in flight matter
+#ifndef GNNC_SPMM_MINB
+#define GNNC_SPMM_MINB 1
+#endif
 
 struct SpmmArgs {
   const int32_t *row_ptr;
@@ -89,6 +97,18 @@ __device__ __forceinline__ void load_b_hint(float4 &dst, const float *p, bool ho
   dst = hot ? ldg_f4_keep(p) : ldg_f4_stream(p);
 }
 __device__ __forceinline__ void load_b_hint(float &dst, const float *p, bool) { dst = __ldg(p); }
+// fp16 operand rows (GC_SPMM_B_F16): four halves (8 bytes) per column slot,
+// widened to fp32 in registers (exact)
+__device__ __forceinline__ void load_bh(float4 &dst, const char *p) {
+  uint32_t lo, hi;
+  asm("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(lo), "=r"(hi) : "l"(p));
+  const float2 a = __half22float2(*reinterpret_cast<const __half2 *>(&lo));
+  const float2 b = __half22float2(*reinterpret_cast<const __half2 *>(&hi));
+  dst = make_float4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ void load_bh(float &dst, const char *p) {
+  dst = __half2float(*reinterpret_cast<const __half *>(p));
+}
 
 __device__ __forceinline__ float epi1(float v, float ds, float old, uint32_t flags) {
   v *= ds;
@@ -139,8 +159,12 @@ __device__ __forceinline__ void store_row(const SpmmArgs &a, int row, int slot, 
 // MODE 2: GAT whose score is an SDDMM over the gathered rows themselves,
 // e = LeakyReLU(a_src.B_i + a_dst.B_j): one gather of B_j feeds both the
 // score and the aggregation (needs the whole row in one column pass).
-template <int LPR, int NV, bool VEC, bool HAS_VAL, bool HAS_DCOL, int MODE, bool HINT>
-__global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
+// BH (MODE 0 only): B holds fp16 rows (GC_SPMM_B_F16, the TF32 class's
+// half-width gather operand), half the gathered bytes per edge.
+template <int LPR, int NV, bool VEC, bool HAS_VAL, bool HAS_DCOL, int MODE, bool HINT,
+          bool BH = false>
+__global__ void __launch_bounds__(kThreads, GNNC_SPMM_MINB) spmm_kernel(const SpmmArgs a) {
+  static_assert(!BH || (MODE == 0 && !HINT), "fp16 operand rows: plain SpMM without L1 tags");
   using T = typename Lanes<VEC>::T;
   constexpr bool GAT = MODE != 0;
   constexpr bool SD = MODE == 2;
@@ -182,8 +206,9 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
 #pragma unroll
   for (int v = 0; v < NV; ++v) acc[v] = zero_of(T{});
   constexpr int kSlotStride = LPR * Lanes<VEC>::W;  // floats between a lane's column slots
-  const char *bbase = reinterpret_cast<const char *>(a.B + coff[0]);
-  const uint32_t ldb_bytes = (uint32_t)(a.ldb * 4);
+  constexpr int ESZ = BH ? 2 : 4;  // bytes per operand element
+  const char *bbase = reinterpret_cast<const char *>(a.B) + (int64_t)coff[0] * ESZ;
+  const uint32_t ldb_bytes = (uint32_t)(a.ldb * ESZ);
 
   const int len = end - beg;
   const int wmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)len);
@@ -269,14 +294,15 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(const SpmmArgs a) {
       for (int u = 0; u < U; ++u) {
         const int je = __shfl_sync(0xffffffffu, j, e0 + u, LPR);
         const bool ok = (e0 + u) < cnt;
-        const float *brow = reinterpret_cast<const float *>(
-            bbase + (uint64_t)(uint32_t)je * ldb_bytes);
+        const char *brow_c = bbase + (uint64_t)(uint32_t)je * ldb_bytes;
+        const float *brow = reinterpret_cast<const float *>(brow_c);
         bool hote = false;
         if (HINT) hote = __shfl_sync(0xffffffffu, (int)hot, e0 + u, LPR) != 0;
 #pragma unroll
         for (int vv = 0; vv < NV; ++vv) {
           if (ok && colok[vv]) {
-            if (HINT) load_b_hint(bv[u][vv], brow + vv * kSlotStride, hote);
+            if constexpr (BH) load_bh(bv[u][vv], brow_c + vv * kSlotStride * ESZ);
+            else if (HINT) load_b_hint(bv[u][vv], brow + vv * kSlotStride, hote);
             else load_b(bv[u][vv], brow + vv * kSlotStride);
           }
         }
@@ -386,7 +412,7 @@ __global__ void __launch_bounds__(kThreads)
   store_row<LPR, NV, VEC>(a, sr.x, -1, gl, c0, ds, acc);
 }
 
-template <int LPR, int NV, bool VEC, int MODE>
+template <int LPR, int NV, bool VEC, int MODE, bool BH = false>
 int launch_cfg(const SpmmArgs &a, const int4 *split_rows, int64_t n_split, cudaStream_t st) {
   constexpr int GPB = kThreads / LPR;
   constexpr int64_t kColsPerPass = (int64_t)LPR * NV * Lanes<VEC>::W;
@@ -398,7 +424,12 @@ int launch_cfg(const SpmmArgs &a, const int4 *split_rows, int64_t n_split, cudaS
   if (a.n_items > 0) {
     dim3 grid((unsigned)((a.n_items + GPB - 1) / GPB), (unsigned)ychunks);
     const bool hv = a.values != nullptr, hd = a.d_col != nullptr;
-    if constexpr (MODE != 0) {
+    if constexpr (BH) {
+      if (hv && hd) spmm_kernel<LPR, NV, VEC, true, true, 0, false, true><<<grid, kThreads, 0, st>>>(a);
+      else if (hv) spmm_kernel<LPR, NV, VEC, true, false, 0, false, true><<<grid, kThreads, 0, st>>>(a);
+      else if (hd) spmm_kernel<LPR, NV, VEC, false, true, 0, false, true><<<grid, kThreads, 0, st>>>(a);
+      else spmm_kernel<LPR, NV, VEC, false, false, 0, false, true><<<grid, kThreads, 0, st>>>(a);
+    } else if constexpr (MODE != 0) {
       if (a.hints) spmm_kernel<LPR, NV, VEC, false, false, MODE, true><<<grid, kThreads, 0, st>>>(a);
       else spmm_kernel<LPR, NV, VEC, false, false, MODE, false><<<grid, kThreads, 0, st>>>(a);
     } else if (a.hints) {
@@ -464,6 +495,31 @@ int dispatch(SpmmArgs &a, int64_t n_rows, int algo, const int32_t *items, int64_
   }
   GC_REQUIRE(a.ldb < (int64_t(1) << 30), GC_ERR_SHAPE, "%s: leading dimension too large", who);
   const int64_t K = a.K;
+  if (MODE == 0 && (a.flags & GC_SPMM_B_F16)) {
+    // fp16 operand rows: 8-byte column slots, the float4 lane-group shapes
+    GC_REQUIRE(K % 4 == 0 && a.ldb % 4 == 0 && (reinterpret_cast<uintptr_t>(a.B) & 7u) == 0 &&
+                   a.ldc % 4 == 0 && aligned16(a.C) && (a.partial == nullptr || aligned16(a.partial)),
+               GC_ERR_UNSUPPORTED, "%s: fp16 operand needs K %% 4 == 0, ldb %% 4 == 0, 8-byte "
+               "aligned B and 16-byte aligned C", who);
+    GC_REQUIRE(!a.hints, GC_ERR_UNSUPPORTED, "%s: no hub tags with an fp16 operand", who);
+    cudaStream_t sth = as_stream(stream);
+    const int sh = (int)((a.flags >> 8) & 3u);
+    if (K <= 8) return launch_cfg<2, 1, true, 0, true>(a, sr, n_split, sth);
+    if (K <= 16) return sh ? launch_cfg<2, 2, true, 0, true>(a, sr, n_split, sth)
+                           : launch_cfg<4, 1, true, 0, true>(a, sr, n_split, sth);
+    if (K <= 32) return sh == 2 ? launch_cfg<2, 4, true, 0, true>(a, sr, n_split, sth)
+                      : sh == 1 ? launch_cfg<4, 2, true, 0, true>(a, sr, n_split, sth)
+                                : launch_cfg<8, 1, true, 0, true>(a, sr, n_split, sth);
+    if (K <= 64) return sh == 2 ? launch_cfg<4, 4, true, 0, true>(a, sr, n_split, sth)
+                      : sh == 1 ? launch_cfg<8, 2, true, 0, true>(a, sr, n_split, sth)
+                                : launch_cfg<16, 1, true, 0, true>(a, sr, n_split, sth);
+    if (K <= 128) return sh == 2 ? launch_cfg<8, 4, true, 0, true>(a, sr, n_split, sth)
+                       : sh == 1 ? launch_cfg<16, 2, true, 0, true>(a, sr, n_split, sth)
+                                 : launch_cfg<32, 1, true, 0, true>(a, sr, n_split, sth);
+    return sh == 2 ? launch_cfg<8, 8, true, 0, true>(a, sr, n_split, sth)
+         : sh == 1 ? launch_cfg<16, 4, true, 0, true>(a, sr, n_split, sth)
+                   : launch_cfg<32, 2, true, 0, true>(a, sr, n_split, sth);
+  }
   const bool vec = (K % 4 == 0) && (a.ldb % 4 == 0) && (a.ldc % 4 == 0) && aligned16(a.B) &&
                    aligned16(a.C) && (a.partial == nullptr || aligned16(a.partial));
   if constexpr (MODE == 2) {
@@ -502,6 +558,50 @@ int dispatch(SpmmArgs &a, int64_t n_rows, int algo, const int32_t *items, int64_
   return launch_cfg<32, 4, false, MODE>(a, sr, n_split, st);
 }
 
+// Half-width gather operand (the TF32 class): per row j of X, e_j is chosen
+// so that max_k |X[j,k]| * 2^-e_j lies in [2^14, 2^15) and
+//   Xh[j,k] = fp16_rn(X[j,k] * 2^-e_j),   sigma[j] = (d ? d[j] : 1) * 2^e_j,
+// so X[j,:] * d[j] = sigma[j] * Xh[j,:] up to the fp16 rounding of each
+// element (11 significant bits — the same input rounding TF32 applies).
+// One warp per row, float4 reads, 8-byte writes.
+__global__ void __launch_bounds__(256)
+    pack_rows_f16_kernel(const float *__restrict__ X, int64_t ldx, int64_t n, int64_t K,
+                         const float *__restrict__ d, __half *__restrict__ Xh, int64_t ldh,
+                         float *__restrict__ sigma, bool vec) {
+  const int lane = threadIdx.x % 32;
+  const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; r < n; r += n_warps) {
+    const float *x = X + r * ldx;
+    float mx = 0.0f;
+    if (vec)
+      for (int64_t c = 4 * lane; c < K; c += 128) {
+        const float4 v = ldg_f4(x + c);
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+      }
+    else
+      for (int64_t c = lane; c < K; c += 32) mx = fmaxf(mx, fabsf(__ldg(x + c)));
+    mx = group_max<32>(mx);
+    // exponent of mx (frexp-style, exact): mx = m * 2^E, m in [1, 2)
+    const int E = mx > 0.0f ? ((int)((__float_as_uint(mx) >> 23) & 0xff) - 127) : 0;
+    const int e = mx > 0.0f && isfinite(mx) ? max(min(E - 14, 110), -110) : 0;
+    const float down = __uint_as_float((uint32_t)(127 - e) << 23);  // 2^-e, |e| <= 110
+    __half *h = Xh + r * ldh;
+    if (vec)
+      for (int64_t c = 4 * lane; c < K; c += 128) {
+        const float4 v = ldg_f4(x + c);
+        const __half2 a = __floats2half2_rn(v.x * down, v.y * down);
+        const __half2 b = __floats2half2_rn(v.z * down, v.w * down);
+        uint2 packed;
+        packed.x = *reinterpret_cast<const uint32_t *>(&a);
+        packed.y = *reinterpret_cast<const uint32_t *>(&b);
+        *reinterpret_cast<uint2 *>(h + c) = packed;
+      }
+    else
+      for (int64_t c = lane; c < K; c += 32) h[c] = __float2half_rn(__ldg(x + c) * down);
+    if (lane == 0) sigma[r] = (d ? __ldg(d + r) : 1.0f) * __uint_as_float((uint32_t)(127 + e) << 23);
+  }
+}
+
 __global__ void tag_hub_kernel(const int32_t *__restrict__ col, int64_t nnz,
                                const uint8_t *__restrict__ hot, int32_t *__restrict__ out) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz;
@@ -515,6 +615,21 @@ __global__ void tag_hub_kernel(const int32_t *__restrict__ col, int64_t nnz,
 }  // namespace gnnc
 
 using namespace gnnc;
+
+extern "C" int gc_pack_rows_f16(const float *X, int64_t ldx, int64_t n_rows, int64_t K,
+                                const float *d, void *Xh, int64_t ldh, float *sigma,
+                                void *stream) {
+  GC_REQUIRE(n_rows >= 0 && K >= 0 && ldx >= K && ldh >= K, GC_ERR_SHAPE,
+             "gc_pack_rows_f16: bad shape");
+  if (n_rows == 0) return GC_OK;
+  GC_REQUIRE(X && Xh && sigma, GC_ERR_VALUE, "gc_pack_rows_f16: null operand");
+  const bool vec = K % 4 == 0 && ldx % 4 == 0 && ldh % 4 == 0 && aligned16(X) &&
+                   (reinterpret_cast<uintptr_t>(Xh) & 7u) == 0;
+  const int64_t blocks = std::min<int64_t>((n_rows + 7) / 8, (int64_t)sm_count() * 16);
+  pack_rows_f16_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
+      X, ldx, n_rows, K, d, static_cast<__half *>(Xh), ldh, sigma, vec);
+  return check_launch("pack_rows_f16_kernel");
+}
 
 extern "C" int gc_tag_hub_columns(const int32_t *col_idx, int64_t nnz, const uint8_t *hot,
                                   int32_t *col_tagged, void *stream) {
@@ -534,7 +649,8 @@ extern "C" int gc_spmm_f32(const int32_t *row_ptr, const int32_t *col_idx, const
                            size_t ws_bytes, void *stream) {
   GC_REQUIRE(n_rows >= 0 && n_cols >= 0 && K >= 0, GC_ERR_SHAPE, "gc_spmm_f32: negative size");
   GC_REQUIRE(ldb >= K && ldc >= K, GC_ERR_SHAPE, "gc_spmm_f32: leading dimension < K");
-  GC_REQUIRE((flags & ~(GC_RELU | GC_ACCUMULATE | GC_HUB_TAGGED | GC_SPMM_SHRINK_MASK)) == 0,
+  GC_REQUIRE((flags & ~(GC_RELU | GC_ACCUMULATE | GC_HUB_TAGGED | GC_SPMM_SHRINK_MASK |
+                         GC_SPMM_B_F16)) == 0,
              GC_ERR_VALUE, "gc_spmm_f32: unknown flags 0x%x", flags);
   if (n_rows == 0 || K == 0) return GC_OK;
   GC_REQUIRE(row_ptr && C && (B || n_cols == 0), GC_ERR_VALUE, "gc_spmm_f32: null operand");

@@ -128,7 +128,7 @@ HUB_MIN_NNZ = 1 << 24            # smaller graphs stay on the SpMM alone
 HUB_MEM_BUDGET = 8 << 30         # bytes of dense blocks per pattern
 STAIR_MAX_STEPS = 16
 STAIR_FIRST_BAND = 1024          # rows / columns of the first histogram band
-AUTOTUNE_ROUNDS = 5              # interleaved timing rounds per candidate
+AUTOTUNE_ROUNDS = 7              # interleaved timing rounds per candidate
 STAIR_BAND_RATIO = 2 ** 0.5      # growth of the histogram bands
 STAIR_CLUSTERS = 74              # CTA pairs of a B200 (balance bound of the top tile)
 
@@ -506,12 +506,19 @@ def _stair_gemm(plan, K: int, packed, out: torch.Tensor, d_row: torch.Tensor, fl
 
 
 def tail_part(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, out: torch.Tensor, *,
-              d_row: torch.Tensor, values=None, relu=False, rows: tuple[int, int] | None = None):
-    """out (rows [lo, hi)) += the remaining edges (ReLU on the total)."""
+              d_row: torch.Tensor, values=None, relu=False, rows: tuple[int, int] | None = None,
+              x_tail=None):
+    """out (rows [lo, hi)) += the remaining edges (ReLU on the total).
+    ``x_tail``: the gathered operand as fp16 rows (``sparse.HalfRows``, with
+    the column scaling of the unit tail folded into its scales)."""
     plan = hub_plan(a, spec)
     lo, hi = rows if rows is not None else (0, a.n_rows)
     tail = plan.tail_block(values, lo, hi)
-    if values is None:
+    if x_tail is not None:
+        _spmm(tail, x_tail, weighted=values is not None,
+              d_row=d_row[lo:hi] if values is None else None, relu=relu, out=out,
+              accumulate=True, timer="spmm_tail")
+    elif values is None:
         _spmm(tail, x, weighted=False, d_row=d_row[lo:hi], d_col=d, relu=relu, out=out,
               accumulate=True, timer="spmm_tail")
     else:
@@ -522,7 +529,7 @@ def hybrid_aggregate(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, *,
                      d_row: torch.Tensor | None = None, values: torch.Tensor | None = None,
                      relu: bool = False, out: torch.Tensor | None = None,
                      accumulate: bool = False, rows: tuple[int, int] | None = None,
-                     packed: tuple | None = None) -> torch.Tensor:
+                     packed: tuple | None = None, x_tail=None) -> torch.Tensor:
     """C = epi(D_row Ã D X) for a unit-valued pattern ``a`` via the dense/tail
     split ``spec`` (``d`` scales the columns — None when x already carries
     the column scaling; ``d_row`` the rows, default ``d`` itself for a square
@@ -530,7 +537,8 @@ def hybrid_aggregate(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, *,
     same-pattern matrix's values used for the tail instead of d_i·d_j (the
     precompute composition streams Ñ's values).  ``accumulate``: C += ...
     (ReLU on the total).  ``rows=(lo, hi)`` (block plans only) computes that
-    row block (``out`` then has hi-lo rows); ``packed`` reuses one ``pack``."""
+    row block (``out`` then has hi-lo rows); ``packed`` reuses one ``pack``;
+    ``x_tail``: fp16 rows of x for the tail (see :func:`tail_part`)."""
     dev = _require_cuda(a.col_idx, x)
     if x.dim() != 2 or x.shape[0] != a.n_cols or x.stride(1) != 1:
         raise ShapeError("hybrid_aggregate: x must be a row-major n_cols x K tensor")
@@ -551,7 +559,8 @@ def hybrid_aggregate(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, *,
     def run():
         dense_part(a, x, d, spec, out, d_row=d_row, accumulate=accumulate, packed=packed,
                    rows=rows)
-        tail_part(a, x, d, spec, out, d_row=d_row, values=values, relu=relu, rows=rows)
+        tail_part(a, x, d, spec, out, d_row=d_row, values=values, relu=relu, rows=rows,
+                  x_tail=x_tail)
         return 0
 
     _timed_call("spmm", dev, run)
@@ -587,15 +596,21 @@ def _time_interleaved(runs: dict, rounds: int) -> dict:
     return {k: float(sorted(v)[len(v) // 2]) for k, v in samples.items()}
 
 
-def split_key(K: int, weighted: bool) -> tuple:
-    """Cache key of the split choice: per K, weighted (Ñ values) or not, and
-    the operand term format of the current numerics class (a cell costs MMAs
-    in proportion to the term count, so the classes choose separately)."""
-    return ("hubsplit-choice", int(K), bool(weighted), term_format())
+def split_key(K: int, weighted: bool = False) -> tuple:
+    """Cache key of the split choice: per K and operand term format of the
+    current numerics class (a cell costs MMAs in proportion to the term
+    count, so the classes choose separately).  Weighted (Ñ values, the
+    precompute composition) and unit tails share the choice: the pattern and
+    the dense part are the same, the tail differs by one value stream — one
+    measurement per pattern keeps autotune noise from making the
+    compositions differ by their splits rather than by their algebra."""
+    del weighted
+    return ("hubsplit-choice", int(K), term_format())
 
 
 def choose_split(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, *,
-                 d_row: torch.Tensor | None = None, values: torch.Tensor | None = None):
+                 d_row: torch.Tensor | None = None, values: torch.Tensor | None = None,
+                 x_tail=None):
     """Split spec for (pattern, K): 0 (plain SpMM) unless a dense split is
     measurably faster, chosen on the first call and cached on the pattern.
 
@@ -642,11 +657,16 @@ def choose_split(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, *,
     src = a if values is None else a.with_values(values)
 
     def plain():
+        if x_tail is not None:
+            _spmm(src, x_tail, weighted=values is not None,
+                  d_row=None if values is not None else d_row, out=scratch, timer=None)
+            return
         _spmm(src, x, weighted=values is not None, d_row=None if values is not None else d_row,
               d_col=None if values is not None else d, out=scratch, timer=None)
 
     def hybrid(spec):
-        return lambda: hybrid_aggregate(a, x, d, spec, d_row=d_row, values=values, out=scratch)
+        return lambda: hybrid_aggregate(a, x, d, spec, d_row=d_row, values=values, out=scratch,
+                                        x_tail=x_tail)
 
     best, times, build_s = 0, {}, 0.0
     for spec in cands:

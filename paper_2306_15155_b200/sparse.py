@@ -572,6 +572,8 @@ def _variant(a: CsrMatrix, K: int, mode: str, probe) -> tuple[bool, int]:
     if a.nnz < PLAN_MIN_NNZ:
         return False, 0
     hints = [False, True] if hint_mode == "auto" else [hint_mode == "1"]
+    if mode == "spmmh":
+        hints = [False]  # no L1-tag variant with fp16 operand rows
     shrinks = _shrink_candidates(K, mode) if shrink_mode == "auto" else [int(shrink_mode)]
     if len(hints) * len(shrinks) == 1:
         return hints[0], shrinks[0]
@@ -651,14 +653,59 @@ def gat_sddmm_aggregate(a: CsrMatrix, a_src: torch.Tensor, a_dst: torch.Tensor, 
     return out
 
 
+class HalfRows:
+    """The TF32 class's half-width gather operand (``gc_pack_rows_f16``): fp16
+    rows ``xh`` and per-row scales ``sigma`` with sigma[j] * xh[j] = d[j] *
+    x[j] to 11 significant bits — TF32's input rounding — so an aggregation
+    gathers 2 bytes per feature instead of 4.  Pass it as the dense operand
+    of :func:`spmm` / :func:`spmm_unweighted` (``d_col`` is then carried by
+    sigma)."""
+
+    __slots__ = ("xh", "sigma", "K")
+
+    def __init__(self, xh: torch.Tensor, sigma: torch.Tensor, K: int):
+        self.xh, self.sigma, self.K = xh, sigma, int(K)
+
+    @property
+    def shape(self) -> tuple[int, int]:
+        return (self.xh.shape[0], self.K)
+
+    @property
+    def device(self) -> torch.device:
+        return self.xh.device
+
+
+def pack_rows_f16(x: torch.Tensor, d: torch.Tensor | None = None) -> HalfRows:
+    """x (n x K fp32, device) -> HalfRows with d (optional, per row) folded
+    into the scales."""
+    _require_cuda(x, d)
+    if x.dim() != 2 or x.stride(1) != 1:
+        raise ShapeError("pack_rows_f16: x must be a row-major 2-D tensor")
+    n, K = x.shape
+    if d is not None and tuple(d.shape) != (n,):
+        raise ShapeError("pack_rows_f16: d must have one entry per row")
+    ldh = (K + 3) // 4 * 4
+    xh = torch.empty(n, ldh, dtype=torch.float16, device=x.device)
+    sigma = torch.empty(n, dtype=torch.float32, device=x.device)
+    nat.check(nat.load().gc_pack_rows_f16(x.data_ptr(), _ld(x), n, K, _ptr(d), xh.data_ptr(), ldh,
+                                          sigma.data_ptr(), _stream(x.device)), "pack_rows_f16")
+    return HalfRows(xh, sigma, K)
+
+
 def _spmm(a: CsrMatrix, b, *, weighted: bool, d_row=None, d_col=None, relu=False, out=None,
           accumulate=False, algo: str = "auto", what="spmm", timer: str | None = "spmm"):
     dev = a.device
-    op = _Operand(b, dev)
-    bt = op.t
+    half = isinstance(b, HalfRows)
+    if half:
+        if d_col is not None:
+            raise ShapeError(f"{what}: an fp16 operand carries d_col in its row scales")
+        op, bt, d_col = None, b.xh, b.sigma
+    else:
+        op = _Operand(b, dev)
+        bt = op.t
     if a.n_cols != bt.shape[0]:
         raise ShapeError(f"{what}: a is {a.n_rows}x{a.n_cols}, b has {bt.shape[0]} rows")
-    K = bt.shape[1]
+    K = b.K if half else bt.shape[1]
     _require_cuda(a.col_idx, bt)
     if out is None:
         out = torch.empty(a.n_rows, K, dtype=torch.float32, device=dev)
@@ -669,7 +716,8 @@ def _spmm(a: CsrMatrix, b, *, weighted: bool, d_row=None, d_col=None, relu=False
     for d, n, nm in ((d_row, a.n_rows, "d_row"), (d_col, a.n_cols, "d_col")):
         if d is not None and tuple(d.shape) != (n,):
             raise ShapeError(f"{what}: {nm} must have {n} entries")
-    flags = (nat.GC_RELU if relu else 0) | (nat.GC_ACCUMULATE if accumulate else 0)
+    flags = (nat.GC_RELU if relu else 0) | (nat.GC_ACCUMULATE if accumulate else 0) | \
+        (nat.GC_SPMM_B_F16 if half else 0)
     code, items, n_items, split, n_split, ws = _plan_args(a, K, algo, dev)
     lib = nat.load()
 
@@ -688,12 +736,12 @@ def _spmm(a: CsrMatrix, b, *, weighted: bool, d_row=None, d_col=None, relu=False
             scratch = torch.empty(a.n_rows, K, dtype=torch.float32, device=dev)
         nat.check(launch(cols, extra, scratch, flags & ~nat.GC_ACCUMULATE), what)
 
-    hints, shrink = _variant(a, K, "spmm", probe)
+    hints, shrink = _variant(a, K, "spmmh" if half else "spmm", probe)
     cols = a.hub_tagged_cols(K) if hints else a.col_idx
     extra = (nat.GC_HUB_TAGGED if hints else 0) | nat.GC_SPMM_SHRINK(shrink)
     rc = _timed_call(timer, dev, lambda: launch(cols, extra)) if timer else launch(cols, extra)
     nat.check(rc, what)
-    return op.wrap(out)
+    return out if half else op.wrap(out)
 
 
 def gat_aggregate(a: CsrMatrix, s: torch.Tensor, t: torch.Tensor, slope: float, b, *,

@@ -27,7 +27,10 @@ SIZES = [(32, 32), (128, 128), (512, 512), (1024, 1024), (32, 256), (256, 32), (
 NS = [2 ** 14, 2 ** 16, 2 ** 18, 2 ** 20, 2 ** 21]
 DEGREES = [2, 8, 32, 128, 512]
 MAX_NNZ = 200_000_000
-NAMED = ("arxiv", "reddit", "products")  # benchmark shapes: train-only, never in the held-out split
+NAMED = ("arxiv", "reddit", "products")  # benchmark shapes: evaluated leave-one-shape-out
+# the named shapes also run the bench's square K sweep
+NAMED_SIZES = [(32, 32), (64, 64), (128, 128), (256, 256), (512, 512), (1024, 1024), (32, 256),
+               (256, 32), (64, 1024), (1024, 64)]
 
 
 def graph_plan(quick: bool = False) -> list[tuple[str, str, int, int]]:
@@ -69,7 +72,8 @@ def cmd_profile(args) -> None:
             print(f"skip {gid}: {e}", file=sys.stderr, flush=True)
             continue
         for model in args.models.split(","):
-            sizes = SIZES if model == "gcn" else [s for s in SIZES if s[0] <= 512 and s[1] <= 512]
+            base = NAMED_SIZES if args.graphs == "named" else SIZES
+            sizes = base if model == "gcn" else [s for s in base if s[0] <= 512 and s[1] <= 512]
             with warnings.catch_warnings():
                 warnings.simplefilter("ignore")
                 recs = profiling.profile([(gid, a)], sizes, model, reps=args.reps,
@@ -84,9 +88,10 @@ def cmd_profile(args) -> None:
     fh.close()
 
 
-def evaluate(model, records, comps) -> dict:
+def evaluate(model, records, comps, detail: bool = False) -> dict:
     from .selector import SelectorInput, select
 
+    rows = []
     groups: dict = {}
     for r in records:
         groups.setdefault((r.graph_id, r.k1, r.k2), {})[r.composition] = r
@@ -101,16 +106,23 @@ def evaluate(model, records, comps) -> dict:
                                            hw_descriptor=tuple(r0.hw_desc)))
         sel.append(g[pick].median_time_s / best)
         orc.append(1.0)
+        if detail:
+            fastest = min(comps, key=lambda c: g[c].median_time_s)
+            rows.append({"k1": r0.k1, "k2": r0.k2, "selected": pick, "fastest": fastest,
+                         "selected_over_fastest": round(sel[-1], 4)})
         for c in comps:
             static[c].append(g[c].median_time_s / best)
 
     def gm(x):
         return float(np.exp(np.mean(np.log(x)))) if x else float("nan")
 
-    return {"groups": len(sel), "selected_over_oracle_geomean": gm(sel),
-            "selected_over_oracle_max": float(max(sel)) if sel else None,
-            "within_1.1x": float(np.mean(np.array(sel) <= 1.1)) if sel else None,
-            "static_over_oracle_geomean": {c: gm(v) for c, v in static.items()}}
+    out = {"groups": len(sel), "selected_over_oracle_geomean": gm(sel),
+           "selected_over_oracle_max": float(max(sel)) if sel else None,
+           "within_1.1x": float(np.mean(np.array(sel) <= 1.1)) if sel else None,
+           "static_over_oracle_geomean": {c: gm(v) for c, v in static.items()}}
+    if detail:
+        out["per_group"] = sorted(rows, key=lambda x: (x["k1"], x["k2"]))
+    return out
 
 
 def cmd_train(args) -> None:
@@ -137,6 +149,20 @@ def cmd_train(args) -> None:
             m = train(tr, model_tag, hyper, compositions=comps)
         rep = {"train_graphs": len({r.graph_id for r in tr}), "test_graphs": sorted(test_g),
                "hyper": vars(hyper), "train": evaluate(m, tr, comps), "test": evaluate(m, te, comps)}
+        # leave-one-named-shape-out: the model never saw that benchmark shape
+        # (nor the random held-out graphs); evaluated on every (k1, k2) of it
+        lono = {}
+        for shape in NAMED:
+            held = [r for r in mine if r.graph_id == shape]
+            if not held:
+                continue
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                m_s = train([r for r in tr if r.graph_id != shape], model_tag, hyper,
+                            compositions=comps)
+            lono[shape] = evaluate(m_s, held, comps, detail=True)
+        if lono:
+            rep["leave_one_named_shape_out"] = lono
         with warnings.catch_warnings():
             warnings.simplefilter("ignore")
             full = train(mine, model_tag, hyper, compositions=comps)

@@ -78,7 +78,53 @@ def test_spmm_weighted_unweighted(oracle, plgraph, K, algo, monkeypatch):
     assert oracle.rel_err(outd, ref) < SP_TOL
 
 
-def test_spmm_unweighted_bit_identical_to_unit_weights(plgraph):
+@pytest.mark.parametrize("K", [4, 12, 32, 64, 256, 1024])
+def test_pack_rows_f16_semantics(K):
+    """gc_pack_rows_f16: xh = fp16_rn(x * 2^-e) with max|x_j| * 2^-e in
+    [2^14, 2^15), sigma = d * 2^e (exact), rows of zeros -> sigma = d."""
+    rng = np.random.default_rng(K)
+    x = f32(rng.uniform(-1, 1, (300, K)) * 2.0 ** rng.integers(-30, 30, (300, 1)))
+    x[7] = 0
+    d = f32(rng.uniform(0.1, 1, 300))
+    hr = sparse.pack_rows_f16(torch.from_numpy(x).to(DEV), torch.from_numpy(d).to(DEV))
+    mx = np.abs(x).max(1)
+    e = np.where(mx > 0, np.frexp(mx)[1] - 1 - 14, 0)
+    ref_h = (x * np.ldexp(1.0, -e)[:, None]).astype(np.float16)
+    assert np.array_equal(hr.xh[:, :K].cpu().numpy(), ref_h)
+    assert np.array_equal(hr.sigma.cpu().numpy(), f32(d * np.ldexp(1.0, e)))
+    # dequantised rows carry 11 significant bits
+    deq = hr.xh[:, :K].float().cpu().numpy() * hr.sigma.cpu().numpy()[:, None]
+    rel = np.abs(deq - x * d[:, None]).max(1) / np.maximum(np.abs(x * d[:, None]).max(1), 1e-30)
+    assert rel.max() <= 2.0 ** -11
+
+
+@pytest.mark.parametrize("K", [8, 32, 128, 256, 512])
+@pytest.mark.parametrize("algo", ["row", "split"])
+@pytest.mark.parametrize("weighted", [False, True])
+def test_spmm_fp16_operand_bit_exact_to_dequantised(plgraph, K, algo, weighted, monkeypatch):
+    """GC_SPMM_B_F16: the fp16-row gather computes exactly what the fp32 kernel
+    computes on the dequantised rows with d_col = sigma (same order), and
+    plain ReLU / accumulate epilogues."""
+    if algo == "split":
+        monkeypatch.setattr(sparse, "SPLIT_CHUNK", 16)
+    rng = np.random.default_rng(K + 5)
+    a = plgraph.with_values(torch.from_numpy(f32(rng.uniform(0.5, 2, plgraph.nnz))).to(DEV))
+    x = torch.from_numpy(f32(rng.standard_normal((a.n_cols, K)))).to(DEV)
+    d = torch.from_numpy(f32(rng.uniform(0.1, 1, a.n_rows))).to(DEV)
+    hr = sparse.pack_rows_f16(x, d)
+    deq = hr.xh[:, :K].float().contiguous()
+    f = gc.spmm if weighted else gc.spmm_unweighted
+    got = f(a, hr, d_row=d, relu=True, algo=algo)
+    ref = f(a, deq, d_row=d, d_col=hr.sigma, relu=True, algo=algo)
+    assert torch.equal(got, ref)
+    acc = torch.ones_like(got)
+    f(a, hr, d_row=d, out=acc, accumulate=True, algo=algo)
+    ref2 = torch.ones_like(got)
+    f(a, deq, d_row=d, d_col=hr.sigma, out=ref2, accumulate=True, algo=algo)
+    assert torch.equal(acc, ref2)
+
+
+def test_spmm_unweighted_bit_identical_to_unit_weights(plgraph):def test_spmm_unweighted_bit_identical_to_unit_weights(plgraph):
     rng = np.random.default_rng(1)
     b = torch.from_numpy(f32(rng.standard_normal((plgraph.n_cols, 64)))).to(DEV)
     ones = plgraph.with_values(torch.ones(plgraph.nnz, device=DEV))
