@@ -97,17 +97,22 @@ __device__ __forceinline__ void load_b_hint(float4 &dst, const float *p, bool ho
   dst = hot ? ldg_f4_keep(p) : ldg_f4_stream(p);
 }
 __device__ __forceinline__ void load_b_hint(float &dst, const float *p, bool) { dst = __ldg(p); }
-// fp16 operand rows (GC_SPMM_B_F16): four halves (8 bytes) per column slot,
-// widened to fp32 in registers (exact)
-__device__ __forceinline__ void load_bh(float4 &dst, const char *p) {
-  uint32_t lo, hi;
-  asm("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(lo), "=r"(hi) : "l"(p));
-  const float2 a = __half22float2(*reinterpret_cast<const __half2 *>(&lo));
-  const float2 b = __half22float2(*reinterpret_cast<const __half2 *>(&hi));
-  dst = make_float4(a.x, a.y, b.x, b.y);
+// fp16 operand rows (GC_SPMM_B_F16): one 16-byte load = eight halves = two
+// adjacent float4 column slots, widened to fp32 in registers (exact)
+__device__ __forceinline__ uint4 ldg_u4(const char *p) {
+  uint4 r;
+  asm("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p));
+  return r;
 }
-__device__ __forceinline__ void load_bh(float &dst, const char *p) {
-  dst = __half2float(*reinterpret_cast<const __half *>(p));
+__device__ __forceinline__ float2 h2f(uint32_t q) {
+  return __half22float2(*reinterpret_cast<const __half2 *>(&q));
+}
+__device__ __forceinline__ void widen_h8(uint4 q, float4 &lo4, float4 &hi4) {
+  const float2 a = h2f(q.x), b = h2f(q.y), c = h2f(q.z), d = h2f(q.w);
+  lo4 = make_float4(a.x, a.y, b.x, b.y);
+  hi4 = make_float4(c.x, c.y, d.x, d.y);
 }
 
 __device__ __forceinline__ float epi1(float v, float ds, float old, uint32_t flags) {
@@ -117,19 +122,23 @@ __device__ __forceinline__ float epi1(float v, float ds, float old, uint32_t fla
   return v;
 }
 
-template <int LPR, int NV, bool VEC>
+// Column of lane gl's slot v.  BH (fp16 rows): slots 2u and 2u+1 are the two
+// halves of one 8-column (16-byte) chunk, so each gather is a full 16-byte
+// load; otherwise slot v holds 4 columns at stride 4·LPR.
+template <int LPR, int NV, bool VEC, bool BH = false>
 __device__ __forceinline__ int64_t col_of(int64_t c0, int v, int gl) {
+  if (BH) return c0 + (int64_t)(v >> 1) * LPR * 8 + gl * 8 + (v & 1) * 4;
   return VEC ? c0 + (int64_t)v * LPR * 4 + gl * 4 : c0 + (int64_t)v * LPR + gl;
 }
 
-template <int LPR, int NV, bool VEC>
+template <int LPR, int NV, bool VEC, bool BH = false>
 __device__ __forceinline__ void store_row(const SpmmArgs &a, int row, int slot, int gl,
                                           int64_t c0, float ds,
                                           const typename Lanes<VEC>::T (&acc)[NV]) {
   const uint32_t flags = a.flags;
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
-    const int64_t c = col_of<LPR, NV, VEC>(c0, v, gl);
+    const int64_t c = col_of<LPR, NV, VEC, BH>(c0, v, gl);
     if (c >= a.K) continue;
     if (slot >= 0) {  // raw partial sum, combined later by spmm_fixup
       float *dst = a.partial + (int64_t)slot * a.K + c;
@@ -164,14 +173,17 @@ __device__ __forceinline__ void store_row(const SpmmArgs &a, int row, int slot, 
 template <int LPR, int NV, bool VEC, bool HAS_VAL, bool HAS_DCOL, int MODE, bool HINT,
           bool BH = false>
 __global__ void __launch_bounds__(kThreads, GNNC_SPMM_MINB) spmm_kernel(const SpmmArgs a) {
-  static_assert(!BH || (MODE == 0 && !HINT), "fp16 operand rows: plain SpMM without L1 tags");
+  static_assert(!BH || (MODE == 0 && !HINT && VEC && NV % 2 == 0),
+                "fp16 operand rows: plain SpMM without L1 tags, 16-byte chunks of two slots");
   using T = typename Lanes<VEC>::T;
   constexpr bool GAT = MODE != 0;
   constexpr bool SD = MODE == 2;
   constexpr int GPB = kThreads / LPR;
   // edges unrolled per step: ~8 independent 16-byte gathers in flight per lane
   // (never more than LPR: the edge batch is shuffled within the lane group)
-  constexpr int U0 = NV >= 8 ? 1 : NV >= 4 ? 2 : NV >= 2 ? 4 : 8;
+  // (BH: one 16-byte load covers two slots, so count loads, not slots)
+  constexpr int NVL = BH ? NV / 2 : NV;
+  constexpr int U0 = NVL >= 8 ? 1 : NVL >= 4 ? 2 : NVL >= 2 ? 4 : 8;
   constexpr int U = U0 < LPR ? U0 : LPR;
   const int g = threadIdx.x / LPR;
   const int gl = threadIdx.x % LPR;
@@ -198,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, GNNC_SPMM_MINB) spmm_kernel(const Sp
   const int kcols = (int)a.K;
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
-    coff[v] = (int)col_of<LPR, NV, VEC>(c0, v, gl);
+    coff[v] = (int)col_of<LPR, NV, VEC, BH>(c0, v, gl);
     colok[v] = coff[v] < kcols;
   }
 
@@ -285,6 +297,39 @@ __global__ void __launch_bounds__(kThreads, GNNC_SPMM_MINB) spmm_kernel(const Sp
     const int cntw = min(LPR, wmax - base);
 #pragma unroll 1
     for (int e0 = 0; e0 < cntw; e0 += U) {
+      if constexpr (BH) {
+        // fp16 rows: U edges x NV/2 raw 16-byte chunks in flight (4 registers
+        // each), widened to fp32 only at the FMA
+        constexpr int NVH = NV / 2;
+        uint4 rw[U][NVH];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int je = __shfl_sync(0xffffffffu, j, e0 + u, LPR);
+          const bool ok = (e0 + u) < cnt;
+          const char *brow_c = bbase + (uint64_t)(uint32_t)je * ldb_bytes;
+#pragma unroll
+          for (int c = 0; c < NVH; ++c)
+            if (ok && colok[2 * c])
+              rw[u][c] = ldg_u4(brow_c + (coff[2 * c] - coff[0]) * ESZ);
+        }
+        const float w = mine ? v * dj : 0.0f;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const float we = __shfl_sync(0xffffffffu, w, e0 + u, LPR);
+          if ((e0 + u) < cnt) {
+#pragma unroll
+            for (int c = 0; c < NVH; ++c) {
+              if (colok[2 * c]) {
+                float4 lo4, hi4;
+                widen_h8(rw[u][c], lo4, hi4);
+                fma_into(acc[2 * c], we, lo4);
+                fma_into(acc[2 * c + 1], we, hi4);
+              }
+            }
+          }
+        }
+        continue;
+      }
       // bv slots of edges past the row end (or columns past K) are never
       // loaded and never consumed: loads and FMAs share one predicate.
       // Row address = lane base + je * ldb (one 32x32->64 IMAD.WIDE per
@@ -294,15 +339,14 @@ __global__ void __launch_bounds__(kThreads, GNNC_SPMM_MINB) spmm_kernel(const Sp
       for (int u = 0; u < U; ++u) {
         const int je = __shfl_sync(0xffffffffu, j, e0 + u, LPR);
         const bool ok = (e0 + u) < cnt;
-        const char *brow_c = bbase + (uint64_t)(uint32_t)je * ldb_bytes;
-        const float *brow = reinterpret_cast<const float *>(brow_c);
+        const float *brow = reinterpret_cast<const float *>(
+            bbase + (uint64_t)(uint32_t)je * ldb_bytes);
         bool hote = false;
         if (HINT) hote = __shfl_sync(0xffffffffu, (int)hot, e0 + u, LPR) != 0;
 #pragma unroll
         for (int vv = 0; vv < NV; ++vv) {
           if (ok && colok[vv]) {
-            if constexpr (BH) load_bh(bv[u][vv], brow_c + vv * kSlotStride * ESZ);
-            else if (HINT) load_b_hint(bv[u][vv], brow + vv * kSlotStride, hote);
+            if (HINT) load_b_hint(bv[u][vv], brow + vv * kSlotStride, hote);
             else load_b(bv[u][vv], brow + vv * kSlotStride);
           }
         }
@@ -365,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, GNNC_SPMM_MINB) spmm_kernel(const Sp
   } else if (slot < 0 && live && a.d_row) {
     ds = __ldg(a.d_row + row);
   }
-  if (live) store_row<LPR, NV, VEC>(a, row, slot, gl, c0, ds, acc);
+  if (live) store_row<LPR, NV, VEC, BH>(a, row, slot, gl, c0, ds, acc);
 }
 
 // Combine the partial sums of split rows in slot order, then the epilogue.
@@ -496,26 +540,27 @@ int dispatch(SpmmArgs &a, int64_t n_rows, int algo, const int32_t *items, int64_
   GC_REQUIRE(a.ldb < (int64_t(1) << 30), GC_ERR_SHAPE, "%s: leading dimension too large", who);
   const int64_t K = a.K;
   if (MODE == 0 && (a.flags & GC_SPMM_B_F16)) {
-    // fp16 operand rows: 8-byte column slots, the float4 lane-group shapes
-    GC_REQUIRE(K % 4 == 0 && a.ldb % 4 == 0 && (reinterpret_cast<uintptr_t>(a.B) & 7u) == 0 &&
-                   a.ldc % 4 == 0 && aligned16(a.C) && (a.partial == nullptr || aligned16(a.partial)),
-               GC_ERR_UNSUPPORTED, "%s: fp16 operand needs K %% 4 == 0, ldb %% 4 == 0, 8-byte "
-               "aligned B and 16-byte aligned C", who);
+    // fp16 operand rows: each lane gathers 16-byte chunks (8 columns = two
+    // float4 slots), so the lane groups are half as wide as the fp32 shapes
+    GC_REQUIRE(K % 8 == 0 && a.ldb % 8 == 0 && aligned16(a.B) && a.ldc % 4 == 0 &&
+                   aligned16(a.C) && (a.partial == nullptr || aligned16(a.partial)),
+               GC_ERR_UNSUPPORTED, "%s: fp16 operand needs K %% 8 == 0, ldb %% 8 == 0 and "
+               "16-byte aligned B and C", who);
     GC_REQUIRE(!a.hints, GC_ERR_UNSUPPORTED, "%s: no hub tags with an fp16 operand", who);
     cudaStream_t sth = as_stream(stream);
     const int sh = (int)((a.flags >> 8) & 3u);
-    if (K <= 8) return launch_cfg<2, 1, true, 0, true>(a, sr, n_split, sth);
-    if (K <= 16) return sh ? launch_cfg<2, 2, true, 0, true>(a, sr, n_split, sth)
-                           : launch_cfg<4, 1, true, 0, true>(a, sr, n_split, sth);
-    if (K <= 32) return sh == 2 ? launch_cfg<2, 4, true, 0, true>(a, sr, n_split, sth)
-                      : sh == 1 ? launch_cfg<4, 2, true, 0, true>(a, sr, n_split, sth)
-                                : launch_cfg<8, 1, true, 0, true>(a, sr, n_split, sth);
-    if (K <= 64) return sh == 2 ? launch_cfg<4, 4, true, 0, true>(a, sr, n_split, sth)
-                      : sh == 1 ? launch_cfg<8, 2, true, 0, true>(a, sr, n_split, sth)
-                                : launch_cfg<16, 1, true, 0, true>(a, sr, n_split, sth);
-    if (K <= 128) return sh == 2 ? launch_cfg<8, 4, true, 0, true>(a, sr, n_split, sth)
-                       : sh == 1 ? launch_cfg<16, 2, true, 0, true>(a, sr, n_split, sth)
-                                 : launch_cfg<32, 1, true, 0, true>(a, sr, n_split, sth);
+    if (K <= 16) return launch_cfg<2, 2, true, 0, true>(a, sr, n_split, sth);
+    if (K <= 32) return sh ? launch_cfg<2, 4, true, 0, true>(a, sr, n_split, sth)
+                           : launch_cfg<4, 2, true, 0, true>(a, sr, n_split, sth);
+    if (K <= 64) return sh == 2 ? launch_cfg<2, 8, true, 0, true>(a, sr, n_split, sth)
+                      : sh == 1 ? launch_cfg<4, 4, true, 0, true>(a, sr, n_split, sth)
+                                : launch_cfg<8, 2, true, 0, true>(a, sr, n_split, sth);
+    if (K <= 128) return sh == 2 ? launch_cfg<4, 8, true, 0, true>(a, sr, n_split, sth)
+                       : sh == 1 ? launch_cfg<8, 4, true, 0, true>(a, sr, n_split, sth)
+                                 : launch_cfg<16, 2, true, 0, true>(a, sr, n_split, sth);
+    if (K <= 256) return sh == 2 ? launch_cfg<8, 8, true, 0, true>(a, sr, n_split, sth)
+                       : sh == 1 ? launch_cfg<16, 4, true, 0, true>(a, sr, n_split, sth)
+                                 : launch_cfg<32, 2, true, 0, true>(a, sr, n_split, sth);
     return sh == 2 ? launch_cfg<8, 8, true, 0, true>(a, sr, n_split, sth)
          : sh == 1 ? launch_cfg<16, 4, true, 0, true>(a, sr, n_split, sth)
                    : launch_cfg<32, 2, true, 0, true>(a, sr, n_split, sth);
@@ -563,43 +608,57 @@ int dispatch(SpmmArgs &a, int64_t n_rows, int algo, const int32_t *items, int64_
 //   Xh[j,k] = fp16_rn(X[j,k] * 2^-e_j),   sigma[j] = (d ? d[j] : 1) * 2^e_j,
 // so X[j,:] * d[j] = sigma[j] * Xh[j,:] up to the fp16 rounding of each
 // element (11 significant bits — the same input rounding TF32 applies).
-// One warp per row, float4 reads, 8-byte writes.
+// A group of LPR lanes per row (LPR = K/4 up to 32: narrow rows do not leave
+// lanes idle), float4 reads kept in registers between the max and the
+// conversion when the row fits one pass, 8-byte writes.
+template <int LPR>
 __global__ void __launch_bounds__(256)
     pack_rows_f16_kernel(const float *__restrict__ X, int64_t ldx, int64_t n, int64_t K,
                          const float *__restrict__ d, __half *__restrict__ Xh, int64_t ldh,
                          float *__restrict__ sigma, bool vec) {
-  const int lane = threadIdx.x % 32;
-  const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x / 32);
-  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; r < n; r += n_warps) {
-    const float *x = X + r * ldx;
-    float mx = 0.0f;
-    if (vec)
-      for (int64_t c = 4 * lane; c < K; c += 128) {
-        const float4 v = ldg_f4(x + c);
-        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
-      }
-    else
-      for (int64_t c = lane; c < K; c += 32) mx = fmaxf(mx, fabsf(__ldg(x + c)));
-    mx = group_max<32>(mx);
-    // exponent of mx (frexp-style, exact): mx = m * 2^E, m in [1, 2)
-    const int E = mx > 0.0f ? ((int)((__float_as_uint(mx) >> 23) & 0xff) - 127) : 0;
-    const int e = mx > 0.0f && isfinite(mx) ? max(min(E - 14, 110), -110) : 0;
-    const float down = __uint_as_float((uint32_t)(127 - e) << 23);  // 2^-e, |e| <= 110
-    __half *h = Xh + r * ldh;
-    if (vec)
-      for (int64_t c = 4 * lane; c < K; c += 128) {
-        const float4 v = ldg_f4(x + c);
-        const __half2 a = __floats2half2_rn(v.x * down, v.y * down);
-        const __half2 b = __floats2half2_rn(v.z * down, v.w * down);
-        uint2 packed;
-        packed.x = *reinterpret_cast<const uint32_t *>(&a);
-        packed.y = *reinterpret_cast<const uint32_t *>(&b);
-        *reinterpret_cast<uint2 *>(h + c) = packed;
-      }
-    else
-      for (int64_t c = lane; c < K; c += 32) h[c] = __float2half_rn(__ldg(x + c) * down);
-    if (lane == 0) sigma[r] = (d ? __ldg(d + r) : 1.0f) * __uint_as_float((uint32_t)(127 + e) << 23);
+  const int gl = threadIdx.x % LPR;
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPR;
+  const bool live = r < n;
+  const float *x = X + (live ? r : 0) * ldx;
+  float mx = 0.0f;
+  // the lane's first two chunks stay in registers between the max and the
+  // conversion (a row of K <= 8·LPR is read once)
+  const int64_t c0 = 4 * gl, c1 = c0 + 4 * LPR, step = 4 * LPR;
+  float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
+  auto amax4 = [](float4 v) {
+    return fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+  };
+  if (vec && live) {
+    if (c0 < K) v0 = ldg_f4(x + c0);
+    if (c1 < K) v1 = ldg_f4(x + c1);
+    mx = fmaxf(amax4(v0), amax4(v1));
+    for (int64_t c = c1 + step; c < K; c += step) mx = fmaxf(mx, amax4(ldg_f4(x + c)));
+  } else if (live) {
+    for (int64_t c = gl; c < K; c += LPR) mx = fmaxf(mx, fabsf(__ldg(x + c)));
   }
+  mx = group_max<LPR>(mx);
+  if (!live) return;
+  // exponent of mx (exact): mx = m * 2^E, m in [1, 2)
+  const int E = mx > 0.0f ? ((int)((__float_as_uint(mx) >> 23) & 0xff) - 127) : 0;
+  const int e = mx > 0.0f && isfinite(mx) ? max(min(E - 14, 110), -110) : 0;
+  const float down = __uint_as_float((uint32_t)(127 - e) << 23);  // 2^-e, |e| <= 110
+  __half *h = Xh + r * ldh;
+  auto put4 = [&](int64_t c, float4 v) {
+    const __half2 a = __floats2half2_rn(v.x * down, v.y * down);
+    const __half2 b = __floats2half2_rn(v.z * down, v.w * down);
+    uint2 packed;
+    packed.x = *reinterpret_cast<const uint32_t *>(&a);
+    packed.y = *reinterpret_cast<const uint32_t *>(&b);
+    *reinterpret_cast<uint2 *>(h + c) = packed;
+  };
+  if (vec) {
+    if (c0 < K) put4(c0, v0);
+    if (c1 < K) put4(c1, v1);
+    for (int64_t c = c1 + step; c < K; c += step) put4(c, ldg_f4(x + c));
+  } else {
+    for (int64_t c = gl; c < K; c += LPR) h[c] = __float2half_rn(__ldg(x + c) * down);
+  }
+  if (gl == 0) sigma[r] = (d ? __ldg(d + r) : 1.0f) * __uint_as_float((uint32_t)(127 + e) << 23);
 }
 
 __global__ void tag_hub_kernel(const int32_t *__restrict__ col, int64_t nnz,
@@ -625,9 +684,23 @@ extern "C" int gc_pack_rows_f16(const float *X, int64_t ldx, int64_t n_rows, int
   GC_REQUIRE(X && Xh && sigma, GC_ERR_VALUE, "gc_pack_rows_f16: null operand");
   const bool vec = K % 4 == 0 && ldx % 4 == 0 && ldh % 4 == 0 && aligned16(X) &&
                    (reinterpret_cast<uintptr_t>(Xh) & 7u) == 0;
-  const int64_t blocks = std::min<int64_t>((n_rows + 7) / 8, (int64_t)sm_count() * 16);
-  pack_rows_f16_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(
-      X, ldx, n_rows, K, d, static_cast<__half *>(Xh), ldh, sigma, vec);
+  const int64_t q = vec ? (K + 3) / 4 : K;  // lanes a row could use
+  const int lpr = q >= 32 ? 32 : q >= 16 ? 16 : q >= 8 ? 8 : q >= 4 ? 4 : q >= 2 ? 2 : 1;
+  const int64_t blocks = (n_rows * lpr + 255) / 256;
+  GC_REQUIRE(blocks < INT32_MAX, GC_ERR_SHAPE, "gc_pack_rows_f16: too many rows");
+  __half *xh = static_cast<__half *>(Xh);
+  cudaStream_t st = as_stream(stream);
+#define GC_PACK(L) \
+  pack_rows_f16_kernel<L><<<(unsigned)blocks, 256, 0, st>>>(X, ldx, n_rows, K, d, xh, ldh, sigma, vec)
+  switch (lpr) {
+    case 1: GC_PACK(1); break;
+    case 2: GC_PACK(2); break;
+    case 4: GC_PACK(4); break;
+    case 8: GC_PACK(8); break;
+    case 16: GC_PACK(16); break;
+    default: GC_PACK(32); break;
+  }
+#undef GC_PACK
   return check_launch("pack_rows_f16_kernel");
 }
 

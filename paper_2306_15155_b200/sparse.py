@@ -684,7 +684,7 @@ def pack_rows_f16(x: torch.Tensor, d: torch.Tensor | None = None) -> HalfRows:
     n, K = x.shape
     if d is not None and tuple(d.shape) != (n,):
         raise ShapeError("pack_rows_f16: d must have one entry per row")
-    ldh = (K + 3) // 4 * 4
+    ldh = (K + 7) // 8 * 8  # 16-byte rows for the gather kernel
     xh = torch.empty(n, ldh, dtype=torch.float16, device=x.device)
     sigma = torch.empty(n, dtype=torch.float32, device=x.device)
     nat.check(nat.load().gc_pack_rows_f16(x.data_ptr(), _ld(x), n, K, _ptr(d), xh.data_ptr(), ldh,

@@ -124,7 +124,7 @@ def test_spmm_fp16_operand_bit_exact_to_dequantised(plgraph, K, algo, weighted, 
     assert torch.equal(acc, ref2)
 
 
-def test_spmm_unweighted_bit_identical_to_unit_weights(plgraph):def test_spmm_unweighted_bit_identical_to_unit_weights(plgraph):
+def test_spmm_unweighted_bit_identical_to_unit_weights(plgraph):
     rng = np.random.default_rng(1)
     b = torch.from_numpy(f32(rng.standard_normal((plgraph.n_cols, 64)))).to(DEV)
     ones = plgraph.with_values(torch.ones(plgraph.nnz, device=DEV))
