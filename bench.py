@@ -647,6 +647,9 @@ def main():
         # ---- composition sweep ---------------------------------------------------
         if not args.no_sweep:
             result["sweep"] = sweep(gc, g, feats, args, dev, pk, parity)
+            if not args.no_extra:  # GAT on the same Reddit shape (selector check)
+                result["gat_reddit"] = gat_rows_reddit(gc, g.a_tilde, feats, 256, parity,
+                                                       tol_of(gc), dev, selector_pick, timed_runs)
         del parity
         if not args.no_extra:
             result["extra_configs"] = extra_configs(gc, args, dev, pk)
@@ -847,6 +850,31 @@ def cora_config(gc, args, dev) -> dict:
     return out
 
 
+def selector_pick(row_comps: dict, model: str, feats, K: int) -> dict:
+    """The B200 selector's choice for this group and its time over the
+    fastest composition measured (north-star target: <= 1.1)."""
+    from paper_2306_15155_b200 import selector
+
+    mdl = selector.load_b200_model(model)
+    if mdl is None:
+        return {}
+    sel = selector.select(mdl, selector.SelectorInput(features=feats, k1=K, k2=K))
+    best = min(row_comps, key=lambda c: row_comps[c]["ms"])
+    out = {"fastest": best, "selected": sel}
+    if sel in row_comps:
+        out["selected_over_fastest"] = round(row_comps[sel]["ms"] / row_comps[best]["ms"], 3)
+    return out
+
+
+def timed_runs(runs: dict, rounds: int = 3, reps: int = 3) -> dict:
+    """Median over interleaved rounds of each run's CUDA-event median."""
+    ts = {c: [] for c in runs}
+    for _ in range(rounds):
+        for c, fn in runs.items():
+            ts[c].append(_time_layer(fn, reps))
+    return {c: float(np.median(v)) for c, v in ts.items()}
+
+
 def extra_configs(gc, args, dev, pk) -> dict:
     """BASELINE configs[0] (Cora), [2] (single/4-head GAT on arxiv, SDDMM vs
     reassociated attention, reuse vs recompute, K = 32..1024) and [3] (GCN +
@@ -857,27 +885,8 @@ def extra_configs(gc, args, dev, pk) -> dict:
     from paper_2306_15155_b200 import graphs, selector
 
     res = {"cora": cora_config(gc, args, dev)}
-    models = {t: selector.load_b200_model(t) for t in ("gcn", "gat")}
     tol = tol_of(gc)
-
-    def pick(row_comps: dict, model: str, feats, K: int) -> dict:
-        """The B200 selector's choice for this group and its time over the
-        fastest composition measured (north-star target: <= 1.1)."""
-        if models[model] is None:
-            return {}
-        sel = selector.select(models[model], selector.SelectorInput(features=feats, k1=K, k2=K))
-        best = min(row_comps, key=lambda c: row_comps[c]["ms"])
-        out = {"fastest": best, "selected": sel}
-        if sel in row_comps:
-            out["selected_over_fastest"] = round(row_comps[sel]["ms"] / row_comps[best]["ms"], 3)
-        return out
-
-    def timed(runs: dict, rounds: int = 3, reps: int = 3) -> dict:
-        ts = {c: [] for c in runs}
-        for _ in range(rounds):
-            for c, fn in runs.items():
-                ts[c].append(_time_layer(fn, reps))
-        return {c: float(np.median(v)) for c, v in ts.items()}
+    pick, timed = selector_pick, timed_runs
 
     # ---- GAT on ogbn-arxiv-shaped RMAT ---------------------------------------
     A = graphs.shape_graph("arxiv", seed=args.seed, device=dev)
@@ -910,7 +919,11 @@ def extra_configs(gc, args, dev, pk) -> dict:
             del h, w, specs
             torch.cuda.empty_cache()
     res["gat_arxiv"] = {"n": n, "m_tilde": m, "rows": gat}
-    del at, par
+    # GCN on the same arxiv shape (every composition, with the selector check)
+    ga = gc.NormalizedGraph(a_tilde=at, d_inv_sqrt=gc.inv_sqrt_degrees(at)).with_precomputed()
+    res["gcn_arxiv"] = {"n": n, "m_tilde": m,
+                        "rows": gcn_rows(gc, ga, feats, (32, 256, 1024), par, tol, dev, pick, timed)}
+    del at, par, ga
     torch.cuda.empty_cache()
     # ---- products-shaped: GCN (4 compositions) + GAT -------------------------
     A = graphs.shape_graph("products", seed=args.seed, device=dev)
@@ -920,7 +933,7 @@ def extra_configs(gc, args, dev, pk) -> dict:
     par = Parity(g.a_tilde, args.parity_rows, seed=args.seed + 2)
     n, m = g.a_tilde.n_rows, g.a_tilde.nnz
     rows = []
-    for K in (32, 256):
+    for K in (32, 256, 1024):
         gen = torch.Generator(device=dev)
         gen.manual_seed(K)
         h = torch.rand(n, K, device=dev, generator=gen) - 0.5
@@ -961,6 +974,60 @@ def extra_configs(gc, args, dev, pk) -> dict:
     del g, par
     torch.cuda.empty_cache()
     return res
+
+
+def gcn_rows(gc, g, feats, ks, par, tol, dev, pick, timed) -> list[dict]:
+    """Every GCN composition at each K on graph ``g`` (interleaved timing,
+    row-sampled parity) and the selector's pick over the fastest."""
+    import torch
+
+    from paper_2306_15155_b200 import selector
+
+    n, m = g.a_tilde.n_rows, g.a_tilde.nnz
+    rows = []
+    for K in ks:
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(K + 17)
+        h = torch.rand(n, K, device=dev, generator=gen) - 0.5
+        w = torch.rand(K, K, device=dev, generator=gen) - 0.5
+        specs = {c: gc.GcnLayerSpec(K, K, w, composition=c.split(":")[0], order=c.split(":")[1])
+                 for c in selector.B200_COMPOSITIONS["gcn"]}
+        t = timed({c: (lambda s=s: gc.gcn_layer(g, h, s)) for c, s in specs.items()})
+        row = {"K": K, "compositions": {}}
+        for c, spec in specs.items():
+            row["compositions"][c] = {"ms": round(t[c] * 1e3, 4), "edges_per_s": round(m / t[c], 1),
+                                      "parity": par.gcn(gc.gcn_layer(g, h, spec), h, w, c, tol)}
+        row.update(pick(row["compositions"], "gcn", feats, K))
+        rows.append(row)
+        del h, w
+        torch.cuda.empty_cache()
+    return rows
+
+
+def gat_rows_reddit(gc, a_tilde, feats, K, par, tol, dev, pick, timed) -> dict:
+    """Single-head GAT, every composition, on the Reddit shape at one K."""
+    import torch
+
+    from paper_2306_15155_b200 import selector
+
+    n, m = a_tilde.n_rows, a_tilde.nnz
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(K + 29)
+    h = torch.rand(n, K, device=dev, generator=gen) - 0.5
+    w = torch.rand(K, K, device=dev, generator=gen) - 0.5
+    a_s = torch.rand(K, device=dev, generator=gen) - 0.5
+    a_d = torch.rand(K, device=dev, generator=gen) - 0.5
+    specs = {c: gc.GatLayerSpec(K, K, w, a_s, a_d, composition=c.split(":")[0],
+                                attention=c.split(":")[1])
+             for c in selector.B200_COMPOSITIONS["gat"]}
+    t = timed({c: (lambda s=s: gc.gat_layer(a_tilde, h, s)) for c, s in specs.items()})
+    row = {"K": K, "heads": 1, "compositions": {}}
+    for c, spec in specs.items():
+        row["compositions"][c] = {"ms": round(t[c] * 1e3, 4), "edges_per_s": round(m / t[c], 1),
+                                  "parity": par.gat(gc.gat_layer(a_tilde, h, spec), h, w, a_s, a_d,
+                                                    1, c, tol)}
+    row.update(pick(row["compositions"], "gat", feats, K))
+    return row
 
 
 def partitioned_products(args, rank: int, world: int, dev) -> dict | None:

@@ -122,10 +122,13 @@ GNNC_API int gc_spmm_plan_fill(const int32_t *row_ptr_host, int64_t n_rows, int3
  * an online softmax so alpha is never materialised.  Rows without edges give 0.
  * Same plan/workspace protocol as gc_spmm_f32; NNZ_SPLIT needs
  * n_slots*(4*K + 8) + 8 bytes of workspace (partial rows, then 8-byte aligned
- * (max, sum) pairs). */
+ * (max, sum) pairs).  GC_SPMM_B_F16: B holds fp16 rows (gc_pack_rows_f16) and
+ * sigma their row scales (NULL otherwise); sigma_j scales row j in the
+ * aggregation, not the softmax. */
 GNNC_API int gc_gat_aggregate_f32(const int32_t *row_ptr, const int32_t *col_idx, const float *s,
                                   const float *t, float slope, const float *B, int64_t ldb,
-                                  int64_t n_rows, int64_t n_cols, int64_t K, float *C, int64_t ldc,
+                                  const float *sigma, int64_t n_rows, int64_t n_cols, int64_t K,
+                                  float *C, int64_t ldc,
                                   uint32_t flags, int algo, const int32_t *items, int64_t n_items,
                                   const int32_t *split_rows, int64_t n_split_rows, void *workspace,
                                   size_t ws_bytes, void *stream);
@@ -155,11 +158,14 @@ GNNC_API int gc_tag_hub_columns(const int32_t *col_idx, int64_t nnz, const uint8
  * pattern); a rank's row block of a partitioned graph passes its own rows of
  * HW as B_self and the gathered HW as B.  Needs K % 4 == 0, K <= 1024,
  * 16-byte aligned B/B_self/C/a_src/a_dst (else GC_ERR_UNSUPPORTED).
- * Plan/workspace protocol as gc_gat_aggregate_f32. */
+ * Plan/workspace protocol as gc_gat_aggregate_f32.  GC_SPMM_B_F16: B holds
+ * fp16 rows with row scales sigma (the score uses sigma_j * a_dst.Bh[j,:]);
+ * B_self must then be the fp32 source rows. */
 GNNC_API int gc_gat_sddmm_aggregate_f32(const int32_t *row_ptr, const int32_t *col_idx,
                                         const float *a_src, const float *a_dst, float slope,
                                         const float *B, int64_t ldb, const float *B_self,
-                                        int64_t ld_self, int64_t n_rows, int64_t K,
+                                        int64_t ld_self, const float *sigma, int64_t n_rows,
+                                        int64_t K,
                                         float *C, int64_t ldc, uint32_t flags, int algo,
                                         const int32_t *items, int64_t n_items,
                                         const int32_t *split_rows, int64_t n_split_rows,

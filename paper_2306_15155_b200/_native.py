@@ -71,10 +71,11 @@ _SIGNATURES = {
                                    _SZ, _P]),
     "gc_scale_rows_f32": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _P, _I64, _U32, _P]),
     "gc_node_proj_f32": (ctypes.c_int, [_P, _I64, _I64, _I64, _I32, _I64, _P, _P, _P, _P, _P]),
-    "gc_gat_sddmm_aggregate_f32": (ctypes.c_int, [_P, _P, _P, _P, _F, _P, _I64, _P, _I64, _I64, _I64,
-                                                  _P, _I64,
+    "gc_gat_sddmm_aggregate_f32": (ctypes.c_int, [_P, _P, _P, _P, _F, _P, _I64, _P, _I64, _P, _I64,
+                                                  _I64, _P, _I64,
                                                   _U32, ctypes.c_int, _P, _I64, _P, _I64, _P, _SZ, _P]),
-    "gc_gat_aggregate_f32": (ctypes.c_int, [_P, _P, _P, _P, _F, _P, _I64, _I64, _I64, _I64, _P, _I64,
+    "gc_gat_aggregate_f32": (ctypes.c_int, [_P, _P, _P, _P, _F, _P, _I64, _P, _I64, _I64, _I64, _P,
+                                            _I64,
                                             _U32, ctypes.c_int, _P, _I64, _P, _I64, _P, _SZ, _P]),
     "gc_edge_softmax_heavy_threshold": (ctypes.c_int, [_I64, _I64]),
     "gc_edge_softmax_f32": (ctypes.c_int, [_P, _P, _P, _P, _I32, _F, _I64, _I64, _P, _I64, _P, _P]),

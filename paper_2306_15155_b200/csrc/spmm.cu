@@ -173,8 +173,12 @@ __device__ __forceinline__ void store_row(const SpmmArgs &a, int row, int slot, 
 template <int LPR, int NV, bool VEC, bool HAS_VAL, bool HAS_DCOL, int MODE, bool HINT,
           bool BH = false>
 __global__ void __launch_bounds__(kThreads, GNNC_SPMM_MINB) spmm_kernel(const SpmmArgs a) {
-  static_assert(!BH || (MODE == 0 && !HINT && VEC && NV % 2 == 0),
-                "fp16 operand rows: plain SpMM without L1 tags, 16-byte chunks of two slots");
+  static_assert(!BH || (!HINT && VEC && NV % 2 == 0),
+                "fp16 operand rows: no L1 tags, 16-byte chunks of two slots");
+  // GAT modes with fp16 rows: the row scale sigma_j (a.d_col) is gathered
+  // per edge beside t_j; it scales the gathered row in the score (SD) and
+  // in the aggregation, never the softmax denominator
+  constexpr bool SIG = BH && MODE != 0;
   using T = typename Lanes<VEC>::T;
   constexpr bool GAT = MODE != 0;
   constexpr bool SD = MODE == 2;
@@ -227,6 +231,7 @@ __global__ void __launch_bounds__(kThreads, GNNC_SPMM_MINB) spmm_kernel(const Sp
   // GAT: online softmax state; m is identical on every lane of the group,
   // zl sums this lane's own edge weights relative to m.
   float si = (MODE == 1 && live) ? __ldg(a.s + row) : 0.0f;
+  float gs1 = 1.0f;  // SIG: sigma of this lane's edge in the next batch
   float m = -INFINITY, zl = 0.0f;
   T adst[NV];
   if constexpr (SD) {  // source term a_src.B_i and this lane's slice of a_dst
@@ -257,6 +262,7 @@ __global__ void __launch_bounds__(kThreads, GNNC_SPMM_MINB) spmm_kernel(const Sp
     j1 = ldg_stream_i32(a.col_idx + beg + gl);
     if (HAS_VAL) v1 = ldg_stream_f32(a.values + beg + gl);
     if (NEEDG) g1 = __ldg((MODE == 1 ? a.t : a.d_col) + (HINT ? (j1 & 0x7FFFFFFF) : j1));
+    if (SIG) gs1 = __ldg(a.d_col + j1);
   }
   if (LPR + gl < len) {
     j2 = ldg_stream_i32(a.col_idx + beg + LPR + gl);
@@ -267,11 +273,13 @@ __global__ void __launch_bounds__(kThreads, GNNC_SPMM_MINB) spmm_kernel(const Sp
     const bool hot = HINT && j1 < 0;
     const float v = v1;
     const float g = g1;
+    const float gsig = gs1;
     const bool mine = base + gl < len;
     j1 = j2;
     v1 = v2;
     if (NEEDG && base + LPR + gl < len)
       g1 = __ldg((MODE == 1 ? a.t : a.d_col) + (HINT ? (j1 & 0x7FFFFFFF) : j1));
+    if (SIG && base + LPR + gl < len) gs1 = __ldg(a.d_col + j1);
     if (base + 2 * LPR + gl < len) {
       j2 = ldg_stream_i32(a.col_idx + beg + base + 2 * LPR + gl);
       if (HAS_VAL) v2 = ldg_stream_f32(a.values + beg + base + 2 * LPR + gl);
@@ -297,9 +305,10 @@ __global__ void __launch_bounds__(kThreads, GNNC_SPMM_MINB) spmm_kernel(const Sp
     const int cntw = min(LPR, wmax - base);
 #pragma unroll 1
     for (int e0 = 0; e0 < cntw; e0 += U) {
+      T bv[U][NV];
       if constexpr (BH) {
-        // fp16 rows: U edges x NV/2 raw 16-byte chunks in flight (4 registers
-        // each), widened to fp32 only at the FMA
+        // fp16 rows: U edges x NV/2 raw 16-byte chunks in flight (4
+        // registers each), widened to fp32 once all have been issued
         constexpr int NVH = NV / 2;
         uint4 rw[U][NVH];
 #pragma unroll
@@ -309,34 +318,16 @@ __global__ void __launch_bounds__(kThreads, GNNC_SPMM_MINB) spmm_kernel(const Sp
           const char *brow_c = bbase + (uint64_t)(uint32_t)je * ldb_bytes;
 #pragma unroll
           for (int c = 0; c < NVH; ++c)
-            if (ok && colok[2 * c])
-              rw[u][c] = ldg_u4(brow_c + (coff[2 * c] - coff[0]) * ESZ);
+            if (ok && colok[2 * c]) rw[u][c] = ldg_u4(brow_c + (coff[2 * c] - coff[0]) * ESZ);
         }
-        const float w = mine ? v * dj : 0.0f;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const float we = __shfl_sync(0xffffffffu, w, e0 + u, LPR);
-          if ((e0 + u) < cnt) {
+        for (int u = 0; u < U; ++u)
 #pragma unroll
-            for (int c = 0; c < NVH; ++c) {
-              if (colok[2 * c]) {
-                float4 lo4, hi4;
-                widen_h8(rw[u][c], lo4, hi4);
-                fma_into(acc[2 * c], we, lo4);
-                fma_into(acc[2 * c + 1], we, hi4);
-              }
-            }
-          }
-        }
-        continue;
+          for (int c = 0; c < NVH; ++c)
+            if ((e0 + u) < cnt && colok[2 * c]) widen_h8(rw[u][c], bv[u][2 * c], bv[u][2 * c + 1]);
       }
-      // bv slots of edges past the row end (or columns past K) are never
-      // loaded and never consumed: loads and FMAs share one predicate.
-      // Row address = lane base + je * ldb (one 32x32->64 IMAD.WIDE per
-      // edge); the NV slots of a row sit at compile-time offsets.
-      T bv[U][NV];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
+      for (int u = 0; u < U && !BH; ++u) {
         const int je = __shfl_sync(0xffffffffu, j, e0 + u, LPR);
         const bool ok = (e0 + u) < cnt;
         const float *brow = reinterpret_cast<const float *>(
@@ -354,14 +345,15 @@ __global__ void __launch_bounds__(kThreads, GNNC_SPMM_MINB) spmm_kernel(const Sp
       if constexpr (SD) {
         // per-edge score from the row just gathered, then an online-softmax
         // update in edge order (m, zl identical on every lane of the group)
-        float eu[U];
+        float eu[U], su[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
+          su[u] = SIG ? __shfl_sync(0xffffffffu, gsig, e0 + u, LPR) : 1.0f;
           float part = 0.0f;
 #pragma unroll
           for (int vv = 0; vv < NV; ++vv)
             if ((e0 + u) < cnt && colok[vv]) part += dot_of(bv[u][vv], adst[vv]);
-          part = group_sum<LPR>(part);
+          part = group_sum<LPR>(part) * su[u];
           eu[u] = (e0 + u) < cnt ? leaky(si + part, a.slope) : -INFINITY;
         }
 #pragma unroll
@@ -376,16 +368,17 @@ __global__ void __launch_bounds__(kThreads, GNNC_SPMM_MINB) spmm_kernel(const Sp
             }
             const float w = __expf(eu[u] - m);
             zl += w;
+            const float wa = w * su[u];
 #pragma unroll
             for (int vv = 0; vv < NV; ++vv)
-              if (colok[vv]) fma_into(acc[vv], w, bv[u][vv]);
+              if (colok[vv]) fma_into(acc[vv], wa, bv[u][vv]);
           }
         }
       } else {
         // unit weights (value-blind, no d_j): no weight shuffle; fma(1, b, acc)
         // rounds exactly like the weighted kernel with unit values
         constexpr bool UNIT = !HAS_VAL && !HAS_DCOL && MODE == 0;
-        const float w = mine ? v * dj : 0.0f;
+        const float w = mine ? v * dj * (SIG ? gsig : 1.0f) : 0.0f;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const float we = UNIT ? 1.0f : __shfl_sync(0xffffffffu, w, e0 + u, LPR);
@@ -468,7 +461,9 @@ int launch_cfg(const SpmmArgs &a, const int4 *split_rows, int64_t n_split, cudaS
   if (a.n_items > 0) {
     dim3 grid((unsigned)((a.n_items + GPB - 1) / GPB), (unsigned)ychunks);
     const bool hv = a.values != nullptr, hd = a.d_col != nullptr;
-    if constexpr (BH) {
+    if constexpr (BH && MODE != 0) {
+      spmm_kernel<LPR, NV, VEC, false, false, MODE, false, true><<<grid, kThreads, 0, st>>>(a);
+    } else if constexpr (BH) {
       if (hv && hd) spmm_kernel<LPR, NV, VEC, true, true, 0, false, true><<<grid, kThreads, 0, st>>>(a);
       else if (hv) spmm_kernel<LPR, NV, VEC, true, false, 0, false, true><<<grid, kThreads, 0, st>>>(a);
       else if (hd) spmm_kernel<LPR, NV, VEC, false, true, 0, false, true><<<grid, kThreads, 0, st>>>(a);
@@ -539,7 +534,7 @@ int dispatch(SpmmArgs &a, int64_t n_rows, int algo, const int32_t *items, int64_
   }
   GC_REQUIRE(a.ldb < (int64_t(1) << 30), GC_ERR_SHAPE, "%s: leading dimension too large", who);
   const int64_t K = a.K;
-  if (MODE == 0 && (a.flags & GC_SPMM_B_F16)) {
+  if (a.flags & GC_SPMM_B_F16) {
     // fp16 operand rows: each lane gathers 16-byte chunks (8 columns = two
     // float4 slots), so the lane groups are half as wide as the fp32 shapes
     GC_REQUIRE(K % 8 == 0 && a.ldb % 8 == 0 && aligned16(a.B) && a.ldc % 4 == 0 &&
@@ -547,23 +542,28 @@ int dispatch(SpmmArgs &a, int64_t n_rows, int algo, const int32_t *items, int64_
                GC_ERR_UNSUPPORTED, "%s: fp16 operand needs K %% 8 == 0, ldb %% 8 == 0 and "
                "16-byte aligned B and C", who);
     GC_REQUIRE(!a.hints, GC_ERR_UNSUPPORTED, "%s: no hub tags with an fp16 operand", who);
+    GC_REQUIRE(MODE == 0 || a.d_col != nullptr, GC_ERR_VALUE, "%s: fp16 rows need sigma", who);
+    GC_REQUIRE(MODE != 2 || (a.B_self != a.B && a.B_self != nullptr), GC_ERR_VALUE,
+               "%s: fp16 rows need fp32 source rows B_self", who);
     cudaStream_t sth = as_stream(stream);
     const int sh = (int)((a.flags >> 8) & 3u);
-    if (K <= 16) return launch_cfg<2, 2, true, 0, true>(a, sr, n_split, sth);
-    if (K <= 32) return sh ? launch_cfg<2, 4, true, 0, true>(a, sr, n_split, sth)
-                           : launch_cfg<4, 2, true, 0, true>(a, sr, n_split, sth);
-    if (K <= 64) return sh == 2 ? launch_cfg<2, 8, true, 0, true>(a, sr, n_split, sth)
-                      : sh == 1 ? launch_cfg<4, 4, true, 0, true>(a, sr, n_split, sth)
-                                : launch_cfg<8, 2, true, 0, true>(a, sr, n_split, sth);
-    if (K <= 128) return sh == 2 ? launch_cfg<4, 8, true, 0, true>(a, sr, n_split, sth)
-                       : sh == 1 ? launch_cfg<8, 4, true, 0, true>(a, sr, n_split, sth)
-                                 : launch_cfg<16, 2, true, 0, true>(a, sr, n_split, sth);
-    if (K <= 256) return sh == 2 ? launch_cfg<8, 8, true, 0, true>(a, sr, n_split, sth)
-                       : sh == 1 ? launch_cfg<16, 4, true, 0, true>(a, sr, n_split, sth)
-                                 : launch_cfg<32, 2, true, 0, true>(a, sr, n_split, sth);
-    return sh == 2 ? launch_cfg<8, 8, true, 0, true>(a, sr, n_split, sth)
-         : sh == 1 ? launch_cfg<16, 4, true, 0, true>(a, sr, n_split, sth)
-                   : launch_cfg<32, 2, true, 0, true>(a, sr, n_split, sth);
+    if (MODE == 2 && K > 512) return launch_cfg<32, 8, true, MODE, true>(a, sr, n_split, sth);
+    if (MODE == 2 && K > 256) return launch_cfg<32, 4, true, MODE, true>(a, sr, n_split, sth);
+    if (K <= 16) return launch_cfg<2, 2, true, MODE, true>(a, sr, n_split, sth);
+    if (K <= 32) return sh ? launch_cfg<2, 4, true, MODE, true>(a, sr, n_split, sth)
+                           : launch_cfg<4, 2, true, MODE, true>(a, sr, n_split, sth);
+    if (K <= 64) return sh == 2 ? launch_cfg<2, 8, true, MODE, true>(a, sr, n_split, sth)
+                      : sh == 1 ? launch_cfg<4, 4, true, MODE, true>(a, sr, n_split, sth)
+                                : launch_cfg<8, 2, true, MODE, true>(a, sr, n_split, sth);
+    if (K <= 128) return sh == 2 ? launch_cfg<4, 8, true, MODE, true>(a, sr, n_split, sth)
+                       : sh == 1 ? launch_cfg<8, 4, true, MODE, true>(a, sr, n_split, sth)
+                                 : launch_cfg<16, 2, true, MODE, true>(a, sr, n_split, sth);
+    if (K <= 256) return sh == 2 ? launch_cfg<8, 8, true, MODE, true>(a, sr, n_split, sth)
+                       : sh == 1 ? launch_cfg<16, 4, true, MODE, true>(a, sr, n_split, sth)
+                                 : launch_cfg<32, 2, true, MODE, true>(a, sr, n_split, sth);
+    return sh == 2 ? launch_cfg<8, 8, true, MODE, true>(a, sr, n_split, sth)
+         : sh == 1 ? launch_cfg<16, 4, true, MODE, true>(a, sr, n_split, sth)
+                   : launch_cfg<32, 2, true, MODE, true>(a, sr, n_split, sth);
   }
   const bool vec = (K % 4 == 0) && (a.ldb % 4 == 0) && (a.ldc % 4 == 0) && aligned16(a.B) &&
                    aligned16(a.C) && (a.partial == nullptr || aligned16(a.partial));
@@ -749,7 +749,8 @@ extern "C" int gc_spmm_f32(const int32_t *row_ptr, const int32_t *col_idx, const
 extern "C" int gc_gat_sddmm_aggregate_f32(const int32_t *row_ptr, const int32_t *col_idx,
                                           const float *a_src, const float *a_dst, float slope,
                                           const float *B, int64_t ldb, const float *B_self,
-                                          int64_t ld_self, int64_t n_rows, int64_t K,
+                                          int64_t ld_self, const float *sigma, int64_t n_rows,
+                                          int64_t K,
                                           float *C, int64_t ldc, uint32_t flags, int algo,
                                           const int32_t *items, int64_t n_items,
                                           const int32_t *split_rows, int64_t n_split_rows,
@@ -757,8 +758,8 @@ extern "C" int gc_gat_sddmm_aggregate_f32(const int32_t *row_ptr, const int32_t 
   GC_REQUIRE(n_rows >= 0 && K >= 1, GC_ERR_SHAPE, "gc_gat_sddmm_aggregate_f32: bad size");
   GC_REQUIRE(ldb >= K && ldc >= K, GC_ERR_SHAPE,
              "gc_gat_sddmm_aggregate_f32: leading dimension < K");
-  GC_REQUIRE((flags & ~(GC_RELU | GC_HUB_TAGGED | GC_SPMM_SHRINK_MASK)) == 0, GC_ERR_VALUE,
-             "gc_gat_sddmm_aggregate_f32: unknown flags 0x%x", flags);
+  GC_REQUIRE((flags & ~(GC_RELU | GC_HUB_TAGGED | GC_SPMM_SHRINK_MASK | GC_SPMM_B_F16)) == 0,
+             GC_ERR_VALUE, "gc_gat_sddmm_aggregate_f32: unknown flags 0x%x", flags);
   GC_REQUIRE(slope > 0.0f && slope < 1.0f, GC_ERR_VALUE,
              "gc_gat_sddmm_aggregate_f32: leaky_slope must lie in (0, 1)");
   if (n_rows == 0) return GC_OK;
@@ -775,6 +776,7 @@ extern "C" int gc_gat_sddmm_aggregate_f32(const int32_t *row_ptr, const int32_t 
   a.ldb = ldb;
   a.B_self = B_self ? B_self : B;
   a.ld_self = B_self ? ld_self : ldb;
+  a.d_col = sigma;  // GC_SPMM_B_F16: per-row scales of the fp16 rows
   a.K = K;
   a.C = C;
   a.ldc = ldc;
@@ -789,7 +791,8 @@ extern "C" int gc_gat_sddmm_aggregate_f32(const int32_t *row_ptr, const int32_t 
 
 extern "C" int gc_gat_aggregate_f32(const int32_t *row_ptr, const int32_t *col_idx,
                                     const float *s, const float *t, float slope, const float *B,
-                                    int64_t ldb, int64_t n_rows, int64_t n_cols, int64_t K,
+                                    int64_t ldb, const float *sigma, int64_t n_rows, int64_t n_cols,
+                                    int64_t K,
                                     float *C, int64_t ldc, uint32_t flags, int algo,
                                     const int32_t *items, int64_t n_items,
                                     const int32_t *split_rows, int64_t n_split_rows,
@@ -797,8 +800,8 @@ extern "C" int gc_gat_aggregate_f32(const int32_t *row_ptr, const int32_t *col_i
   GC_REQUIRE(n_rows >= 0 && n_cols >= 0 && K >= 0, GC_ERR_SHAPE,
              "gc_gat_aggregate_f32: negative size");
   GC_REQUIRE(ldb >= K && ldc >= K, GC_ERR_SHAPE, "gc_gat_aggregate_f32: leading dimension < K");
-  GC_REQUIRE((flags & ~(GC_RELU | GC_HUB_TAGGED | GC_SPMM_SHRINK_MASK)) == 0, GC_ERR_VALUE,
-             "gc_gat_aggregate_f32: unknown flags 0x%x", flags);
+  GC_REQUIRE((flags & ~(GC_RELU | GC_HUB_TAGGED | GC_SPMM_SHRINK_MASK | GC_SPMM_B_F16)) == 0,
+             GC_ERR_VALUE, "gc_gat_aggregate_f32: unknown flags 0x%x", flags);
   GC_REQUIRE(slope > 0.0f && slope < 1.0f, GC_ERR_VALUE,
              "gc_gat_aggregate_f32: leaky_slope must lie in (0, 1)");
   if (n_rows == 0 || K == 0) return GC_OK;
@@ -819,6 +822,7 @@ extern "C" int gc_gat_aggregate_f32(const int32_t *row_ptr, const int32_t *col_i
   a.s = s;
   a.t = t;
   a.slope = slope;
+  a.d_col = sigma;  // GC_SPMM_B_F16: per-row scales of the fp16 rows
   return dispatch<1>(a, n_rows, algo, items, n_items, split_rows, n_split_rows, workspace,
                         ws_bytes, stream, "gc_gat_aggregate_f32");
 }

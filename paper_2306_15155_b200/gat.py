@@ -47,6 +47,7 @@ from .sparse import (
     call_spmm_hook,
     gat_aggregate,
     gemm,
+    pack_rows_f16,
     relu_,
     spmm,
 )
@@ -225,15 +226,19 @@ def gat_layer_reuse(a_tilde: CsrMatrix, h, spec: GatLayerSpec, *, spmm_fn=None):
         out = torch.cat(outs, 1).contiguous()
         return op.wrap(relu_(out) if relu else out)
     out = torch.empty(a_tilde.n_rows, k2 * H, dtype=torch.float32, device=hw.device)
+    half = _half(hw[:, :k2])
     if spec.attention is AttentionForm.SDDMM:
         if a_tilde.n_rows == a_tilde.n_cols:
             # fused: the gathered HW_j row gives its score and its aggregated term
+            # (TF32 class: gathered as fp16 rows, the source rows stay fp32)
             a_src, a_dst = spec.attn_src.to(hw.device), spec.attn_dst.to(hw.device)
             done = all(gat_sddmm_aggregate(a_tilde, a_src[i * k2:(i + 1) * k2],
                                            a_dst[i * k2:(i + 1) * k2], spec.leaky_slope,
-                                           hw[:, i * k2:(i + 1) * k2], relu=relu,
-                                           out=out[:, i * k2:(i + 1) * k2]) is not None
-                       for i in range(H))
+                                           pack_rows_f16(hw[:, i * k2:(i + 1) * k2]) if half
+                                           else hw[:, i * k2:(i + 1) * k2], relu=relu,
+                                           out=out[:, i * k2:(i + 1) * k2],
+                                           b_self=hw[:, i * k2:(i + 1) * k2] if half else None)
+                       is not None for i in range(H))
             if done:
                 return op.wrap(out)
         att = atten_calc(a_tilde, hw, spec)
@@ -244,8 +249,9 @@ def gat_layer_reuse(a_tilde: CsrMatrix, h, spec: GatLayerSpec, *, spmm_fn=None):
         raise ShapeError("attention expects a square adjacency")
     s, t = _projections(hw, spec, spec.attn_src.to(hw.device), spec.attn_dst.to(hw.device), k2, k2)
     for i in range(H):
-        gat_aggregate(a_tilde, s[i], t[i], spec.leaky_slope, hw[:, i * k2:(i + 1) * k2], relu=relu,
-                      out=out[:, i * k2:(i + 1) * k2])
+        b = hw[:, i * k2:(i + 1) * k2]
+        gat_aggregate(a_tilde, s[i], t[i], spec.leaky_slope, pack_rows_f16(b) if half else b,
+                      relu=relu, out=out[:, i * k2:(i + 1) * k2])
     return op.wrap(out)
 
 
@@ -272,10 +278,19 @@ def gat_layer_recompute(a_tilde: CsrMatrix, h, spec: GatLayerSpec, *, spmm_fn=No
         raise ShapeError("attention expects a square adjacency")
     u, v = _folded_attention_vectors(spec)
     s, t = _projections(op.t, spec, u, v, k1, 0)
+    x = pack_rows_f16(op.t) if _half(op.t) else op.t  # one pack, shared by the heads
     for i in range(H):
-        ah = gat_aggregate(a_tilde, s[i], t[i], spec.leaky_slope, op.t)
+        ah = gat_aggregate(a_tilde, s[i], t[i], spec.leaky_slope, x)
         gemm(ah, spec.weights[:, i * k2:(i + 1) * k2], relu=relu, out=out[:, i * k2:(i + 1) * k2])
     return op.wrap(out)
+
+
+def _half(x: torch.Tensor) -> bool:
+    """TF32 class: the aggregation gathers fp16 rows of its operand (as the
+    GCN layers do, gcn.half_gather)."""
+    from .gcn import half_gather
+
+    return half_gather(x)
 
 
 def gat_layer(a_tilde: CsrMatrix, h, spec: GatLayerSpec, *, spmm_fn=None):

@@ -555,8 +555,10 @@ SPMM_SHRINK = os.environ.get("GNNC_SPMM_SHRINK", "auto")  # lane-group variant: 
 
 
 def _shrink_candidates(K: int, mode: str = "spmm") -> list[int]:
-    if mode == "gatsd" and K > 256:
+    if mode in ("gatsd", "gatsdh") and K > 256:
         return [0]  # one wide lane-group shape only (whole row per pass)
+    if mode.endswith("h"):  # fp16 rows: lane groups of 16-byte chunks
+        return [0] if K <= 16 else ([0, 1] if K <= 32 else [0, 1, 2])
     return [0] if K <= 8 else ([0, 1] if K <= 16 else [0, 1, 2])
 
 
@@ -572,7 +574,7 @@ def _variant(a: CsrMatrix, K: int, mode: str, probe) -> tuple[bool, int]:
     if a.nnz < PLAN_MIN_NNZ:
         return False, 0
     hints = [False, True] if hint_mode == "auto" else [hint_mode == "1"]
-    if mode == "spmmh":
+    if mode.endswith("h"):
         hints = [False]  # no L1-tag variant with fp16 operand rows
     shrinks = _shrink_candidates(K, mode) if shrink_mode == "auto" else [int(shrink_mode)]
     if len(hints) * len(shrinks) == 1:
@@ -613,8 +615,13 @@ def gat_sddmm_aggregate(a: CsrMatrix, a_src: torch.Tensor, a_dst: torch.Tensor, 
     square pattern.  Returns None when the operand shape is outside the
     kernel's range (K > 1024, unaligned)."""
     dev = a.device
-    bt = b
-    K = bt.shape[1]
+    half = isinstance(b, HalfRows)
+    bt = b.xh if half else b
+    K = b.K if half else bt.shape[1]
+    if half and b_self is None:
+        if a.n_rows != a.n_cols:
+            raise ShapeError("gat_sddmm_aggregate: fp16 rows need fp32 source rows b_self")
+        raise ShapeError("gat_sddmm_aggregate: fp16 rows need the fp32 rows as b_self")
     if bt.shape[0] != a.n_cols:
         raise ShapeError("gat_sddmm_aggregate: one B row per column of the pattern required")
     if b_self is None and a.n_rows != a.n_cols:
@@ -622,7 +629,7 @@ def gat_sddmm_aggregate(a: CsrMatrix, a_src: torch.Tensor, a_dst: torch.Tensor, 
     if b_self is not None and (tuple(b_self.shape) != (a.n_rows, K) or b_self.stride(1) != 1):
         raise ShapeError("gat_sddmm_aggregate: b_self must be a row-major n_rows x K tensor")
     if (K > 1024 or K % 4 or _ld(bt) % 4 or bt.data_ptr() % 16 or a_src.data_ptr() % 16
-            or a_dst.data_ptr() % 16
+            or a_dst.data_ptr() % 16 or (half and (K % 8 or _ld(bt) % 8))
             or (b_self is not None and (_ld(b_self) % 4 or b_self.data_ptr() % 16))):
         return None
     _require_cuda(a.col_idx, bt, a_src, a_dst)
@@ -632,12 +639,13 @@ def gat_sddmm_aggregate(a: CsrMatrix, a_src: torch.Tensor, a_dst: torch.Tensor, 
         return None
     code, items, n_items, split, n_split, ws = _plan_args(a, K, algo, dev, gat=True)
     lib = nat.load()
-    flags = nat.GC_RELU if relu else 0
+    flags = (nat.GC_RELU if relu else 0) | (nat.GC_SPMM_B_F16 if half else 0)
 
     def launch(cols, extra):
         return lib.gc_gat_sddmm_aggregate_f32(
             a.row_ptr.data_ptr(), cols.data_ptr(), a_src.data_ptr(), a_dst.data_ptr(), float(slope),
-            bt.data_ptr(), _ld(bt), _ptr(b_self), 0 if b_self is None else _ld(b_self), a.n_rows, K,
+            bt.data_ptr(), _ld(bt), _ptr(b_self), 0 if b_self is None else _ld(b_self),
+            b.sigma.data_ptr() if half else None, a.n_rows, K,
             out.data_ptr(), _ld(out), flags | extra, code,
             _ptr(items), n_items, _ptr(split), n_split, _ptr(ws), 0 if ws is None else ws.numel() * 4,
             _stream(dev))
@@ -645,7 +653,7 @@ def gat_sddmm_aggregate(a: CsrMatrix, a_src: torch.Tensor, a_dst: torch.Tensor, 
     def probe(cols, extra):
         nat.check(launch(cols, extra), "gat_sddmm_aggregate")
 
-    hints, shrink = _variant(a, K, "gatsd", probe)
+    hints, shrink = _variant(a, K, "gatsdh" if half else "gatsd", probe)
     cols = a.hub_tagged_cols(K) if hints else a.col_idx
     extra = (nat.GC_HUB_TAGGED if hints else 0) | nat.GC_SPMM_SHRINK(shrink)
     rc = _timed_call("spmm", dev, lambda: launch(cols, extra))
@@ -750,13 +758,14 @@ def gat_aggregate(a: CsrMatrix, s: torch.Tensor, t: torch.Tensor, slope: float, 
     the softmax computed online inside the SpMM (α never written) —
     gat.py:72-95 followed by spmm(α, B) (gat.py:127-143) in one kernel."""
     dev = a.device
-    op = _Operand(b, dev)
-    bt = op.t
+    half = isinstance(b, HalfRows)
+    op = None if half else _Operand(b, dev)
+    bt = b.xh if half else op.t
     if a.n_cols != bt.shape[0]:
         raise ShapeError(f"gat_aggregate: a is {a.n_rows}x{a.n_cols}, b has {bt.shape[0]} rows")
     if tuple(s.shape) != (a.n_rows,) or tuple(t.shape) != (a.n_cols,):
         raise ShapeError("gat_aggregate: s/t must have one entry per row/column")
-    K = bt.shape[1]
+    K = b.K if half else bt.shape[1]
     _require_cuda(a.col_idx, bt, s, t)
     if out is None:
         out = torch.empty(a.n_rows, K, dtype=torch.float32, device=dev)
@@ -764,24 +773,25 @@ def gat_aggregate(a: CsrMatrix, s: torch.Tensor, t: torch.Tensor, slope: float, 
         raise ShapeError(f"gat_aggregate: out must be a row-major {a.n_rows}x{K} tensor")
     code, items, n_items, split, n_split, ws = _plan_args(a, K, algo, dev, gat=True)
     lib = nat.load()
-    flags = nat.GC_RELU if relu else 0
+    flags = (nat.GC_RELU if relu else 0) | (nat.GC_SPMM_B_F16 if half else 0)
 
     def launch(cols, extra, dst=out):
         return lib.gc_gat_aggregate_f32(
             a.row_ptr.data_ptr(), cols.data_ptr(), s.data_ptr(), t.data_ptr(), float(slope),
-            bt.data_ptr(), _ld(bt), a.n_rows, a.n_cols, K, dst.data_ptr(), _ld(dst), flags | extra,
+            bt.data_ptr(), _ld(bt), b.sigma.data_ptr() if half else None, a.n_rows, a.n_cols, K,
+            dst.data_ptr(), _ld(dst), flags | extra,
             code, _ptr(items), n_items, _ptr(split), n_split, _ptr(ws),
             0 if ws is None else ws.numel() * 4, _stream(dev))
 
     def probe(cols, extra):
         nat.check(launch(cols, extra), "gat_aggregate")  # writes `out`; the real launch follows
 
-    hints, shrink = _variant(a, K, "gat", probe)
+    hints, shrink = _variant(a, K, "gath" if half else "gat", probe)
     cols = a.hub_tagged_cols(K) if hints else a.col_idx
     extra = (nat.GC_HUB_TAGGED if hints else 0) | nat.GC_SPMM_SHRINK(shrink)
     rc = _timed_call("spmm", dev, lambda: launch(cols, extra))
     nat.check(rc, "gat_aggregate")
-    return op.wrap(out)
+    return out if half else op.wrap(out)
 
 
 def device_hook(fn):

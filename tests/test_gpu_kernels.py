@@ -520,6 +520,37 @@ def test_fused_gat_aggregate_matches_oracle(oracle, plgraph, K, algo, monkeypatc
         assert oracle.rel_err(out, ref) < 2e-5, (K, algo, relu)
 
 
+@pytest.mark.parametrize("K", [8, 32, 256, 512])
+@pytest.mark.parametrize("algo", ["row", "split"])
+def test_fused_gat_fp16_rows_match_oracle_on_dequantised(oracle, plgraph, K, algo, monkeypatch):
+    """GC_SPMM_B_F16 in both GAT modes: the reassociated-score aggregation
+    and the SDDMM-score aggregation over fp16 rows equal the oracle run on the
+    dequantised rows sigma_j * xh_j (the score's source rows stay fp32)."""
+    if algo == "split":
+        monkeypatch.setattr(sparse, "SPLIT_CHUNK", 16)
+    rng = np.random.default_rng(K + 300)
+    n = plgraph.n_rows
+    dev = lambda x: torch.from_numpy(x).to(DEV)  # noqa: E731
+    hw = f32(rng.uniform(-1, 1, (n, K)) * 2.0 ** rng.integers(-3, 3, (n, 1)))
+    hr = sparse.pack_rows_f16(dev(hw))
+    deq = hr.xh[:, :K].double().cpu().numpy() * hr.sigma.double().cpu().numpy()[:, None]
+    oa = to_oracle(oracle, plgraph)
+    s, t = f32(rng.standard_normal(n) * 3), f32(rng.standard_normal(n) * 3)
+    out = sparse.gat_aggregate(plgraph, dev(s), dev(t), 0.2, hr, relu=True, algo=algo)
+    ref = np.maximum(oracle.spmm(oa.with_values(oracle.edge_softmax(oa, s, t, 0.2)), deq), 0)
+    assert oracle.rel_err(out.cpu().numpy(), ref) < 2e-5
+    a_s, a_d = f32(rng.uniform(-0.5, 0.5, K)), f32(rng.uniform(-0.5, 0.5, K))
+    out = sparse.gat_sddmm_aggregate(plgraph, dev(a_s), dev(a_d), 0.2, hr, b_self=dev(hw),
+                                     algo=algo)
+    assert out is not None
+    ss = hw.astype(np.float64) @ a_s.astype(np.float64)
+    tt = deq @ a_d.astype(np.float64)
+    ref = oracle.spmm(oa.with_values(oracle.edge_softmax(oa, ss, tt, 0.2)), deq)
+    assert oracle.rel_err(out.cpu().numpy(), ref) < 2e-5
+    with pytest.raises(gc.ShapeError):
+        sparse.gat_sddmm_aggregate(plgraph, dev(a_s), dev(a_d), 0.2, hr)
+
+
 def test_fused_gat_aggregate_empty_rows(oracle):
     rng = np.random.default_rng(7)
     a = rand_csr(rng, 60, 60, 0.1, unit=True, empty_rows=(0, 13, 59))
