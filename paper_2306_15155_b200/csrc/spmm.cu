@@ -33,6 +33,18 @@ constexpr int kThreads = 256;
 #ifndef GNNC_SPMM_MINB
 #define GNNC_SPMM_MINB 1
 #endif
+// the same for the fp16-row (GC_SPMM_B_F16) instances (SDDMM-score GAT
+// rows hold the score operands too: half as many), and their edges unrolled
+// per step (16-byte chunks in flight per lane = U x NV/2).  Measured on
+// Reddit / products K = 256 (profiles/data/ab_bh_unroll_r02.json): U = 4 at
+// 4 CTAs/SM 1.65 / 7.68 ms per layer, U = 8 at 1 CTA/SM (96 registers)
+// 1.99 / 8.79 ms — the gathers need warps in flight more than chunks per lane.
+#ifndef GNNC_SPMM_BH_MINB
+#define GNNC_SPMM_BH_MINB 4
+#endif
+#ifndef GNNC_SPMM_BH_U
+#define GNNC_SPMM_BH_U 4
+#endif
 
 struct SpmmArgs {
   const int32_t *row_ptr;
@@ -172,7 +184,10 @@ __device__ __forceinline__ void store_row(const SpmmArgs &a, int row, int slot, 
 // half-width gather operand), half the gathered bytes per edge.
 template <int LPR, int NV, bool VEC, bool HAS_VAL, bool HAS_DCOL, int MODE, bool HINT,
           bool BH = false>
-__global__ void __launch_bounds__(kThreads, GNNC_SPMM_MINB) spmm_kernel(const SpmmArgs a) {
+__global__ void __launch_bounds__(kThreads, BH ? (MODE == 2 ? (GNNC_SPMM_BH_MINB + 1) / 2
+                                                         : GNNC_SPMM_BH_MINB)
+                                              : GNNC_SPMM_MINB)
+    spmm_kernel(const SpmmArgs a) {
   static_assert(!BH || (!HINT && VEC && NV % 2 == 0),
                 "fp16 operand rows: no L1 tags, 16-byte chunks of two slots");
   // GAT modes with fp16 rows: the row scale sigma_j (a.d_col) is gathered
@@ -187,8 +202,10 @@ __global__ void __launch_bounds__(kThreads, GNNC_SPMM_MINB) spmm_kernel(const Sp
   // (never more than LPR: the edge batch is shuffled within the lane group)
   // (BH: one 16-byte load covers two slots, so count loads, not slots)
   constexpr int NVL = BH ? NV / 2 : NV;
-  constexpr int U0 = NVL >= 8 ? 1 : NVL >= 4 ? 2 : NVL >= 2 ? 4 : 8;
+  constexpr int U0 = BH ? (GNNC_SPMM_BH_U / NVL > 0 ? GNNC_SPMM_BH_U / NVL : 1)
+                        : NVL >= 8 ? 1 : NVL >= 4 ? 2 : NVL >= 2 ? 4 : 8;
   constexpr int U = U0 < LPR ? U0 : LPR;
+  static_assert(LPR % U == 0, "an edge batch of LPR lanes is consumed U edges at a time");
   const int g = threadIdx.x / LPR;
   const int gl = threadIdx.x % LPR;
   const int64_t item = (int64_t)blockIdx.x * GPB + g;
@@ -305,10 +322,10 @@ __global__ void __launch_bounds__(kThreads, GNNC_SPMM_MINB) spmm_kernel(const Sp
     const int cntw = min(LPR, wmax - base);
 #pragma unroll 1
     for (int e0 = 0; e0 < cntw; e0 += U) {
-      T bv[U][NV];
       if constexpr (BH) {
         // fp16 rows: U edges x NV/2 raw 16-byte chunks in flight (4
-        // registers each), widened to fp32 once all have been issued
+        // registers each); each chunk is widened to fp32 where it is used
+        // (never all at once: that would double the live registers)
         constexpr int NVH = NV / 2;
         uint4 rw[U][NVH];
 #pragma unroll
@@ -320,14 +337,70 @@ __global__ void __launch_bounds__(kThreads, GNNC_SPMM_MINB) spmm_kernel(const Sp
           for (int c = 0; c < NVH; ++c)
             if (ok && colok[2 * c]) rw[u][c] = ldg_u4(brow_c + (coff[2 * c] - coff[0]) * ESZ);
         }
+        if constexpr (SD) {
+          float eu[U], su[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u)
+          for (int u = 0; u < U; ++u) {
+            su[u] = SIG ? __shfl_sync(0xffffffffu, gsig, e0 + u, LPR) : 1.0f;
+            float part = 0.0f;
 #pragma unroll
-          for (int c = 0; c < NVH; ++c)
-            if ((e0 + u) < cnt && colok[2 * c]) widen_h8(rw[u][c], bv[u][2 * c], bv[u][2 * c + 1]);
+            for (int c = 0; c < NVH; ++c) {
+              if ((e0 + u) < cnt && colok[2 * c]) {
+                float4 lo4, hi4;
+                widen_h8(rw[u][c], lo4, hi4);
+                part += dot_of(lo4, adst[2 * c]) + dot_of(hi4, adst[2 * c + 1]);
+              }
+            }
+            part = group_sum<LPR>(part) * su[u];
+            eu[u] = (e0 + u) < cnt ? leaky(si + part, a.slope) : -INFINITY;
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if ((e0 + u) < cnt) {
+              if (eu[u] > m) {
+                const float sc = __expf(m - eu[u]);
+#pragma unroll
+                for (int vv = 0; vv < NV; ++vv) scale_into(acc[vv], sc);
+                zl *= sc;
+                m = eu[u];
+              }
+              const float w = __expf(eu[u] - m);
+              zl += w;
+              const float wa = w * su[u];
+#pragma unroll
+              for (int c = 0; c < NVH; ++c) {
+                if (colok[2 * c]) {
+                  float4 lo4, hi4;
+                  widen_h8(rw[u][c], lo4, hi4);
+                  fma_into(acc[2 * c], wa, lo4);
+                  fma_into(acc[2 * c + 1], wa, hi4);
+                }
+              }
+            }
+          }
+        } else {
+          const float w = mine ? v * dj * (SIG ? gsig : 1.0f) : 0.0f;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const float we = __shfl_sync(0xffffffffu, w, e0 + u, LPR);
+            if ((e0 + u) < cnt) {
+#pragma unroll
+              for (int c = 0; c < NVH; ++c) {
+                if (colok[2 * c]) {
+                  float4 lo4, hi4;
+                  widen_h8(rw[u][c], lo4, hi4);
+                  fma_into(acc[2 * c], we, lo4);
+                  fma_into(acc[2 * c + 1], we, hi4);
+                }
+              }
+            }
+          }
+        }
+        continue;
       }
+      T bv[U][NV];
 #pragma unroll
-      for (int u = 0; u < U && !BH; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int je = __shfl_sync(0xffffffffu, j, e0 + u, LPR);
         const bool ok = (e0 + u) < cnt;
         const float *brow = reinterpret_cast<const float *>(

@@ -25,11 +25,11 @@ METRICS = {
     "occ": ("sm__warps_active.avg.pct_of_peak_sustained_active", 1.0),
     "sm_thru": ("sm__throughput.avg.pct_of_peak_sustained_elapsed", 1.0),
     "issue": ("sm__inst_issued.avg.pct_of_peak_sustained_active", 1.0),
-    "tensor": ("sm__pipe_tensor_op_gmma_cycles_active.avg.pct_of_peak_sustained_active", 1.0),
+    "regs": ("launch__registers_per_thread", 1.0),
     "utc": ("sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active", 1.0),
 }
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3,
-              "msecond": 1e6, "second": 1e9}
+              "msecond": 1e6, "second": 1e9, "ns": 1, "us": 1e3, "ms": 1e6, "s": 1e9}
 
 
 def rows_of(rep: Path) -> list[dict]:
@@ -59,18 +59,18 @@ def main():
     ap.add_argument("--peak-gbs", type=float, default=6650.0)
     args = ap.parse_args()
     print("| report | id | kernel | µs | DRAM rd+wr GB | DRAM GB/s (frac) | L2 hit % | L2 thru % "
-          "| warps active % | issue % | tensor % |")
-    print("|---|---|---|---|---|---|---|---|---|---|---|")
+          "| warps active % | regs | issue % | tensor % |")
+    print("|---|---|---|---|---|---|---|---|---|---|---|---|")
     for rep in args.reports:
         for r in rows_of(Path(rep)):
             d = (r.get("dram_rd", 0) + r.get("dram_wr", 0))
             us = r.get("dur_us", 0)
             gbs = d / (us * 1e-6) / 1e9 if us else 0
-            ten = r.get("utc", r.get("tensor", float("nan")))
+            ten = r.get("utc", float("nan"))
             print(f"| {Path(rep).stem} | {r['id']} | `{r['kernel']}` | {us:.1f} | {d / 1e9:.3f} | "
                   f"{gbs:.0f} ({gbs / args.peak_gbs:.2f}) | {r.get('l2_hit', float('nan')):.1f} | "
                   f"{r.get('l2_thru', float('nan')):.1f} | {r.get('occ', float('nan')):.1f} | "
-                  f"{r.get('issue', float('nan')):.1f} | {ten:.1f} |")
+                  f"{r.get('regs', float('nan')):.0f} | {r.get('issue', float('nan')):.1f} | {ten:.1f} |")
 
 
 if __name__ == "__main__":
