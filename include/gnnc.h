@@ -281,6 +281,24 @@ GNNC_API int64_t gc_hub_terms_rows(int64_t K);
 GNNC_API int gc_hub_pack(const float *X, int64_t ldx, int64_t K, const int32_t *hub_cols,
                 int64_t T, const float *d_col, int32_t fmt, void *Bt, float *scale_ws,
                 void *stream);
+/* The TF32 GEMM with the TF32 class's gather operand as output: per row of
+ * C = diag(row_scale) A W, Xh[row,:] = fp16_rn(C[row,:] * 2^-e) (max in
+ * [2^14, 2^15); ldh = N rounded up to 8, pad zeroed) and sigma[row] = 2^e —
+ * what gc_pack_rows_f16 makes of C, without writing C.  N <= 256 (the whole
+ * row in one TMEM tile, two passes over it in the epilogue); workspace as
+ * gc_gemm_f32. */
+GNNC_API int gc_gemm_f16rows_f32(const float *A, int64_t lda, const float *W, int64_t ldw,
+                                 int64_t M, int64_t K, int64_t N, const float *row_scale,
+                                 void *Xh, int64_t ldh, float *sigma, void *workspace,
+                                 size_t ws_bytes, void *stream);
+
+/* gc_hub_pack from the fp16 gather operand (gc_pack_rows_f16): x_j =
+ * sigma_j * Xh[j,:] (ldh in elements); one-term formats GC_HUB_F16 /
+ * GC_HUB_F16_MN only (the TF32 class).  Lets the dense part and the tail of
+ * the split read one operand. */
+GNNC_API int gc_hub_pack_f16rows(const void *Xh, int64_t ldh, const float *sigma, int64_t K,
+                                 const int32_t *hub_cols, int64_t T, const float *d_col,
+                                 int32_t fmt, void *Bt, float *scale_ws, void *stream);
 GNNC_API int gc_hub_gemm(const void *A_hub, int64_t lda, int64_t n_rows, int64_t T,
                 const void *Bt, int64_t K, int32_t fmt, const float *scale_ws, float *C,
                 int64_t ldc, const float *d_row, uint32_t flags, void *stream);

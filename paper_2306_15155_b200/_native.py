@@ -67,6 +67,8 @@ _SIGNATURES = {
     "gc_sddmm_f32": (ctypes.c_int, [_P, _P, _P, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _P]),
     "gc_sddmm_norm_f32": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I64, _P, _P]),
     "gc_gemm_workspace_bytes": (_SZ, [_I64, _I64]),
+    "gc_gemm_f16rows_f32": (ctypes.c_int, [_P, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _P,
+                                           _P, _SZ, _P]),
     "gc_gemm_f32": (ctypes.c_int, [_P, _I64, _P, _I64, _I64, _I64, _I64, _P, _I64, _P, _U32, _P,
                                    _SZ, _P]),
     "gc_scale_rows_f32": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _P, _I64, _U32, _P]),
@@ -85,6 +87,7 @@ _SIGNATURES = {
     "gc_partition_rows": (ctypes.c_int, [_P, _I64, _I32, _P]),
     "gc_hub_terms_rows": (_I64, [_I64]),
     "gc_hub_pack": (ctypes.c_int, [_P, _I64, _I64, _P, _I64, _P, _I32, _P, _P, _P]),
+    "gc_hub_pack_f16rows": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _I64, _P, _I32, _P, _P, _P]),
     "gc_hub_gemm": (ctypes.c_int, [_P, _I64, _I64, _I64, _P, _I64, _I32, _P, _P, _I64, _P, _U32,
                                    _P]),
     "gc_hub_stair_supported": (ctypes.c_int, [_I64]),

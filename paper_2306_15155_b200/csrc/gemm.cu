@@ -237,6 +237,12 @@ struct GemmEpi {
   int64_t M, N;
   uint32_t flags;
   const float *scale;  // optional device scalar multiplied into every row (f16x2 unscale)
+  // fp16-row output (gc_gemm_f16rows_f32, the TF32 class's gather operand):
+  // Ch[row] = fp16_rn(out_row * 2^-e_row), sigma[row] = 2^e_row, with the
+  // row max in [2^14, 2^15); needs the whole row in one N tile (BN >= N)
+  __half *Ch;
+  int64_t ldh;
+  float *sigma;
 };
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
@@ -435,6 +441,49 @@ __device__ __forceinline__ void gemm_tc_body(const CUtensorMap &map_a, const CUt
       if (ep.scale) rs *= __ldg(ep.scale);
       float *crow = ep.C + (int64_t)row * ep.ldc;
       const uint32_t taddr = tmem_base + (uint32_t)(acc * BN) + ((uint32_t)(q * 32) << 16);
+      if (ep.Ch) {
+        // fp16 rows (TF32 class): pass 1 finds the row max in TMEM, pass 2
+        // converts with the exact power-of-two scale; the whole row is this
+        // tile (n0 == 0, BN >= N)
+        float mx = 0.0f;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 16) {
+          if (c >= ep.N) break;  // warp-uniform
+          float v[16];
+          tmem_ld16(taddr + (uint32_t)c, v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (c + i < ep.N) mx = fmaxf(mx, fabsf(v[i] * rs));
+        }
+        const int E = mx > 0.0f ? ((int)((__float_as_uint(mx) >> 23) & 0xff) - 127) : 0;
+        const int e = mx > 0.0f && isfinite(mx) ? max(min(E - 14, 110), -110) : 0;
+        const float down = __uint_as_float((uint32_t)(127 - e) << 23) * rs;
+        __half *hrow = ep.Ch + (int64_t)row * ep.ldh;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 16) {
+          if (c >= ep.ldh) break;  // warp-uniform (ldh: N rounded up to 8)
+          float v[16];
+          tmem_ld16(taddr + (uint32_t)c, v);
+          if (!row_ok) continue;
+          __half2 hv[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            hv[i] = __floats2half2_rn(c + 2 * i < ep.N ? v[2 * i] * down : 0.0f,
+                                      c + 2 * i + 1 < ep.N ? v[2 * i + 1] * down : 0.0f);
+          if (c + 16 <= ep.ldh) {
+            uint4 *dst = reinterpret_cast<uint4 *>(hrow + c);
+            dst[0] = *reinterpret_cast<const uint4 *>(&hv[0]);
+            dst[1] = *reinterpret_cast<const uint4 *>(&hv[4]);
+          } else {  // the last 8 halves of a row whose padded width is 8 mod 16
+            *reinterpret_cast<uint4 *>(hrow + c) = *reinterpret_cast<const uint4 *>(&hv[0]);
+          }
+        }
+        if (row_ok) ep.sigma[row] = __uint_as_float((uint32_t)(127 + e) << 23);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty_bar(acc));
+        continue;
+      }
 #pragma unroll 1
       for (int c = 0; c < BN; c += 16) {
         if (n0 + c >= ep.N) break;  // warp-uniform
@@ -1622,16 +1671,25 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     hub_absmax_kernel(const float *__restrict__ X, int64_t ldx, int64_t K,
                       const int32_t *__restrict__ hub_cols, int64_t T,
-                      const float *__restrict__ d, unsigned *__restrict__ out) {
+                      const float *__restrict__ d, unsigned *__restrict__ out,
+                      const __half *__restrict__ Xh = nullptr,
+                      const float *__restrict__ sigma = nullptr) {
+  // Xh (fp16 rows, row scales sigma) replaces X when given: x = sigma_j * Xh[j]
   const int lane = threadIdx.x % 32;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int64_t n_warps = (int64_t)gridDim.x * blockDim.x / 32;
   float m = 0.0f;
   for (int64_t t = warp; t < T; t += n_warps) {
     const int64_t j = __ldg(hub_cols + t);
-    const float *row = X + j * ldx;
     float mr = 0.0f;
-    for (int64_t f = lane; f < K; f += 32) mr = fmaxf(mr, fabsf(__ldg(row + f)));
+    if (Xh) {
+      const __half *row = Xh + j * ldx;
+      for (int64_t f = lane; f < K; f += 32) mr = fmaxf(mr, fabsf(__half2float(row[f])));
+      mr *= fabsf(__ldg(sigma + j));
+    } else {
+      const float *row = X + j * ldx;
+      for (int64_t f = lane; f < K; f += 32) mr = fmaxf(mr, fabsf(__ldg(row + f)));
+    }
     m = fmaxf(m, d ? mr * fabsf(__ldg(d + j)) : mr);
   }
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -1648,7 +1706,9 @@ __global__ void __launch_bounds__(256)
     hub_pack_f16_kernel(const float *__restrict__ X, int64_t ldx, int64_t K,
                         const int32_t *__restrict__ hub_cols, int64_t T,
                         const float *__restrict__ d, int64_t kp, const unsigned *__restrict__ amax,
-                        float *__restrict__ inv_scale, __half *__restrict__ Bt) {
+                        float *__restrict__ inv_scale, __half *__restrict__ Bt,
+                        const __half *__restrict__ Xh = nullptr,
+                        const float *__restrict__ sigma = nullptr) {
   __shared__ float tile[64][33];
   const float mx = __uint_as_float(*amax);
   const int e = mx > 0.0f ? ilogbf(mx) : 0;
@@ -1661,7 +1721,7 @@ __global__ void __launch_bounds__(256)
     float x = 0.0f;
     if (t < T && f < K) {
       const int64_t j = __ldg(hub_cols + t);
-      x = __ldg(X + j * ldx + f);
+      x = Xh ? __half2float(Xh[j * ldx + f]) * __ldg(sigma + j) : __ldg(X + j * ldx + f);
       if (d) x *= __ldg(d + j);
     }
     tile[i][threadIdx.x] = x * sc;
@@ -1689,7 +1749,8 @@ __global__ void __launch_bounds__(256)
                            const int32_t *__restrict__ hub_cols, int64_t T,
                            const float *__restrict__ d, int64_t kp,
                            const unsigned *__restrict__ amax, float *__restrict__ inv_scale,
-                           __half *__restrict__ Bm, int vec) {
+                           __half *__restrict__ Bm, int vec, const __half *__restrict__ Xh = nullptr,
+                           const float *__restrict__ sigma = nullptr) {
   const float mx = __uint_as_float(*amax);
   const int e = mx > 0.0f ? ilogbf(mx) : 0;
   const float sc = ldexpf(1.0f, 13 - e);
@@ -1699,10 +1760,15 @@ __global__ void __launch_bounds__(256)
   for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; t < T; t += n_warps) {
     const int64_t j = __ldg(hub_cols + t);
     const float *row = X + j * ldx;
-    const float s = d ? __ldg(d + j) * sc : sc;
+    const __half *hrow = Xh ? Xh + j * ldx : nullptr;
+    float s = d ? __ldg(d + j) * sc : sc;
+    if (Xh) s *= __ldg(sigma + j);
     for (int64_t f = 8 * lane; f < kp; f += 256) {
       float v[8];
-      if (vec && f + 8 <= K) {
+      if (Xh) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = f + i < K ? __half2float(hrow[f + i]) : 0.0f;
+      } else if (vec && f + 8 <= K) {
         const float4 a = __ldg(reinterpret_cast<const float4 *>(row + f));
         const float4 b = __ldg(reinterpret_cast<const float4 *>(row + f + 4));
         v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
@@ -1947,6 +2013,90 @@ extern "C" int gc_hub_pack(const float *X, int64_t ldx, int64_t K, const int32_t
   else
     hub_pack_f16_kernel<2><<<grid, dim3(32, 8), 0, st>>>(X, ldx, K, hub_cols, T, d_col, kp, amax,
                                                          scale_ws + 1, static_cast<__half *>(Bt));
+  return check_launch("hub_pack_f16_kernel");
+}
+
+extern "C" int gc_gemm_f16rows_f32(const float *A, int64_t lda, const float *W, int64_t ldw,
+                                   int64_t M, int64_t K, int64_t N, const float *row_scale,
+                                   void *Xh, int64_t ldh, float *sigma, void *workspace,
+                                   size_t ws_bytes, void *stream) {
+  GC_REQUIRE(M >= 0 && K >= 1 && N >= 1 && lda >= K && ldw >= N, GC_ERR_SHAPE,
+             "gc_gemm_f16rows_f32: bad shape");
+  GC_REQUIRE(N <= 256 && ldh == (N + 7) / 8 * 8, GC_ERR_UNSUPPORTED,
+             "gc_gemm_f16rows_f32: needs N <= 256 (one N tile) and ldh = N rounded up to 8");
+  if (M == 0) return GC_OK;
+  GC_REQUIRE(A && W && Xh && sigma && aligned16(Xh), GC_ERR_VALUE,
+             "gc_gemm_f16rows_f32: null or unaligned operand");
+  GC_REQUIRE((lda % 4) == 0 && aligned16(A), GC_ERR_UNSUPPORTED,
+             "gc_gemm_f16rows_f32: needs lda %% 4 == 0 and a 16-byte aligned A");
+  GC_REQUIRE(M < (int64_t)INT32_MAX, GC_ERR_SHAPE, "gc_gemm_f16rows_f32: M exceeds TMA range");
+  const size_t need = gc_gemm_workspace_bytes(K, N);
+  GC_REQUIRE(workspace && ws_bytes >= need && aligned16(workspace), GC_ERR_WORKSPACE,
+             "gc_gemm_f16rows_f32: needs %zu workspace bytes (16-byte aligned)", need);
+  cudaStream_t st = as_stream(stream);
+  const int64_t ldt = (K + 3) / 4 * 4;
+  float *wt = static_cast<float *>(workspace);
+  {
+    dim3 grid((unsigned)((N + 31) / 32), (unsigned)((ldt + 31) / 32));
+    transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(W, ldw, K, N, wt, ldt, nullptr);
+    int rc = check_launch("transpose_kernel");
+    if (rc) return rc;
+  }
+  const int bn = N <= 16 ? 16 : N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
+  GemmEpi ep{nullptr, 0, row_scale, M, N, 0u, nullptr,
+             static_cast<__half *>(Xh), ldh, sigma};
+  CUtensorMap ma, mb, mc;
+  int rc = make_map(&ma, A, M, K, lda, BM);
+  if (rc) return rc;
+  rc = make_map(&mb, wt, N, K, ldt, bn);
+  if (rc) return rc;
+  memset(&mc, 0, sizeof(mc));
+  switch (bn) {
+    case 16: return launch_tf32<16>(ma, mb, mc, 0, ep, K, st);
+    case 32: return launch_tf32<32>(ma, mb, mc, 0, ep, K, st);
+    case 64: return launch_tf32<64>(ma, mb, mc, 0, ep, K, st);
+    case 128: return launch_tf32<128>(ma, mb, mc, 0, ep, K, st);
+    default: return launch_tf32<256>(ma, mb, mc, 0, ep, K, st);
+  }
+}
+
+extern "C" int gc_hub_pack_f16rows(const void *Xh, int64_t ldh, const float *sigma, int64_t K,
+                                   const int32_t *hub_cols, int64_t T, const float *d_col,
+                                   int32_t fmt, void *Bt, float *scale_ws, void *stream) {
+  GC_REQUIRE(K >= 1 && T >= 0 && ldh >= K, GC_ERR_SHAPE, "gc_hub_pack_f16rows: bad shape");
+  GC_REQUIRE(fmt == GC_HUB_F16 || fmt == GC_HUB_F16_MN, GC_ERR_VALUE,
+             "gc_hub_pack_f16rows: one-term fp16 formats only (format %d)", fmt);
+  if (T == 0) return GC_OK;
+  GC_REQUIRE(Xh && sigma && hub_cols && Bt && scale_ws, GC_ERR_VALUE,
+             "gc_hub_pack_f16rows: null operand");
+  GC_REQUIRE(T % 64 == 0, GC_ERR_SHAPE, "gc_hub_pack_f16rows: T must be a multiple of 64");
+  const int64_t kp = gc_hub_terms_rows(K);
+  cudaStream_t st = as_stream(stream);
+  const __half *xh = static_cast<const __half *>(Xh);
+  unsigned *amax = reinterpret_cast<unsigned *>(scale_ws);
+  if (cudaMemsetAsync(amax, 0, sizeof(unsigned), st) != cudaSuccess) {
+    set_error("gc_hub_pack_f16rows: %s", cudaGetErrorString(cudaGetLastError()));
+    return GC_ERR_CUDA;
+  }
+  const int64_t blocks = std::min<int64_t>((T + 7) / 8, (int64_t)sm_count() * 8);
+  hub_absmax_kernel<<<(unsigned)blocks, 256, 0, st>>>(nullptr, ldh, K, hub_cols, T, d_col, amax,
+                                                      xh, sigma);
+  int rc = check_launch("hub_absmax_kernel");
+  if (rc) return rc;
+  if (fmt == GC_HUB_F16_MN) {
+    GC_REQUIRE(aligned16(Bt) && kp % 8 == 0, GC_ERR_UNSUPPORTED,
+               "gc_hub_pack_f16rows: Bt alignment");
+    const int64_t nb = std::min<int64_t>((T + 7) / 8, (int64_t)sm_count() * 16);
+    hub_pack_f16_mn_kernel<<<(unsigned)nb, 256, 0, st>>>(nullptr, ldh, K, hub_cols, T, d_col, kp,
+                                                         amax, scale_ws + 1,
+                                                         static_cast<__half *>(Bt), 0, xh, sigma);
+    return check_launch("hub_pack_f16_mn_kernel");
+  }
+  dim3 grid((unsigned)((T + 63) / 64), (unsigned)((kp + 31) / 32));
+  GC_REQUIRE(grid.y < 65536, GC_ERR_SHAPE, "gc_hub_pack_f16rows: K too large");
+  hub_pack_f16_kernel<1><<<grid, dim3(32, 8), 0, st>>>(nullptr, ldh, K, hub_cols, T, d_col, kp,
+                                                       amax, scale_ws + 1,
+                                                       static_cast<__half *>(Bt), xh, sigma);
   return check_launch("hub_pack_f16_kernel");
 }
 

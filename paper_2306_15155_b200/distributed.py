@@ -45,7 +45,7 @@ import torch
 import torch.distributed as dist
 
 from . import _native as nat
-from .sparse import CsrMatrix, ShapeError
+from .sparse import CsrMatrix, HalfRows, ShapeError, pack_rows_f16
 
 
 def partition_rows(row_ptr, parts: int) -> np.ndarray:
@@ -206,6 +206,28 @@ def all_gather_padded(x_local: torch.Tensor, part: RowPartition, group=None, asy
     return full, work
 
 
+def all_gather_half(hr: HalfRows, part: RowPartition, group=None, async_op=False):
+    """All-gather fp16 rows with their scales in ONE collective (TF32 class:
+    half the bytes of the fp32 operand): each row travels as its ldh halves
+    followed by 8 halves whose first two hold the float32 scale's bits.
+    Returns (HalfRows over the padded gather buffer, work handle, finish) —
+    call ``finish()`` after ``work.wait()`` to extract the scales."""
+    ldh = hr.xh.shape[1]
+    w = ldh + 8  # row pitch stays a multiple of 16 bytes
+    send, full = part.gather_buffers(w, torch.float16, hr.xh.device, tag="half")
+    rows = hr.xh.shape[0]
+    send[:rows, :ldh].copy_(hr.xh)
+    send[:rows, ldh:ldh + 2].copy_(hr.sigma.view(torch.float16).view(rows, 2))
+    work = dist.all_gather_into_tensor(full, send, group=group, async_op=async_op)
+    out = HalfRows(full[:, :ldh], torch.empty(0), hr.K)
+
+    def finish():
+        out.sigma = full[:, ldh:ldh + 2].contiguous().view(torch.float32).view(-1)
+        return out
+
+    return out, work, finish
+
+
 def all_gather_rows(x_local: torch.Tensor, part: RowPartition, group=None) -> torch.Tensor:
     """Assemble the full n x k operand from every rank's row block (padded
     all_gather_into_tensor, then the padding is dropped).  Returns a fresh
@@ -238,6 +260,10 @@ class CudaOps:
         if hub_d is not None:
             pat = a
             vals = a.values if weighted else None
+            # fp16 rows carry the unit tail's column scale in their row
+            # scales; Ñ's weighted tail keeps it in its values, so only then
+            # does the dense part scale its columns
+            dcol = hub_d[1] if (weighted or not isinstance(b, HalfRows)) else None
             if weighted:  # Ñ block: the split runs on the unit pattern twin
                 key = ("unit_twin",)
                 if key not in a._plans:
@@ -245,10 +271,12 @@ class CudaOps:
                     twin._unit = True
                     a._plans[key] = twin
                 pat = a._plans[key]
-            spec = hub.choose_split(pat, b, hub_d[1], d_row=hub_d[0], values=vals)
+            spec = hub.choose_split(pat, b, dcol, d_row=hub_d[0], values=vals)
             if spec:
-                return hub.hybrid_aggregate(pat, b, hub_d[1], spec, d_row=hub_d[0], values=vals,
+                return hub.hybrid_aggregate(pat, b, dcol, spec, d_row=hub_d[0], values=vals,
                                             relu=relu, out=out, accumulate=accumulate)
+        if isinstance(b, HalfRows):
+            d_col = None  # carried by the row scales
         f = spmm if weighted else spmm_unweighted
         return f(a, b, d_row=d_row, d_col=d_col, relu=relu, out=out, accumulate=accumulate)
 
@@ -322,6 +350,10 @@ def dist_gcn_layer(part: RowPartition, h_local: torch.Tensor, w: torch.Tensor, *
     hub_unit = hub_unit and d is not None
     d_loc = d[part.lo:part.hi] if (dyn or hub_unit) else None
     weighted = not (dyn and part.local.has_unit_values)
+    if ops is CudaOps and _half_gathered(part, w.shape[1] if order == "update_first"
+                                         else h_local.shape[1], h_local):
+        return _dist_gcn_half(part, h_local, w, dyn, order, d, d_loc, weighted, group,
+                              overlap, hub_unit)
     if part.rows == 0:
         src = ops.gemm(h_local, w) if order == "update_first" else h_local
         all_gather_padded(src, part, group)
@@ -355,6 +387,51 @@ def dist_gcn_layer(part: RowPartition, h_local: torch.Tensor, w: torch.Tensor, *
     x = ops.spmm(pat, full, d_row=dl, d_col=d_pad if dyn else None, relu=False, weighted=weighted,
                  **hub_kw)
     return ops.gemm(x, w, relu=True)
+
+
+def _half_gathered(part: RowPartition, k: int, like: torch.Tensor) -> bool:
+    """The TF32 class's fp16 gather rows (gcn.half_gather), decided on the
+    gathered operand's size so every rank takes the same branch."""
+    from . import gcn
+    from .sparse import get_gemm_precision
+
+    return (gcn.HALF_GATHER and get_gemm_precision() == "tf32" and like.is_cuda and k % 8 == 0
+            and part.world * part.max_rows * k * 4 > gcn.HALF_MIN_BYTES)
+
+
+def _dist_gcn_half(part, h_local, w, dyn, order, d, d_loc, weighted, group, overlap, hub_unit):
+    """dist_gcn_layer in the TF32 class with fp16 gather rows: the local
+    operand is packed once (d folded for the dynamic composition), the
+    all-gather moves fp16 rows + scales (half the bytes), and every pass
+    reads HalfRows."""
+    ops = CudaOps
+    src = ops.gemm(h_local, w) if order == "update_first" else h_local
+    if part.rows == 0:  # still joins the collective
+        k = src.shape[1]
+        ldh = (k + 7) // 8 * 8
+        empty = HalfRows(torch.zeros(0, ldh, dtype=torch.float16, device=src.device),
+                         torch.zeros(0, dtype=torch.float32, device=src.device), k)
+        _, work, _ = all_gather_half(empty, part, group)
+        return torch.zeros(0, w.shape[1], dtype=torch.float32, device=h_local.device)
+    hr = pack_rows_f16(src, d_loc if dyn else None)
+    dl = d_loc if dyn else None
+    last = order == "update_first"
+    if overlap:
+        loc, rem = part.split_local_remote()
+        full, work, finish = all_gather_half(hr, part, group, async_op=True)
+        loc_kw = {"hub_d": (d_loc, d_loc)} if hub_unit else {}
+        y = ops.spmm(loc, hr, d_row=dl, relu=False, weighted=weighted, **loc_kw)
+        work.wait()
+        full = finish()
+        hub_kw = {"hub_d": (d_loc, part.pad_vector(d))} if hub_unit else {}
+        y = ops.spmm(rem, full, d_row=dl, relu=last, weighted=weighted, out=y, accumulate=True,
+                     **hub_kw)
+        return y if last else ops.gemm(y, w, relu=True)
+    full, work, finish = all_gather_half(hr, part, group)
+    full = finish()
+    hub_kw = {"hub_d": (d_loc, part.pad_vector(d))} if hub_unit else {}
+    y = ops.spmm(part.padded(), full, d_row=dl, relu=last, weighted=weighted, **hub_kw)
+    return y if last else ops.gemm(y, w, relu=True)
 
 
 def _pad4(n: int) -> int:

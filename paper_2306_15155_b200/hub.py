@@ -53,7 +53,8 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .sparse import CsrMatrix, ShapeError, _ld, _require_cuda, _spmm, _stream, _timed_call
+from .sparse import (CsrMatrix, HalfRows, ShapeError, _ld, _ptr, _require_cuda, _spmm, _stream,
+                     _timed_call)
 
 HUB_SPLIT = os.environ.get("GNNC_HUB_SPLIT", "auto")
 # term format of the dense operand: "auto" (default: one fp16 term in the TF32
@@ -424,14 +425,23 @@ def pack(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec):
     format used (``term_format``)."""
     plan = hub_plan(a, spec)
     lib = nat.load()
-    K = x.shape[1]
+    half = isinstance(x, HalfRows)
+    K = x.K if half else x.shape[1]
     kp = int(lib.gc_hub_terms_rows(K))
     fmt = term_format(plan.fmt)
     if fmt == nat.GC_HUB_F16 and not getattr(plan, "abits", False) \
             and lib.gc_hub_f16_mn_supported(K):
         fmt = nat.GC_HUB_F16_MN  # rows as gathered: no transpose in the pack
+    if half and fmt not in (nat.GC_HUB_F16, nat.GC_HUB_F16_MN):
+        raise ShapeError("hub pack: fp16 gather rows carry the one-term (TF32 class) format only")
     bt = torch.empty(_TERMS[fmt] * kp * plan.T, dtype=_block_dtype(fmt), device=x.device)
     sc = torch.empty(2, dtype=torch.float32, device=x.device)
+    if half:  # the dense part reads the same fp16 rows as the tail
+        nat.check(lib.gc_hub_pack_f16rows(x.xh.data_ptr(), _ld(x.xh), x.sigma.data_ptr(), K,
+                                          plan.hub_cols.data_ptr(), plan.T, _ptr(d), fmt,
+                                          bt.data_ptr(), sc.data_ptr(), _stream(x.device)),
+                  "hub_pack_f16rows")
+        return bt, sc, fmt
     nat.check(lib.gc_hub_pack(x.data_ptr(), _ld(x), K, plan.hub_cols.data_ptr(), plan.T,
                               None if d is None else d.data_ptr(), fmt, bt.data_ptr(),
                               sc.data_ptr(),
@@ -450,7 +460,7 @@ def dense_part(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, out: torch.
     dev = x.device
     lib = nat.load()
     st = _stream(dev)
-    K = x.shape[1]
+    K = x.K if isinstance(x, HalfRows) else x.shape[1]
     zero_done = None
     if plan.kind == "stair" and plan.rows0 < a.n_rows and not accumulate \
             and (rows is None or tuple(rows) == (0, a.n_rows)):
@@ -539,15 +549,21 @@ def hybrid_aggregate(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, *,
     (ReLU on the total).  ``rows=(lo, hi)`` (block plans only) computes that
     row block (``out`` then has hi-lo rows); ``packed`` reuses one ``pack``;
     ``x_tail``: fp16 rows of x for the tail (see :func:`tail_part`)."""
-    dev = _require_cuda(a.col_idx, x)
-    if x.dim() != 2 or x.shape[0] != a.n_cols or x.stride(1) != 1:
+    if isinstance(x, HalfRows):  # one fp16 operand for the dense part and the tail
+        if x.shape[0] != a.n_cols:
+            raise ShapeError("hybrid_aggregate: x must have n_cols rows")
+        if d is not None and values is None:
+            raise ShapeError("hybrid_aggregate: fp16 rows carry the column scaling (d=None)")
+        x_tail = x
+    elif x.dim() != 2 or x.shape[0] != a.n_cols or x.stride(1) != 1:
         raise ShapeError("hybrid_aggregate: x must be a row-major n_cols x K tensor")
+    dev = _require_cuda(a.col_idx, x.xh if isinstance(x, HalfRows) else x)
     if d_row is None:
         if a.n_rows != a.n_cols or d is None:
             raise ShapeError("hybrid_aggregate: d_row is required for a rectangular pattern "
                              "or an already column-scaled x (d=None)")
         d_row = d
-    K = x.shape[1]
+    K = x.shape[1]  # (HalfRows.shape is (n, K) too)
     lo, hi = rows if rows is not None else (0, a.n_rows)
     if out is None:
         if accumulate:
@@ -641,7 +657,12 @@ def choose_split(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, *,
     key = split_key(K, values is not None)
     if key in a._plans:
         return a._plans[key]
-    if a.nnz < HUB_MIN_NNZ or x.stride(1) != 1:
+    if isinstance(x, HalfRows):
+        x_tail = x
+    elif x.stride(1) != 1:
+        a._plans[key] = 0
+        return 0
+    if a.nnz < HUB_MIN_NNZ:
         a._plans[key] = 0
         return 0
     cands = _candidates(K)

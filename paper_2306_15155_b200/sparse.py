@@ -963,6 +963,34 @@ def gemm(a, b, *, row_scale=None, relu=False, precision: str | None = None, out=
     return oa.wrap(out) if (oa.host and ob.host) else out
 
 
+def gemm_f16rows(a: torch.Tensor, b: torch.Tensor, *, row_scale=None) -> HalfRows | None:
+    """(diag(row_scale) a @ b) produced directly as the TF32 class's fp16
+    gather operand (``HalfRows``) by the TF32 tcgen05 GEMM's epilogue — the
+    fp32 product is never written.  None when the shape is outside the fused
+    epilogue's range (N > 256, unaligned A): the caller then packs."""
+    _require_cuda(a, b, row_scale)
+    M, K = a.shape
+    N = b.shape[1]
+    if b.shape[0] != K:
+        raise ShapeError(f"gemm: inner dimensions {K} != {b.shape[0]}")
+    if N > 256 or K < 1 or a.stride(1) != 1 or _ld(a) % 4 or a.data_ptr() % 16:
+        return None
+    if row_scale is not None and tuple(row_scale.shape) != (M,):
+        raise ShapeError("gemm: row_scale must have one entry per row")
+    bt = b.contiguous() if b.stride(1) != 1 else b
+    lib = nat.load()
+    ldh = (N + 7) // 8 * 8
+    xh = torch.empty(M, ldh, dtype=torch.float16, device=a.device)
+    sigma = torch.empty(M, dtype=torch.float32, device=a.device)
+    ws = torch.empty(max(int(lib.gc_gemm_workspace_bytes(K, N)), 16), dtype=torch.uint8,
+                     device=a.device)
+    rc = _timed_call("gemm", a.device, lambda: lib.gc_gemm_f16rows_f32(
+        a.data_ptr(), _ld(a), bt.data_ptr(), _ld(bt), M, K, N, _ptr(row_scale), xh.data_ptr(), ldh,
+        sigma.data_ptr(), ws.data_ptr(), ws.numel(), _stream(a.device)))
+    nat.check(rc, "gemm_f16rows")
+    return HalfRows(xh, sigma, N)
+
+
 def scale_rows(d, b, *, relu: bool = False):
     """Row scaling out[i,k] = d[i] * b[i,k] (sparse.py:294-300)."""
     dev = b.device if isinstance(b, torch.Tensor) else default_device()

@@ -149,3 +149,66 @@ def test_partitioned_gat_layer_on_gpu(oracle, comp, att, heads):
     a_d = rng.uniform(-0.5, 0.5, k2 * heads).astype(np.float32).astype(np.float64)
     ref = oracle.gat_layer_multihead(at, h, w, a_s, a_d, heads, 0.2, comp, "relu")
     assert oracle.rel_err(full, ref) <= 1e-4
+
+
+def _half_worker(rank, world, port, comp, order, overlap, q):
+    import sys
+    from pathlib import Path
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2306_15155_b200 as gc
+        from paper_2306_15155_b200 import gcn, graphs, hub
+        from paper_2306_15155_b200.distributed import RowPartition, all_gather_rows, dist_gcn_layer
+
+        gcn.HALF_MIN_BYTES = 0  # fp16 gathers at test size
+        hub.HUB_SPLIT = "stair:40"
+        dev = torch.device("cuda", 0)
+        a = graphs.synthetic_graph("rmat", 6000, 300000, seed=5, device=dev)
+        g = gc.NormalizedGraph.from_adjacency(a).with_precomputed()
+        rng = np.random.default_rng(9)
+        h = torch.from_numpy(rng.uniform(-0.5, 0.5, (6000, 40)).astype(np.float32)).to(dev)
+        w = torch.from_numpy(rng.uniform(-0.5, 0.5, (40, 32)).astype(np.float32)).to(dev)
+        gc.set_gemm_precision("tf32")
+        part = RowPartition.of(g.n_tilde if comp == "precompute" else g.a_tilde, rank, world)
+        out = dist_gcn_layer(part, h[part.lo:part.hi], w, composition=comp, order=order,
+                             d=g.d_inv_sqrt.to(dev), overlap=overlap, hub_unit=True)
+        full = all_gather_rows(out.cpu(), part)
+        if rank == 0:
+            q.put(full.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("overlap", [False, True])
+@pytest.mark.parametrize("comp,order", [("dynamic", "update_first"), ("dynamic", "aggregate_first"),
+                                        ("precompute", "update_first")])
+def test_partitioned_layer_fp16_gather_on_gpu(oracle, comp, order, overlap):
+    """TF32 class, fp16 rows + scales all-gathered in one collective (half the
+    bytes), the staircase split on each rank reading the same fp16 rows:
+    against the oracle at the class's tolerance."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_half_worker, args=(r, 2, port, comp, order, overlap, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    full = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from paper_2306_15155_b200 import graphs
+
+    rp, ci, v = graphs.synthetic_graph("rmat", 6000, 300000, seed=5, device="cuda").numpy()
+    og = oracle.GcnGraph.from_adjacency(oracle.Csr(6000, 6000, rp, ci, v))
+    rng = np.random.default_rng(9)
+    h = rng.uniform(-0.5, 0.5, (6000, 40)).astype(np.float32).astype(np.float64)
+    w = rng.uniform(-0.5, 0.5, (40, 32)).astype(np.float32).astype(np.float64)
+    ref = oracle.gcn_layer(og, h, w, comp, order)
+    assert oracle.rel_err(full, ref) <= 3e-3

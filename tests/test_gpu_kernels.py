@@ -267,6 +267,28 @@ def test_gemm_3xtf32_wide_dynamic_range(oracle):
     assert float(np.abs(tf.cpu().numpy() - ref).max() / np.abs(ref).max()) > 10 * err
 
 
+@pytest.mark.parametrize("M,K,N", [(1, 8, 8), (300, 64, 40), (1000, 256, 256), (4097, 128, 16),
+                                   (2000, 1433, 16), (777, 96, 200)])
+@pytest.mark.parametrize("scaled", [False, True])
+def test_gemm_f16rows_epilogue_equals_pack(M, K, N, scaled):
+    """gc_gemm_f16rows_f32 (the TF32 GEMM emitting the fp16 gather operand
+    from TMEM) is bit-identical to gc_pack_rows_f16 of the TF32 GEMM's fp32
+    output (same row max, same power-of-two scale, same two roundings)."""
+    rng = np.random.default_rng(M + K + N)
+    a = torch.from_numpy(f32(rng.uniform(-0.5, 0.5, (M, K)) * 2.0 ** rng.integers(-6, 6, (M, 1)))).to(DEV)
+    w = torch.from_numpy(f32(rng.uniform(-0.5, 0.5, (K, N)))).to(DEV)
+    if K % 4:  # TMA needs a 16-byte row pitch (gemm pads; the fused path does not)
+        ap = torch.zeros(M, (K + 3) // 4 * 4, device=DEV)
+        ap[:, :K] = a
+        a = ap[:, :K]
+    rs = torch.from_numpy(f32(rng.uniform(0.1, 1.0, M))).to(DEV) if scaled else None
+    hr = sparse.gemm_f16rows(a, w, row_scale=rs)
+    assert hr is not None and hr.K == N
+    ref = sparse.pack_rows_f16(gc.gemm(a, w, row_scale=rs, precision="tf32"))
+    assert torch.equal(hr.xh.view(torch.int16), ref.xh.view(torch.int16))
+    assert torch.equal(hr.sigma, ref.sigma)
+
+
 def test_gemm_known_and_errors():
     out = gc.gemm(np.array([[1.0, 2.0], [3.0, 4.0]]), np.array([[5.0], [6.0]]), precision="fp32")
     assert np.array_equal(out, [[17.0], [39.0]])
@@ -732,6 +754,45 @@ def test_hub_gemm_term_split(oracle, K, T, fmt):
     assert oracle.rel_err(out.cpu().numpy(), ref) < (1e-3 if fmt in ("f16", "f16mn") else 1e-6)
 
 
+@pytest.mark.parametrize("K", [8, 32, 96, 256, 512])
+@pytest.mark.parametrize("fmt", ["f16", "f16mn"])
+@pytest.mark.parametrize("with_d", [False, True])
+def test_hub_pack_from_fp16_rows_bit_exact(K, fmt, with_d):
+    """gc_hub_pack_f16rows (the dense part reading the fp16 gather operand)
+    packs exactly what gc_hub_pack packs from the dequantised fp32 rows
+    sigma_j * xh_j (exact in fp32: sigma is a power of two here)."""
+    from paper_2306_15155_b200 import _native as nat
+    f = {"f16": nat.GC_HUB_F16, "f16mn": nat.GC_HUB_F16_MN}[fmt]
+    lib = nat.load()
+    if fmt == "f16mn" and not lib.gc_hub_f16_mn_supported(K):
+        pytest.skip("MN-major one-term operand needs CTA pairs and K > 64")
+    rng = np.random.default_rng(K + 31)
+    ncols, T = 3000, 128
+    x = torch.from_numpy(f32(rng.standard_normal((ncols, K)) * 4.0 ** rng.integers(-4, 4, (ncols, 1)))).to(DEV)
+    hr = sparse.pack_rows_f16(x)
+    deq = (hr.xh[:, :K].float() * hr.sigma[:, None]).contiguous()
+    hub_cols = torch.from_numpy(np.sort(rng.choice(ncols, T, replace=False)).astype(np.int32)).to(DEV)
+    d = torch.from_numpy(f32(rng.uniform(0.05, 1.0, ncols))).to(DEV) if with_d else None
+    kp = lib.gc_hub_terms_rows(K)
+    st = torch.cuda.current_stream().cuda_stream
+    outs = []
+    for half in (True, False):
+        bt = torch.empty(kp * T, dtype=torch.float16, device=DEV)
+        sc = torch.empty(2, dtype=torch.float32, device=DEV)
+        dp = None if d is None else d.data_ptr()
+        if half:
+            rc = lib.gc_hub_pack_f16rows(hr.xh.data_ptr(), hr.xh.stride(0), hr.sigma.data_ptr(), K,
+                                         hub_cols.data_ptr(), T, dp, f, bt.data_ptr(),
+                                         sc.data_ptr(), st)
+        else:
+            rc = lib.gc_hub_pack(deq.data_ptr(), K, K, hub_cols.data_ptr(), T, dp, f,
+                                 bt.data_ptr(), sc.data_ptr(), st)
+        nat.check(rc, "pack")
+        outs.append((bt.cpu(), sc[1:].cpu()))
+    assert torch.equal(outs[0][0].view(torch.int16), outs[1][0].view(torch.int16))
+    assert torch.equal(outs[0][1], outs[1][1])
+
+
 @pytest.mark.parametrize("K", [3, 32, 256])
 @pytest.mark.parametrize("T", [64, 128])
 @pytest.mark.parametrize("precompute", [False, True])
@@ -750,6 +811,33 @@ def test_hybrid_aggregate_matches_oracle(oracle, hub_pl, K, T, precompute):
     plan = hub.hub_plan(g.a_tilde, T)
     assert plan.hub_edges + plan.tail.nnz == g.a_tilde.nnz
     assert plan.hub_edges == int(plan.a_hub.float().sum())
+
+
+@pytest.mark.parametrize("comp", ["precompute", "dynamic"])
+@pytest.mark.parametrize("order", ["aggregate_first", "update_first"])
+@pytest.mark.parametrize("split", ["0", "128"])
+def test_gcn_layer_fp16_gathers_tf32_class(oracle, hub_pl, comp, order, split, monkeypatch):
+    """TF32 class with the fp16 gather operand forced on a small graph (the
+    size threshold lifted): plain SpMM and the hybrid split's tail, every
+    composition, against the oracle at the class's 1e-2 (and well inside)."""
+    from paper_2306_15155_b200 import gcn, hub
+    monkeypatch.setattr(gcn, "HALF_MIN_BYTES", 0)
+    monkeypatch.setattr(hub, "HUB_SPLIT", split)
+    g = gc.NormalizedGraph.from_adjacency(hub_pl).with_precomputed()
+    og = oracle.GcnGraph.from_adjacency(to_oracle(oracle, hub_pl))
+    rng = np.random.default_rng(4)
+    k1, k2 = 48, 32
+    h = f32(rng.uniform(-0.5, 0.5, (hub_pl.n_rows, k1)))
+    w = f32(rng.uniform(-0.5, 0.5, (k1, k2)))
+    spec = gc.GcnLayerSpec(k1, k2, w, composition=comp, order=order)
+    assert gc.get_gemm_precision() == "tf32"
+    packs = []
+    real_pack = gcn.pack_rows_f16
+    monkeypatch.setattr(gcn, "pack_rows_f16", lambda *a, **k: packs.append(1) or real_pack(*a, **k))
+    out = gc.gcn_layer(g, torch.from_numpy(h).to(DEV), spec).cpu().numpy()
+    assert packs, "the fp16 gather operand was used"
+    ref = oracle.gcn_layer(og, h.astype(np.float64), w.astype(np.float64), comp, order)
+    assert oracle.rel_err(out, ref) <= 3e-3
 
 
 @pytest.mark.parametrize("comp", ["precompute", "dynamic"])
