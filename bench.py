@@ -167,14 +167,26 @@ class ClockSampler:
                 "samples_under_load": len(load), "interval_ms": 50}
 
 
-def spmm_alg_bytes(n_rows: int, m: int, K: int, weighted: bool, dcol: bool, drow: bool) -> int:
+def spmm_alg_bytes(n_rows: int, m: int, K: int, weighted: bool, dcol: bool, drow: bool,
+                   half: bool = False) -> int:
     """Edge-gather model of SURVEY.md §8(d): row_ptr + col_idx + (values) +
-    (d_j gathers) + one K-row of B per edge + the output (+ d_i)."""
-    b = 4 * (n_rows + 1) + 4 * m + 4 * m * K + 4 * n_rows * K
+    (d_j gathers) + one K-row of B per edge + the output (+ d_i).  ``half``:
+    the TF32 class's fp16 rows — 2K bytes per gathered row plus its 4-byte
+    scale (which carries d_j)."""
+    b = 4 * (n_rows + 1) + 4 * m + (2 if half else 4) * m * K + 4 * n_rows * K
     b += 4 * m if weighted else 0
-    b += 4 * m if dcol else 0
+    b += 4 * m if (dcol or half) else 0
     b += 4 * n_rows if drow else 0
     return b
+
+
+def uses_half(gc, n_cols: int, K: int) -> bool:
+    """Whether the TF32 class gathers fp16 rows for an n_cols x K operand
+    (gcn.half_gather's rule)."""
+    from paper_2306_15155_b200 import gcn
+
+    return (gcn.HALF_GATHER and gc.get_gemm_precision() == "tf32" and K % 8 == 0
+            and n_cols * K * 4 > gcn.HALF_MIN_BYTES)
 
 
 def layer_flops(n: int, m: int, k1: int, k2: int, order: str) -> int:
@@ -547,7 +559,8 @@ def main():
         plan = hub.hub_plan(pat, split)
         mt = plan.tail.nnz
         nr = pat.n_rows
-        tail_bytes = spmm_alg_bytes(nr, mt, K, weighted, dyn, dyn) + 4 * nr * K
+        half = uses_half(gc, pat.n_cols, K)
+        tail_bytes = spmm_alg_bytes(nr, mt, K, weighted, dyn, dyn, half) + 4 * nr * K
         ach = tail_bytes / (tail_ms * 1e-3) / 1e9
         traffic = traffic_lookup(f"{args.shape}/K{K}/{comp}/tail/{hub.spec_label(split)}", world)
         roof = {"kernel": "spmm_kernel (tail of the dense split)", "bound": "hbm",
@@ -556,7 +569,9 @@ def main():
                 "alg_bytes_per_launch": tail_bytes, "kernel_ms": round(tail_ms, 4),
                 "share_of_step": round(tail_ms / ms, 3), "peak_source": pk["source"],
                 "model": "edge-gather over the tail edges: 4(n+1)+4m_t[+4m_t values][+4m_t d_j]"
-                         "+4m_tK+4nK(+4nK C read)[+4n]; frac > 1 = gathered rows served by L2",
+                         "+4m_tK (2m_tK + 4m_t scales with fp16 rows)+4nK(+4nK C read)[+4n]; "
+                         "frac > 1 = gathered rows served by L2",
+                "fp16_rows": half,
                 "tail_edges": mt}
         roof.update(_dram_side(traffic, tail_ms, pk, tail_bytes))
         cell_flops = 2 * plan.cells * K * hub.term_count()
@@ -578,7 +593,8 @@ def main():
                     "model": "cell flops 2·cells·K per 16-bit term (f16: 1 term, TF32-equivalent "
                              "11-bit rounding of D·X; f16x2: 2 terms); useful flops 2·edges·K"}
     elif spmm_ms:
-        spmm_bytes = spmm_alg_bytes(a_used.n_rows, a_used.nnz, K, weighted, dyn, dyn)
+        spmm_bytes = spmm_alg_bytes(a_used.n_rows, a_used.nnz, K, weighted, dyn, dyn,
+                                    uses_half(gc, a_used.n_cols, K))
         ach = spmm_bytes / (spmm_ms * 1e-3) / 1e9
         traffic = traffic_lookup(f"{args.shape}/K{K}/{comp}", world)
         roof = {"kernel": "spmm_kernel", "bound": "hbm", "achieved": round(ach, 1),
@@ -752,7 +768,7 @@ def sweep(gc, g, feats, args, dev, pk, parity) -> list[dict]:
             sp = float(np.median(kt.durations_ms("spmm")))
             rounds[comp].append(med)
             dyn = base == "dynamic"
-            b = spmm_alg_bytes(n, m, K, not dyn, dyn, dyn)
+            b = spmm_alg_bytes(n, m, K, not dyn, dyn, dyn, uses_half(gc, n, K))
             entry["compositions"][comp] = {
                 "ms": round(med * 1e3, 4), "edges_per_s": round(m / med, 1),
                 "gflops": round(layer_flops(n, m, K, K, order) / med / 1e9, 1),
@@ -949,7 +965,7 @@ def extra_configs(gc, args, dev, pk) -> dict:
             torch.cuda.synchronize()
             sp = float(np.median(kt.durations_ms("spmm")))
             dyn = base == "dynamic"
-            b = spmm_alg_bytes(n, m, K, not dyn, dyn, dyn)
+            b = spmm_alg_bytes(n, m, K, not dyn, dyn, dyn, uses_half(gc, n, K))
             row["gcn"][comp] = {"ms": round(t[comp] * 1e3, 4), "edges_per_s": round(m / t[comp], 1),
                                 "spmm_ms": round(sp, 4),
                                 "spmm_hbm_frac": round(b / (sp * 1e-3) / 1e9 / pk["hbm_gbs"], 3),

@@ -519,6 +519,16 @@ __device__ __forceinline__ void gemm_tc_body(const CUtensorMap &map_a, const CUt
         if (!row_ok) continue;
         const int64_t col = n0 + c;
         if (accum) {  // C = relu?(old + rs * acc), the SpMM epilogue's order
+          if (vec && col + 16 <= ep.N) {  // 16-byte read-modify-write
+#pragma unroll
+            for (int i = 0; i < 16; i += 4) {
+              float4 o = *reinterpret_cast<const float4 *>(crow + col + i);
+              o.x += v[i], o.y += v[i + 1], o.z += v[i + 2], o.w += v[i + 3];
+              if (relu) o.x = fmaxf(o.x, 0.f), o.y = fmaxf(o.y, 0.f), o.z = fmaxf(o.z, 0.f), o.w = fmaxf(o.w, 0.f);
+              stg_f4(crow + col + i, o);
+            }
+            continue;
+          }
 #pragma unroll
           for (int i = 0; i < 16; ++i)
             if (col + i < ep.N) {
@@ -1101,6 +1111,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ABITS ? kGemmThreads
         if (!row_ok) continue;
         const int64_t col = n0 + c;
         if (accum) {
+          if (vec && col + 16 <= ep.N) {  // 16-byte read-modify-write
+#pragma unroll
+            for (int i = 0; i < 16; i += 4) {
+              float4 o = *reinterpret_cast<const float4 *>(crow + col + i);
+              o.x += v[i], o.y += v[i + 1], o.z += v[i + 2], o.w += v[i + 3];
+              if (relu) o.x = fmaxf(o.x, 0.f), o.y = fmaxf(o.y, 0.f), o.z = fmaxf(o.z, 0.f), o.w = fmaxf(o.w, 0.f);
+              stg_f4(crow + col + i, o);
+            }
+            continue;
+          }
 #pragma unroll
           for (int i = 0; i < 16; ++i)
             if (col + i < ep.N) {

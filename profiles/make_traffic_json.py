@@ -1,26 +1,81 @@
-"""Collect ncu per-launch DRAM traffic of the SpMM (profiles/run_ncu_traffic.sh
-output) into profiles/traffic.json, keyed like bench.py's roofline lookup."""
+"""Launch-list summary and profiles/traffic.json from an ncu launch list
+(`profiles/run_ncu_r02.sh`: --metrics gpu__time_duration.sum,
+dram__bytes_read.sum, dram__bytes_write.sum over the bench's timed steps).
 
+Prints a markdown table (per kernel: launches, µs per launch, share of the
+profiled steps, DRAM GB per launch) and records, for the bench's roofline
+lookup, the DRAM bytes per launch of the dominant SpMM (the tail of the dense
+split when one is chosen) under the key bench.py uses:
+  "<shape>/K<K>/<composition>[/tail/<split>]".
+
+    python profiles/make_traffic_json.py gpurun_out/ncu_r02 [--shape reddit --k 256]
+"""
+
+from __future__ import annotations
+
+import argparse
 import csv
 import json
-import sys
+from collections import OrderedDict
 from pathlib import Path
 
-src = Path(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/ncu_traffic")
-out = {}
-for f in sorted(src.glob("*.csv")):
-    rows = list(csv.reader(f.open()))
+
+def launches(path: Path) -> list[dict]:
+    rows = list(csv.reader(path.open()))
     hi = next(i for i, r in enumerate(rows) if "Metric Name" in r)
-    hdr, data = rows[hi], rows[hi + 1:]
-    mi, vi, ui = hdr.index("Metric Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    vals = {}
-    for r in data:
-        v = float(r[vi].replace(",", ""))
-        vals[r[mi]] = v * scale.get(r[ui], 1)
-    comp = f.stem.replace("_", ":", 1)
-    comp = comp.replace("precompute:", "precompute:").replace("dynamic:", "dynamic:")
-    out[f"reddit/K256/{comp}"] = int(vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"])
-    out[f"reddit/K256/{comp}/detail"] = vals
-Path("profiles/traffic.json").write_text(json.dumps(out, indent=1) + "\n")
-print(json.dumps(out, indent=1))
+    hdr = rows[hi]
+    col = {k: hdr.index(k) for k in ("ID", "Kernel Name", "Metric Name", "Metric Value")}
+    by_id: "OrderedDict[str, dict]" = OrderedDict()
+    for r in rows[hi + 1:]:
+        if len(r) < len(hdr):
+            continue
+        rec = by_id.setdefault(r[col["ID"]], {"kernel": r[col["Kernel Name"]]})
+        rec[r[col["Metric Name"]]] = float(r[col["Metric Value"]].replace(",", ""))
+    return list(by_id.values())
+
+
+def short(name: str) -> str:
+    name = name.replace("unnamed>::", "").replace("void ", "")
+    return name.split("(")[0]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("src")
+    ap.add_argument("--shape", default="reddit")
+    ap.add_argument("--k", type=int, default=256)
+    ap.add_argument("--steps", type=int, default=2)
+    args = ap.parse_args()
+    src = Path(args.src)
+    recs = launches(src / "launches.csv")
+    forced = (src / "forced.txt").read_text().split() if (src / "forced.txt").exists() else []
+    split = next((f.split("=")[1] for f in forced if f.startswith("split=")), "0")
+    comp = next((f.split("=")[1] for f in forced if f.startswith("composition=")), "")
+    total = sum(r.get("gpu__time_duration.sum", 0) for r in recs)
+    agg: "OrderedDict[str, list]" = OrderedDict()
+    for r in recs:
+        agg.setdefault(short(r["kernel"]), []).append(r)
+    print(f"forced: split={split} composition={comp}; {len(recs)} launches over {args.steps} steps\n")
+    print("| kernel | launches | µs / launch | share | DRAM GB / launch |")
+    print("|---|---|---|---|---|")
+    for k, rs in sorted(agg.items(), key=lambda kv: -sum(x.get("gpu__time_duration.sum", 0)
+                                                          for x in kv[1])):
+        t = sum(x.get("gpu__time_duration.sum", 0) for x in rs)
+        d = sum(x.get("dram__bytes_read.sum", 0) + x.get("dram__bytes_write.sum", 0) for x in rs)
+        print(f"| `{k}` | {len(rs)} | {t / len(rs) / 1e3:.1f} | {t / total:.3f} | "
+              f"{d / len(rs) / 1e9:.3f} |")
+    spmm = [r for r in recs if short(r["kernel"]).startswith("spmm_kernel")]
+    if not spmm:
+        return
+    dram = [int(r.get("dram__bytes_read.sum", 0) + r.get("dram__bytes_write.sum", 0)) for r in spmm]
+    key = f"{args.shape}/K{args.k}/{comp}" + (f"/tail/{split}" if split not in ("0", "") else "")
+    out_p = Path("profiles/traffic.json")
+    data = json.loads(out_p.read_text()) if out_p.exists() else {}
+    data[key] = int(sum(dram) / len(dram))
+    data[key + "/source"] = str(src / "launches.csv")
+    out_p.write_text(json.dumps(data, indent=1) + "\n")
+    print(f"\n{key}: {data[key]} DRAM bytes per launch (mean of {len(dram)})")
+
+
+if __name__ == "__main__":
+    main()

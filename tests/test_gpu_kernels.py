@@ -831,9 +831,10 @@ def test_gcn_layer_fp16_gathers_tf32_class(oracle, hub_pl, comp, order, split, m
     w = f32(rng.uniform(-0.5, 0.5, (k1, k2)))
     spec = gc.GcnLayerSpec(k1, k2, w, composition=comp, order=order)
     assert gc.get_gemm_precision() == "tf32"
-    packs = []
-    real_pack = gcn.pack_rows_f16
+    packs = []  # the fp16 rows come from the pack kernel or the GEMM epilogue
+    real_pack, real_gemm = gcn.pack_rows_f16, gcn.gemm_f16rows
     monkeypatch.setattr(gcn, "pack_rows_f16", lambda *a, **k: packs.append(1) or real_pack(*a, **k))
+    monkeypatch.setattr(gcn, "gemm_f16rows", lambda *a, **k: packs.append(2) or real_gemm(*a, **k))
     out = gc.gcn_layer(g, torch.from_numpy(h).to(DEV), spec).cpu().numpy()
     assert packs, "the fp16 gather operand was used"
     ref = oracle.gcn_layer(og, h.astype(np.float64), w.astype(np.float64), comp, order)
