@@ -54,7 +54,7 @@ import torch
 
 from . import _native as nat
 from .sparse import (CsrMatrix, HalfRows, ShapeError, _ld, _ptr, _require_cuda, _spmm, _stream,
-                     _timed_call, relu_)
+                     _timed_call)
 
 HUB_SPLIT = os.environ.get("GNNC_HUB_SPLIT", "auto")
 # term format of the dense operand: "auto" (default: one fp16 term in the TF32
@@ -450,8 +450,6 @@ def pack(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec):
 
 
 _SIDE_STREAMS: dict = {}
-# "1": run the tail SpMM before the staircase GEMM (see hybrid_aggregate)
-TAIL_FIRST = os.environ.get("GNNC_TAIL_FIRST", "0") == "1"
 
 
 def dense_part(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, out: torch.Tensor, *,
@@ -574,28 +572,7 @@ def hybrid_aggregate(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec, *,
     elif tuple(out.shape) != (hi - lo, K) or out.stride(1) != 1:
         raise ShapeError(f"hybrid_aggregate: out must be a row-major {hi - lo}x{K} tensor")
 
-    tail_first = TAIL_FIRST and not accumulate and rows is None and hub_plan(a, spec).kind == "stair"
-
     def run():
-        if tail_first:
-            # the tail first (writes every row, no zero fill, reads x while it
-            # is still L2-resident from its producer), then the staircase
-            # accumulates; ReLU over the total
-            lo_hi = (0, a.n_rows)
-            plan = hub_plan(a, spec)
-            tail = plan.tail_block(values, *lo_hi)
-            xt = x_tail
-            if xt is not None:
-                _spmm(tail, xt, weighted=values is not None,
-                      d_row=d_row if values is None else None, out=out, timer="spmm_tail")
-            elif values is None:
-                _spmm(tail, x, weighted=False, d_row=d_row, d_col=d, out=out, timer="spmm_tail")
-            else:
-                _spmm(tail, x, weighted=True, out=out, timer="spmm_tail")
-            dense_part(a, x, d, spec, out, d_row=d_row, accumulate=True, packed=packed)
-            if relu:
-                relu_(out)
-            return 0
         dense_part(a, x, d, spec, out, d_row=d_row, accumulate=accumulate, packed=packed,
                    rows=rows)
         tail_part(a, x, d, spec, out, d_row=d_row, values=values, relu=relu, rows=rows,
