@@ -682,9 +682,10 @@ int dispatch(SpmmArgs &a, int64_t n_rows, int algo, const int32_t *items, int64_
 // so X[j,:] * d[j] = sigma[j] * Xh[j,:] up to the fp16 rounding of each
 // element (11 significant bits — the same input rounding TF32 applies).
 // A group of LPR lanes per row (LPR = K/4 up to 32: narrow rows do not leave
-// lanes idle), float4 reads kept in registers between the max and the
-// conversion when the row fits one pass, 8-byte writes.
-template <int LPR>
+// lanes idle); each lane keeps its NC float4 chunks in registers between the
+// max and the conversion, so the row is read once (K <= 4·LPR·NC, up to
+// 4096), 8-byte writes.
+template <int LPR, int NC>
 __global__ void __launch_bounds__(256)
     pack_rows_f16_kernel(const float *__restrict__ X, int64_t ldx, int64_t n, int64_t K,
                          const float *__restrict__ d, __half *__restrict__ Xh, int64_t ldh,
@@ -694,18 +695,19 @@ __global__ void __launch_bounds__(256)
   const bool live = r < n;
   const float *x = X + (live ? r : 0) * ldx;
   float mx = 0.0f;
-  // the lane's first two chunks stay in registers between the max and the
-  // conversion (a row of K <= 8·LPR is read once)
-  const int64_t c0 = 4 * gl, c1 = c0 + 4 * LPR, step = 4 * LPR;
-  float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
-  auto amax4 = [](float4 v) {
-    return fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
-  };
+  const int64_t step = 4 * LPR;
+  float4 v[NC];
+#pragma unroll
+  for (int i = 0; i < NC; ++i) v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   if (vec && live) {
-    if (c0 < K) v0 = ldg_f4(x + c0);
-    if (c1 < K) v1 = ldg_f4(x + c1);
-    mx = fmaxf(amax4(v0), amax4(v1));
-    for (int64_t c = c1 + step; c < K; c += step) mx = fmaxf(mx, amax4(ldg_f4(x + c)));
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      const int64_t c = 4 * gl + i * step;
+      if (c < K) {
+        v[i] = ldg_f4(x + c);
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[i].x), fabsf(v[i].y)), fmaxf(fabsf(v[i].z), fabsf(v[i].w))));
+      }
+    }
   } else if (live) {
     for (int64_t c = gl; c < K; c += LPR) mx = fmaxf(mx, fabsf(__ldg(x + c)));
   }
@@ -716,18 +718,19 @@ __global__ void __launch_bounds__(256)
   const int e = mx > 0.0f && isfinite(mx) ? max(min(E - 14, 110), -110) : 0;
   const float down = __uint_as_float((uint32_t)(127 - e) << 23);  // 2^-e, |e| <= 110
   __half *h = Xh + r * ldh;
-  auto put4 = [&](int64_t c, float4 v) {
-    const __half2 a = __floats2half2_rn(v.x * down, v.y * down);
-    const __half2 b = __floats2half2_rn(v.z * down, v.w * down);
-    uint2 packed;
-    packed.x = *reinterpret_cast<const uint32_t *>(&a);
-    packed.y = *reinterpret_cast<const uint32_t *>(&b);
-    *reinterpret_cast<uint2 *>(h + c) = packed;
-  };
   if (vec) {
-    if (c0 < K) put4(c0, v0);
-    if (c1 < K) put4(c1, v1);
-    for (int64_t c = c1 + step; c < K; c += step) put4(c, ldg_f4(x + c));
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      const int64_t c = 4 * gl + i * step;
+      if (c < K) {
+        const __half2 a = __floats2half2_rn(v[i].x * down, v[i].y * down);
+        const __half2 b = __floats2half2_rn(v[i].z * down, v[i].w * down);
+        uint2 packed;
+        packed.x = *reinterpret_cast<const uint32_t *>(&a);
+        packed.y = *reinterpret_cast<const uint32_t *>(&b);
+        *reinterpret_cast<uint2 *>(h + c) = packed;
+      }
+    }
   } else {
     for (int64_t c = gl; c < K; c += LPR) h[c] = __float2half_rn(__ldg(x + c) * down);
   }
@@ -756,22 +759,29 @@ extern "C" int gc_pack_rows_f16(const float *X, int64_t ldx, int64_t n_rows, int
   if (n_rows == 0) return GC_OK;
   GC_REQUIRE(X && Xh && sigma, GC_ERR_VALUE, "gc_pack_rows_f16: null operand");
   const bool vec = K % 4 == 0 && ldx % 4 == 0 && ldh % 4 == 0 && aligned16(X) &&
-                   (reinterpret_cast<uintptr_t>(Xh) & 7u) == 0;
+                   (reinterpret_cast<uintptr_t>(Xh) & 7u) == 0 && K <= 4096;
   const int64_t q = vec ? (K + 3) / 4 : K;  // lanes a row could use
   const int lpr = q >= 32 ? 32 : q >= 16 ? 16 : q >= 8 ? 8 : q >= 4 ? 4 : q >= 2 ? 2 : 1;
+  const int64_t chunks = vec ? (q + lpr - 1) / lpr : 1;  // float4 chunks per lane
   const int64_t blocks = (n_rows * lpr + 255) / 256;
   GC_REQUIRE(blocks < INT32_MAX, GC_ERR_SHAPE, "gc_pack_rows_f16: too many rows");
   __half *xh = static_cast<__half *>(Xh);
   cudaStream_t st = as_stream(stream);
-#define GC_PACK(L) \
-  pack_rows_f16_kernel<L><<<(unsigned)blocks, 256, 0, st>>>(X, ldx, n_rows, K, d, xh, ldh, sigma, vec)
+#define GC_PACK(L, C)                                                                        \
+  pack_rows_f16_kernel<L, C><<<(unsigned)blocks, 256, 0, st>>>(X, ldx, n_rows, K, d, xh, ldh, \
+                                                              sigma, vec)
   switch (lpr) {
-    case 1: GC_PACK(1); break;
-    case 2: GC_PACK(2); break;
-    case 4: GC_PACK(4); break;
-    case 8: GC_PACK(8); break;
-    case 16: GC_PACK(16); break;
-    default: GC_PACK(32); break;
+    case 1: GC_PACK(1, 1); break;
+    case 2: GC_PACK(2, 1); break;
+    case 4: GC_PACK(4, 1); break;
+    case 8: GC_PACK(8, 1); break;
+    case 16: GC_PACK(16, 1); break;
+    default:
+      if (chunks <= 2) GC_PACK(32, 2);
+      else if (chunks <= 4) GC_PACK(32, 4);
+      else if (chunks <= 8) GC_PACK(32, 8);
+      else GC_PACK(32, 32);
+      break;
   }
 #undef GC_PACK
   return check_launch("pack_rows_f16_kernel");
