@@ -186,10 +186,10 @@ __device__ __forceinline__ void softmax_row_cta(int64_t row, const int32_t *__re
       const float e = EGIVEN ? alpha[(int64_t)h * nnz + p]
                              : leaky(si[h] + __ldg(t + (int64_t)h * n_rows + j), slope);
       if (e > m[h]) {
-        z[h] = z[h] * expf(m[h] - e) + 1.0f;
+        z[h] = z[h] * __expf(m[h] - e) + 1.0f;
         m[h] = e;
       } else {
-        z[h] += expf(e - m[h]);
+        z[h] += __expf(e - m[h]);
       }
     }
   }
@@ -197,7 +197,7 @@ __device__ __forceinline__ void softmax_row_cta(int64_t row, const int32_t *__re
   for (int h = 0; h < kMaxHeads; ++h) {
     if (h >= heads) break;
     const float mg = group_max<32>(m[h]);
-    const float zl = (m[h] == -INFINITY) ? 0.f : z[h] * expf(m[h] - mg);
+    const float zl = (m[h] == -INFINITY) ? 0.f : z[h] * __expf(m[h] - mg);
     const float zg = group_sum<32>(zl);
     if (lane == 0) red_m[warp][h] = mg, red_z[warp][h] = zg;
   }
@@ -208,9 +208,9 @@ __device__ __forceinline__ void softmax_row_cta(int64_t row, const int32_t *__re
     for (int w = 0; w < kThreads / 32; ++w) mm = fmaxf(mm, red_m[w][h]);
     float zz = 0.f;
     for (int w = 0; w < kThreads / 32; ++w)
-      if (red_m[w][h] != -INFINITY) zz += red_z[w][h] * expf(red_m[w][h] - mm);
+      if (red_m[w][h] != -INFINITY) zz += red_z[w][h] * __expf(red_m[w][h] - mm);
     fin_m[h] = mm;
-    fin_z[h] = zz;
+    fin_z[h] = 1.0f / zz;  // reciprocal: one multiply per edge below
   }
   __syncthreads();
   for (int p = beg + threadIdx.x; p < end; p += kThreads) {
@@ -220,7 +220,7 @@ __device__ __forceinline__ void softmax_row_cta(int64_t row, const int32_t *__re
       if (h >= heads) break;
       const float e = EGIVEN ? alpha[(int64_t)h * nnz + p]
                              : leaky(si[h] + __ldg(t + (int64_t)h * n_rows + j), slope);
-      alpha[(int64_t)h * nnz + p] = expf(e - fin_m[h]) / fin_z[h];
+      alpha[(int64_t)h * nnz + p] = __expf(e - fin_m[h]) * fin_z[h];
     }
   }
 }
@@ -252,38 +252,80 @@ __global__ void __launch_bounds__(kThreads)
     m[h] = -INFINITY;
     z[h] = 0.f;
   }
-  for (int p = beg + gl; p < end; p += LPR) {
-    const int j = EGIVEN ? 0 : __ldg(col_idx + p);
+  // The lane's first CE edges keep their column and head-0 score in
+  // registers (unrolled: no local-memory indexing), so pass 2 re-gathers
+  // nothing for rows of <= CE * LPR edges — the dependent col -> t_j load
+  // pair was the kernel's latency chain.
+  constexpr int CE = 4;
+  int jc[CE];
+  float ec[CE];
+  auto score = [&](int h, int p, int j) {
+    return EGIVEN ? alpha[(int64_t)h * nnz + p]
+                  : leaky(si[h] + __ldg(t + (int64_t)h * n_rows + j), slope);
+  };
+  auto update = [&](int h, float e) {
+    if (e > m[h]) {
+      z[h] = z[h] * __expf(m[h] - e) + 1.0f;
+      m[h] = e;
+    } else {
+      z[h] += __expf(e - m[h]);
+    }
+  };
 #pragma unroll
-    for (int h = 0; h < kMaxHeads; ++h) {
-      if (h >= heads) break;
-      const float e = EGIVEN ? alpha[(int64_t)h * nnz + p]
-                             : leaky(si[h] + __ldg(t + (int64_t)h * n_rows + j), slope);
-      if (e > m[h]) {
-        z[h] = z[h] * expf(m[h] - e) + 1.0f;
-        m[h] = e;
-      } else {
-        z[h] += expf(e - m[h]);
+  for (int k = 0; k < CE; ++k) {
+    const int p = beg + gl + k * LPR;
+    jc[k] = 0;
+    ec[k] = 0.f;
+    if (p < end) {
+      const int j = EGIVEN ? 0 : __ldg(col_idx + p);
+      jc[k] = j;
+#pragma unroll
+      for (int h = 0; h < kMaxHeads; ++h) {
+        if (h >= heads) break;
+        const float e = score(h, p, j);
+        if (h == 0) ec[k] = e;
+        update(h, e);
       }
     }
   }
-#pragma unroll
-  for (int h = 0; h < kMaxHeads; ++h) {
-    if (h >= heads) break;
-    const float mg = group_max<LPR>(m[h]);
-    const float zl = (m[h] == -INFINITY) ? 0.f : z[h] * expf(m[h] - mg);
-    z[h] = group_sum<LPR>(zl);
-    m[h] = mg;
-  }
-  if (!live || end == beg) return;
-  for (int p = beg + gl; p < end; p += LPR) {
+  for (int p = beg + gl + CE * LPR; p < end; p += LPR) {
     const int j = EGIVEN ? 0 : __ldg(col_idx + p);
 #pragma unroll
     for (int h = 0; h < kMaxHeads; ++h) {
       if (h >= heads) break;
-      const float e = EGIVEN ? alpha[(int64_t)h * nnz + p]
-                             : leaky(si[h] + __ldg(t + (int64_t)h * n_rows + j), slope);
-      alpha[(int64_t)h * nnz + p] = expf(e - m[h]) / z[h];
+      update(h, score(h, p, j));
+    }
+  }
+  float inv[kMaxHeads];
+#pragma unroll
+  for (int h = 0; h < kMaxHeads; ++h) {
+    inv[h] = 0.f;
+    if (h >= heads) break;
+    const float mg = group_max<LPR>(m[h]);
+    const float zl = (m[h] == -INFINITY) ? 0.f : z[h] * __expf(m[h] - mg);
+    z[h] = group_sum<LPR>(zl);
+    m[h] = mg;
+    inv[h] = 1.0f / z[h];
+  }
+  if (!live || end == beg) return;
+#pragma unroll
+  for (int k = 0; k < CE; ++k) {
+    const int p = beg + gl + k * LPR;
+    if (p < end) {
+#pragma unroll
+      for (int h = 0; h < kMaxHeads; ++h) {
+        if (h >= heads) break;
+        const float e = h == 0 ? ec[k] : score(h, p, jc[k]);
+        alpha[(int64_t)h * nnz + p] = __expf(e - m[h]) * inv[h];
+      }
+    }
+  }
+  for (int p = beg + gl + CE * LPR; p < end; p += LPR) {
+    const int j = EGIVEN ? 0 : __ldg(col_idx + p);
+#pragma unroll
+    for (int h = 0; h < kMaxHeads; ++h) {
+      if (h >= heads) break;
+      alpha[(int64_t)h * nnz + p] = __expf(score(h, p, j) - m[h]) * inv[h];
     }
   }
 }
