@@ -188,9 +188,9 @@ def main(argv=None):
                     help="sweep: configs[4] uniform/RMAT grid; named: the arxiv/reddit/products shapes")
     pt = sub.add_parser("train")
     pt.add_argument("--records", required=True)
-    pt.add_argument("--trees", type=int, default=150)
-    pt.add_argument("--lr", type=float, default=0.1)
-    pt.add_argument("--depth", type=int, default=4)
+    pt.add_argument("--trees", type=int, default=300)
+    pt.add_argument("--lr", type=float, default=0.05)
+    pt.add_argument("--depth", type=int, default=6)
     pt.add_argument("--report", default=None)
     args = p.parse_args(argv)
     {"profile": cmd_profile, "train": cmd_train}[args.cmd](args)
