@@ -770,12 +770,14 @@ extern "C" int gc_pack_rows_f16(const float *X, int64_t ldx, int64_t n_rows, int
 #define GC_PACK(L, C)                                                                        \
   pack_rows_f16_kernel<L, C><<<(unsigned)blocks, 256, 0, st>>>(X, ldx, n_rows, K, d, xh, ldh, \
                                                               sigma, vec)
+  // (below 32 lanes lpr is the largest power of two <= q, so a lane holds at
+  // most two chunks)
   switch (lpr) {
-    case 1: GC_PACK(1, 1); break;
-    case 2: GC_PACK(2, 1); break;
-    case 4: GC_PACK(4, 1); break;
-    case 8: GC_PACK(8, 1); break;
-    case 16: GC_PACK(16, 1); break;
+    case 1: GC_PACK(1, 2); break;
+    case 2: GC_PACK(2, 2); break;
+    case 4: GC_PACK(4, 2); break;
+    case 8: GC_PACK(8, 2); break;
+    case 16: GC_PACK(16, 2); break;
     default:
       if (chunks <= 2) GC_PACK(32, 2);
       else if (chunks <= 4) GC_PACK(32, 4);
