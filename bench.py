@@ -611,7 +611,7 @@ def main():
                   "dense_split_autotune_s": stats.get("autotune_s"),
                   "dense_split_peak_extra_bytes": stats.get("peak_extra_bytes"),
                   "dense_split_resident_bytes": stats.get("resident_plan_bytes"),
-                  "spmm_variant_autotune_ms": pat._plans.get(("variant", "spmm", K, "times"))})
+                  })
     sel_s = (setup.get("features_s") or 0.0) + setup["select_s"] + (stats.get("autotune_s") or 0.0)
     setup["selection_overhead_iterations"] = round(sel_s / layer_s, 1)
     setup["selection_overhead_note"] = ("(features + selector inference + dense-split autotune) / "
@@ -648,8 +648,10 @@ def main():
         "setup": setup,
     }
     result["clocks"] = clocks.summary()
-    result["spmm_variant"] = {"chosen": pat._plans.get(("variant", "spmm", K)),
-                              "autotune_ms": pat._plans.get(("variant", "spmm", K, "times"))}
+    vmode = "spmmh" if uses_half(gc, pat.n_cols, K) else "spmm"
+    tail_pat = hub.hub_plan(pat, split).tail if split else pat
+    result["spmm_variant"] = {"mode": vmode, "chosen": tail_pat._plans.get(("variant", vmode, K)),
+                              "autotune_ms": tail_pat._plans.get(("variant", vmode, K, "times"))}
 
     if rank == 0 and world == 1:
         parity = Parity(g.a_tilde, args.parity_rows, seed=args.seed)
