@@ -868,7 +868,7 @@ def cora_config(gc, args, dev) -> dict:
     return out
 
 
-def selector_pick(row_comps: dict, model: str, feats, K: int) -> dict:
+def selector_pick(row_comps: dict, model: str, feats, K: int, k2: int | None = None) -> dict:
     """The B200 selector's choice for this group and its time over the
     fastest composition measured (north-star target: <= 1.1)."""
     from paper_2306_15155_b200 import selector
@@ -876,7 +876,7 @@ def selector_pick(row_comps: dict, model: str, feats, K: int) -> dict:
     mdl = selector.load_b200_model(model)
     if mdl is None:
         return {}
-    sel = selector.select(mdl, selector.SelectorInput(features=feats, k1=K, k2=K))
+    sel = selector.select(mdl, selector.SelectorInput(features=feats, k1=K, k2=k2 or K))
     best = min(row_comps, key=lambda c: row_comps[c]["ms"])
     out = {"fastest": best, "selected": sel}
     if sel in row_comps:
@@ -932,7 +932,8 @@ def extra_configs(gc, args, dev, pk) -> dict:
                 row["compositions"][c] = {"ms": round(t[c] * 1e3, 4), "edges_per_s": round(m / t[c], 1),
                                           "parity": par.gat(gc.gat_layer(at, h, s), h, w, a_s, a_d,
                                                             heads, c, tol)}
-            row.update(pick(row["compositions"], "gat", feats, K))
+            # a multi-head layer's output width is heads * k2 (the selector's k2)
+            row.update(pick(row["compositions"], "gat", feats, K, k2=K * heads))
             gat.append(row)
             del h, w, specs
             torch.cuda.empty_cache()

@@ -88,6 +88,8 @@ struct Lanes<false> {
 __device__ __forceinline__ float4 zero_of(float4) { return make_float4(0.f, 0.f, 0.f, 0.f); }
 __device__ __forceinline__ float zero_of(float) { return 0.f; }
 __device__ __forceinline__ void fma_into(float4 &acc, float w, float4 b) {
+  // (packed FFMA2 measured no faster: the operand packing costs the issue
+  // slots it saves — profiles/data/ab_ffma2_r02.json)
   acc.x = fmaf(w, b.x, acc.x);
   acc.y = fmaf(w, b.y, acc.y);
   acc.z = fmaf(w, b.z, acc.z);

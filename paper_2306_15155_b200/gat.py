@@ -229,15 +229,17 @@ def gat_layer_reuse(a_tilde: CsrMatrix, h, spec: GatLayerSpec, *, spmm_fn=None):
     half = _half(hw[:, :k2])
     if spec.attention is AttentionForm.SDDMM:
         if a_tilde.n_rows == a_tilde.n_cols:
-            # fused: the gathered HW_j row gives its score and its aggregated term
-            # (TF32 class: gathered as fp16 rows, the source rows stay fp32)
+            # fused: the gathered HW_j row gives its score and its aggregated term.
+            # fp32 rows even in the TF32 class: the score operands double the
+            # live registers of this mode, and with fp16 rows its occupancy
+            # halves (arxiv K = 256: 0.67 vs 0.43 ms; ncu 22 % warps active,
+            # profiles/r02_ncu_summary.md); gc_gat_sddmm_aggregate_f32 accepts
+            # fp16 rows (GC_SPMM_B_F16) for callers that want the bytes
             a_src, a_dst = spec.attn_src.to(hw.device), spec.attn_dst.to(hw.device)
             done = all(gat_sddmm_aggregate(a_tilde, a_src[i * k2:(i + 1) * k2],
                                            a_dst[i * k2:(i + 1) * k2], spec.leaky_slope,
-                                           pack_rows_f16(hw[:, i * k2:(i + 1) * k2]) if half
-                                           else hw[:, i * k2:(i + 1) * k2], relu=relu,
-                                           out=out[:, i * k2:(i + 1) * k2],
-                                           b_self=hw[:, i * k2:(i + 1) * k2] if half else None)
+                                           hw[:, i * k2:(i + 1) * k2], relu=relu,
+                                           out=out[:, i * k2:(i + 1) * k2])
                        is not None for i in range(H))
             if done:
                 return op.wrap(out)

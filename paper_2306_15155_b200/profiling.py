@@ -230,7 +230,12 @@ def profile(graphs: list[tuple[str, CsrMatrix]], sizes: list[tuple[int, int]], m
                 su = (setup_s if comp.startswith("precompute") else 0.0) + max(first_s - med, 0.0)
                 if not amortize_precompute and su:
                     med += su / reps
-                records.append(ProfileRecord(graph_id=graph_id, model=model, k1=k1, k2=k2,
+                # multi-head GAT: the record's k2 is the layer's output width
+                # heads*k2 (what a selector sees for a multi-head layer), and
+                # the group id carries the head count
+                records.append(ProfileRecord(graph_id=graph_id if heads == 1 else
+                                             f"{graph_id}/h{heads}", model=model, k1=k1,
+                                             k2=k2 * heads,
                                              composition=comp, features=feats, hw_tag=hw_tag,
                                              median_time_s=med, iterations=reps, setup_time_s=su,
                                              cv=cv, unreliable=cv > 0.3, hw_desc=tuple(hw_desc)))

@@ -78,6 +78,14 @@ def cmd_profile(args) -> None:
                 warnings.simplefilter("ignore")
                 recs = profiling.profile([(gid, a)], sizes, model, reps=args.reps,
                                          warmup=args.warmup)
+            if model == "gat" and args.graphs == "named" and args.heads > 1:
+                # multi-head groups (records keyed "<shape>/h<heads>", k2 =
+                # heads * k2): the bench's 4-head GAT configs
+                with warnings.catch_warnings():
+                    warnings.simplefilter("ignore")
+                    recs += profiling.profile([(gid, a)], [(32, 32), (256, 256), (1024, 1024)],
+                                              model, reps=args.reps, warmup=args.warmup,
+                                              heads=args.heads)
             for r in recs:
                 fh.write(json.dumps(r.to_dict()) + "\n")
             fh.flush()
@@ -137,7 +145,7 @@ def cmd_train(args) -> None:
         mine = [r for r in recs if r.model == model_tag and r.composition in comps]
         if not mine:
             continue
-        graphs_ = sorted({r.graph_id for r in mine if r.graph_id not in NAMED})
+        graphs_ = sorted({r.graph_id for r in mine if r.graph_id.split("/")[0] not in NAMED})
         rng = np.random.default_rng(0)
         test_g = set(rng.choice(graphs_, size=max(1, len(graphs_) // 5), replace=False).tolist())
         tr = [r for r in mine if r.graph_id not in test_g]
@@ -153,12 +161,12 @@ def cmd_train(args) -> None:
         # (nor the random held-out graphs); evaluated on every (k1, k2) of it
         lono = {}
         for shape in NAMED:
-            held = [r for r in mine if r.graph_id == shape]
+            held = [r for r in mine if r.graph_id.split("/")[0] == shape]
             if not held:
                 continue
             with warnings.catch_warnings():
                 warnings.simplefilter("ignore")
-                m_s = train([r for r in tr if r.graph_id != shape], model_tag, hyper,
+                m_s = train([r for r in tr if r.graph_id.split("/")[0] != shape], model_tag, hyper,
                             compositions=comps)
             lono[shape] = evaluate(m_s, held, comps, detail=True)
         if lono:
@@ -184,6 +192,10 @@ def main(argv=None):
     pp.add_argument("--reps", type=int, default=3)
     pp.add_argument("--warmup", type=int, default=1)
     pp.add_argument("--quick", action="store_true")
+    pp.add_argument("--heads", type=int, default=1,
+                    help="named graphs: also profile GAT with this many heads (records keyed "
+                         "'<shape>/h<heads>', k2 = heads*k2; kept out of the shipped models: "
+                         "they cost held-out single-head quality, see DESIGN.md §6)")
     pp.add_argument("--graphs", choices=("sweep", "named"), default="sweep",
                     help="sweep: configs[4] uniform/RMAT grid; named: the arxiv/reddit/products shapes")
     pt = sub.add_parser("train")
