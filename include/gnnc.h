@@ -141,6 +141,14 @@ GNNC_API int gc_gat_aggregate_f32(const int32_t *row_ptr, const int32_t *col_idx
  * d_col = sigma then gathers 2 bytes per feature instead of 4. */
 GNNC_API int gc_pack_rows_f16(const float *X, int64_t ldx, int64_t n_rows, int64_t K,
                               const float *d, void *Xh, int64_t ldh, float *sigma, void *stream);
+/* The same with n_proj <= 16 row projections computed from the fp32 rows in
+ * the same pass (the GAT node scores s, t = X a_src, X a_dst of gat.py:110-111,
+ * replacing gc_node_proj_f32 when the rows are packed anyway):
+ * proj_out[p * n_rows + r] = X[r,:] . P[p,:] (P: n_proj x K, 16-byte
+ * aligned; K % 4 == 0). */
+GNNC_API int gc_pack_rows_f16_proj(const float *X, int64_t ldx, int64_t n_rows, int64_t K,
+                                   const float *d, void *Xh, int64_t ldh, float *sigma,
+                                   const float *P, int32_t n_proj, float *proj_out, void *stream);
 
 /* col_tagged[p] = col_idx[p] | (hot[col_idx[p]] ? 1<<31 : 0): a copy of the
  * pattern whose hub columns (hot: uint8 per column) are tagged for

@@ -98,6 +98,8 @@ _SIGNATURES = {
                                          _I64, _I64, _I32, _P, _P, _I64, _P, _U32, _P]),
     "gc_tag_hub_columns": (ctypes.c_int, [_P, _I64, _P, _P, _P]),
     "gc_pack_rows_f16": (ctypes.c_int, [_P, _I64, _I64, _I64, _P, _P, _I64, _P, _P]),
+    "gc_pack_rows_f16_proj": (ctypes.c_int, [_P, _I64, _I64, _I64, _P, _P, _I64, _P, _P, _I32, _P,
+                                             _P]),
 }
 
 

@@ -687,11 +687,15 @@ int dispatch(SpmmArgs &a, int64_t n_rows, int algo, const int32_t *items, int64_
 // lanes idle); each lane keeps its NC float4 chunks in registers between the
 // max and the conversion, so the row is read once (K <= 4·LPR·NC, up to
 // 4096), 8-byte writes.
+// Optional projections (the GAT node scores, fused so the rows are read
+// once): proj_out[p * n + r] = X[r,:] . P[p,:] for p < n_proj, in the same
+// lane order and reduction tree as node_proj_kernel when LPR == 32.
 template <int LPR, int NC>
 __global__ void __launch_bounds__(256)
     pack_rows_f16_kernel(const float *__restrict__ X, int64_t ldx, int64_t n, int64_t K,
                          const float *__restrict__ d, __half *__restrict__ Xh, int64_t ldh,
-                         float *__restrict__ sigma, bool vec) {
+                         float *__restrict__ sigma, bool vec, const float *__restrict__ P = nullptr,
+                         int n_proj = 0, float *__restrict__ proj_out = nullptr) {
   const int gl = threadIdx.x % LPR;
   const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPR;
   const bool live = r < n;
@@ -714,6 +718,17 @@ __global__ void __launch_bounds__(256)
     for (int64_t c = gl; c < K; c += LPR) mx = fmaxf(mx, fabsf(__ldg(x + c)));
   }
   mx = group_max<LPR>(mx);
+  for (int q = 0; q < n_proj; ++q) {  // (vec only; warp-uniform loop)
+    const float *pq = P + (int64_t)q * K;
+    float acc = 0.0f;
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      const int64_t c = 4 * gl + i * step;
+      if (live && c < K) acc = fma4_dot(v[i], ldg_f4(pq + c), acc);
+    }
+    acc = group_sum<LPR>(acc);
+    if (live && gl == 0) proj_out[(int64_t)q * n + r] = acc;
+  }
   if (!live) return;
   // exponent of mx (exact): mx = m * 2^E, m in [1, 2)
   const int E = mx > 0.0f ? ((int)((__float_as_uint(mx) >> 23) & 0xff) - 127) : 0;
@@ -753,15 +768,32 @@ __global__ void tag_hub_kernel(const int32_t *__restrict__ col, int64_t nnz,
 
 using namespace gnnc;
 
+extern "C" int gc_pack_rows_f16_proj(const float *X, int64_t ldx, int64_t n_rows, int64_t K,
+                                     const float *d, void *Xh, int64_t ldh, float *sigma,
+                                     const float *P, int32_t n_proj, float *proj_out,
+                                     void *stream);
+
 extern "C" int gc_pack_rows_f16(const float *X, int64_t ldx, int64_t n_rows, int64_t K,
                                 const float *d, void *Xh, int64_t ldh, float *sigma,
                                 void *stream) {
+  return gc_pack_rows_f16_proj(X, ldx, n_rows, K, d, Xh, ldh, sigma, nullptr, 0, nullptr, stream);
+}
+
+extern "C" int gc_pack_rows_f16_proj(const float *X, int64_t ldx, int64_t n_rows, int64_t K,
+                                     const float *d, void *Xh, int64_t ldh, float *sigma,
+                                     const float *P, int32_t n_proj, float *proj_out,
+                                     void *stream) {
   GC_REQUIRE(n_rows >= 0 && K >= 0 && ldx >= K && ldh >= K, GC_ERR_SHAPE,
              "gc_pack_rows_f16: bad shape");
+  GC_REQUIRE(n_proj >= 0 && n_proj <= 16 && (n_proj == 0 || (P && proj_out)), GC_ERR_VALUE,
+             "gc_pack_rows_f16: projections need P and proj_out, n_proj <= 16");
   if (n_rows == 0) return GC_OK;
   GC_REQUIRE(X && Xh && sigma, GC_ERR_VALUE, "gc_pack_rows_f16: null operand");
   const bool vec = K % 4 == 0 && ldx % 4 == 0 && ldh % 4 == 0 && aligned16(X) &&
                    (reinterpret_cast<uintptr_t>(Xh) & 7u) == 0 && K <= 4096;
+  GC_REQUIRE(n_proj == 0 || (vec && aligned16(P)), GC_ERR_UNSUPPORTED,
+             "gc_pack_rows_f16: projections need the vectorised row layout (K %% 4 == 0, "
+             "16-byte aligned X, P)");
   const int64_t q = vec ? (K + 3) / 4 : K;  // lanes a row could use
   const int lpr = q >= 32 ? 32 : q >= 16 ? 16 : q >= 8 ? 8 : q >= 4 ? 4 : q >= 2 ? 2 : 1;
   const int64_t chunks = vec ? (q + lpr - 1) / lpr : 1;  // float4 chunks per lane
@@ -771,7 +803,7 @@ extern "C" int gc_pack_rows_f16(const float *X, int64_t ldx, int64_t n_rows, int
   cudaStream_t st = as_stream(stream);
 #define GC_PACK(L, C)                                                                        \
   pack_rows_f16_kernel<L, C><<<(unsigned)blocks, 256, 0, st>>>(X, ldx, n_rows, K, d, xh, ldh, \
-                                                              sigma, vec)
+                                                              sigma, vec, P, n_proj, proj_out)
   // (below 32 lanes lpr is the largest power of two <= q, so a lane holds at
   // most two chunks)
   switch (lpr) {

@@ -249,7 +249,16 @@ def gat_layer_reuse(a_tilde: CsrMatrix, h, spec: GatLayerSpec, *, spmm_fn=None):
         return op.wrap(out)
     if a_tilde.n_rows != a_tilde.n_cols:
         raise ShapeError("attention expects a square adjacency")
-    s, t = _projections(hw, spec, spec.attn_src.to(hw.device), spec.attn_dst.to(hw.device), k2, k2)
+    a_src, a_dst = spec.attn_src.to(hw.device), spec.attn_dst.to(hw.device)
+    if half and k2 % 4 == 0:
+        # TF32 class: each head's slice of HW is packed to fp16 rows and its
+        # node scores s, t come out of the same pass (rows read once)
+        for i in range(H):
+            cs = slice(i * k2, (i + 1) * k2)
+            hr, st = pack_rows_f16(hw[:, cs], proj=torch.stack([a_src[cs], a_dst[cs]]))
+            gat_aggregate(a_tilde, st[0], st[1], spec.leaky_slope, hr, relu=relu, out=out[:, cs])
+        return op.wrap(out)
+    s, t = _projections(hw, spec, a_src, a_dst, k2, k2)
     for i in range(H):
         b = hw[:, i * k2:(i + 1) * k2]
         gat_aggregate(a_tilde, s[i], t[i], spec.leaky_slope, pack_rows_f16(b) if half else b,
@@ -279,8 +288,14 @@ def gat_layer_recompute(a_tilde: CsrMatrix, h, spec: GatLayerSpec, *, spmm_fn=No
     if a_tilde.n_rows != a_tilde.n_cols:
         raise ShapeError("attention expects a square adjacency")
     u, v = _folded_attention_vectors(spec)
-    s, t = _projections(op.t, spec, u, v, k1, 0)
-    x = pack_rows_f16(op.t) if _half(op.t) else op.t  # one pack, shared by the heads
+    if _half(op.t) and k1 % 4 == 0 and 2 * H <= 16:
+        # one pack of H shared by the heads, with every head's s, t from the
+        # same pass over the rows
+        x, st = pack_rows_f16(op.t, proj=torch.cat([u.view(H, k1), v.view(H, k1)]))
+        s, t = st[:H], st[H:]
+    else:
+        s, t = _projections(op.t, spec, u, v, k1, 0)
+        x = pack_rows_f16(op.t) if _half(op.t) else op.t  # one pack, shared by the heads
     for i in range(H):
         ah = gat_aggregate(a_tilde, s[i], t[i], spec.leaky_slope, x)
         gemm(ah, spec.weights[:, i * k2:(i + 1) * k2], relu=relu, out=out[:, i * k2:(i + 1) * k2])

@@ -683,10 +683,12 @@ class HalfRows:
         return self.xh.device
 
 
-def pack_rows_f16(x: torch.Tensor, d: torch.Tensor | None = None) -> HalfRows:
+def pack_rows_f16(x: torch.Tensor, d: torch.Tensor | None = None, proj: torch.Tensor | None = None):
     """x (n x K fp32, device) -> HalfRows with d (optional, per row) folded
-    into the scales."""
-    _require_cuda(x, d)
+    into the scales.  ``proj`` (p x K, p <= 16): also return the row
+    projections x @ proj.T as a [p, n] tensor, computed from the fp32 rows in
+    the same pass (the GAT node scores; returns (HalfRows, proj_out))."""
+    _require_cuda(x, d, proj)
     if x.dim() != 2 or x.stride(1) != 1:
         raise ShapeError("pack_rows_f16: x must be a row-major 2-D tensor")
     n, K = x.shape
@@ -695,9 +697,20 @@ def pack_rows_f16(x: torch.Tensor, d: torch.Tensor | None = None) -> HalfRows:
     ldh = (K + 7) // 8 * 8  # 16-byte rows for the gather kernel
     xh = torch.empty(n, ldh, dtype=torch.float16, device=x.device)
     sigma = torch.empty(n, dtype=torch.float32, device=x.device)
-    nat.check(nat.load().gc_pack_rows_f16(x.data_ptr(), _ld(x), n, K, _ptr(d), xh.data_ptr(), ldh,
-                                          sigma.data_ptr(), _stream(x.device)), "pack_rows_f16")
-    return HalfRows(xh, sigma, K)
+    if proj is None:
+        nat.check(nat.load().gc_pack_rows_f16(x.data_ptr(), _ld(x), n, K, _ptr(d), xh.data_ptr(),
+                                              ldh, sigma.data_ptr(), _stream(x.device)),
+                  "pack_rows_f16")
+        return HalfRows(xh, sigma, K)
+    pj = proj.to(torch.float32).contiguous()
+    if pj.dim() != 2 or pj.shape[1] != K or pj.shape[0] > 16:
+        raise ShapeError("pack_rows_f16: proj must be p x K with p <= 16")
+    out = torch.empty(pj.shape[0], n, dtype=torch.float32, device=x.device)
+    nat.check(nat.load().gc_pack_rows_f16_proj(x.data_ptr(), _ld(x), n, K, _ptr(d), xh.data_ptr(),
+                                               ldh, sigma.data_ptr(), pj.data_ptr(), pj.shape[0],
+                                               out.data_ptr(), _stream(x.device)),
+              "pack_rows_f16_proj")
+    return HalfRows(xh, sigma, K), out
 
 
 def _spmm(a: CsrMatrix, b, *, weighted: bool, d_row=None, d_col=None, relu=False, out=None,

@@ -98,6 +98,29 @@ def test_pack_rows_f16_semantics(K):
     assert rel.max() <= 2.0 ** -11
 
 
+@pytest.mark.parametrize("K", [8, 64, 256, 1024])
+@pytest.mark.parametrize("n_proj", [2, 8])
+def test_pack_rows_f16_projections(K, n_proj):
+    """The node scores fused into the pack (gc_pack_rows_f16_proj): the same
+    fp16 rows as the plain pack, projections equal to X @ P^T (float64
+    reference, 1e-6), and bit-identical to node_proj_kernel when the lane
+    layout matches (K a multiple of 128)."""
+    from paper_2306_15155_b200.gat import GatLayerSpec, _projections
+    rng = np.random.default_rng(K + n_proj)
+    x = torch.from_numpy(f32(rng.standard_normal((500, K)))).to(DEV)
+    P = torch.from_numpy(f32(rng.uniform(-0.5, 0.5, (n_proj, K)))).to(DEV)
+    hr, pr = sparse.pack_rows_f16(x, proj=P)
+    plain = sparse.pack_rows_f16(x)
+    assert torch.equal(hr.xh.view(torch.int16), plain.xh.view(torch.int16))
+    assert torch.equal(hr.sigma, plain.sigma)
+    ref = (P.double() @ x.double().T).cpu().numpy()
+    assert np.abs(pr.cpu().numpy() - ref).max() <= 1e-6 * max(1.0, np.abs(ref).max())
+    if K % 128 == 0 and n_proj == 2:
+        spec = GatLayerSpec(K, K, np.zeros((K, K)), P[0].cpu().numpy(), P[1].cpu().numpy())
+        s, t = _projections(x, spec, P[0].contiguous(), P[1].contiguous(), K, K)
+        assert torch.equal(s[0], pr[0]) and torch.equal(t[0], pr[1])
+
+
 @pytest.mark.parametrize("K", [8, 32, 128, 256, 512])
 @pytest.mark.parametrize("algo", ["row", "split"])
 @pytest.mark.parametrize("weighted", [False, True])
