@@ -186,9 +186,13 @@ __device__ __forceinline__ void store_row(const SpmmArgs &a, int row, int slot, 
 // half-width gather operand), half the gathered bytes per edge.
 template <int LPR, int NV, bool VEC, bool HAS_VAL, bool HAS_DCOL, int MODE, bool HINT,
           bool BH = false>
+// (fp32 rows with <= 2 slots: 4 CTAs/SM for the SpMM, 3 for the GAT modes —
+// the round-1 build's occupancy; at their natural 80-100 registers they ran
+// one CTA/SM fewer, the SDDMM-score mode 35 % slower on arxiv; wider rows
+// keep their registers, capping them spills)
 __global__ void __launch_bounds__(kThreads, BH ? (MODE == 2 ? (GNNC_SPMM_BH_MINB + 1) / 2
                                                          : GNNC_SPMM_BH_MINB)
-                                              : GNNC_SPMM_MINB)
+                                              : (NV > 2 ? GNNC_SPMM_MINB : MODE == 0 ? 4 : 3))
     spmm_kernel(const SpmmArgs a) {
   static_assert(!BH || (!HINT && VEC && NV % 2 == 0),
                 "fp16 operand rows: no L1 tags, 16-byte chunks of two slots");
