@@ -112,7 +112,8 @@ STAIR_CANDIDATES_SMALL_K = {128: ((0.018, 1.0), (0.03, 1.0), (0.06, 1.0)),
 def _stair_candidates(K: int):
     """δ candidates for this K, tuned on the two-term format; a dense cell
     costs MMAs in proportion to the term count, so δ scales with it (the
-    one-term format also keeps the two-term table's smallest δ)."""
+    one-term format also keeps the two-term table's two smallest δ: with
+    fp16 tail rows the tail is cheaper, so sparser staircases can win)."""
     cands = STAIR_CANDIDATES
     for k, c in sorted(STAIR_CANDIDATES_SMALL_K.items()):
         if K <= k:
@@ -123,7 +124,7 @@ def _stair_candidates(K: int):
         return cands
     out = [(max(round(dl * f, 3), 0.001), sl) for dl, sl in cands]
     if f < 1.0:
-        out.append(cands[0])
+        out.extend(cands[:2])
     return tuple(dict.fromkeys(out))
 HUB_MIN_NNZ = 1 << 24            # smaller graphs stay on the SpMM alone
 HUB_MEM_BUDGET = 8 << 30         # bytes of dense blocks per pattern
