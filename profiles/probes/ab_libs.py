@@ -3,6 +3,7 @@ and shape, one short bench.py run (no sweep / extras / CPU), reporting the
 step time and the per-kernel CUDA-event times.
 
     python profiles/probes/ab_libs.py --libs a.so,b.so --shapes reddit,products [--k 256]
+    python profiles/probes/ab_libs.py --libs default,env:GNNC_SPMM_STAGED=43
 """
 import argparse
 import json
@@ -25,7 +26,9 @@ for rnd in range(args.rounds):
         for k in args.k.split(","):
             for lib in args.libs.split(","):
                 env = dict(os.environ)
-                if lib != "default":
+                if lib.startswith("env:"):  # env:KEY=VAL+KEY=VAL on the default library
+                    env.update(kv.split("=", 1) for kv in lib[4:].split("+"))
+                elif lib != "default":
                     env["GNNC_LIB_PATH"] = str(Path(lib).resolve())
                 out = f"/tmp/ab_{os.getpid()}.json"
                 cmd = [sys.executable, str(ROOT / "bench.py"), "--shape", shape, "--k", k, "--steps", "20",
