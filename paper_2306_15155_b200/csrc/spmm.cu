@@ -42,6 +42,11 @@ constexpr int kThreads = 256;
 #ifndef GNNC_SPMM_BH_MINB
 #define GNNC_SPMM_BH_MINB 4
 #endif
+// fp16-weight FMA (fma.rn.f32.f16) for batches whose weights are exact in
+// fp16; 0 keeps widen + FFMA everywhere (A/B builds)
+#ifndef GNNC_SPMM_F16W
+#define GNNC_SPMM_F16W 1
+#endif
 #ifndef GNNC_SPMM_BH_U
 #define GNNC_SPMM_BH_U 4
 #endif
@@ -127,6 +132,15 @@ __device__ __forceinline__ void widen_h8(uint4 q, float4 &lo4, float4 &hi4) {
   const float2 a = h2f(q.x), b = h2f(q.y), c = h2f(q.z), d = h2f(q.w);
   lo4 = make_float4(a.x, a.y, b.x, b.y);
   hi4 = make_float4(c.x, c.y, d.x, d.y);
+}
+
+// a0 += w * q.lo, a1 += w * q.hi with w and q's halves fp16, a0/a1 fp32
+// (sm_100 mixed-precision FMA: the fp16 product is exact, one rounding)
+__device__ __forceinline__ void fma_h2(float &a0, float &a1, uint32_t w, uint32_t q) {
+  asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %3;\n\t"
+      "fma.rn.f32.f16 %0, %2, l, %0;\n\tfma.rn.f32.f16 %1, %2, h, %1;\n\t}"
+      : "+f"(a0), "+f"(a1)
+      : "h"((unsigned short)w), "r"(q));
 }
 
 __device__ __forceinline__ float epi1(float v, float ds, float old, uint32_t flags) {
@@ -246,7 +260,12 @@ __global__ void __launch_bounds__(kThreads, BH ? (MODE == 2 ? (GNNC_SPMM_BH_MINB
   for (int v = 0; v < NV; ++v) acc[v] = zero_of(T{});
   constexpr int kSlotStride = LPR * Lanes<VEC>::W;  // floats between a lane's column slots
   constexpr int ESZ = BH ? 2 : 4;  // bytes per operand element
-  const char *bbase = reinterpret_cast<const char *>(a.B) + (int64_t)coff[0] * ESZ;
+  // FLAT (fp16 rows, one group per warp, one 16-byte chunk per lane): lanes
+  // whose columns lie past K gather column 0 instead (never stored), so the
+  // inner loop carries no column predicate
+  constexpr bool FLATC = BH && MODE == 0 && LPR == 32 && NV == 2;
+  const int cbase = (FLATC && !colok[0]) ? 0 : coff[0];
+  const char *bbase = reinterpret_cast<const char *>(a.B) + (int64_t)cbase * ESZ;
   const uint32_t ldb_bytes = (uint32_t)(a.ldb * ESZ);
 
   const int len = end - beg;
@@ -291,6 +310,13 @@ __global__ void __launch_bounds__(kThreads, BH ? (MODE == 2 ? (GNNC_SPMM_BH_MINB
     j2 = ldg_stream_i32(a.col_idx + beg + LPR + gl);
     if (HAS_VAL) v2 = ldg_stream_f32(a.values + beg + LPR + gl);
   }
+  if constexpr (BH && MODE == 0 && LPR == 32) {
+    // unpredicated gathers (FLAT below): lanes past the row's end gather
+    // one of the row's own columns, so no other row's values enter it
+    const int j0 = __shfl_sync(0xffffffffu, j1, 0);
+    if (gl >= len) j1 = j0;
+    if (LPR + gl >= len) j2 = j0;
+  }
   for (int base = 0; base < wmax; base += LPR) {
     const int j = HINT ? (j1 & 0x7FFFFFFF) : j1;  // HINT: bit 31 tags a hub column
     const bool hot = HINT && j1 < 0;
@@ -324,6 +350,19 @@ __global__ void __launch_bounds__(kThreads, BH ? (MODE == 2 ? (GNNC_SPMM_BH_MINB
       dj = mine ? __expf(e - m) : 0.0f;
       zl += dj;
     }
+    // fp16 weights (MODE 0, fp16 rows): when every weight of the batch is
+    // exact in fp16 — unit values times a power-of-two row scale sigma_j —
+    // the FMA takes the fp16 element directly (fma.rn.f32.f16: a product of
+    // two fp16 values is exact in fp32, so the sum is bit-identical to the
+    // widen + FFMA path, one instruction per element instead of two)
+    bool hw = false;
+    uint32_t wh = 0;
+    if constexpr (BH && MODE == 0 && GNNC_SPMM_F16W) {
+      const float w = mine ? v * dj : 0.0f;
+      const __half h = __float2half_rn(w);
+      wh = __half_as_ushort(h);
+      hw = __all_sync(0xffffffffu, __half2float(h) == w);
+    }
     const int cnt = len - base;  // edges left for this group (may be <= 0)
     const int cntw = min(LPR, wmax - base);
 #pragma unroll 1
@@ -333,15 +372,20 @@ __global__ void __launch_bounds__(kThreads, BH ? (MODE == 2 ? (GNNC_SPMM_BH_MINB
         // registers each); each chunk is widened to fp32 where it is used
         // (never all at once: that would double the live registers)
         constexpr int NVH = NV / 2;
+        // one group per warp (MODE 0): past the row's end a lane's column
+        // is a valid stale or zero index and its weight is 0, so the gathers
+        // and FMAs run unpredicated (the adds of w = 0 leave acc unchanged)
+        constexpr bool FLAT = MODE == 0 && LPR == 32;
         uint4 rw[U][NVH];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int je = __shfl_sync(0xffffffffu, j, e0 + u, LPR);
-          const bool ok = (e0 + u) < cnt;
+          const bool ok = FLAT || (e0 + u) < cnt;
           const char *brow_c = bbase + (uint64_t)(uint32_t)je * ldb_bytes;
 #pragma unroll
           for (int c = 0; c < NVH; ++c)
-            if (ok && colok[2 * c]) rw[u][c] = ldg_u4(brow_c + (coff[2 * c] - coff[0]) * ESZ);
+            if (ok && (FLATC || colok[2 * c]))
+              rw[u][c] = ldg_u4(brow_c + (coff[2 * c] - coff[0]) * ESZ);
         }
         if constexpr (SD) {
           float eu[U], su[U];
@@ -384,15 +428,31 @@ __global__ void __launch_bounds__(kThreads, BH ? (MODE == 2 ? (GNNC_SPMM_BH_MINB
               }
             }
           }
+        } else if (MODE == 0 && hw) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const uint32_t we = __shfl_sync(0xffffffffu, wh, e0 + u, LPR);
+            if (FLAT || (e0 + u) < cnt) {
+#pragma unroll
+              for (int c = 0; c < NVH; ++c) {
+                if (FLATC || colok[2 * c]) {
+                  fma_h2(acc[2 * c].x, acc[2 * c].y, we, rw[u][c].x);
+                  fma_h2(acc[2 * c].z, acc[2 * c].w, we, rw[u][c].y);
+                  fma_h2(acc[2 * c + 1].x, acc[2 * c + 1].y, we, rw[u][c].z);
+                  fma_h2(acc[2 * c + 1].z, acc[2 * c + 1].w, we, rw[u][c].w);
+                }
+              }
+            }
+          }
         } else {
           const float w = mine ? v * dj * (SIG ? gsig : 1.0f) : 0.0f;
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const float we = __shfl_sync(0xffffffffu, w, e0 + u, LPR);
-            if ((e0 + u) < cnt) {
+            if (FLAT || (e0 + u) < cnt) {
 #pragma unroll
               for (int c = 0; c < NVH; ++c) {
-                if (colok[2 * c]) {
+                if (FLATC || colok[2 * c]) {
                   float4 lo4, hi4;
                   widen_h8(rw[u][c], lo4, hi4);
                   fma_into(acc[2 * c], we, lo4);

@@ -3,7 +3,7 @@ and shape, one short bench.py run (no sweep / extras / CPU), reporting the
 step time and the per-kernel CUDA-event times.
 
     python profiles/probes/ab_libs.py --libs a.so,b.so --shapes reddit,products [--k 256]
-    python profiles/probes/ab_libs.py --libs default,env:GNNC_SPMM_STAGED=43
+    python profiles/probes/ab_libs.py --libs default,env:GNNC_HUB_SPLIT=stair:8:10
 """
 import argparse
 import json

@@ -121,20 +121,32 @@ def test_pack_rows_f16_projections(K, n_proj):
         assert torch.equal(s[0], pr[0]) and torch.equal(t[0], pr[1])
 
 
-@pytest.mark.parametrize("K", [8, 32, 128, 256, 512])
+@pytest.mark.parametrize("K", [8, 32, 128, 200, 256, 512])
 @pytest.mark.parametrize("algo", ["row", "split"])
 @pytest.mark.parametrize("weighted", [False, True])
-def test_spmm_fp16_operand_bit_exact_to_dequantised(plgraph, K, algo, weighted, monkeypatch):
+@pytest.mark.parametrize("scales", ["d", "pow2", "mixed"])
+def test_spmm_fp16_operand_bit_exact_to_dequantised(plgraph, K, algo, weighted, scales,
+                                                    monkeypatch):
     """GC_SPMM_B_F16: the fp16-row gather computes exactly what the fp32 kernel
     computes on the dequantised rows with d_col = sigma (same order), and
-    plain ReLU / accumulate epilogues."""
+    plain ReLU / accumulate epilogues.  scales "pow2": sigma_j pure powers of
+    two, so unit-valued batches take the fp16-weight FMA (fma.rn.f32.f16);
+    "mixed": some rows scaled out of fp16 range (sigma < 2^-24), so batches
+    switch between the two FMA forms within a row."""
     if algo == "split":
         monkeypatch.setattr(sparse, "SPLIT_CHUNK", 16)
     rng = np.random.default_rng(K + 5)
-    a = plgraph.with_values(torch.from_numpy(f32(rng.uniform(0.5, 2, plgraph.nnz))).to(DEV))
-    x = torch.from_numpy(f32(rng.standard_normal((a.n_cols, K)))).to(DEV)
+    if weighted and scales != "d":
+        vals = np.where(rng.random(plgraph.nnz) < 0.9, 1.0, rng.uniform(0.5, 2, plgraph.nnz))
+    else:
+        vals = rng.uniform(0.5, 2, plgraph.nnz)
+    a = plgraph.with_values(torch.from_numpy(f32(vals)).to(DEV))
+    xn = rng.standard_normal((a.n_cols, K))
+    if scales == "mixed":
+        xn[rng.random(a.n_cols) < 0.3] *= 1e-12
+    x = torch.from_numpy(f32(xn)).to(DEV)
     d = torch.from_numpy(f32(rng.uniform(0.1, 1, a.n_rows))).to(DEV)
-    hr = sparse.pack_rows_f16(x, d)
+    hr = sparse.pack_rows_f16(x, d if scales == "d" else None)
     deq = hr.xh[:, :K].float().contiguous()
     f = gc.spmm if weighted else gc.spmm_unweighted
     got = f(a, hr, d_row=d, relu=True, algo=algo)
