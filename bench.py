@@ -629,8 +629,9 @@ def main():
                    "numerics": ("TF32 class (parity tol 1e-2): fp32 storage and accumulation; the "
                                 "update GEMM rounds its inputs to TF32 and the dense part of the "
                                 "aggregation rounds D*X to one fp16 term (the same 11-bit input "
-                                "rounding); the SpMM tail gathers fp32.  The fp32 class (tol 1e-4) "
-                                "is timed in 'fp32_class'.")
+                                "rounding); the SpMM tail gathers fp16 rows with per-row "
+                                "power-of-two scales (operands above 64 MiB; the same 11-bit "
+                                "rounding).  The fp32 class (tol 1e-4) is timed in 'fp32_class'.")
                    if gc.get_gemm_precision() == "tf32" else
                    "fp32 class: 3xTF32 GEMM, two-term fp16 dense aggregation operand; tol 1e-4",
                    "l2": "inputs larger than L2 (CSR 0.9 GB, H 0.24 GB at K=256); no flush",

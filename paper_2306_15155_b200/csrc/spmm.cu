@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(kThreads, BH ? (MODE == 2 ? (GNNC_SPMM_BH_MINB
   // FLAT (fp16 rows, one group per warp, one 16-byte chunk per lane): lanes
   // whose columns lie past K gather column 0 instead (never stored), so the
   // inner loop carries no column predicate
-  constexpr bool FLATC = BH && MODE == 0 && LPR == 32 && NV == 2;
+  constexpr bool FLATC = BH && MODE != 2 && LPR == 32 && NV == 2;
   const int cbase = (FLATC && !colok[0]) ? 0 : coff[0];
   const char *bbase = reinterpret_cast<const char *>(a.B) + (int64_t)cbase * ESZ;
   const uint32_t ldb_bytes = (uint32_t)(a.ldb * ESZ);
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, BH ? (MODE == 2 ? (GNNC_SPMM_BH_MINB
     j2 = ldg_stream_i32(a.col_idx + beg + LPR + gl);
     if (HAS_VAL) v2 = ldg_stream_f32(a.values + beg + LPR + gl);
   }
-  if constexpr (BH && MODE == 0 && LPR == 32) {
+  if constexpr (BH && MODE != 2 && LPR == 32) {
     // unpredicated gathers (FLAT below): lanes past the row's end gather
     // one of the row's own columns, so no other row's values enter it
     const int j0 = __shfl_sync(0xffffffffu, j1, 0);
@@ -372,10 +372,10 @@ __global__ void __launch_bounds__(kThreads, BH ? (MODE == 2 ? (GNNC_SPMM_BH_MINB
         // registers each); each chunk is widened to fp32 where it is used
         // (never all at once: that would double the live registers)
         constexpr int NVH = NV / 2;
-        // one group per warp (MODE 0): past the row's end a lane's column
-        // is a valid stale or zero index and its weight is 0, so the gathers
-        // and FMAs run unpredicated (the adds of w = 0 leave acc unchanged)
-        constexpr bool FLAT = MODE == 0 && LPR == 32;
+        // one group per warp (SpMM and GAT reassoc): past the row's end a
+        // lane gathers one of the row's own columns with weight 0, so the
+        // gathers and FMAs run unpredicated (adding 0 leaves acc unchanged)
+        constexpr bool FLAT = MODE != 2 && LPR == 32;
         uint4 rw[U][NVH];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -742,11 +742,15 @@ int dispatch(SpmmArgs &a, int64_t n_rows, int algo, const int32_t *items, int64_
   return launch_cfg<32, 4, false, MODE>(a, sr, n_split, st);
 }
 
-// Half-width gather operand (the TF32 class): per row j of X, e_j is chosen
-// so that max_k |X[j,k]| * 2^-e_j lies in [2^14, 2^15) and
-//   Xh[j,k] = fp16_rn(X[j,k] * 2^-e_j),   sigma[j] = (d ? d[j] : 1) * 2^e_j,
+// Half-width gather operand (the TF32 class): with Y[j,:] = d[j] * X[j,:]
+// (fp32; Y = X without d), e_j is chosen so that max_k |Y[j,k]| * 2^-e_j lies
+// in [2^14, 2^15) and
+//   Xh[j,k] = fp16_rn(Y[j,k] * 2^-e_j),   sigma[j] = 2^e_j,
 // so X[j,:] * d[j] = sigma[j] * Xh[j,:] up to the fp16 rounding of each
 // element (11 significant bits — the same input rounding TF32 applies).
+// sigma stays a power of two (d folded into the values, as the GEMM epilogue
+// folds its row scale), so unit-valued SpMM batches weigh their edges in fp16
+// exactly (the fp16-weight FMA of spmm_kernel).
 // A group of LPR lanes per row (LPR = K/4 up to 32: narrow rows do not leave
 // lanes idle); each lane keeps its NC float4 chunks in registers between the
 // max and the conversion, so the row is read once (K <= 4·LPR·NC, up to
@@ -766,6 +770,7 @@ __global__ void __launch_bounds__(256)
   const float *x = X + (live ? r : 0) * ldx;
   float mx = 0.0f;
   const int64_t step = 4 * LPR;
+  const float dr = (d && live) ? __ldg(d + r) : 1.0f;
   float4 v[NC];
 #pragma unroll
   for (int i = 0; i < NC; ++i) v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -775,11 +780,12 @@ __global__ void __launch_bounds__(256)
       const int64_t c = 4 * gl + i * step;
       if (c < K) {
         v[i] = ldg_f4(x + c);
-        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[i].x), fabsf(v[i].y)), fmaxf(fabsf(v[i].z), fabsf(v[i].w))));
+        const float4 y = d ? make_float4(v[i].x * dr, v[i].y * dr, v[i].z * dr, v[i].w * dr) : v[i];
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(y.x), fabsf(y.y)), fmaxf(fabsf(y.z), fabsf(y.w))));
       }
     }
   } else if (live) {
-    for (int64_t c = gl; c < K; c += LPR) mx = fmaxf(mx, fabsf(__ldg(x + c)));
+    for (int64_t c = gl; c < K; c += LPR) mx = fmaxf(mx, fabsf(d ? __ldg(x + c) * dr : __ldg(x + c)));
   }
   mx = group_max<LPR>(mx);
   for (int q = 0; q < n_proj; ++q) {  // (vec only; warp-uniform loop)
@@ -804,8 +810,10 @@ __global__ void __launch_bounds__(256)
     for (int i = 0; i < NC; ++i) {
       const int64_t c = 4 * gl + i * step;
       if (c < K) {
-        const __half2 a = __floats2half2_rn(v[i].x * down, v[i].y * down);
-        const __half2 b = __floats2half2_rn(v[i].z * down, v[i].w * down);
+        float4 y = v[i];
+        if (d) y = make_float4(y.x * dr, y.y * dr, y.z * dr, y.w * dr);
+        const __half2 a = __floats2half2_rn(y.x * down, y.y * down);
+        const __half2 b = __floats2half2_rn(y.z * down, y.w * down);
         uint2 packed;
         packed.x = *reinterpret_cast<const uint32_t *>(&a);
         packed.y = *reinterpret_cast<const uint32_t *>(&b);
@@ -813,9 +821,10 @@ __global__ void __launch_bounds__(256)
       }
     }
   } else {
-    for (int64_t c = gl; c < K; c += LPR) h[c] = __float2half_rn(__ldg(x + c) * down);
+    for (int64_t c = gl; c < K; c += LPR)
+      h[c] = __float2half_rn((d ? __ldg(x + c) * dr : __ldg(x + c)) * down);
   }
-  if (gl == 0) sigma[r] = (d ? __ldg(d + r) : 1.0f) * __uint_as_float((uint32_t)(127 + e) << 23);
+  if (gl == 0) sigma[r] = __uint_as_float((uint32_t)(127 + e) << 23);
 }
 
 __global__ void tag_hub_kernel(const int32_t *__restrict__ col, int64_t nnz,

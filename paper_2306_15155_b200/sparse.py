@@ -684,8 +684,9 @@ class HalfRows:
 
 
 def pack_rows_f16(x: torch.Tensor, d: torch.Tensor | None = None, proj: torch.Tensor | None = None):
-    """x (n x K fp32, device) -> HalfRows with d (optional, per row) folded
-    into the scales.  ``proj`` (p x K, p <= 16): also return the row
+    """x (n x K fp32, device) -> HalfRows of d·x (d optional, per row; folded
+    into the rows before the fp16 rounding, so the row scales sigma are
+    powers of two).  ``proj`` (p x K, p <= 16): also return the row
     projections x @ proj.T as a [p, n] tensor, computed from the fp32 rows in
     the same pass (the GAT node scores; returns (HalfRows, proj_out))."""
     _require_cuda(x, d, proj)

@@ -80,18 +80,20 @@ def test_spmm_weighted_unweighted(oracle, plgraph, K, algo, monkeypatch):
 
 @pytest.mark.parametrize("K", [4, 12, 32, 64, 256, 1024])
 def test_pack_rows_f16_semantics(K):
-    """gc_pack_rows_f16: xh = fp16_rn(x * 2^-e) with max|x_j| * 2^-e in
-    [2^14, 2^15), sigma = d * 2^e (exact), rows of zeros -> sigma = d."""
+    """gc_pack_rows_f16: with y = fp32(d * x), xh = fp16_rn(y * 2^-e) with
+    max|y_j| * 2^-e in [2^14, 2^15) and sigma = 2^e (a power of two, d folded
+    into the values); rows of zeros -> sigma = 1."""
     rng = np.random.default_rng(K)
     x = f32(rng.uniform(-1, 1, (300, K)) * 2.0 ** rng.integers(-30, 30, (300, 1)))
     x[7] = 0
     d = f32(rng.uniform(0.1, 1, 300))
     hr = sparse.pack_rows_f16(torch.from_numpy(x).to(DEV), torch.from_numpy(d).to(DEV))
-    mx = np.abs(x).max(1)
+    y = f32(x * d[:, None])
+    mx = np.abs(y).max(1)
     e = np.where(mx > 0, np.frexp(mx)[1] - 1 - 14, 0)
-    ref_h = (x * np.ldexp(1.0, -e)[:, None]).astype(np.float16)
+    ref_h = (y * np.ldexp(1.0, -e)[:, None]).astype(np.float16)
     assert np.array_equal(hr.xh[:, :K].cpu().numpy(), ref_h)
-    assert np.array_equal(hr.sigma.cpu().numpy(), f32(d * np.ldexp(1.0, e)))
+    assert np.array_equal(hr.sigma.cpu().numpy(), f32(np.ldexp(1.0, e)))
     # dequantised rows carry 11 significant bits
     deq = hr.xh[:, :K].float().cpu().numpy() * hr.sigma.cpu().numpy()[:, None]
     rel = np.abs(deq - x * d[:, None]).max(1) / np.maximum(np.abs(x * d[:, None]).max(1), 1e-30)
