@@ -669,6 +669,7 @@ def main():
             if not args.no_extra:  # GAT on the same Reddit shape (selector check)
                 result["gat_reddit"] = gat_rows_reddit(gc, g.a_tilde, feats, 256, parity,
                                                        tol_of(gc), dev, selector_pick, timed_runs)
+                result["epoch_reddit"] = epoch_row(gc, g, feats, "reddit", parity, tol_of(gc), dev)
         del parity
         if not args.no_extra:
             result["extra_configs"] = extra_configs(gc, args, dev, pk)
@@ -943,6 +944,7 @@ def extra_configs(gc, args, dev, pk) -> dict:
     ga = gc.NormalizedGraph(a_tilde=at, d_inv_sqrt=gc.inv_sqrt_degrees(at)).with_precomputed()
     res["gcn_arxiv"] = {"n": n, "m_tilde": m,
                         "rows": gcn_rows(gc, ga, feats, (32, 256, 1024), par, tol, dev, pick, timed)}
+    res["epoch_arxiv"] = epoch_row(gc, ga, feats, "arxiv", par, tol, dev, with_gat=True)
     del at, par, ga
     torch.cuda.empty_cache()
     # ---- products-shaped: GCN (4 compositions) + GAT -------------------------
@@ -991,9 +993,88 @@ def extra_configs(gc, args, dev, pk) -> dict:
         del h, w
         torch.cuda.empty_cache()
     res["products"] = {"n": n, "m_tilde": m, "rows": rows}
+    res["epoch_products"] = epoch_row(gc, g, feats, "products", par, tol, dev)
     del g, par
     torch.cuda.empty_cache()
     return res
+
+
+# north_star asks for layer AND epoch throughput per named shape.  One epoch
+# here = a full-graph forward pass of a 2-layer model with the dataset's own
+# feature and class widths (input -> 256 -> classes; the reference's own
+# 2-layer model is Cora's 1433 -> 16 -> 7, timed in cora_config), each layer's
+# composition picked by the B200 selector.  Training (backward) is out of
+# scope in the reference itself.
+EPOCH_DIMS = {"reddit": (602, 256, 41), "arxiv": (128, 256, 40), "products": (100, 256, 47)}
+
+
+def _pick(model: str, feats, k1: int, k2: int) -> str:
+    from paper_2306_15155_b200 import selector
+
+    mdl = selector.load_b200_model(model)
+    if mdl is None:
+        return "dynamic:aggregate_first" if model == "gcn" else "reuse:reassoc"
+    return selector.select(mdl, selector.SelectorInput(features=feats, k1=k1, k2=k2))
+
+
+def epoch_row(gc, g, feats, shape: str, par, tol, dev, with_gat: bool = False) -> dict:
+    try:
+        return _epoch_row(gc, g, feats, shape, par, tol, dev, with_gat)
+    except Exception as e:  # noqa: BLE001 — recorded in the line, never silently dropped
+        return {"error": repr(e)[:400]}
+
+
+def _epoch_row(gc, g, feats, shape: str, par, tol, dev, with_gat: bool = False) -> dict:
+    """2-layer GCN (and optionally 1-head GAT) epoch on graph ``g``: ms per
+    epoch (CUDA-event median of 5 after 2 warm-ups), edges/s = 2·m / t,
+    GFLOP/s from the chosen orders, and each layer's row-sampled parity
+    against the oracle given that layer's actual input."""
+    import torch
+
+    k0, k1, k2 = EPOCH_DIMS[shape]
+    n, m = g.a_tilde.n_rows, g.a_tilde.nnz
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(k0 * 1000 + k2)
+    h = torch.rand(n, k0, device=dev, generator=gen) - 0.5
+    ws = [torch.rand(a, b, device=dev, generator=gen) - 0.5 for a, b in ((k0, k1), (k1, k2))]
+    dims = ((k0, k1), (k1, k2))
+    comps = [_pick("gcn", feats, a, b) for a, b in dims]
+    specs = [gc.GcnLayerSpec(a, b, w, composition=c.split(":")[0], order=c.split(":")[1])
+             for (a, b), w, c in zip(dims, ws, comps)]
+    t = _time_layer(lambda: gc.gcn_forward(g, h, specs), 5)
+    y1 = gc.gcn_layer(g, h, specs[0])
+    y2 = gc.gcn_layer(g, y1, specs[1])
+    flops = sum(layer_flops(n, m, a, b, c.split(":")[1]) for (a, b), c in zip(dims, comps))
+    out = {"dims": [k0, k1, k2], "gcn": {
+        "compositions": comps, "ms": round(t * 1e3, 4), "edges_per_s": round(2 * m / t, 1),
+        "gflops": round(flops / t / 1e9, 1),
+        "parity": [par.gcn(y1, h, ws[0], comps[0], tol), par.gcn(y2, y1, ws[1], comps[1], tol)]}}
+    del y1, y2
+    if with_gat:
+        att = [(torch.rand(b, device=dev, generator=gen) - 0.5,
+                torch.rand(b, device=dev, generator=gen) - 0.5) for _, b in dims]
+        gcomps = [_pick("gat", feats, a, b) for a, b in dims]
+        gspecs = [gc.GatLayerSpec(a, b, w, s_, d_, composition=c.split(":")[0],
+                                  attention=c.split(":")[1])
+                  for (a, b), w, (s_, d_), c in zip(dims, ws, att, gcomps)]
+
+        def fwd():
+            x = h
+            for sp in gspecs:
+                x = gc.gat_layer(g.a_tilde, x, sp)
+            return x
+
+        t = _time_layer(fwd, 5)
+        z1 = gc.gat_layer(g.a_tilde, h, gspecs[0])
+        z2 = gc.gat_layer(g.a_tilde, z1, gspecs[1])
+        out["gat"] = {"compositions": gcomps, "ms": round(t * 1e3, 4),
+                      "edges_per_s": round(2 * m / t, 1),
+                      "parity": [par.gat(z1, h, ws[0], *att[0], 1, gcomps[0], tol),
+                                 par.gat(z2, z1, ws[1], *att[1], 1, gcomps[1], tol)]}
+        del z1, z2
+    del h, ws
+    torch.cuda.empty_cache()
+    return out
 
 
 def gcn_rows(gc, g, feats, ks, par, tol, dev, pick, timed) -> list[dict]:

@@ -689,6 +689,10 @@ int dispatch(SpmmArgs &a, int64_t n_rows, int algo, const int32_t *items, int64_
     if (MODE == 2 && K > 512) return launch_cfg<32, 8, true, MODE, true>(a, sr, n_split, sth);
     if (MODE == 2 && K > 256) return launch_cfg<32, 4, true, MODE, true>(a, sr, n_split, sth);
     if (K <= 16) return launch_cfg<2, 2, true, MODE, true>(a, sr, n_split, sth);
+    // column blocks: 16 columns per pass; the grid's y passes launch in order
+    // (x fastest), so each pass's gathers hit an n x 16 slice of B
+    if (MODE != 2 && sh == 3 && K > 32)
+      return launch_cfg<2, 2, true, MODE, true>(a, sr, n_split, sth);
     if (K <= 32) return sh ? launch_cfg<2, 4, true, MODE, true>(a, sr, n_split, sth)
                            : launch_cfg<4, 2, true, MODE, true>(a, sr, n_split, sth);
     if (K <= 64) return sh == 2 ? launch_cfg<2, 8, true, MODE, true>(a, sr, n_split, sth)

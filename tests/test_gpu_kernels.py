@@ -681,6 +681,37 @@ def test_spmm_and_gat_kernel_variants(oracle, plgraph, K, shrink, hints, monkeyp
     assert oracle.rel_err(outg, refg) < 2e-5
 
 
+@pytest.mark.parametrize("K", [64, 128, 256, 512])
+@pytest.mark.parametrize("shrink", ["0", "1", "2", "3"])
+@pytest.mark.parametrize("algo", ["row", "split"])
+def test_fp16_row_kernel_variants(oracle, plgraph, K, shrink, algo, monkeypatch):
+    """Every fp16-row lane-group shape, including the column blocks (3: 16
+    columns per pass), computes the SpMM bit-identically to the fp32 kernel on
+    the dequantised rows, and the GAT reassoc aggregation to 2e-5."""
+    monkeypatch.setattr(sparse, "PLAN_MIN_NNZ", 0)
+    monkeypatch.setattr(sparse, "SPMM_SHRINK", shrink)
+    if algo == "split":
+        monkeypatch.setattr(sparse, "SPLIT_CHUNK", 16)
+    rng = np.random.default_rng(K + int(shrink))
+    n = plgraph.n_rows
+    x = torch.from_numpy(f32(rng.standard_normal((n, K)))).to(DEV)
+    d = torch.from_numpy(f32(rng.uniform(0.1, 1, n))).to(DEV)
+    hr = sparse.pack_rows_f16(x, d)
+    deq = hr.xh[:, :K].float().contiguous()
+    got = gc.spmm_unweighted(plgraph, hr, d_row=d, algo=algo)
+    monkeypatch.setattr(sparse, "SPMM_SHRINK", "0")
+    ref = gc.spmm_unweighted(plgraph, deq, d_row=d, d_col=hr.sigma, algo=algo)
+    assert torch.equal(got, ref)
+    monkeypatch.setattr(sparse, "SPMM_SHRINK", shrink)
+    s, t = f32(rng.standard_normal(n) * 3), f32(rng.standard_normal(n) * 3)
+    out = sparse.gat_aggregate(plgraph, torch.from_numpy(s).to(DEV), torch.from_numpy(t).to(DEV),
+                               0.2, hr, algo=algo)
+    oa = to_oracle(oracle, plgraph)
+    deq64 = hr.xh[:, :K].double().cpu().numpy() * hr.sigma.double().cpu().numpy()[:, None]
+    ref = oracle.spmm(oa.with_values(oracle.edge_softmax(oa, s, t, 0.2)), deq64)
+    assert oracle.rel_err(out.cpu().numpy(), ref) < 2e-5
+
+
 def test_variant_autotune_caches_a_choice(monkeypatch):
     monkeypatch.setattr(sparse, "HUB_AUTOTUNE_MIN_NNZ", 0)
     monkeypatch.setattr(sparse, "PLAN_MIN_NNZ", 0)
