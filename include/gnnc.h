@@ -138,12 +138,14 @@ GNNC_API int gc_gat_aggregate_f32(const int32_t *row_ptr, const int32_t *col_idx
                                   const int32_t *split_rows, int64_t n_split_rows, void *workspace,
                                   size_t ws_bytes, void *stream);
 
-/* Half-width gather operand of the TF32 numerics class: per row j,
- *   Xh[j,:] = fp16_rn(X[j,:] * 2^-e_j)  (max |.| in [2^14, 2^15)),
- *   sigma[j] = (d ? d[j] : 1) * 2^e_j,
+/* Half-width gather operand of the TF32 numerics class: per row j, with
+ * Y[j,:] = fp32(d[j] * X[j,:]) (Y = X when d is NULL),
+ *   Xh[j,:] = fp16_rn(Y[j,:] * 2^-e_j)  (max |.| in [2^14, 2^15)),
+ *   sigma[j] = 2^e_j  (a power of two: d folds into the rows),
  * so sigma[j] * Xh[j,:] = d[j] * X[j,:] to fp16's 11 significant bits (the
  * input rounding TF32 applies).  gc_spmm_f32 with GC_SPMM_B_F16 and
- * d_col = sigma then gathers 2 bytes per feature instead of 4. */
+ * d_col = sigma then gathers 2 bytes per feature instead of 4, and weighs
+ * unit-valued edges in fp16 exactly (sigma in fp16 range). */
 GNNC_API int gc_pack_rows_f16(const float *X, int64_t ldx, int64_t n_rows, int64_t K,
                               const float *d, void *Xh, int64_t ldh, float *sigma, void *stream);
 /* The same with n_proj <= 16 row projections computed from the fp32 rows in

@@ -42,6 +42,19 @@ constexpr int kThreads = 256;
 #ifndef GNNC_SPMM_BH_MINB
 #define GNNC_SPMM_BH_MINB 4
 #endif
+// one 16-byte chunk per lane, one row per warp (LPR = 32, NV = 2, the
+// unpredicated loop): 40 registers, 6 CTAs/SM — the gathers
+// are latency-bound (long-scoreboard stalls), so warps in flight pay:
+// Reddit tail 0.96 -> 0.84 ms, products 6.9 -> 6.0 ms per layer over 4 CTAs
+// (profiles/data/ab_occupancy_r02.json)
+#ifndef GNNC_SPMM_BH_MINB1
+#define GNNC_SPMM_BH_MINB1 6
+#endif
+// (the GAT reassoc aggregation keeps 4: its online-softmax state spills at
+// 40 registers — arxiv K = 256 0.47 vs 0.32 ms)
+#ifndef GNNC_SPMM_BH_MINB1_GAT
+#define GNNC_SPMM_BH_MINB1_GAT 4
+#endif
 // fp16-weight FMA (fma.rn.f32.f16) for batches whose weights are exact in
 // fp16; 0 keeps widen + FFMA everywhere (A/B builds)
 #ifndef GNNC_SPMM_F16W
@@ -205,7 +218,10 @@ template <int LPR, int NV, bool VEC, bool HAS_VAL, bool HAS_DCOL, int MODE, bool
 // one CTA/SM fewer, the SDDMM-score mode 35 % slower on arxiv; wider rows
 // keep their registers, capping them spills)
 __global__ void __launch_bounds__(kThreads, BH ? (MODE == 2 ? (GNNC_SPMM_BH_MINB + 1) / 2
-                                                         : GNNC_SPMM_BH_MINB)
+                                                         : LPR == 32 && NV == 2
+                                                               ? (MODE == 0 ? GNNC_SPMM_BH_MINB1
+                                                                            : GNNC_SPMM_BH_MINB1_GAT)
+                                                               : GNNC_SPMM_BH_MINB)
                                               : (NV > 2 ? GNNC_SPMM_MINB : MODE == 0 ? 4 : 3))
     spmm_kernel(const SpmmArgs a) {
   static_assert(!BH || (!HINT && VEC && NV % 2 == 0),
