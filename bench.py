@@ -574,6 +574,8 @@ def main():
                 "fp16_rows": half,
                 "tail_edges": mt}
         roof.update(_dram_side(traffic, tail_ms, pk, tail_bytes))
+        roof["l2_side"] = l2_lookup(f"{args.shape}/K{K}/{comp}/tail/{hub.spec_label(split)}",
+                                    world, tail_ms)
         cell_flops = 2 * plan.cells * K * hub.term_count()
         useful = 2 * plan.hub_edges * K
         tf = cell_flops / (hub_ms * 1e-3) / 1e12
@@ -699,6 +701,20 @@ def traffic_lookup(key: str, world: int):
         return None
     v = json.loads(tf.read_text()).get(key)
     return v if isinstance(v, int) else None
+
+
+def l2_lookup(key: str, world: int, kernel_ms: float | None):
+    """The L2 side of the dominant kernel (the roof a gather served from L2
+    meets before HBM): bytes through the L2 slices per launch from the ncu
+    --set full capture of the same configuration, the rate they imply at
+    the live kernel time, and ncu's L2 / L1 throughput fractions."""
+    tf = ROOT / "profiles" / "traffic.json"
+    if world != 1 or not tf.exists() or not kernel_ms:
+        return None
+    v = json.loads(tf.read_text()).get(key + "/l2")
+    if not isinstance(v, dict):
+        return None
+    return dict(v, l2_gbs_live=round(v["l2_bytes"] / (kernel_ms * 1e-3) / 1e9, 1))
 
 
 def fp32_class(gc, g, spec, h_dev, w_dev, comp, args, m, parity) -> dict:

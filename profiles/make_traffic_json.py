@@ -73,6 +73,22 @@ def main():
     data = json.loads(out_p.read_text()) if out_p.exists() else {}
     data[key] = int(sum(dram) / len(dram))
     data[key + "/source"] = str(src / "launches.csv")
+    # L2 side of the same kernel from the --set full capture (if present):
+    # bytes through the L2 slices and ncu's L2 / L1 throughput fractions
+    full = src / "spmm_tail_reddit_k256.raw.csv.gz"
+    if full.exists():
+        import gzip
+        rows = list(csv.reader(gzip.open(full, "rt")))
+        hdr, r = rows[0], rows[2]
+        get = lambda k: float(r[hdr.index(k)].replace(",", ""))  # noqa: E731
+        data[key + "/l2"] = {
+            "l2_bytes": int(get("lts__t_sectors.sum") * 32),
+            "lts_throughput_pct": round(get("lts__throughput.avg.pct_of_peak_sustained_elapsed"), 1),
+            "l1tex_throughput_pct": round(get("l1tex__throughput.avg.pct_of_peak_sustained_active"), 1),
+            "l2_hit_pct": round(get("lts__t_sector_hit_rate.pct"), 1),
+            "warps_active_pct": round(get("sm__warps_active.avg.pct_of_peak_sustained_active"), 1),
+            "kernel_us": round(get("gpu__time_duration.sum"), 1),
+            "source": str(full)}
     out_p.write_text(json.dumps(data, indent=1) + "\n")
     print(f"\n{key}: {data[key]} DRAM bytes per launch (mean of {len(dram)})")
 
