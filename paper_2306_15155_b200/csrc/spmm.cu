@@ -50,15 +50,20 @@ constexpr int kThreads = 256;
 #ifndef GNNC_SPMM_BH_MINB1
 #define GNNC_SPMM_BH_MINB1 6
 #endif
-// (the GAT reassoc aggregation keeps 4: its online-softmax state spills at
-// 40 registers — arxiv K = 256 0.47 vs 0.32 ms)
+// (the GAT reassoc aggregation runs 5 CTAs/SM at 47 registers: its
+// online-softmax state spills at 40 — arxiv K = 256 0.47 ms at 6 CTAs,
+// 0.33 at 4, 0.31 at 5; products 8.26 -> 7.72 ms from 4 to 5)
 #ifndef GNNC_SPMM_BH_MINB1_GAT
-#define GNNC_SPMM_BH_MINB1_GAT 4
+#define GNNC_SPMM_BH_MINB1_GAT 5
 #endif
 // fp16-weight FMA (fma.rn.f32.f16) for batches whose weights are exact in
 // fp16; 0 keeps widen + FFMA everywhere (A/B builds)
 #ifndef GNNC_SPMM_F16W
 #define GNNC_SPMM_F16W 1
+#endif
+// unpredicated one-row-per-warp edge loop for fp32 rows too (0: predicated)
+#ifndef GNNC_SPMM_FLAT32
+#define GNNC_SPMM_FLAT32 1
 #endif
 #ifndef GNNC_SPMM_BH_U
 #define GNNC_SPMM_BH_U 4
@@ -326,7 +331,11 @@ __global__ void __launch_bounds__(kThreads, BH ? (MODE == 2 ? (GNNC_SPMM_BH_MINB
     j2 = ldg_stream_i32(a.col_idx + beg + LPR + gl);
     if (HAS_VAL) v2 = ldg_stream_f32(a.values + beg + LPR + gl);
   }
-  if constexpr (BH && MODE != 2 && LPR == 32) {
+  // one row per warp, weights gathered or given (not the unit-weight form,
+  // which adds B rows with weight 1): the edge loop runs unpredicated
+  constexpr bool FLAT = MODE != 2 && LPR == 32 && (BH || HAS_VAL || HAS_DCOL || MODE == 1) &&
+                        (BH || GNNC_SPMM_FLAT32);
+  if constexpr (FLAT) {
     // unpredicated gathers (FLAT below): lanes past the row's end gather
     // one of the row's own columns, so no other row's values enter it
     const int j0 = __shfl_sync(0xffffffffu, j1, 0);
@@ -391,7 +400,6 @@ __global__ void __launch_bounds__(kThreads, BH ? (MODE == 2 ? (GNNC_SPMM_BH_MINB
         // one group per warp (SpMM and GAT reassoc): past the row's end a
         // lane gathers one of the row's own columns with weight 0, so the
         // gathers and FMAs run unpredicated (adding 0 leaves acc unchanged)
-        constexpr bool FLAT = MODE != 2 && LPR == 32;
         uint4 rw[U][NVH];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -484,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, BH ? (MODE == 2 ? (GNNC_SPMM_BH_MINB
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int je = __shfl_sync(0xffffffffu, j, e0 + u, LPR);
-        const bool ok = (e0 + u) < cnt;
+        const bool ok = FLAT || (e0 + u) < cnt;
         const float *brow = reinterpret_cast<const float *>(
             bbase + (uint64_t)(uint32_t)je * ldb_bytes);
         bool hote = false;
@@ -537,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, BH ? (MODE == 2 ? (GNNC_SPMM_BH_MINB
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const float we = UNIT ? 1.0f : __shfl_sync(0xffffffffu, w, e0 + u, LPR);
-          if ((e0 + u) < cnt) {
+          if (FLAT || (e0 + u) < cnt) {
 #pragma unroll
             for (int vv = 0; vv < NV; ++vv)
               if (colok[vv]) fma_into(acc[vv], we, bv[u][vv]);
