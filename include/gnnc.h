@@ -101,6 +101,18 @@ GNNC_API int gc_spmm_f32(const int32_t *row_ptr, const int32_t *col_idx, const f
                 const int32_t *split_rows, int64_t n_split_rows, void *workspace,
                 size_t ws_bytes, void *stream);
 
+/* Aggregate-first layer with the narrow update fused into the SpMM epilogue
+ * (replaces `gemm(spmm(a, h), w)` of reference gcn.py:119-122 /
+ * gcn.py:131-134 for small k2): C = epi(D_row A D_col B) W with W row-major
+ * K1 x K2, K1 % 4 == 0, K1 <= 256, K2 <= 32, B 16-byte aligned (ldb % 4 ==
+ * 0); flags: GC_RELU.  The n x K1 aggregate stays in registers; it is the
+ * SpMM's own sum (same edge order), the product with W an fp32 dot. */
+GNNC_API int gc_spmm_gemm_f32(const int32_t *row_ptr, const int32_t *col_idx,
+                              const float *values, const float *d_row, const float *d_col,
+                              const float *B, int64_t ldb, int64_t n_rows, int64_t n_cols,
+                              int64_t K1, const float *W, int64_t K2, float *C, int64_t ldc,
+                              uint32_t flags, void *stream);
+
 /* Host-side planner for GC_SPMM_NNZ_SPLIT (one pass over a host copy of
  * row_ptr).  Rows with more than `chunk` edges become ceil(deg/chunk)
  * items whose partial sums land in consecutive workspace slots; every other

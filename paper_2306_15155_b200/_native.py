@@ -61,6 +61,8 @@ _SIGNATURES = {
     "gc_device_sm_count": (ctypes.c_int, [ctypes.c_int]),
     "gc_spmm_f32": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _I64, _U32,
                                    ctypes.c_int, _P, _I64, _P, _I64, _P, _SZ, _P]),
+    "gc_spmm_gemm_f32": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _P, _I64,
+                                        _P, _I64, _U32, _P]),
     "gc_spmm_plan_count": (ctypes.c_int, [_P, _I64, _I32, _i64p, _i64p, _i64p]),
     "gc_spmm_plan_fill": (ctypes.c_int, [_P, _I64, _I32, _U32, _P, _P]),
     "gc_spmm_default_chunk": (ctypes.c_int32, [_I64, _I64, _I64, ctypes.c_int]),

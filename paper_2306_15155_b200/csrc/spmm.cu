@@ -966,6 +966,136 @@ extern "C" int gc_spmm_f32(const int32_t *row_ptr, const int32_t *col_idx, const
                          ws_bytes, stream, "gc_spmm_f32");
 }
 
+// ---------------------------------------------------------------------------
+// Aggregate-first layer with a narrow update fused into the epilogue (SURVEY
+// N4, reference gcn.py:119-122 `gemm(spmm(a, h), w)`): C = epi(D_row A D_col
+// B) W for K1 <= 256, K2 <= 32 — the n x K1 aggregate never leaves
+// registers.  One lane group per row (LPR = K1/4 up to 32 lanes, NV float4
+// slots each, one column pass), edges in order (the aggregate is the SpMM's
+// own sum, bit for bit), then per output column c a lane-partial dot with
+// W[:, c] (W^T staged in shared memory, read as float4) and a group sum.
+template <int LPR, int NV>
+__global__ void __launch_bounds__(kThreads)
+    spmm_w_kernel(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ col_idx,
+                  const float *__restrict__ values, const float *__restrict__ d_row,
+                  const float *__restrict__ d_col, const float *__restrict__ B, int64_t ldb,
+                  int K1, const float *__restrict__ W, int K2, float *__restrict__ C,
+                  int64_t ldc, int64_t n_rows, uint32_t flags) {
+  constexpr int U = LPR < 4 ? LPR : 4;
+  constexpr int K1P = LPR * NV * 4;  // padded row width (one pass)
+  extern __shared__ __align__(16) float wt_smem[];  // [K2][K1P]: W^T, zero padded
+  for (int i = threadIdx.x; i < K2 * K1P; i += kThreads) {
+    const int c = i / K1P, k = i % K1P;
+    wt_smem[i] = k < K1 ? __ldg(W + (int64_t)k * K2 + c) : 0.0f;
+  }
+  __syncthreads();
+  const int gl = threadIdx.x % LPR;
+  const int64_t row = ((int64_t)blockIdx.x * kThreads + threadIdx.x) / LPR;
+  const bool live = row < n_rows;
+  int beg = 0, end = 0;
+  if (live) {
+    beg = __ldg(row_ptr + row);
+    end = __ldg(row_ptr + row + 1);
+  }
+  bool colok[NV];
+  int coff[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    coff[v] = v * LPR * 4 + gl * 4;
+    colok[v] = coff[v] < K1;
+  }
+  float4 acc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int len = end - beg;
+  const int wmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)len);
+  for (int base = 0; base < wmax; base += LPR) {
+    int j = 0;
+    float w = 0.0f;  // lanes past the row's end: row 0 with weight 0
+    if (base + gl < len) {
+      j = ldg_stream_i32(col_idx + beg + base + gl);
+      w = values ? ldg_stream_f32(values + beg + base + gl) : 1.0f;
+      if (d_col) w *= __ldg(d_col + j);
+    }
+    const int cntw = min(LPR, wmax - base);
+#pragma unroll 1
+    for (int e0 = 0; e0 < cntw; e0 += U) {
+      float4 bv[U][NV];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int je = __shfl_sync(0xffffffffu, j, e0 + u, LPR);
+        const float *brow = B + (int64_t)je * ldb;
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+          if (colok[v]) bv[u][v] = ldg_f4(brow + coff[v]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float we = __shfl_sync(0xffffffffu, w, e0 + u, LPR);
+        if (base + e0 + u < len) {
+#pragma unroll
+          for (int v = 0; v < NV; ++v)
+            if (colok[v]) fma_into(acc[v], we, bv[u][v]);
+        }
+      }
+    }
+  }
+  const float ds = (live && d_row) ? __ldg(d_row + row) : 1.0f;
+  const float4 *wt4 = reinterpret_cast<const float4 *>(wt_smem);
+  for (int c = 0; c < K2; ++c) {
+    float part = 0.0f;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) part += dot_of(acc[v], wt4[(c * K1P + coff[v]) / 4]);
+    part = group_sum<LPR>(part);
+    if (live && gl == c % LPR) {
+      float o = part * ds;
+      if (flags & GC_RELU) o = fmaxf(o, 0.0f);
+      C[row * ldc + c] = o;
+    }
+  }
+}
+
+template <int LPR, int NV>
+int launch_spmm_w(const int32_t *row_ptr, const int32_t *col_idx, const float *values,
+                  const float *d_row, const float *d_col, const float *B, int64_t ldb, int K1,
+                  const float *W, int K2, float *C, int64_t ldc, int64_t n_rows, uint32_t flags,
+                  cudaStream_t st) {
+  const int smem = K2 * LPR * NV * 4 * (int)sizeof(float);
+  const int64_t groups_per_block = kThreads / LPR;
+  const unsigned grid = (unsigned)((n_rows + groups_per_block - 1) / groups_per_block);
+  spmm_w_kernel<LPR, NV><<<grid, kThreads, smem, st>>>(row_ptr, col_idx, values, d_row, d_col, B,
+                                                       ldb, K1, W, K2, C, ldc, n_rows, flags);
+  return check_launch("spmm_w_kernel");
+}
+
+extern "C" int gc_spmm_gemm_f32(const int32_t *row_ptr, const int32_t *col_idx,
+                                const float *values, const float *d_row, const float *d_col,
+                                const float *B, int64_t ldb, int64_t n_rows, int64_t n_cols,
+                                int64_t K1, const float *W, int64_t K2, float *C, int64_t ldc,
+                                uint32_t flags, void *stream) {
+  GC_REQUIRE(n_rows >= 0 && n_cols >= 0 && K1 >= 0 && K2 >= 0, GC_ERR_SHAPE,
+             "gc_spmm_gemm_f32: negative size");
+  GC_REQUIRE((flags & ~GC_RELU) == 0, GC_ERR_VALUE, "gc_spmm_gemm_f32: unknown flags 0x%x", flags);
+  GC_REQUIRE(K1 % 4 == 0 && K1 <= 256 && K2 <= 32, GC_ERR_UNSUPPORTED,
+             "gc_spmm_gemm_f32: needs K1 %% 4 == 0, K1 <= 256 and K2 <= 32 (K1=%lld, K2=%lld)",
+             (long long)K1, (long long)K2);
+  GC_REQUIRE(ldb >= K1 && ldb % 4 == 0 && ldc >= K2, GC_ERR_SHAPE,
+             "gc_spmm_gemm_f32: ldb must be >= K1 and a multiple of 4, ldc >= K2");
+  if (n_rows == 0 || K2 == 0) return GC_OK;
+  GC_REQUIRE(row_ptr && C && W && (B || n_cols == 0) && aligned16(B), GC_ERR_VALUE,
+             "gc_spmm_gemm_f32: null or misaligned operand");
+  GC_REQUIRE(n_rows < INT32_MAX && n_cols < INT32_MAX, GC_ERR_SHAPE,
+             "gc_spmm_gemm_f32: int32 index range exceeded");
+  cudaStream_t st = as_stream(stream);
+  const int k1 = (int)K1, k2 = (int)K2;
+  if (K1 <= 8) return launch_spmm_w<2, 1>(row_ptr, col_idx, values, d_row, d_col, B, ldb, k1, W, k2, C, ldc, n_rows, flags, st);
+  if (K1 <= 16) return launch_spmm_w<4, 1>(row_ptr, col_idx, values, d_row, d_col, B, ldb, k1, W, k2, C, ldc, n_rows, flags, st);
+  if (K1 <= 32) return launch_spmm_w<8, 1>(row_ptr, col_idx, values, d_row, d_col, B, ldb, k1, W, k2, C, ldc, n_rows, flags, st);
+  if (K1 <= 64) return launch_spmm_w<16, 1>(row_ptr, col_idx, values, d_row, d_col, B, ldb, k1, W, k2, C, ldc, n_rows, flags, st);
+  if (K1 <= 128) return launch_spmm_w<32, 1>(row_ptr, col_idx, values, d_row, d_col, B, ldb, k1, W, k2, C, ldc, n_rows, flags, st);
+  return launch_spmm_w<32, 2>(row_ptr, col_idx, values, d_row, d_col, B, ldb, k1, W, k2, C, ldc, n_rows, flags, st);
+}
+
 extern "C" int gc_gat_sddmm_aggregate_f32(const int32_t *row_ptr, const int32_t *col_idx,
                                           const float *a_src, const float *a_dst, float slope,
                                           const float *B, int64_t ldb, const float *B_self,

@@ -523,6 +523,11 @@ def _as_values(x, dev) -> torch.Tensor:
 
 SPLIT_CHUNK = int(os.environ.get("GNNC_SPLIT_CHUNK", "0"))  # 0: per-launch default
 PLAN_MIN_NNZ = 1 << 16  # below this a row-per-group launch needs no plan
+# fused aggregate-then-update (spmm_gemm) for narrow updates on graphs small
+# enough that the plain lane-group SpMM needs no nnz-split plan (GNNC_SPMM_GEMM=0
+# keeps the two-kernel form)
+SPMM_GEMM = os.environ.get("GNNC_SPMM_GEMM", "1") != "0"
+SPMM_GEMM_MAX_DEG = 1024  # one lane group per row: no heavy-row splitting
 # L1 policy tags on hub columns: "0" off, "1" on, "auto" (default): measured
 # once per (pattern, K) on the first large launch and cached — the tags win on
 # graphs whose hubs fit L1 (arxiv-like) and lose where L2 reuse already
@@ -867,6 +872,39 @@ def spmm_unweighted(a: CsrMatrix, b, **kw):
     """SpMM over the pattern only; ``a.values`` is never read (sparse.py:250-264).
     Bit-identical to ``spmm`` with unit values (same per-row order)."""
     return _spmm(a, b, weighted=False, what="spmm_unweighted", **kw)
+
+
+def spmm_gemm(a: CsrMatrix, b: torch.Tensor, w: torch.Tensor, *, weighted: bool = True,
+              d_row=None, d_col=None, relu: bool = False) -> torch.Tensor:
+    """epi(D_row A D_col B) W in one kernel (gc_spmm_gemm_f32): the
+    aggregate-first layer's update fused into the SpMM epilogue for a narrow
+    W (K1 <= 256, K1 % 4 == 0, K2 <= 32) — reference gcn.py:119-122's
+    ``gemm(spmm(a, h), w)`` without the n x K1 round trip.  ``weighted``:
+    read ``a.values`` (else unit weights)."""
+    _require_cuda(a.col_idx, b, w, d_row, d_col)
+    if b.dim() != 2 or b.shape[0] != a.n_cols or b.stride(1) != 1:
+        raise ShapeError("spmm_gemm: b must be a row-major n_cols x K1 tensor")
+    K1, K2 = b.shape[1], w.shape[1]
+    if tuple(w.shape) != (K1, K2):
+        raise ShapeError(f"spmm_gemm: w must be {K1} x k2")
+    wt = w.to(torch.float32).contiguous()
+    out = torch.empty(a.n_rows, K2, dtype=torch.float32, device=b.device)
+    nat.check(nat.load().gc_spmm_gemm_f32(
+        a.row_ptr.data_ptr(), a.col_idx.data_ptr(), _ptr(a.values) if weighted else None,
+        _ptr(d_row), _ptr(d_col), b.data_ptr(), _ld(b), a.n_rows, a.n_cols, K1, wt.data_ptr(), K2,
+        out.data_ptr(), K2, nat.GC_RELU if relu else 0, _stream(b.device)), "spmm_gemm")
+    return out
+
+
+def spmm_gemm_eligible(a: CsrMatrix, b, k2: int) -> bool:
+    """Shapes the fused aggregate-then-update kernel takes: fp32 rows
+    (K1 <= 256, K1 % 4 == 0, 16-byte rows), k2 <= 32, and rows short enough
+    for one lane group each (max degree <= SPMM_GEMM_MAX_DEG: the kernel has
+    no heavy-row splitting; power-law graphs keep the two-kernel form)."""
+    return (SPMM_GEMM and isinstance(b, torch.Tensor) and b.is_cuda and b.dim() == 2
+            and b.dtype == torch.float32 and b.stride(1) == 1 and b.shape[1] % 4 == 0
+            and _ld(b) % 4 == 0 and b.data_ptr() % 16 == 0 and 0 < b.shape[1] <= 256
+            and 0 < k2 <= 32 and a.max_degree() <= SPMM_GEMM_MAX_DEG)
 
 
 # ---------------------------------------------------------------------------

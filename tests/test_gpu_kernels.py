@@ -1156,3 +1156,80 @@ def test_full_size_normalisation_sddmm_exact(shape):
     vals = nt.values if hasattr(nt, "values") else nt
     ref = d[a.row_of_nnz()] * d[a.col_idx.long()]
     assert torch.equal(vals, ref)
+
+
+# ---- aggregate-first layer with W fused into the SpMM epilogue --
+
+
+@pytest.mark.parametrize("K1", [4, 8, 16, 32, 64, 128, 200, 256])
+@pytest.mark.parametrize("K2", [1, 7, 16, 32])
+@pytest.mark.parametrize("weighted", [False, True])
+def test_spmm_gemm_matches_oracle(oracle, K1, K2, weighted):
+    """gc_spmm_gemm_f32 = relu(D_row A D_col B) W (reference gcn.py:119-122
+    `gemm(spmm(a, h), w)`) to fp32 accuracy, including empty rows."""
+    rng = np.random.default_rng(K1 * 100 + K2)
+    a = rand_csr(rng, 300, 280, 0.04, unit=not weighted, empty_rows=(0, 17, 299))
+    oa = to_oracle(oracle, a)
+    b = f32(rng.standard_normal((280, K1)))
+    w = f32(rng.standard_normal((K1, K2)))
+    dr, dc = f32(rng.uniform(0.1, 1, 300)), f32(rng.uniform(0.1, 1, 280))
+    t = lambda x: torch.from_numpy(x).to(DEV)  # noqa: E731
+    out = sparse.spmm_gemm(a, t(b), t(w), weighted=weighted, d_row=t(dr), d_col=t(dc),
+                           relu=True).cpu().numpy()
+    agg = oracle.spmm(oa, oracle.scale_rows(dc, b)) if weighted else \
+        oracle.spmm_unweighted(oa, oracle.scale_rows(dc, b))
+    ref = np.maximum(oracle.gemm(oracle.scale_rows(dr, agg), w), 0)
+    assert oracle.rel_err(out, ref) < 1e-5
+    assert np.all(out[[0, 17, 299]] == 0)
+    plain = sparse.spmm_gemm(a, t(b), t(w), weighted=weighted).cpu().numpy()
+    ref_plain = oracle.gemm(oracle.spmm(oa, b) if weighted else oracle.spmm_unweighted(oa, b), w)
+    assert oracle.rel_err(plain, ref_plain) < 1e-5
+
+
+def test_spmm_gemm_rejects_unsupported_shapes():
+    rng = np.random.default_rng(1)
+    a = rand_csr(rng, 20, 20, 0.2)
+    b = torch.rand(20, 6, device=DEV)
+    from paper_2306_15155_b200._native import NativeError
+
+    with pytest.raises(NativeError):
+        sparse.spmm_gemm(a, b, torch.rand(6, 4, device=DEV))  # K1 % 4 != 0
+    b = torch.rand(20, 8, device=DEV)
+    with pytest.raises(NativeError):
+        sparse.spmm_gemm(a, b, torch.rand(8, 33, device=DEV))  # K2 > 32
+    with pytest.raises(gc.ShapeError):
+        sparse.spmm_gemm(a, b, torch.rand(7, 4, device=DEV))
+
+
+@pytest.mark.parametrize("comp", ["precompute", "dynamic"])
+@pytest.mark.parametrize("k1,k2", [(16, 7), (64, 32), (128, 16), (256, 8)])
+def test_gcn_aggregate_first_fused_update(oracle, comp, k1, k2, monkeypatch):
+    """The aggregate-first layer takes the fused kernel on a bounded-degree
+    graph (no nnz-split plan) and matches the oracle layer and the two-kernel
+    form; the fp32 class to 1e-4."""
+    gc.set_gemm_precision("fp32")
+    try:
+        A = graphs.synthetic_graph("uniform", 3000, 24000, seed=k1 + k2, device=DEV)
+        g = gc.NormalizedGraph.from_adjacency(A).with_precomputed()
+        assert sparse.spmm_gemm_eligible(g.a_tilde, torch.empty(1, k1, device=DEV), k2)
+        rng = np.random.default_rng(k1 + k2)
+        h = f32(rng.uniform(-0.5, 0.5, (g.a_tilde.n_rows, k1)))
+        w = f32(rng.uniform(-0.5, 0.5, (k1, k2)))
+        spec = gc.GcnLayerSpec(k1, k2, w, composition=comp, order="aggregate_first")
+        calls = []
+        from paper_2306_15155_b200 import gcn as gcn_mod
+
+        real = sparse.spmm_gemm
+        monkeypatch.setattr(gcn_mod, "spmm_gemm", lambda *a, **k: calls.append(1) or real(*a, **k))
+        fused = gc.gcn_layer(g, torch.from_numpy(h).to(DEV), spec).cpu().numpy()
+        assert calls, "the fused kernel did not run"
+        host = g.a_tilde.numpy()
+        at = oracle.Csr(g.a_tilde.n_rows, g.a_tilde.n_cols, *host)
+        og = oracle.GcnGraph(at, oracle.inv_sqrt_degrees(at))
+        ref = oracle.gcn_layer(og, h, w, comp, "aggregate_first")
+        assert oracle.rel_err(fused, ref) < 1e-4
+        monkeypatch.setattr(sparse, "SPMM_GEMM", False)
+        two = gc.gcn_layer(g, torch.from_numpy(h).to(DEV), spec).cpu().numpy()
+        assert oracle.rel_err(fused, two) < 1e-5
+    finally:
+        gc.set_gemm_precision("tf32")
