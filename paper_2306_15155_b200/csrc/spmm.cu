@@ -61,10 +61,6 @@ constexpr int kThreads = 256;
 #ifndef GNNC_SPMM_F16W
 #define GNNC_SPMM_F16W 1
 #endif
-// unpredicated one-row-per-warp edge loop for fp32 rows too (0: predicated)
-#ifndef GNNC_SPMM_FLAT32
-#define GNNC_SPMM_FLAT32 1
-#endif
 #ifndef GNNC_SPMM_BH_U
 #define GNNC_SPMM_BH_U 4
 #endif
@@ -331,10 +327,10 @@ __global__ void __launch_bounds__(kThreads, BH ? (MODE == 2 ? (GNNC_SPMM_BH_MINB
     j2 = ldg_stream_i32(a.col_idx + beg + LPR + gl);
     if (HAS_VAL) v2 = ldg_stream_f32(a.values + beg + LPR + gl);
   }
-  // one row per warp, weights gathered or given (not the unit-weight form,
-  // which adds B rows with weight 1): the edge loop runs unpredicated
-  constexpr bool FLAT = MODE != 2 && LPR == 32 && (BH || HAS_VAL || HAS_DCOL || MODE == 1) &&
-                        (BH || GNNC_SPMM_FLAT32);
+  // fp16 rows, one row per warp: the edge loop runs unpredicated
+  // (fp32 rows measured ~1 % slower unpredicated — the fp32 class at Reddit
+  // K = 256, 2.70 vs 2.68 ms — so they keep the predicated loop)
+  constexpr bool FLAT = BH && MODE != 2 && LPR == 32;
   if constexpr (FLAT) {
     // unpredicated gathers (FLAT below): lanes past the row's end gather
     // one of the row's own columns, so no other row's values enter it
