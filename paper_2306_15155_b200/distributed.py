@@ -228,6 +228,44 @@ def all_gather_half(hr: HalfRows, part: RowPartition, group=None, async_op=False
     return out, work, finish
 
 
+def all_gather_half_multi(hrs: list, extra: torch.Tensor | None, part: RowPartition, group=None):
+    """All-gather several fp16 row operands (e.g. one per GAT head, each with
+    its own row scales) plus ``extra`` fp32 columns (the GAT target scores
+    t) in ONE collective.  Row layout in halves: each operand's ldh halves,
+    then the scales and the extra columns as fp32 bit patterns, padded to a
+    multiple of 8 halves (16 bytes).  Returns (list of HalfRows over the
+    gather buffer, extra_full [world*max_rows, E] fp32)."""
+    dev = hrs[0].xh.device
+    offs, o = [], 0
+    for hr in hrs:
+        offs.append(o)
+        o += hr.xh.shape[1]
+    n_sc = len(hrs)
+    E = 0 if extra is None else extra.shape[1]
+    tail = (2 * (n_sc + E) + 7) // 8 * 8
+    w = o + tail
+    send, full = part.gather_buffers(w, torch.float16, dev, tag=f"halfm{len(hrs)}")
+    rows = hrs[0].xh.shape[0]
+    if rows:
+        for hr, off in zip(hrs, offs):
+            send[:rows, off:off + hr.xh.shape[1]].copy_(hr.xh)
+        scal = torch.stack([hr.sigma for hr in hrs], 1)
+        if E:
+            scal = torch.cat([scal, extra.to(torch.float32)], 1)
+        send[:rows, o:o + 2 * (n_sc + E)].copy_(scal.contiguous().view(torch.float16))
+    dist.all_gather_into_tensor(full, send, group=group)
+    scal_full = full[:, o:o + 2 * (n_sc + E)].contiguous().view(torch.float32)
+    outs = [HalfRows(full[:, off:off + hr.xh.shape[1]], scal_full[:, i].contiguous(), hr.K)
+            for i, (hr, off) in enumerate(zip(hrs, offs))]
+    return outs, (scal_full[:, n_sc:].contiguous() if E else None)
+
+
+def _empty_half(k: int, dev) -> HalfRows:
+    ldh = (k + 7) // 8 * 8
+    return HalfRows(torch.zeros(0, ldh, dtype=torch.float16, device=dev),
+                    torch.zeros(0, dtype=torch.float32, device=dev), k)
+
+
 def all_gather_rows(x_local: torch.Tensor, part: RowPartition, group=None) -> torch.Tensor:
     """Assemble the full n x k operand from every rank's row block (padded
     all_gather_into_tensor, then the padding is dropped).  Returns a fresh
@@ -472,6 +510,20 @@ def dist_gat_layer(part: RowPartition, h_local: torch.Tensor, spec, *, ops=CudaO
                                         relu=relu, out=out[:, cs])
             return out
         s, t = ops.node_scores(hw, a_src, a_dst, H, k2, k2)
+        if ops is CudaOps and k2 % 8 == 0 and _half_gathered(part, H * k2, hw):
+            # TF32 class: per-head fp16 rows + scales and t in one collective
+            hrs = [pack_rows_f16(hw[:, i * k2:(i + 1) * k2]) if part.rows else
+                   _empty_half(k2, dev) for i in range(H)]
+            full_h, t_full = all_gather_half_multi(hrs, t.t() if part.rows else
+                                                   torch.zeros(0, H, device=dev), part, group)
+            if part.rows == 0:
+                return out
+            t_full = t_full.t().contiguous()
+            for i in range(H):
+                cs = slice(i * k2, (i + 1) * k2)
+                ops.gat_aggregate(pat, s[i], t_full[i], slope, full_h[i], relu=relu,
+                                  out=out[:, cs])
+            return out
         wid = H * k2
         full, _ = all_gather_padded(torch.cat([hw, t.t(), hw.new_zeros(hw.shape[0], _pad4(H) - H)],
                                               1), part, group, tag="gat")
@@ -507,6 +559,18 @@ def dist_gat_layer(part: RowPartition, h_local: torch.Tensor, spec, *, ops=CudaO
         u = torch.cat([x[:, 0] for x in uv]).contiguous()
         v = torch.cat([x[:, 1] for x in uv]).contiguous()
     s, t = ops.node_scores(h_local, u, v, H, k1, 0)
+    if ops is CudaOps and _half_gathered(part, k1, h_local):
+        # TF32 class: fp16 rows of H + scales and t in one collective
+        hr = pack_rows_f16(h_local) if part.rows else _empty_half(k1, dev)
+        full_h, t_full = all_gather_half_multi([hr], t.t() if part.rows else
+                                               torch.zeros(0, H, device=dev), part, group)
+        if part.rows == 0:
+            return out
+        t_full = t_full.t().contiguous()
+        for i in range(H):
+            ah = ops.gat_aggregate(pat, s[i], t_full[i], slope, full_h[0], relu=False)
+            ops.gemm(ah, w[:, i * k2:(i + 1) * k2], relu=relu, out=out[:, i * k2:(i + 1) * k2])
+        return out
     full, _ = all_gather_padded(torch.cat([h_local, t.t(), h_local.new_zeros(h_local.shape[0],
                                                                              _pad4(k1 + H) - k1 - H)],
                                           1), part, group, tag="gat")

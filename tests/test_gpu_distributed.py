@@ -85,7 +85,7 @@ def test_partitioned_layer_with_hub_split_on_gpu(oracle, comp, order, overlap):
     _ = gc
 
 
-def _gat_worker(rank, world, port, comp, att, heads, q):
+def _gat_worker(rank, world, port, comp, att, heads, q, half=False):
     import sys
     from pathlib import Path
 
@@ -108,13 +108,20 @@ def _gat_worker(rank, world, port, comp, att, heads, q):
         w = rng.uniform(-0.5, 0.5, (k1, k2 * heads)).astype(np.float32)
         a_s = rng.uniform(-0.5, 0.5, k2 * heads).astype(np.float32)
         a_d = rng.uniform(-0.5, 0.5, k2 * heads).astype(np.float32)
-        gc.set_gemm_precision("fp32")
+        from paper_2306_15155_b200 import distributed, gcn
+
+        used = []
+        if half:  # TF32 class with fp16 gathers at test size
+            gcn.HALF_MIN_BYTES = 0
+            real = distributed.all_gather_half_multi
+            distributed.all_gather_half_multi = lambda *a, **k: used.append(1) or real(*a, **k)
+        gc.set_gemm_precision("tf32" if half else "fp32")
         spec = gc.GatLayerSpec(k1, k2, w, a_s, a_d, composition=comp, attention=att, heads=heads)
         part = RowPartition.of(at, rank, world)
         out = dist_gat_layer(part, h[part.lo:part.hi], spec)
         full = all_gather_rows(out.cpu(), part)
         if rank == 0:
-            q.put(full.numpy())
+            q.put((full.numpy(), bool(used)) if half else full.numpy())
     finally:
         dist.destroy_process_group()
 
@@ -149,6 +156,38 @@ def test_partitioned_gat_layer_on_gpu(oracle, comp, att, heads):
     a_d = rng.uniform(-0.5, 0.5, k2 * heads).astype(np.float32).astype(np.float64)
     ref = oracle.gat_layer_multihead(at, h, w, a_s, a_d, heads, 0.2, comp, "relu")
     assert oracle.rel_err(full, ref) <= 1e-4
+
+
+@pytest.mark.parametrize("comp", ["reuse", "recompute"])
+@pytest.mark.parametrize("heads", [1, 4])
+def test_partitioned_gat_layer_fp16_gather_on_gpu(oracle, comp, heads):
+    """TF32 class: the reassoc GAT partition all-gathers fp16 rows (one set of
+    row scales per head) and t in one collective; against the oracle at the
+    class's tolerance."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gat_worker, args=(r, 2, port, comp, "reassoc", heads, q, True))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    full, used = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert used, "the fp16 all-gather did not run"
+    from paper_2306_15155_b200 import graphs
+
+    rp, ci, v = graphs.powerlaw_graph(3000, 30, seed=12, device="cuda").numpy()
+    at = oracle.add_self_loops(oracle.Csr(3000, 3000, rp, ci, v))
+    rng = np.random.default_rng(21)
+    k1, k2 = 48, 32
+    h = rng.uniform(-0.5, 0.5, (3000, k1)).astype(np.float32).astype(np.float64)
+    w = rng.uniform(-0.5, 0.5, (k1, k2 * heads)).astype(np.float32).astype(np.float64)
+    a_s = rng.uniform(-0.5, 0.5, k2 * heads).astype(np.float32).astype(np.float64)
+    a_d = rng.uniform(-0.5, 0.5, k2 * heads).astype(np.float32).astype(np.float64)
+    ref = oracle.gat_layer_multihead(at, h, w, a_s, a_d, heads, 0.2, comp, "relu")
+    assert oracle.rel_err(full, ref) <= 5e-3
 
 
 def _half_worker(rank, world, port, comp, order, overlap, q):
