@@ -57,12 +57,7 @@ extern "C" {
                                    with L1::no_allocate (SpMM / GAT aggregation only) */
 #define GC_SPMM_SHRINK(s) ((uint32_t)(s) << 8) /* SpMM/GAT lane-group variant s in {0,1,2}:
                                                  (K/4 >> s) lanes per row, each owning 4<<s
-                                                 columns; more rows per warp for short rows.
-                                                 s = 3 (fp16 rows, SpMM and GAT reassoc,
-                                                 K > 32): column blocks — 2 lanes x 8
-                                                 columns per row, K/16 passes run one after
-                                                 another over all rows, each gathering from
-                                                 an n x 16 slice of B (L2-sized) */
+                                                 columns; more rows per warp for short rows */
 #define GC_SPMM_SHRINK_MASK (3u << 8)
 #define GC_SPMM_B_F16 (1u << 10) /* gc_spmm_f32: B holds fp16 rows (ldb in elements; K % 4 == 0,
                                   * ldb % 4 == 0, 8-byte aligned), see gc_pack_rows_f16 */

@@ -709,10 +709,6 @@ int dispatch(SpmmArgs &a, int64_t n_rows, int algo, const int32_t *items, int64_
     if (MODE == 2 && K > 512) return launch_cfg<32, 8, true, MODE, true>(a, sr, n_split, sth);
     if (MODE == 2 && K > 256) return launch_cfg<32, 4, true, MODE, true>(a, sr, n_split, sth);
     if (K <= 16) return launch_cfg<2, 2, true, MODE, true>(a, sr, n_split, sth);
-    // column blocks: 16 columns per pass; the grid's y passes launch in order
-    // (x fastest), so each pass's gathers hit an n x 16 slice of B
-    if (MODE != 2 && sh == 3 && K > 32)
-      return launch_cfg<2, 2, true, MODE, true>(a, sr, n_split, sth);
     if (K <= 32) return sh ? launch_cfg<2, 4, true, MODE, true>(a, sr, n_split, sth)
                            : launch_cfg<4, 2, true, MODE, true>(a, sr, n_split, sth);
     if (K <= 64) return sh == 2 ? launch_cfg<2, 8, true, MODE, true>(a, sr, n_split, sth)
@@ -986,13 +982,6 @@ __global__ void __launch_bounds__(kThreads)
   }
   __syncthreads();
   const int gl = threadIdx.x % LPR;
-  const int64_t row = ((int64_t)blockIdx.x * kThreads + threadIdx.x) / LPR;
-  const bool live = row < n_rows;
-  int beg = 0, end = 0;
-  if (live) {
-    beg = __ldg(row_ptr + row);
-    end = __ldg(row_ptr + row + 1);
-  }
   bool colok[NV];
   int coff[NV];
 #pragma unroll
@@ -1000,53 +989,65 @@ __global__ void __launch_bounds__(kThreads)
     coff[v] = v * LPR * 4 + gl * 4;
     colok[v] = coff[v] < K1;
   }
-  float4 acc[NV];
-#pragma unroll
-  for (int v = 0; v < NV; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-  const int len = end - beg;
-  const int wmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)len);
-  for (int base = 0; base < wmax; base += LPR) {
-    int j = 0;
-    float w = 0.0f;  // lanes past the row's end: row 0 with weight 0
-    if (base + gl < len) {
-      j = ldg_stream_i32(col_idx + beg + base + gl);
-      w = values ? ldg_stream_f32(values + beg + base + gl) : 1.0f;
-      if (d_col) w *= __ldg(d_col + j);
+  const float4 *wt4 = reinterpret_cast<const float4 *>(wt_smem);
+  // grid-stride over row groups: W^T is staged once per CTA
+  for (int64_t row = ((int64_t)blockIdx.x * kThreads + threadIdx.x) / LPR; ;
+       row += (int64_t)gridDim.x * (kThreads / LPR)) {
+    const int64_t first = row - (int64_t)(threadIdx.x / LPR);  // warp-uniform exit test
+    if (__shfl_sync(0xffffffffu, (int)(first >= n_rows), 0)) break;
+    const bool live = row < n_rows;
+    int beg = 0, end = 0;
+    if (live) {
+      beg = __ldg(row_ptr + row);
+      end = __ldg(row_ptr + row + 1);
     }
-    const int cntw = min(LPR, wmax - base);
-#pragma unroll 1
-    for (int e0 = 0; e0 < cntw; e0 += U) {
-      float4 bv[U][NV];
+    float4 acc[NV];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int je = __shfl_sync(0xffffffffu, j, e0 + u, LPR);
-        const float *brow = B + (int64_t)je * ldb;
-#pragma unroll
-        for (int v = 0; v < NV; ++v)
-          if (colok[v]) bv[u][v] = ldg_f4(brow + coff[v]);
+    for (int v = 0; v < NV; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int len = end - beg;
+    const int wmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)len);
+    for (int base = 0; base < wmax; base += LPR) {
+      int j = 0;
+      float w = 0.0f;  // lanes past the row's end: row 0 with weight 0
+      if (base + gl < len) {
+        j = ldg_stream_i32(col_idx + beg + base + gl);
+        w = values ? ldg_stream_f32(values + beg + base + gl) : 1.0f;
+        if (d_col) w *= __ldg(d_col + j);
       }
+      const int cntw = min(LPR, wmax - base);
+#pragma unroll 1
+      for (int e0 = 0; e0 < cntw; e0 += U) {
+        float4 bv[U][NV];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const float we = __shfl_sync(0xffffffffu, w, e0 + u, LPR);
-        if (base + e0 + u < len) {
+        for (int u = 0; u < U; ++u) {
+          const int je = __shfl_sync(0xffffffffu, j, e0 + u, LPR);
+          const float *brow = B + (int64_t)je * ldb;
 #pragma unroll
           for (int v = 0; v < NV; ++v)
-            if (colok[v]) fma_into(acc[v], we, bv[u][v]);
+            if (colok[v]) bv[u][v] = ldg_f4(brow + coff[v]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const float we = __shfl_sync(0xffffffffu, w, e0 + u, LPR);
+          if (base + e0 + u < len) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v)
+              if (colok[v]) fma_into(acc[v], we, bv[u][v]);
+          }
         }
       }
     }
-  }
-  const float ds = (live && d_row) ? __ldg(d_row + row) : 1.0f;
-  const float4 *wt4 = reinterpret_cast<const float4 *>(wt_smem);
-  for (int c = 0; c < K2; ++c) {
-    float part = 0.0f;
+    const float ds = (live && d_row) ? __ldg(d_row + row) : 1.0f;
+    for (int c = 0; c < K2; ++c) {
+      float part = 0.0f;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) part += dot_of(acc[v], wt4[(c * K1P + coff[v]) / 4]);
-    part = group_sum<LPR>(part);
-    if (live && gl == c % LPR) {
-      float o = part * ds;
-      if (flags & GC_RELU) o = fmaxf(o, 0.0f);
-      C[row * ldc + c] = o;
+      for (int v = 0; v < NV; ++v) part += dot_of(acc[v], wt4[(c * K1P + coff[v]) / 4]);
+      part = group_sum<LPR>(part);
+      if (live && gl == c % LPR) {
+        float o = part * ds;
+        if (flags & GC_RELU) o = fmaxf(o, 0.0f);
+        C[row * ldc + c] = o;
+      }
     }
   }
 }
@@ -1058,7 +1059,12 @@ int launch_spmm_w(const int32_t *row_ptr, const int32_t *col_idx, const float *v
                   cudaStream_t st) {
   const int smem = K2 * LPR * NV * 4 * (int)sizeof(float);
   const int64_t groups_per_block = kThreads / LPR;
-  const unsigned grid = (unsigned)((n_rows + groups_per_block - 1) / groups_per_block);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // enough CTAs to fill the SMs (W^T staged once per CTA), never more than rows
+  const int64_t need = (n_rows + groups_per_block - 1) / groups_per_block;
+  const unsigned grid = (unsigned)std::min<int64_t>(need, (int64_t)sms * 8);
   spmm_w_kernel<LPR, NV><<<grid, kThreads, smem, st>>>(row_ptr, col_idx, values, d_row, d_col, B,
                                                        ldb, K1, W, K2, C, ldc, n_rows, flags);
   return check_launch("spmm_w_kernel");

@@ -563,11 +563,7 @@ def _shrink_candidates(K: int, mode: str = "spmm") -> list[int]:
     if mode in ("gatsd", "gatsdh") and K > 256:
         return [0]  # one wide lane-group shape only (whole row per pass)
     if mode.endswith("h"):  # fp16 rows: lane groups of 16-byte chunks
-        if K <= 16:
-            return [0]
-        # 3: column blocks (16 columns per pass, pass after pass over all
-        # rows) — for gather operands far larger than L2
-        return [0, 1] if K <= 32 else ([0, 1, 2, 3] if mode in ("spmmh", "gath") else [0, 1, 2])
+        return [0] if K <= 16 else ([0, 1] if K <= 32 else [0, 1, 2])
     return [0] if K <= 8 else ([0, 1] if K <= 16 else [0, 1, 2])
 
 
