@@ -950,8 +950,9 @@ def extra_configs(gc, args, dev, pk) -> dict:
                 row["compositions"][c] = {"ms": round(t[c] * 1e3, 4), "edges_per_s": round(m / t[c], 1),
                                           "parity": par.gat(gc.gat_layer(at, h, s), h, w, a_s, a_d,
                                                             heads, c, tol)}
-            # a multi-head layer's output width is heads * k2 (the selector's k2)
-            row.update(pick(row["compositions"], "gat", feats, K, k2=K * heads))
+            # a multi-head layer is `heads` single-head layers (GatLayerSpec):
+            # the selector is asked about one head's (k1, k2)
+            row.update(pick(row["compositions"], "gat", feats, K, k2=K))
             gat.append(row)
             del h, w, specs
             torch.cuda.empty_cache()
