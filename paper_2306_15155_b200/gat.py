@@ -47,6 +47,8 @@ from .sparse import (
     call_spmm_hook,
     gat_aggregate,
     gemm,
+    gemm_f16rows,
+    get_gemm_precision,
     pack_rows_f16,
     relu_,
     spmm,
@@ -212,11 +214,48 @@ def _check_h(a_tilde: CsrMatrix, h, spec: GatLayerSpec) -> None:
         raise ShapeError(f"embeddings shape {shape} != ({a_tilde.n_rows}, {spec.k1})")
 
 
+def _reuse_f16rows(a_tilde: CsrMatrix, x: torch.Tensor, spec: GatLayerSpec) -> bool:
+    """TF32 class, several heads, reassociated attention, each head's HW at
+    most 256 wide and large enough for fp16 gathers: each head's GEMM emits
+    its fp16 rows directly (no fp32 HW written and re-read by the packs) —
+    arxiv 4 heads K = 256 1.11 vs 1.17 ms; one head keeps the single GEMM +
+    pack with fused scores (0.310 vs 0.315 ms), profiles/data/gat_reuse_f16_r02.json."""
+    from . import gcn
+
+    k2 = spec.k2
+    return (spec.heads > 1 and spec.attention is AttentionForm.REASSOC
+            and a_tilde.n_rows == a_tilde.n_cols
+            and gcn.HALF_GATHER and get_gemm_precision() == "tf32" and x.is_cuda
+            and k2 % 8 == 0 and k2 <= 256 and x.shape[0] * k2 * 4 > gcn.HALF_MIN_BYTES)
+
+
+def _reuse_reassoc_f16rows(a_tilde: CsrMatrix, x: torch.Tensor, spec: GatLayerSpec,
+                           relu: bool) -> torch.Tensor:
+    """Reuse composition, reassociated attention, TF32 class: per head,
+    HW_h as fp16 rows straight from the GEMM epilogue (gemm_f16rows); the
+    node scores s = H (W_h a_src), t = H (W_h a_dst) from the folded vectors
+    in one pass over H for every head (the recompute path's projections —
+    the same values up to fp32 association)."""
+    k1, k2, H = spec.k1, spec.k2, spec.heads
+    u, v = _folded_attention_vectors(spec)
+    s, t = _projections(x, spec, u, v, k1, 0)
+    out = torch.empty(a_tilde.n_rows, k2 * H, dtype=torch.float32, device=x.device)
+    for i in range(H):
+        cs = slice(i * k2, (i + 1) * k2)
+        hr = gemm_f16rows(x, spec.weights[:, cs].contiguous())
+        if hr is None:  # outside the fused epilogue's range: fp32 GEMM, then pack
+            hr = pack_rows_f16(gemm(x, spec.weights[:, cs].contiguous()))
+        gat_aggregate(a_tilde, s[i], t[i], spec.leaky_slope, hr, relu=relu, out=out[:, cs])
+    return out
+
+
 def gat_layer_reuse(a_tilde: CsrMatrix, h, spec: GatLayerSpec, *, spmm_fn=None):
     """HW once, reused for attention and aggregation (SpMM at k2) — gat.py:121-129."""
     _check_h(a_tilde, h, spec)
     op = _Operand(h, a_tilde.device)
     relu = spec.activation == "relu"
+    if spmm_fn is None and _reuse_f16rows(a_tilde, op.t, spec):
+        return op.wrap(_reuse_reassoc_f16rows(a_tilde, op.t, spec, relu))
     hw = gemm(op.t, spec.weights)
     k2, H = spec.k2, spec.heads
     if spmm_fn is not None:
