@@ -1233,3 +1233,27 @@ def test_gcn_aggregate_first_fused_update(oracle, comp, k1, k2, monkeypatch):
         assert oracle.rel_err(fused, two) < 1e-5
     finally:
         gc.set_gemm_precision("tf32")
+
+
+@pytest.mark.parametrize("kind", ["uniform", "rmat"])
+@pytest.mark.parametrize("seed", [0, 1, 2])
+@pytest.mark.parametrize("K", [64, 256, 512])
+def test_fp16_spmm_random_graphs_bit_exact_and_oracle(oracle, kind, seed, K):
+    """Random uniform / power-law graphs (seeded): the fp16-row SpMM (fp16-
+    weight FMA for unit edges, split plans for the heavy rows) equals the fp32
+    kernel on the dequantised rows bit for bit, and the oracle on the
+    dequantised rows to fp32 accuracy."""
+    a = gc.add_self_loops(graphs.synthetic_graph(kind, 5000 + 700 * seed, 120000 + 20000 * seed,
+                                                 seed=seed, device=DEV))
+    rng = np.random.default_rng(seed * 10 + K)
+    x = torch.from_numpy(f32(rng.standard_normal((a.n_cols, K))
+                             * 2.0 ** rng.integers(-8, 8, (a.n_cols, 1)))).to(DEV)
+    d = gc.inv_sqrt_degrees(a).to(DEV)
+    hr = sparse.pack_rows_f16(x, d)
+    got = gc.spmm_unweighted(a, hr, d_row=d, relu=False)
+    deq = hr.xh[:, :K].float().contiguous()
+    assert torch.equal(got, gc.spmm_unweighted(a, deq, d_row=d, d_col=hr.sigma))
+    deq64 = hr.xh[:, :K].double().cpu().numpy() * hr.sigma.double().cpu().numpy()[:, None]
+    ref = oracle.scale_rows(d.double().cpu().numpy(),
+                            oracle.spmm_unweighted(to_oracle(oracle, a), deq64))
+    assert oracle.rel_err(got.cpu().numpy(), ref) < 1e-5
