@@ -61,6 +61,13 @@ extern "C" {
 #define GC_SPMM_SHRINK_MASK (3u << 8)
 #define GC_SPMM_B_F16 (1u << 10) /* gc_spmm_f32: B holds fp16 rows (ldb in elements; K % 4 == 0,
                                   * ldb % 4 == 0, 8-byte aligned), see gc_pack_rows_f16 */
+#define GC_SPMM_SIG_CHUNKS(c) ((uint32_t)((c) - 1) << 12) /* fp16 rows (GC_SPMM_B_F16): c >= 1
+                                   scales per row (d_col / sigma is n x c, one per 256-column
+                                   chunk; K = 256 c), as gc_gemm_f16rows_f32 emits for N > 256;
+                                   SpMM and GAT reassoc aggregation only */
+#define GC_SPMM_SIG_MASK (15u << 12)
+#define GC_HUB_SIG_CHUNKS(c) ((int32_t)((c) - 1) << 8) /* gc_hub_pack_f16rows fmt: c scales
+                                   per row (256-column chunks) */
 #define GC_GEMM_TF32 (1u << 4)  /* tcgen05.mma kind::tf32, TMEM accumulators, TMA operands */
 #define GC_GEMM_FP32 (1u << 5)  /* exact fp32 CUDA-core path (rtol 1e-4 parity mode) */
 #define GC_GEMM_TF32X3 (1u << 7) /* 3xTF32 on tcgen05: hi·hi + hi·lo + lo·hi, fp32-class (1e-4) */
@@ -306,9 +313,11 @@ GNNC_API int gc_hub_pack(const float *X, int64_t ldx, int64_t K, const int32_t *
 /* The TF32 GEMM with the TF32 class's gather operand as output: per row of
  * C = diag(row_scale) A W, Xh[row,:] = fp16_rn(C[row,:] * 2^-e) (max in
  * [2^14, 2^15); ldh = N rounded up to 8, pad zeroed) and sigma[row] = 2^e —
- * what gc_pack_rows_f16 makes of C, without writing C.  N <= 256 (the whole
- * row in one TMEM tile, two passes over it in the epilogue); workspace as
- * gc_gemm_f32. */
+ * what gc_pack_rows_f16 makes of C, without writing C.  N <= 256: the whole
+ * row in one TMEM tile (two passes over it in the epilogue), one scale per
+ * row; N a multiple of 256: one scale per row and 256-column chunk, sigma
+ * is M x (N/256) (consumers pass GC_SPMM_SIG_CHUNKS / GC_HUB_SIG_CHUNKS);
+ * workspace as gc_gemm_f32. */
 GNNC_API int gc_gemm_f16rows_f32(const float *A, int64_t lda, const float *W, int64_t ldw,
                                  int64_t M, int64_t K, int64_t N, const float *row_scale,
                                  void *Xh, int64_t ldh, float *sigma, void *workspace,

@@ -28,6 +28,16 @@ GC_SPMM_B_F16 = 1 << 10
 
 def GC_SPMM_SHRINK(s: int) -> int:  # noqa: N802 - mirrors the C macro
     return (int(s) & 3) << 8
+
+
+def GC_SPMM_SIG_CHUNKS(c: int) -> int:  # noqa: N802 - mirrors the C macro
+    return (int(c) - 1) << 12
+
+
+def GC_HUB_SIG_CHUNKS(c: int) -> int:  # noqa: N802 - mirrors the C macro
+    return (int(c) - 1) << 8
+
+
 GC_GEMM_TF32 = 1 << 4
 GC_GEMM_FP32 = 1 << 5
 GC_GEMM_TF32X3 = 1 << 7

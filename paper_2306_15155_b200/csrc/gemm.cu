@@ -238,11 +238,13 @@ struct GemmEpi {
   uint32_t flags;
   const float *scale;  // optional device scalar multiplied into every row (f16x2 unscale)
   // fp16-row output (gc_gemm_f16rows_f32, the TF32 class's gather operand):
-  // Ch[row] = fp16_rn(out_row * 2^-e_row), sigma[row] = 2^e_row, with the
-  // row max in [2^14, 2^15); needs the whole row in one N tile (BN >= N)
+  // Ch[row, chunk] = fp16_rn(out * 2^-e), sigma[row * sig_ld + chunk] = 2^e,
+  // each N tile's row max in [2^14, 2^15) — one scale per row when the row
+  // is one tile (BN >= N), one per 256-column chunk otherwise (sig_ld chunks)
   __half *Ch;
   int64_t ldh;
   float *sigma;
+  int sig_ld;
 };
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
@@ -442,35 +444,37 @@ __device__ __forceinline__ void gemm_tc_body(const CUtensorMap &map_a, const CUt
       float *crow = ep.C + (int64_t)row * ep.ldc;
       const uint32_t taddr = tmem_base + (uint32_t)(acc * BN) + ((uint32_t)(q * 32) << 16);
       if (ep.Ch) {
-        // fp16 rows (TF32 class): pass 1 finds the row max in TMEM, pass 2
-        // converts with the exact power-of-two scale; the whole row is this
-        // tile (n0 == 0, BN >= N)
+        // fp16 rows (TF32 class): pass 1 finds the tile row's max in TMEM,
+        // pass 2 converts with the exact power-of-two scale (one scale per
+        // row and N tile: the whole row when BN >= N, else 256-column chunks)
+        const int nv = ep.N - n0;  // valid columns of this tile
         float mx = 0.0f;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 16) {
-          if (c >= ep.N) break;  // warp-uniform
+          if (c >= nv) break;  // warp-uniform
           float v[16];
           tmem_ld16(taddr + (uint32_t)c, v);
 #pragma unroll
           for (int i = 0; i < 16; ++i)
-            if (c + i < ep.N) mx = fmaxf(mx, fabsf(v[i] * rs));
+            if (c + i < nv) mx = fmaxf(mx, fabsf(v[i] * rs));
         }
         const int E = mx > 0.0f ? ((int)((__float_as_uint(mx) >> 23) & 0xff) - 127) : 0;
         const int e = mx > 0.0f && isfinite(mx) ? max(min(E - 14, 110), -110) : 0;
         const float down = __uint_as_float((uint32_t)(127 - e) << 23) * rs;
-        __half *hrow = ep.Ch + (int64_t)row * ep.ldh;
+        __half *hrow = ep.Ch + (int64_t)row * ep.ldh + n0;
+        const int64_t nh = ep.ldh - n0;  // padded columns of this tile
 #pragma unroll 1
         for (int c = 0; c < BN; c += 16) {
-          if (c >= ep.ldh) break;  // warp-uniform (ldh: N rounded up to 8)
+          if (c >= nh) break;  // warp-uniform (ldh: N rounded up to 8)
           float v[16];
           tmem_ld16(taddr + (uint32_t)c, v);
           if (!row_ok) continue;
           __half2 hv[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i)
-            hv[i] = __floats2half2_rn(c + 2 * i < ep.N ? v[2 * i] * down : 0.0f,
-                                      c + 2 * i + 1 < ep.N ? v[2 * i + 1] * down : 0.0f);
-          if (c + 16 <= ep.ldh) {
+            hv[i] = __floats2half2_rn(c + 2 * i < nv ? v[2 * i] * down : 0.0f,
+                                      c + 2 * i + 1 < nv ? v[2 * i + 1] * down : 0.0f);
+          if (c + 16 <= nh) {
             uint4 *dst = reinterpret_cast<uint4 *>(hrow + c);
             dst[0] = *reinterpret_cast<const uint4 *>(&hv[0]);
             dst[1] = *reinterpret_cast<const uint4 *>(&hv[4]);
@@ -478,7 +482,8 @@ __device__ __forceinline__ void gemm_tc_body(const CUtensorMap &map_a, const CUt
             *reinterpret_cast<uint4 *>(hrow + c) = *reinterpret_cast<const uint4 *>(&hv[0]);
           }
         }
-        if (row_ok) ep.sigma[row] = __uint_as_float((uint32_t)(127 + e) << 23);
+        if (row_ok)
+          ep.sigma[(int64_t)row * ep.sig_ld + n0 / BN] = __uint_as_float((uint32_t)(127 + e) << 23);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty_bar(acc));
@@ -1686,6 +1691,11 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// scale chunk of feature f: 256-column chunks when sig_ld > 1, else the row's
+__device__ __forceinline__ int64_t sig_chunk(int64_t f, int sig_ld) {
+  return sig_ld > 1 ? (f >> 8) : 0;
+}
+
 // |(D X)[hub_cols]| maximum (as float bits; non-negative floats order like
 // ints): a warp per gathered row, lanes across its K floats.
 __global__ void __launch_bounds__(256)
@@ -1693,8 +1703,9 @@ __global__ void __launch_bounds__(256)
                       const int32_t *__restrict__ hub_cols, int64_t T,
                       const float *__restrict__ d, unsigned *__restrict__ out,
                       const __half *__restrict__ Xh = nullptr,
-                      const float *__restrict__ sigma = nullptr) {
-  // Xh (fp16 rows, row scales sigma) replaces X when given: x = sigma_j * Xh[j]
+                      const float *__restrict__ sigma = nullptr, int sig_ld = 1) {
+  // Xh (fp16 rows, scales sigma) replaces X when given: x = sigma_j * Xh[j]
+  // (sig_ld > 1: one scale per 256-column chunk, sigma[j * sig_ld + f / 256])
   const int lane = threadIdx.x % 32;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int64_t n_warps = (int64_t)gridDim.x * blockDim.x / 32;
@@ -1704,8 +1715,8 @@ __global__ void __launch_bounds__(256)
     float mr = 0.0f;
     if (Xh) {
       const __half *row = Xh + j * ldx;
-      for (int64_t f = lane; f < K; f += 32) mr = fmaxf(mr, fabsf(__half2float(row[f])));
-      mr *= fabsf(__ldg(sigma + j));
+      for (int64_t f = lane; f < K; f += 32)
+        mr = fmaxf(mr, fabsf(__half2float(row[f]) * __ldg(sigma + j * sig_ld + sig_chunk(f, sig_ld))));
     } else {
       const float *row = X + j * ldx;
       for (int64_t f = lane; f < K; f += 32) mr = fmaxf(mr, fabsf(__ldg(row + f)));
@@ -1728,7 +1739,7 @@ __global__ void __launch_bounds__(256)
                         const float *__restrict__ d, int64_t kp, const unsigned *__restrict__ amax,
                         float *__restrict__ inv_scale, __half *__restrict__ Bt,
                         const __half *__restrict__ Xh = nullptr,
-                        const float *__restrict__ sigma = nullptr) {
+                        const float *__restrict__ sigma = nullptr, int sig_ld = 1) {
   __shared__ float tile[64][33];
   const float mx = __uint_as_float(*amax);
   const int e = mx > 0.0f ? ilogbf(mx) : 0;
@@ -1741,7 +1752,8 @@ __global__ void __launch_bounds__(256)
     float x = 0.0f;
     if (t < T && f < K) {
       const int64_t j = __ldg(hub_cols + t);
-      x = Xh ? __half2float(Xh[j * ldx + f]) * __ldg(sigma + j) : __ldg(X + j * ldx + f);
+      x = Xh ? __half2float(Xh[j * ldx + f]) * __ldg(sigma + j * sig_ld + sig_chunk(f, sig_ld))
+             : __ldg(X + j * ldx + f);
       if (d) x *= __ldg(d + j);
     }
     tile[i][threadIdx.x] = x * sc;
@@ -1770,7 +1782,7 @@ __global__ void __launch_bounds__(256)
                            const float *__restrict__ d, int64_t kp,
                            const unsigned *__restrict__ amax, float *__restrict__ inv_scale,
                            __half *__restrict__ Bm, int vec, const __half *__restrict__ Xh = nullptr,
-                           const float *__restrict__ sigma = nullptr) {
+                           const float *__restrict__ sigma = nullptr, int sig_ld = 1) {
   const float mx = __uint_as_float(*amax);
   const int e = mx > 0.0f ? ilogbf(mx) : 0;
   const float sc = ldexpf(1.0f, 13 - e);
@@ -1781,9 +1793,10 @@ __global__ void __launch_bounds__(256)
     const int64_t j = __ldg(hub_cols + t);
     const float *row = X + j * ldx;
     const __half *hrow = Xh ? Xh + j * ldx : nullptr;
-    float s = d ? __ldg(d + j) * sc : sc;
-    if (Xh) s *= __ldg(sigma + j);
+    const float s0 = d ? __ldg(d + j) * sc : sc;
     for (int64_t f = 8 * lane; f < kp; f += 256) {
+      // (8 features never straddle a 256-column scale chunk)
+      const float s = Xh ? s0 * __ldg(sigma + j * sig_ld + sig_chunk(f, sig_ld)) : s0;
       float v[8];
       if (Xh) {
 #pragma unroll
@@ -2042,8 +2055,9 @@ extern "C" int gc_gemm_f16rows_f32(const float *A, int64_t lda, const float *W, 
                                    size_t ws_bytes, void *stream) {
   GC_REQUIRE(M >= 0 && K >= 1 && N >= 1 && lda >= K && ldw >= N, GC_ERR_SHAPE,
              "gc_gemm_f16rows_f32: bad shape");
-  GC_REQUIRE(N <= 256 && ldh == (N + 7) / 8 * 8, GC_ERR_UNSUPPORTED,
-             "gc_gemm_f16rows_f32: needs N <= 256 (one N tile) and ldh = N rounded up to 8");
+  GC_REQUIRE((N <= 256 || N % 256 == 0) && ldh == (N + 7) / 8 * 8, GC_ERR_UNSUPPORTED,
+             "gc_gemm_f16rows_f32: needs N <= 256 or a multiple of 256, and ldh = N rounded "
+             "up to 8");
   if (M == 0) return GC_OK;
   GC_REQUIRE(A && W && Xh && sigma && aligned16(Xh), GC_ERR_VALUE,
              "gc_gemm_f16rows_f32: null or unaligned operand");
@@ -2063,8 +2077,9 @@ extern "C" int gc_gemm_f16rows_f32(const float *A, int64_t lda, const float *W, 
     if (rc) return rc;
   }
   const int bn = N <= 16 ? 16 : N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
+  // one scale per row (N <= 256) or per 256-column chunk: sigma is M x sig_ld
   GemmEpi ep{nullptr, 0, row_scale, M, N, 0u, nullptr,
-             static_cast<__half *>(Xh), ldh, sigma};
+             static_cast<__half *>(Xh), ldh, sigma, N <= 256 ? 1 : (int)(N / 256)};
   CUtensorMap ma, mb, mc;
   int rc = make_map(&ma, A, M, K, lda, BM);
   if (rc) return rc;
@@ -2083,7 +2098,12 @@ extern "C" int gc_gemm_f16rows_f32(const float *A, int64_t lda, const float *W, 
 extern "C" int gc_hub_pack_f16rows(const void *Xh, int64_t ldh, const float *sigma, int64_t K,
                                    const int32_t *hub_cols, int64_t T, const float *d_col,
                                    int32_t fmt, void *Bt, float *scale_ws, void *stream) {
+  // GC_HUB_SIG_CHUNKS(c) in fmt: sigma holds c scales per row (256 columns each)
+  const int sig_ld = (int)(((uint32_t)fmt >> 8) & 15u) + 1;
+  fmt &= 0xff;
   GC_REQUIRE(K >= 1 && T >= 0 && ldh >= K, GC_ERR_SHAPE, "gc_hub_pack_f16rows: bad shape");
+  GC_REQUIRE(sig_ld == 1 || (int64_t)sig_ld * 256 == K, GC_ERR_SHAPE,
+             "gc_hub_pack_f16rows: %d scale chunks need K = %d", sig_ld, sig_ld * 256);
   GC_REQUIRE(fmt == GC_HUB_F16 || fmt == GC_HUB_F16_MN, GC_ERR_VALUE,
              "gc_hub_pack_f16rows: one-term fp16 formats only (format %d)", fmt);
   if (T == 0) return GC_OK;
@@ -2100,7 +2120,7 @@ extern "C" int gc_hub_pack_f16rows(const void *Xh, int64_t ldh, const float *sig
   }
   const int64_t blocks = std::min<int64_t>((T + 7) / 8, (int64_t)sm_count() * 8);
   hub_absmax_kernel<<<(unsigned)blocks, 256, 0, st>>>(nullptr, ldh, K, hub_cols, T, d_col, amax,
-                                                      xh, sigma);
+                                                      xh, sigma, sig_ld);
   int rc = check_launch("hub_absmax_kernel");
   if (rc) return rc;
   if (fmt == GC_HUB_F16_MN) {
@@ -2109,14 +2129,16 @@ extern "C" int gc_hub_pack_f16rows(const void *Xh, int64_t ldh, const float *sig
     const int64_t nb = std::min<int64_t>((T + 7) / 8, (int64_t)sm_count() * 16);
     hub_pack_f16_mn_kernel<<<(unsigned)nb, 256, 0, st>>>(nullptr, ldh, K, hub_cols, T, d_col, kp,
                                                          amax, scale_ws + 1,
-                                                         static_cast<__half *>(Bt), 0, xh, sigma);
+                                                         static_cast<__half *>(Bt), 0, xh, sigma,
+                                                         sig_ld);
     return check_launch("hub_pack_f16_mn_kernel");
   }
   dim3 grid((unsigned)((T + 63) / 64), (unsigned)((kp + 31) / 32));
   GC_REQUIRE(grid.y < 65536, GC_ERR_SHAPE, "gc_hub_pack_f16rows: K too large");
   hub_pack_f16_kernel<1><<<grid, dim3(32, 8), 0, st>>>(nullptr, ldh, K, hub_cols, T, d_col, kp,
                                                        amax, scale_ws + 1,
-                                                       static_cast<__half *>(Bt), xh, sigma);
+                                                       static_cast<__half *>(Bt), xh, sigma,
+                                                       sig_ld);
   return check_launch("hub_pack_f16_kernel");
 }
 

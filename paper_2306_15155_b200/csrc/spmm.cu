@@ -89,6 +89,8 @@ struct SpmmArgs {
   bool hints;         // col_idx carries hub tags in bit 31 (gc_tag_hub_columns)
   const float *B_self; // GAT-SDDMM: row i's own features (a_src.B_self[i]); B for a square
   int64_t ld_self;     //   pattern, a rank's own rows for a row block of a partition
+  int sig_ld;          // fp16 rows: scales per row (> 1: one per 256-column pass, d_col is
+                       //   n_cols x sig_ld and pass blockIdx.y reads column blockIdx.y)
 };
 
 template <bool VEC>
@@ -261,6 +263,11 @@ __global__ void __launch_bounds__(kThreads, BH ? (MODE == 2 ? (GNNC_SPMM_BH_MINB
   }
   constexpr int64_t kColsPerPass = (int64_t)LPR * NV * Lanes<VEC>::W;
   const int64_t c0 = (int64_t)blockIdx.y * kColsPerPass;
+  // d_col index of column j: per row, or per (row, 256-column pass) for fp16
+  // rows with chunked scales (the entry points check kColsPerPass == 256)
+  const int64_t sig_ld = a.sig_ld > 1 ? a.sig_ld : 1;
+  const int64_t sig_off = a.sig_ld > 1 ? (int64_t)blockIdx.y : 0;
+  auto sig_at = [&](int j) -> int64_t { return (int64_t)j * sig_ld + sig_off; };
 
   // column slots of this lane (32-bit: K is a feature width, far below 2^31)
   bool colok[NV];
@@ -320,8 +327,10 @@ __global__ void __launch_bounds__(kThreads, BH ? (MODE == 2 ? (GNNC_SPMM_BH_MINB
   if (gl < len) {
     j1 = ldg_stream_i32(a.col_idx + beg + gl);
     if (HAS_VAL) v1 = ldg_stream_f32(a.values + beg + gl);
-    if (NEEDG) g1 = __ldg((MODE == 1 ? a.t : a.d_col) + (HINT ? (j1 & 0x7FFFFFFF) : j1));
-    if (SIG) gs1 = __ldg(a.d_col + j1);
+    if (NEEDG)
+      g1 = __ldg(MODE == 1 ? a.t + (HINT ? (j1 & 0x7FFFFFFF) : j1)
+                           : a.d_col + sig_at(HINT ? (j1 & 0x7FFFFFFF) : j1));
+    if (SIG) gs1 = __ldg(a.d_col + sig_at(j1));
   }
   if (LPR + gl < len) {
     j2 = ldg_stream_i32(a.col_idx + beg + LPR + gl);
@@ -348,8 +357,9 @@ __global__ void __launch_bounds__(kThreads, BH ? (MODE == 2 ? (GNNC_SPMM_BH_MINB
     j1 = j2;
     v1 = v2;
     if (NEEDG && base + LPR + gl < len)
-      g1 = __ldg((MODE == 1 ? a.t : a.d_col) + (HINT ? (j1 & 0x7FFFFFFF) : j1));
-    if (SIG && base + LPR + gl < len) gs1 = __ldg(a.d_col + j1);
+      g1 = __ldg(MODE == 1 ? a.t + (HINT ? (j1 & 0x7FFFFFFF) : j1)
+                           : a.d_col + sig_at(HINT ? (j1 & 0x7FFFFFFF) : j1));
+    if (SIG && base + LPR + gl < len) gs1 = __ldg(a.d_col + sig_at(j1));
     if (base + 2 * LPR + gl < len) {
       j2 = ldg_stream_i32(a.col_idx + beg + base + 2 * LPR + gl);
       if (HAS_VAL) v2 = ldg_stream_f32(a.values + beg + base + 2 * LPR + gl);
@@ -702,6 +712,11 @@ int dispatch(SpmmArgs &a, int64_t n_rows, int algo, const int32_t *items, int64_
                "16-byte aligned B and C", who);
     GC_REQUIRE(!a.hints, GC_ERR_UNSUPPORTED, "%s: no hub tags with an fp16 operand", who);
     GC_REQUIRE(MODE == 0 || a.d_col != nullptr, GC_ERR_VALUE, "%s: fp16 rows need sigma", who);
+    // chunked scales: one per 256-column pass (every fp16 shape above K = 256
+    // runs 256 columns per pass); not for the SDDMM score (whole row per pass)
+    GC_REQUIRE(a.sig_ld <= 1 || (MODE != 2 && a.d_col && K == (int64_t)a.sig_ld * 256),
+               GC_ERR_UNSUPPORTED, "%s: %d scale chunks need K = %d (SpMM / GAT reassoc)", who,
+               a.sig_ld, a.sig_ld * 256);
     GC_REQUIRE(MODE != 2 || (a.B_self != a.B && a.B_self != nullptr), GC_ERR_VALUE,
                "%s: fp16 rows need fp32 source rows B_self", who);
     cudaStream_t sth = as_stream(stream);
@@ -935,6 +950,7 @@ extern "C" int gc_spmm_f32(const int32_t *row_ptr, const int32_t *col_idx, const
   GC_REQUIRE(n_rows >= 0 && n_cols >= 0 && K >= 0, GC_ERR_SHAPE, "gc_spmm_f32: negative size");
   GC_REQUIRE(ldb >= K && ldc >= K, GC_ERR_SHAPE, "gc_spmm_f32: leading dimension < K");
   GC_REQUIRE((flags & ~(GC_RELU | GC_ACCUMULATE | GC_HUB_TAGGED | GC_SPMM_SHRINK_MASK |
+                         GC_SPMM_SIG_MASK |
                          GC_SPMM_B_F16)) == 0,
              GC_ERR_VALUE, "gc_spmm_f32: unknown flags 0x%x", flags);
   if (n_rows == 0 || K == 0) return GC_OK;
@@ -952,7 +968,8 @@ extern "C" int gc_spmm_f32(const int32_t *row_ptr, const int32_t *col_idx, const
   a.K = K;
   a.C = C;
   a.ldc = ldc;
-  a.flags = flags;
+  a.flags = flags & ~GC_SPMM_SIG_MASK;
+  a.sig_ld = (int)((flags & GC_SPMM_SIG_MASK) >> 12) + 1;
   a.hints = (flags & GC_HUB_TAGGED) != 0;
   return dispatch<0>(a, n_rows, algo, items, n_items, split_rows, n_split_rows, workspace,
                          ws_bytes, stream, "gc_spmm_f32");
@@ -1110,7 +1127,8 @@ extern "C" int gc_gat_sddmm_aggregate_f32(const int32_t *row_ptr, const int32_t 
   GC_REQUIRE(n_rows >= 0 && K >= 1, GC_ERR_SHAPE, "gc_gat_sddmm_aggregate_f32: bad size");
   GC_REQUIRE(ldb >= K && ldc >= K, GC_ERR_SHAPE,
              "gc_gat_sddmm_aggregate_f32: leading dimension < K");
-  GC_REQUIRE((flags & ~(GC_RELU | GC_HUB_TAGGED | GC_SPMM_SHRINK_MASK | GC_SPMM_B_F16)) == 0,
+  GC_REQUIRE((flags & ~(GC_RELU | GC_HUB_TAGGED | GC_SPMM_SHRINK_MASK | GC_SPMM_B_F16 |
+                         GC_SPMM_SIG_MASK)) == 0,
              GC_ERR_VALUE, "gc_gat_sddmm_aggregate_f32: unknown flags 0x%x", flags);
   GC_REQUIRE(slope > 0.0f && slope < 1.0f, GC_ERR_VALUE,
              "gc_gat_sddmm_aggregate_f32: leaky_slope must lie in (0, 1)");
@@ -1132,7 +1150,8 @@ extern "C" int gc_gat_sddmm_aggregate_f32(const int32_t *row_ptr, const int32_t 
   a.K = K;
   a.C = C;
   a.ldc = ldc;
-  a.flags = flags;
+  a.flags = flags & ~GC_SPMM_SIG_MASK;
+  a.sig_ld = (int)((flags & GC_SPMM_SIG_MASK) >> 12) + 1;
   a.hints = (flags & GC_HUB_TAGGED) != 0;
   a.a_src = a_src;
   a.a_dst = a_dst;
@@ -1152,7 +1171,8 @@ extern "C" int gc_gat_aggregate_f32(const int32_t *row_ptr, const int32_t *col_i
   GC_REQUIRE(n_rows >= 0 && n_cols >= 0 && K >= 0, GC_ERR_SHAPE,
              "gc_gat_aggregate_f32: negative size");
   GC_REQUIRE(ldb >= K && ldc >= K, GC_ERR_SHAPE, "gc_gat_aggregate_f32: leading dimension < K");
-  GC_REQUIRE((flags & ~(GC_RELU | GC_HUB_TAGGED | GC_SPMM_SHRINK_MASK | GC_SPMM_B_F16)) == 0,
+  GC_REQUIRE((flags & ~(GC_RELU | GC_HUB_TAGGED | GC_SPMM_SHRINK_MASK | GC_SPMM_B_F16 |
+                         GC_SPMM_SIG_MASK)) == 0,
              GC_ERR_VALUE, "gc_gat_aggregate_f32: unknown flags 0x%x", flags);
   GC_REQUIRE(slope > 0.0f && slope < 1.0f, GC_ERR_VALUE,
              "gc_gat_aggregate_f32: leaky_slope must lie in (0, 1)");
@@ -1169,7 +1189,8 @@ extern "C" int gc_gat_aggregate_f32(const int32_t *row_ptr, const int32_t *col_i
   a.K = K;
   a.C = C;
   a.ldc = ldc;
-  a.flags = flags;
+  a.flags = flags & ~GC_SPMM_SIG_MASK;
+  a.sig_ld = (int)((flags & GC_SPMM_SIG_MASK) >> 12) + 1;
   a.hints = (flags & GC_HUB_TAGGED) != 0;
   a.s = s;
   a.t = t;

@@ -212,6 +212,8 @@ def all_gather_half(hr: HalfRows, part: RowPartition, group=None, async_op=False
     followed by 8 halves whose first two hold the float32 scale's bits.
     Returns (HalfRows over the padded gather buffer, work handle, finish) —
     call ``finish()`` after ``work.wait()`` to extract the scales."""
+    if hr.chunks != 1:
+        raise ShapeError("all_gather_half: one scale per row expected (gc_pack_rows_f16)")
     ldh = hr.xh.shape[1]
     w = ldh + 8  # row pitch stays a multiple of 16 bytes
     send, full = part.gather_buffers(w, torch.float16, hr.xh.device, tag="half")
@@ -236,6 +238,8 @@ def all_gather_half_multi(hrs: list, extra: torch.Tensor | None, part: RowPartit
     multiple of 8 halves (16 bytes).  Returns (list of HalfRows over the
     gather buffer, extra_full [world*max_rows, E] fp32)."""
     dev = hrs[0].xh.device
+    if any(hr.chunks != 1 for hr in hrs):
+        raise ShapeError("all_gather_half_multi: one scale per row expected (gc_pack_rows_f16)")
     offs, o = [], 0
     for hr in hrs:
         offs.append(o)

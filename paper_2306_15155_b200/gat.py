@@ -216,7 +216,8 @@ def _check_h(a_tilde: CsrMatrix, h, spec: GatLayerSpec) -> None:
 
 def _reuse_f16rows(a_tilde: CsrMatrix, x: torch.Tensor, spec: GatLayerSpec) -> bool:
     """TF32 class, several heads, reassociated attention, each head's HW at
-    most 256 wide and large enough for fp16 gathers: each head's GEMM emits
+    most 256 wide or a multiple of 256 (one scale per 256-column chunk) and
+    large enough for fp16 gathers: each head's GEMM emits
     its fp16 rows directly (no fp32 HW written and re-read by the packs) —
     arxiv 4 heads K = 256 1.11 vs 1.17 ms; one head keeps the single GEMM +
     pack with fused scores (0.310 vs 0.315 ms), profiles/data/gat_reuse_f16_r02.json."""
@@ -226,7 +227,8 @@ def _reuse_f16rows(a_tilde: CsrMatrix, x: torch.Tensor, spec: GatLayerSpec) -> b
     return (spec.heads > 1 and spec.attention is AttentionForm.REASSOC
             and a_tilde.n_rows == a_tilde.n_cols
             and gcn.HALF_GATHER and get_gemm_precision() == "tf32" and x.is_cuda
-            and k2 % 8 == 0 and k2 <= 256 and x.shape[0] * k2 * 4 > gcn.HALF_MIN_BYTES)
+            and k2 % 8 == 0 and (k2 <= 256 or k2 % 256 == 0)
+            and x.shape[0] * k2 * 4 > gcn.HALF_MIN_BYTES)
 
 
 def _reuse_reassoc_f16rows(a_tilde: CsrMatrix, x: torch.Tensor, spec: GatLayerSpec,

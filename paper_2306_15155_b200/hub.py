@@ -438,8 +438,9 @@ def pack(a: CsrMatrix, x: torch.Tensor, d: torch.Tensor, spec):
     bt = torch.empty(_TERMS[fmt] * kp * plan.T, dtype=_block_dtype(fmt), device=x.device)
     sc = torch.empty(2, dtype=torch.float32, device=x.device)
     if half:  # the dense part reads the same fp16 rows as the tail
+        fmt_c = fmt | (nat.GC_HUB_SIG_CHUNKS(x.chunks) if x.chunks > 1 else 0)
         nat.check(lib.gc_hub_pack_f16rows(x.xh.data_ptr(), _ld(x.xh), x.sigma.data_ptr(), K,
-                                          plan.hub_cols.data_ptr(), plan.T, _ptr(d), fmt,
+                                          plan.hub_cols.data_ptr(), plan.T, _ptr(d), fmt_c,
                                           bt.data_ptr(), sc.data_ptr(), _stream(x.device)),
                   "hub_pack_f16rows")
         return bt, sc, fmt

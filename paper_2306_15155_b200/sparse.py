@@ -527,6 +527,9 @@ PLAN_MIN_NNZ = 1 << 16  # below this a row-per-group launch needs no plan
 # enough that the plain lane-group SpMM needs no nnz-split plan (GNNC_SPMM_GEMM=0
 # keeps the two-kernel form)
 SPMM_GEMM = os.environ.get("GNNC_SPMM_GEMM", "1") != "0"
+# GEMM epilogue emitting fp16 rows with one scale per 256-column chunk for
+# N > 256 (GNNC_F16ROWS_CHUNKED=0: fp32 product, then a per-row pack)
+F16ROWS_CHUNKED = os.environ.get("GNNC_F16ROWS_CHUNKED", "1") != "0"
 SPMM_GEMM_MAX_DEG = 1024  # one lane group per row: no heavy-row splitting
 # L1 policy tags on hub columns: "0" off, "1" on, "auto" (default): measured
 # once per (pattern, K) on the first large launch and cached — the tags win on
@@ -634,7 +637,7 @@ def gat_sddmm_aggregate(a: CsrMatrix, a_src: torch.Tensor, a_dst: torch.Tensor, 
     if b_self is not None and (tuple(b_self.shape) != (a.n_rows, K) or b_self.stride(1) != 1):
         raise ShapeError("gat_sddmm_aggregate: b_self must be a row-major n_rows x K tensor")
     if (K > 1024 or K % 4 or _ld(bt) % 4 or bt.data_ptr() % 16 or a_src.data_ptr() % 16
-            or a_dst.data_ptr() % 16 or (half and (K % 8 or _ld(bt) % 8))
+            or a_dst.data_ptr() % 16 or (half and (K % 8 or _ld(bt) % 8 or b.chunks > 1))
             or (b_self is not None and (_ld(b_self) % 4 or b_self.data_ptr() % 16))):
         return None
     _require_cuda(a.col_idx, bt, a_src, a_dst)
@@ -644,7 +647,7 @@ def gat_sddmm_aggregate(a: CsrMatrix, a_src: torch.Tensor, a_dst: torch.Tensor, 
         return None
     code, items, n_items, split, n_split, ws = _plan_args(a, K, algo, dev, gat=True)
     lib = nat.load()
-    flags = (nat.GC_RELU if relu else 0) | (nat.GC_SPMM_B_F16 if half else 0)
+    flags = (nat.GC_RELU if relu else 0) | (nat.GC_SPMM_B_F16 | b.sig_flags() if half else 0)
 
     def launch(cols, extra):
         return lib.gc_gat_sddmm_aggregate_f32(
@@ -678,6 +681,15 @@ class HalfRows:
 
     def __init__(self, xh: torch.Tensor, sigma: torch.Tensor, K: int):
         self.xh, self.sigma, self.K = xh, sigma, int(K)
+
+    @property
+    def chunks(self) -> int:
+        """Scales per row: 1, or one per 256-column chunk (sigma is n x c) as
+        the GEMM epilogue emits them for K > 256 (gemm_f16rows)."""
+        return 1 if self.sigma.dim() == 1 else int(self.sigma.shape[1])
+
+    def sig_flags(self) -> int:
+        return nat.GC_SPMM_SIG_CHUNKS(self.chunks) if self.chunks > 1 else 0
 
     @property
     def shape(self) -> tuple[int, int]:
@@ -740,11 +752,13 @@ def _spmm(a: CsrMatrix, b, *, weighted: bool, d_row=None, d_col=None, relu=False
             out.zero_()
     elif tuple(out.shape) != (a.n_rows, K) or out.stride(1) != 1:
         raise ShapeError(f"{what}: out must be a row-major {a.n_rows}x{K} tensor")
-    for d, n, nm in ((d_row, a.n_rows, "d_row"), (d_col, a.n_cols, "d_col")):
+    for d, n, nm in ((d_row, a.n_rows, "d_row"), (None if half else d_col, a.n_cols, "d_col")):
         if d is not None and tuple(d.shape) != (n,):
             raise ShapeError(f"{what}: {nm} must have {n} entries")
+    if half and d_col.shape[0] != a.n_cols:  # (the fp16 rows' scales: n_cols [x chunks])
+        raise ShapeError(f"{what}: the fp16 rows' scales must have {a.n_cols} rows")
     flags = (nat.GC_RELU if relu else 0) | (nat.GC_ACCUMULATE if accumulate else 0) | \
-        (nat.GC_SPMM_B_F16 if half else 0)
+        (nat.GC_SPMM_B_F16 | b.sig_flags() if half else 0)
     code, items, n_items, split, n_split, ws = _plan_args(a, K, algo, dev)
     lib = nat.load()
 
@@ -792,7 +806,7 @@ def gat_aggregate(a: CsrMatrix, s: torch.Tensor, t: torch.Tensor, slope: float, 
         raise ShapeError(f"gat_aggregate: out must be a row-major {a.n_rows}x{K} tensor")
     code, items, n_items, split, n_split, ws = _plan_args(a, K, algo, dev, gat=True)
     lib = nat.load()
-    flags = (nat.GC_RELU if relu else 0) | (nat.GC_SPMM_B_F16 if half else 0)
+    flags = (nat.GC_RELU if relu else 0) | (nat.GC_SPMM_B_F16 | b.sig_flags() if half else 0)
 
     def launch(cols, extra, dst=out):
         return lib.gc_gat_aggregate_f32(
@@ -1025,7 +1039,8 @@ def gemm_f16rows(a: torch.Tensor, b: torch.Tensor, *, row_scale=None) -> HalfRow
     N = b.shape[1]
     if b.shape[0] != K:
         raise ShapeError(f"gemm: inner dimensions {K} != {b.shape[0]}")
-    if N > 256 or K < 1 or a.stride(1) != 1 or _ld(a) % 4 or a.data_ptr() % 16:
+    if (N > 256 and (N % 256 or not F16ROWS_CHUNKED)) or K < 1 or a.stride(1) != 1 \
+            or _ld(a) % 4 or a.data_ptr() % 16:
         return None
     if row_scale is not None and tuple(row_scale.shape) != (M,):
         raise ShapeError("gemm: row_scale must have one entry per row")
@@ -1033,7 +1048,8 @@ def gemm_f16rows(a: torch.Tensor, b: torch.Tensor, *, row_scale=None) -> HalfRow
     lib = nat.load()
     ldh = (N + 7) // 8 * 8
     xh = torch.empty(M, ldh, dtype=torch.float16, device=a.device)
-    sigma = torch.empty(M, dtype=torch.float32, device=a.device)
+    # one scale per row, or per row and 256-column chunk (N > 256)
+    sigma = torch.empty((M,) if N <= 256 else (M, N // 256), dtype=torch.float32, device=a.device)
     ws = torch.empty(max(int(lib.gc_gemm_workspace_bytes(K, N)), 16), dtype=torch.uint8,
                      device=a.device)
     rc = _timed_call("gemm", a.device, lambda: lib.gc_gemm_f16rows_f32(

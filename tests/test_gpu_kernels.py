@@ -1257,3 +1257,123 @@ def test_fp16_spmm_random_graphs_bit_exact_and_oracle(oracle, kind, seed, K):
     ref = oracle.scale_rows(d.double().cpu().numpy(),
                             oracle.spmm_unweighted(to_oracle(oracle, a), deq64))
     assert oracle.rel_err(got.cpu().numpy(), ref) < 1e-5
+
+
+# ---- fp16 rows with one scale per 256-column chunk (gemm_f16rows, N > 256) ----
+
+
+def _chunked_rows(x: torch.Tensor) -> "sparse.HalfRows":
+    """HalfRows with one scale per 256-column chunk, built by packing each
+    chunk on its own (what the GEMM epilogue emits per N tile)."""
+    parts = [sparse.pack_rows_f16(x[:, c:c + 256].contiguous()) for c in range(0, x.shape[1], 256)]
+    xh = torch.cat([p.xh for p in parts], 1).contiguous()
+    return sparse.HalfRows(xh, torch.stack([p.sigma for p in parts], 1).contiguous(), x.shape[1])
+
+
+@pytest.mark.parametrize("M,K,N", [(1000, 64, 512), (3001, 200, 1024), (777, 256, 768)])
+@pytest.mark.parametrize("scaled", [False, True])
+def test_gemm_f16rows_chunked_scales_equal_chunk_packs(M, K, N, scaled):
+    """N a multiple of 256: the epilogue emits one scale per row and 256-column
+    N tile, bit-identical to packing each chunk of the TF32 GEMM's output."""
+    rng = np.random.default_rng(M + N)
+    a = torch.from_numpy(f32(rng.uniform(-0.5, 0.5, (M, K)) * 2.0 ** rng.integers(-6, 6, (M, 1)))).to(DEV)
+    w = torch.from_numpy(f32(rng.uniform(-0.5, 0.5, (K, N)) * 2.0 ** rng.integers(-4, 4, (1, N)))).to(DEV)
+    rs = torch.from_numpy(f32(rng.uniform(0.1, 1.0, M))).to(DEV) if scaled else None
+    hr = sparse.gemm_f16rows(a, w, row_scale=rs)
+    assert hr is not None and hr.chunks == N // 256
+    ref = _chunked_rows(gc.gemm(a, w, row_scale=rs, precision="tf32"))
+    assert torch.equal(hr.xh.view(torch.int16), ref.xh.view(torch.int16))
+    assert torch.equal(hr.sigma, ref.sigma)
+
+
+@pytest.mark.parametrize("K", [512, 1024])
+@pytest.mark.parametrize("algo", ["row", "split"])
+@pytest.mark.parametrize("shrink", ["0", "1", "2"])
+def test_spmm_and_gat_chunked_scales(oracle, plgraph, K, algo, shrink, monkeypatch):
+    """SpMM over chunked-scale fp16 rows: each 256-column pass equals the fp32
+    kernel on that chunk's dequantised rows with d_col = the chunk's scales
+    (bit for bit); GAT reassoc against the oracle on the dequantised rows."""
+    monkeypatch.setattr(sparse, "PLAN_MIN_NNZ", 0)
+    monkeypatch.setattr(sparse, "SPMM_SHRINK", shrink)
+    if algo == "split":
+        monkeypatch.setattr(sparse, "SPLIT_CHUNK", 16)
+    rng = np.random.default_rng(K + int(shrink))
+    n = plgraph.n_rows
+    x = torch.from_numpy(f32(rng.standard_normal((n, K)) * 2.0 ** rng.integers(-5, 5, (1, K)))).to(DEV)
+    d = torch.from_numpy(f32(rng.uniform(0.1, 1, n))).to(DEV)
+    hr = _chunked_rows(x)
+    got = gc.spmm_unweighted(plgraph, hr, d_row=d, algo=algo)
+    monkeypatch.setattr(sparse, "SPMM_SHRINK", "0")
+    for c in range(K // 256):
+        cs = slice(c * 256, (c + 1) * 256)
+        deq = hr.xh[:, cs].float().contiguous()
+        ref = gc.spmm_unweighted(plgraph, deq, d_row=d, d_col=hr.sigma[:, c].contiguous(), algo=algo)
+        assert torch.equal(got[:, cs], ref), f"chunk {c}"
+    monkeypatch.setattr(sparse, "SPMM_SHRINK", shrink)
+    s, t = f32(rng.standard_normal(n) * 3), f32(rng.standard_normal(n) * 3)
+    out = sparse.gat_aggregate(plgraph, torch.from_numpy(s).to(DEV), torch.from_numpy(t).to(DEV),
+                               0.2, hr, algo=algo)
+    sig = np.repeat(hr.sigma.double().cpu().numpy(), 256, axis=1)
+    deq64 = hr.xh.double().cpu().numpy() * sig
+    oa = to_oracle(oracle, plgraph)
+    ref = oracle.spmm(oa.with_values(oracle.edge_softmax(oa, s, t, 0.2)), deq64)
+    assert oracle.rel_err(out.cpu().numpy(), ref) < 2e-5
+
+
+@pytest.mark.parametrize("K", [512, 1024])
+@pytest.mark.parametrize("fmt", ["f16", "f16mn"])
+def test_hub_pack_chunked_scales_bit_exact(K, fmt):
+    from paper_2306_15155_b200 import _native as nat
+    f = {"f16": nat.GC_HUB_F16, "f16mn": nat.GC_HUB_F16_MN}[fmt]
+    lib = nat.load()
+    if fmt == "f16mn" and not lib.gc_hub_f16_mn_supported(K):
+        pytest.skip("MN-major one-term operand needs CTA pairs")
+    rng = np.random.default_rng(K + 7)
+    ncols, T = 3000, 128
+    x = torch.from_numpy(f32(rng.standard_normal((ncols, K)) * 2.0 ** rng.integers(-4, 4, (1, K)))).to(DEV)
+    hr = _chunked_rows(x)
+    deq = (hr.xh.float() * torch.repeat_interleave(hr.sigma, 256, dim=1)).contiguous()
+    hub_cols = torch.from_numpy(np.sort(rng.choice(ncols, T, replace=False)).astype(np.int32)).to(DEV)
+    kp = lib.gc_hub_terms_rows(K)
+    st = torch.cuda.current_stream().cuda_stream
+    outs = []
+    for half in (True, False):
+        bt = torch.empty(kp * T, dtype=torch.float16, device=DEV)
+        sc = torch.empty(2, dtype=torch.float32, device=DEV)
+        if half:
+            rc = lib.gc_hub_pack_f16rows(hr.xh.data_ptr(), hr.xh.stride(0), hr.sigma.data_ptr(), K,
+                                         hub_cols.data_ptr(), T, None,
+                                         f | nat.GC_HUB_SIG_CHUNKS(K // 256), bt.data_ptr(),
+                                         sc.data_ptr(), st)
+        else:
+            rc = lib.gc_hub_pack(deq.data_ptr(), K, K, hub_cols.data_ptr(), T, None, f,
+                                 bt.data_ptr(), sc.data_ptr(), st)
+        nat.check(rc, "pack")
+        outs.append((bt.view(torch.int16).clone(), sc.clone()))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("comp", ["precompute", "dynamic"])
+def test_gcn_update_first_chunked_fp16_rows(oracle, hub_pl, comp, monkeypatch):
+    """Update-first at k2 = 512 in the TF32 class: the GEMM epilogue emits
+    fp16 rows with two scales per row, consumed by the plain SpMM and by the
+    hybrid split's dense part and tail; against the oracle."""
+    from paper_2306_15155_b200 import gcn, hub
+    monkeypatch.setattr(gcn, "HALF_MIN_BYTES", 0)
+    g = gc.NormalizedGraph.from_adjacency(hub_pl).with_precomputed()
+    og = oracle.GcnGraph.from_adjacency(to_oracle(oracle, hub_pl))
+    rng = np.random.default_rng(5)
+    k1, k2 = 64, 512
+    h = f32(rng.uniform(-0.5, 0.5, (hub_pl.n_rows, k1)))
+    w = f32(rng.uniform(-0.5, 0.5, (k1, k2)))
+    spec = gc.GcnLayerSpec(k1, k2, w, composition=comp, order="update_first")
+    seen = []
+    real = gcn.gemm_f16rows
+    monkeypatch.setattr(gcn, "gemm_f16rows",
+                        lambda *a, **k: (lambda r: seen.append(r.chunks) or r)(real(*a, **k)))
+    ref = oracle.gcn_layer(og, h.astype(np.float64), w.astype(np.float64), comp, "update_first")
+    for split in ("0", "128"):
+        monkeypatch.setattr(hub, "HUB_SPLIT", split)
+        out = gc.gcn_layer(g, torch.from_numpy(h).to(DEV), spec).cpu().numpy()
+        assert oracle.rel_err(out, ref) <= 3e-3, split
+    assert seen and all(c == 2 for c in seen)
