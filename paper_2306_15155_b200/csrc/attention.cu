@@ -124,6 +124,37 @@ __global__ void __launch_bounds__(kThreads)
   const int lane = threadIdx.x % 32;
   if (row >= n_rows) return;
   const float *hr = HW + row * ld;
+  if (vec && head_stride == 0 && k2 <= 1024) {
+    // every head projects the same row (the folded-vector scores s = H (W a)):
+    // the row is read once into registers, all loads in flight together; the
+    // per-head sums keep the loop's order, so results are unchanged
+    float4 xv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int64_t c = 4 * lane + 128 * i;
+      xv[i] = c < k2 ? ldg_f4(hr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (int h = 0; h < heads; ++h) {
+      const float *al = a_src + (int64_t)h * k2;
+      const float *ar = a_dst + (int64_t)h * k2;
+      float ss = 0.f, tt = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int64_t c = 4 * lane + 128 * i;
+        if (c < k2) {
+          ss = fma4_dot(xv[i], ldg_f4(al + c), ss);
+          tt = fma4_dot(xv[i], ldg_f4(ar + c), tt);
+        }
+      }
+      ss = group_sum<32>(ss);
+      tt = group_sum<32>(tt);
+      if (lane == 0) {
+        s[(int64_t)h * n_rows + row] = ss;
+        if (t) t[(int64_t)h * n_rows + row] = tt;
+      }
+    }
+    return;
+  }
   for (int h = 0; h < heads; ++h) {
     const float *x = hr + (int64_t)h * head_stride;
     const float *al = a_src + (int64_t)h * k2;
